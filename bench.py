@@ -1,0 +1,419 @@
+"""Benchmark of the B200 RoPeSLR attention forward (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3]
+
+Workload (default): BASELINE config 3, HunyuanVideo-13B-shaped attention:
+B=1, H=24, d_h=128, grid 33x45x80 (L=118800), flat 128-token blocks
+(929 blocks, last one 16 tokens), 90% sparsity -> top-93 key blocks per
+query block, r=64, bf16.  Heads are partitioned 24/12/6/3 at N=1/2/4/8
+(one process per GPU, torchrun); the only collective is the all-reduce of
+the partial gate logits ([B, L] float32).  A step = one forward of this
+rank's heads: K1 selection, K3 compensator + gate, (all-reduce), K2+K4
+fused attention/epilogue.
+
+Prints ONE JSON line on rank 0.  `value` = effective TFLOP/s of the whole
+job: (sparse + low-rank + fusion algorithmic FLOPs over all ranks, the
+sparse term from the measured attended pairs) / max-over-ranks step time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    "cfg3": dict(name="hunyuan13b_attn_L118800_H24_d128_b128_s90", grid=(33, 45, 80), H=24, d=128,
+                 split=(16, 56, 56), block=128, sparsity=0.9, r=64),
+    "cfg1": dict(name="wan1.3b_attn_L32760_H12_d128_b64_s90", grid=(21, 30, 52), H=12, d=128,
+                 split=(44, 42, 42), block=64, sparsity=0.9, r=64),
+    "cfg2_b128": dict(name="wan1.3b_attn_L32760_H12_d128_b128_s90", grid=(21, 30, 52), H=12, d=128,
+                      split=(44, 42, 42), block=128, sparsity=0.9, r=64),
+}
+METRIC = "RoPeSLR attn fwd ms & effective TFLOPS/GPU, L=118800, 90% sparse, 1/2/4/8 B200"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+        return p
+    p = dict(PEAKS_FALLBACK)
+    p["source"] = "fallback (B200_PROFILING.md)"
+    return p
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, flag in zip(names, parts[5:9]):
+                if flag.lower() in ("active", "1"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_oracle_sample(q0, k0, v0, x_np, pe_np, params_np, cfg, topk, qblocks):
+    """Oracle (oracle/restated.py, float64 NumPy) for one head: selection
+    over all blocks + exact attention and fusion for `qblocks` query blocks.
+    Returns (seconds, algorithmic FLOPs of the sample)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import restated as R
+
+    L, d = q0.shape
+    block = cfg["block"]
+    t0 = time.perf_counter()
+    members = R.flat_block_members(L, block)
+    scores = R.block_scores(q0, k0, members)
+    selected, _ = R.select_blocks(scores, topk=topk)
+    out, attended = R.attend_selected(q0, k0, v0, members, selected, qblocks=qblocks)
+    rows = np.concatenate([members[b] for b in qblocks])
+    c = R.grid_coords(*cfg["grid"])[rows]
+    pe = pe_np[0][c[:, 0]] + pe_np[1][c[:, 1]] + pe_np[2][c[:, 2]]
+    x_hat = x_np[rows] + params_np["alpha"][None] * pe
+    g = R.gate(x_hat, params_np["w_g"], params_np["b_g"])
+    o_lr = R.lowrank_compensator(x_hat, params_np["w_a"], params_np["w_b"], 0)
+    _ = R.rms_norm(out[rows], params_np["rms_sparse"]) + g[:, None] * R.rms_norm(o_lr, params_np["rms_lowrank"])
+    dt = time.perf_counter() - t0
+    n = len(rows)
+    flops = 4.0 * d * attended + 4.0 * n * d * cfg["r"] + 2.0 * n * d
+    return dt, flops
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- inputs
+def make_inputs(cfg, h0, h1, dev, seed=0):
+    """This rank's heads [h0, h1): seeded per global head so every N sees the
+    same tensors.  Q,K,V ~ N(0,1), RoPE in float64 then bf16; X ~ N(0,1);
+    PE tables ~ N(0,0.02); W_A, W_B ~ N(0,1/sqrt(d)); alpha 0.1; w_g ~ N(0,0.05)."""
+    import torch
+
+    import paper_2605_20659_b200 as P
+
+    grid = P.GridShape(*cfg["grid"])
+    rope = P.RopeConfig(*cfg["split"])
+    H, d, r = cfg["H"], cfg["d"], cfg["r"]
+    L, D = grid.size, H * d
+    qkv = [[], [], []]
+    for h in range(h0, h1):
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed * 100003 + h)
+        for which in range(3):
+            t = torch.randn((1, 1, L, d), generator=gen, device=dev)
+            t = P.rotate_rows(t, grid, rope) if which < 2 else t
+            qkv[which].append(t.to(torch.bfloat16))
+    q, k, v = (torch.cat(t, 1).contiguous() for t in qkv)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed * 100003 + 7777)
+    x_full = torch.randn((1, L, D), generator=gen, device=dev).to(torch.bfloat16)
+    pe = P.PETables(*(torch.randn((n, D), generator=gen, device=dev) * 0.02 for n in cfg["grid"]))
+    params = P.MechanismParams(
+        w_a=torch.randn((H, d, r), generator=gen, device=dev) / math.sqrt(d),
+        w_b=torch.randn((H, r, d), generator=gen, device=dev) / math.sqrt(d),
+        alpha=torch.full((D,), 0.1, device=dev), w_g=torch.randn((D,), generator=gen, device=dev) * 0.05,
+        b_g=-2.0, rms_sparse=torch.ones(d, device=dev), rms_lowrank=torch.ones(d, device=dev))
+    x_local = x_full[:, :, h0 * d:h1 * d].contiguous()
+    del x_full
+    return q, k, v, x_local, params.heads(h0, h1), pe, grid
+
+
+# ---------------------------------------------------------------- arms
+def run_reference(args, cfg, rank, world):
+    """Reference arm: the reference's CPU algorithm (oracle port of
+    mechanism.py, float64 NumPy, all host threads) on a bounded sample."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import restated as R
+
+    rng = np.random.default_rng(0)
+    grid = cfg["grid"]
+    L = grid[0] * grid[1] * grid[2]
+    d, r, block = cfg["d"], cfg["r"], cfg["block"]
+    D = cfg["H"] * d
+    nb = -(-L // block)
+    topk = max(1, int(math.floor((1 - cfg["sparsity"]) * nb + 0.5)))
+
+    def bf16(a):
+        u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+        u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+        return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+    q0 = bf16(R.rotate_rows(rng.standard_normal((L, d)), grid, cfg["split"]))
+    k0 = bf16(R.rotate_rows(rng.standard_normal((L, d)), grid, cfg["split"]))
+    v0 = bf16(rng.standard_normal((L, d)))
+    x_np = bf16(rng.standard_normal((L, D)))
+    pe_np = [rng.standard_normal((n, D)) * 0.02 for n in grid]
+    params_np = dict(w_a=rng.standard_normal((1, d, r)) / math.sqrt(d), w_b=rng.standard_normal((1, r, d)) / math.sqrt(d),
+                     alpha=np.full(D, 0.1), w_g=rng.standard_normal(D) * 0.05, b_g=-2.0,
+                     rms_sparse=np.ones(d), rms_lowrank=np.ones(d))
+    qblocks = list(range(args.ref_qblocks))
+    times, flops = [], 0.0
+    for i in range(args.warmup + args.steps):
+        dt, fl = cpu_oracle_sample(q0, k0, v0, x_np, pe_np, params_np, cfg, topk, qblocks)
+        if i >= args.warmup:
+            times.append(dt)
+            flops = fl
+    sec = statistics.mean(times)
+    value = flops / sec / 1e12
+    sample = (f"head 0 of {cfg['name']}: selection over all {nb} blocks + attention/compensator/fusion of "
+              f"query blocks 0..{args.ref_qblocks - 1} (float64 NumPy, oracle/restated.py)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), 3D RoPE, bf16-rounded)",
+        "config": {"workload": cfg["name"], "sample": "bounded CPU sample", "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_20659_b200 as P
+    from paper_2605_20659_b200.distributed import gate_allreduce, head_slice
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if P.lib().ropeslr_device_check(local_rank) != 0:
+        raise SystemExit("bench: device is not an sm_100 B200")
+    H, d, r = cfg["H"], cfg["d"], cfg["r"]
+    h0, h1 = head_slice(H, world, rank)
+    Hl = h1 - h0
+    q, k, v, x, params, pe, grid = make_inputs(cfg, h0, h1, dev)
+    L = grid.size
+    nb = -(-L // cfg["block"])
+    settings = P.ForwardSettings(P.SparseSettings.for_sparsity(cfg["block"], L, cfg["sparsity"]))
+    reduce_ = gate_allreduce() if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-resident timed region
+    k2_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k2_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    out_buf = torch.empty((1, L, Hl, d), dtype=torch.bfloat16, device=dev)
+
+    def step(i=None):
+        prep = P.prepare(q, k, v, x, grid, params, settings, pe, head_offset=h0)
+        if reduce_ is not None:
+            reduce_(prep.g_logit)
+        if i is not None:
+            k2_start[i].record(stream)
+        out, _ = P.attend(prep, params, settings, out=out_buf)
+        if i is not None:
+            k2_end[i].record(stream)
+        return prep
+
+    prep = None
+    for _ in range(args.warmup):
+        prep = step()
+    torch.cuda.synchronize()
+    attended_local = int(prep.sel.attended.sum())
+    barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    k2_ms_local = statistics.mean(a.elapsed_time(b) for a, b in zip(k2_start, k2_end))
+    clock_summary = clocks.summary()
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv, hx = (t.cpu().pin_memory() for t in (q, k, v, x))
+        hout = torch.empty((1, L, Hl * d), dtype=torch.bfloat16).pin_memory()
+        bi = sum(t.numel() * t.element_size() for t in (hq, hk, hv, hx))
+        bo = hout.numel() * hout.element_size()
+
+        def e2e_step():
+            dq, dk, dv, dx = (t.to(dev, non_blocking=True) for t in (hq, hk, hv, hx))
+            o = P.forward(dq, dk, dv, dx, grid, params, settings, pe, head_offset=h0, gate_reduce=reduce_)
+            hout.copy_(o, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(2, args.steps // 2)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms_local = e0.elapsed_time(e1) / n_e2e
+        e2e = dict(ms=e2e_ms_local, bi=bi, bo=bo)
+
+    # ---- reduce over ranks
+    vals = torch.tensor([ms_local, k2_ms_local, (e2e or {}).get("ms", 0.0)], dtype=torch.float64, device=dev)
+    att = torch.tensor([attended_local], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(att, op=dist.ReduceOp.SUM)
+    ms, k2_ms, e2e_ms = (float(a) for a in vals.tolist())
+    attended_total = int(att.item())
+
+    if rank != 0:
+        return
+    B = 1
+    flops_total = P.flops.total_ropeslr(attended_total, B, H, L, d, r)
+    sparse_flops_local = 4.0 * d * attended_local
+    value = flops_total / (ms * 1e-3) / 1e12
+    peaks = load_peaks()
+    peak = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
+    achieved = sparse_flops_local / (k2_ms_local * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) Q/K/V with 3D RoPE, X, PE tables; random-init params)",
+        "config": {"workload": cfg["name"], "B": B, "L": L, "H": H, "d_h": d, "block": cfg["block"],
+                   "n_blocks": nb, "topk": settings.sparse.topk, "rank_r": r,
+                   "heads_per_gpu": Hl, "parallelism": f"head-parallel x{world}",
+                   "l2": "inputs (2.9 GB) larger than L2; no explicit flush"},
+        "tflops_per_gpu": value / world,
+        "sparse_attn_ms": k2_ms,
+        "attended_pairs": attended_total,
+        "sparsity": 1.0 - attended_total / (H * float(L) ** 2),
+        "roofline": {"bound": "tensor", "kernel": "sparse_attn_tc_kernel (K2+K4 fused)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": peaks["source"] + ", bf16 dense sustained (kernel timed inside a long step)",
+                     "peak_burst": peaks.get("bf16_tflops"), "frac_of_burst": achieved / peaks.get("bf16_tflops", 1),
+                     "traffic": None,
+                     "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)"},
+        "clocks": clock_summary,
+        "gpu_launches": 5 * args.steps,
+    }
+    if e2e is not None:
+        line["e2e"] = {"value": flops_total / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                       "ms_per_step": e2e_ms, "h2d_bytes_per_step": e2e["bi"], "d2h_bytes_per_step": e2e["bo"]}
+    if world == 1 and not args.no_cpu_baseline:
+        q0, k0, v0 = (t[0, 0].double().cpu().numpy() for t in (q, k, v))
+        x_np = x[0].double().cpu().numpy()
+        pe_np = [t.double().cpu().numpy() for t in (pe.pe_t, pe.pe_x, pe.pe_y)]
+        params_np = {n: getattr(params, n).double().cpu().numpy() for n in
+                     ("w_a", "w_b", "alpha", "w_g", "rms_sparse", "rms_lowrank")}
+        params_np["b_g"] = params.b_g
+        qbs = list(range(args.cpu_qblocks))
+        dt, fl = cpu_oracle_sample(q0, k0, v0, x_np, pe_np, params_np, cfg, settings.sparse.topk, qbs)
+        line["cpu_baseline"] = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": blas_threads(),
+                                "kind": "port", "seconds": dt,
+                                "sample": f"head 0, selection over all {nb} blocks + attention/compensator/fusion "
+                                          f"of query blocks 0..{args.cpu_qblocks - 1} (float64 NumPy oracle)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(CONFIGS), default="cfg3")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-qblocks", type=int, default=300)
+    ap.add_argument("--ref-qblocks", type=int, default=100)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

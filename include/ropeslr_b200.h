@@ -1,0 +1,188 @@
+/*
+ * ropeslr_b200.h -- C ABI of the B200-native RoPeSLR attention forward.
+ *
+ * The reference (arxiv 2605.20659, /root/reference/pkg/src/ropeslr) is a pure
+ * Python/NumPy package with no FFI; its "plugin API" is the Python function
+ * set of mechanism.py.  Each entry point below replaces one of those
+ * functions (cited as mechanism.py:LINE) and is what a ctypes / cffi binding
+ * on the reference side would bind.  The Python package
+ * paper_2605_20659_b200 binds exactly these symbols.
+ *
+ * Conventions
+ *   - Plain pointers to device memory, sizes in elements, caller-allocated
+ *     outputs, stream-ordered (the `stream` argument is a cudaStream_t, 0 is
+ *     the legacy default stream).  No hidden allocation: scratch comes from a
+ *     caller-provided workspace whose size the *_workspace_bytes queries give.
+ *   - Layouts (row-major, innermost last):
+ *       Q, K, V          [B, H, L, d]   post-RoPE, dtype = shape.dtype
+ *       X                [B, L, *]      token rows; the local heads' columns
+ *                                       start at x_col_offset with row stride
+ *                                       x_row_stride (elements)
+ *       out, y_lr        [B, L, H, d]   == the reference's (L, d_model) rows
+ *       o_sparse, o_lr   [B, H, L, d]   float32 debug/intermediate outputs
+ *       g_logit          [B, L]         float32, x_hat . w_g over the local
+ *                                       columns (no bias, no sigmoid)
+ *       idx              [B, H, nb, kmax] int32, selected key blocks in
+ *                                       ascending block order
+ *       cnt              [B, H, nb]     int32 selected count per query block
+ *       mask             [B, H, nb, nb] uint8 (the reference's `selected`)
+ *       attended         [B, H]         int64 attended (query, key) pairs
+ *     with nb = ceil(L / block) flat blocks, the last one ragged.
+ *   - Parameters are float32: w_a [H,d,r], w_b [H,r,d], alpha/w_g [D_total],
+ *     rms_sparse/rms_lowrank [d], per-axis PE tables [T|Hg|Wg, D_total].
+ *   - Errors: a negative ropeslr_status; nothing is launched on error.  The
+ *     Python layer maps every nonzero status to ValueError, mirroring the
+ *     reference's ValueError on bad shapes/ranges (mechanism.py:230-233,
+ *     266-270, 282-283, 297-300).
+ *   - Threading: no global mutable state apart from a per-device attribute
+ *     cache; calls on different streams may run concurrently.
+ */
+#ifndef ROPESLR_B200_H
+#define ROPESLR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ROPESLR_ABI_VERSION 1
+
+typedef enum ropeslr_status {
+  ROPESLR_OK = 0,
+  ROPESLR_ERR_SHAPE = -1,      /* inconsistent or unsupported sizes */
+  ROPESLR_ERR_DTYPE = -2,      /* unsupported dtype code */
+  ROPESLR_ERR_ALIGN = -3,      /* pointer not 16-byte aligned */
+  ROPESLR_ERR_DIVIS = -4,      /* 3D block does not divide the grid */
+  ROPESLR_ERR_LAUNCH = -5,     /* CUDA launch / runtime error */
+  ROPESLR_ERR_VALUE = -6,      /* out-of-range scalar (keep, eps, topk, ...) */
+  ROPESLR_ERR_WORKSPACE = -7,  /* workspace missing or too small */
+  ROPESLR_ERR_ARCH = -8,       /* device is not sm_100 */
+  ROPESLR_ERR_NULL = -9        /* required pointer is NULL */
+} ropeslr_status;
+
+typedef enum ropeslr_dtype { ROPESLR_F32 = 0, ROPESLR_BF16 = 1 } ropeslr_dtype;
+typedef enum ropeslr_compensator { ROPESLR_LOWRANK = 0, ROPESLR_LINEAR = 1 } ropeslr_compensator;
+/* Sparse-attention implementation: AUTO picks the tcgen05/TMEM kernel for
+ * bf16 with d == 128 and block in {64, 128}, the CUDA-core kernel otherwise. */
+typedef enum ropeslr_impl { ROPESLR_IMPL_AUTO = 0, ROPESLR_IMPL_SIMT = 1, ROPESLR_IMPL_TCGEN05 = 2 } ropeslr_impl;
+
+typedef struct ropeslr_shape {
+  int64_t B;      /* batch */
+  int64_t H;      /* heads handled by this call (the local head slice) */
+  int64_t L;      /* real tokens; no padding */
+  int64_t d;      /* head dim */
+  int32_t block;  /* flat block size in tokens (query blocks == key blocks) */
+  int32_t dtype;  /* ropeslr_dtype of Q/K/V/X/out/y_lr */
+} ropeslr_shape;
+
+/* Selection rule.  topk > 0: keep the k best blocks (BASELINE configs);
+ * topk == 0: the reference's cumulative-mass rule, smallest prefix of the
+ * stable descending block-softmax order whose mass reaches keep - 1e-12
+ * (mechanism.py:316-320, decomposition.py:105-111). */
+typedef struct ropeslr_select_params {
+  int32_t topk;
+  double keep;
+} ropeslr_select_params;
+
+/* Token-side inputs of the compensator / gate (mechanism.py:426-447). */
+typedef struct ropeslr_token_args {
+  const void* x;           /* X at [b=0, l=0, first local column] */
+  int64_t x_row_stride;    /* elements between consecutive tokens */
+  int64_t head_offset;     /* global index of local head 0 (for PE/alpha/w_g columns) */
+  int64_t d_model;         /* D_total = columns of alpha / w_g / PE tables */
+  int32_t grid_t, grid_h, grid_w;  /* 3D latent grid, grid_t*grid_h*grid_w == L */
+  int32_t use_pe;          /* x_hat = x + alpha * PE when nonzero */
+  const float* pe_t;       /* [grid_t, D_total] */
+  const float* pe_x;       /* [grid_h, D_total] */
+  const float* pe_y;       /* [grid_w, D_total] */
+  const float* alpha;      /* [D_total] */
+  const float* w_g;        /* [D_total] */
+} ropeslr_token_args;
+
+/* ---------------------------------------------------------------- misc */
+int ropeslr_abi_version(void);
+const char* ropeslr_status_string(int status);
+/* ROPESLR_OK when `device` is an sm_100 part the kernels were built for. */
+int ropeslr_device_check(int device);
+/* Number of flat blocks: ceil(L / block). */
+int64_t ropeslr_num_blocks(int64_t L, int32_t block);
+
+/* ------------------------------------------------ K1: block selection
+ * Replaces the routing half of block_sparse_attention (mechanism.py:305-320,
+ * 326): fp64 mean-pooling of Q and K per block, fp64 scores / sqrt(d),
+ * stable descending order (ties to the lower block index), top-k or
+ * cumulative-mass count, ascending index list.  `mask` and `scores`
+ * ([B,H,nb,nb] float64) may be NULL.  kmax must be >= min(topk, nb) in top-k
+ * mode and >= nb in keep mode. */
+size_t ropeslr_select_workspace_bytes(const ropeslr_shape* shape);
+int ropeslr_select_blocks(const ropeslr_shape* shape, const ropeslr_select_params* sel,
+                          const void* q, const void* k,
+                          int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask,
+                          int64_t* attended, double* scores,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------ K2: block-sparse softmax attention
+ * Replaces the exact-attention half of block_sparse_attention
+ * (mechanism.py:321-326): each query block attends, with an exact softmax,
+ * to the tokens of its selected key blocks.  Writes the un-normalised-branch
+ * output o_sparse [B,H,L,d] float32.  `row_perm` (nullable, [L] int32) maps
+ * the flat position of a query row to its token index (3D tiles, see
+ * DESIGN.md); outputs are written at the token index. */
+int ropeslr_sparse_attention(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
+                             const int32_t* idx, int32_t kmax, const int32_t* cnt,
+                             const int32_t* row_perm, float* o_sparse, int32_t impl, void* stream);
+
+/* -------------------------------------- K3: compensators and the gate
+ * Low-rank compensator (mechanism.py:225-235, 441-446) with PE injection
+ * (mechanism.py:212-218, 429-432), then RMSNorm (mechanism.py:238-246) with
+ * rms_lowrank: y_lr = RMS(sigmoid(sigmoid(x_hat_h W_A[h]) W_B[h])) * rms_lowrank.
+ * Optionally fuses the gate logits over the local columns (g_logit, nullable)
+ * and writes the raw compensator output o_lr (nullable, float32 [B,H,L,d]). */
+int ropeslr_lowrank_branch(const ropeslr_shape* shape, const ropeslr_token_args* tok,
+                           const float* w_a, const float* w_b, int32_t rank,
+                           const float* rms_lowrank, float eps,
+                           void* y_lr, float* o_lr, float* g_logit, void* stream);
+
+/* Gate logits alone: g_logit[b,l] = sum over the local columns of
+ * x_hat[b,l,c] * w_g[c] (mechanism.py:249-255, 434; bias and sigmoid are
+ * applied in the fused epilogue so that head-sharded ranks can all-reduce
+ * the partial logits first). */
+int ropeslr_gate_logits(const ropeslr_shape* shape, const ropeslr_token_args* tok,
+                        float* g_logit, void* stream);
+
+/* Linear-attention compensator (mechanism.py:33-36, 350-362): from the
+ * caller's projections q_lin/k_lin/v_lin [B,H,L,d] (x_hat @ w_{q,k,v}[h], no
+ * RoPE): phi = elu + 1, state S = phi(k)^T v (d x d) and z = sum phi(k),
+ * reduced over L in fixed order (deterministic), then
+ * o = phi(q) S / max(phi(q).z, 1e-8) and y_lr = RMS(o) * rms_lowrank. */
+size_t ropeslr_linear_workspace_bytes(const ropeslr_shape* shape);
+int ropeslr_linear_branch(const ropeslr_shape* shape, const void* q_lin, const void* k_lin,
+                          const void* v_lin, const float* rms_lowrank, float eps,
+                          void* y_lr, float* o_lr, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
+/* ------------------------------------------------ K4: fused epilogue
+ * out = RMS(o_sparse) * rms_sparse + sigmoid(g_logit + b_g) * y_lr
+ * (mechanism.py:437-451).  Standalone form used after the CUDA-core
+ * attention kernel; the tcgen05 kernel fuses it (ropeslr_attend_fused). */
+int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const void* y_lr,
+                        const float* g_logit, float b_g, const float* rms_sparse, float eps,
+                        void* out, void* stream);
+
+/* K2 + K4 in one launch where the tcgen05 path applies (else K2 then K4):
+ * attention, normalisation by the softmax denominator, RMSNorm, gated
+ * combination with y_lr and the bf16/f32 store of out.  o_sparse (nullable)
+ * additionally receives the raw sparse-branch output. */
+int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
+                         const int32_t* idx, int32_t kmax, const int32_t* cnt,
+                         const int32_t* row_perm, const void* y_lr, const float* g_logit, float b_g,
+                         const float* rms_sparse, float eps, void* out, float* o_sparse,
+                         int32_t impl, void* workspace, size_t workspace_bytes, void* stream);
+size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* shape, int32_t impl);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROPESLR_B200_H */

@@ -1,0 +1,102 @@
+"""ctypes binding of the C ABI in include/ropeslr_b200.h.
+
+The library is built in-tree (``build.py``) and loaded from this package
+directory.  There is no fallback: if the shared library is missing or was
+built for another architecture, every op raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libropeslr_b200.so")
+
+F32, BF16 = 0, 1
+LOWRANK, LINEAR = 0, 1
+IMPL = {"auto": 0, "simt": 1, "tcgen05": 2}
+
+c_i32, c_i64, c_f32, c_f64, c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double, ctypes.c_size_t
+c_vp = ctypes.c_void_p
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("B", c_i64), ("H", c_i64), ("L", c_i64), ("d", c_i64), ("block", c_i32), ("dtype", c_i32)]
+
+
+class SelectParams(ctypes.Structure):
+    _fields_ = [("topk", c_i32), ("keep", c_f64)]
+
+
+class TokenArgs(ctypes.Structure):
+    _fields_ = [("x", c_vp), ("x_row_stride", c_i64), ("head_offset", c_i64), ("d_model", c_i64),
+                ("grid_t", c_i32), ("grid_h", c_i32), ("grid_w", c_i32), ("use_pe", c_i32),
+                ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp)]
+
+
+P = ctypes.POINTER
+_SIGNATURES = {
+    "ropeslr_abi_version": (c_i32, []),
+    "ropeslr_status_string": (ctypes.c_char_p, [c_i32]),
+    "ropeslr_device_check": (c_i32, [c_i32]),
+    "ropeslr_num_blocks": (c_i64, [c_i64, c_i32]),
+    "ropeslr_select_workspace_bytes": (c_sz, [P(Shape)]),
+    "ropeslr_select_blocks": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp, c_sz, c_vp]),
+    "ropeslr_sparse_attention": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "ropeslr_lowrank_branch": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp, c_i32, c_vp, c_f32, c_vp, c_vp, c_vp,
+                                       c_vp]),
+    "ropeslr_gate_logits": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp]),
+    "ropeslr_linear_workspace_bytes": (c_sz, [P(Shape)]),
+    "ropeslr_linear_branch": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_f32, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "ropeslr_fuse_output": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_f32, c_vp, c_f32, c_vp, c_vp]),
+    "ropeslr_attend_fused": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp,
+                                     c_f32, c_vp, c_vp, c_i32, c_vp, c_sz, c_vp]),
+    "ropeslr_attend_workspace_bytes": (c_sz, [P(Shape), c_i32]),
+}
+EXPORTED = tuple(_SIGNATURES)
+
+_lock = threading.Lock()
+_lib = None
+
+
+class RopeSLRError(ValueError):
+    """Nonzero status from the C ABI (a ValueError, like the reference's)."""
+
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: {msg} (status {status})")
+        self.status = status
+
+
+def lib() -> ctypes.CDLL:
+    """Load libropeslr_b200.so once; raise if it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2605_20659_b200.build` "
+                    "(there is no CPU fallback for the RoPeSLR op)")
+            handle = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            if handle.ropeslr_abi_version() != 1:
+                raise RuntimeError("libropeslr_b200.so ABI version mismatch")
+            _lib = handle
+    return _lib
+
+
+def check(fn: str, status: int) -> None:
+    if status != 0:
+        msg = lib().ropeslr_status_string(status).decode()
+        raise RopeSLRError(fn, status, msg)
+
+
+def call(fn: str, *args) -> None:
+    check(fn, getattr(lib(), fn)(*args))

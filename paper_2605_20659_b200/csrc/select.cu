@@ -1,0 +1,327 @@
+// K1: block routing of the RoPeSLR sparse branch.
+//
+// Restates mechanism.py:305-320 (+ the attended-pair count of :326) for flat,
+// possibly ragged blocks on the GPU:
+//   pool      mean of each block's Q and K rows, accumulated in float64
+//             (mechanism.py:306-308).  Sums of <= block bf16/f32 values are
+//             exact in float64 for realistic data, so the pooled means match
+//             the NumPy oracle bit for bit before the division by the count.
+//   scores    (pooled_q @ pooled_k^T) / sqrt(d) in float64 (mechanism.py:309).
+//   select    stable descending order of the block softmax (ties -> lower
+//             block index, mechanism.py:317), then top-k or count_for_mass
+//             (decomposition.py:105-111); emits the ascending index list the
+//             attention kernel walks (mechanism.py:321 `sorted(chosen)`).
+// All three are HBM/L2-bound; see DESIGN.md for the byte counts.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+
+namespace ropeslr {
+
+// grid (nb, B*H, 2): z = 0 pools Q, z = 1 pools K.  pooled: [2][BH][nb][d].
+template <typename T>
+__global__ void __launch_bounds__(256) pool_blocks_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                          double* __restrict__ pooled, int64_t L, int d, int block,
+                                                          int nb, int64_t BH) {
+  extern __shared__ double sred[];
+  const int64_t bh = blockIdx.y;
+  const T* src = (blockIdx.z == 0 ? q : k) + bh * L * d;
+  const int b = blockIdx.x;
+  const int rows = block_size(L, block, b);
+  const int64_t r0 = static_cast<int64_t>(b) * block;
+  const int chunks = d / 8;
+  const int lanes_r = blockDim.x / chunks;
+  const int tid = threadIdx.x;
+  const int ch = tid % chunks;
+  const int rr = tid / chunks;
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  if (rr < lanes_r) {
+    for (int r = rr; r < rows; r += lanes_r) {
+      float v[8];
+      load8(src + (r0 + r) * d + ch * 8, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(v[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sred[rr * d + ch * 8 + i] = acc[i];
+  }
+  __syncthreads();
+  double* dst = pooled + ((static_cast<int64_t>(blockIdx.z) * BH + bh) * nb + b) * d;
+  for (int c = tid; c < d; c += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < lanes_r; ++j) s += sred[j * d + c];
+    dst[c] = s / static_cast<double>(rows);
+  }
+}
+
+// scores[bh, i, j] = dot(pooled_q[bh, i], pooled_k[bh, j]) / sqrt(d), float64.
+// 64x64 output tile per CTA, 4x4 per thread, k-chunks of 16 staged in smem.
+__global__ void __launch_bounds__(256) block_scores_kernel(const double* __restrict__ pooled, double* __restrict__ scores,
+                                                           int nb, int d, int64_t BH, double sqrt_d) {
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int64_t bh = blockIdx.z;
+  const double* pq = pooled + bh * nb * d;
+  const double* pk = pooled + (BH + bh) * nb * d;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < d; k0 += 16) {
+    for (int e = tid; e < 64 * 16; e += 256) {
+      int r = e / 16, c = e % 16;
+      int gi = i0 + r, gj = j0 + r, gc = k0 + c;
+      As[c][r] = (gi < nb && gc < d) ? pq[static_cast<int64_t>(gi) * d + gc] : 0.0;
+      Bs[c][r] = (gj < nb && gc < d) ? pk[static_cast<int64_t>(gj) * d + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = As[c][ty + 16 * u];
+        b[u] = Bs[c][tx + 16 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+  double* out = scores + bh * nb * nb;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    int gi = i0 + ty + 16 * u;
+    if (gi >= nb) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      int gj = j0 + tx + 16 * v;
+      if (gj < nb) out[static_cast<int64_t>(gi) * nb + gj] = acc[u][v] / sqrt_d;
+    }
+  }
+}
+
+// Order-preserving map double -> uint64, inverted so that an ascending sort
+// yields descending scores.  +0 and -0 compare equal in the reference's
+// softmax, so -0 is folded onto +0 to keep the lower-index tie rule.
+__device__ __forceinline__ uint64_t desc_key(double s) {
+  if (s == 0.0) s = 0.0;
+  uint64_t u = static_cast<uint64_t>(__double_as_longlong(s));
+  uint64_t asc = (u >> 63) ? ~u : (u | (1ull << 63));
+  return ~asc;
+}
+
+// One CTA per (bh, query block) row.
+__global__ void __launch_bounds__(256) select_rows_kernel(const double* __restrict__ scores, int nb, int n2,
+                                                          int64_t L, int block, int topk, double keep, int kmax,
+                                                          int32_t* __restrict__ idx, int32_t* __restrict__ cnt,
+                                                          uint8_t* __restrict__ mask,
+                                                          unsigned long long* __restrict__ attended) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* ids = reinterpret_cast<uint32_t*>(keys + n2);
+  int* flags = reinterpret_cast<int*>(ids + n2);
+  __shared__ int s_nkeep;
+  __shared__ double s_red[8];
+
+  const int64_t row = blockIdx.x;  // bh * nb + qb
+  const int64_t bh = row / nb;
+  const int qb = static_cast<int>(row % nb);
+  const double* srow = scores + row * nb;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+
+  for (int i = tid; i < n2; i += blockDim.x) {
+    if (i < nb) {
+      keys[i] = desc_key(srow[i]);
+      ids[i] = static_cast<uint32_t>(i);
+    } else {
+      keys[i] = ~0ull;
+      ids[i] = 0xFFFFFFFFu;
+    }
+  }
+  for (int i = tid; i < nb; i += blockDim.x) flags[i] = 0;
+  __syncthreads();
+
+  // bitonic sort ascending on (key, id): stable descending order of scores
+  for (int kk = 2; kk <= n2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n2; i += blockDim.x) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          uint64_t ka = keys[i], kb = keys[ixj];
+          uint32_t ia = ids[i], ib = ids[ixj];
+          bool a_gt_b = (ka > kb) || (ka == kb && ia > ib);
+          bool up = (i & kk) == 0;
+          if (a_gt_b == up) {
+            keys[i] = kb;
+            keys[ixj] = ka;
+            ids[i] = ib;
+            ids[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  if (topk > 0) {
+    if (tid == 0) s_nkeep = topk < nb ? topk : nb;
+  } else {
+    // cumulative-mass rule on the block softmax (mechanism.py:310-311, 318)
+    const double smax = srow[ids[0]];
+    double part = 0.0;
+    for (int i = tid; i < nb; i += blockDim.x) part += exp(srow[i] - smax);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) s_red[warp] = part;
+    __syncthreads();
+    if (warp == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < (int)(blockDim.x / 32); ++w) sum += s_red[w];
+      double carry = 0.0;
+      int found = nb;
+      const double target = keep - kMassSlack;
+      for (int base = 0; base < nb; base += 32) {
+        int i = base + lane;
+        double p = (i < nb) ? exp(srow[ids[i]] - smax) / sum : 0.0;
+        // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          double t = __shfl_up_sync(0xffffffffu, p, o);
+          if (lane >= o) p += t;
+        }
+        double c = carry + p;
+        unsigned bal = __ballot_sync(0xffffffffu, (i < nb) && (c >= target));
+        if (bal) {
+          found = base + __ffs(bal);  // count = position + 1
+          break;
+        }
+        carry += __shfl_sync(0xffffffffu, p, 31);
+      }
+      if (lane == 0) s_nkeep = found;
+    }
+  }
+  __syncthreads();
+  const int nkeep = s_nkeep;
+  for (int i = tid; i < nkeep; i += blockDim.x) flags[ids[i]] = 1;
+  __syncthreads();
+
+  if (mask != nullptr) {
+    uint8_t* mrow = mask + row * nb;
+    for (int i = tid; i < nb; i += blockDim.x) mrow[i] = static_cast<uint8_t>(flags[i]);
+  }
+  if (warp == 0) {
+    int32_t* irow = idx + row * kmax;
+    int carry = 0;
+    long long ksum = 0;
+    for (int base = 0; base < nb; base += 32) {
+      int i = base + lane;
+      int f = (i < nb) ? flags[i] : 0;
+      unsigned bal = __ballot_sync(0xffffffffu, f);
+      int pos = carry + __popc(bal & ((1u << lane) - 1u));
+      if (f) {
+        irow[pos] = i;
+        ksum += block_size(L, block, i);
+      }
+      carry += __popc(bal);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+    if (lane == 0) {
+      cnt[row] = nkeep;
+      atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
+    }
+  }
+}
+
+}  // namespace ropeslr
+
+using namespace ropeslr;
+
+static int next_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+extern "C" size_t ropeslr_select_workspace_bytes(const ropeslr_shape* s) {
+  if (s == nullptr || s->block <= 0) return 0;
+  const int64_t nb = ceil_div(s->L, s->block);
+  const int64_t BH = s->B * s->H;
+  size_t pooled = static_cast<size_t>(2 * BH * nb * s->d) * sizeof(double);
+  size_t scores = static_cast<size_t>(BH * nb * nb) * sizeof(double);
+  return ((pooled + 255) / 256) * 256 + ((scores + 255) / 256) * 256;
+}
+
+extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_select_params* sel, const void* q,
+                                     const void* k, int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask,
+                                     int64_t* attended, double* scores_out, void* ws, size_t ws_bytes,
+                                     void* stream_) {
+  if (s == nullptr || sel == nullptr) return ROPESLR_ERR_NULL;
+  if (s->B < 1 || s->H < 1 || s->L < 1 || s->block < 1) return ROPESLR_ERR_SHAPE;
+  if (s->d < 8 || s->d > 256 || s->d % 8) return ROPESLR_ERR_SHAPE;
+  if (s->dtype != ROPESLR_F32 && s->dtype != ROPESLR_BF16) return ROPESLR_ERR_DTYPE;
+  if (!q || !k || !idx || !cnt || !attended) return ROPESLR_ERR_NULL;
+  if (!aligned16(q) || !aligned16(k)) return ROPESLR_ERR_ALIGN;
+  const int64_t nb64 = ceil_div(s->L, s->block);
+  if (nb64 > 8192) return ROPESLR_ERR_SHAPE;
+  const int nb = static_cast<int>(nb64);
+  if (sel->topk < 0) return ROPESLR_ERR_VALUE;
+  if (sel->topk == 0 && !(sel->keep > 0.0 && sel->keep <= 1.0)) return ROPESLR_ERR_VALUE;
+  const int need = sel->topk > 0 ? (sel->topk < nb ? sel->topk : nb) : nb;
+  if (kmax < need) return ROPESLR_ERR_SHAPE;
+  if (ws == nullptr || ws_bytes < ropeslr_select_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  const int64_t BH = s->B * s->H;
+  const int d = static_cast<int>(s->d);
+  double* pooled = static_cast<double*>(ws);
+  size_t pooled_bytes = ((static_cast<size_t>(2 * BH * nb * d) * sizeof(double) + 255) / 256) * 256;
+  double* scores = scores_out ? scores_out : reinterpret_cast<double*>(static_cast<char*>(ws) + pooled_bytes);
+
+  if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  {
+    dim3 grid(nb, static_cast<unsigned>(BH), 2);
+    const int chunks = d / 8;
+    const int lanes_r = 256 / chunks;
+    size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
+    if (s->dtype == ROPESLR_BF16)
+      pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                                static_cast<const __nv_bfloat16*>(k), pooled, s->L,
+                                                                d, s->block, nb, BH);
+    else
+      pool_blocks_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q), static_cast<const float*>(k),
+                                                        pooled, s->L, d, s->block, nb, BH);
+    if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  }
+  {
+    dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
+              static_cast<unsigned>(BH));
+    block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
+    if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  }
+  {
+    const int n2 = next_pow2(nb);
+    size_t sm = static_cast<size_t>(n2) * (sizeof(uint64_t) + sizeof(uint32_t)) + static_cast<size_t>(nb) * sizeof(int);
+    static_assert(sizeof(unsigned long long) == sizeof(int64_t), "int64 atomics");
+    if (sm > 48 * 1024) {
+      if (cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sm)) != cudaSuccess)
+        return ROPESLR_ERR_LAUNCH;
+    }
+    select_rows_kernel<<<static_cast<unsigned>(BH * nb), 256, sm, st>>>(
+        scores, nb, n2, s->L, s->block, sel->topk, sel->keep, kmax, idx, cnt, mask,
+        reinterpret_cast<unsigned long long*>(attended));
+    if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  }
+  return ROPESLR_OK;
+}

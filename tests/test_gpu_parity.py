@@ -1,0 +1,213 @@
+"""Parity of the CUDA path (through the C ABI) with the float64 oracle.
+
+Golden fixtures (tests/golden, generated from the unmodified reference by
+oracle/make_golden.py): masks bit-exact, outputs within the north-star
+tolerance (bf16: max-abs 2e-2, mean-rel 1e-2; f32: 1e-4 / 1e-5).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+import gpu_helpers as G
+import restated as R
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2605_20659_b200 as P
+
+    assert P.lib().ropeslr_device_check(torch.cuda.current_device()) == 0, "not an sm_100 device"
+
+
+IMPLS = ["auto", "simt"]
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("name", golden_io.names())
+def test_golden_forward(name, impl):
+    import paper_2605_20659_b200 as P
+
+    g = golden_io.load(name)
+    q, k, v, x, params, pe, st, grid, lin = G.golden_to_device(g)
+    tr = P.forward(q, k, v, x, grid, params, st, pe, lin_proj=lin, trace=True, impl=impl)
+    torch.cuda.synchronize()
+    sel = tr.selected[0].cpu().numpy()
+    np.testing.assert_array_equal(sel, g["ref_selected"], err_msg=f"{name}: mask differs from the reference")
+    np.testing.assert_allclose(tr.sparsity[0].cpu().numpy(), g["ref_sparsity"], rtol=0, atol=1e-15)
+    dt = g["dtype"]
+    # the sparse branch before normalisation: relative to its own scale
+    o_sp = tr.o_sparse[0].cpu().numpy()
+    ref = g["ref_o_sparse"]
+    scale = float(np.sqrt(np.mean(ref ** 2)))
+    G.assert_close(o_sp / scale, ref / scale, dt, f"{name} o_sparse/rms")
+    G.assert_close(tr.o_lowrank[0].cpu().numpy(), g["ref_o_lowrank"], dt, f"{name} o_lowrank")
+    G.assert_close(tr.g[0].cpu().numpy(), g["ref_g"], dt, f"{name} gate")
+    G.assert_close(tr.output[0].float().cpu().numpy(), g["ref_output"], dt, f"{name} output")
+
+
+@pytest.mark.parametrize("name", ["bf16_d128_keep", "bf16_d128_b128", "ragged_topk_bf16"])
+def test_tcgen05_matches_simt(name):
+    """The tensor-core kernel and the CUDA-core kernel agree (independent paths)."""
+    import paper_2605_20659_b200 as P
+
+    g = golden_io.load(name)
+    q, k, v, x, params, pe, st, grid, lin = G.golden_to_device(g)
+    a = P.forward(q, k, v, x, grid, params, st, pe, trace=True, impl="tcgen05")
+    b = P.forward(q, k, v, x, grid, params, st, pe, trace=True, impl="simt")
+    assert torch.equal(a.selected, b.selected)
+    ra, rb = a.o_sparse.double(), b.o_sparse.double()
+    rel = (ra - rb).abs().max() / rb.pow(2).mean().sqrt()
+    assert rel < 2e-2, f"tcgen05 vs simt o_sparse rel err {rel:.3e}"
+
+
+def test_deterministic():
+    import paper_2605_20659_b200 as P
+
+    g = golden_io.load("bf16_d128_b128")
+    q, k, v, x, params, pe, st, grid, lin = G.golden_to_device(g)
+    a = P.forward(q, k, v, x, grid, params, st, pe, trace=True)
+    b = P.forward(q, k, v, x, grid, params, st, pe, trace=True)
+    assert torch.equal(a.output, b.output)
+    assert torch.equal(a.o_sparse, b.o_sparse)
+
+
+# ---------------------------------------------------------------- edge cases
+
+
+def _small(L_grid=(2, 4, 16), H=2, d=128, seed=0, dtype=torch.bfloat16):
+    return G.make_full_inputs(L_grid, H, d, (44, 42, 42) if d == 128 else (16, 24, 24), 64 if d == 128 else 16,
+                              seed=seed, dtype=dtype)
+
+
+def _oracle_sparse(q, k, v, block, keep=None, topk=None):
+    out, sels = [], []
+    for h in range(q.shape[1]):
+        qh, kh, vh = (t[0, h].double().cpu().numpy() for t in (q, k, v))
+        members = R.flat_block_members(qh.shape[0], block)
+        o, s, _, _, _ = R.block_sparse_attention(qh, kh, vh, members, keep=keep, topk=topk)
+        out.append(o)
+        sels.append(s)
+    return np.stack(out), np.stack(sels)
+
+
+@pytest.mark.parametrize("impl", ["tcgen05", "simt"])
+@pytest.mark.parametrize("grid_shape,block,topk", [
+    ((1, 1, 40), 64, 1),        # L < block: one ragged block
+    ((1, 5, 13), 64, 1),        # L = 65: last block of one token
+    ((3, 7, 11), 128, 2),       # ragged 128 blocks
+    ((2, 8, 16), 64, 4),        # topk == nb: full attention
+    ((2, 8, 16), 64, 9),        # topk > nb clamps to nb
+])
+def test_ragged_and_full(grid_shape, block, topk, impl):
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small(grid_shape)
+    st = P.ForwardSettings(P.SparseSettings(block=block, topk=topk))
+    res = P.block_sparse_attention(q, k, v, st.sparse, impl=impl)
+    ref_out, ref_sel = _oracle_sparse(q, k, v, block, topk=topk)
+    np.testing.assert_array_equal(res.selected[0].cpu().numpy(), ref_sel)
+    got = res.output[0].double().cpu().numpy()
+    scale = float(np.sqrt(np.mean(ref_out ** 2)))
+    G.assert_close(got / scale, ref_out / scale, "bf16", "o_sparse/rms")
+    if topk >= -(-grid.size // block):
+        # full coverage == dense softmax attention
+        for h in range(q.shape[1]):
+            qh, kh, vh = (t[0, h].double() for t in (q, k, v))
+            a = torch.softmax(qh @ kh.T / np.sqrt(q.shape[-1]), dim=-1) @ vh
+            G.assert_close(got[h] / scale, a.cpu().numpy() / scale, "bf16", "dense")
+
+
+@pytest.mark.parametrize("keep", [1e-9, 0.3, 0.8, 1.0])
+def test_keep_rule(keep):
+    """Cumulative-mass rule (mechanism.py:316-320) incl. the floor of one
+    block and keep = 1."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((4, 8, 16), H=3)
+    sp = P.SparseSettings(block=64, keep=keep)
+    res = P.block_sparse_attention(q, k, v, sp)
+    ref_out, ref_sel = _oracle_sparse(q, k, v, 64, keep=keep)
+    np.testing.assert_array_equal(res.selected[0].cpu().numpy(), ref_sel)
+    if keep == 1e-9:
+        assert (res.selected.sum(-1) == 1).all()
+
+
+def test_tie_goes_to_lower_block():
+    """Identical key blocks score identically; the stable order keeps the
+    lower block index (mechanism.py:317, test_decomposition.py:157-162)."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((2, 8, 16), H=1)
+    k = k.clone()
+    k[:, :, 128:192] = k[:, :, 0:64]    # block 2 == block 0
+    k[:, :, 192:256] = k[:, :, 64:128]  # block 3 == block 1
+    res = P.block_sparse_attention(q, k, v, P.SparseSettings(block=64, topk=1))
+    sel = res.selected[0, 0].cpu().numpy()
+    ref_out, ref_sel = _oracle_sparse(q, k, v, 64, topk=1)
+    np.testing.assert_array_equal(sel, ref_sel[0])
+    assert not sel[:, 2:].any()
+
+
+def test_batch_two_matches_single():
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((2, 8, 16), H=2)
+    q2, k2, v2, x2, _, _, _ = _small((2, 8, 16), H=2, seed=5)
+    st = P.ForwardSettings(P.SparseSettings(block=64, topk=2))
+    qb, kb, vb, xb = (torch.cat(p, 0) for p in ((q, q2), (k, k2), (v, v2), (x, x2)))
+    both = P.forward(qb, kb, vb, xb, grid, params, st, pe)
+    one = P.forward(q2, k2, v2, x2, grid, params, st, pe)
+    assert torch.equal(both[1], one[0])
+
+
+def test_spec_known_answers():
+    """SPEC.md:466, 484, 493 on the device."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((2, 8, 16), H=2)
+    st = P.ForwardSettings(P.SparseSettings(block=64, topk=2))
+    p0 = P.MechanismParams(**{**params.__dict__, "w_a": torch.zeros_like(params.w_a),
+                              "w_b": torch.zeros_like(params.w_b)})
+    tr = P.forward(q, k, v, x, grid, p0, st, pe, trace=True)
+    assert torch.all(tr.o_lowrank == 0.5)
+    p1 = P.MechanismParams(**{**params.__dict__, "w_g": torch.zeros_like(params.w_g), "b_g": 0.0})
+    tr = P.forward(q, k, v, x, grid, p1, st, pe, trace=True)
+    assert torch.allclose(tr.g, torch.full_like(tr.g, 0.5))
+    p2 = P.MechanismParams(**{**params.__dict__, "b_g": -50.0})
+    tr = P.forward(q, k, v, x, grid, p2, st, pe, trace=True)
+    o = tr.o_sparse[0].double()
+    ysp = o / torch.sqrt(o.pow(2).mean(-1, keepdim=True) + 1e-6)
+    want = ysp.permute(1, 0, 2).reshape(grid.size, -1)
+    G.assert_close(tr.output[0].double().cpu().numpy(), want.cpu().numpy(), "bf16", "gate-off")
+
+
+def test_zero_values_zero_sparse_branch():
+    """Zero V -> zero sparse output -> RMSNorm(0) = 0."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((2, 8, 16), H=1)
+    st = P.ForwardSettings(P.SparseSettings(block=64, topk=2), use_pe=False)
+    p2 = P.MechanismParams(**{**params.__dict__, "b_g": -50.0})
+    tr = P.forward(q, k, v * 0, x, grid, p2, st, None, trace=True)
+    assert torch.all(tr.o_sparse == 0)
+    assert float(tr.output.float().abs().max()) < 1e-12
+
+
+def test_bad_inputs_raise_value_error():
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((2, 8, 16), H=1)
+    with pytest.raises(ValueError):
+        P.block_sparse_attention(q, k[:, :, :-1], v, P.SparseSettings(64, topk=1))
+    with pytest.raises(ValueError):
+        P.block_sparse_attention(q, k, v, P.SparseSettings((1, 3, 16)), grid=grid)  # 3 does not divide 8
+    with pytest.raises(ValueError):
+        P.block_sparse_attention(q.half(), k.half(), v.half(), P.SparseSettings(64, topk=1))
+    with pytest.raises(ValueError):
+        P.forward(q, k, v, x[:, :, :-8], grid, params, P.ForwardSettings(P.SparseSettings(64, topk=1)), pe)
