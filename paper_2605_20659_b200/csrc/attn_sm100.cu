@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100_ptx.cuh"
@@ -91,7 +92,32 @@ struct Params {
   float eps;
   __nv_bfloat16* out;
   float* o_sparse;
+  int kv_evict_last;
 };
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x on the FMA pipe for a pair: x = n + f (n = rint(x), |f| <= 1/2),
+// 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, far below the
+// bf16 rounding of P), 2^n added to the exponent field.  x is clamped at -126.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(make_float2(0.05517125502228737f, 0.05517125502228737f), f,
+                        make_float2(0.2426103800535202f, 0.2426103800535202f));
+  q = __ffma2_rn(q, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+  q = __ffma2_rn(q, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
 
 template <int BLK>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -142,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
-      const uint64_t pol_kv = policy_evict_last();
+      const uint64_t pol_kv = p.kv_evict_last ? policy_evict_last() : policy_evict_normal();
       const uint64_t pol_q = policy_evict_first();
       uint32_t g = 0, uc = 0;
       for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
@@ -253,19 +279,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&bars[S_EMPTY + s]);
+        // raw scores; the softmax scale is folded into one FFMA2 below
+        if (kreal < BLK) {
+#pragma unroll
+          for (int c = 0; c < BLK; ++c)
+            if (c >= kreal) sr[c] = __float_as_uint(-INFINITY);
+        }
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < BLK; ++c) {
-          float v = __uint_as_float(sr[c]) * p.scale_log2;
-          v = (c < kreal) ? v : -INFINITY;
-          sr[c] = __float_as_uint(v);
-          mx = fmaxf(mx, v);
-        }
+        for (int c = 0; c < BLK; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+        mx *= p.scale_log2;
         if (j == 0) {
           m_run = mx;
         } else if (mx > m_run + 8.f) {
           // lazy rescale: only when the running max grows by more than 2^8
-          const float alpha = exp2f(m_run - mx);
+          const float alpha = ex2_approx(m_run - mx);
           const uint32_t gp = gg - 1;
           mbar_wait(&bars[PV_DONE + (gp & 1)], (gp >> 1) & 1);
           tc_fence_after();
@@ -282,16 +310,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           l_run *= alpha;
           m_run = mx;
         }
-        float rowsum = 0.f;
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+        const float2 nm2 = make_float2(-m_run, -m_run);
+        float2 sum2 = make_float2(0.f, 0.f);
         uint32_t pk[BLK / 2];
 #pragma unroll
-        for (int c = 0; c < BLK; c += 2) {
-          const float p0 = exp2f(__uint_as_float(sr[c]) - m_run);
-          const float p1 = exp2f(__uint_as_float(sr[c + 1]) - m_run);
-          rowsum += p0 + p1;
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-          pk[c / 2] = *reinterpret_cast<uint32_t*>(&h2);
+        for (int i = 0; i < BLK / 2; ++i) {
+          const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), sc2, nm2);
+          float2 e2;
+          if ((i & 3) == 3) {
+            e2 = ex2_poly2(x2);  // FMA-pipe exp2 for 1/4 of the scores: offloads the MUFU
+          } else {
+            e2.x = ex2_approx(x2.x);
+            e2.y = ex2_approx(x2.y);
+          }
+          sum2 = __fadd2_rn(sum2, e2);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(e2.x, e2.y);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h2);
         }
+        const float rowsum = sum2.x + sum2.y;
         l_run += rowsum;
         mbar_wait(&bars[P_EMPTY + s], ph ^ 1);
         uint8_t* prow = sP + s * Lay::P_BYTES + row * 128;
@@ -342,11 +379,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int c = 0; c < D; c += 8) {
             float yv[8], ov[8];
-            load8(y + c, yv);
+            {
+              const uint4 u = __ldcs(reinterpret_cast<const uint4*>(y + c));
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 f2 = __bfloat1622float2(h[i]);
+                yv[2 * i] = f2.x;
+                yv[2 * i + 1] = f2.y;
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               ov[i] = fmaf(gate, yv[i], __uint_as_float(ob[c + i]) * inv * p.rms_sp[c + i]);
-            store8(dst + c, ov);
+            uint4 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(ov[2 * i], ov[2 * i + 1]);
+            __stcs(reinterpret_cast<uint4*>(dst + c), u);
           }
         }
       }
@@ -455,6 +505,8 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.num_units = s->B * s->H * prm.nb;
   prm.perm = perm;
   prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
+  const char* pol = getenv("ROPESLR_KV_EVICT_LAST");
+  prm.kv_evict_last = (pol != nullptr && pol[0] == '1') ? 1 : 0;
   return prm;
 }
 
