@@ -139,11 +139,17 @@ int ropeslr_sparse_attention(const ropeslr_shape* shape, const void* q, const vo
  * (mechanism.py:212-218, 429-432), then RMSNorm (mechanism.py:238-246) with
  * rms_lowrank: y_lr = RMS(sigmoid(sigmoid(x_hat_h W_A[h]) W_B[h])) * rms_lowrank.
  * Optionally fuses the gate logits over the local columns (g_logit, nullable)
- * and writes the raw compensator output o_lr (nullable, float32 [B,H,L,d]). */
+ * and writes the raw compensator output o_lr (nullable, float32 [B,H,L,d]).
+ * bf16 with d == 128 runs on the tensor cores: the PE injection is folded
+ * into per-axis [T|Hg|Wg, rank] tables ((alpha*P_axis)_h W_A[h]) built in the
+ * workspace, so X is read once and x_hat is never materialised. */
+size_t ropeslr_lowrank_workspace_bytes(const ropeslr_shape* shape, const ropeslr_token_args* tok,
+                                       int32_t rank);
 int ropeslr_lowrank_branch(const ropeslr_shape* shape, const ropeslr_token_args* tok,
                            const float* w_a, const float* w_b, int32_t rank,
                            const float* rms_lowrank, float eps,
-                           void* y_lr, float* o_lr, float* g_logit, void* stream);
+                           void* y_lr, float* o_lr, float* g_logit,
+                           void* workspace, size_t workspace_bytes, void* stream);
 
 /* Gate logits alone: g_logit[b,l] = sum over the local columns of
  * x_hat[b,l,c] * w_g[c] (mechanism.py:249-255, 434; bias and sigmoid are

@@ -304,6 +304,12 @@ __global__ void __launch_bounds__(256) fuse_output_kernel(const float* __restric
   }
 }
 
+size_t lowrank_tc_workspace_bytes(int64_t H, int r, int T, int Hg, int Wg);
+bool lowrank_tc_eligible(const ropeslr_shape* s, int r);
+int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
+                      int r, const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, void* ws,
+                      cudaStream_t st);
+
 static TokenCtx make_ctx(const ropeslr_shape* s, const ropeslr_token_args* t) {
   TokenCtx c;
   c.L = s->L;
@@ -342,9 +348,16 @@ static int check_shape(const ropeslr_shape* s) {
 
 using namespace ropeslr;
 
+extern "C" size_t ropeslr_lowrank_workspace_bytes(const ropeslr_shape* s, const ropeslr_token_args* t,
+                                                  int32_t rank) {
+  if (!s || !t) return 0;
+  if (!lowrank_tc_eligible(s, rank)) return 0;
+  return lowrank_tc_workspace_bytes(s->H, rank, t->grid_t, t->grid_h, t->grid_w);
+}
+
 extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a,
                                       const float* w_b, int32_t rank, const float* rms_lowrank, float eps, void* y_lr,
-                                      float* o_lr, float* g_logit, void* stream) {
+                                      float* o_lr, float* g_logit, void* ws, size_t ws_bytes, void* stream) {
   int st = check_shape(s);
   if (st) return st;
   if ((st = check_token_args(s, t))) return st;
@@ -352,6 +365,12 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
   if (s->d < 8 || s->d > 128 || s->d % 8) return ROPESLR_ERR_SHAPE;
   if (rank < 1 || rank > 256) return ROPESLR_ERR_SHAPE;
   if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  if (lowrank_tc_eligible(s, rank)) {
+    if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned16(y_lr)) return ROPESLR_ERR_ALIGN;
+    if (!ws || ws_bytes < ropeslr_lowrank_workspace_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
+    return launch_lowrank_tc(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
+                             static_cast<cudaStream_t>(stream));
+  }
   const int d = static_cast<int>(s->d), r = rank;
   size_t sm = sizeof(float) * (static_cast<size_t>(kTok) * (d + 1) + d * r + kTok * (r + 1) + r * d + kTok);
   dim3 grid(static_cast<unsigned>(ceil_div(s->L, kTok)), static_cast<unsigned>(s->B));

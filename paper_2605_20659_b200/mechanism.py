@@ -450,9 +450,11 @@ def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams
     if settings.compensator == "lowrank":
         if params.w_a.shape[0] != H or params.w_b.shape != (H, params.rank, d):
             raise ValueError("compensator weights do not match the head slice")
+        ws = _workspace(_lib.lib().ropeslr_lowrank_workspace_bytes(ctypes_ref(shp), ctypes_ref(tok), params.rank),
+                        dev)
         _lib.call("ropeslr_lowrank_branch", ctypes_ref(shp), ctypes_ref(tok), params.w_a.data_ptr(),
                   params.w_b.data_ptr(), params.rank, params.rms_lowrank.data_ptr(), float(settings.rms_eps),
-                  y_lr.data_ptr(), _ptr(o_lr), g_logit.data_ptr(), st)
+                  y_lr.data_ptr(), _ptr(o_lr), g_logit.data_ptr(), ws.data_ptr(), ws.numel(), st)
     else:
         if lin_proj is None:
             raise ValueError("the linear compensator needs the projections (q_lin, k_lin, v_lin)")
