@@ -243,6 +243,129 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
   }
 }
 
+// Top-k rows, one warp per (bh, query block) row, nb <= 32 * NPER.
+// MSB-first radix select (8-bit digits) on the order-preserving keys finds
+// the k-th best key T; rows keep every key < T and, on exact ties at T, the
+// lowest block indices (the stable order of mechanism.py:317).  The keys
+// stay in registers; each warp owns a 256-bin histogram in shared memory.
+template <int NPER>
+__global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __restrict__ scores, int nb,
+                                                               int64_t rows, int64_t L, int block, int topk, int kmax,
+                                                               int32_t* __restrict__ idx, int32_t* __restrict__ cnt,
+                                                               uint8_t* __restrict__ mask,
+                                                               unsigned long long* __restrict__ attended) {
+  __shared__ int hist_all[8][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (row >= rows) return;
+  int* hist = hist_all[warp];
+  const int64_t bh = row / nb;
+  const int qb = static_cast<int>(row % nb);
+  const double* srow = scores + row * nb;
+  uint64_t key[NPER];
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    key[i] = c < nb ? desc_key(srow[c]) : ~0ull;
+  }
+  int need = topk < nb ? topk : nb;
+  uint64_t prefix = 0, pmask = 0;
+  bool exact = false;  // the remaining bucket is taken whole
+#pragma unroll 1
+  for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if ((key[i] & pmask) == prefix && lane + 32 * i < nb) atomicAdd(&hist[(key[i] >> shift) & 255], 1);
+    __syncwarp();
+    int h8[8];
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      h8[i] = hist[lane * 8 + i];
+      tot += h8[i];
+    }
+    int incl = tot;  // inclusive scan of lane totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int excl = incl - tot;
+    // the bucket where the running count first reaches `need`
+    const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
+    const int src = __ffs(owner) - 1;
+    int bucket = 0, before = 0, cnt_b = 0;
+    if (lane == src) {
+      int run = excl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (run + h8[i] >= need) {
+          bucket = lane * 8 + i;
+          before = run;
+          cnt_b = h8[i];
+          break;
+        }
+        run += h8[i];
+      }
+    }
+    bucket = __shfl_sync(0xffffffffu, bucket, src);
+    before = __shfl_sync(0xffffffffu, before, src);
+    cnt_b = __shfl_sync(0xffffffffu, cnt_b, src);
+    need -= before;
+    prefix |= static_cast<uint64_t>(bucket) << shift;
+    pmask |= 255ull << shift;
+    __syncwarp();
+    if (cnt_b == need) {
+      exact = true;
+      break;
+    }
+  }
+  // selected: masked key below the prefix, or inside the final bucket (whole,
+  // or its `need` lowest-index members on exact ties)
+  bool sel[NPER];
+  int taken = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const bool valid = lane + 32 * i < nb;
+    const uint64_t km = key[i] & pmask;
+    bool s = valid && km < prefix;
+    const bool tie = valid && km == prefix;
+    if (exact) {
+      s = s || tie;
+    } else {
+      const unsigned bal = __ballot_sync(0xffffffffu, tie);
+      const int pos = taken + __popc(bal & ((1u << lane) - 1u));
+      s = s || (tie && pos < need);
+      taken += __popc(bal);
+    }
+    sel[i] = s;
+  }
+  int32_t* irow = idx + row * kmax;
+  uint8_t* mrow = mask ? mask + row * nb : nullptr;
+  int carry = 0;
+  long long ksum = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    const unsigned bal = __ballot_sync(0xffffffffu, sel[i]);
+    if (sel[i]) {
+      irow[carry + __popc(bal & ((1u << lane) - 1u))] = c;
+      ksum += block_size(L, block, c);
+    }
+    if (mrow && c < nb) mrow[c] = sel[i] ? 1 : 0;
+    carry += __popc(bal);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+  if (lane == 0) {
+    cnt[row] = carry;
+    atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
+  }
+}
+
 }  // namespace ropeslr
 
 using namespace ropeslr;
@@ -308,6 +431,24 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
               static_cast<unsigned>(BH));
     block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
     if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  }
+  if (sel->topk > 0 && nb <= 1024) {
+    const int64_t rows = BH * nb;
+    const unsigned grid = static_cast<unsigned>(ceil_div(rows, 8));
+    auto* att = reinterpret_cast<unsigned long long*>(attended);
+#define ROPESLR_SEL_CASE(NPER_)                                                                                 \
+  select_topk_warp_kernel<NPER_><<<grid, 256, 0, st>>>(scores, nb, rows, s->L, s->block, sel->topk, kmax, idx, \
+                                                        cnt, mask, att)
+    if (nb <= 128)
+      ROPESLR_SEL_CASE(4);
+    else if (nb <= 256)
+      ROPESLR_SEL_CASE(8);
+    else if (nb <= 512)
+      ROPESLR_SEL_CASE(16);
+    else
+      ROPESLR_SEL_CASE(32);
+#undef ROPESLR_SEL_CASE
+    return launch_status();
   }
   {
     const int n2 = next_pow2(nb);

@@ -154,6 +154,21 @@ def test_tie_goes_to_lower_block():
     assert not sel[:, 2:].any()
 
 
+@pytest.mark.parametrize("topk", [1, 3, 7])
+def test_all_scores_tied_takes_lowest_indices(topk):
+    """Every key block identical -> every score of a row ties -> the first
+    top-k block indices (stable descending order)."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((4, 8, 16), H=2)
+    k = k[:, :, :64].repeat(1, 1, 8, 1).contiguous()
+    res = P.block_sparse_attention(q, k, v, P.SparseSettings(block=64, topk=topk))
+    sel = res.selected.cpu().numpy()
+    want = np.zeros(8, dtype=bool)
+    want[:topk] = True
+    assert (sel == want).all()
+
+
 def test_batch_two_matches_single():
     import paper_2605_20659_b200 as P
 
