@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(256) fuse_output_kernel(const float* __restric
   }
 }
 
-size_t lowrank_tc_workspace_bytes(int64_t H, int r, int T, int Hg, int Wg);
+size_t lowrank_tc_workspace_bytes(int64_t B, int64_t H, int64_t L, int r, int T, int Hg, int Wg);
 bool lowrank_tc_eligible(const ropeslr_shape* s, int r);
 int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
                       int r, const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, void* ws,
@@ -352,7 +352,7 @@ extern "C" size_t ropeslr_lowrank_workspace_bytes(const ropeslr_shape* s, const 
                                                   int32_t rank) {
   if (!s || !t) return 0;
   if (!lowrank_tc_eligible(s, rank)) return 0;
-  return lowrank_tc_workspace_bytes(s->H, rank, t->grid_t, t->grid_h, t->grid_w);
+  return lowrank_tc_workspace_bytes(s->B, s->H, s->L, rank, t->grid_t, t->grid_h, t->grid_w);
 }
 
 extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a,

@@ -134,10 +134,11 @@ struct MainArgs {
   float eps;
   __nv_bfloat16* y_lr;  // [B, L, H, d]
   float* o_lr;          // [B, H, L, d] or null
-  float* g_logit;       // [B, L] or null
+  float* g_part;        // [B, H, L] per-head gate partials (reduced by gate_reduce_kernel)
 };
 
-// grid (ceil(L / 128), B), block 256.  R = rank (multiple of 16, <= 128).
+// grid (ceil(L / 128), H, B), block 256: one (token tile, head) per CTA.
+// R = rank (multiple of 16, <= 128).
 template <int R>
 __global__ void __launch_bounds__(kWarps * 32) lowrank_tc_kernel(MainArgs a) {
   constexpr int NA = R + 16;        // GEMM1 output columns (rank + gate hi/lo + pad)
@@ -149,7 +150,8 @@ __global__ void __launch_bounds__(kWarps * 32) lowrank_tc_kernel(MainArgs a) {
   uint8_t* sX = sWb + D * WBP;                // [kTokTile][XP]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int64_t b = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int h = blockIdx.y;
   const int64_t tok0 = static_cast<int64_t>(blockIdx.x) * kTokTile;
   const int nrows = a.T + a.Hg + a.Wg;
   // this thread's two token rows (g, g + 8) of the warp's 16-token slab
@@ -165,12 +167,11 @@ __global__ void __launch_bounds__(kWarps * 32) lowrank_tc_kernel(MainArgs a) {
     cy[i] = static_cast<int>(tt % a.Wg);
   }
   float gacc[2] = {0.f, 0.f};
+  {
   const uint32_t sWa_u = static_cast<uint32_t>(__cvta_generic_to_shared(sWa));
   const uint32_t sWb_u = static_cast<uint32_t>(__cvta_generic_to_shared(sWb));
   const uint32_t sX_u = static_cast<uint32_t>(__cvta_generic_to_shared(sX)) + warp * 16 * XP;
 
-  for (int h = 0; h < a.H; ++h) {
-    __syncthreads();  // previous head's smem consumers are done
     {
       const uint4* wa = reinterpret_cast<const uint4*>(a.waT + static_cast<int64_t>(h) * NA * D);
       for (int e = tid; e < NA * D / 8; e += blockDim.x) {
@@ -315,23 +316,35 @@ __global__ void __launch_bounds__(kWarps * 32) lowrank_tc_kernel(MainArgs a) {
                *reinterpret_cast<const uint4*>(slab + row * XP + c * 16));
     }
   }
-  if (a.g_logit != nullptr && t4 == 0) {
+  if (t4 == 0) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
-      if (tk[i] < a.L) a.g_logit[b * a.L + tk[i]] = gacc[i];
+      if (tk[i] < a.L) a.g_part[(b * a.H + h) * a.L + tk[i]] = gacc[i];
   }
+}
+
+// g_logit[b, l] = sum_h g_part[b, h, l] in fixed head order (deterministic).
+__global__ void gate_reduce_kernel(const float* __restrict__ g_part, int H, int64_t L, int64_t BL,
+                                   float* __restrict__ g_logit) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= BL) return;
+  const int64_t b = e / L, l = e % L;
+  const float* src = g_part + b * H * L + l;
+  float s = 0.f;
+  for (int h = 0; h < H; ++h) s += src[static_cast<int64_t>(h) * L];
+  g_logit[e] = s;
 }
 
 }  // namespace lr
 
-size_t lowrank_tc_workspace_bytes(int64_t H, int r, int T, int Hg, int Wg) {
+size_t lowrank_tc_workspace_bytes(int64_t B, int64_t H, int64_t L, int r, int T, int Hg, int Wg) {
   const size_t nrows = static_cast<size_t>(T + Hg + Wg);
   size_t wa = static_cast<size_t>(H) * (r + 16) * lr::D * 2;
   size_t wb = static_cast<size_t>(H) * lr::D * r * 2;
   size_t z = static_cast<size_t>(H) * nrows * r * 4;
   size_t gg = static_cast<size_t>(H) * nrows * 4;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  return up(wa) + up(wb) + up(z) + up(gg);
+  return up(wa) + up(wb) + up(z) + up(gg) + up(static_cast<size_t>(B * H * L) * 4);
 }
 
 bool lowrank_tc_eligible(const ropeslr_shape* s, int r) {
@@ -369,6 +382,8 @@ int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const
   f.Z = reinterpret_cast<float*>(p);
   p += up(static_cast<size_t>(H) * nrows * r * 4);
   f.G = reinterpret_cast<float*>(p);
+  p += up(static_cast<size_t>(H) * nrows * 4);
+  float* g_part = reinterpret_cast<float*>(p);
   lowrank_fold_kernel<<<dim3(nrows + 1, H), 128, 0, st>>>(f);
   if (launch_status()) return ROPESLR_ERR_LAUNCH;
 
@@ -389,8 +404,8 @@ int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const
   m.eps = eps;
   m.y_lr = static_cast<__nv_bfloat16*>(y_lr);
   m.o_lr = o_lr;
-  m.g_logit = g_logit;
-  dim3 grid(static_cast<unsigned>(ceil_div(s->L, kTokTile)), static_cast<unsigned>(s->B));
+  m.g_part = g_part;
+  dim3 grid(static_cast<unsigned>(ceil_div(s->L, kTokTile)), static_cast<unsigned>(H), static_cast<unsigned>(s->B));
 #define ROPESLR_LR_CASE(R_)                                                                                   \
   case R_: {                                                                                                  \
     const size_t sm = static_cast<size_t>(R_ + 16) * (D * 2 + 16) + static_cast<size_t>(D) * (R_ * 2 + 16) + \
@@ -411,6 +426,11 @@ int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const
       return ROPESLR_ERR_SHAPE;
   }
 #undef ROPESLR_LR_CASE
+  if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  if (g_logit != nullptr) {
+    const int64_t BL = s->B * s->L;
+    gate_reduce_kernel<<<static_cast<unsigned>(ceil_div(BL, 256)), 256, 0, st>>>(g_part, H, s->L, BL, g_logit);
+  }
   return launch_status();
 }
 
