@@ -42,6 +42,9 @@ CONFIGS = {
                       split=(44, 42, 42), block=128, sparsity=0.9, r=64),
 }
 METRIC = "RoPeSLR attn fwd ms & effective TFLOPS/GPU, L=118800, 90% sparse, 1/2/4/8 B200"
+# our launches per step: pool_blocks, block_scores, select_topk_warp (K1);
+# lowrank_fold, lowrank_tc, gate_reduce (K3); sparse_attn_tc (K2+K4)
+KERNELS_PER_STEP = 7
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -76,7 +79,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -306,9 +309,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         bo = hout.numel() * hout.element_size()
 
         def e2e_step():
-            dq, dk, dv, dx = (t.to(dev, non_blocking=True) for t in (hq, hk, hv, hx))
-            o = P.forward(dq, dk, dv, dx, grid, params, settings, pe, head_offset=h0, gate_reduce=reduce_)
-            hout.copy_(o, non_blocking=True)
+            # the public host-buffer API: H2D of X and Q/K/V (head chunks), the
+            # kernels and D2H of each chunk's output overlap inside the call
+            P.forward_host(hq, hk, hv, hx, grid, params, settings, pe, out=hout, head_offset=h0,
+                           gate_reduce=reduce_, chunk_heads=args.chunk_heads)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -362,7 +366,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "traffic": None,
                      "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)"},
         "clocks": clock_summary,
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": KERNELS_PER_STEP * args.steps,
     }
     if e2e is not None:
         line["e2e"] = {"value": flops_total / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
@@ -386,7 +390,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=list(CONFIGS), default="cfg3")
@@ -394,6 +398,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-qblocks", type=int, default=300)
     ap.add_argument("--ref-qblocks", type=int, default=100)
+    ap.add_argument("--chunk-heads", type=int, default=0, help="heads per H2D/compute chunk of the e2e path (0 = auto)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

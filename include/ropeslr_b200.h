@@ -188,6 +188,45 @@ int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* 
                          int32_t impl, void* workspace, size_t workspace_bytes, void* stream);
 size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* shape, int32_t impl);
 
+/* ------------------------------------- whole forward from HOST buffers
+ * The reference's calling convention (NumPy arrays in host memory,
+ * mechanism.py:491-512) for the low-rank compensator: copies X, then Q/K/V
+ * in head chunks, to the device on an internal copy stream, runs K3 once X
+ * is resident and K1 + K2/K4 per chunk as each chunk lands, and copies each
+ * chunk's output columns back on a second copy stream, so PCIe traffic in
+ * both directions overlaps the kernels.  Device scratch (activations,
+ * routing, staged parameters) comes from `workspace`.  Parameter pointers may
+ * be host or device memory.  Stream-ordered on `stream`: the host outputs
+ * are valid once `stream` has been synchronised.  Host activation buffers
+ * should be pinned (pageable memory works, without the overlap). */
+typedef struct ropeslr_host_forward {
+  ropeslr_shape shape;            /* H = heads of this call; dtype of q/k/v/x/out */
+  ropeslr_select_params sel;
+  const void* q;                  /* host [B, H, L, d] post-RoPE */
+  const void* k;
+  const void* v;
+  ropeslr_token_args tok;         /* tok.x: host X rows (x_row_stride elements apart) */
+  const float* w_a;               /* [H, d, r] */
+  const float* w_b;               /* [H, r, d] */
+  int32_t rank;
+  const float* rms_sparse;        /* [d] */
+  const float* rms_lowrank;       /* [d] */
+  float b_g;
+  float eps;
+  void* out;                      /* host [B, L, *]: this call's heads from column 0 */
+  int64_t out_row_stride;         /* elements between consecutive output rows */
+  int64_t* attended;              /* host [B, H] attended pairs, nullable */
+  int32_t chunk_heads;            /* heads per pipeline chunk; 0 = automatic */
+  /* Called once, on the calling thread, after the gate logits [B, L]
+   * (float32, device) have been enqueued on `stream` and before any use:
+   * head-parallel ranks enqueue their all-reduce here.  Nullable. */
+  void (*gate_hook)(float* g_logit, int64_t n, void* stream, void* user);
+  void* gate_hook_user;
+} ropeslr_host_forward;
+
+size_t ropeslr_forward_host_workspace_bytes(const ropeslr_host_forward* args);
+int ropeslr_forward_host(const ropeslr_host_forward* args, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,16 @@ class TokenArgs(ctypes.Structure):
                 ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp)]
 
 
+GateHook = ctypes.CFUNCTYPE(None, c_vp, c_i64, c_vp, c_vp)
+
+
+class HostForward(ctypes.Structure):
+    _fields_ = [("shape", Shape), ("sel", SelectParams), ("q", c_vp), ("k", c_vp), ("v", c_vp), ("tok", TokenArgs),
+                ("w_a", c_vp), ("w_b", c_vp), ("rank", c_i32), ("rms_sparse", c_vp), ("rms_lowrank", c_vp),
+                ("b_g", c_f32), ("eps", c_f32), ("out", c_vp), ("out_row_stride", c_i64), ("attended", c_vp),
+                ("chunk_heads", c_i32), ("gate_hook", GateHook), ("gate_hook_user", c_vp)]
+
+
 P = ctypes.POINTER
 _SIGNATURES = {
     "ropeslr_abi_version": (c_i32, []),
@@ -56,6 +66,8 @@ _SIGNATURES = {
     "ropeslr_attend_fused": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp,
                                      c_f32, c_vp, c_vp, c_i32, c_vp, c_sz, c_vp]),
     "ropeslr_attend_workspace_bytes": (c_sz, [P(Shape), c_i32]),
+    "ropeslr_forward_host_workspace_bytes": (c_sz, [P(HostForward)]),
+    "ropeslr_forward_host": (c_i32, [P(HostForward), c_vp, c_sz, c_vp]),
 }
 EXPORTED = tuple(_SIGNATURES)
 

@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(256) sparse_attn_simt_kernel(const T* __restri
       l[i] = l[i] * corr + psum;
 #pragma unroll
       for (int c = 0; c < DPL; ++c) o[i][c] *= corr;
-#pragma unroll
+#pragma unroll 1
       for (int u = 0; u < 4; ++u) {
+#pragma unroll 4
         for (int t = 0; t < 32; ++t) {
           const int kk = 32 * u + t;
           if (kk >= krows) break;

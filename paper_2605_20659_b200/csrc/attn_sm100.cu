@@ -102,6 +102,8 @@ struct Params {
   float eps;
   __nv_bfloat16* out;
   float* o_sparse;
+  int out_H;   // heads per token row of out / y_lr (>= H when a head chunk writes into a wider row)
+  int out_h0;  // first head of this call inside that row
   int kv_evict_last;
   int debug_mode;  // 0 normal; 1 no softmax math; 2 every K/V load hits block 0; 3 no K/V TMA
 };
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                               __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
         }
         if (p.out) {
-          const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.H + h) * D + col0;
+          const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
           const __nv_bfloat16* y = p.y_lr + orow;
           __nv_bfloat16* dst = p.out + orow;
 #pragma unroll
@@ -613,6 +615,8 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.L = s->L;
   prm.num_units = s->B * s->H * prm.nb;
   prm.perm = perm;
+  prm.out_H = static_cast<int>(s->H);
+  prm.out_h0 = 0;
   prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
   const char* pol = getenv("ROPESLR_KV_EVICT_LAST");
   prm.kv_evict_last = (pol != nullptr && pol[0] == '1') ? 1 : 0;
@@ -647,6 +651,32 @@ extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t
   if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
   return 0;
 }
+
+namespace ropeslr {
+// K2 + K4 (tcgen05 path only) writing heads [out_h0, out_h0 + H) of
+// out / y_lr rows that hold out_H heads: a head chunk of a wider forward
+// (forward_host.cu).
+int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k, const void* v, const int32_t* idx,
+                            int32_t kmax, const int32_t* cnt, const void* y_lr, const float* g_logit, float b_g,
+                            const float* rms_sparse, float eps, void* out, int out_H, int out_h0,
+                            cudaStream_t stream) {
+  int st = check_attn_args(s, q, k, v, idx, kmax, cnt);
+  if (st) return st;
+  if (!tc::tc_eligible(s)) return ROPESLR_ERR_VALUE;
+  if (out_h0 < 0 || out_h0 + s->H > out_H) return ROPESLR_ERR_SHAPE;
+  tc::Params prm = base_params(s, idx, kmax, cnt, nullptr);
+  prm.y_lr = static_cast<const __nv_bfloat16*>(y_lr);
+  prm.g_logit = g_logit;
+  prm.b_g = b_g;
+  prm.rms_sp = rms_sparse;
+  prm.eps = eps;
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.out_H = out_H;
+  prm.out_h0 = out_h0;
+  return launch_tc_dispatch(s, q, k, v, prm, stream);
+}
+bool attend_tc_eligible(const ropeslr_shape* s) { return tc::tc_eligible(s); }
+}  // namespace ropeslr
 
 extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                                     const int32_t* idx, int32_t kmax, const int32_t* cnt, const int32_t* row_perm,

@@ -306,6 +306,11 @@ __global__ void __launch_bounds__(256) fuse_output_kernel(const float* __restric
 
 size_t lowrank_tc_workspace_bytes(int64_t B, int64_t H, int64_t L, int r, int T, int Hg, int Wg);
 bool lowrank_tc_eligible(const ropeslr_shape* s, int r);
+bool lowrank_umma_eligible(const ropeslr_shape* s, const ropeslr_token_args* t, int r);
+size_t lowrank_umma_workspace_bytes(const ropeslr_shape* s, const ropeslr_token_args* t, int r);
+int launch_lowrank_umma(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
+                        int r, const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit,
+                        void* ws, cudaStream_t st);
 int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
                       int r, const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, void* ws,
                       cudaStream_t st);
@@ -351,6 +356,7 @@ using namespace ropeslr;
 extern "C" size_t ropeslr_lowrank_workspace_bytes(const ropeslr_shape* s, const ropeslr_token_args* t,
                                                   int32_t rank) {
   if (!s || !t) return 0;
+  if (lowrank_umma_eligible(s, t, rank)) return lowrank_umma_workspace_bytes(s, t, rank);
   if (!lowrank_tc_eligible(s, rank)) return 0;
   return lowrank_tc_workspace_bytes(s->B, s->H, s->L, rank, t->grid_t, t->grid_h, t->grid_w);
 }
@@ -365,6 +371,13 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
   if (s->d < 8 || s->d > 128 || s->d % 8) return ROPESLR_ERR_SHAPE;
   if (rank < 1 || rank > 256) return ROPESLR_ERR_SHAPE;
   if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  if (lowrank_umma_eligible(s, t, rank)) {
+    // tcgen05 / TMA path (bf16, d = 128, r in {16, 32, 48, 64})
+    if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned16(y_lr)) return ROPESLR_ERR_ALIGN;
+    if (!ws || ws_bytes < ropeslr_lowrank_workspace_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
+    return launch_lowrank_umma(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
+                               static_cast<cudaStream_t>(stream));
+  }
   if (lowrank_tc_eligible(s, rank)) {
     if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned16(y_lr)) return ROPESLR_ERR_ALIGN;
     if (!ws || ws_bytes < ropeslr_lowrank_workspace_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;

@@ -617,3 +617,95 @@ def forward_from_x(x: torch.Tensor, grid: GridShape, cfg: RopeConfig, backbone: 
         lin = tuple(torch.einsum("bld,hde->bhle", x_hat, w.to(torch.float64)).to(dtype)
                     for w in (backbone.w_q, backbone.w_k, backbone.w_v))
     return forward(q, k, v, xd, grid, params, settings, pe, lin_proj=lin, trace=trace, impl=impl)
+
+
+def forward_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, grid: GridShape,
+                 params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
+                 out: Optional[torch.Tensor] = None, head_offset: int = 0,
+                 gate_reduce: Optional[Callable[[torch.Tensor], None]] = None, chunk_heads: int = 0,
+                 device=None, sync: bool = True, want_attended: bool = False):
+    """The forward from HOST tensors, the reference's calling convention
+    (NumPy arrays in host memory, mechanism.py:491-512), through the C ABI
+    ``ropeslr_forward_host``: the host->device copies of X and of Q/K/V (in
+    head chunks) and the device->host copy of each chunk's output overlap the
+    kernels.  q, k, v: CPU [B, H, L, d] post-RoPE; x: CPU [B, L, H*d] (or a
+    column slice of a wider X); pinned memory gives the overlap.  Low-rank
+    compensator only.  Returns out (CPU [B, L, H*d]), plus the attended-pair
+    counts [B, H] when ``want_attended``."""
+    if settings.compensator != "lowrank":
+        raise ValueError("forward_host supports the low-rank compensator")
+    if isinstance(settings.sparse.block, tuple):
+        raise ValueError("forward_host takes flat blocks; use forward() for 3D tiles")
+    for t in (q, k, v, x):
+        if t.is_cuda:
+            raise ValueError("forward_host takes host tensors; use forward() for device tensors")
+    if q.dim() != 4 or k.shape != q.shape or v.shape != q.shape:
+        raise ValueError(f"expected host Q/K/V of one shape [B, H, L, d], got {tuple(q.shape)}")
+    if not (q.dtype == k.dtype == v.dtype == x.dtype):
+        raise ValueError("Q/K/V/X dtypes differ")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    B, H, L, d = q.shape
+    if x.dim() != 3 or x.shape[:2] != (B, L) or x.shape[2] < H * d or x.stride(2) != 1:
+        raise ValueError(f"expected host X [B, L, >= H*d] with unit column stride, got {tuple(x.shape)}")
+    if x.stride(0) != L * x.stride(1):
+        raise ValueError("X rows must have batch stride L * row stride")
+    if params.d_h != d or params.w_a.shape[0] != H:
+        raise ValueError("parameters do not match the head count / head dim")
+    dev = torch.device(device) if device is not None else params.w_a.device
+    if out is None:
+        out = torch.empty((B, L, H * d), dtype=q.dtype, pin_memory=q.is_pinned())
+    if out.is_cuda or out.shape[:2] != (B, L) or out.shape[2] < H * d or out.stride(2) != 1 or out.dtype != q.dtype:
+        raise ValueError("out must be a host tensor [B, L, >= H*d] of the input dtype")
+    attended = torch.zeros((B, H), dtype=torch.int64) if want_attended else None
+    tok = _token_args(x, grid, params, pe, settings.use_pe, head_offset, H, d)
+    args = _lib.HostForward()
+    args.shape = _lib.Shape(B, H, L, d, settings.sparse.block, _dtype_code(q))
+    args.sel = _lib.SelectParams(int(settings.sparse.topk), float(settings.sparse.keep))
+    args.q, args.k, args.v = q.data_ptr(), k.data_ptr(), v.data_ptr()
+    args.tok = tok
+    args.w_a, args.w_b, args.rank = params.w_a.data_ptr(), params.w_b.data_ptr(), params.rank
+    args.rms_sparse, args.rms_lowrank = params.rms_sparse.data_ptr(), params.rms_lowrank.data_ptr()
+    args.b_g, args.eps = float(params.b_g), float(settings.rms_eps)
+    args.out, args.out_row_stride = out.data_ptr(), out.stride(1)
+    args.attended = _ptr(attended)
+    args.chunk_heads = int(chunk_heads)
+    hook, hook_error = None, []
+    if gate_reduce is not None:
+        def _hook(g_ptr, n, stream_ptr, _user):
+            try:
+                g = _device_view_f32(g_ptr, n, dev).view(B, L)
+                cur = torch.cuda.current_stream(dev)
+                if (stream_ptr or 0) == cur.cuda_stream:
+                    gate_reduce(g)
+                else:
+                    with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=dev)):
+                        gate_reduce(g)
+            except BaseException as e:  # noqa: BLE001 -- re-raised after the C call returns
+                hook_error.append(e)
+        hook = _lib.GateHook(_hook)
+        args.gate_hook = hook
+    ws_bytes = _lib.lib().ropeslr_forward_host_workspace_bytes(ctypes_ref(args))
+    if ws_bytes == 0:
+        raise ValueError("forward_host: inconsistent arguments")
+    with torch.cuda.device(dev):
+        ws = _workspace(ws_bytes, dev)
+        st = _stream(dev)
+        _lib.call("ropeslr_forward_host", ctypes_ref(args), ws.data_ptr(), ws.numel(), st)
+        if hook_error:
+            torch.cuda.current_stream(dev).synchronize()
+            raise hook_error[0]
+        if sync:
+            torch.cuda.current_stream(dev).synchronize()
+        else:
+            # keep the workspace alive until the stream reaches this point
+            ws.record_stream(torch.cuda.current_stream(dev))
+    del hook
+    return (out, attended) if want_attended else out
+
+
+def _device_view_f32(ptr: int, n: int, dev) -> torch.Tensor:
+    """A float32 tensor over n elements of device memory owned by the caller."""
+    class _Buf:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4", "data": (int(ptr), False), "version": 3}
+
+    return torch.as_tensor(_Buf(), device=dev)
