@@ -13,22 +13,23 @@
 // tiles t = blockIdx.x, + gridDim.x, ...  Warp roles:
 //
 //   warp 0        TMA producer: X tile [128 tokens x 128 cols] (two 64-col
-//                 boxes, 128-byte swizzle) into a 3-stage ring
-//   warp 1        MMA issuer:  D1_w = X W_A^T   (M 128, N r+16, K 128)
-//                              D2_w = H1_w W_B^T (M 128, N 128, K 64)
-//                 in the order MMA1(i), MMA2(i-1), ...
+//                 boxes, 128-byte swizzle) into a 4-stage ring
+//   warp 1        MMA issuer:  D1_w = X W_A^T    (M 128, N r+16, K 128, A/B smem)
+//                              D2_w = H1_w W_B^T (M 128, N 128, K 64, A in TMEM)
+//                 as soon as their inputs are ready (GEMM2 first)
 //   warp 2        TMEM allocation (512 columns)
-//   warps 4-11    two epilogue warpgroups, WG w owns tiles i = w (mod 2) and
-//                 the TMEM buffers D1_w, D2_w and the smem operand H1_w.
-//                 Thread = token row: D1 row + Z gathers -> sigmoid -> bf16
-//                 into the swizzled H1 tile (GEMM2's A operand); gate partial;
-//                 D2 row -> sigmoid (written back to TMEM) -> RMSNorm *
-//                 rms_lowrank -> bf16 y_lr row.
-//
-// TMEM columns: D1_0 [0, 128), D1_1 [128, 256), D2_0 [256, 384), D2_1 [384, 512).
+//   warps 4-15    three epilogue warpgroups, WG w owns tiles i = w (mod 3),
+//                 the TMEM columns [128w, 128w + 128) (D1, then D2) and
+//                 [384 + 32w, +32) (H1_w).  Thread = token row: D1 row + Z
+//                 gathers -> sigmoid -> bf16 pairs stored to H1_w in TMEM
+//                 (GEMM2's A operand); gate partial; D2 row -> sigmoid ->
+//                 RMSNorm * rms_lowrank -> bf16 y_lr row.
+// Shared memory holds the 4-stage X ring (128 KiB, enough bytes in flight to
+// cover HBM latency), the W_A / W_B images and the Z / G tables.
 // HBM traffic per (token, head): 256 B of X in, 256 B of y_lr out.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
@@ -43,8 +44,10 @@ using namespace sm100;
 constexpr int D = 128;        // head dim
 constexpr int M = 128;        // tokens per tile (MMA rows)
 constexpr int KR = 64;        // GEMM2 K: rank padded to one 128-byte swizzle atom
-constexpr int XSTAGES = 3;
-constexpr int kThreads = 384;
+constexpr int XSTAGES = 4;
+constexpr int NWG = 3;                 // epilogue warpgroups
+constexpr int kThreads = 128 + NWG * 128;
+constexpr uint32_t H1_COL = 384;       // TMEM columns [384 + 32w, 384 + 32w + 32): H1_w, bf16 pairs
 
 template <int R>
 struct Lay {
@@ -52,22 +55,23 @@ struct Lay {
   static constexpr int X_BYTES = M * D * 2;      // 32 KiB
   static constexpr int WA_BYTES = N1 * D * 2;    // two 64-col atoms of N1 rows
   static constexpr int WB_BYTES = D * KR * 2;    // 16 KiB
-  static constexpr int H1_BYTES = M * KR * 2;    // 16 KiB
   static constexpr int OFF_X = 0;
   static constexpr int OFF_WA = OFF_X + XSTAGES * X_BYTES;
   static constexpr int OFF_WB = OFF_WA + (WA_BYTES + 1023) / 1024 * 1024;
-  static constexpr int OFF_H1 = OFF_WB + WB_BYTES;
-  static constexpr int OFF_BAR = OFF_H1 + 2 * H1_BYTES;
-  static constexpr int NBAR = 2 * XSTAGES + 12;   // X ring full/empty + 6 per-warpgroup pairs
-  static constexpr int OFF_TAB = OFF_BAR + 256;  // Z [nrows][R + 4] f32, then G [nrows] f32
+  static constexpr int OFF_BAR = OFF_WB + WB_BYTES;
+  static constexpr int NBAR = 2 * XSTAGES + 4 * NWG;  // X ring full/empty + 4 per warpgroup
+  static constexpr int OFF_RMS = OFF_BAR + 256;       // rms_lowrank [128] f32
+  static constexpr int OFF_TAB = OFF_RMS + D * 4;     // Z [nrows][R + 4] f32, then G [nrows] f32
+  static constexpr int ZP = R + 4;                    // Z row pitch (floats): float4 rows spread over the banks
   static_assert(NBAR * 8 + 4 <= 256, "barrier block overflows");
-  static constexpr int ZP = R + 4;               // Z row pitch (floats): float4 rows spread over the banks
   static int bytes(int nrows) { return OFF_TAB + nrows * (ZP + 1) * 4; }
 };
 
-enum Bar { XF = 0, XE = XSTAGES, D1F = 2 * XSTAGES, D1E = D1F + 2, H1F = D1E + 2, H1E = H1F + 2, D2F = H1E + 2,
-           D2E = D2F + 2, BAR_END = D2E + 2 };
-static_assert(BAR_END == 2 * XSTAGES + 12, "barrier enum and Lay::NBAR disagree");
+// Per warpgroup w: D1F (GEMM1 done), H1F (H1 written to TMEM), D2F (GEMM2
+// done), RE (its TMEM region read out: the next GEMM1 may overwrite it).
+enum Bar { XF = 0, XE = XSTAGES, D1F = 2 * XSTAGES, H1F = D1F + NWG, D2F = H1F + NWG, RE = D2F + NWG,
+           BAR_END = RE + NWG };
+static_assert(BAR_END == 2 * XSTAGES + 4 * NWG, "barrier enum and Lay::NBAR disagree");
 
 struct FoldArgs {
   const float* w_a;   // [H, d, r]
@@ -193,9 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
   uint8_t* sX = smem + Lay_::OFF_X;
   uint8_t* sWA = smem + Lay_::OFF_WA;
   uint8_t* sWB = smem + Lay_::OFF_WB;
-  uint8_t* sH1 = smem + Lay_::OFF_H1;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay_::OFF_BAR);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Lay_::OFF_BAR + Lay_::NBAR * 8);
+  float* sRms = reinterpret_cast<float*>(smem + Lay_::OFF_RMS);
   const int nrows = a.T + a.Hg + a.Wg;
   float* sZ = reinterpret_cast<float*>(smem + Lay_::OFF_TAB);
   float* sG = sZ + nrows * ZP;
@@ -216,12 +220,13 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
       *reinterpret_cast<float4*>(sZ + row * ZP + c4 * 4) = reinterpret_cast<const float4*>(z)[e];
     }
     for (int e = threadIdx.x; e < nrows; e += kThreads) sG[e] = a.G[static_cast<int64_t>(h) * nrows + e];
+    for (int e = threadIdx.x; e < D; e += kThreads) sRms[e] = a.rms_lr[e];
     fence_proxy_async_smem();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmX);
     for (int i = 0; i < Lay_::NBAR; ++i) {
-      const bool per_thread = (i >= D1E && i < D1E + 2) || (i >= H1F && i < H1F + 2) || (i >= D2E && i < D2E + 2);
+      const bool per_thread = (i >= H1F && i < H1F + NWG) || (i >= RE && i < RE + NWG);
       mbar_init(&bars[i], per_thread ? 128 : 1);
     }
     fence_mbar_init();
@@ -254,157 +259,180 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
+    // Tile i belongs to warpgroup w = i % NWG and its 128-column TMEM region
+    // (GEMM1 writes columns [0, N1), GEMM2 then all 128).  The warp polls
+    // instead of issuing in a fixed order: GEMM2 of the oldest tile whose H1
+    // is ready goes first, else GEMM1 of the next tile once its X stage has
+    // landed and its region has been drained -- so no warpgroup waits behind
+    // another one's epilogue.
     constexpr uint32_t idesc1 = idesc_bf16_f32(M, N1, false, false);
     constexpr uint32_t idesc2 = idesc_bf16_f32(M, D, false, false);
     const uint64_t dX0 = desc_sw128(smem_u32(sX), 16, 1024);
     const uint64_t dWA = desc_sw128(smem_u32(sWA), 16, 1024);
-    const uint64_t dH10 = desc_sw128(smem_u32(sH1), 16, 1024);
     const uint64_t dWB = desc_sw128(smem_u32(sWB), 16, 1024);
     const bool leader = elect_one();
-    for (int i = 0; i <= n_my; ++i) {
-      if (i < n_my) {
-        const int s = i % XSTAGES, w = i & 1;
-        mbar_wait(&bars[XF + s], (i / XSTAGES) & 1);
-        mbar_wait(&bars[D1E + w], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        if (leader) {
-          const uint64_t dX = dX0 + static_cast<uint64_t>((s * Lay_::X_BYTES) >> 4);
+    int n1 = 0, n2 = 0;
+    while (n2 < n_my) {
+      bool issued = false;
+      if (n2 < n1) {
+        const int w = n2 % NWG;
+        if (__all_sync(0xffffffffu, mbar_try_wait(&bars[H1F + w], (n2 / NWG) & 1))) {
+          tc_fence_after();
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint64_t da = dX + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
-            const uint64_t db = dWA + static_cast<uint64_t>(((kk >> 2) * (N1 * 128) + (kk & 3) * 32) >> 4);
-            mma_bf16_ss(tmem + w * 128, da, db, idesc1, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < KR / 16; ++kk) {
+              const uint64_t off = static_cast<uint64_t>((kk * 32) >> 4);
+              mma_bf16_ts(tmem + w * 128, tmem + H1_COL + w * 32 + kk * 8, dWB + off, idesc2, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&bars[D2F + w]);
           }
-          mma_commit(&bars[XE + s]);
-          mma_commit(&bars[D1F + w]);
+          __syncwarp();
+          ++n2;
+          issued = true;
         }
-        __syncwarp();
       }
-      if (i >= 1) {
-        const int j = i - 1, w = j & 1;
-        mbar_wait(&bars[H1F + w], (j >> 1) & 1);
-        mbar_wait(&bars[D2E + w], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        if (leader) {
-          const uint64_t dA = dH10 + static_cast<uint64_t>((w * Lay_::H1_BYTES) >> 4);
+      if (!issued && n1 < n_my) {
+        const int s = n1 % XSTAGES, w = n1 % NWG;
+        if (__all_sync(0xffffffffu, mbar_try_wait(&bars[XF + s], (n1 / XSTAGES) & 1) &&
+                                        mbar_try_wait(&bars[RE + w], ((n1 / NWG) & 1) ^ 1))) {
+          tc_fence_after();
+          if (leader) {
+            const uint64_t dX = dX0 + static_cast<uint64_t>((s * Lay_::X_BYTES) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < KR / 16; ++kk) {
-            const uint64_t off = static_cast<uint64_t>((kk * 32) >> 4);
-            mma_bf16_ss(tmem + 256 + w * 128, dA + off, dWB + off, idesc2, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint64_t da = dX + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
+              const uint64_t db = dWA + static_cast<uint64_t>(((kk >> 2) * (N1 * 128) + (kk & 3) * 32) >> 4);
+              mma_bf16_ss(tmem + w * 128, da, db, idesc1, kk > 0 ? 1u : 0u);
+            }
+            mma_commit(&bars[XE + s]);
+            mma_commit(&bars[D1F + w]);
           }
-          mma_commit(&bars[H1E + w]);
-          mma_commit(&bars[D2F + w]);
+          __syncwarp();
+          ++n1;
         }
-        __syncwarp();
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue warpgroups
     const int w = (warp - 4) >> 2;
     const int row = (threadIdx.x - 128) & 127;
-    const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    const uint32_t tD1 = lane_addr + w * 128;
-    const uint32_t tD2 = lane_addr + 256 + w * 128;
-    uint8_t* h1row = sH1 + w * Lay_::H1_BYTES;
-    const int64_t hw = static_cast<int64_t>(a.Hg) * a.Wg;
-    for (int i = w; i < n_my; i += 2) {
-      const int n = i >> 1;  // use count of this warpgroup's buffers
-      const int64_t tok = static_cast<int64_t>(first + i * stride) * M + row;
+    const uint32_t tlane = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t treg = tlane + w * 128;
+    const uint32_t th1 = tlane + H1_COL + w * 32;
+    const int hw = a.Hg * a.Wg;
+    for (int i = w; i < n_my; i += NWG) {
+      const uint32_t ph = (i / NWG) & 1;
+      const int t = first + i * stride;
+      const int64_t tok = static_cast<int64_t>(t) * M + row;
       const bool live = tok < a.L;
-      const int64_t tt = live ? tok : a.L - 1;
-      const int ct = static_cast<int>(tt / hw);
-      const int cx = a.T + static_cast<int>((tt % hw) / a.Wg);
-      const int cy = a.T + a.Hg + static_cast<int>(tt % a.Wg);
+      const int tt = static_cast<int>(live ? tok : a.L - 1);
+      const int ct = tt / hw;
+      const int rem = tt - ct * hw;
+      const int cxr = rem / a.Wg;
+      const int cx = a.T + cxr;
+      const int cy = a.T + a.Hg + (rem - cxr * a.Wg);
 
-      // ---- GEMM1 row -> + Z -> sigmoid -> bf16 H1 row; gate partial
-      mbar_wait(&bars[D1F + w], n & 1);
+      // ---- GEMM1 row (+ Z gathers) -> sigmoid -> bf16 H1 row; gate partial
+      mbar_wait(&bars[D1F + w], ph);
       tc_fence_after();
-      uint32_t d1[96];
-      tmem_ld32(tD1, d1);
-      tmem_ld32(tD1 + 32, d1 + 32);
-      if (N1 > 64) tmem_ld32(tD1 + 64, d1 + 64);
+      // one round trip: all of the row's GEMM1 columns (+ the gate pair) at once
+      uint32_t d1[R];
+      uint32_t gg[2];
+#pragma unroll
+      for (int c = 0; c < R / 16; ++c) tmem_ld16(treg + c * 16, d1 + c * 16);
+      tmem_ld2(treg + R, gg);
       tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&bars[D1E + w]);
-      float gpart = __uint_as_float(d1[R]) + __uint_as_float(d1[R + 1]);
+      float gpart = __uint_as_float(gg[0]) + __uint_as_float(gg[1]);
       if (a.use_pe) gpart += (sG[ct] + sG[cx]) + sG[cy];
-      uint32_t hp[KR / 2];
       const float* zt = sZ + ct * ZP;
       const float* zx = sZ + cx * ZP;
       const float* zy = sZ + cy * ZP;
 #pragma unroll
-      for (int c4 = 0; c4 < R / 4; ++c4) {
-        const float4 a4 = *reinterpret_cast<const float4*>(zt + c4 * 4);
-        const float4 b4 = *reinterpret_cast<const float4*>(zx + c4 * 4);
-        const float4 e4 = *reinterpret_cast<const float4*>(zy + c4 * 4);
-        const float v0 = __uint_as_float(d1[c4 * 4 + 0]) + ((a4.x + b4.x) + e4.x);
-        const float v1 = __uint_as_float(d1[c4 * 4 + 1]) + ((a4.y + b4.y) + e4.y);
-        const float v2 = __uint_as_float(d1[c4 * 4 + 2]) + ((a4.z + b4.z) + e4.z);
-        const float v3 = __uint_as_float(d1[c4 * 4 + 3]) + ((a4.w + b4.w) + e4.w);
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(sigmoid_fast(v0), sigmoid_fast(v1));
-        __nv_bfloat162 p1 = __floats2bfloat162_rn(sigmoid_fast(v2), sigmoid_fast(v3));
-        hp[c4 * 2] = *reinterpret_cast<uint32_t*>(&p0);
-        hp[c4 * 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
+      for (int c = 0; c < R / 16; ++c) {
+        uint32_t hp[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col = c * 16 + q * 4;
+          const float4 a4 = *reinterpret_cast<const float4*>(zt + col);
+          const float4 b4 = *reinterpret_cast<const float4*>(zx + col);
+          const float4 e4 = *reinterpret_cast<const float4*>(zy + col);
+          const float v0 = __uint_as_float(d1[col + 0]) + ((a4.x + b4.x) + e4.x);
+          const float v1 = __uint_as_float(d1[col + 1]) + ((a4.y + b4.y) + e4.y);
+          const float v2 = __uint_as_float(d1[col + 2]) + ((a4.z + b4.z) + e4.z);
+          const float v3 = __uint_as_float(d1[col + 3]) + ((a4.w + b4.w) + e4.w);
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(sigmoid_fast(v0), sigmoid_fast(v1));
+          __nv_bfloat162 p1 = __floats2bfloat162_rn(sigmoid_fast(v2), sigmoid_fast(v3));
+          hp[q * 2] = *reinterpret_cast<uint32_t*>(&p0);
+          hp[q * 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
+        }
+        tmem_st8(th1 + c * 8, hp);
       }
+      if (R < KR) {
+        const uint32_t zero[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-      for (int c = R / 2; c < KR / 2; ++c) hp[c] = 0u;
-      mbar_wait(&bars[H1E + w], (n & 1) ^ 1);
-#pragma unroll
-      for (int c = 0; c < KR / 8; ++c)
-        *reinterpret_cast<uint4*>(h1row + sw128(row, c)) = make_uint4(hp[4 * c], hp[4 * c + 1], hp[4 * c + 2], hp[4 * c + 3]);
-      fence_proxy_async_smem();
+        for (int c = R / 16; c < KR / 16; ++c) tmem_st8(th1 + c * 8, zero);
+      }
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars[H1F + w]);
       if (live) a.g_part[(static_cast<int64_t>(b) * a.H + h) * a.L + tok] = gpart;
 
-      // ---- GEMM2 row -> sigmoid (kept in TMEM) -> RMSNorm -> bf16 y_lr row
-      mbar_wait(&bars[D2F + w], n & 1);
+      // ---- GEMM2 row -> sigmoid -> RMSNorm -> bf16 y_lr row.  Pass 1 reads
+      // the row in two 64-column halves (one TMEM round trip each), applies
+      // the sigmoid, accumulates the fp32 sum of squares and writes the
+      // values back as fp16 pairs (2^-11 relative rounding, an eighth of the
+      // final bf16 ulp) into columns [0, 64) of the region; pass 2 reads those
+      // 64 packed columns in one round trip.
+      mbar_wait(&bars[D2F + w], ph);
       tc_fence_after();
       float ss = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tD2 + c * 32, o);
+#pragma unroll
+      for (int p2 = 0; p2 < 2; ++p2) {
+        uint32_t o[64];
+        tmem_ld32(treg + p2 * 64, o);
+        tmem_ld32(treg + p2 * 64 + 32, o + 32);
         tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float s = sigmoid_fast(__uint_as_float(o[e]));
-          ss = fmaf(s, s, ss);
-          o[e] = __float_as_uint(s);
+        for (int e = 0; e < 64; e += 2) {
+          const float s0 = sigmoid_fast(__uint_as_float(o[e]));
+          const float s1 = sigmoid_fast(__uint_as_float(o[e + 1]));
+          ss = fmaf(s0, s0, ss);
+          ss = fmaf(s1, s1, ss);
+          __half2 hh = __floats2half2_rn(s0, s1);
+          o[e / 2] = *reinterpret_cast<uint32_t*>(&hh);
         }
-        tmem_st32(tD2 + c * 32, o);
+        tmem_st32(treg + p2 * 32, o);
       }
       tmem_wait_st();
+      uint32_t sv[D / 2];
+      tmem_ld32(treg, sv);
+      tmem_ld32(treg + 32, sv + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars[RE + w]);
+      if (!live) continue;
       const float inv = rsqrtf(ss * (1.f / D) + a.eps);
       const int64_t yrow = ((static_cast<int64_t>(b) * a.L + tt) * a.H + h) * D;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tD2 + c * 32, o);
-        tmem_wait_ld();
-        if (c == D / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&bars[D2E + w]);
-        }
-        if (!live) continue;
+      uint4* dst = reinterpret_cast<uint4*>(a.y_lr + yrow);
+#pragma unroll
+      for (int e = 0; e < D / 8; ++e) {
+        const float4 w0 = *reinterpret_cast<const float4*>(sRms + 8 * e);
+        const float4 w1 = *reinterpret_cast<const float4*>(sRms + 8 * e + 4);
+        const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&sv[4 * e]));
+        const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&sv[4 * e + 1]));
+        const float2 f2 = __half22float2(*reinterpret_cast<const __half2*>(&sv[4 * e + 2]));
+        const float2 f3 = __half22float2(*reinterpret_cast<const __half2*>(&sv[4 * e + 3]));
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(f0.x * inv * w0.x, f0.y * inv * w0.y);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(f1.x * inv * w0.z, f1.y * inv * w0.w);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(f2.x * inv * w1.x, f2.y * inv * w1.y);
+        __nv_bfloat162 p3 = __floats2bfloat162_rn(f3.x * inv * w1.z, f3.y * inv * w1.w);
+        __stcs(dst + e, make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                                   *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3)));
         if (a.o_lr) {
-          float* dst = a.o_lr + ((static_cast<int64_t>(b) * a.H + h) * a.L + tok) * D + c * 32;
-#pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(dst + e) = make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]),
-                                                              __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+          float* od = a.o_lr + ((static_cast<int64_t>(b) * a.H + h) * a.L + tok) * D + 8 * e;
+          *reinterpret_cast<float4*>(od) = make_float4(f0.x, f0.y, f1.x, f1.y);
+          *reinterpret_cast<float4*>(od + 4) = make_float4(f2.x, f2.y, f3.x, f3.y);
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float2 wv = *reinterpret_cast<const float2*>(a.rms_lr + c * 32 + 2 * e);
-          __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(o[2 * e]) * inv * wv.x,
-                                                    __uint_as_float(o[2 * e + 1]) * inv * wv.y);
-          pk[e] = *reinterpret_cast<uint32_t*>(&hb);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(a.y_lr + yrow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) __stcs(dst + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
       }
     }
   }
