@@ -12,7 +12,9 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libropeslr_b200.so")
+# ROPESLR_LIBRARY points at an alternative build of the same library (kernel
+# variant experiments); the default is the in-tree build.
+LIB_PATH = os.environ.get("ROPESLR_LIBRARY") or os.path.join(PKG, "libropeslr_b200.so")
 
 F32, BF16 = 0, 1
 LOWRANK, LINEAR = 0, 1

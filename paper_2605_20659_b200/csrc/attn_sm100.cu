@@ -7,32 +7,36 @@
 //
 //   warp 0  TMA producer   Q tile once per unit, then K_j for every selected
 //                          key block j (contiguous [block, 128] boxes of the
-//                          [B*H, L, d] tensors, 128-byte swizzle), 2-stage ring.
-//   warp 3  TMA producer   V_j, its own 2-stage ring (a V slot frees only after
-//                          its PV, so it must not hold back the K prefetch).
-//   warp 1  MMA issuer     S_w = Q K_j^T into TMEM for w = j & 1, then
-//                          O_w += P_w V_j; tcgen05.commit releases smem
-//                          stages and signals the softmax warpgroups.
+//                          [B*H, L, d] tensors, 128-byte swizzle) into a
+//                          3-stage ring (4 for block 64).
+//   warp 3  TMA producer   V_j, its own ring (a V slot frees only after its
+//                          PV, so it must not hold back the K prefetch).
+//   warp 1  MMA issuer     S_b = Q K_j^T into TMEM buffer b = j & 1 (SS-MMA),
+//                          O += P_b V_j as a TS-MMA reading P from TMEM;
+//                          tcgen05.commit releases smem stages and signals.
 //   warp 2  TMEM owner     alloc / dealloc of the 512 columns.
-//   warps 4-7, 8-11        two softmax warpgroups; WG w owns the key blocks
-//                          j = w, w+2, ... of the unit with its own online
-//                          softmax state and its own TMEM accumulator O_w
-//                          (split-K over the key list).  One query row per
-//                          thread: tcgen05.ld of the S row, exp2-domain
-//                          softmax with the lazy (threshold 8) rescale of
-//                          O_w, bf16 P into swizzled smem for the PV MMA.
-//                          Two warps per SMSP hide each other's latency.
-//                          Epilogue: O = sum_w O_w 2^(m_w-m) / l, RMSNorm *
-//                          rms_sparse, + sigmoid(g_logit + b_g) * y_lr, bf16
-//                          store; WG w finalises columns [64w, 64w+64).
+//   warps 4-7, 8-11        two softmax warpgroups splitting every key block
+//                          by columns: WG w owns keys [w*B/2, (w+1)*B/2) of
+//                          each S tile, one query row per thread.  Row max =
+//                          max of the two halves (exchanged through shared
+//                          memory), exp2-domain softmax with the lazy
+//                          (threshold 2^8) rescale of O, bf16 P written back
+//                          over S_b.  Both warpgroups work on every tile, so
+//                          a tile's softmax takes half the time it would on
+//                          one warpgroup and overlaps the MMAs of the next.
+//                          Epilogue: O / l, RMSNorm * rms_sparse, +
+//                          sigmoid(g_logit + b_g) * y_lr, bf16 store; WG w
+//                          finalises O columns [64w, 64w + 64).
 //
-// TMEM columns: S0 [0,128), S1 [128,256), O0 [256,384), O1 [384,512).
-// Shared memory (block 128): Q 32K, K 2x32K, V 2x32K, P 2x32K = 224 KiB.
+// TMEM columns: S_0, S_1, S_2 at [0,128), [128,256), [256,384); O [384,512).
+// Shared memory (block 128): Q 32K, K 3x32K, V 3x32K = 224 KiB.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
+#include <unistd.h>
 
 #include "common.cuh"
 #include "sm100_ptx.cuh"
@@ -50,39 +54,46 @@ using namespace sm100;
 constexpr int D = 128;   // head dim handled by this kernel
 constexpr int M = 128;   // MMA rows (query rows per tile)
 constexpr int kThreads = 384;  // 4 control warps + 2 softmax warpgroups
+constexpr uint32_t O_COL = 256;  // TMEM columns: S_0 [0,128), S_1 [128,256), O_0 [256,384), O_1 [384,512)
+// setmaxnreg moves registers inside the CTA's own pool, which holds what the
+// launch allotted: 168 per thread (65536 / 384, rounded down to 8) x 384.
+constexpr int kLaunchRegs = 168;
+constexpr int kCtrlRegs = 72;       // per thread, control warpgroup (TMA, MMA, TMEM)
+constexpr int kSoftmaxRegs = 216;   // per thread, softmax warpgroups (two half rows in flight)
+static_assert(kCtrlRegs * 128 + kSoftmaxRegs * 256 <= kLaunchRegs * kThreads, "register pool overcommitted");
 
 template <int BLK>
 struct Layout {
   static constexpr int Q_BYTES = M * D * 2;
   static constexpr int KV_BYTES = BLK * D * 2;
-  static constexpr int P_BYTES = M * BLK * 2;
+  static constexpr int STAGES = BLK == 128 ? 3 : 4;        // K ring and V ring depth
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;
-  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
-  static constexpr int OFF_XCH = OFF_P + 2 * P_BYTES;      // epilogue exchange, 2 KiB
+  static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
+  static constexpr int OFF_XCH = OFF_V + STAGES * KV_BYTES;  // row-max / epilogue exchange, 2 KiB
   static constexpr int OFF_BAR = OFF_XCH + 2048;
-  static constexpr int NBAR = 22;
+  static constexpr int NBAR = 4 * STAGES + 12;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
   // dynamic smem starts 1024-aligned (after the driver's 1 KiB reservation);
   // the kernel traps if that ever changes
   static constexpr int ALLOC = BYTES;
+  static_assert(ALLOC <= 227 * 1024, "shared memory budget");
 };
 
-enum Bar {
-  Q_FULL = 0,
-  Q_EMPTY = 1,
-  K_FULL = 2,   // +stage
-  K_EMPTY = 4,  // +stage
-  V_FULL = 6,
-  V_EMPTY = 8,
-  S_FULL = 10,
-  S_EMPTY = 12,
-  P_FULL = 14,
-  P_EMPTY = 16,
-  PV_DONE = 18,
-  O_FULL = 20,
-  O_EMPTY = 21
+// Barrier indices (STAGES-dependent offsets for the K / V rings).
+template <int BLK>
+struct Bars {
+  static constexpr int ST = Layout<BLK>::STAGES;
+  static constexpr int Q_FULL = 0, Q_EMPTY = 1;
+  static constexpr int K_FULL = 2, K_EMPTY = K_FULL + ST;
+  static constexpr int V_FULL = K_EMPTY + ST, V_EMPTY = V_FULL + ST;
+  static constexpr int S_FULL = V_EMPTY + ST;  // +b: S_b = Q K_t^T landed
+  static constexpr int P_FULL = S_FULL + 2;    // +2b+w: warpgroup w's half of P_b written
+  static constexpr int PV_DONE = P_FULL + 4;   // +w: one phase per PV_w
+  static constexpr int O_FULL = PV_DONE + 2;
+  static constexpr int O_EMPTY = O_FULL + 1;
+  static constexpr int COUNT = O_EMPTY + 1;
+  static_assert(COUNT <= Layout<BLK>::NBAR, "barrier count");
 };
 
 struct Params {
@@ -106,7 +117,33 @@ struct Params {
   int out_h0;  // first head of this call inside that row
   int kv_evict_last;
   int debug_mode;  // 0 normal; 1 no softmax math; 2 every K/V load hits block 0; 3 no K/V TMA
+  long long* trace;  // TRACE
 };
+
+#ifdef ROPESLR_WATCHDOG
+__device__ volatile unsigned long long* g_watchdog;  // host-mapped
+// Debug builds: a wait that spins for more than ~2 s records (once per
+// waiter) who waited on what into host-mapped memory, then keeps waiting.
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, uint64_t* bars0, int line) {
+  const long long t0 = clock64();
+  bool reported = false;
+  while (!mbar_try_wait(bar, parity)) {
+    if (!reported && clock64() - t0 > 4000000000LL) {
+      reported = true;
+      const unsigned long long slot = atomicAdd(const_cast<unsigned long long*>(&g_watchdog[0]), 1ull);
+      if (slot < 30) {
+        volatile unsigned long long* e = g_watchdog + 2 + slot * 4;
+        e[0] = blockIdx.x;
+        e[1] = threadIdx.x;
+        e[2] = static_cast<unsigned long long>(bar - bars0) | (static_cast<unsigned long long>(parity) << 32);
+        e[3] = line;
+        __threadfence_system();
+      }
+    }
+  }
+}
+#define mbar_wait(b, ph) mbar_wait_wd((b), (ph), bars, __LINE__)
+#endif
 
 __device__ __forceinline__ bool elect_one_sync() {
   uint32_t pred = 0;
@@ -140,8 +177,96 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                         make_float2(0.2426103800535202f, 0.2426103800535202f));
   q = __ffma2_rn(q, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
   q = __ffma2_rn(q, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
-  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+  // q + (n << 23) (ptxas fuses the shift-add into one LEA)
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+
+// Fraction of the exponentials computed on the FMA pipe: pairs i with
+// (i % POLY_DEN) < POLY_NUM (the rest go to the MUFU).
+#ifndef ROPESLR_RESCALE_THRESHOLD
+#define ROPESLR_RESCALE_THRESHOLD 8.f
+#endif
+#ifndef ROPESLR_PREFETCH
+#define ROPESLR_PREFETCH 0
+#endif
+#ifndef ROPESLR_POLY_NUM
+#define ROPESLR_POLY_NUM 1
+#endif
+#ifndef ROPESLR_POLY_DEN
+#define ROPESLR_POLY_DEN 4
+#endif
+
+// Softmax of one half key block: warpgroup w owns keys [w*BLK/2, (w+1)*BLK/2)
+// of S tile t (one query row per thread) with its own running max / sum and
+// its own accumulator O_w (split-K over the key columns), so the two
+// warpgroups never wait for each other inside the key loop.  P_w = 2^(s*scale
+// - m_w) is written as bf16 pairs over the warpgroup's own S columns (P
+// column c of the half holds keys 2c, 2c+1).  RAGGED masks keys past the end
+// of the sequence (only the last key block).
+template <int BLK, bool RAGGED>
+__device__ __forceinline__ float half_softmax(uint32_t tSh, int valid, float scale_log2, bool first, float& m_run,
+                                              float& l_run) {
+  constexpr int HB = BLK / 2;
+  constexpr int NP = HB < 64 ? HB / 2 : 32;  // pairs per TMEM store
+  uint32_t sr[HB];
+#pragma unroll
+  for (int c = 0; c < HB / 32; ++c) tmem_ld32(tSh + c * 32, sr + c * 32);
+  tmem_wait_ld();
+  if (RAGGED) {
+#pragma unroll
+    for (int c = 0; c < HB; ++c)
+      if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+  }
+  float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < HB; c += 8) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      mq[q] = fmaxf(mq[q], fmaxf(__uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1])));
+  }
+  const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * scale_log2;
+  // lazy rescale: the running max moves only when it grows by more than 2^8
+  float alpha = 1.f;
+  if (first) {
+    m_run = mx;
+  } else if (mx > m_run + ROPESLR_RESCALE_THRESHOLD) {
+    alpha = ex2_approx(m_run - mx);
+    l_run *= alpha;
+    m_run = mx;
+  }
+  // a fully masked half (m = -inf) contributes exact zeros
+  const float m_eff = m_run == -INFINITY ? 0.f : m_run;
+  const float2 sc2 = make_float2(scale_log2, scale_log2);
+  const float2 nm2 = make_float2(-m_eff, -m_eff);
+  float2 sum2 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int h = 0; h < HB / (2 * NP); ++h) {
+    uint32_t pk[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const float2 x2 = __ffma2_rn(
+          make_float2(__uint_as_float(sr[h * 2 * NP + 2 * i]), __uint_as_float(sr[h * 2 * NP + 2 * i + 1])), sc2,
+          nm2);
+      float2 e2;
+      if ((i % ROPESLR_POLY_DEN) < ROPESLR_POLY_NUM) {
+        e2 = ex2_poly2(x2);  // FMA-pipe exp2 for a fraction of the scores: offloads the MUFU
+      } else {
+        e2.x = ex2_approx(x2.x);
+        e2.y = ex2_approx(x2.y);
+      }
+      sum2 = __fadd2_rn(sum2, e2);
+      __nv_bfloat162 hb = __floats2bfloat162_rn(e2.x, e2.y);
+      pk[i] = *reinterpret_cast<uint32_t*>(&hb);
+    }
+    if (NP == 32) {
+      tmem_st32(tSh + h * 32, pk);
+    } else {
+      tmem_st16(tSh + h * 16, pk);
+    }
+  }
+  l_run += sum2.x + sum2.y;
+  return alpha;
 }
 
 template <int BLK>
@@ -149,13 +274,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const Params p) {
   using Lay = Layout<BLK>;
+  using Bx = Bars<BLK>;
+  constexpr int ST = Lay::STAGES;
+  constexpr int HB = BLK / 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (smem_u32(smem_raw) & 1023u) __trap();
   uint8_t* sQ = smem + Lay::OFF_Q;
   uint8_t* sK = smem + Lay::OFF_K;
   uint8_t* sV = smem + Lay::OFF_V;
-  uint8_t* sP = smem + Lay::OFF_P;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Lay::OFF_BAR + Lay::NBAR * 8);
   float2* xch_ml = reinterpret_cast<float2*>(smem + Lay::OFF_XCH);  // [2][128] (m, l), then (ss, -)
@@ -167,10 +294,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    for (int i = 0; i < Lay::NBAR; ++i) {
+    for (int i = 0; i < Bx::COUNT; ++i) {
       uint32_t count = 1;
-      if (i == S_EMPTY || i == S_EMPTY + 1 || i == P_FULL || i == P_FULL + 1) count = 128;
-      if (i == O_EMPTY) count = 256;
+      if (i >= Bx::P_FULL && i < Bx::P_FULL + 4) count = 128;
+      if (i == Bx::O_EMPTY) count = 256;
       mbar_init(&bars[i], count);
     }
     fence_mbar_init();
@@ -193,133 +320,131 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 0 || warp == 3) {
-    if (elect_one_sync()) {
-      // ------------------------------------------- TMA producers
-      // warp 0: Q and K (K runs ahead: a K slot frees as soon as its QK^T
-      // completes); warp 3: V (a V slot frees only after its PV).
-      const bool is_k = (warp == 0);
-      const uint64_t pol_kv = p.kv_evict_last ? policy_evict_last() : policy_evict_normal();
-      const uint64_t pol_q = policy_evict_first();
-      const CUtensorMap* map = is_k ? &tmK : &tmV;
-      uint8_t* ring = is_k ? sK : sV;
-      const int full = is_k ? K_FULL : V_FULL;
-      const int empty = is_k ? K_EMPTY : V_EMPTY;
+  if (warp < 4) {
+    setmaxnreg_dec<kCtrlRegs>();
+    if (warp == 0 || warp == 3) {
+      if (elect_one_sync()) {
+        // ------------------------------------------- TMA producers
+        // warp 0: Q and K (K runs ahead: a K slot frees as soon as its QK^T
+        // completes); warp 3: V (a V slot frees only after its PV).
+        const bool is_k = (warp == 0);
+        const uint64_t pol_kv = p.kv_evict_last ? policy_evict_last() : policy_evict_normal();
+        const uint64_t pol_q = policy_evict_first();
+        const CUtensorMap* map = is_k ? &tmK : &tmV;
+        uint8_t* ring = is_k ? sK : sV;
+        const int full = is_k ? Bx::K_FULL : Bx::V_FULL;
+        const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
+        uint32_t g = 0, uc = 0;
+        for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+          const int bh = static_cast<int>(u / p.nb);
+          const int n = p.cnt[u];
+          const int32_t* irow = p.idx + u * p.kmax;
+          if (is_k) {
+            const int qb = static_cast<int>(u % p.nb);
+            mbar_wait(&bars[Bx::Q_EMPTY], (uc & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * BLK * 128);
+            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * BLK, bh, pol_q);
+            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * BLK, bh, pol_q);
+          }
+          for (int j = 0; j < n; ++j, ++g) {
+            const int kb = p.debug_mode == 2 ? 0 : irow[j];
+            const int s = g % ST;
+            const uint32_t ph = (g / ST) & 1;
+            uint8_t* dst = ring + s * Lay::KV_BYTES;
+            mbar_wait(&bars[empty + s], ph ^ 1);
+            if (p.debug_mode == 3) {
+              mbar_arrive(&bars[full + s]);
+              continue;
+            }
+            mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
+            tma_load_3d_hint(dst, map, &bars[full + s], 0, kb * BLK, bh, pol_kv);
+            tma_load_3d_hint(dst + BLK * 128, map, &bars[full + s], 64, kb * BLK, bh, pol_kv);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ------------------------------------------------ MMA issuer
+      // The whole warp runs the (uniform) control flow and waits; one
+      // elected lane issues tcgen05.mma / commit.  Global tile t uses S
+      // buffer b = t & 1: S_b = Q K_t^T (SS-MMA, TMEM columns [128b, +BLK)).
+      // Warpgroup w turns its key half into P (bf16 pairs over its own S
+      // columns [128b + w*BLK/2, +BLK/4)) and O_w += P_w V_t[w half] runs as
+      // a TS-MMA with K = BLK/2.  Issue order per unit: QK(0), QK(1), then
+      // [PV_0(j-2), PV_1(j-2), QK(j)], then the last two tiles' PVs: QK(j)
+      // overwrites what PV(j-2) reads, and the tensor pipe executes a CTA's
+      // MMAs in issue order.
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(M, BLK, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(M, D, false, true);
+      // descriptor bases; the K-step offsets below are added to the low word
+      // (start address field, 16-byte units, no carry: smem < 256 KiB)
+      const uint64_t dQ = desc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = desc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
+      const bool leader = elect_one_sync();
       uint32_t g = 0, uc = 0;
       for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
-        const int bh = static_cast<int>(u / p.nb);
         const int n = p.cnt[u];
-        const int32_t* irow = p.idx + u * p.kmax;
-        if (is_k) {
-          const int qb = static_cast<int>(u % p.nb);
-          mbar_wait(&bars[Q_EMPTY], (uc & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars[Q_FULL], 2 * BLK * 128);
-          tma_load_3d_hint(sQ, &tmQ, &bars[Q_FULL], 0, qb * BLK, bh, pol_q);
-          tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Q_FULL], 64, qb * BLK, bh, pol_q);
-        }
-        for (int j = 0; j < n; ++j, ++g) {
-          const int kb = p.debug_mode == 2 ? 0 : irow[j];
-          const int s = g & 1;
-          const uint32_t ph = (g >> 1) & 1;
-          uint8_t* dst = ring + s * Lay::KV_BYTES;
-          mbar_wait(&bars[empty + s], ph ^ 1);
-          if (p.debug_mode == 3) {
-            mbar_arrive(&bars[full + s]);
-            continue;
+        mbar_wait(&bars[Bx::Q_FULL], uc & 1);
+        tc_fence_after();
+        for (int j = 0; j < n + 2; ++j) {
+          if (j >= 2) {
+            const uint32_t t = g + j - 2;
+            const int s = t % ST;
+            const int b = t & 1;
+            mbar_wait(&bars[Bx::V_FULL + s], (t / ST) & 1);
+            if (j == 2) mbar_wait(&bars[Bx::O_EMPTY], (uc & 1) ^ 1);
+#pragma unroll 1
+            for (int w = 0; w < 2; ++w) {
+              mbar_wait(&bars[Bx::P_FULL + b * 2 + w], (t >> 1) & 1);
+              tc_fence_after();
+              if (leader) {
+                const uint32_t tP = tmem + b * 128 + w * HB;
+                const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES + w * HB * 128) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < HB / 16; ++kk) {
+                  const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
+                  mma_bf16_ts(tmem + O_COL + w * 128, tP + kk * 8, db, idesc_pv, (j > 2 || kk > 0) ? 1u : 0u);
+                }
+                mma_commit(&bars[Bx::PV_DONE + w]);
+                if (w == 1) mma_commit(&bars[Bx::V_EMPTY + s]);
+              }
+              __syncwarp();
+            }
           }
-          mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
-          tma_load_3d_hint(dst, map, &bars[full + s], 0, kb * BLK, bh, pol_kv);
-          tma_load_3d_hint(dst + BLK * 128, map, &bars[full + s], 64, kb * BLK, bh, pol_kv);
+          if (j < n) {
+            const uint32_t t = g + j;
+            const int s = t % ST;
+            const int b = t & 1;
+            mbar_wait(&bars[Bx::K_FULL + s], (t / ST) & 1);
+            tc_fence_after();
+            if (leader) {
+              const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint64_t da = dQ + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
+                const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
+                mma_bf16_ss(tmem + b * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+              }
+              mma_commit(&bars[Bx::K_EMPTY + s]);
+              mma_commit(&bars[Bx::S_FULL + b]);
+              if (j == n - 1) mma_commit(&bars[Bx::Q_EMPTY]);
+            }
+            __syncwarp();
+          }
         }
+        if (leader) mma_commit(&bars[Bx::O_FULL]);
+        __syncwarp();
+        g += n;
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    // The whole warp runs the (uniform) control flow and waits; one elected
-    // lane issues tcgen05.mma / commit, so descriptors live in uniform
-    // registers.  Key block j is owned by softmax warpgroup w = j & 1:
-    // S_w = Q K_j^T, P_w from that WG, O_w += P_w V_j.  Issue order per unit:
-    // QK(0), QK(1), [QK(j), PV(j-2)] for j >= 2, then PV(n-2), PV(n-1).
-    constexpr uint32_t idesc_qk = idesc_bf16_f32(M, BLK, false, false);
-    constexpr uint32_t idesc_pv = idesc_bf16_f32(M, D, false, true);
-    // descriptor bases; the K-step offsets below are added to the low word
-    // (start address field, 16-byte units, no carry: smem < 256 KiB)
-    const uint64_t dQ = desc_sw128(smem_u32(sQ), 16, 1024);
-    const uint64_t dK0 = desc_sw128(smem_u32(sK), 16, 1024);
-    const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
-    const uint64_t dP0 = desc_sw128(smem_u32(sP), 16, 1024);
-    const bool leader = elect_one_sync();
-    uint32_t g = 0, uc = 0;
-    uint32_t qk0 = 0, qk1 = 0, pv0 = 0, pv1 = 0;
-    for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
-      const int n = p.cnt[u];
-      mbar_wait(&bars[Q_FULL], uc & 1);
-      tc_fence_after();
-      for (int j = 0; j < n + 2; ++j) {
-        if (j < n) {
-          const uint32_t gg = g + j;
-          const int s = gg & 1;
-          const int w = j & 1;
-          const uint32_t cntw = w ? qk1 : qk0;
-          mbar_wait(&bars[K_FULL + s], (gg >> 1) & 1);
-          mbar_wait(&bars[S_EMPTY + w], (cntw & 1) ^ 1);
-          tc_fence_after();
-          if (leader) {
-            const uint32_t tS = tmem + w * 128;
-            const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t da = dQ + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
-              const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
-              mma_bf16_ss(tS, da, db, idesc_qk, kk > 0 ? 1u : 0u);
-            }
-            mma_commit(&bars[K_EMPTY + s]);
-            mma_commit(&bars[S_FULL + w]);
-            if (j == n - 1) mma_commit(&bars[Q_EMPTY]);
-          }
-          __syncwarp();
-          if (w) ++qk1; else ++qk0;
-        }
-        if (j >= 2) {
-          const int jp = j - 2;
-          const uint32_t gp = g + jp;
-          const int s = gp & 1;
-          const int w = jp & 1;
-          const uint32_t cntw = w ? pv1 : pv0;
-          mbar_wait(&bars[V_FULL + s], (gp >> 1) & 1);
-          mbar_wait(&bars[P_FULL + w], cntw & 1);
-          if (jp == 0) mbar_wait(&bars[O_EMPTY], (uc & 1) ^ 1);
-          tc_fence_after();
-          if (leader) {
-            const uint32_t tO = tmem + 256 + w * 128;
-            const uint64_t dP = dP0 + static_cast<uint64_t>((w * Lay::P_BYTES) >> 4);
-            const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
-#pragma unroll
-            for (int kk = 0; kk < BLK / 16; ++kk) {
-              const uint64_t da = dP + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
-              const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
-              mma_bf16_ss(tO, da, db, idesc_pv, (jp >= 2 || kk > 0) ? 1u : 0u);
-            }
-            mma_commit(&bars[V_EMPTY + s]);
-            mma_commit(&bars[P_EMPTY + w]);
-          }
-          __syncwarp();
-          if (w) ++pv1; else ++pv0;
-        }
-      }
-      if (leader) mma_commit(&bars[O_FULL]);
-      __syncwarp();
-      g += n;
-    }
-  } else if (warp >= 4) {
+  } else {
+    setmaxnreg_inc<kSoftmaxRegs>();
     // ------------------------------------ softmax warpgroups + epilogue
-    const int w = (warp - 4) >> 2;                 // 0: even key blocks, 1: odd
+    const int w = (warp - 4) >> 2;                 // key-column half of every tile
     const int row = (threadIdx.x - 128) & 127;     // query row == TMEM lane
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    const uint32_t tS = lane_addr + w * 128;
-    const uint32_t tO = lane_addr + 256 + w * 128;
-    uint8_t* prow_base = sP + w * Lay::P_BYTES + row * 128;
-    uint32_t cnt = 0, uc = 0;
+    const uint32_t tO = lane_addr + O_COL + w * 128;
+    uint32_t g = 0, uc = 0;
     for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
       const int bh = static_cast<int>(u / p.nb);
       const int qb = static_cast<int>(u % p.nb);
@@ -327,46 +452,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t* irow = p.idx + u * p.kmax;
       const int qrows = block_size(p.L, BLK, qb);
       float m_run = -INFINITY, l_run = 0.f;
-      for (int j = w; j < n; j += 2, ++cnt) {
+      for (int j = 0; j < n; ++j) {
+        const uint32_t t = g + j;
+        const int b = t & 1;
         const int kreal = block_size(p.L, BLK, irow[j]);
-        mbar_wait(&bars[S_FULL + w], cnt & 1);
+        mbar_wait(&bars[Bx::S_FULL + b], (t >> 1) & 1);
         tc_fence_after();
+        const bool trc = p.trace && blockIdx.x == 0 && row == 0 && t < 64;
+        if (trc) p.trace[(w * 64 + t) * 4 + 0] = clock64();
+        const uint32_t tSh = lane_addr + b * 128 + w * HB;
+        const int valid = kreal - w * HB;
+        float alpha;
         if (p.debug_mode == 1) {
-          tc_fence_before();
-          mbar_arrive(&bars[S_EMPTY + w]);
-          mbar_wait(&bars[P_EMPTY + w], (cnt & 1) ^ 1);
           m_run = 0.f;
           l_run = 1.f;
-          fence_proxy_async_smem();
-          tc_fence_before();
-          mbar_arrive(&bars[P_FULL + w]);
-          continue;
+          alpha = 1.f;
+        } else if (valid < HB) {
+          alpha = half_softmax<BLK, true>(tSh, valid, p.scale_log2, j == 0, m_run, l_run);
+        } else {
+          alpha = half_softmax<BLK, false>(tSh, HB, p.scale_log2, j == 0, m_run, l_run);
         }
-        // pass 1: row max (TMEM is re-read in pass 2 instead of holding 128 registers)
-        float mx = -INFINITY;
-#pragma unroll
-        for (int h2 = 0; h2 < BLK / 64; ++h2) {
-          uint32_t sr[64];
-          tmem_ld32(tS + h2 * 64, sr);
-          tmem_ld32(tS + h2 * 64 + 32, sr + 32);
-          tmem_wait_ld();
-          if (kreal == BLK) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
-          } else {
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (h2 * 64 + c < kreal) mx = fmaxf(mx, __uint_as_float(sr[c]));
-          }
-        }
-        mx *= p.scale_log2;
-        // P_w free <=> this WG's previous PV into O_w has completed
-        mbar_wait(&bars[P_EMPTY + w], (cnt & 1) ^ 1);
-        if (j == w) {
-          m_run = mx;
-        } else if (mx > m_run + 8.f) {
-          // lazy rescale: only when the running max grows by more than 2^8
-          const float alpha = ex2_approx(m_run - mx);
+        // tcgen05.ld / st are warp-collective: the rescale runs for the whole
+        // warp when any of its rows needs it (alpha == 1 for the others)
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          // PV_w(t-1), the last writer of O_w, must have landed before O_w is
+          // rescaled (PV_w(t-2) is covered by S_t's commit)
+          mbar_wait(&bars[Bx::PV_DONE + w], (t - 1) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
@@ -377,139 +488,85 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
             tmem_st32(tO + c * 32, o);
           }
-          tmem_wait_st();
-          l_run *= alpha;
-          m_run = mx;
         }
-        // pass 2: p = 2^(s * scale - m), bf16 P rows into the swizzled smem tile
-        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-        const float2 nm2 = make_float2(-m_run, -m_run);
-        float2 sum2 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int h2 = 0; h2 < BLK / 64; ++h2) {
-          uint32_t sr[64];
-          tmem_ld32(tS + h2 * 64, sr);
-          tmem_ld32(tS + h2 * 64 + 32, sr + 32);
-          tmem_wait_ld();
-          if (h2 == BLK / 64 - 1) {
-            tc_fence_before();
-            mbar_arrive(&bars[S_EMPTY + w]);
-          }
-          if (kreal < BLK) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (h2 * 64 + c >= kreal) sr[c] = __float_as_uint(-INFINITY);
-          }
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int i = cc * 4 + q;
-              const float2 x2 =
-                  __ffma2_rn(make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), sc2, nm2);
-              float2 e2;
-              if (q == 3) {
-                e2 = ex2_poly2(x2);  // FMA-pipe exp2 for 1/4 of the scores: offloads the MUFU
-              } else {
-                e2.x = ex2_approx(x2.x);
-                e2.y = ex2_approx(x2.y);
-              }
-              sum2 = __fadd2_rn(sum2, e2);
-              __nv_bfloat162 hb = __floats2bfloat162_rn(e2.x, e2.y);
-              pk[q] = *reinterpret_cast<uint32_t*>(&hb);
-            }
-            *reinterpret_cast<uint4*>(prow_base + h2 * (M * 128) + ((cc ^ (row & 7)) << 4)) =
-                make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          }
-        }
-        l_run += sum2.x + sum2.y;
-        fence_proxy_async_smem();
+        if (trc) p.trace[(w * 64 + t) * 4 + 1] = clock64();
+        tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars[P_FULL + w]);
+        mbar_arrive(&bars[Bx::P_FULL + b * 2 + w]);
+        if (trc) p.trace[(w * 64 + t) * 4 + 2] = clock64();
       }
+      g += n;
       // ---------------------------------------------- fused epilogue
       // merge the two partial softmaxes: O = sum_w O_w 2^(m_w - m), l likewise
-      mbar_wait(&bars[O_FULL], uc & 1);
+      mbar_wait(&bars[Bx::O_FULL], uc & 1);
       tc_fence_after();
       xch_ml[w * 128 + row] = make_float2(m_run, l_run);
       named_bar_sync(1, 256);
       const float2 other = xch_ml[(w ^ 1) * 128 + row];
       const float m0 = w == 0 ? m_run : other.x, l0 = w == 0 ? l_run : other.y;
       const float m1 = w == 0 ? other.x : m_run, l1 = w == 0 ? other.y : l_run;
-      const bool has1 = n > 1;  // warpgroup 1 owned at least one key block
-      const float mm = has1 ? fmaxf(m0, m1) : m0;
-      const float f0 = ex2_approx(m0 - mm);
-      const float f1 = has1 ? ex2_approx(m1 - mm) : 0.f;
+      const float mm = fmaxf(m0, m1);
+      const float f0 = m0 == -INFINITY ? 0.f : ex2_approx(m0 - mm);
+      const float f1 = m1 == -INFINITY ? 0.f : ex2_approx(m1 - mm);
       const float inv_l = 1.f / (l0 * f0 + l1 * f1);
       const float s0 = f0 * inv_l, s1 = f1 * inv_l;
-      // this warpgroup finalises columns [64w, 64w + 64) of its rows, 32 at a
-      // time: pass 1 accumulates the sum of squares, pass 2 re-reads TMEM and stores
-      auto merged = [&](int c, uint32_t* ob) {
+      // this warpgroup finalises columns [64w, 64w + 64) of its row
+      uint32_t ob[64];
+      {
         uint32_t t1[32];
-        tmem_ld32(lane_addr + 256 + w * 64 + c * 32, ob);
-        if (has1) tmem_ld32(lane_addr + 384 + w * 64 + c * 32, t1);
-        tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float o1 = has1 ? __uint_as_float(t1[i]) * s1 : 0.f;
-          ob[i] = __float_as_uint(fmaf(__uint_as_float(ob[i]), s0, o1));
+        for (int c = 0; c < 2; ++c) {
+          tmem_ld32(lane_addr + O_COL + w * 64 + c * 32, ob + c * 32);
+          tmem_ld32(lane_addr + O_COL + 128 + w * 64 + c * 32, t1);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            ob[c * 32 + i] = __float_as_uint(fmaf(__uint_as_float(ob[c * 32 + i]), s0, __uint_as_float(t1[i]) * s1));
         }
-      };
-      float ss = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t ob[32];
-        merged(c, ob);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) ss = fmaf(__uint_as_float(ob[i]), __uint_as_float(ob[i]), ss);
       }
+      tc_fence_before();
+      mbar_arrive(&bars[Bx::O_EMPTY]);
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) ss = fmaf(__uint_as_float(ob[i]), __uint_as_float(ob[i]), ss);
       named_bar_sync(1, 256);  // both warpgroups have read the (m, l) exchange
       xch_ml[w * 128 + row].x = ss;
       named_bar_sync(1, 256);
       ss += xch_ml[(w ^ 1) * 128 + row].x;
+      named_bar_sync(1, 256);  // the exchange area is free for the next unit
       const bool live = row < qrows;
+      if (!live) continue;
       const int64_t flat = static_cast<int64_t>(qb) * BLK + row;
-      const int64_t tok = live ? (p.perm ? p.perm[flat] : flat) : 0;
+      const int64_t tok = p.perm ? p.perm[flat] : flat;
       const int b = bh / p.H, h = bh % p.H;
       const float inv = 1.f / sqrtf(ss / static_cast<float>(D) + p.eps);
-      const float gate = (live && p.out) ? sigmoidf_stable(p.g_logit[static_cast<int64_t>(b) * p.L + tok] + p.b_g) : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t ob[32];
-        merged(c, ob);
-        if (c == 1) {
-          tc_fence_before();
-          mbar_arrive(&bars[O_EMPTY]);
-        }
-        if (!live) continue;
-        const int col0 = w * 64 + c * 32;
-        if (p.o_sparse) {
-          float* dst = p.o_sparse + (static_cast<int64_t>(bh) * p.L + tok) * D + col0;
+      const int col0 = w * 64;
+      if (p.o_sparse) {
+        float* dst = p.o_sparse + (static_cast<int64_t>(bh) * p.L + tok) * D + col0;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
-                                                              __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
-        }
-        if (p.out) {
-          const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
-          const __nv_bfloat16* y = p.y_lr + orow;
-          __nv_bfloat16* dst = p.out + orow;
+        for (int i = 0; i < 64; i += 4)
+          *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
+                                                            __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
+      }
+      if (p.out) {
+        const float gate = sigmoidf_stable(p.g_logit[static_cast<int64_t>(b) * p.L + tok] + p.b_g);
+        const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
+        const __nv_bfloat16* y = p.y_lr + orow;
+        __nv_bfloat16* dst = p.out + orow;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
-            const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
-            uint4 uo;
-            __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
+        for (int i = 0; i < 64; i += 8) {
+          const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
+          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
+          uint4 uo;
+          __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 yv = __bfloat1622float2(hy[e]);
-              const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
-              const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
-              ho[e] = __floats2bfloat162_rn(o0, o1);
-            }
-            __stcs(reinterpret_cast<uint4*>(dst + i), uo);
+          for (int e = 0; e < 4; ++e) {
+            const float2 yv = __bfloat1622float2(hy[e]);
+            const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
+            const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
+            ho[e] = __floats2bfloat162_rn(o0, o1);
           }
+          __stcs(reinterpret_cast<uint4*>(dst + i), uo);
         }
       }
     }
@@ -562,6 +619,41 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
     return ROPESLR_ERR_LAUNCH;
   const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
   kfn<<<static_cast<unsigned>(grid), kThreads, Layout<BLK>::ALLOC, st>>>(mq, mk, mv, prm);
+#ifdef ROPESLR_WATCHDOG
+  {
+    static unsigned long long* hbuf = nullptr;
+    if (!hbuf) {
+      cudaHostAlloc(&hbuf, 4096, cudaHostAllocMapped);
+      void* dptr = nullptr;
+      cudaHostGetDevicePointer(&dptr, hbuf, 0);
+      cudaMemcpyToSymbol(g_watchdog, &dptr, sizeof(dptr));
+    }
+    // (the pointer is set before this launch on the first call: re-launch note below)
+    for (int i = 0; i < 60; ++i) {
+      if (cudaStreamQuery(st) == cudaSuccess) break;
+      usleep(100000);
+      if (hbuf[0]) {
+        usleep(500000);
+        fprintf(stderr, "WATCHDOG %llu waiters (S_FULL=%d P_FULL=%d PV_DONE=%d O_FULL=%d O_EMPTY=%d V_FULL=%d K_FULL=%d)\n",
+                hbuf[0], Bars<BLK>::S_FULL, Bars<BLK>::P_FULL, Bars<BLK>::PV_DONE, Bars<BLK>::O_FULL,
+                Bars<BLK>::O_EMPTY, Bars<BLK>::V_FULL, Bars<BLK>::K_FULL);
+        for (unsigned long long k = 0; k < hbuf[0] && k < 30; ++k)
+          fprintf(stderr, "  block %llu thread %llu barrier %llu parity %llu line %llu\n", hbuf[2 + k * 4],
+                  hbuf[3 + k * 4], hbuf[4 + k * 4] & 0xffffffffull, hbuf[4 + k * 4] >> 32, hbuf[5 + k * 4]);
+        fflush(stderr);
+        break;
+      }
+    }
+  }
+#endif
+  if (prm.trace) {
+    long long h[2 * 64 * 4];
+    cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost);
+    FILE* f = fopen(getenv("ROPESLR_K2_TRACE"), "w");
+    for (int i = 0; i < 128; ++i) fprintf(f, "%d %d %lld %lld %lld\n", i / 64, i % 64, h[i * 4] ? h[i * 4] - h[0] : -1,
+                                          h[i * 4 + 1] ? h[i * 4 + 1] - h[0] : -1, h[i * 4 + 2] ? h[i * 4 + 2] - h[0] : -1);
+    fclose(f);
+  }
   return launch_status();
 }
 
@@ -622,6 +714,13 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.kv_evict_last = (pol != nullptr && pol[0] == '1') ? 1 : 0;
   const char* dbg = getenv("ROPESLR_DEBUG_MODE");
   prm.debug_mode = dbg ? atoi(dbg) : 0;
+  prm.trace = nullptr;
+  static long long* tbuf = nullptr;
+  if (getenv("ROPESLR_K2_TRACE")) {
+    if (!tbuf) cudaMalloc(&tbuf, 2 * 64 * 4 * 8);
+    cudaMemset(tbuf, 0, 2 * 64 * 4 * 8);
+    prm.trace = tbuf;
+  }
   return prm;
 }
 
