@@ -53,26 +53,27 @@ using namespace sm100;
 
 constexpr int D = 128;   // head dim handled by this kernel
 constexpr int M = 128;   // MMA rows (query rows per tile)
-constexpr int kThreads = 384;  // 4 control warps + 2 softmax warpgroups
+constexpr int kThreads = 640;  // 4 control warps + 4 softmax warpgroups (two pairs)
 constexpr uint32_t O_COL = 256;  // TMEM columns: S_0 [0,128), S_1 [128,256), O_0 [256,384), O_1 [384,512)
 // setmaxnreg moves registers inside the CTA's own pool, which holds what the
-// launch allotted: 168 per thread (65536 / 384, rounded down to 8) x 384.
-constexpr int kLaunchRegs = 168;
-constexpr int kCtrlRegs = 72;       // per thread, control warpgroup (TMA, MMA, TMEM)
-constexpr int kSoftmaxRegs = 216;   // per thread, softmax warpgroups (two half rows in flight)
-static_assert(kCtrlRegs * 128 + kSoftmaxRegs * 256 <= kLaunchRegs * kThreads, "register pool overcommitted");
+// launch allotted: 96 per thread (65536 / 640, rounded down to 8) x 640.
+constexpr int kLaunchRegs = 96;
+constexpr int kCtrlRegs = 56;       // per thread, control warpgroup (TMA, MMA, TMEM)
+constexpr int kSoftmaxRegs = 104;   // per thread, softmax warpgroups
+static_assert(kCtrlRegs * 128 + kSoftmaxRegs * 512 <= kLaunchRegs * kThreads, "register pool overcommitted");
 
 template <int BLK>
 struct Layout {
   static constexpr int Q_BYTES = M * D * 2;
   static constexpr int KV_BYTES = BLK * D * 2;
-  static constexpr int STAGES = BLK == 128 ? 3 : 4;        // K ring and V ring depth
+  static constexpr int KST = BLK == 128 ? 2 : 4;  // K ring depth (a K slot frees as soon as its QK^T lands)
+  static constexpr int VST = BLK == 128 ? 3 : 4;  // V ring depth (a V slot frees only after its PV)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
-  static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
-  static constexpr int OFF_XCH = OFF_V + STAGES * KV_BYTES;  // row-max / epilogue exchange, 2 KiB
-  static constexpr int OFF_BAR = OFF_XCH + 2048;
-  static constexpr int NBAR = 4 * STAGES + 12;
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+  static constexpr int OFF_XCH = OFF_V + VST * KV_BYTES;  // row-max / epilogue exchange, 4 KiB
+  static constexpr int OFF_BAR = OFF_XCH + 4096;
+  static constexpr int NBAR = 2 * KST + 2 * VST + 12;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
   // dynamic smem starts 1024-aligned (after the driver's 1 KiB reservation);
   // the kernel traps if that ever changes
@@ -80,17 +81,16 @@ struct Layout {
   static_assert(ALLOC <= 227 * 1024, "shared memory budget");
 };
 
-// Barrier indices (STAGES-dependent offsets for the K / V rings).
+// Barrier indices.  Tile t belongs to softmax pair p = t & 1.
 template <int BLK>
 struct Bars {
-  static constexpr int ST = Layout<BLK>::STAGES;
+  static constexpr int KST = Layout<BLK>::KST, VST = Layout<BLK>::VST;
   static constexpr int Q_FULL = 0, Q_EMPTY = 1;
-  static constexpr int K_FULL = 2, K_EMPTY = K_FULL + ST;
-  static constexpr int V_FULL = K_EMPTY + ST, V_EMPTY = V_FULL + ST;
-  static constexpr int S_FULL = V_EMPTY + ST;  // +b: S_b = Q K_t^T landed
-  static constexpr int P_FULL = S_FULL + 2;    // +2b+w: warpgroup w's half of P_b written
-  static constexpr int PV_DONE = P_FULL + 4;   // +w: one phase per PV_w
-  static constexpr int O_FULL = PV_DONE + 2;
+  static constexpr int K_FULL = 2, K_EMPTY = K_FULL + KST;
+  static constexpr int V_FULL = K_EMPTY + KST, V_EMPTY = V_FULL + VST;
+  static constexpr int S_FULL = V_EMPTY + VST;  // +p: S_p = Q K_t^T landed
+  static constexpr int P_FULL = S_FULL + 2;     // +p: both warpgroups of pair p wrote P_p
+  static constexpr int O_FULL = P_FULL + 2;
   static constexpr int O_EMPTY = O_FULL + 1;
   static constexpr int COUNT = O_EMPTY + 1;
   static_assert(COUNT <= Layout<BLK>::NBAR, "barrier count");
@@ -197,22 +197,18 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 #define ROPESLR_POLY_DEN 4
 #endif
 
-// Softmax of one half key block: warpgroup w owns keys [w*BLK/2, (w+1)*BLK/2)
-// of S tile t (one query row per thread) with its own running max / sum and
-// its own accumulator O_w (split-K over the key columns), so the two
-// warpgroups never wait for each other inside the key loop.  P_w = 2^(s*scale
-// - m_w) is written as bf16 pairs over the warpgroup's own S columns (P
-// column c of the half holds keys 2c, 2c+1).  RAGGED masks keys past the end
-// of the sequence (only the last key block).
+// Softmax of one key block by one pair of warpgroups, split by key
+// columns: warpgroup w of the pair owns keys [w*BLK/2, (w+1)*BLK/2), one
+// query row per thread, its half row already in registers.
+//
+// half_max: this half's max (masked past the end of the sequence when
+// RAGGED), exchanged with the partner warpgroup through shared memory; the
+// pair barrier also guarantees both halves of S have been read before
+// either warpgroup overwrites S with P.
 template <int BLK, bool RAGGED>
-__device__ __forceinline__ float half_softmax(uint32_t tSh, int valid, float scale_log2, bool first, float& m_run,
-                                              float& l_run) {
+__device__ __forceinline__ float half_max(uint32_t (&sr)[BLK / 2], int valid, float* xmax_mine,
+                                          const float* xmax_other, int bar_id) {
   constexpr int HB = BLK / 2;
-  constexpr int NP = HB < 64 ? HB / 2 : 32;  // pairs per TMEM store
-  uint32_t sr[HB];
-#pragma unroll
-  for (int c = 0; c < HB / 32; ++c) tmem_ld32(tSh + c * 32, sr + c * 32);
-  tmem_wait_ld();
   if (RAGGED) {
 #pragma unroll
     for (int c = 0; c < HB; ++c)
@@ -225,29 +221,28 @@ __device__ __forceinline__ float half_softmax(uint32_t tSh, int valid, float sca
     for (int q = 0; q < 4; ++q)
       mq[q] = fmaxf(mq[q], fmaxf(__uint_as_float(sr[c + 2 * q]), __uint_as_float(sr[c + 2 * q + 1])));
   }
-  const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * scale_log2;
-  // lazy rescale: the running max moves only when it grows by more than 2^8
-  float alpha = 1.f;
-  if (first) {
-    m_run = mx;
-  } else if (mx > m_run + ROPESLR_RESCALE_THRESHOLD) {
-    alpha = ex2_approx(m_run - mx);
-    l_run *= alpha;
-    m_run = mx;
-  }
-  // a fully masked half (m = -inf) contributes exact zeros
-  const float m_eff = m_run == -INFINITY ? 0.f : m_run;
+  const float lmx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+  *xmax_mine = lmx;
+  named_bar_sync(bar_id, 256);
+  return fmaxf(lmx, *xmax_other);
+}
+
+// half_exp: P = 2^(s*scale - m) as bf16 pairs written over S (P column c
+// holds keys 2c, 2c+1), 16 columns per TMEM store; returns this half's sum.
+template <int BLK>
+__device__ __forceinline__ float half_exp(const uint32_t (&sr)[BLK / 2], uint32_t tPh, float scale_log2,
+                                          float m_run) {
+  constexpr int HB = BLK / 2;
   const float2 sc2 = make_float2(scale_log2, scale_log2);
-  const float2 nm2 = make_float2(-m_eff, -m_eff);
+  const float2 nm2 = make_float2(-m_run, -m_run);
   float2 sum2 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int h = 0; h < HB / (2 * NP); ++h) {
-    uint32_t pk[NP];
+  for (int h = 0; h < HB / 32; ++h) {
+    uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < NP; ++i) {
+    for (int i = 0; i < 16; ++i) {
       const float2 x2 = __ffma2_rn(
-          make_float2(__uint_as_float(sr[h * 2 * NP + 2 * i]), __uint_as_float(sr[h * 2 * NP + 2 * i + 1])), sc2,
-          nm2);
+          make_float2(__uint_as_float(sr[h * 32 + 2 * i]), __uint_as_float(sr[h * 32 + 2 * i + 1])), sc2, nm2);
       float2 e2;
       if ((i % ROPESLR_POLY_DEN) < ROPESLR_POLY_NUM) {
         e2 = ex2_poly2(x2);  // FMA-pipe exp2 for a fraction of the scores: offloads the MUFU
@@ -259,14 +254,9 @@ __device__ __forceinline__ float half_softmax(uint32_t tSh, int valid, float sca
       __nv_bfloat162 hb = __floats2bfloat162_rn(e2.x, e2.y);
       pk[i] = *reinterpret_cast<uint32_t*>(&hb);
     }
-    if (NP == 32) {
-      tmem_st32(tSh + h * 32, pk);
-    } else {
-      tmem_st16(tSh + h * 16, pk);
-    }
+    tmem_st16(tPh + h * 16, pk);
   }
-  l_run += sum2.x + sum2.y;
-  return alpha;
+  return sum2.x + sum2.y;
 }
 
 template <int BLK>
@@ -275,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const __grid_constant__ CUtensorMap tmV, const Params p) {
   using Lay = Layout<BLK>;
   using Bx = Bars<BLK>;
-  constexpr int ST = Lay::STAGES;
+  constexpr int KST = Lay::KST, VST = Lay::VST;
   constexpr int HB = BLK / 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
@@ -285,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = smem + Lay::OFF_V;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Lay::OFF_BAR + Lay::NBAR * 8);
-  float2* xch_ml = reinterpret_cast<float2*>(smem + Lay::OFF_XCH);  // [2][128] (m, l), then (ss, -)
+  float* xch = reinterpret_cast<float*>(smem + Lay::OFF_XCH);  // 1024 floats
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -296,8 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmV);
     for (int i = 0; i < Bx::COUNT; ++i) {
       uint32_t count = 1;
-      if (i >= Bx::P_FULL && i < Bx::P_FULL + 4) count = 128;
-      if (i == Bx::O_EMPTY) count = 256;
+      if (i == Bx::P_FULL || i == Bx::P_FULL + 1) count = 256;
+      if (i == Bx::O_EMPTY) count = 512;
       mbar_init(&bars[i], count);
     }
     fence_mbar_init();
@@ -325,9 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 || warp == 3) {
       if (elect_one_sync()) {
         // ------------------------------------------- TMA producers
-        // warp 0: Q and K (K runs ahead: a K slot frees as soon as its QK^T
-        // completes); warp 3: V (a V slot frees only after its PV).
+        // warp 0: Q and K; warp 3: V (a V slot frees only after its PV, so
+        // it must not hold back the K prefetch).
         const bool is_k = (warp == 0);
+        const int st = is_k ? KST : VST;
         const uint64_t pol_kv = p.kv_evict_last ? policy_evict_last() : policy_evict_normal();
         const uint64_t pol_q = policy_evict_first();
         const CUtensorMap* map = is_k ? &tmK : &tmV;
@@ -348,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           for (int j = 0; j < n; ++j, ++g) {
             const int kb = p.debug_mode == 2 ? 0 : irow[j];
-            const int s = g % ST;
-            const uint32_t ph = (g / ST) & 1;
+            const int s = g % st;
+            const uint32_t ph = (g / st) & 1;
             uint8_t* dst = ring + s * Lay::KV_BYTES;
             mbar_wait(&bars[empty + s], ph ^ 1);
             if (p.debug_mode == 3) {
@@ -364,19 +355,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else if (warp == 1) {
       // ------------------------------------------------ MMA issuer
-      // The whole warp runs the (uniform) control flow and waits; one
-      // elected lane issues tcgen05.mma / commit.  Global tile t uses S
-      // buffer b = t & 1: S_b = Q K_t^T (SS-MMA, TMEM columns [128b, +BLK)).
-      // Warpgroup w turns its key half into P (bf16 pairs over its own S
-      // columns [128b + w*BLK/2, +BLK/4)) and O_w += P_w V_t[w half] runs as
-      // a TS-MMA with K = BLK/2.  Issue order per unit: QK(0), QK(1), then
-      // [PV_0(j-2), PV_1(j-2), QK(j)], then the last two tiles' PVs: QK(j)
-      // overwrites what PV(j-2) reads, and the tensor pipe executes a CTA's
-      // MMAs in issue order.
+      // Global tile t belongs to softmax pair p = t & 1: S_p = Q K_t^T
+      // (SS-MMA into TMEM columns [128p, +BLK)); the pair overwrites S_p with
+      // P_p (bf16 pairs, columns [128p, +BLK/2)); O_p += P_p V_t (TS-MMA, A
+      // from TMEM, O_p at columns [256 + 128p, +128)).  Issue order per unit:
+      // QK(0), QK(1), then [PV(j-2), QK(j)], then PV(n-2), PV(n-1): QK(j)
+      // overwrites what PV(j-2) reads, the tensor pipe executes a CTA's MMAs
+      // in issue order, and S_FULL's commit after QK(j) also covers PV(j-2),
+      // so a pair may rescale O_p as soon as it sees S_p.
       constexpr uint32_t idesc_qk = idesc_bf16_f32(M, BLK, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(M, D, false, true);
-      // descriptor bases; the K-step offsets below are added to the low word
-      // (start address field, 16-byte units, no carry: smem < 256 KiB)
       const uint64_t dQ = desc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dK0 = desc_sw128(smem_u32(sK), 16, 1024);
       const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
@@ -389,33 +377,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < n + 2; ++j) {
           if (j >= 2) {
             const uint32_t t = g + j - 2;
-            const int s = t % ST;
-            const int b = t & 1;
-            mbar_wait(&bars[Bx::V_FULL + s], (t / ST) & 1);
+            const int s = t % VST;
+            const int pr = t & 1;
+            mbar_wait(&bars[Bx::V_FULL + s], (t / VST) & 1);
+            mbar_wait(&bars[Bx::P_FULL + pr], (t >> 1) & 1);
             if (j == 2) mbar_wait(&bars[Bx::O_EMPTY], (uc & 1) ^ 1);
-#pragma unroll 1
-            for (int w = 0; w < 2; ++w) {
-              mbar_wait(&bars[Bx::P_FULL + b * 2 + w], (t >> 1) & 1);
-              tc_fence_after();
-              if (leader) {
-                const uint32_t tP = tmem + b * 128 + w * HB;
-                const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES + w * HB * 128) >> 4);
+            tc_fence_after();
+            if (leader) {
+              const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
 #pragma unroll
-                for (int kk = 0; kk < HB / 16; ++kk) {
-                  const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
-                  mma_bf16_ts(tmem + O_COL + w * 128, tP + kk * 8, db, idesc_pv, (j > 2 || kk > 0) ? 1u : 0u);
-                }
-                mma_commit(&bars[Bx::PV_DONE + w]);
-                if (w == 1) mma_commit(&bars[Bx::V_EMPTY + s]);
+              for (int kk = 0; kk < BLK / 16; ++kk) {
+                const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
+                mma_bf16_ts(tmem + O_COL + pr * 128, tmem + pr * 128 + kk * 8, db, idesc_pv,
+                            (j >= 4 || kk > 0) ? 1u : 0u);
               }
-              __syncwarp();
+              mma_commit(&bars[Bx::V_EMPTY + s]);
             }
+            __syncwarp();
           }
           if (j < n) {
             const uint32_t t = g + j;
-            const int s = t % ST;
-            const int b = t & 1;
-            mbar_wait(&bars[Bx::K_FULL + s], (t / ST) & 1);
+            const int s = t % KST;
+            const int pr = t & 1;
+            mbar_wait(&bars[Bx::K_FULL + s], (t / KST) & 1);
             tc_fence_after();
             if (leader) {
               const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
@@ -423,10 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int kk = 0; kk < D / 16; ++kk) {
                 const uint64_t da = dQ + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
                 const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
-                mma_bf16_ss(tmem + b * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+                mma_bf16_ss(tmem + pr * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
               }
               mma_commit(&bars[Bx::K_EMPTY + s]);
-              mma_commit(&bars[Bx::S_FULL + b]);
+              mma_commit(&bars[Bx::S_FULL + pr]);
               if (j == n - 1) mma_commit(&bars[Bx::Q_EMPTY]);
             }
             __syncwarp();
@@ -440,10 +424,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     setmaxnreg_inc<kSoftmaxRegs>();
     // ------------------------------------ softmax warpgroups + epilogue
-    const int w = (warp - 4) >> 2;                 // key-column half of every tile
+    const int q = (warp - 4) >> 2;                 // softmax warpgroup 0..3
+    const int pr = q >> 1;                         // pair: tiles t with t & 1 == pr
+    const int w = q & 1;                           // key-column half within the pair
     const int row = (threadIdx.x - 128) & 127;     // query row == TMEM lane
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    const uint32_t tO = lane_addr + O_COL + w * 128;
+    const uint32_t tS = lane_addr + pr * 128;
+    const uint32_t tOh = lane_addr + O_COL + pr * 128 + w * (D / 2);
     uint32_t g = 0, uc = 0;
     for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
       const int bh = static_cast<int>(u / p.nb);
@@ -452,99 +439,109 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t* irow = p.idx + u * p.kmax;
       const int qrows = block_size(p.L, BLK, qb);
       float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j) {
+      // this pair's tiles of the unit: j = j0, j0 + 2, ...
+      const int j0 = (pr - static_cast<int>(g & 1)) & 1;
+      for (int j = j0; j < n; j += 2) {
         const uint32_t t = g + j;
-        const int b = t & 1;
         const int kreal = block_size(p.L, BLK, irow[j]);
-        mbar_wait(&bars[Bx::S_FULL + b], (t >> 1) & 1);
+        mbar_wait(&bars[Bx::S_FULL + pr], (t >> 1) & 1);
         tc_fence_after();
         const bool trc = p.trace && blockIdx.x == 0 && row == 0 && t < 64;
         if (trc) p.trace[(w * 64 + t) * 4 + 0] = clock64();
-        const uint32_t tSh = lane_addr + b * 128 + w * HB;
+        uint32_t sr[HB];
+#pragma unroll
+        for (int c = 0; c < HB / 32; ++c) tmem_ld32(tS + w * HB + c * 32, sr + c * 32);
+        tmem_wait_ld();
+        float* xm = xch + (pr * 2 + ((t >> 1) & 1)) * 256;  // [pair][tile parity][wg][row]
         const int valid = kreal - w * HB;
-        float alpha;
-        if (p.debug_mode == 1) {
-          m_run = 0.f;
-          l_run = 1.f;
-          alpha = 1.f;
-        } else if (valid < HB) {
-          alpha = half_softmax<BLK, true>(tSh, valid, p.scale_log2, j == 0, m_run, l_run);
-        } else {
-          alpha = half_softmax<BLK, false>(tSh, HB, p.scale_log2, j == 0, m_run, l_run);
+        float mx = valid < HB ? half_max<BLK, true>(sr, valid, xm + w * 128 + row, xm + (w ^ 1) * 128 + row, 1 + pr)
+                              : half_max<BLK, false>(sr, HB, xm + w * 128 + row, xm + (w ^ 1) * 128 + row, 1 + pr);
+        mx *= p.scale_log2;
+        // lazy rescale: the running max moves only when it grows by more
+        // than 2^8 (both warpgroups of the pair take the same decision)
+        float alpha = 1.f;
+        if (j == j0) {
+          m_run = mx;
+        } else if (mx > m_run + ROPESLR_RESCALE_THRESHOLD) {
+          alpha = ex2_approx(m_run - mx);
+          l_run *= alpha;
+          m_run = mx;
         }
+        l_run += half_exp<BLK>(sr, tS + w * (HB / 2), p.scale_log2, m_run);
         // tcgen05.ld / st are warp-collective: the rescale runs for the whole
-        // warp when any of its rows needs it (alpha == 1 for the others)
+        // warp when any of its rows needs it (alpha == 1 for the others).
+        // PV(t-2), the last writer of O_p, completed before S_p landed.
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
-          // PV_w(t-1), the last writer of O_w, must have landed before O_w is
-          // rescaled (PV_w(t-2) is covered by S_t's commit)
-          mbar_wait(&bars[Bx::PV_DONE + w], (t - 1) & 1);
-          tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
+          for (int c = 0; c < D / 64; ++c) {
             uint32_t o[32];
-            tmem_ld32(tO + c * 32, o);
+            tmem_ld32(tOh + c * 32, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(tO + c * 32, o);
+            tmem_st32(tOh + c * 32, o);
           }
         }
         if (trc) p.trace[(w * 64 + t) * 4 + 1] = clock64();
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bars[Bx::P_FULL + b * 2 + w]);
+        mbar_arrive(&bars[Bx::P_FULL + pr]);
         if (trc) p.trace[(w * 64 + t) * 4 + 2] = clock64();
       }
       g += n;
       // ---------------------------------------------- fused epilogue
-      // merge the two partial softmaxes: O = sum_w O_w 2^(m_w - m), l likewise
+      // merge the two pairs' partial softmaxes: O = sum_p O_p 2^(m_p - m) / l;
+      // warpgroup q finalises output columns [32q, 32q + 32) of its row
       mbar_wait(&bars[Bx::O_FULL], uc & 1);
       tc_fence_after();
-      xch_ml[w * 128 + row] = make_float2(m_run, l_run);
-      named_bar_sync(1, 256);
-      const float2 other = xch_ml[(w ^ 1) * 128 + row];
-      const float m0 = w == 0 ? m_run : other.x, l0 = w == 0 ? l_run : other.y;
-      const float m1 = w == 0 ? other.x : m_run, l1 = w == 0 ? other.y : l_run;
-      const float mm = fmaxf(m0, m1);
-      const float f0 = m0 == -INFINITY ? 0.f : ex2_approx(m0 - mm);
-      const float f1 = m1 == -INFINITY ? 0.f : ex2_approx(m1 - mm);
-      const float inv_l = 1.f / (l0 * f0 + l1 * f1);
-      const float s0 = f0 * inv_l, s1 = f1 * inv_l;
-      // this warpgroup finalises columns [64w, 64w + 64) of its row
-      uint32_t ob[64];
+      named_bar_sync(3, 512);  // every pair's last max exchange has been read
+      float2* xml = reinterpret_cast<float2*>(xch);  // [4 wg][128] (m, l_half)
+      xml[q * 128 + row] = make_float2(m_run, l_run);
+      named_bar_sync(3, 512);
+      const float2 a0 = xml[0 * 128 + row], a1 = xml[1 * 128 + row];
+      const float2 b0 = xml[2 * 128 + row], b1 = xml[3 * 128 + row];
+      const float mA = a0.x, lA = a0.y + a1.y, mB = b0.x, lB = b0.y + b1.y;
+      const float mm = fmaxf(mA, mB);
+      const float fA = mA == -INFINITY ? 0.f : ex2_approx(mA - mm);
+      const float fB = mB == -INFINITY ? 0.f : ex2_approx(mB - mm);
+      const float inv_l = 1.f / (lA * fA + lB * fB);
+      const float sA = fA * inv_l, sB = fB * inv_l;
+      uint32_t ob[32];
       {
-        uint32_t t1[32];
+        uint32_t tb[32];
+        tmem_ld32(lane_addr + O_COL + q * 32, ob);
+        tmem_ld32(lane_addr + O_COL + 128 + q * 32, tb);
+        tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          tmem_ld32(lane_addr + O_COL + w * 64 + c * 32, ob + c * 32);
-          tmem_ld32(lane_addr + O_COL + 128 + w * 64 + c * 32, t1);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            ob[c * 32 + i] = __float_as_uint(fmaf(__uint_as_float(ob[c * 32 + i]), s0, __uint_as_float(t1[i]) * s1));
+        for (int i = 0; i < 32; ++i) {
+          // an O_p with no tile in this unit holds stale data: weight 0, and
+          // never multiply it (it could be inf / NaN)
+          const float oa = sA != 0.f ? __uint_as_float(ob[i]) * sA : 0.f;
+          const float obb = sB != 0.f ? __uint_as_float(tb[i]) * sB : 0.f;
+          ob[i] = __float_as_uint(oa + obb);
         }
       }
       tc_fence_before();
       mbar_arrive(&bars[Bx::O_EMPTY]);
       float ss = 0.f;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) ss = fmaf(__uint_as_float(ob[i]), __uint_as_float(ob[i]), ss);
-      named_bar_sync(1, 256);  // both warpgroups have read the (m, l) exchange
-      xch_ml[w * 128 + row].x = ss;
-      named_bar_sync(1, 256);
-      ss += xch_ml[(w ^ 1) * 128 + row].x;
-      named_bar_sync(1, 256);  // the exchange area is free for the next unit
+      for (int i = 0; i < 32; ++i) ss = fmaf(__uint_as_float(ob[i]), __uint_as_float(ob[i]), ss);
+      named_bar_sync(3, 512);  // the (m, l) exchange has been read
+      xch[q * 128 + row] = ss;
+      named_bar_sync(3, 512);
+      ss = (xch[row] + xch[128 + row]) + (xch[256 + row] + xch[384 + row]);
+      named_bar_sync(3, 512);  // the exchange area is free for the next unit
       const bool live = row < qrows;
       if (!live) continue;
       const int64_t flat = static_cast<int64_t>(qb) * BLK + row;
       const int64_t tok = p.perm ? p.perm[flat] : flat;
       const int b = bh / p.H, h = bh % p.H;
       const float inv = 1.f / sqrtf(ss / static_cast<float>(D) + p.eps);
-      const int col0 = w * 64;
+      const int col0 = q * 32;
       if (p.o_sparse) {
         float* dst = p.o_sparse + (static_cast<int64_t>(bh) * p.L + tok) * D + col0;
 #pragma unroll
-        for (int i = 0; i < 64; i += 4)
+        for (int i = 0; i < 32; i += 4)
           *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
                                                             __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
       }
@@ -554,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const __nv_bfloat16* y = p.y_lr + orow;
         __nv_bfloat16* dst = p.out + orow;
 #pragma unroll
-        for (int i = 0; i < 64; i += 8) {
+        for (int i = 0; i < 32; i += 8) {
           const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
           const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
           uint4 uo;
