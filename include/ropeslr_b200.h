@@ -123,6 +123,33 @@ int ropeslr_select_blocks(const ropeslr_shape* shape, const ropeslr_select_param
                           int64_t* attended, double* scores,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* Selection from precomputed float64 block means pooled [2, B*H, nb, d]
+ * (Q means, then K means; e.g. from ropeslr_rope_pool): the scores and
+ * selection stages of ropeslr_select_blocks.  `scores` may be NULL, then
+ * the workspace holds them. */
+size_t ropeslr_select_pooled_workspace_bytes(const ropeslr_shape* shape);
+int ropeslr_select_from_pooled(const ropeslr_shape* shape, const ropeslr_select_params* sel, const double* pooled,
+                               int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
+                               double* scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------- fused 3D RoPE + block pooling (pre-pass)
+ * The caller-side rotation of the reference (rope3d.rotate_rows,
+ * rope3d.py:102-143) fused with K1's pooling (mechanism.py:306-308): reads
+ * un-rotated Q/K [B,H,L,d], writes the rotated Q/K (same dtype; float64
+ * math, cast float64 -> float32 -> storage dtype like torch) and the float64
+ * block means of the rotated, cast values, pooled [2, B*H, nb, d].  Pairs
+ * (2j, 2j+1) in [t | x | y] order, angle = coord * base^(-2(m-1)/d_axis). */
+typedef struct ropeslr_rope_args {
+  int32_t d_t, d_x, d_y;            /* per-axis head-dim split, even, sum = d */
+  int32_t grid_t, grid_h, grid_w;   /* 3D latent grid, product = L */
+  double base;                      /* frequency base (10000) */
+} ropeslr_rope_args;
+
+size_t ropeslr_rope_pool_workspace_bytes(const ropeslr_rope_args* rope);
+int ropeslr_rope_pool(const ropeslr_shape* shape, const ropeslr_rope_args* rope, const void* q_in, const void* k_in,
+                      void* q_out, void* k_out, double* pooled, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* ------------------------------------ K2: block-sparse softmax attention
  * Replaces the exact-attention half of block_sparse_attention
  * (mechanism.py:321-326): each query block attends, with an exact softmax,

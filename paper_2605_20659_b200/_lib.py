@@ -38,6 +38,11 @@ class TokenArgs(ctypes.Structure):
                 ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp)]
 
 
+class RopeArgs(ctypes.Structure):
+    _fields_ = [("d_t", c_i32), ("d_x", c_i32), ("d_y", c_i32), ("grid_t", c_i32), ("grid_h", c_i32),
+                ("grid_w", c_i32), ("base", c_f64)]
+
+
 GateHook = ctypes.CFUNCTYPE(None, c_vp, c_i64, c_vp, c_vp)
 
 
@@ -68,6 +73,11 @@ _SIGNATURES = {
     "ropeslr_attend_fused": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp,
                                      c_f32, c_vp, c_vp, c_i32, c_vp, c_sz, c_vp]),
     "ropeslr_attend_workspace_bytes": (c_sz, [P(Shape), c_i32]),
+    "ropeslr_select_pooled_workspace_bytes": (c_sz, [P(Shape)]),
+    "ropeslr_select_from_pooled": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                           c_vp, c_sz, c_vp]),
+    "ropeslr_rope_pool_workspace_bytes": (c_sz, [P(RopeArgs)]),
+    "ropeslr_rope_pool": (c_i32, [P(Shape), P(RopeArgs), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_forward_host_workspace_bytes": (c_sz, [P(HostForward)]),
     "ropeslr_forward_host": (c_i32, [P(HostForward), c_vp, c_sz, c_vp]),
 }

@@ -707,8 +707,11 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.out_H = static_cast<int>(s->H);
   prm.out_h0 = 0;
   prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
+  // K/V tiles are re-read by many query blocks of the head: keep them in L2
+  // (evict_last) ahead of the streamed Q / y_lr / out; ROPESLR_KV_EVICT_LAST=0
+  // turns the hint off
   const char* pol = getenv("ROPESLR_KV_EVICT_LAST");
-  prm.kv_evict_last = (pol != nullptr && pol[0] == '1') ? 1 : 0;
+  prm.kv_evict_last = (pol != nullptr && pol[0] == '0') ? 0 : 1;
   const char* dbg = getenv("ROPESLR_DEBUG_MODE");
   prm.debug_mode = dbg ? atoi(dbg) : 0;
   prm.trace = nullptr;

@@ -1,0 +1,222 @@
+// Fused 3D RoPE + block pooling: the step before K1 selection (SURVEY.md
+// section 8f, "next" #1).  Un-rotated Q and K [B, H, L, d] go in; rotated Q
+// and K (same dtype) and the float64 block means of the *rotated, cast*
+// values (what K1 pools, mechanism.py:306-308) come out, from one HBM pass
+// instead of a rotation pass plus a pooling pass.
+//
+// The rotation restates rope3d.rotate_rows (rope3d.py:102-143) exactly as
+// the package's torch path computes it (paper_2605_20659_b200/rope3d.py):
+// angle = coord_axis * base^(-2(m-1)/d_axis) in float64, cos / sin in
+// float64, (e, o) -> (c*e - s*o, s*e + c*o) with each product and sum
+// rounded separately (no FMA contraction), then cast to the storage dtype
+// the way torch does (float64 -> float32 -> bfloat16).  The cos / sin
+// values depend only on (axis coordinate, pair), so they are tabulated per
+// axis ([n_axis, d_axis / 2]) by rope_tables_kernel.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+
+namespace ropeslr {
+namespace rp {
+
+constexpr int kMaxPairs = 128;  // d <= 256
+
+struct Tables {
+  const double* cs;  // [rows, 2] interleaved (cos, sin); row = base of the pair's axis + coordinate
+  int pair_axis[kMaxPairs];   // axis of pair j (0 t, 1 x, 2 y)
+  int pair_col[kMaxPairs];    // m - 1 within the axis
+  int axis_half[3];           // d_axis / 2
+  int axis_row0[3];           // first table row of each axis (rows of axis a: n_a * d_a/2 entries)
+};
+
+// entries: axis a, coordinate c, pair m -> (cos, sin) of c * theta_{a,m}
+__global__ void rope_tables_kernel(double* cs, const double* thetas, int n_t, int n_x, int n_y, int h_t, int h_x,
+                                   int h_y) {
+  const int total = n_t * h_t + n_x * h_x + n_y * h_y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    int a, r = e, coord, m;
+    if (r < n_t * h_t) {
+      a = 0;
+      coord = r / h_t;
+      m = r % h_t;
+    } else if ((r -= n_t * h_t) < n_x * h_x) {
+      a = 1;
+      coord = r / h_x;
+      m = r % h_x;
+    } else {
+      r -= n_x * h_x;
+      a = 2;
+      coord = r / h_y;
+      m = r % h_y;
+    }
+    const int off = a == 0 ? 0 : (a == 1 ? h_t : h_t + h_x);
+    const double ang = static_cast<double>(coord) * thetas[off + m];
+    cs[2 * e] = cos(ang);
+    cs[2 * e + 1] = sin(ang);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T cast_out(double v);
+template <>
+__device__ __forceinline__ float cast_out<float>(double v) {
+  return __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 cast_out<__nv_bfloat16>(double v) {
+  return __float2bfloat16_rn(__double2float_rn(v));  // torch: float64 -> float -> bfloat16
+}
+
+// grid (nb, B*H, 2): z = 0 Q, z = 1 K; 256 threads; each thread owns 8
+// consecutive columns (4 pairs) of the rows r = rr, rr + lanes_r, ...
+template <typename T>
+__global__ void __launch_bounds__(256) rope_pool_kernel(const T* __restrict__ q_in, const T* __restrict__ k_in,
+                                                        T* __restrict__ q_out, T* __restrict__ k_out,
+                                                        double* __restrict__ pooled, const Tables tab, int64_t L,
+                                                        int d, int block, int nb, int64_t BH, int grid_h,
+                                                        int grid_w) {
+  extern __shared__ double sred[];
+  const int64_t bh = blockIdx.y;
+  const T* src = (blockIdx.z == 0 ? q_in : k_in) + bh * L * d;
+  T* dst = (blockIdx.z == 0 ? q_out : k_out) + bh * L * d;
+  const int b = blockIdx.x;
+  const int rows = block_size(L, block, b);
+  const int64_t r0 = static_cast<int64_t>(b) * block;
+  const int chunks = d / 8;
+  const int lanes_r = blockDim.x / chunks;
+  const int tid = threadIdx.x;
+  const int ch = tid % chunks;
+  const int rr = tid / chunks;
+  const int64_t frame = static_cast<int64_t>(grid_h) * grid_w;
+  int ax[4], col[4], half[4], row0[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = ch * 4 + u;
+    ax[u] = tab.pair_axis[j];
+    col[u] = tab.pair_col[j];
+    half[u] = tab.axis_half[ax[u]];
+    row0[u] = tab.axis_row0[ax[u]];
+  }
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  if (rr < lanes_r) {
+    for (int r = rr; r < rows; r += lanes_r) {
+      const int64_t pos = r0 + r;
+      const int ct = static_cast<int>(pos / frame);
+      const int cx = static_cast<int>((pos % frame) / grid_w);
+      const int cy = static_cast<int>(pos % grid_w);
+      float v[8];
+      load8(src + pos * d + ch * 8, v);
+      double out[8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int coord = ax[u] == 0 ? ct : (ax[u] == 1 ? cx : cy);
+        const double2 csv = *reinterpret_cast<const double2*>(tab.cs + 2 * (row0[u] + coord * half[u] + col[u]));
+        const double e = v[2 * u], o = v[2 * u + 1];
+        out[2 * u] = __dsub_rn(__dmul_rn(csv.x, e), __dmul_rn(csv.y, o));
+        out[2 * u + 1] = __dadd_rn(__dmul_rn(csv.y, e), __dmul_rn(csv.x, o));
+      }
+      T ov[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ov[i] = cast_out<T>(out[i]);
+        acc[i] += static_cast<double>(to_f(ov[i]));  // pool the values K2 will see
+      }
+      if (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(dst + pos * d + ch * 8) = *reinterpret_cast<const uint4*>(ov);
+      } else {
+        *reinterpret_cast<float4*>(dst + pos * d + ch * 8) = *reinterpret_cast<const float4*>(ov);
+        *reinterpret_cast<float4*>(dst + pos * d + ch * 8 + 4) = *reinterpret_cast<const float4*>(ov + 4);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sred[rr * d + ch * 8 + i] = acc[i];
+  }
+  __syncthreads();
+  double* pdst = pooled + ((static_cast<int64_t>(blockIdx.z) * BH + bh) * nb + b) * d;
+  for (int c = tid; c < d; c += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < lanes_r; ++j) s += sred[j * d + c];
+    pdst[c] = s / static_cast<double>(rows);
+  }
+}
+
+int table_rows(const ropeslr_rope_args* r) {
+  return r->grid_t * (r->d_t / 2) + r->grid_h * (r->d_x / 2) + r->grid_w * (r->d_y / 2);
+}
+
+}  // namespace rp
+}  // namespace ropeslr
+
+using namespace ropeslr;
+
+extern "C" size_t ropeslr_rope_pool_workspace_bytes(const ropeslr_rope_args* r) {
+  if (!r) return 0;
+  const size_t half = static_cast<size_t>(r->d_t + r->d_x + r->d_y) / 2;
+  return (static_cast<size_t>(rp::table_rows(r)) * 2 + half) * sizeof(double) + 256;
+}
+
+extern "C" int ropeslr_rope_pool(const ropeslr_shape* s, const ropeslr_rope_args* r, const void* q_in,
+                                 const void* k_in, void* q_out, void* k_out, double* pooled, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  if (!s || !r) return ROPESLR_ERR_NULL;
+  if (s->B < 1 || s->H < 1 || s->L < 1 || s->block < 1) return ROPESLR_ERR_SHAPE;
+  if (s->d < 8 || s->d > 2 * rp::kMaxPairs || s->d % 8) return ROPESLR_ERR_SHAPE;
+  if (s->dtype != ROPESLR_F32 && s->dtype != ROPESLR_BF16) return ROPESLR_ERR_DTYPE;
+  if (r->d_t < 0 || r->d_x < 0 || r->d_y < 0 || (r->d_t | r->d_x | r->d_y) & 1) return ROPESLR_ERR_VALUE;
+  if (r->d_t + r->d_x + r->d_y != s->d) return ROPESLR_ERR_SHAPE;
+  if (r->grid_t < 1 || r->grid_h < 1 || r->grid_w < 1) return ROPESLR_ERR_SHAPE;
+  if (static_cast<int64_t>(r->grid_t) * r->grid_h * r->grid_w != s->L) return ROPESLR_ERR_SHAPE;
+  if (!(r->base > 0.0) || !isfinite(r->base)) return ROPESLR_ERR_VALUE;
+  if (!q_in || !k_in || !q_out || !k_out || !pooled) return ROPESLR_ERR_NULL;
+  if (!aligned16(q_in) || !aligned16(k_in) || !aligned16(q_out) || !aligned16(k_out)) return ROPESLR_ERR_ALIGN;
+  if (!ws || ws_bytes < ropeslr_rope_pool_workspace_bytes(r)) return ROPESLR_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  // theta_{a,m} = base^(-2(m-1)/d_a) on the host (C pow, as Python's ** does)
+  const int ht = r->d_t / 2, hx = r->d_x / 2, hy = r->d_y / 2;
+  double thetas[rp::kMaxPairs];
+  rp::Tables tab;
+  int j = 0;
+  const int dims[3] = {r->d_t, r->d_x, r->d_y};
+  const int halves[3] = {ht, hx, hy};
+  const int ns[3] = {r->grid_t, r->grid_h, r->grid_w};
+  int row0 = 0;
+  for (int a = 0; a < 3; ++a) {
+    tab.axis_half[a] = halves[a];
+    tab.axis_row0[a] = row0;
+    row0 += ns[a] * halves[a];
+    for (int m = 0; m < halves[a]; ++m, ++j) {
+      thetas[j] = pow(r->base, -2.0 * m / dims[a]);
+      tab.pair_axis[j] = a;
+      tab.pair_col[j] = m;
+    }
+  }
+  double* cs = static_cast<double*>(ws);
+  double* dthetas = cs + 2 * static_cast<size_t>(rp::table_rows(r));
+  if (cudaMemcpyAsync(dthetas, thetas, sizeof(double) * j, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  rp::rope_tables_kernel<<<static_cast<unsigned>(ceil_div(rp::table_rows(r), 256)), 256, 0, st>>>(
+      cs, dthetas, r->grid_t, r->grid_h, r->grid_w, ht, hx, hy);
+  if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  tab.cs = cs;
+  const int64_t BH = s->B * s->H;
+  const int d = static_cast<int>(s->d);
+  const int nb = static_cast<int>(ceil_div(s->L, s->block));
+  dim3 grid(nb, static_cast<unsigned>(BH), 2);
+  const int lanes_r = 256 / (d / 8);
+  const size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
+  if (s->dtype == ROPESLR_BF16)
+    rp::rope_pool_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(
+        static_cast<const __nv_bfloat16*>(q_in), static_cast<const __nv_bfloat16*>(k_in),
+        static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_out), pooled, tab, s->L, d, s->block, nb,
+        BH, r->grid_h, r->grid_w);
+  else
+    rp::rope_pool_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q_in), static_cast<const float*>(k_in),
+                                                       static_cast<float*>(q_out), static_cast<float*>(k_out), pooled,
+                                                       tab, s->L, d, s->block, nb, BH, r->grid_h, r->grid_w);
+  return launch_status();
+}

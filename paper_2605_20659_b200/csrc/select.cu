@@ -39,7 +39,19 @@ __global__ void __launch_bounds__(256) pool_blocks_kernel(const T* __restrict__ 
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0;
   if (rr < lanes_r) {
-    for (int r = rr; r < rows; r += lanes_r) {
+    // four row loads in flight per thread (bf16 sums of <= 128 values are
+    // exact in float64, so the order does not matter)
+    int r = rr;
+    for (; r + 3 * lanes_r < rows; r += 4 * lanes_r) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load8(src + (r0 + r + u * lanes_r) * d + ch * 8, v[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(v[u][i]);
+    }
+    for (; r < rows; r += lanes_r) {
       float v[8];
       load8(src + (r0 + r) * d + ch * 8, v);
 #pragma unroll
@@ -376,25 +388,13 @@ static int next_pow2(int n) {
   return p;
 }
 
-extern "C" size_t ropeslr_select_workspace_bytes(const ropeslr_shape* s) {
-  if (s == nullptr || s->block <= 0) return 0;
-  const int64_t nb = ceil_div(s->L, s->block);
-  const int64_t BH = s->B * s->H;
-  size_t pooled = static_cast<size_t>(2 * BH * nb * s->d) * sizeof(double);
-  size_t scores = static_cast<size_t>(BH * nb * nb) * sizeof(double);
-  return ((pooled + 255) / 256) * 256 + ((scores + 255) / 256) * 256;
-}
-
-extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_select_params* sel, const void* q,
-                                     const void* k, int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask,
-                                     int64_t* attended, double* scores_out, void* ws, size_t ws_bytes,
-                                     void* stream_) {
+static int check_select(const ropeslr_shape* s, const ropeslr_select_params* sel, int32_t kmax, const int32_t* idx,
+                        const int32_t* cnt, const int64_t* attended) {
   if (s == nullptr || sel == nullptr) return ROPESLR_ERR_NULL;
   if (s->B < 1 || s->H < 1 || s->L < 1 || s->block < 1) return ROPESLR_ERR_SHAPE;
   if (s->d < 8 || s->d > 256 || s->d % 8) return ROPESLR_ERR_SHAPE;
   if (s->dtype != ROPESLR_F32 && s->dtype != ROPESLR_BF16) return ROPESLR_ERR_DTYPE;
-  if (!q || !k || !idx || !cnt || !attended) return ROPESLR_ERR_NULL;
-  if (!aligned16(q) || !aligned16(k)) return ROPESLR_ERR_ALIGN;
+  if (!idx || !cnt || !attended) return ROPESLR_ERR_NULL;
   const int64_t nb64 = ceil_div(s->L, s->block);
   if (nb64 > 8192) return ROPESLR_ERR_SHAPE;
   const int nb = static_cast<int>(nb64);
@@ -402,30 +402,27 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
   if (sel->topk == 0 && !(sel->keep > 0.0 && sel->keep <= 1.0)) return ROPESLR_ERR_VALUE;
   const int need = sel->topk > 0 ? (sel->topk < nb ? sel->topk : nb) : nb;
   if (kmax < need) return ROPESLR_ERR_SHAPE;
-  if (ws == nullptr || ws_bytes < ropeslr_select_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
+  return ROPESLR_OK;
+}
 
-  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+static size_t pooled_bytes(const ropeslr_shape* s) {
+  const int64_t nb = ceil_div(s->L, s->block);
+  return ((static_cast<size_t>(2 * s->B * s->H * nb * s->d) * sizeof(double) + 255) / 256) * 256;
+}
+
+static size_t scores_bytes(const ropeslr_shape* s) {
+  const int64_t nb = ceil_div(s->L, s->block);
+  return ((static_cast<size_t>(s->B * s->H * nb * nb) * sizeof(double) + 255) / 256) * 256;
+}
+
+// Scores from the pooled means, then top-k / cumulative-mass selection.
+static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
+                              int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
+                              double* scores, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
   const int d = static_cast<int>(s->d);
-  double* pooled = static_cast<double*>(ws);
-  size_t pooled_bytes = ((static_cast<size_t>(2 * BH * nb * d) * sizeof(double) + 255) / 256) * 256;
-  double* scores = scores_out ? scores_out : reinterpret_cast<double*>(static_cast<char*>(ws) + pooled_bytes);
-
+  const int nb = static_cast<int>(ceil_div(s->L, s->block));
   if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-  {
-    dim3 grid(nb, static_cast<unsigned>(BH), 2);
-    const int chunks = d / 8;
-    const int lanes_r = 256 / chunks;
-    size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
-    if (s->dtype == ROPESLR_BF16)
-      pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                                                static_cast<const __nv_bfloat16*>(k), pooled, s->L,
-                                                                d, s->block, nb, BH);
-    else
-      pool_blocks_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q), static_cast<const float*>(k),
-                                                        pooled, s->L, d, s->block, nb, BH);
-    if (launch_status()) return ROPESLR_ERR_LAUNCH;
-  }
   {
     dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
               static_cast<unsigned>(BH));
@@ -450,19 +447,74 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
 #undef ROPESLR_SEL_CASE
     return launch_status();
   }
+  const int n2 = next_pow2(nb);
+  size_t sm = static_cast<size_t>(n2) * (sizeof(uint64_t) + sizeof(uint32_t)) + static_cast<size_t>(nb) * sizeof(int);
+  static_assert(sizeof(unsigned long long) == sizeof(int64_t), "int64 atomics");
+  if (sm > 48 * 1024) {
+    if (cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm)) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
+  }
+  select_rows_kernel<<<static_cast<unsigned>(BH * nb), 256, sm, st>>>(
+      scores, nb, n2, s->L, s->block, sel->topk, sel->keep, kmax, idx, cnt, mask,
+      reinterpret_cast<unsigned long long*>(attended));
+  return launch_status();
+}
+
+extern "C" size_t ropeslr_select_workspace_bytes(const ropeslr_shape* s) {
+  if (s == nullptr || s->block <= 0) return 0;
+  return pooled_bytes(s) + scores_bytes(s);
+}
+
+extern "C" size_t ropeslr_select_pooled_workspace_bytes(const ropeslr_shape* s) {
+  if (s == nullptr || s->block <= 0) return 0;
+  return scores_bytes(s);
+}
+
+extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_select_params* sel, const void* q,
+                                     const void* k, int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask,
+                                     int64_t* attended, double* scores_out, void* ws, size_t ws_bytes,
+                                     void* stream_) {
+  int stt = check_select(s, sel, kmax, idx, cnt, attended);
+  if (stt) return stt;
+  if (!q || !k) return ROPESLR_ERR_NULL;
+  if (!aligned16(q) || !aligned16(k)) return ROPESLR_ERR_ALIGN;
+  if (ws == nullptr || ws_bytes < ropeslr_select_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  const int64_t BH = s->B * s->H;
+  const int d = static_cast<int>(s->d);
+  const int nb = static_cast<int>(ceil_div(s->L, s->block));
+  double* pooled = static_cast<double*>(ws);
+  double* scores = scores_out ? scores_out : reinterpret_cast<double*>(static_cast<char*>(ws) + pooled_bytes(s));
   {
-    const int n2 = next_pow2(nb);
-    size_t sm = static_cast<size_t>(n2) * (sizeof(uint64_t) + sizeof(uint32_t)) + static_cast<size_t>(nb) * sizeof(int);
-    static_assert(sizeof(unsigned long long) == sizeof(int64_t), "int64 atomics");
-    if (sm > 48 * 1024) {
-      if (cudaFuncSetAttribute(select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(sm)) != cudaSuccess)
-        return ROPESLR_ERR_LAUNCH;
-    }
-    select_rows_kernel<<<static_cast<unsigned>(BH * nb), 256, sm, st>>>(
-        scores, nb, n2, s->L, s->block, sel->topk, sel->keep, kmax, idx, cnt, mask,
-        reinterpret_cast<unsigned long long*>(attended));
+    dim3 grid(nb, static_cast<unsigned>(BH), 2);
+    const int chunks = d / 8;
+    const int lanes_r = 256 / chunks;
+    size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
+    if (s->dtype == ROPESLR_BF16)
+      pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                                static_cast<const __nv_bfloat16*>(k), pooled, s->L,
+                                                                d, s->block, nb, BH);
+    else
+      pool_blocks_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q), static_cast<const float*>(k),
+                                                        pooled, s->L, d, s->block, nb, BH);
     if (launch_status()) return ROPESLR_ERR_LAUNCH;
   }
-  return ROPESLR_OK;
+  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores, st);
+}
+
+extern "C" int ropeslr_select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel,
+                                          const double* pooled, int32_t* idx, int32_t kmax, int32_t* cnt,
+                                          uint8_t* mask, int64_t* attended, double* scores_out, void* ws,
+                                          size_t ws_bytes, void* stream_) {
+  int stt = check_select(s, sel, kmax, idx, cnt, attended);
+  if (stt) return stt;
+  if (!pooled) return ROPESLR_ERR_NULL;
+  double* scores = scores_out;
+  if (scores == nullptr) {
+    if (ws == nullptr || ws_bytes < ropeslr_select_pooled_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
+    scores = static_cast<double*>(ws);
+  }
+  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores,
+                            static_cast<cudaStream_t>(stream_));
 }

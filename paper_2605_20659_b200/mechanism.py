@@ -338,8 +338,11 @@ def block_layout(L: int, settings: SparseSettings, grid: Optional[GridShape], de
 
 
 def select_blocks(q: torch.Tensor, k: torch.Tensor, settings: SparseSettings, grid: Optional[GridShape] = None,
-                  *, want_mask: bool = True, want_scores: bool = False, _layout=None) -> Selection:
-    """Block routing of block_sparse_attention (mechanism.py:305-320)."""
+                  *, want_mask: bool = True, want_scores: bool = False, _layout=None,
+                  pooled: Optional[torch.Tensor] = None) -> Selection:
+    """Block routing of block_sparse_attention (mechanism.py:305-320).
+    ``pooled`` ([2, B*H, nb, d] float64 block means, e.g. from ``rope_pool``)
+    skips the pooling stage."""
     _check_qkv(q, k)
     B, H, L, d = q.shape
     block, perm = _layout if _layout is not None else block_layout(L, settings, grid, q.device)
@@ -356,11 +359,19 @@ def select_blocks(q: torch.Tensor, k: torch.Tensor, settings: SparseSettings, gr
     attended = torch.empty((B, H), dtype=torch.int64, device=dev)
     scores = torch.empty((B, H, nb, nb), dtype=torch.float64, device=dev) if want_scores else None
     shp = _shape(q, block)
-    ws = _workspace(_lib.lib().ropeslr_select_workspace_bytes(ctypes_ref(shp)), dev)
     sel = _lib.SelectParams(int(settings.topk), float(settings.keep))
-    _lib.call("ropeslr_select_blocks", ctypes_ref(shp), ctypes_ref(sel), q.data_ptr(), k.data_ptr(), idx.data_ptr(),
-              kmax, cnt.data_ptr(), _ptr(mask), attended.data_ptr(), _ptr(scores), ws.data_ptr(), ws.numel(),
-              _stream(dev))
+    if pooled is not None:
+        if pooled.shape != (2, B * H, nb, d) or pooled.dtype != torch.float64 or not pooled.is_contiguous():
+            raise ValueError(f"pooled must be contiguous float64 [2, {B * H}, {nb}, {d}]")
+        ws = _workspace(_lib.lib().ropeslr_select_pooled_workspace_bytes(ctypes_ref(shp)), dev)
+        _lib.call("ropeslr_select_from_pooled", ctypes_ref(shp), ctypes_ref(sel), pooled.data_ptr(), idx.data_ptr(),
+                  kmax, cnt.data_ptr(), _ptr(mask), attended.data_ptr(), _ptr(scores), ws.data_ptr(), ws.numel(),
+                  _stream(dev))
+    else:
+        ws = _workspace(_lib.lib().ropeslr_select_workspace_bytes(ctypes_ref(shp)), dev)
+        _lib.call("ropeslr_select_blocks", ctypes_ref(shp), ctypes_ref(sel), q.data_ptr(), k.data_ptr(),
+                  idx.data_ptr(), kmax, cnt.data_ptr(), _ptr(mask), attended.data_ptr(), _ptr(scores), ws.data_ptr(),
+                  ws.numel(), _stream(dev))
     return Selection(idx=idx, cnt=cnt, mask=None if mask is None else mask.bool(), attended=attended,
                      scores=scores, kmax=kmax, block=block, perm=perm)
 
@@ -369,6 +380,31 @@ def ctypes_ref(obj):
     import ctypes
 
     return ctypes.byref(obj)
+
+
+def rope_pool(q: torch.Tensor, k: torch.Tensor, grid: GridShape, cfg: RopeConfig, block: int):
+    """Fused 3D RoPE + block pooling (the pre-pass of K1): un-rotated Q/K
+    [B, H, L, d] -> rotated Q/K (same dtype; rope3d.py:102-143, computed like
+    ``rope3d.rotate_rows`` then cast) and the float64 block means of the
+    rotated values, [2, B*H, nb, d] (mechanism.py:306-308), in one pass."""
+    _check_qkv(q, k)
+    B, H, L, d = q.shape
+    if grid.size != L:
+        raise ValueError(f"grid size {grid.size} != sequence length {L}")
+    if cfg.d_h != d:
+        raise ValueError(f"rotary split {cfg.split} does not sum to the head dim {d}")
+    if isinstance(block, tuple) or int(block) < 1:
+        raise ValueError("rope_pool takes a flat token block")
+    q, k = q.contiguous(), k.contiguous()
+    nb = -(-L // int(block))
+    q_out, k_out = torch.empty_like(q), torch.empty_like(k)
+    pooled = torch.empty((2, B * H, nb, d), dtype=torch.float64, device=q.device)
+    shp = _shape(q, int(block))
+    ra = _lib.RopeArgs(cfg.d_t, cfg.d_x, cfg.d_y, grid.t, grid.h, grid.w, float(cfg.base))
+    ws = _workspace(_lib.lib().ropeslr_rope_pool_workspace_bytes(ctypes_ref(ra)), q.device)
+    _lib.call("ropeslr_rope_pool", ctypes_ref(shp), ctypes_ref(ra), q.data_ptr(), k.data_ptr(), q_out.data_ptr(),
+              k_out.data_ptr(), pooled.data_ptr(), ws.data_ptr(), ws.numel(), _stream(q.device))
+    return q_out, k_out, pooled
 
 
 # ---------------------------------------------------------------------------
@@ -514,9 +550,11 @@ class Prepared:
 def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, grid: GridShape,
             params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False,
-            head_offset: int = 0) -> Prepared:
+            head_offset: int = 0, rope: Optional[RopeConfig] = None) -> Prepared:
     """K1 (routing, mechanism.py:305-320) and K3 (compensator + partial gate
-    logits, mechanism.py:429-447) for the local heads."""
+    logits, mechanism.py:429-447) for the local heads.  With ``rope`` the
+    given Q/K are un-rotated: the fused RoPE + pooling pre-pass rotates them
+    (rope3d.py:102-143) and feeds its block means straight to the selection."""
     _check_qkv(q, k, v)
     B, H, L, d = q.shape
     if x.dtype != q.dtype:
@@ -525,11 +563,16 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
         raise ValueError("parameters do not match the head count / head dim")
     layout = block_layout(L, settings.sparse, grid, q.device)
     block, perm = layout
+    pooled = None
+    if rope is not None:
+        if perm is not None:
+            raise ValueError("the fused RoPE pre-pass takes flat blocks")
+        q, k, pooled = rope_pool(q, k, grid, rope, block)
     if perm is not None:
         pl = perm.long()
         q, k, v = q.index_select(2, pl), k.index_select(2, pl), v.index_select(2, pl)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    sel = select_blocks(q, k, settings.sparse, want_mask=trace, _layout=layout)
+    sel = select_blocks(q, k, settings.sparse, want_mask=trace, _layout=layout, pooled=pooled)
     y_lr, o_lr, g_logit = compensator_branch(x, grid, params, settings, pe, head_offset=head_offset,
                                              lin_proj=lin_proj, want_o_lr=trace, H_local=H)
     return Prepared(q=q, k=k, v=v, sel=sel, y_lr=y_lr, o_lr=o_lr, g_logit=g_logit, block=block, perm=perm)
@@ -559,17 +602,21 @@ def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *
 def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, grid: GridShape,
             params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False, impl: str = "auto",
-            head_offset: int = 0, gate_reduce: Optional[Callable[[torch.Tensor], None]] = None):
+            head_offset: int = 0, gate_reduce: Optional[Callable[[torch.Tensor], None]] = None,
+            rope: Optional[RopeConfig] = None):
     """RoPeSLR forward (mechanism.py:491-512, Algorithm 1).
 
     q, k, v: post-RoPE [B, H, L, d] (bf16 or f32); x: token features
     [B, L, H*d] of the same dtype (may be a column slice of a wider X for a
     head-parallel rank, with ``head_offset`` its first global head and
     ``gate_reduce`` an in-place all-reduce of the partial gate logits).
+    With ``rope`` (a RopeConfig), q and k are the un-rotated projections and
+    the fused RoPE + pooling pre-pass rotates them on the way in.
 
     Returns the output [B, L, H*d] (x's dtype), or a ForwardTrace when
     ``trace`` (adds the float32 branch outputs, the gate and the masks)."""
-    prep = prepare(q, k, v, x, grid, params, settings, pe, lin_proj=lin_proj, trace=trace, head_offset=head_offset)
+    prep = prepare(q, k, v, x, grid, params, settings, pe, lin_proj=lin_proj, trace=trace, head_offset=head_offset,
+                   rope=rope)
     if gate_reduce is not None:
         gate_reduce(prep.g_logit)
     out, o_sparse = attend(prep, params, settings, impl=impl, want_o_sparse=trace)
