@@ -387,25 +387,82 @@ def run_ours(args, cfg, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_dit(args, rank, world, local_rank):
+    """BASELINE config 4: one denoising step of the Wan2.1-1.3B-shaped DiT
+    (random init, bf16) with RoPeSLR self-attention at 90% sparsity; the
+    sequence is sharded across the ranks and the op runs under the Ulysses
+    all-to-all (NCCL).  Reports ms per step (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_20659_b200.dit import WanConfig, make_model
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = WanConfig()
+    model = make_model(cfg, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    latent = torch.randn((1, cfg.in_channels, 21, 60, 104), generator=gen, device=dev).to(torch.bfloat16)
+    text = torch.randn((1, cfg.text_len, cfg.text_dim), generator=gen, device=dev).to(torch.bfloat16)
+    t = torch.tensor([500.0], device=dev)
+    group = dist.group.WORLD if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.no_grad():
+        for _ in range(args.warmup):
+            model(latent, t, text, group=group)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clocks:
+            e0.record(stream)
+            for _ in range(args.steps):
+                out = model(latent, t, text, group=group)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank != 0:
+        return
+    ms = float(ms.item())
+    line = {
+        "metric": "Wan2.1-1.3B DiT denoising step (RoPeSLR 90% self-attention), ms", "value": ms, "unit": "ms",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic latent 16x21x60x104, 512 synthetic text tokens, random-init weights",
+        "config": {"workload": "cfg4_wan1.3b_dit_step_L32760", "blocks": cfg.blocks, "dim": cfg.dim,
+                   "heads": cfg.heads, "ffn": cfg.ffn, "block": cfg.block, "sparsity": cfg.sparsity,
+                   "parallelism": f"sequence x{world} (Ulysses all-to-all around RoPeSLR)"},
+        "clocks": clocks.summary(), "output_finite": bool(torch.isfinite(out.float()).all()),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS), default="cfg3")
+    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4"], default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-qblocks", type=int, default=300)
     ap.add_argument("--ref-qblocks", type=int, default=100)
     ap.add_argument("--chunk-heads", type=int, default=0, help="heads per H2D/compute chunk of the e2e path (0 = auto)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = CONFIGS.get(args.config)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
+        run_reference(args, cfg or CONFIGS["cfg1"], rank, world)
         return
     import torch
     import torch.distributed as dist
@@ -414,7 +471,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, cfg, rank, world, local_rank)
+        if args.config == "cfg4":
+            run_dit(args, rank, world, local_rank)
+        else:
+            run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:
             dist.destroy_process_group()

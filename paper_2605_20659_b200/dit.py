@@ -1,0 +1,191 @@
+"""Wan2.1-1.3B-architecture DiT with RoPeSLR self-attention (BASELINE
+config 4): the caller of the op in an end-to-end denoising step.
+
+This is not the reference's code -- the reference has no model (SURVEY.md
+8f "next" #2) -- but a random-init stand-in with the published shape:
+30 blocks, hidden 1536, 12 heads of 128, FFN 8960, cross-attention to 512
+text tokens of width 4096, a 16-channel latent patched 1x2x2.  Per block:
+
+  adaLN-modulated LayerNorm -> Q/K/V projections (cuBLAS) with RMSNorm on
+  Q and K -> RoPeSLR attention (the op; Q/K rotated by its fused RoPE +
+  pooling pre-pass; X = the modulated hidden state feeds the low-rank
+  compensator and gate) -> output projection, gated residual;
+  cross-attention to the text tokens (torch SDPA); modulated FFN (GELU-tanh).
+
+With a process group, the sequence is sharded across the ranks and the op
+runs under ulysses_attention (all-to-all seq <-> head around it); every
+other layer is token-wise and needs no communication.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .mechanism import ForwardSettings, MechanismParams, PETables, SparseSettings, forward
+from .rope3d import GridShape, RopeConfig
+from .ulysses import seq_slice, ulysses_attention
+
+
+@dataclass(frozen=True)
+class WanConfig:
+    """Wan2.1-1.3B shape (BASELINE config 4)."""
+
+    dim: int = 1536
+    heads: int = 12
+    ffn: int = 8960
+    blocks: int = 30
+    text_len: int = 512
+    text_dim: int = 4096
+    in_channels: int = 16
+    patch: tuple = (1, 2, 2)
+    freq_dim: int = 256
+    rank: int = 64
+    sparsity: float = 0.9
+    block: int = 64
+    rope_split: tuple = (44, 42, 42)
+    eps: float = 1e-6
+
+    @property
+    def head_dim(self) -> int:
+        return self.dim // self.heads
+
+
+class RMSNorm(nn.Module):
+    def __init__(self, dim, eps):
+        super().__init__()
+        self.eps = eps
+        self.weight = nn.Parameter(torch.ones(dim))
+
+    def forward(self, x):
+        xf = x.float()
+        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.eps)).to(x.dtype) * self.weight
+
+
+def sinusoidal(t: torch.Tensor, dim: int) -> torch.Tensor:
+    half = dim // 2
+    freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=torch.float64, device=t.device) / half)
+    a = t.double()[:, None] * freqs[None]
+    return torch.cat([torch.cos(a), torch.sin(a)], dim=1).float()
+
+
+class WanBlock(nn.Module):
+    def __init__(self, cfg: WanConfig):
+        super().__init__()
+        D = cfg.dim
+        self.cfg = cfg
+        self.norm1 = nn.LayerNorm(D, eps=cfg.eps, elementwise_affine=False)
+        self.q, self.k, self.v, self.o = (nn.Linear(D, D) for _ in range(4))
+        self.norm_q, self.norm_k = RMSNorm(D, cfg.eps), RMSNorm(D, cfg.eps)
+        self.norm3 = nn.LayerNorm(D, eps=cfg.eps, elementwise_affine=True)
+        self.cq, self.ck, self.cv, self.co = (nn.Linear(D, D) for _ in range(4))
+        self.norm_cq, self.norm_ck = RMSNorm(D, cfg.eps), RMSNorm(D, cfg.eps)
+        self.norm2 = nn.LayerNorm(D, eps=cfg.eps, elementwise_affine=False)
+        self.ffn1, self.ffn2 = nn.Linear(D, cfg.ffn), nn.Linear(cfg.ffn, D)
+        self.modulation = nn.Parameter(torch.randn(1, 6, D) / math.sqrt(D))
+        # the RoPeSLR parameter set of this layer (mechanism.py:100-133)
+        H, d, r = cfg.heads, cfg.head_dim, cfg.rank
+        self.w_a = nn.Parameter(torch.randn(H, d, r) / math.sqrt(d))
+        self.w_b = nn.Parameter(torch.randn(H, r, d) / math.sqrt(r))
+        self.alpha = nn.Parameter(torch.full((D,), 0.1))
+        self.w_g = nn.Parameter(torch.randn(D) * 0.02)
+        self.rms_sparse = nn.Parameter(torch.ones(d))
+        self.rms_lowrank = nn.Parameter(torch.ones(d))
+
+    def ropeslr_params(self) -> MechanismParams:
+        f = lambda t: t.detach().float().contiguous()  # noqa: E731
+        return MechanismParams(w_a=f(self.w_a), w_b=f(self.w_b), alpha=f(self.alpha), w_g=f(self.w_g), b_g=-2.0,
+                               rms_sparse=f(self.rms_sparse), rms_lowrank=f(self.rms_lowrank))
+
+    def forward(self, x, e, ctx, grid: GridShape, pe: PETables, settings: ForwardSettings, rope: RopeConfig,
+                group=None):
+        cfg = self.cfg
+        B, Lr, D = x.shape
+        H, d = cfg.heads, cfg.head_dim
+        sh_a, sc_a, g_a, sh_f, sc_f, g_f = (self.modulation + e).chunk(6, dim=1)
+        y = (self.norm1(x.float()) * (1 + sc_a) + sh_a).to(x.dtype)
+        q = self.norm_q(self.q(y)).view(B, Lr, H, d)
+        k = self.norm_k(self.k(y)).view(B, Lr, H, d)
+        v = self.v(y).view(B, Lr, H, d)
+        params = self.ropeslr_params()
+        if group is not None:
+            a = ulysses_attention(q, k, v, y, grid, params, settings, pe, group=group, rope=rope)
+        else:
+            qh, kh, vh = (t.permute(0, 2, 1, 3).contiguous() for t in (q, k, v))
+            a = forward(qh, kh, vh, y.contiguous(), grid, params, settings, pe, rope=rope)
+        x = x + (self.o(a).float() * g_a).to(x.dtype)
+        # cross-attention to the text tokens
+        c = self.norm3(x)
+        cq = self.norm_cq(self.cq(c)).view(B, Lr, H, d).transpose(1, 2)
+        ck = self.norm_ck(self.ck(ctx)).view(B, -1, H, d).transpose(1, 2)
+        cv = self.cv(ctx).view(B, -1, H, d).transpose(1, 2)
+        ca = F.scaled_dot_product_attention(cq, ck, cv).transpose(1, 2).reshape(B, Lr, D)
+        x = x + self.co(ca)
+        y = (self.norm2(x.float()) * (1 + sc_f) + sh_f).to(x.dtype)
+        x = x + (self.ffn2(F.gelu(self.ffn1(y), approximate="tanh")).float() * g_f).to(x.dtype)
+        return x
+
+
+class WanDiT(nn.Module):
+    """Patch embedding, text / time embeddings, the blocks, the output head."""
+
+    def __init__(self, cfg: WanConfig):
+        super().__init__()
+        D = cfg.dim
+        self.cfg = cfg
+        pt, ph, pw = cfg.patch
+        self.patch_embed = nn.Linear(cfg.in_channels * pt * ph * pw, D)
+        self.text_embed = nn.Sequential(nn.Linear(cfg.text_dim, D), nn.GELU(approximate="tanh"), nn.Linear(D, D))
+        self.time_embed = nn.Sequential(nn.Linear(cfg.freq_dim, D), nn.SiLU(), nn.Linear(D, D))
+        self.time_proj = nn.Sequential(nn.SiLU(), nn.Linear(D, 6 * D))
+        self.blocks = nn.ModuleList(WanBlock(cfg) for _ in range(cfg.blocks))
+        self.head_norm = nn.LayerNorm(D, eps=cfg.eps, elementwise_affine=False)
+        self.head_mod = nn.Parameter(torch.randn(1, 2, D) / math.sqrt(D))
+        self.head = nn.Linear(D, cfg.in_channels * pt * ph * pw)
+        d = cfg.head_dim
+        self.rope = RopeConfig(*cfg.rope_split)
+        # learnable 3D absolute PE of RoPeSLR, per-axis tables (shared by the blocks)
+        self.pe_tables = None
+
+    def patchify(self, latent: torch.Tensor):
+        """[B, C, T, Hh, Ww] -> tokens [B, L, C*pt*ph*pw] and the token grid."""
+        B, C, T, Hh, Ww = latent.shape
+        pt, ph, pw = self.cfg.patch
+        g = GridShape(T // pt, Hh // ph, Ww // pw)
+        x = latent.view(B, C, g.t, pt, g.h, ph, g.w, pw).permute(0, 2, 4, 6, 1, 3, 5, 7)
+        return x.reshape(B, g.size, C * pt * ph * pw), g
+
+    def forward(self, latent, t, text, group=None):
+        cfg = self.cfg
+        tokens, grid = self.patchify(latent)
+        world, rank = (torch.distributed.get_world_size(group), torch.distributed.get_rank(group)) if group else (1, 0)
+        a, b = seq_slice(grid.size, world, rank)
+        x = self.patch_embed(tokens[:, a:b])
+        ctx = self.text_embed(text)
+        e0 = self.time_embed(sinusoidal(t, cfg.freq_dim).to(x.dtype))
+        e = self.time_proj(e0).view(-1, 6, cfg.dim).float()
+        if self.pe_tables is None or self.pe_tables.pe_t.shape[0] != grid.t:
+            gen = torch.Generator(device=x.device).manual_seed(1234)
+            self.pe_tables = PETables(*(torch.randn((n, cfg.dim), generator=gen, device=x.device) * 0.02
+                                        for n in grid.as_tuple()))
+        nb = -(-grid.size // cfg.block)
+        settings = ForwardSettings(SparseSettings(block=cfg.block, topk=SparseSettings.topk_for_sparsity(nb, cfg.sparsity)))
+        for blk in self.blocks:
+            x = blk(x, e, ctx, grid, self.pe_tables, settings, self.rope, group=group)
+        sh, sc = (self.head_mod + e0.float()[:, None]).chunk(2, dim=1)
+        return self.head((self.head_norm(x.float()) * (1 + sc) + sh).to(x.dtype))
+
+
+def make_model(cfg: Optional[WanConfig] = None, device="cuda", dtype=torch.bfloat16, seed=0) -> WanDiT:
+    torch.manual_seed(seed)
+    m = WanDiT(cfg or WanConfig())
+    for mod in m.modules():
+        if isinstance(mod, nn.Linear):
+            nn.init.normal_(mod.weight, std=0.02)
+            nn.init.zeros_(mod.bias)
+    return m.to(device=device, dtype=dtype).eval()
