@@ -300,6 +300,21 @@ def run_ours(args, cfg, rank, world, local_rank):
     k2_ms_local = statistics.mean(a.elapsed_time(b) for a, b in zip(k2_start, k2_end))
     clock_summary = clocks.summary()
 
+    # ---- the fused RoPE + pooling pre-pass, measured
+    # alone on this rank's Q/K taken as the un-rotated projections
+    rope_ms = None
+    if not args.no_rope_pass:
+        rope = P.RopeConfig(*cfg["split"])
+        for _ in range(2):
+            P.rope_pool(q, k, grid, rope, cfg["block"])
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(5):
+            P.rope_pool(q, k, grid, rope, cfg["block"])
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rope_ms = r0.elapsed_time(r1) / 5
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -357,6 +372,11 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "l2": "inputs (2.9 GB) larger than L2; no explicit flush"},
         "tflops_per_gpu": value / world,
         "sparse_attn_ms": k2_ms,
+        "rope_pool_prepass": None if rope_ms is None else {
+            "ms": rope_ms, "bytes": 4 * q.numel() * q.element_size(),
+            "GB_per_s": 4 * q.numel() * q.element_size() / (rope_ms * 1e-3) / 1e9,
+            "frac_of_hbm": 4 * q.numel() * q.element_size() / (rope_ms * 1e-3) / 1e9 / load_peaks().get("hbm_gbs", 6650.0),
+            "note": "rank 0: read un-rotated Q,K + write rotated Q,K (pooled means ride along)"},
         "attended_pairs": attended_total,
         "sparsity": 1.0 - attended_total / (H * float(L) ** 2),
         "roofline": {"bound": "tensor", "kernel": "sparse_attn_tc_kernel (K2+K4 fused)",
@@ -453,6 +473,7 @@ def main():
     ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4"], default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rope-pass", action="store_true", help="skip timing the fused RoPE + pooling pre-pass")
     ap.add_argument("--cpu-qblocks", type=int, default=300)
     ap.add_argument("--ref-qblocks", type=int, default=100)
     ap.add_argument("--chunk-heads", type=int, default=0, help="heads per H2D/compute chunk of the e2e path (0 = auto)")

@@ -358,6 +358,76 @@ def fused_forward(x, sparse_out, pe, params: dict, compensator: str = "lowrank",
 
 
 # ---------------------------------------------------------------------------
+# Stage-I backward (mechanism.py:411-423, 456-488, 519-565): gradients of the
+# alignment loss w.r.t. the new parameter set, the sparse branch constant.
+
+
+def rms_backward(d_y, o, scale, eps: float = RMS_EPS):
+    """mechanism._rms_backward (mechanism.py:417-423) with the cache of
+    mechanism._rms_cache (mechanism.py:411-414) recomputed from o."""
+    o = np.asarray(o, np.float64)
+    inv = 1.0 / np.sqrt(np.mean(o * o, axis=1, keepdims=True) + eps)
+    u = o * inv
+    d_scale = np.sum(d_y * u, axis=0)
+    d_u = d_y * np.asarray(scale, np.float64)[None, :]
+    dot = np.sum(d_u * o, axis=1, keepdims=True)
+    d_o = d_u * inv - o * (inv ** 3 * dot / o.shape[1])
+    return d_o, d_scale
+
+
+def fused_backward(g_out, x, sparse_out, pe, params: dict, use_pe: bool = True, eps: float = RMS_EPS) -> dict:
+    """mechanism._fused_backward (mechanism.py:456-488), low-rank compensator:
+    d loss / d output = g_out (L, D) -> gradients of w_a, w_b, alpha, w_g, b_g,
+    rms_sparse, rms_lowrank (same names and shapes as the parameters)."""
+    x = np.asarray(x, np.float64)
+    H = len(sparse_out)
+    d = sparse_out[0].shape[1]
+    w_a = np.asarray(params["w_a"], np.float64)
+    w_b = np.asarray(params["w_b"], np.float64)
+    w_g = np.asarray(params["w_g"], np.float64)
+    alpha = np.asarray(params["alpha"], np.float64)
+    x_hat = x + alpha[None, :] * np.asarray(pe, np.float64) if use_pe else x
+    g = sigmoid(x_hat @ w_g + float(params["b_g"]))
+    grads = {n: np.zeros_like(np.asarray(params[n], np.float64)) for n in
+             ("w_a", "w_b", "alpha", "w_g", "rms_sparse", "rms_lowrank")}
+    grads["b_g"] = 0.0
+    d_g = np.zeros(x.shape[0])
+    d_xhat = np.zeros_like(x_hat)
+    for h in range(H):
+        gh = np.asarray(g_out, np.float64)[:, h * d:(h + 1) * d]
+        _, d_rs = rms_backward(gh, sparse_out[h], params["rms_sparse"], eps)
+        grads["rms_sparse"] += d_rs
+        xh = x_hat[:, h * d:(h + 1) * d]
+        h1 = sigmoid(xh @ w_a[h])
+        o_lr = sigmoid(h1 @ w_b[h])
+        y_lr = rms_norm(o_lr, params["rms_lowrank"], eps)
+        d_g += np.sum(gh * y_lr, axis=1)
+        d_o_lr, d_rl = rms_backward(gh * g[:, None], o_lr, params["rms_lowrank"], eps)
+        grads["rms_lowrank"] += d_rl
+        d_z2 = d_o_lr * o_lr * (1.0 - o_lr)
+        grads["w_b"][h] += h1.T @ d_z2
+        d_z1 = (d_z2 @ w_b[h].T) * h1 * (1.0 - h1)
+        grads["w_a"][h] += xh.T @ d_z1
+        d_xhat[:, h * d:(h + 1) * d] += d_z1 @ w_a[h].T
+    d_zg = d_g * g * (1.0 - g)
+    grads["w_g"] += x_hat.T @ d_zg
+    grads["b_g"] += float(d_zg.sum())
+    d_xhat += np.outer(d_zg, w_g)
+    if use_pe:
+        grads["alpha"] += np.sum(d_xhat * np.asarray(pe, np.float64), axis=0)
+    return grads
+
+
+def align_loss_and_grads(x, sparse_out, pe, target, params: dict, use_pe: bool = True, eps: float = RMS_EPS):
+    """One sample of mechanism._loss_and_grads (mechanism.py:552-565): mean
+    squared error against the target and its parameter gradients."""
+    out = fused_forward(x, sparse_out, pe, params, use_pe=use_pe, eps=eps)["output"]
+    diff = out - np.asarray(target, np.float64)
+    loss = float(np.mean(diff * diff))
+    return loss, fused_backward(2.0 * diff / diff.size, x, sparse_out, pe, params, use_pe, eps)
+
+
+# ---------------------------------------------------------------------------
 # flops accounting (flops.py:30-63)
 
 
