@@ -103,11 +103,16 @@ __global__ void __launch_bounds__(256) rope_pool_kernel(const T* __restrict__ q_
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0;
   if (rr < lanes_r) {
+    // grid coordinates of the first row, then stepped by lanes_r tokens
+    // (L < 2^31: 32-bit index arithmetic)
+    int p0 = static_cast<int>(r0 + rr);
+    int ct = p0 / static_cast<int>(frame);
+    int rem = p0 - ct * static_cast<int>(frame);
+    int cx = rem / grid_w;
+    int cy = rem - cx * grid_w;
+    const int step_x = lanes_r / grid_w, step_y = lanes_r % grid_w;
     for (int r = rr; r < rows; r += lanes_r) {
       const int64_t pos = r0 + r;
-      const int ct = static_cast<int>(pos / frame);
-      const int cx = static_cast<int>((pos % frame) / grid_w);
-      const int cy = static_cast<int>(pos % grid_w);
       float v[8];
       load8(src + pos * d + ch * 8, v);
       double out[8];
@@ -130,6 +135,17 @@ __global__ void __launch_bounds__(256) rope_pool_kernel(const T* __restrict__ q_
       } else {
         *reinterpret_cast<float4*>(dst + pos * d + ch * 8) = *reinterpret_cast<const float4*>(ov);
         *reinterpret_cast<float4*>(dst + pos * d + ch * 8 + 4) = *reinterpret_cast<const float4*>(ov + 4);
+      }
+      // advance (t, x, y) by lanes_r tokens
+      cy += step_y;
+      cx += step_x;
+      if (cy >= grid_w) {
+        cy -= grid_w;
+        ++cx;
+      }
+      while (cx >= grid_h) {
+        cx -= grid_h;
+        ++ct;
       }
     }
 #pragma unroll
