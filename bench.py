@@ -464,13 +464,64 @@ def run_dit(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_sweep(args, local_rank):
+    """BASELINE config 2: sparsity 80/90/95% x block 64/128 on the Wan2.1
+    shape (H=12, d=128, L=32760, r=64).  One JSON line per point with the
+    sparse branch (K2+K4) TF/s against the bf16 peak and the low-rank branch
+    (K3) HBM GB/s against the copy peak, each timed alone with CUDA events."""
+    import torch
+
+    import paper_2605_20659_b200 as P
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    peaks = load_peaks()
+    base = dict(name="wan1.3b_attn_L32760_H12_d128", grid=(21, 30, 52), H=12, d=128, split=(44, 42, 42), r=64)
+    q, k, v, x, params, pe, grid = make_inputs(dict(base, block=64, sparsity=0.9), 0, base["H"], dev)
+    L = grid.size
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, n):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    for block in (64, 128):
+        for sparsity in (0.8, 0.9, 0.95):
+            st = P.ForwardSettings(P.SparseSettings.for_sparsity(block, L, sparsity))
+            prep = P.prepare(q, k, v, x, grid, params, st, pe)
+            out = torch.empty((1, L, base["H"], base["d"]), dtype=torch.bfloat16, device=dev)
+            k2_ms = timed(lambda: P.attend(prep, params, st, out=out), max(3, args.steps))
+            k3_ms = timed(lambda: P.compensator_branch(x, grid, params, st, pe), max(3, args.steps))
+            torch.cuda.synchronize()
+            att = int(prep.sel.attended.sum())
+            tf = 4.0 * base["d"] * att / (k2_ms * 1e-3) / 1e12
+            k3_bytes = 2 * x.numel() * x.element_size()
+            gbs = k3_bytes / (k3_ms * 1e-3) / 1e9
+            print(json.dumps({
+                "metric": "config 2 sweep point", "config": {"workload": f"{base['name']}_b{block}_s{int(sparsity * 100)}",
+                                                            "block": block, "sparsity": sparsity,
+                                                            "topk": st.sparse.topk},
+                "sparse_branch": {"ms": k2_ms, "TFLOP_per_s": tf, "frac_of_bf16_peak": tf / peaks["bf16_tflops"],
+                                  "peak": peaks["bf16_tflops"], "attended_pairs": att},
+                "lowrank_branch": {"ms": k3_ms, "GB_per_s": gbs, "frac_of_hbm": gbs / peaks["hbm_gbs"],
+                                   "bytes": k3_bytes},
+                "dtype": "bf16", "data": "synthetic (seeded N(0,1), 3D RoPE)"}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4"], default="cfg3")
+    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep"], default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rope-pass", action="store_true", help="skip timing the fused RoPE + pooling pre-pass")
@@ -494,6 +545,8 @@ def main():
     try:
         if args.config == "cfg4":
             run_dit(args, rank, world, local_rank)
+        elif args.config == "cfg2_sweep":
+            run_sweep(args, local_rank)
         else:
             run_ours(args, cfg, rank, world, local_rank)
     finally:
