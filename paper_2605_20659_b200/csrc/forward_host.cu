@@ -55,6 +55,28 @@ int chunk_heads(const ropeslr_host_forward* a) {
   return c < 1 ? 1 : c;
 }
 
+// Head chunks: Hc heads each, except that the last Hc heads go one per chunk,
+// so the compute and the output copy left after the final input copy are
+// one head's worth.
+struct Chunk {
+  int64_t h0, hc;
+};
+
+Chunk chunk_at(int64_t H, int Hc, int c) {
+  const int64_t tail = Hc > 1 && H > Hc ? Hc : 0;
+  const int64_t n1 = ceil_div(H - tail, Hc);
+  if (c < n1) {
+    const int64_t h0 = static_cast<int64_t>(c) * Hc;
+    return {h0, (H - tail - h0) < Hc ? (H - tail - h0) : Hc};
+  }
+  return {H - tail + (c - n1), 1};
+}
+
+int chunk_count(int64_t H, int Hc) {
+  const int64_t tail = Hc > 1 && H > Hc ? Hc : 0;
+  return static_cast<int>(ceil_div(H - tail, Hc) + tail);
+}
+
 // Workspace carve-up (offsets only; base may be null for sizing).
 struct Plan {
   int Hc, nchunks;
@@ -68,7 +90,7 @@ Plan make_plan(const ropeslr_host_forward* a) {
   const ropeslr_shape& s = a->shape;
   const size_t es = elem_bytes(s);
   p.Hc = chunk_heads(a);
-  p.nchunks = static_cast<int>(ceil_div(s.H, p.Hc));
+  p.nchunks = chunk_count(s.H, p.Hc);
   p.nb = ceil_div(s.L, s.block);
   p.kmax = kmax_of(a, p.nb);
   const size_t act = static_cast<size_t>(s.B * s.H * s.L * s.d) * es;
@@ -236,8 +258,8 @@ extern "C" int ropeslr_forward_host(const ropeslr_host_forward* a, void* workspa
                             static_cast<const uint8_t*>(a->v)};
   const size_t doff[3] = {p.q, p.k, p.v};
   for (int c = 0; c < p.nchunks; ++c) {
-    const int64_t h0 = static_cast<int64_t>(c) * p.Hc;
-    const int64_t hc = (H - h0) < p.Hc ? (H - h0) : p.Hc;
+    const Chunk ck = chunk_at(H, p.Hc, c);
+    const int64_t h0 = ck.h0, hc = ck.hc;
     for (int t = 0; t < 3; ++t) {
       uint8_t* dst = base + doff[t] + static_cast<size_t>(B * h0) * head_bytes;
       ROPESLR_TRY_CUDA(cudaMemcpy2DAsync(dst, hc * head_bytes, hsrc[t] + h0 * head_bytes, H * head_bytes,
@@ -268,8 +290,8 @@ extern "C" int ropeslr_forward_host(const ropeslr_host_forward* a, void* workspa
   int32_t* idx = reinterpret_cast<int32_t*>(base + p.idx);
   int32_t* cnt = reinterpret_cast<int32_t*>(base + p.cnt);
   for (int c = 0; c < p.nchunks; ++c) {
-    const int64_t h0 = static_cast<int64_t>(c) * p.Hc;
-    const int64_t hc = (H - h0) < p.Hc ? (H - h0) : p.Hc;
+    const Chunk ck = chunk_at(H, p.Hc, c);
+    const int64_t h0 = ck.h0, hc = ck.hc;
     ropeslr_shape sc = s;
     sc.H = hc;
     const size_t coff = static_cast<size_t>(B * h0) * head_bytes;
