@@ -383,7 +383,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": peaks["source"] + ", bf16 dense sustained (kernel timed inside a long step)",
                      "peak_burst": peaks.get("bf16_tflops"), "frac_of_burst": achieved / peaks.get("bf16_tflops", 1),
-                     "traffic": None,
+                     # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the
+                     # committed ncu --set full capture (profiles/r01c_ncu_summary.md)
+                     "traffic": 11.46e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
+                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01c_ncu_summary.md",
                      "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)"},
         "clocks": clock_summary,
         "gpu_launches": KERNELS_PER_STEP * args.steps,

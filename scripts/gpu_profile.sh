@@ -13,4 +13,4 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k "$KRE" -c
   -o gpurun_out/${tag}_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline "$@" \
   > gpurun_out/${tag}_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/${tag}_full.log
-tail -2 gpurun_out/${tag}_launches.log gpurun_out/${tag}_full.log
+tail -n 2 gpurun_out/${tag}_launches.log; tail -n 2 gpurun_out/${tag}_full.log
