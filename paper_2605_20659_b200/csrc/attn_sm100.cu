@@ -431,6 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t tS = lane_addr + pr * 128;
     const uint32_t tOh = lane_addr + O_COL + pr * 128 + w * (D / 2);
+    // rows >= BLK of the 128-row MMA tile are padding (block 64)
+    const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
     uint32_t g = 0, uc = 0;
     for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
       const int bh = static_cast<int>(u / p.nb);
@@ -448,11 +450,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const bool trc = p.trace && blockIdx.x == 0 && row == 0 && t < 64;
         if (trc) p.trace[(w * 64 + t) * 4 + 0] = clock64();
+        float* xm = xch + (pr * 2 + ((t >> 1) & 1)) * 256;  // [pair][tile parity][wg][row]
+        if (!rows_live) {
+          // block 64: TMEM lanes 64-127 hold the zero query rows of the MMA
+          // tile; their warps only keep the pair barrier and P_FULL counts
+          named_bar_sync(1 + pr, 256);
+          tc_fence_before();
+          mbar_arrive(&bars[Bx::P_FULL + pr]);
+          continue;
+        }
         uint32_t sr[HB];
 #pragma unroll
         for (int c = 0; c < HB / 32; ++c) tmem_ld32(tS + w * HB + c * 32, sr + c * 32);
         tmem_wait_ld();
-        float* xm = xch + (pr * 2 + ((t >> 1) & 1)) * 256;  // [pair][tile parity][wg][row]
         const int valid = kreal - w * HB;
         float mx = valid < HB ? half_max<BLK, true>(sr, valid, xm + w * 128 + row, xm + (w ^ 1) * 128 + row, 1 + pr)
                               : half_max<BLK, false>(sr, HB, xm + w * 128 + row, xm + (w ^ 1) * 128 + row, 1 + pr);
