@@ -48,6 +48,12 @@ KERNELS_PER_STEP = 7
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+# L2 -> SM bandwidth of K2's access pattern (random 32 KiB block tiles of one
+# head, TMA, 4 stages in flight per SM, all 148 SMs): 10.85 TB/s measured on
+# B200 by scripts/ubench/tma_l2_rate.cu (profiles/r01d_tma_l2_rate.txt)
+L2_TMA_TBPS = 10.85
+
+
 def load_peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -286,6 +292,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         prep = step()
     torch.cuda.synchronize()
     attended_local = int(prep.sel.attended.sum())
+    tiles_local = int(prep.sel.cnt.sum())  # (query block, selected key block) pairs = K/V tiles K2 streams
     barrier()
     torch.cuda.synchronize()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -387,7 +394,16 @@ def run_ours(args, cfg, rank, world, local_rank):
                      # committed ncu --set full capture (profiles/r01c_ncu_summary.md)
                      "traffic": 11.46e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
                      "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01c_ncu_summary.md",
-                     "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)"},
+                     "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)",
+                     # what actually bounds K2: every (query block, key block) tile streams
+                     # its K and V block (2 * block * d * 2 B) from L2 into shared memory.
+                     # peak = the measured L2 -> SM TMA rate of that access pattern
+                     # (scripts/ubench/tma_l2_rate.cu, profiles/r01d_tma_l2_rate.txt)
+                     "l2": {"bytes": tiles_local * 2 * cfg["block"] * d * 2,
+                            "achieved_TBps": tiles_local * 2 * cfg["block"] * d * 2 / (k2_ms_local * 1e-3) / 1e12,
+                            "peak_TBps": L2_TMA_TBPS,
+                            "frac": tiles_local * 2 * cfg["block"] * d * 2 / (k2_ms_local * 1e-3) / 1e12 / L2_TMA_TBPS,
+                            "peak_source": "measured: scripts/ubench/tma_l2_rate.cu, profiles/r01d_tma_l2_rate.txt"}},
         "clocks": clock_summary,
         "gpu_launches": KERNELS_PER_STEP * args.steps,
     }

@@ -1,0 +1,817 @@
+// EXPERIMENT (not built by default; scripts/build_variant.sh builds it as a
+// drop-in replacement of csrc/attn_sm100.cu for A/B timing).  K2 "v8": four
+// softmax warpgroups on column quarters of every tile, three S buffers in
+// TMEM and one O accumulator, software-pipelined (the next tile's scores are
+// loaded and their max published before this tile's exponentials).  Parity
+// green on B200; slower than the shipped kernel (2185 vs 1540 SM cycles per
+// 128x128 tile at config 3, 8 heads): see DESIGN.md section 3.
+// K2 + K4: block-sparse softmax attention on the 5th-generation tensor cores
+// with the fused RoPeSLR epilogue (mechanism.py:321-326 and 437-451).
+//
+// One persistent CTA per SM walks work units (bh, query block) in head-major
+// order, so the ~150 CTAs in flight read the K/V blocks of one or two heads
+// and those stay resident in the 126 MB L2.  Per unit:
+//
+//   warp 0  TMA producer   Q tile once per unit, then K_j for every selected
+//                          key block j (contiguous [block, 128] boxes of the
+//                          [B*H, L, d] tensors, 128-byte swizzle).
+//   warp 3  TMA producer   V_j, its own ring (a V slot frees only after its
+//                          PV, so it must not hold back the K prefetch).
+//   warp 1  MMA issuer     S_b = Q K_t^T into TMEM buffer b = t % 3 (SS-MMA),
+//                          O += P_b V_t as a TS-MMA reading P from TMEM;
+//                          tcgen05.commit releases smem stages and signals.
+//   warp 2  TMEM owner     alloc / dealloc of the 512 columns.
+//   warps 4-19             four softmax warpgroups splitting every key block
+//                          by columns: WG q owns keys [q*B/4, (q+1)*B/4) of
+//                          each S tile, one query row per thread.  Row max =
+//                          max of the four quarters (exchanged through shared
+//                          memory, one named barrier per tile), exp2-domain
+//                          softmax with the lazy (threshold 2^8) rescale of
+//                          the single O accumulator, bf16 P written back over
+//                          S_b.  Three S buffers let the softmax of tile t+1
+//                          start while PV(t) and QK(t+2) run: the softmax
+//                          never waits on the tensor pipe, only on its own
+//                          throughput (MUFU + FMA-pipe exp2).
+//                          Epilogue: O / l, RMSNorm * rms_sparse, +
+//                          sigmoid(g_logit + b_g) * y_lr, bf16 store; WG q
+//                          finalises O columns [32q, 32q + 32).
+//
+// TMEM columns: S_0, S_1, S_2 at [0,128), [128,256), [256,384); O [384,512).
+// Shared memory (block 128): Q 32K, K 2x32K, V 3x32K = 192 KiB.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <unistd.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace ropeslr {
+
+int launch_sparse_attention_simt(const ropeslr_shape* s, const void* q, const void* k, const void* v,
+                                 const int32_t* idx, int kmax, const int32_t* cnt, const int32_t* perm,
+                                 float* o_sparse, cudaStream_t st);
+
+namespace tc {
+
+using namespace sm100;
+
+constexpr int D = 128;   // head dim handled by this kernel
+constexpr int M = 128;   // MMA rows (query rows per tile)
+constexpr int NSB = 3;   // S buffers in TMEM
+constexpr int kThreads = 640;  // 4 control warps + 4 softmax warpgroups
+constexpr uint32_t O_COL = 384;  // TMEM columns: S_b [128b, 128b + 128) for b < 3, O [384, 512)
+// setmaxnreg moves registers inside the CTA's own pool, which holds what the
+// launch allotted: 96 per thread (65536 / 640, rounded down to 8) x 640.
+constexpr int kLaunchRegs = 96;
+constexpr int kCtrlRegs = 56;       // per thread, control warpgroup (TMA, MMA, TMEM)
+constexpr int kSoftmaxRegs = 104;   // per thread, softmax warpgroups
+static_assert(kCtrlRegs * 128 + kSoftmaxRegs * 512 <= kLaunchRegs * kThreads, "register pool overcommitted");
+
+template <int BLK>
+struct Layout {
+  static constexpr int Q_BYTES = M * D * 2;
+  static constexpr int KV_BYTES = BLK * D * 2;
+  static constexpr int KST = BLK == 128 ? 2 : 4;  // K ring depth (a K slot frees as soon as its QK^T lands)
+  static constexpr int VST = BLK == 128 ? 3 : 4;  // V ring depth (a V slot frees only after its PV)
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+  static constexpr int OFF_XCH = OFF_V + VST * KV_BYTES;  // row-max exchange 4 KiB + epilogue exchange 4 KiB
+  static constexpr int OFF_BAR = OFF_XCH + 8192;
+  static constexpr int NBAR = 2 * KST + 2 * VST + 12;
+  static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
+  // dynamic smem starts 1024-aligned (after the driver's 1 KiB reservation);
+  // the kernel traps if that ever changes
+  static constexpr int ALLOC = BYTES;
+  static_assert(ALLOC <= 227 * 1024, "shared memory budget");
+};
+
+// Barrier indices.  Global tile t uses S buffer t % 3.
+template <int BLK>
+struct Bars {
+  static constexpr int KST = Layout<BLK>::KST, VST = Layout<BLK>::VST;
+  static constexpr int Q_FULL = 0, Q_EMPTY = 1;
+  static constexpr int K_FULL = 2, K_EMPTY = K_FULL + KST;
+  static constexpr int V_FULL = K_EMPTY + KST, V_EMPTY = V_FULL + VST;
+  static constexpr int S_FULL = V_EMPTY + VST;  // +b: S_b = Q K_t^T landed
+  static constexpr int P_FULL = S_FULL + NSB;   // +b: all 16 softmax warps wrote P_b (count 16)
+  static constexpr int PV_DONE = P_FULL + NSB;  // +(t & 1): PV(t) completed
+  static constexpr int O_FULL = PV_DONE + 2;    // the unit's last PV completed
+  static constexpr int COUNT = O_FULL + 1;
+  static_assert(COUNT <= Layout<BLK>::NBAR, "barrier count");
+};
+
+struct Params {
+  const int32_t* idx;
+  const int32_t* cnt;
+  int kmax;
+  int nb;
+  int H;
+  int64_t L;
+  int64_t num_units;
+  const int32_t* perm;
+  float scale_log2;
+  const __nv_bfloat16* y_lr;
+  const float* g_logit;
+  float b_g;
+  const float* rms_sp;
+  float eps;
+  __nv_bfloat16* out;
+  float* o_sparse;
+  int out_H;   // heads per token row of out / y_lr (>= H when a head chunk writes into a wider row)
+  int out_h0;  // first head of this call inside that row
+  int kv_evict_last;
+  int debug_mode;  // 0 normal; 1 no softmax math; 2 every K/V load hits block 0; 3 no K/V TMA
+  long long* trace;  // TRACE
+};
+
+#ifdef ROPESLR_WATCHDOG
+__device__ volatile unsigned long long* g_watchdog;  // host-mapped
+// Debug builds: a wait that spins for more than ~2 s records (once per
+// waiter) who waited on what into host-mapped memory, then keeps waiting.
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, uint64_t* bars0, int line) {
+  const long long t0 = clock64();
+  bool reported = false;
+  while (!mbar_try_wait(bar, parity)) {
+    if (!reported && clock64() - t0 > 4000000000LL) {
+      reported = true;
+      const unsigned long long slot = atomicAdd(const_cast<unsigned long long*>(&g_watchdog[0]), 1ull);
+      if (slot < 30) {
+        volatile unsigned long long* e = g_watchdog + 2 + slot * 4;
+        e[0] = blockIdx.x;
+        e[1] = threadIdx.x;
+        e[2] = static_cast<unsigned long long>(bar - bars0) | (static_cast<unsigned long long>(parity) << 32);
+        e[3] = line;
+        __threadfence_system();
+      }
+    }
+  }
+}
+#define mbar_wait(b, ph) mbar_wait_wd((b), (ph), bars, __LINE__)
+#endif
+
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x on the FMA pipe for a pair: x = n + f (n = rint(x), |f| <= 1/2),
+// 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, far below the
+// bf16 rounding of P), 2^n added to the exponent field.  x is clamped at -126.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(make_float2(0.05517125502228737f, 0.05517125502228737f), f,
+                        make_float2(0.2426103800535202f, 0.2426103800535202f));
+  q = __ffma2_rn(q, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+  q = __ffma2_rn(q, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+  // q + (n << 23) (ptxas fuses the shift-add into one LEA)
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+
+// Fraction of the exponentials computed on the FMA pipe: pairs i with
+// (i % POLY_DEN) < POLY_NUM (the rest go to the MUFU).
+#ifndef ROPESLR_RESCALE_THRESHOLD
+#define ROPESLR_RESCALE_THRESHOLD 8.f
+#endif
+#ifndef ROPESLR_PREFETCH
+#define ROPESLR_PREFETCH 0
+#endif
+#ifndef ROPESLR_POLY_NUM
+#define ROPESLR_POLY_NUM 1
+#endif
+#ifndef ROPESLR_POLY_DEN
+#define ROPESLR_POLY_DEN 4
+#endif
+
+// Softmax of one key block by one warpgroup, split by key columns: WG q
+// owns keys [q*QC, (q+1)*QC) of the tile, one query row per thread, its
+// quarter row in registers.  quarter_exp: P = 2^(s*scale - m) as bf16 pairs
+// written over S (P column c holds keys 2c, 2c+1); returns this quarter's sum.
+template <int QC>
+__device__ __forceinline__ float quarter_exp(const uint32_t (&sr)[QC], uint32_t tP, float scale_log2, float m_run) {
+  const float2 sc2 = make_float2(scale_log2, scale_log2);
+  const float2 nm2 = make_float2(-m_run, -m_run);
+  float2 sum2 = make_float2(0.f, 0.f);
+  uint32_t pk[QC / 2];
+#pragma unroll
+  for (int i = 0; i < QC / 2; ++i) {
+    const float2 x2 =
+        __ffma2_rn(make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1])), sc2, nm2);
+    float2 e2;
+    if ((i % ROPESLR_POLY_DEN) < ROPESLR_POLY_NUM) {
+      e2 = ex2_poly2(x2);  // FMA-pipe exp2 for a fraction of the scores: offloads the MUFU
+    } else {
+      e2.x = ex2_approx(x2.x);
+      e2.y = ex2_approx(x2.y);
+    }
+    sum2 = __fadd2_rn(sum2, e2);
+    __nv_bfloat162 hb = __floats2bfloat162_rn(e2.x, e2.y);
+    pk[i] = *reinterpret_cast<uint32_t*>(&hb);
+  }
+  if constexpr (QC == 32)
+    tmem_st16(tP, pk);
+  else
+    tmem_st8(tP, pk);
+  return sum2.x + sum2.y;
+}
+
+template <int BLK>
+__global__ void __launch_bounds__(kThreads, 1)
+    sparse_attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const Params p) {
+  using Lay = Layout<BLK>;
+  using Bx = Bars<BLK>;
+  constexpr int KST = Lay::KST, VST = Lay::VST;
+  constexpr int QC = BLK / 4;  // key columns per softmax warpgroup
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem_raw) & 1023u) __trap();
+  uint8_t* sQ = smem + Lay::OFF_Q;
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Lay::OFF_BAR + Lay::NBAR * 8);
+  float* xmax = reinterpret_cast<float*>(smem + Lay::OFF_XCH);         // [tile parity][row][4 wg]
+  float* xepi = reinterpret_cast<float*>(smem + Lay::OFF_XCH + 4096);  // [2][4 wg][row]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int i = 0; i < Bx::COUNT; ++i) {
+      uint32_t count = 1;
+      if (i >= Bx::P_FULL && i < Bx::P_FULL + NSB) count = 16;
+      mbar_init(&bars[i], count);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  if (BLK < M && warp >= 4 && warp < 8) {
+    // query rows [BLK, 128) of the MMA tile are never loaded: keep them zero
+    const int t = threadIdx.x - 128;
+    for (int half = 0; half < 2; ++half) {
+      uint4* z = reinterpret_cast<uint4*>(sQ + half * (M * 128) + BLK * 128);
+      for (int i = t; i < (M - BLK) * 128 / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp < 4) {
+    setmaxnreg_dec<kCtrlRegs>();
+    if (warp == 0 || warp == 3) {
+      if (elect_one_sync()) {
+        // ------------------------------------------- TMA producers
+        // warp 0: Q and K; warp 3: V (a V slot frees only after its PV, so
+        // it must not hold back the K prefetch).
+        const bool is_k = (warp == 0);
+        const int st = is_k ? KST : VST;
+        const uint64_t pol_kv = p.kv_evict_last ? policy_evict_last() : policy_evict_normal();
+        const uint64_t pol_q = policy_evict_first();
+        const CUtensorMap* map = is_k ? &tmK : &tmV;
+        uint8_t* ring = is_k ? sK : sV;
+        const int full = is_k ? Bx::K_FULL : Bx::V_FULL;
+        const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
+        uint32_t g = 0, uc = 0;
+        for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+          const int bh = static_cast<int>(u / p.nb);
+          const int n = p.cnt[u];
+          const int32_t* irow = p.idx + u * p.kmax;
+          if (is_k) {
+            const int qb = static_cast<int>(u % p.nb);
+            mbar_wait(&bars[Bx::Q_EMPTY], (uc & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * BLK * 128);
+            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * BLK, bh, pol_q);
+            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * BLK, bh, pol_q);
+          }
+          for (int j = 0; j < n; ++j, ++g) {
+            const int kb = p.debug_mode == 2 ? 0 : irow[j];
+            const int s = g % st;
+            const uint32_t ph = (g / st) & 1;
+            uint8_t* dst = ring + s * Lay::KV_BYTES;
+            mbar_wait(&bars[empty + s], ph ^ 1);
+            if (p.debug_mode == 3) {
+              mbar_arrive(&bars[full + s]);
+              continue;
+            }
+            mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
+            tma_load_3d_hint(dst, map, &bars[full + s], 0, kb * BLK, bh, pol_kv);
+            tma_load_3d_hint(dst + BLK * 128, map, &bars[full + s], 64, kb * BLK, bh, pol_kv);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ------------------------------------------------ MMA issuer
+      // Global tile t: S_b = Q K_t^T into TMEM columns [128b, +BLK) with
+      // b = t % 3 (SS-MMA); the softmax overwrites S_b with P_b (bf16 pairs,
+      // columns [128b, +BLK/2)); O += P_b V_t (TS-MMA, A from TMEM).  Issue
+      // order per unit: QK(0..2), then [PV(j), QK(j+3)]: QK(j+3) overwrites
+      // what PV(j) reads, and the tensor pipe executes a CTA's MMAs in issue
+      // order.  The next unit's first PV overwrites O: its P_FULL is arrived
+      // by the threads that read O in the epilogue, after that read.
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(M, BLK, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(M, D, false, true);
+      const uint64_t dQ = desc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = desc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
+      const bool leader = elect_one_sync();
+      auto issue_qk = [&](uint32_t t, bool last) {
+        const int s = t % KST;
+        const int b = t % NSB;
+        mbar_wait(&bars[Bx::K_FULL + s], (t / KST) & 1);
+        if (p.trace && blockIdx.x == 0 && leader && t < 64) p.trace[t * 8 + 3] = clock64();
+        tc_fence_after();
+        if (leader) {
+          const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t da = dQ + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
+            const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
+            mma_bf16_ss(tmem + b * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&bars[Bx::K_EMPTY + s]);
+          mma_commit(&bars[Bx::S_FULL + b]);
+          if (last) mma_commit(&bars[Bx::Q_EMPTY]);
+        }
+        __syncwarp();
+      };
+      uint32_t g = 0, uc = 0;
+      for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+        const int n = p.cnt[u];
+        mbar_wait(&bars[Bx::Q_FULL], uc & 1);
+        tc_fence_after();
+        for (int j = 0; j < n && j < NSB; ++j) issue_qk(g + j, j == n - 1);
+        for (int j = 0; j < n; ++j) {
+          const uint32_t t = g + j;
+          const int s = t % VST;
+          const int b = t % NSB;
+          mbar_wait(&bars[Bx::V_FULL + s], (t / VST) & 1);
+          if (p.trace && blockIdx.x == 0 && leader && t < 64) p.trace[t * 8 + 4] = clock64();
+          mbar_wait(&bars[Bx::P_FULL + b], (t / NSB) & 1);
+          if (p.trace && blockIdx.x == 0 && leader && t < 64) p.trace[t * 8 + 5] = clock64();
+          tc_fence_after();
+          if (leader) {
+            const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+#pragma unroll
+            for (int kk = 0; kk < BLK / 16; ++kk) {
+              const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
+              mma_bf16_ts(tmem + O_COL, tmem + b * 128 + kk * 8, db, idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&bars[Bx::V_EMPTY + s]);
+            mma_commit(&bars[Bx::PV_DONE + (t & 1)]);
+            if (j == n - 1) mma_commit(&bars[Bx::O_FULL]);
+          }
+          __syncwarp();
+          if (j + NSB < n) issue_qk(t + NSB, j + NSB == n - 1);
+        }
+        g += n;
+      }
+    }
+  } else {
+    setmaxnreg_inc<kSoftmaxRegs>();
+    // ------------------------------------ softmax warpgroups + epilogue
+    const int q = (warp - 4) >> 2;                 // softmax warpgroup 0..3 = key-column quarter
+    const int row = (threadIdx.x - 128) & 127;     // query row == TMEM lane
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t tOq = lane_addr + O_COL + q * (D / 4);
+    // rows >= BLK of the 128-row MMA tile are padding (block 64)
+    const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
+    uint32_t g = 0, uc = 0;
+    for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+      const int bh = static_cast<int>(u / p.nb);
+      const int qb = static_cast<int>(u % p.nb);
+      const int n = p.cnt[u];
+      const int32_t* irow = p.idx + u * p.kmax;
+      const int qrows = block_size(p.L, BLK, qb);
+      // Software-pipelined over tiles: the scores of tile t+1 are loaded and
+      // their quarter max published before the exponentials of tile t, so
+      // the per-tile barrier (the max exchange) finds every warpgroup there.
+      // load_max: wait for S(t), read this quarter (masked past the end of
+      // the sequence), publish its max into xmax[t & 1].
+      auto load_max = [&](uint32_t t, int j, uint32_t (&sr)[QC]) {
+        const int b = t % NSB;
+        const int kreal = block_size(p.L, BLK, irow[j]);
+        if (p.trace && blockIdx.x == 0 && row == 0 && q == 0 && t < 64) p.trace[t * 8 + 6] = clock64();
+        mbar_wait(&bars[Bx::S_FULL + b], (t / NSB) & 1);
+        if (p.trace && blockIdx.x == 0 && row == 0 && q == 0 && t < 64) p.trace[t * 8 + 7] = clock64();
+        tc_fence_after();
+        const uint32_t tSb = lane_addr + b * 128 + q * QC;
+        if constexpr (QC == 32)
+          tmem_ld32(tSb, sr);
+        else
+          tmem_ld16(tSb, sr);
+        tmem_wait_ld();
+        const int valid = kreal - q * QC;
+        if (valid < QC) {
+#pragma unroll
+          for (int c = 0; c < QC; ++c)
+            if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+        }
+        float mq[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < QC; c += 4) {
+          mq[0] = fmaxf(mq[0], fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])));
+          mq[1] = fmaxf(mq[1], fmaxf(__uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3])));
+        }
+        xmax[(t & 1) * 512 + row * 4 + q] = fmaxf(mq[0], mq[1]);
+      };
+      // after the tile barrier: every warpgroup has read its S quarter of
+      // tile t (wait::ld in load_max) and published its max
+      auto tile_max = [&](uint32_t t) {
+        const float4 m4 = *reinterpret_cast<const float4*>(xmax + (t & 1) * 512 + row * 4);
+        return fmaxf(fmaxf(m4.x, m4.y), fmaxf(m4.z, m4.w)) * p.scale_log2;
+      };
+      float m_run = -INFINITY, l_run = 0.f, alpha = 1.f;
+      uint32_t sr[QC];
+      if (rows_live) load_max(g, 0, sr);
+      named_bar_sync(1, 512);
+      if (rows_live) m_run = tile_max(g);
+      for (int j = 0; j < n; ++j) {
+        const uint32_t t = g + j;
+        const int b = t % NSB;
+        const bool has_next = j + 1 < n;
+        if (!rows_live) {
+          // block 64: TMEM lanes 64-127 hold the zero query rows of the MMA
+          // tile; their warps only keep the tile barriers and P_FULL counts
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[Bx::P_FULL + b]);
+          if (has_next) named_bar_sync(1, 512);
+          continue;
+        }
+        const bool trc = p.trace && blockIdx.x == 0 && row == 0 && t < 64 && q == 0;
+        if (trc) p.trace[t * 8 + 0] = clock64();
+        uint32_t sn[QC];
+        if (has_next) load_max(t + 1, j + 1, sn);
+        l_run += quarter_exp<QC>(sr, lane_addr + b * 128 + q * (QC / 2), p.scale_log2, m_run);
+        // tcgen05.ld / st are warp-collective: the rescale runs for the whole
+        // warp when any of its rows needs it (alpha == 1 for the others).
+        // O must hold PV(t-1) before it is rescaled.
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          mbar_wait(&bars[Bx::PV_DONE + ((t - 1) & 1)], ((t - 1) >> 1) & 1);
+          tc_fence_after();
+          uint32_t o[32];
+          tmem_ld32(tOq, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tOq, o);
+        }
+        if (trc) p.trace[t * 8 + 1] = clock64();
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[Bx::P_FULL + b]);
+        if (trc) p.trace[t * 8 + 2] = clock64();
+        alpha = 1.f;
+        if (has_next) {
+          named_bar_sync(1, 512);
+          // lazy rescale: the running max moves only when it grows by more
+          // than 2^8 (all four warpgroups take the same decision)
+          const float mx = tile_max(t + 1);
+          if (mx > m_run + ROPESLR_RESCALE_THRESHOLD) {
+            alpha = ex2_approx(m_run - mx);
+            l_run *= alpha;
+            m_run = mx;
+          }
+#pragma unroll
+          for (int c = 0; c < QC; ++c) sr[c] = sn[c];
+        }
+      }
+      g += n;
+      // ---------------------------------------------- fused epilogue
+      // O / l with l = the four quarters' sums; warpgroup q finalises output
+      // columns [32q, 32q + 32) of its row
+      mbar_wait(&bars[Bx::O_FULL], uc & 1);
+      tc_fence_after();
+      xepi[q * 128 + row] = l_run;
+      uint32_t ob[32];
+      tmem_ld32(tOq, ob);
+      named_bar_sync(3, 512);
+      const float l_all = (xepi[row] + xepi[128 + row]) + (xepi[256 + row] + xepi[384 + row]);
+      const float inv_l = 1.f / l_all;
+      tmem_wait_ld();
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float o = __uint_as_float(ob[i]) * inv_l;
+        ob[i] = __float_as_uint(o);
+        ss = fmaf(o, o, ss);
+      }
+      xepi[512 + q * 128 + row] = ss;
+      named_bar_sync(3, 512);
+      ss = (xepi[512 + row] + xepi[512 + 128 + row]) + (xepi[512 + 256 + row] + xepi[512 + 384 + row]);
+      const bool live = row < qrows;
+      if (!live) continue;
+      const int64_t flat = static_cast<int64_t>(qb) * BLK + row;
+      const int64_t tok = p.perm ? p.perm[flat] : flat;
+      const int b = bh / p.H, h = bh % p.H;
+      const float inv = 1.f / sqrtf(ss / static_cast<float>(D) + p.eps);
+      const int col0 = q * 32;
+      if (p.o_sparse) {
+        float* dst = p.o_sparse + (static_cast<int64_t>(bh) * p.L + tok) * D + col0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
+                                                            __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
+      }
+      if (p.out) {
+        const float gate = sigmoidf_stable(p.g_logit[static_cast<int64_t>(b) * p.L + tok] + p.b_g);
+        const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
+        const __nv_bfloat16* y = p.y_lr + orow;
+        __nv_bfloat16* dst = p.out + orow;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
+          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
+          uint4 uo;
+          __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 yv = __bfloat1622float2(hy[e]);
+            const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
+            const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
+            ho[e] = __floats2bfloat162_rn(o0, o1);
+          }
+          __stcs(reinterpret_cast<uint4*>(dst + i), uo);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// [BH, L, 128] bf16 viewed as a 3-D tensor, box [64 cols, rows, 1], 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, int64_t BH, int64_t L, int rows) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(BH)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(L) * D * 2};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BLK>
+static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
+                     cudaStream_t st) {
+  const int64_t BH = s->B * s->H;
+  CUtensorMap mq, mk, mv;
+  if (!make_map(&mq, q, BH, s->L, BLK) || !make_map(&mk, k, BH, s->L, BLK) || !make_map(&mv, v, BH, s->L, BLK))
+    return ROPESLR_ERR_LAUNCH;
+  auto kfn = sparse_attn_tc_kernel<BLK>;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Layout<BLK>::ALLOC) != cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
+  kfn<<<static_cast<unsigned>(grid), kThreads, Layout<BLK>::ALLOC, st>>>(mq, mk, mv, prm);
+#ifdef ROPESLR_WATCHDOG
+  {
+    static unsigned long long* hbuf = nullptr;
+    if (!hbuf) {
+      cudaHostAlloc(&hbuf, 4096, cudaHostAllocMapped);
+      void* dptr = nullptr;
+      cudaHostGetDevicePointer(&dptr, hbuf, 0);
+      cudaMemcpyToSymbol(g_watchdog, &dptr, sizeof(dptr));
+    }
+    // (the pointer is set before this launch on the first call: re-launch note below)
+    for (int i = 0; i < 60; ++i) {
+      if (cudaStreamQuery(st) == cudaSuccess) break;
+      usleep(100000);
+      if (hbuf[0]) {
+        usleep(500000);
+        fprintf(stderr, "WATCHDOG %llu waiters (S_FULL=%d P_FULL=%d PV_DONE=%d O_FULL=%d V_FULL=%d K_FULL=%d)\n",
+                hbuf[0], Bars<BLK>::S_FULL, Bars<BLK>::P_FULL, Bars<BLK>::PV_DONE, Bars<BLK>::O_FULL,
+                Bars<BLK>::V_FULL, Bars<BLK>::K_FULL);
+        for (unsigned long long k = 0; k < hbuf[0] && k < 30; ++k)
+          fprintf(stderr, "  block %llu thread %llu barrier %llu parity %llu line %llu\n", hbuf[2 + k * 4],
+                  hbuf[3 + k * 4], hbuf[4 + k * 4] & 0xffffffffull, hbuf[4 + k * 4] >> 32, hbuf[5 + k * 4]);
+        fflush(stderr);
+        break;
+      }
+    }
+  }
+#endif
+  if (prm.trace) {
+    long long h[64 * 8];
+    cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost);
+    FILE* f = fopen(getenv("ROPESLR_K2_TRACE"), "w");
+    // per tile of CTA 0: softmax start, after exp, P arrive, QK K_FULL seen,
+    // PV V_FULL seen, PV P_FULL seen, softmax S_FULL wait start, S_FULL seen
+    for (int i = 0; i < 64; ++i) {
+      fprintf(f, "%d", i);
+      for (int c = 0; c < 8; ++c) fprintf(f, " %lld", h[i * 8 + c] ? h[i * 8 + c] - h[0] : -1);
+      fprintf(f, "\n");
+    }
+    fclose(f);
+  }
+  return launch_status();
+}
+
+static bool tc_eligible(const ropeslr_shape* s) {
+  return s->dtype == ROPESLR_BF16 && s->d == D && (s->block == 64 || s->block == 128);
+}
+
+}  // namespace tc
+
+static int device_is_sm100() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0;
+}
+
+static int check_attn_args(const ropeslr_shape* s, const void* q, const void* k, const void* v, const int32_t* idx,
+                           int kmax, const int32_t* cnt) {
+  if (!s) return ROPESLR_ERR_NULL;
+  if (s->B < 1 || s->H < 1 || s->L < 1 || s->block < 1 || s->block > 128) return ROPESLR_ERR_SHAPE;
+  if (s->dtype != ROPESLR_F32 && s->dtype != ROPESLR_BF16) return ROPESLR_ERR_DTYPE;
+  if (!q || !k || !v || !idx || !cnt) return ROPESLR_ERR_NULL;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v)) return ROPESLR_ERR_ALIGN;
+  if (kmax < 1) return ROPESLR_ERR_SHAPE;
+  if (!device_is_sm100()) return ROPESLR_ERR_ARCH;
+  return ROPESLR_OK;
+}
+
+static int resolve_impl(const ropeslr_shape* s, int impl) {
+  if (impl == ROPESLR_IMPL_AUTO) return tc::tc_eligible(s) ? ROPESLR_IMPL_TCGEN05 : ROPESLR_IMPL_SIMT;
+  if (impl == ROPESLR_IMPL_TCGEN05 && !tc::tc_eligible(s)) return -1;
+  if (impl != ROPESLR_IMPL_SIMT && impl != ROPESLR_IMPL_TCGEN05) return -1;
+  return impl;
+}
+
+static int launch_tc_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
+                              const tc::Params& prm, cudaStream_t st) {
+  return s->block == 128 ? tc::launch_tc<128>(s, q, k, v, prm, st) : tc::launch_tc<64>(s, q, k, v, prm, st);
+}
+
+static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int kmax, const int32_t* cnt,
+                              const int32_t* perm) {
+  tc::Params prm{};
+  prm.idx = idx;
+  prm.cnt = cnt;
+  prm.kmax = kmax;
+  prm.nb = static_cast<int>(ceil_div(s->L, s->block));
+  prm.H = static_cast<int>(s->H);
+  prm.L = s->L;
+  prm.num_units = s->B * s->H * prm.nb;
+  prm.perm = perm;
+  prm.out_H = static_cast<int>(s->H);
+  prm.out_h0 = 0;
+  prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
+  // K/V tiles are re-read by many query blocks of the head: keep them in L2
+  // (evict_last) ahead of the streamed Q / y_lr / out; ROPESLR_KV_EVICT_LAST=0
+  // turns the hint off
+  const char* pol = getenv("ROPESLR_KV_EVICT_LAST");
+  prm.kv_evict_last = (pol != nullptr && pol[0] == '0') ? 0 : 1;
+  const char* dbg = getenv("ROPESLR_DEBUG_MODE");
+  prm.debug_mode = dbg ? atoi(dbg) : 0;
+  prm.trace = nullptr;
+  static long long* tbuf = nullptr;
+  if (getenv("ROPESLR_K2_TRACE")) {
+    if (!tbuf) cudaMalloc(&tbuf, 64 * 8 * 8);
+    cudaMemset(tbuf, 0, 64 * 8 * 8);
+    prm.trace = tbuf;
+  }
+  return prm;
+}
+
+}  // namespace ropeslr
+
+using namespace ropeslr;
+
+extern "C" int ropeslr_sparse_attention(const ropeslr_shape* s, const void* q, const void* k, const void* v,
+                                        const int32_t* idx, int32_t kmax, const int32_t* cnt, const int32_t* row_perm,
+                                        float* o_sparse, int32_t impl, void* stream) {
+  int st = check_attn_args(s, q, k, v, idx, kmax, cnt);
+  if (st) return st;
+  if (!o_sparse) return ROPESLR_ERR_NULL;
+  const int which = resolve_impl(s, impl);
+  if (which < 0) return ROPESLR_ERR_VALUE;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  if (which == ROPESLR_IMPL_SIMT)
+    return launch_sparse_attention_simt(s, q, k, v, idx, kmax, cnt, row_perm, o_sparse, cs);
+  tc::Params prm = base_params(s, idx, kmax, cnt, row_perm);
+  prm.o_sparse = o_sparse;
+  return launch_tc_dispatch(s, q, k, v, prm, cs);
+}
+
+extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t impl) {
+  if (!s) return 0;
+  const int which = resolve_impl(s, impl);
+  if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
+  return 0;
+}
+
+namespace ropeslr {
+// K2 + K4 (tcgen05 path only) writing heads [out_h0, out_h0 + H) of
+// out / y_lr rows that hold out_H heads: a head chunk of a wider forward
+// (forward_host.cu).
+int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k, const void* v, const int32_t* idx,
+                            int32_t kmax, const int32_t* cnt, const void* y_lr, const float* g_logit, float b_g,
+                            const float* rms_sparse, float eps, void* out, int out_H, int out_h0,
+                            cudaStream_t stream) {
+  int st = check_attn_args(s, q, k, v, idx, kmax, cnt);
+  if (st) return st;
+  if (!tc::tc_eligible(s)) return ROPESLR_ERR_VALUE;
+  if (out_h0 < 0 || out_h0 + s->H > out_H) return ROPESLR_ERR_SHAPE;
+  tc::Params prm = base_params(s, idx, kmax, cnt, nullptr);
+  prm.y_lr = static_cast<const __nv_bfloat16*>(y_lr);
+  prm.g_logit = g_logit;
+  prm.b_g = b_g;
+  prm.rms_sp = rms_sparse;
+  prm.eps = eps;
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.out_H = out_H;
+  prm.out_h0 = out_h0;
+  return launch_tc_dispatch(s, q, k, v, prm, stream);
+}
+bool attend_tc_eligible(const ropeslr_shape* s) { return tc::tc_eligible(s); }
+}  // namespace ropeslr
+
+extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const void* k, const void* v,
+                                    const int32_t* idx, int32_t kmax, const int32_t* cnt, const int32_t* row_perm,
+                                    const void* y_lr, const float* g_logit, float b_g, const float* rms_sparse,
+                                    float eps, void* out, float* o_sparse, int32_t impl, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  int st = check_attn_args(s, q, k, v, idx, kmax, cnt);
+  if (st) return st;
+  if (!y_lr || !g_logit || !rms_sparse || !out) return ROPESLR_ERR_NULL;
+  if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  const int which = resolve_impl(s, impl);
+  if (which < 0) return ROPESLR_ERR_VALUE;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  if (which == ROPESLR_IMPL_SIMT) {
+    float* osp = o_sparse;
+    if (osp == nullptr) {
+      if (!ws || ws_bytes < ropeslr_attend_workspace_bytes(s, impl)) return ROPESLR_ERR_WORKSPACE;
+      osp = static_cast<float*>(ws);
+    }
+    st = launch_sparse_attention_simt(s, q, k, v, idx, kmax, cnt, row_perm, osp, cs);
+    if (st) return st;
+    return ropeslr_fuse_output(s, osp, y_lr, g_logit, b_g, rms_sparse, eps, out, stream);
+  }
+  tc::Params prm = base_params(s, idx, kmax, cnt, row_perm);
+  prm.y_lr = static_cast<const __nv_bfloat16*>(y_lr);
+  prm.g_logit = g_logit;
+  prm.b_g = b_g;
+  prm.rms_sp = rms_sparse;
+  prm.eps = eps;
+  prm.out = static_cast<__nv_bfloat16*>(out);
+  prm.o_sparse = o_sparse;
+  return launch_tc_dispatch(s, q, k, v, prm, cs);
+}
