@@ -105,6 +105,7 @@ struct Params {
   int64_t L;
   int64_t num_units;
   const int32_t* perm;
+  const int32_t* order;  // nullable: unit schedule (schedule_units_kernel), position -> unit
   float scale_log2;
   const __nv_bfloat16* y_lr;
   const float* g_logit;
@@ -326,7 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int full = is_k ? Bx::K_FULL : Bx::V_FULL;
         const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
         uint32_t g = 0, uc = 0;
-        for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+        for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+          const int64_t u = p.order ? p.order[pos] : pos;
           const int bh = static_cast<int>(u / p.nb);
           const int n = p.cnt[u];
           const int32_t* irow = p.idx + u * p.kmax;
@@ -370,7 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
       const bool leader = elect_one_sync();
       uint32_t g = 0, uc = 0;
-      for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+      for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+        const int64_t u = p.order ? p.order[pos] : pos;
         const int n = p.cnt[u];
         mbar_wait(&bars[Bx::Q_FULL], uc & 1);
         tc_fence_after();
@@ -434,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // rows >= BLK of the 128-row MMA tile are padding (block 64)
     const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
     uint32_t g = 0, uc = 0;
-    for (int64_t u = blockIdx.x; u < p.num_units; u += gridDim.x, ++uc) {
+    for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+      const int64_t u = p.order ? p.order[pos] : pos;
       const int bh = static_cast<int>(u / p.nb);
       const int qb = static_cast<int>(u % p.nb);
       const int n = p.cnt[u];
@@ -587,6 +591,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Longest-first unit schedule for variable per-row block counts (the `keep`
+// rule, decomposition.py:105-111).  The persistent kernel's CTA c takes
+// positions c, c + G, c + 2G, ...; here, per head (so the CTAs in flight
+// still share one head's K/V in L2), the head's units are ranked by
+// descending selected-block count (ties by block id) and laid out over the
+// positions in snake order (full rounds of G alternate direction), which
+// balances the CTAs' total work.  One CTA per (batch, head).
+__global__ void schedule_units_kernel(const int32_t* __restrict__ cnt, int nb, int64_t num_units, int G,
+                                      int32_t* __restrict__ order) {
+  extern __shared__ int32_t sc[];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * nb;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) sc[i] = cnt[base + i];
+  __syncthreads();
+  const int64_t full_rounds = num_units / G;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    const int c = sc[i];
+    int rank = 0;
+    for (int j = 0; j < nb; ++j) {
+      const int cj = sc[j];
+      rank += (cj > c) | ((cj == c) & (j < i));
+    }
+    const int64_t pos = base + rank;
+    const int64_t r = pos / G;
+    int64_t slot = pos % G;
+    if ((r & 1) && r < full_rounds) slot = G - 1 - slot;
+    order[r * G + slot] = static_cast<int32_t>(base + i);
+  }
+}
+
 // ------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -714,6 +747,7 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.L = s->L;
   prm.num_units = s->B * s->H * prm.nb;
   prm.perm = perm;
+  prm.order = nullptr;
   prm.out_H = static_cast<int>(s->H);
   prm.out_h0 = 0;
   prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
@@ -754,11 +788,17 @@ extern "C" int ropeslr_sparse_attention(const ropeslr_shape* s, const void* q, c
   return launch_tc_dispatch(s, q, k, v, prm, cs);
 }
 
+namespace ropeslr {
+constexpr int kMaxScheduledBlocks = 8192;  // larger nb: identity order (the O(nb^2) ranking gets slow)
+static int64_t num_units_of(const ropeslr_shape* s) { return s->B * s->H * ceil_div(s->L, s->block); }
+}  // namespace ropeslr
+
 extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t impl) {
   if (!s) return 0;
   const int which = resolve_impl(s, impl);
   if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
-  return 0;
+  // tcgen05 path: the longest-first unit schedule
+  return static_cast<size_t>(num_units_of(s)) * sizeof(int32_t);
 }
 
 namespace ropeslr {
@@ -817,5 +857,18 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
   prm.eps = eps;
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.o_sparse = o_sparse;
+  // with a workspace: the longest-first unit schedule (pays off when the
+  // per-row block counts vary, i.e. the `keep` rule); without: identity
+  // (ROPESLR_SCHEDULE=0 turns it off, for A/B timing)
+  const char* sched_env = getenv("ROPESLR_SCHEDULE");
+  const bool sched = !(sched_env != nullptr && sched_env[0] == '0');
+  if (sched && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl) && prm.nb <= kMaxScheduledBlocks) {
+    const int64_t G = prm.num_units < num_sms() ? prm.num_units : num_sms();
+    int32_t* order = static_cast<int32_t*>(ws);
+    tc::schedule_units_kernel<<<static_cast<unsigned>(s->B * s->H), 512, prm.nb * sizeof(int32_t), cs>>>(
+        cnt, prm.nb, prm.num_units, static_cast<int>(G), order);
+    if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+    prm.order = order;
+  }
   return launch_tc_dispatch(s, q, k, v, prm, cs);
 }

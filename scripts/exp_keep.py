@@ -26,3 +26,12 @@ def run(st, label):
 for keep in (0.3, 0.6, 0.9):
     run(P.ForwardSettings(P.SparseSettings(64, keep=keep)), f"keep {keep}")
 run(P.ForwardSettings(P.SparseSettings.for_sparsity(64, L, 0.9)), "top-51 (90%)")
+# skewed rows (per query block scale of Q, as on real data): the longest-first
+# unit schedule against the plain persistent stride (ROPESLR_SCHEDULE=0)
+from test_gpu_parity import _skew_blocks
+q, k = _skew_blocks(q, k, 64, spread=float(os.environ.get("EXP_SPREAD", "2.0")))
+for keep in (0.5, 0.8):
+    for sched in ("1", "0"):
+        os.environ["ROPESLR_SCHEDULE"] = sched
+        run(P.ForwardSettings(P.SparseSettings(64, keep=keep)), f"skew keep {keep} sched {sched}")
+os.environ["ROPESLR_SCHEDULE"] = "1"

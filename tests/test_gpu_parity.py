@@ -226,3 +226,49 @@ def test_bad_inputs_raise_value_error():
         P.block_sparse_attention(q.half(), k.half(), v.half(), P.SparseSettings(64, topk=1))
     with pytest.raises(ValueError):
         P.forward(q, k, v, x[:, :, :-8], grid, params, P.ForwardSettings(P.SparseSettings(64, topk=1)), pe)
+
+
+def _skew_blocks(q, k, block, seed=1, strength=4.0, spread=2.0):
+    """Give the block scores structure, as real attention has: a shared
+    direction u, key block b shifted by strength*c_b*u (c_b ~ N(0, 1)) and
+    query block j by strength*a_j*u with a_j = exp(U(-spread, spread)).  Rows
+    with a large a_j get a peaked block softmax (few blocks under `keep`),
+    rows with a small one a flat softmax (many blocks)."""
+    B, H, L, d = q.shape
+    nb = -(-L // block)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    u = torch.randn(d, generator=g, dtype=torch.float64)
+    u = u / u.norm()
+    c = torch.randn((B, H, nb), generator=g, dtype=torch.float64)
+    a = torch.exp((torch.rand((B, H, nb), generator=g, dtype=torch.float64) * 2 - 1) * spread)
+
+    def shift(t, w):
+        w = w.repeat_interleave(block, dim=-1)[..., :L].to(t.device)
+        return (t.double() + strength * w[..., None] * u.to(t.device)).to(t.dtype)
+
+    return shift(q, a), shift(k, c)
+
+
+@pytest.mark.parametrize("block", [64, 128])
+def test_keep_schedule_bit_identical(block, monkeypatch):
+    """The longest-first unit schedule (schedule_units_kernel) only changes
+    which CTA runs a (head, query block): the output is bit-identical to the
+    unscheduled launch, every row is written, and the counts really vary."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((8, 16, 64), H=4)
+    q, k = _skew_blocks(q, k, block)
+    st = P.ForwardSettings(P.SparseSettings(block=block, keep=0.6))
+    prep = P.prepare(q, k, v, x, grid, params, st, pe)
+    cnt = prep.sel.cnt.cpu()
+    assert cnt.max() > 2 * cnt.min(), "skewed inputs should give uneven block counts"
+    B, H, L, d = q.shape
+    outs = []
+    for sched in ("1", "0"):
+        monkeypatch.setenv("ROPESLR_SCHEDULE", sched)
+        out = torch.full((B, L, H, d), float("nan"), dtype=q.dtype, device=q.device)
+        P.attend(prep, params, st, out=out)
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.isfinite(outs[0].float()).all()
+    assert torch.equal(outs[0], outs[1])
