@@ -208,10 +208,10 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
  * attention, normalisation by the softmax denominator, RMSNorm, gated
  * combination with y_lr and the bf16/f32 store of out.  o_sparse (nullable)
  * additionally receives the raw sparse-branch output.  Workspace: the
- * CUDA-core path keeps o_sparse there when o_sparse is NULL; the tcgen05 path
- * keeps a longest-first schedule of the (head, query block) units there
- * (balances the persistent CTAs when the `keep` rule gives rows different
- * block counts) and runs unscheduled when workspace is NULL. */
+ * CUDA-core path keeps o_sparse there when o_sparse is NULL; with the
+ * environment variable ROPESLR_SCHEDULE=1 the tcgen05 path keeps a
+ * longest-first schedule of the (head, query block) units there (for rows
+ * with different block counts under the `keep` rule). */
 int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
                          const int32_t* idx, int32_t kmax, const int32_t* cnt,
                          const int32_t* row_perm, const void* y_lr, const float* g_logit, float b_g,
