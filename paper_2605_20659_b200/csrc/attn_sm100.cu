@@ -106,6 +106,8 @@ struct Params {
   int64_t num_units;
   const int32_t* perm;
   const int32_t* order;  // nullable: unit schedule (schedule_units_kernel), position -> unit
+  const __nv_bfloat16* kmat;  // K itself (fixed-reference kernel: the probe key)
+  const float* kbnorm;        // [B*H, nb] max |k| per key block (fixed-reference kernel)
   float scale_log2;
   const __nv_bfloat16* y_lr;
   const float* g_logit;
@@ -591,6 +593,395 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2 + K4, fixed-reference variant ("v9").  Same warp roles, rings and
+// alternating softmax pairs as sparse_attn_tc_kernel, but every query row
+// uses ONE exponent reference m for the whole unit instead of a running max:
+//
+//   m_i = min(|q_i| * max_{k in selected blocks} |k| * scale,  s_i0 + 100)
+//
+// in the log2 domain, with s_i0 the (scaled) score of the first key of the
+// first selected block.  Cauchy-Schwarz makes the first term an upper bound
+// of every score of the row, so P = 2^(s - m) never exceeds 1 when it is the
+// minimum; the second term keeps the gap to a real score under 100 binary
+// orders, far inside the fp32 / bf16 exponent range, so no P underflows
+// that would have mattered (the exact softmax flushes terms 2^-126 below its
+// max as well).  Softmax is shift-invariant: O / l is the same quantity as
+// with the running max, only computed without the per-tile row max, the
+// max exchange between the two warpgroups of a pair, and the O rescale.
+// Hence one O accumulator shared by both pairs, and each warpgroup works
+// on its key half of a tile with no synchronisation with its partner: it
+// writes its P half over the first half of its own S columns, and the PV
+// MMA reads A from those two column ranges.
+//
+// The only other inputs: per-key-block maxima of |k| (key_block_norm_kernel,
+// in the attend workspace) and the K tensor for the probe key s_i0.
+//
+// TMEM columns: S_0 [0,128), S_1 [128,256), O [256,384).
+namespace fx {
+constexpr uint32_t O_COL = 256;
+template <int BLK>
+struct Layout {
+  using Base = tc::Layout<BLK>;
+  static constexpr int Q_BYTES = Base::Q_BYTES, KV_BYTES = Base::KV_BYTES;
+  static constexpr int KST = Base::KST, VST = Base::VST;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
+  // [2 unit parity][4 wg][128 rows] float2 (|q| partial, probe partial) 8 KiB,
+  // then l partials [4][128] 2 KiB, then RMS partials [4][128] 2 KiB
+  static constexpr int OFF_XQ = OFF_V + VST * KV_BYTES;
+  static constexpr int OFF_XL = OFF_XQ + 8192;
+  static constexpr int OFF_XS = OFF_XL + 2048;
+  static constexpr int OFF_BAR = OFF_XS + 2048;
+  static constexpr int NBAR = 2 * KST + 2 * VST + 12;
+  static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
+  static constexpr int ALLOC = BYTES;
+  static_assert(ALLOC <= 227 * 1024, "shared memory budget");
+};
+}  // namespace fx
+
+template <int BLK>
+__global__ void __launch_bounds__(kThreads, 1)
+    sparse_attn_fixed_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                             const __grid_constant__ CUtensorMap tmV, const Params p) {
+  using Lay = fx::Layout<BLK>;
+  using Bx = Bars<BLK>;
+  constexpr int KST = Lay::KST, VST = Lay::VST;
+  constexpr int HB = BLK / 2;   // keys per warpgroup of a pair
+  constexpr int KK = BLK / 16;  // K steps of the PV MMA
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem_raw) & 1023u) __trap();
+  uint8_t* sQ = smem + Lay::OFF_Q;
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Lay::OFF_BAR + Lay::NBAR * 8);
+  float2* xq = reinterpret_cast<float2*>(smem + Lay::OFF_XQ);
+  float* xl = reinterpret_cast<float*>(smem + Lay::OFF_XL);
+  float* xs = reinterpret_cast<float*>(smem + Lay::OFF_XS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int i = 0; i < Bx::COUNT; ++i) {
+      uint32_t count = 1;
+      if (i == Bx::P_FULL || i == Bx::P_FULL + 1) count = 256;
+      if (i == Bx::O_EMPTY) count = 512;
+      if (i == Bx::Q_EMPTY) count = 1 + 16;  // the last QK^T's commit + every softmax warp's read of Q
+      mbar_init(&bars[i], count);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  if (BLK < M && warp >= 4 && warp < 8) {
+    const int t = threadIdx.x - 128;
+    for (int half = 0; half < 2; ++half) {
+      uint4* z = reinterpret_cast<uint4*>(sQ + half * (M * 128) + BLK * 128);
+      for (int i = t; i < (M - BLK) * 128 / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp < 4) {
+    setmaxnreg_dec<kCtrlRegs>();
+    if (warp == 0 || warp == 3) {
+      if (elect_one_sync()) {
+        // ------------------------------------------- TMA producers (as v7)
+        const bool is_k = (warp == 0);
+        const int st = is_k ? KST : VST;
+        const uint64_t pol_kv = p.kv_evict_last ? policy_evict_last() : policy_evict_normal();
+        const uint64_t pol_q = policy_evict_first();
+        const CUtensorMap* map = is_k ? &tmK : &tmV;
+        uint8_t* ring = is_k ? sK : sV;
+        const int full = is_k ? Bx::K_FULL : Bx::V_FULL;
+        const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
+        uint32_t g = 0, uc = 0;
+        for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+          const int64_t u = p.order ? p.order[pos] : pos;
+          const int bh = static_cast<int>(u / p.nb);
+          const int n = p.cnt[u];
+          const int32_t* irow = p.idx + u * p.kmax;
+          if (is_k) {
+            const int qb = static_cast<int>(u % p.nb);
+            mbar_wait(&bars[Bx::Q_EMPTY], (uc & 1) ^ 1);
+            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * BLK * 128);
+            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * BLK, bh, pol_q);
+            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * BLK, bh, pol_q);
+          }
+          for (int j = 0; j < n; ++j, ++g) {
+            const int kb = irow[j];
+            const int s = g % st;
+            const uint32_t ph = (g / st) & 1;
+            uint8_t* dst = ring + s * Lay::KV_BYTES;
+            mbar_wait(&bars[empty + s], ph ^ 1);
+            mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
+            tma_load_3d_hint(dst, map, &bars[full + s], 0, kb * BLK, bh, pol_kv);
+            tma_load_3d_hint(dst + BLK * 128, map, &bars[full + s], 64, kb * BLK, bh, pol_kv);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ------------------------------------------------ MMA issuer
+      // As v7 (QK(0), QK(1), then [PV(j-2), QK(j)]), with one O: PV(t)
+      // accumulates into O whatever the pair; its A operand is the pair's
+      // two P halves, at columns [128p, +BLK/4) and [128p + BLK/2, +BLK/4).
+      constexpr uint32_t idesc_qk = idesc_bf16_f32(M, BLK, false, false);
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(M, D, false, true);
+      const uint64_t dQ = desc_sw128(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = desc_sw128(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
+      const bool leader = elect_one_sync();
+      uint32_t g = 0, uc = 0;
+      for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+        const int64_t u = p.order ? p.order[pos] : pos;
+        const int n = p.cnt[u];
+        mbar_wait(&bars[Bx::Q_FULL], uc & 1);
+        tc_fence_after();
+        for (int j = 0; j < n + 2; ++j) {
+          if (j >= 2) {
+            const uint32_t t = g + j - 2;
+            const int s = t % VST;
+            const int pr = t & 1;
+            mbar_wait(&bars[Bx::V_FULL + s], (t / VST) & 1);
+            mbar_wait(&bars[Bx::P_FULL + pr], (t >> 1) & 1);
+            if (j == 2) mbar_wait(&bars[Bx::O_EMPTY], (uc & 1) ^ 1);
+            tc_fence_after();
+            if (leader) {
+              const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < KK; ++kk) {
+                const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
+                const uint32_t a = tmem + pr * 128 + (kk / (KK / 2)) * HB + (kk % (KK / 2)) * 8;
+                mma_bf16_ts(tmem + fx::O_COL, a, db, idesc_pv, (j > 2 || kk > 0) ? 1u : 0u);
+              }
+              mma_commit(&bars[Bx::V_EMPTY + s]);
+            }
+            __syncwarp();
+          }
+          if (j < n) {
+            const uint32_t t = g + j;
+            const int s = t % KST;
+            const int pr = t & 1;
+            mbar_wait(&bars[Bx::K_FULL + s], (t / KST) & 1);
+            tc_fence_after();
+            if (leader) {
+              const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint64_t da = dQ + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
+                const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
+                mma_bf16_ss(tmem + pr * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+              }
+              mma_commit(&bars[Bx::K_EMPTY + s]);
+              mma_commit(&bars[Bx::S_FULL + pr]);
+              if (j == n - 1) mma_commit(&bars[Bx::Q_EMPTY]);
+            }
+            __syncwarp();
+          }
+        }
+        if (leader) mma_commit(&bars[Bx::O_FULL]);
+        __syncwarp();
+        g += n;
+      }
+    }
+  } else {
+    setmaxnreg_inc<kSoftmaxRegs>();
+    // ------------------------------------ softmax warpgroups + epilogue
+    const int q = (warp - 4) >> 2;                 // softmax warpgroup 0..3
+    const int pr = q >> 1;                         // pair: tiles t with t & 1 == pr
+    const int w = q & 1;                           // key half within the pair
+    const int row = (threadIdx.x - 128) & 127;     // query row == TMEM lane
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    const uint32_t tS = lane_addr + pr * 128 + w * HB;  // this warpgroup's S columns; its P over their first half
+    const uint32_t tOq = lane_addr + fx::O_COL + q * (D / 4);
+    const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
+    // this thread's quarter of its Q row in the 128B-swizzled tile: d in
+    // [32q, 32q + 32) = 16-byte chunks 4(q&1) .. 4(q&1)+3 of half q>>1
+    const uint8_t* qrow = sQ + (q >> 1) * (M * 128) + row * 128;
+    uint32_t g = 0, uc = 0;
+    for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+      const int64_t u = p.order ? p.order[pos] : pos;
+      const int bh = static_cast<int>(u / p.nb);
+      const int qb = static_cast<int>(u % p.nb);
+      const int n = p.cnt[u];
+      const int32_t* irow = p.idx + u * p.kmax;
+      const int qrows = block_size(p.L, BLK, qb);
+      // ---- the unit's exponent reference m (see the header)
+      mbar_wait(&bars[Bx::Q_FULL], uc & 1);
+      {
+        const __nv_bfloat16* krow = p.kmat + (static_cast<int64_t>(bh) * p.L + static_cast<int64_t>(irow[0]) * BLK) *
+                                                 D + q * 32;
+        float ss = 0.f, dot = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int chunk = ((q & 1) * 4 + c) ^ (row & 7);
+          const uint4 qv = *reinterpret_cast<const uint4*>(qrow + chunk * 16);
+          const uint4 kv = __ldg(reinterpret_cast<const uint4*>(krow + c * 8));
+          const __nv_bfloat162* qh = reinterpret_cast<const __nv_bfloat162*>(&qv);
+          const __nv_bfloat162* kh = reinterpret_cast<const __nv_bfloat162*>(&kv);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 a = __bfloat1622float2(qh[e]), b = __bfloat1622float2(kh[e]);
+            ss = fmaf(a.x, a.x, fmaf(a.y, a.y, ss));
+            dot = fmaf(a.x, b.x, fmaf(a.y, b.y, dot));
+          }
+        }
+        xq[((uc & 1) * 4 + q) * 128 + row] = make_float2(ss, dot);
+      }
+      float kmax = 0.f;
+      for (int j = lane; j < n; j += 32) kmax = fmaxf(kmax, __ldg(p.kbnorm + static_cast<int64_t>(bh) * p.nb + irow[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+      named_bar_sync(2, 512);
+      // every warp has read its quarter of Q: the next unit's Q may land
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[Bx::Q_EMPTY]);
+      float m_ref;
+      {
+        const float2* xr = xq + (uc & 1) * 512 + row;
+        const float2 a0 = xr[0], a1 = xr[128], a2 = xr[256], a3 = xr[384];
+        const float qn = sqrtf((a0.x + a1.x) + (a2.x + a3.x));
+        const float probe = ((a0.y + a1.y) + (a2.y + a3.y)) * p.scale_log2;
+        m_ref = fminf(qn * kmax * p.scale_log2, probe + 100.f);
+      }
+      float l_run = 0.f;
+      const int j0 = (pr - static_cast<int>(g & 1)) & 1;
+      for (int j = j0; j < n; j += 2) {
+        const uint32_t t = g + j;
+        mbar_wait(&bars[Bx::S_FULL + pr], (t >> 1) & 1);
+        tc_fence_after();
+        if (rows_live) {
+          const int kreal = block_size(p.L, BLK, irow[j]);
+          uint32_t sr[HB];
+#pragma unroll
+          for (int c = 0; c < HB / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
+          tmem_wait_ld();
+          const int valid = kreal - w * HB;
+          if (valid < HB) {
+#pragma unroll
+            for (int c = 0; c < HB; ++c)
+              if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+          }
+          l_run += half_exp<BLK>(sr, tS, p.scale_log2, m_ref);
+          tmem_wait_st();
+        }
+        tc_fence_before();
+        mbar_arrive(&bars[Bx::P_FULL + pr]);
+      }
+      g += n;
+      // ---------------------------------------------- fused epilogue
+      // l = the four warpgroups' partial sums; warpgroup q finalises output
+      // columns [32q, 32q + 32) of its row
+      mbar_wait(&bars[Bx::O_FULL], uc & 1);
+      tc_fence_after();
+      uint32_t ob[32];
+      tmem_ld32(tOq, ob);
+      xl[q * 128 + row] = l_run;
+      named_bar_sync(3, 512);
+      const float inv_l = 1.f / ((xl[row] + xl[128 + row]) + (xl[256 + row] + xl[384 + row]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars[Bx::O_EMPTY]);
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float o = __uint_as_float(ob[i]) * inv_l;
+        ob[i] = __float_as_uint(o);
+        ss = fmaf(o, o, ss);
+      }
+      xs[q * 128 + row] = ss;
+      named_bar_sync(3, 512);
+      ss = (xs[row] + xs[128 + row]) + (xs[256 + row] + xs[384 + row]);
+      const bool live = row < qrows;
+      if (!live) continue;
+      const int64_t flat = static_cast<int64_t>(qb) * BLK + row;
+      const int64_t tok = p.perm ? p.perm[flat] : flat;
+      const int b = bh / p.H, h = bh % p.H;
+      const float inv = 1.f / sqrtf(ss / static_cast<float>(D) + p.eps);
+      const int col0 = q * 32;
+      if (p.o_sparse) {
+        float* dst = p.o_sparse + (static_cast<int64_t>(bh) * p.L + tok) * D + col0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
+                                                            __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
+      }
+      if (p.out) {
+        const float gate = sigmoidf_stable(p.g_logit[static_cast<int64_t>(b) * p.L + tok] + p.b_g);
+        const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
+        const __nv_bfloat16* y = p.y_lr + orow;
+        __nv_bfloat16* dst = p.out + orow;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
+          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
+          uint4 uo;
+          __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 yv = __bfloat1622float2(hy[e]);
+            const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
+            const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
+            ho[e] = __floats2bfloat162_rn(o0, o1);
+          }
+          __stcs(reinterpret_cast<uint4*>(dst + i), uo);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Per key block: the largest |k| over its real rows (fp32, rounded up by a
+// relative 2^-20 so the Cauchy-Schwarz product stays an upper bound).  One
+// warp per block, 16 lanes per row pair.
+__global__ void key_block_norm_kernel(const __nv_bfloat16* __restrict__ k, int64_t L, int block, int nb, int64_t BH,
+                                      float* __restrict__ out) {
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= BH * nb) return;
+  const int64_t bh = wid / nb;
+  const int b = static_cast<int>(wid % nb);
+  const int rows = block_size(L, block, b);
+  const __nv_bfloat16* base = k + (bh * L + static_cast<int64_t>(b) * block) * D;
+  float best = 0.f;
+  // lanes 0-15 take even rows, 16-31 odd rows; each lane 8 of the 128 columns
+  for (int r = lane >> 4; r < rows; r += 2) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + static_cast<int64_t>(r) * D) + (lane & 15));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float ss = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    best = fmaxf(best, ss);
+  }
+  best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, 16));
+  if (lane == 0) out[wid] = sqrtf(best) * (1.f + 1.0f / (1 << 20));
+}
+
 // Longest-first unit schedule for variable per-row block counts (the `keep`
 // rule, decomposition.py:105-111).  The persistent kernel's CTA c takes
 // positions c, c + G, c + 2G, ...; here, per head (so the CTAs in flight
@@ -697,6 +1088,30 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
   return launch_status();
 }
 
+// The fixed-reference kernel: key-block norms first (into kbnorm), then K2.
+template <int BLK>
+static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
+                        float* kbnorm, cudaStream_t st) {
+  const int64_t BH = s->B * s->H;
+  {
+    const int64_t warps = BH * prm.nb;
+    key_block_norm_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(k), s->L, BLK, prm.nb, BH, kbnorm);
+    if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  }
+  prm.kmat = static_cast<const __nv_bfloat16*>(k);
+  prm.kbnorm = kbnorm;
+  CUtensorMap mq, mk, mv;
+  if (!make_map(&mq, q, BH, s->L, BLK) || !make_map(&mk, k, BH, s->L, BLK) || !make_map(&mv, v, BH, s->L, BLK))
+    return ROPESLR_ERR_LAUNCH;
+  auto kfn = sparse_attn_fixed_kernel<BLK>;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, fx::Layout<BLK>::ALLOC) != cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
+  kfn<<<static_cast<unsigned>(grid), kThreads, fx::Layout<BLK>::ALLOC, st>>>(mq, mk, mv, prm);
+  return launch_status();
+}
+
 static bool tc_eligible(const ropeslr_shape* s) {
   return s->dtype == ROPESLR_BF16 && s->d == D && (s->block == 64 || s->block == 128);
 }
@@ -731,6 +1146,19 @@ static int resolve_impl(const ropeslr_shape* s, int impl) {
   return impl;
 }
 
+static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
+                                 const tc::Params& prm, float* kbnorm, cudaStream_t st) {
+  return s->block == 128 ? tc::launch_fixed<128>(s, q, k, v, prm, kbnorm, st)
+                         : tc::launch_fixed<64>(s, q, k, v, prm, kbnorm, st);
+}
+
+// K2 flavour for the tcgen05 path: the fixed-reference kernel unless
+// ROPESLR_K2=online asks for the running-max (v7) kernel.
+static bool use_fixed_reference() {
+  const char* e = getenv("ROPESLR_K2");
+  return !(e != nullptr && e[0] == 'o');
+}
+
 static int launch_tc_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                               const tc::Params& prm, cudaStream_t st) {
   return s->block == 128 ? tc::launch_tc<128>(s, q, k, v, prm, st) : tc::launch_tc<64>(s, q, k, v, prm, st);
@@ -748,6 +1176,8 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.num_units = s->B * s->H * prm.nb;
   prm.perm = perm;
   prm.order = nullptr;
+  prm.kmat = nullptr;
+  prm.kbnorm = nullptr;
   prm.out_H = static_cast<int>(s->H);
   prm.out_h0 = 0;
   prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
@@ -797,8 +1227,8 @@ extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t
   if (!s) return 0;
   const int which = resolve_impl(s, impl);
   if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
-  // tcgen05 path: the longest-first unit schedule
-  return static_cast<size_t>(num_units_of(s)) * sizeof(int32_t);
+  // tcgen05 path: the longest-first unit schedule, then the key-block norms
+  return 2 * static_cast<size_t>(num_units_of(s)) * sizeof(int32_t);
 }
 
 namespace ropeslr {
@@ -872,5 +1302,7 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
     if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
     prm.order = order;
   }
+  if (use_fixed_reference() && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl))
+    return launch_fixed_dispatch(s, q, k, v, prm, static_cast<float*>(ws) + num_units_of(s), cs);
   return launch_tc_dispatch(s, q, k, v, prm, cs);
 }

@@ -56,7 +56,7 @@ def test_host_functions():
     shp = _lib.Shape(1, 24, 118800, 128, 128, _lib.BF16)
     ws = lib.ropeslr_select_workspace_bytes(ctypes.byref(shp))
     assert ws >= (2 * 24 * 929 * 128 + 24 * 929 * 929) * 8
-    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 0) == 24 * 929 * 4  # tcgen05: the unit schedule
+    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 0) == 2 * 24 * 929 * 4  # tcgen05: unit schedule + key-block norms
     assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 1) == 24 * 118800 * 128 * 4
 
 
