@@ -43,8 +43,9 @@ CONFIGS = {
 }
 METRIC = "RoPeSLR attn fwd ms & effective TFLOPS/GPU, L=118800, 90% sparse, 1/2/4/8 B200"
 # our launches per step: pool_blocks, block_scores, select_topk_warp (K1);
-# lowrank_fold, lowrank_tc, gate_reduce (K3); sparse_attn_tc (K2+K4)
-KERNELS_PER_STEP = 7
+# lowrank_fold, lowrank_umma, gate_sum (K3); key_block_norm, sparse_attn_fixed
+# (K2+K4)
+KERNELS_PER_STEP = 8
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -386,7 +387,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "note": "rank 0: read un-rotated Q,K + write rotated Q,K (pooled means ride along)"},
         "attended_pairs": attended_total,
         "sparsity": 1.0 - attended_total / (H * float(L) ** 2),
-        "roofline": {"bound": "tensor", "kernel": "sparse_attn_tc_kernel (K2+K4 fused)",
+        "roofline": {"bound": "tensor", "kernel": "sparse_attn_fixed_kernel (K2+K4 fused)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": peaks["source"] + ", bf16 dense sustained (kernel timed inside a long step)",
                      "peak_burst": peaks.get("bf16_tflops"), "frac_of_burst": achieved / peaks.get("bf16_tflops", 1),

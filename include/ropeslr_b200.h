@@ -208,10 +208,12 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
  * attention, normalisation by the softmax denominator, RMSNorm, gated
  * combination with y_lr and the bf16/f32 store of out.  o_sparse (nullable)
  * additionally receives the raw sparse-branch output.  Workspace: the
- * CUDA-core path keeps o_sparse there when o_sparse is NULL; with the
- * environment variable ROPESLR_SCHEDULE=1 the tcgen05 path keeps a
- * longest-first schedule of the (head, query block) units there (for rows
- * with different block counts under the `keep` rule). */
+ * CUDA-core path keeps o_sparse there when o_sparse is NULL.  The tcgen05
+ * path keeps the per-key-block maxima of |k| there that its fixed exponent
+ * reference needs (without a workspace it runs the running-max kernel), and,
+ * with the environment variable ROPESLR_SCHEDULE=1, a longest-first schedule
+ * of the (head, query block) units (for rows with different block counts
+ * under the `keep` rule). */
 int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
                          const int32_t* idx, int32_t kmax, const int32_t* cnt,
                          const int32_t* row_perm, const void* y_lr, const float* g_logit, float b_g,

@@ -1,6 +1,12 @@
 // K2 + K4: block-sparse softmax attention on the 5th-generation tensor cores
 // with the fused RoPeSLR epilogue (mechanism.py:321-326 and 437-451).
 //
+// Two kernels share the warp layout below: sparse_attn_tc_kernel keeps a
+// running row max (online softmax, two O accumulators); the default,
+// sparse_attn_fixed_kernel (further down), fixes each row's exponent
+// reference per unit from a Cauchy-Schwarz bound and needs neither the max
+// nor the rescale.  ROPESLR_K2=online selects the first.
+//
 // One persistent CTA per SM walks work units (bh, query block) in head-major
 // order, so the ~150 CTAs in flight read the K/V blocks of one or two heads
 // and those stay resident in the 126 MB L2.  Per unit:
@@ -1237,8 +1243,8 @@ namespace ropeslr {
 // (forward_host.cu).
 int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k, const void* v, const int32_t* idx,
                             int32_t kmax, const int32_t* cnt, const void* y_lr, const float* g_logit, float b_g,
-                            const float* rms_sparse, float eps, void* out, int out_H, int out_h0,
-                            cudaStream_t stream) {
+                            const float* rms_sparse, float eps, void* out, int out_H, int out_h0, void* ws,
+                            size_t ws_bytes, cudaStream_t stream) {
   int st = check_attn_args(s, q, k, v, idx, kmax, cnt);
   if (st) return st;
   if (!tc::tc_eligible(s)) return ROPESLR_ERR_VALUE;
@@ -1252,6 +1258,8 @@ int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.out_H = out_H;
   prm.out_h0 = out_h0;
+  if (use_fixed_reference() && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, ROPESLR_IMPL_TCGEN05))
+    return launch_fixed_dispatch(s, q, k, v, prm, static_cast<float*>(ws) + num_units_of(s), stream);
   return launch_tc_dispatch(s, q, k, v, prm, stream);
 }
 bool attend_tc_eligible(const ropeslr_shape* s) { return tc::tc_eligible(s); }

@@ -26,8 +26,8 @@ namespace ropeslr {
 
 int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k, const void* v, const int32_t* idx,
                             int32_t kmax, const int32_t* cnt, const void* y_lr, const float* g_logit, float b_g,
-                            const float* rms_sparse, float eps, void* out, int out_H, int out_h0,
-                            cudaStream_t stream);
+                            const float* rms_sparse, float eps, void* out, int out_H, int out_h0, void* ws,
+                            size_t ws_bytes, cudaStream_t stream);
 bool attend_tc_eligible(const ropeslr_shape* s);
 
 namespace {
@@ -117,7 +117,9 @@ Plan make_plan(const ropeslr_host_forward* a) {
   p.idx = take(static_cast<size_t>(s.B * p.Hc * p.nb * p.kmax) * 4);
   p.cnt = take(static_cast<size_t>(s.B * p.Hc * p.nb) * 4);
   p.att = take(static_cast<size_t>(p.nchunks) * s.B * p.Hc * 8);
-  p.osp_bytes = p.nchunks == 1 ? ropeslr_attend_workspace_bytes(&sh, ROPESLR_IMPL_AUTO) : 0;
+  // K2 scratch (the CUDA-core path's o_sparse, or the tcgen05 path's unit
+  // schedule and key-block norms); chunks run in stream order and share it
+  p.osp_bytes = ropeslr_attend_workspace_bytes(p.nchunks == 1 ? &sh : &sc, ROPESLR_IMPL_AUTO);
   p.osp = take(p.osp_bytes);
   const size_t D = static_cast<size_t>(a->tok.d_model);
   p.w_a = take(static_cast<size_t>(s.H * s.d * a->rank) * 4);
@@ -309,7 +311,7 @@ extern "C" int ropeslr_forward_host(const ropeslr_host_forward* a, void* workspa
     } else {
       ROPESLR_TRY(attend_fused_tc_strided(&sc, q, k, v, idx, static_cast<int32_t>(p.kmax), cnt, y_lr, g_logit,
                                           a->b_g, rms_sp, a->eps, dout, static_cast<int>(H), static_cast<int>(h0),
-                                          S));
+                                          base + p.osp, p.osp_bytes, S));
     }
     cudaEvent_t ev_done = ss.event();
     if (!ev_done) return ROPESLR_ERR_LAUNCH;
