@@ -626,6 +626,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // TMEM columns: S_0 [0,128), S_1 [128,256), O [256,384).
 namespace fx {
 constexpr uint32_t O_COL = 256;
+constexpr uint32_t Q_COL = 384;  // Q_0 [384, 448), Q_1 [448, 512): the A operand of QK^T, per unit parity
+template <int BLK>
+struct FBars : Bars<BLK> {
+  static constexpr int QT_FULL = Bars<BLK>::COUNT;  // this unit's Q is in TMEM (16 softmax warps)
+  static constexpr int COUNT = QT_FULL + 1;
+};
 template <int BLK>
 struct Layout {
   using Base = tc::Layout<BLK>;
@@ -652,7 +658,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_fixed_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                              const __grid_constant__ CUtensorMap tmV, const Params p) {
   using Lay = fx::Layout<BLK>;
-  using Bx = Bars<BLK>;
+  using Bx = fx::FBars<BLK>;
+  static_assert(Bx::COUNT <= Lay::NBAR, "barrier count");
   constexpr int KST = Lay::KST, VST = Lay::VST;
   constexpr int HB = BLK / 2;   // keys per warpgroup of a pair
   constexpr int KK = BLK / 16;  // K steps of the PV MMA
@@ -679,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t count = 1;
       if (i == Bx::P_FULL || i == Bx::P_FULL + 1) count = 256;
       if (i == Bx::O_EMPTY) count = 512;
-      if (i == Bx::Q_EMPTY) count = 1 + 16;  // the last QK^T's commit + every softmax warp's read of Q
+      if (i == Bx::Q_EMPTY || i == Bx::QT_FULL) count = 16;  // every softmax warp: Q read / stored to TMEM
       mbar_init(&bars[i], count);
     }
     fence_mbar_init();
@@ -746,7 +753,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       // two P halves, at columns [128p, +BLK/4) and [128p + BLK/2, +BLK/4).
       constexpr uint32_t idesc_qk = idesc_bf16_f32(M, BLK, false, false);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(M, D, false, true);
-      const uint64_t dQ = desc_sw128(smem_u32(sQ), 16, 1024);
       const uint64_t dK0 = desc_sw128(smem_u32(sK), 16, 1024);
       const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
       const bool leader = elect_one_sync();
@@ -754,7 +760,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
         const int64_t u = p.order ? p.order[pos] : pos;
         const int n = p.cnt[u];
-        mbar_wait(&bars[Bx::Q_FULL], uc & 1);
+        const uint32_t tQ = tmem + fx::Q_COL + (uc & 1) * (D / 2);
+        mbar_wait(&bars[Bx::QT_FULL], uc & 1);
         tc_fence_after();
         for (int j = 0; j < n + 2; ++j) {
           if (j >= 2) {
@@ -787,13 +794,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
 #pragma unroll
               for (int kk = 0; kk < D / 16; ++kk) {
-                const uint64_t da = dQ + static_cast<uint64_t>(((kk >> 2) * (M * 128) + (kk & 3) * 32) >> 4);
+                // A = Q from TMEM (TS-MMA): only K is read from shared memory
                 const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
-                mma_bf16_ss(tmem + pr * 128, da, db, idesc_qk, kk > 0 ? 1u : 0u);
+                mma_bf16_ts(tmem + pr * 128, tQ + kk * 8, db, idesc_qk, kk > 0 ? 1u : 0u);
               }
               mma_commit(&bars[Bx::K_EMPTY + s]);
               mma_commit(&bars[Bx::S_FULL + pr]);
-              if (j == n - 1) mma_commit(&bars[Bx::Q_EMPTY]);
             }
             __syncwarp();
           }
@@ -817,7 +823,56 @@ __global__ void __launch_bounds__(kThreads, 1)
     // this thread's quarter of its Q row in the 128B-swizzled tile: d in
     // [32q, 32q + 32) = 16-byte chunks 4(q&1) .. 4(q&1)+3 of half q>>1
     const uint8_t* qrow = sQ + (q >> 1) * (M * 128) + row * 128;
+    // prep(unit at position pos, parity uc): wait for its Q tile, store this
+    // thread's quarter of its Q row into TMEM buffer uc & 1 (the A operand of
+    // QK^T: column c holds d = 2c, 2c+1), publish the partial |q|^2 and
+    // probe dot product, free the shared-memory tile, return the unit's
+    // max |k| over its selected blocks (warp-uniform)
+    auto prep = [&](int64_t pos, uint32_t uc) -> float {
+      const int64_t u = p.order ? p.order[pos] : pos;
+      const int bh = static_cast<int>(u / p.nb);
+      const int n = p.cnt[u];
+      const int32_t* irow = p.idx + u * p.kmax;
+      mbar_wait(&bars[Bx::Q_FULL], uc & 1);
+      const __nv_bfloat16* krow =
+          p.kmat + (static_cast<int64_t>(bh) * p.L + static_cast<int64_t>(irow[0]) * BLK) * D + q * 32;
+      float ss = 0.f, dot = 0.f;
+      uint32_t qw[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int chunk = ((q & 1) * 4 + c) ^ (row & 7);
+        const uint4 qv = *reinterpret_cast<const uint4*>(qrow + chunk * 16);
+        const uint4 kv = __ldg(reinterpret_cast<const uint4*>(krow + c * 8));
+        qw[4 * c] = qv.x;
+        qw[4 * c + 1] = qv.y;
+        qw[4 * c + 2] = qv.z;
+        qw[4 * c + 3] = qv.w;
+        const __nv_bfloat162* qh = reinterpret_cast<const __nv_bfloat162*>(&qv);
+        const __nv_bfloat162* kh = reinterpret_cast<const __nv_bfloat162*>(&kv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 a = __bfloat1622float2(qh[e]), b = __bfloat1622float2(kh[e]);
+          ss = fmaf(a.x, a.x, fmaf(a.y, a.y, ss));
+          dot = fmaf(a.x, b.x, fmaf(a.y, b.y, dot));
+        }
+      }
+      tmem_st16(lane_addr + fx::Q_COL + (uc & 1) * (D / 2) + q * 16, qw);
+      xq[((uc & 1) * 4 + q) * 128 + row] = make_float2(ss, dot);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bars[Bx::QT_FULL]);
+        mbar_arrive(&bars[Bx::Q_EMPTY]);
+      }
+      float km = 0.f;
+      for (int j = lane; j < n; j += 32) km = fmaxf(km, __ldg(p.kbnorm + static_cast<int64_t>(bh) * p.nb + irow[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) km = fmaxf(km, __shfl_xor_sync(0xffffffffu, km, o));
+      return km;
+    };
     uint32_t g = 0, uc = 0;
+    float kmax = blockIdx.x < p.num_units ? prep(blockIdx.x, 0) : 0.f;
     for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
       const int64_t u = p.order ? p.order[pos] : pos;
       const int bh = static_cast<int>(u / p.nb);
@@ -826,35 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t* irow = p.idx + u * p.kmax;
       const int qrows = block_size(p.L, BLK, qb);
       // ---- the unit's exponent reference m (see the header)
-      mbar_wait(&bars[Bx::Q_FULL], uc & 1);
-      {
-        const __nv_bfloat16* krow = p.kmat + (static_cast<int64_t>(bh) * p.L + static_cast<int64_t>(irow[0]) * BLK) *
-                                                 D + q * 32;
-        float ss = 0.f, dot = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int chunk = ((q & 1) * 4 + c) ^ (row & 7);
-          const uint4 qv = *reinterpret_cast<const uint4*>(qrow + chunk * 16);
-          const uint4 kv = __ldg(reinterpret_cast<const uint4*>(krow + c * 8));
-          const __nv_bfloat162* qh = reinterpret_cast<const __nv_bfloat162*>(&qv);
-          const __nv_bfloat162* kh = reinterpret_cast<const __nv_bfloat162*>(&kv);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 a = __bfloat1622float2(qh[e]), b = __bfloat1622float2(kh[e]);
-            ss = fmaf(a.x, a.x, fmaf(a.y, a.y, ss));
-            dot = fmaf(a.x, b.x, fmaf(a.y, b.y, dot));
-          }
-        }
-        xq[((uc & 1) * 4 + q) * 128 + row] = make_float2(ss, dot);
-      }
-      float kmax = 0.f;
-      for (int j = lane; j < n; j += 32) kmax = fmaxf(kmax, __ldg(p.kbnorm + static_cast<int64_t>(bh) * p.nb + irow[j]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) kmax = fmaxf(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
       named_bar_sync(2, 512);
-      // every warp has read its quarter of Q: the next unit's Q may land
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[Bx::Q_EMPTY]);
       float m_ref;
       {
         const float2* xr = xq + (uc & 1) * 512 + row;
@@ -888,6 +915,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&bars[Bx::P_FULL + pr]);
       }
       g += n;
+      // the next unit's Q goes to the other TMEM buffer now, so its first
+      // QK^T overlaps this unit's epilogue
+      if (pos + gridDim.x < p.num_units) kmax = prep(pos + gridDim.x, uc + 1);
       // ---------------------------------------------- fused epilogue
       // l = the four warpgroups' partial sums; warpgroup q finalises output
       // columns [32q, 32q + 32) of its row
