@@ -114,6 +114,14 @@ struct Params {
   const int32_t* order;  // nullable: unit schedule (schedule_units_kernel), position -> unit
   const __nv_bfloat16* kmat;  // K itself (fixed-reference kernel: the probe key)
   const float* kbnorm;        // [B*H, nb] max |k| per key block (fixed-reference kernel)
+  // fixed-reference kernel: units whose exponent reference failed (see
+  // sparse_attn_fixed_kernel) are appended to flag_list once (unit_flag
+  // dedupes), and the running-max kernel recomputes them, reading its unit
+  // count from num_units_dev
+  int* unit_flag;
+  int* flag_count;
+  int32_t* flag_list;
+  const int* num_units_dev;
   float scale_log2;
   const __nv_bfloat16* y_lr;
   const float* g_logit;
@@ -318,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  const int64_t nunits = p.num_units_dev ? static_cast<int64_t>(*p.num_units_dev) : p.num_units;
 
   if (warp < 4) {
     setmaxnreg_dec<kCtrlRegs>();
@@ -335,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int full = is_k ? Bx::K_FULL : Bx::V_FULL;
         const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
         uint32_t g = 0, uc = 0;
-        for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+        for (int64_t pos = blockIdx.x; pos < nunits; pos += gridDim.x, ++uc) {
           const int64_t u = p.order ? p.order[pos] : pos;
           const int bh = static_cast<int>(u / p.nb);
           const int n = p.cnt[u];
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dV0 = desc_sw128(smem_u32(sV), BLK * 128, 1024);
       const bool leader = elect_one_sync();
       uint32_t g = 0, uc = 0;
-      for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+      for (int64_t pos = blockIdx.x; pos < nunits; pos += gridDim.x, ++uc) {
         const int64_t u = p.order ? p.order[pos] : pos;
         const int n = p.cnt[u];
         mbar_wait(&bars[Bx::Q_FULL], uc & 1);
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // rows >= BLK of the 128-row MMA tile are padding (block 64)
     const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
     uint32_t g = 0, uc = 0;
-    for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
+    for (int64_t pos = blockIdx.x; pos < nunits; pos += gridDim.x, ++uc) {
       const int64_t u = p.order ? p.order[pos] : pos;
       const int bh = static_cast<int>(u / p.nb);
       const int qb = static_cast<int>(u % p.nb);
@@ -927,7 +936,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32(tOq, ob);
       xl[q * 128 + row] = l_run;
       named_bar_sync(3, 512);
-      const float inv_l = 1.f / ((xl[row] + xl[128 + row]) + (xl[256 + row] + xl[384 + row]));
+      const float l_all = (xl[row] + xl[128 + row]) + (xl[256 + row] + xl[384 + row]);
+      const float inv_l = 1.f / l_all;
+      // the reference m was too low (P, l and O headed for overflow) or too
+      // high (every P flushed): hand the unit to the running-max kernel
+      const bool bad = rows_live && row < qrows && !(l_all >= 1e-30f && l_all <= 1.8e19f);
+      if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag_count != nullptr) {
+        if (atomicExch(p.unit_flag + u, 1) == 0) p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int32_t>(u);
+      }
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bars[Bx::O_EMPTY]);
@@ -1127,8 +1143,13 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
 // The fixed-reference kernel: key-block norms first (into kbnorm), then K2.
 template <int BLK>
 static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
-                        float* kbnorm, cudaStream_t st) {
+                        float* kbnorm, int* fallback, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
+  // fallback area: [unit_flag: num_units][count: 1][list: num_units]
+  prm.unit_flag = fallback;
+  prm.flag_count = fallback + prm.num_units;
+  prm.flag_list = fallback + prm.num_units + 1;
+  if (cudaMemsetAsync(fallback, 0, (prm.num_units + 1) * sizeof(int), st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
   {
     const int64_t warps = BH * prm.nb;
     key_block_norm_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
@@ -1145,7 +1166,16 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
     return ROPESLR_ERR_LAUNCH;
   const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
   kfn<<<static_cast<unsigned>(grid), kThreads, fx::Layout<BLK>::ALLOC, st>>>(mq, mk, mv, prm);
-  return launch_status();
+  if (int e = launch_status()) return e;
+  // the running-max kernel over the flagged units (usually none: its CTAs
+  // read a zero count and retire)
+  Params fb = prm;
+  fb.order = prm.flag_list;
+  fb.num_units_dev = prm.flag_count;
+  fb.unit_flag = nullptr;
+  fb.flag_count = nullptr;
+  fb.flag_list = nullptr;
+  return launch_tc<BLK>(s, q, k, v, fb, st);
 }
 
 static bool tc_eligible(const ropeslr_shape* s) {
@@ -1182,10 +1212,13 @@ static int resolve_impl(const ropeslr_shape* s, int impl) {
   return impl;
 }
 
+// workspace of the fixed-reference path: [schedule: NU][kbnorm: NU][fallback: 2 NU + 1]
 static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
-                                 const tc::Params& prm, float* kbnorm, cudaStream_t st) {
-  return s->block == 128 ? tc::launch_fixed<128>(s, q, k, v, prm, kbnorm, st)
-                         : tc::launch_fixed<64>(s, q, k, v, prm, kbnorm, st);
+                                 const tc::Params& prm, void* ws, cudaStream_t st) {
+  float* kbnorm = static_cast<float*>(ws) + prm.num_units;
+  int* fallback = static_cast<int*>(ws) + 2 * prm.num_units;
+  return s->block == 128 ? tc::launch_fixed<128>(s, q, k, v, prm, kbnorm, fallback, st)
+                         : tc::launch_fixed<64>(s, q, k, v, prm, kbnorm, fallback, st);
 }
 
 // K2 flavour for the tcgen05 path: the fixed-reference kernel unless
@@ -1214,6 +1247,10 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.order = nullptr;
   prm.kmat = nullptr;
   prm.kbnorm = nullptr;
+  prm.unit_flag = nullptr;
+  prm.flag_count = nullptr;
+  prm.flag_list = nullptr;
+  prm.num_units_dev = nullptr;
   prm.out_H = static_cast<int>(s->H);
   prm.out_h0 = 0;
   prm.scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(s->d)));
@@ -1264,7 +1301,8 @@ extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t
   const int which = resolve_impl(s, impl);
   if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
   // tcgen05 path: the longest-first unit schedule, then the key-block norms
-  return 2 * static_cast<size_t>(num_units_of(s)) * sizeof(int32_t);
+  // and the fallback area of the fixed-reference kernel
+  return (4 * static_cast<size_t>(num_units_of(s)) + 1) * sizeof(int32_t);
 }
 
 namespace ropeslr {
@@ -1289,7 +1327,7 @@ int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k
   prm.out_H = out_H;
   prm.out_h0 = out_h0;
   if (use_fixed_reference() && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, ROPESLR_IMPL_TCGEN05))
-    return launch_fixed_dispatch(s, q, k, v, prm, static_cast<float*>(ws) + num_units_of(s), stream);
+    return launch_fixed_dispatch(s, q, k, v, prm, ws, stream);
   return launch_tc_dispatch(s, q, k, v, prm, stream);
 }
 bool attend_tc_eligible(const ropeslr_shape* s) { return tc::tc_eligible(s); }
@@ -1341,6 +1379,6 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
     prm.order = order;
   }
   if (use_fixed_reference() && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl))
-    return launch_fixed_dispatch(s, q, k, v, prm, static_cast<float*>(ws) + num_units_of(s), cs);
+    return launch_fixed_dispatch(s, q, k, v, prm, ws, cs);
   return launch_tc_dispatch(s, q, k, v, prm, cs);
 }

@@ -272,3 +272,36 @@ def test_keep_schedule_bit_identical(block, monkeypatch):
         outs.append(out)
     assert torch.isfinite(outs[0].float()).all()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("scale", [1.0, 4.0, 12.0])
+@pytest.mark.parametrize("block", [64, 128])
+def test_fixed_reference_extreme_logits(scale, block, monkeypatch):
+    """The fixed-reference K2 (sparse_attn_fixed_kernel) picks one exponent
+    reference per row and unit; rows whose scores span too many binary
+    orders for it are recomputed by the running-max kernel.  Q and K scaled
+    by `scale` give score standard deviations of scale^2 nats: at 12 every
+    unit overflows the fixed reference, so the output must equal the
+    running-max kernel's bit for bit; at every scale the sparse branch
+    matches the float64 oracle."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((4, 16, 64), H=2)
+    q = (q.float() * scale).to(q.dtype)
+    k = (k.float() * scale).to(k.dtype)
+    st = P.ForwardSettings(P.SparseSettings(block=block, topk=6))
+    prep = P.prepare(q, k, v, x, grid, params, st, pe)
+    outs = {}
+    for mode in ("fixed", "online"):
+        monkeypatch.setenv("ROPESLR_K2", mode)
+        out, o_sp = P.attend(prep, params, st, want_o_sparse=True)
+        torch.cuda.synchronize()
+        outs[mode] = (out.clone(), o_sp.clone())
+    ref_out, ref_sel = _oracle_sparse(q, k, v, block, topk=6)
+    got = outs["fixed"][1][0].cpu().numpy()
+    for h in range(q.shape[1]):
+        G.assert_close(got[h], ref_out[h], "bf16", f"o_sparse head {h} at scale {scale}")
+    assert torch.isfinite(outs["fixed"][0].float()).all()
+    if scale >= 12.0:
+        assert torch.equal(outs["fixed"][0], outs["online"][0])
+        assert torch.equal(outs["fixed"][1], outs["online"][1])
