@@ -4,8 +4,8 @@
 // Two kernels share the warp layout below: sparse_attn_tc_kernel keeps a
 // running row max (online softmax, two O accumulators); the default,
 // sparse_attn_fixed_kernel (further down), fixes each row's exponent
-// reference per unit from a Cauchy-Schwarz bound and needs neither the max
-// nor the rescale.  ROPESLR_K2=online selects the first.
+// reference per unit from one probe score and needs neither the max nor the
+// rescale.  ROPESLR_K2=online selects the first.
 //
 // One persistent CTA per SM walks work units (bh, query block) in head-major
 // order, so the ~150 CTAs in flight read the K/V blocks of one or two heads
@@ -113,7 +113,6 @@ struct Params {
   const int32_t* perm;
   const int32_t* order;  // nullable: unit schedule (schedule_units_kernel), position -> unit
   const __nv_bfloat16* kmat;  // K itself (fixed-reference kernel: the probe key)
-  const float* kbnorm;        // [B*H, nb] max |k| per key block (fixed-reference kernel)
   // fixed-reference kernel: units whose exponent reference failed (see
   // sparse_attn_fixed_kernel) are appended to flag_list once (unit_flag
   // dedupes), and the running-max kernel recomputes them, reading its unit
@@ -609,30 +608,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// K2 + K4, fixed-reference variant ("v9").  Same warp roles, rings and
-// alternating softmax pairs as sparse_attn_tc_kernel, but every query row
-// uses ONE exponent reference m for the whole unit instead of a running max:
+// K2 + K4, fixed-reference variant.  Same warp roles, rings and alternating
+// softmax pairs as sparse_attn_tc_kernel, but every query row uses ONE
+// exponent reference m for the whole unit instead of a running max:
 //
-//   m_i = min(|q_i| * max_{k in selected blocks} |k| * scale,  s_i0 + 100)
+//   m_i = s_i0 + 64          (log2 domain)
 //
-// in the log2 domain, with s_i0 the (scaled) score of the first key of the
-// first selected block.  Cauchy-Schwarz makes the first term an upper bound
-// of every score of the row, so P = 2^(s - m) never exceeds 1 when it is the
-// minimum; the second term keeps the gap to a real score under 100 binary
-// orders, far inside the fp32 / bf16 exponent range, so no P underflows
-// that would have mattered (the exact softmax flushes terms 2^-126 below its
-// max as well).  Softmax is shift-invariant: O / l is the same quantity as
-// with the running max, only computed without the per-tile row max, the
-// max exchange between the two warpgroups of a pair, and the O rescale.
-// Hence one O accumulator shared by both pairs, and each warpgroup works
-// on its key half of a tile with no synchronisation with its partner: it
-// writes its P half over the first half of its own S columns, and the PV
-// MMA reads A from those two column ranges.
+// with s_i0 the scaled score of a probe key, the first key of the unit's
+// first selected block.  Softmax is shift-invariant, so O / l is the same
+// quantity as with the running max; only the range of P = 2^(s - m) moves:
+// the row max lies at or above s_i0, so the largest P is at least 2^-64 (P
+// of keys more than 62 binary orders below the row max flush to zero,
+// weights < 2^-62 of the max key's that fp32 / bf16 could not resolve in the
+// output anyway), and P stays finite while the row max is within ~160 binary
+// orders (110 nats) of s_i0.  The epilogue checks every row's l against
+// [2^-100, 2^110]; a unit outside goes to the running-max kernel, which
+// recomputes the flagged units in the same stream (see launch_fixed).
+// Without a running max there is no per-tile row max, no max exchange
+// between the two warpgroups of a pair and no O rescale, hence one O
+// accumulator shared by both pairs; each warpgroup works on its key half of
+// a tile with no synchronisation with its partner: it writes its P half over
+// the first half of its own S columns, and the PV MMA reads A from those two
+// column ranges.  The freed TMEM holds Q (QK^T becomes a TS-MMA).
 //
-// The only other inputs: per-key-block maxima of |k| (key_block_norm_kernel,
-// in the attend workspace) and the K tensor for the probe key s_i0.
-//
-// TMEM columns: S_0 [0,128), S_1 [128,256), O [256,384).
+// TMEM columns: S_0 [0,128), S_1 [128,256), O [256,384), Q_0/Q_1 [384,512).
 namespace fx {
 constexpr uint32_t O_COL = 256;
 constexpr uint32_t Q_COL = 384;  // Q_0 [384, 448), Q_1 [448, 512): the A operand of QK^T, per unit parity
@@ -649,7 +648,7 @@ struct Layout {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + KST * KV_BYTES;
-  // [2 unit parity][4 wg][128 rows] float2 (|q| partial, probe partial) 8 KiB,
+  // [2 unit parity][4 wg][128 rows] float2 (spare, probe partial) 8 KiB,
   // then l partials [4][128] 2 KiB, then RMS partials [4][128] 2 KiB
   static constexpr int OFF_XQ = OFF_V + VST * KV_BYTES;
   static constexpr int OFF_XL = OFF_XQ + 8192;
@@ -834,18 +833,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint8_t* qrow = sQ + (q >> 1) * (M * 128) + row * 128;
     // prep(unit at position pos, parity uc): wait for its Q tile, store this
     // thread's quarter of its Q row into TMEM buffer uc & 1 (the A operand of
-    // QK^T: column c holds d = 2c, 2c+1), publish the partial |q|^2 and
-    // probe dot product, free the shared-memory tile, return the unit's
-    // max |k| over its selected blocks (warp-uniform)
-    auto prep = [&](int64_t pos, uint32_t uc) -> float {
+    // QK^T: column c holds d = 2c, 2c+1), publish its part of the probe dot
+    // product, free the shared-memory tile
+    auto prep = [&](int64_t pos, uint32_t uc) {
       const int64_t u = p.order ? p.order[pos] : pos;
       const int bh = static_cast<int>(u / p.nb);
-      const int n = p.cnt[u];
       const int32_t* irow = p.idx + u * p.kmax;
       mbar_wait(&bars[Bx::Q_FULL], uc & 1);
       const __nv_bfloat16* krow =
           p.kmat + (static_cast<int64_t>(bh) * p.L + static_cast<int64_t>(irow[0]) * BLK) * D + q * 32;
-      float ss = 0.f, dot = 0.f;
+      float dot = 0.f;
       uint32_t qw[16];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -861,12 +858,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 a = __bfloat1622float2(qh[e]), b = __bfloat1622float2(kh[e]);
-          ss = fmaf(a.x, a.x, fmaf(a.y, a.y, ss));
           dot = fmaf(a.x, b.x, fmaf(a.y, b.y, dot));
         }
       }
       tmem_st16(lane_addr + fx::Q_COL + (uc & 1) * (D / 2) + q * 16, qw);
-      xq[((uc & 1) * 4 + q) * 128 + row] = make_float2(ss, dot);
+      xq[((uc & 1) * 4 + q) * 128 + row] = make_float2(0.f, dot);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -874,14 +870,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&bars[Bx::QT_FULL]);
         mbar_arrive(&bars[Bx::Q_EMPTY]);
       }
-      float km = 0.f;
-      for (int j = lane; j < n; j += 32) km = fmaxf(km, __ldg(p.kbnorm + static_cast<int64_t>(bh) * p.nb + irow[j]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) km = fmaxf(km, __shfl_xor_sync(0xffffffffu, km, o));
-      return km;
     };
     uint32_t g = 0, uc = 0;
-    float kmax = blockIdx.x < p.num_units ? prep(blockIdx.x, 0) : 0.f;
+    if (blockIdx.x < p.num_units) prep(blockIdx.x, 0);
     for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
       const int64_t u = p.order ? p.order[pos] : pos;
       const int bh = static_cast<int>(u / p.nb);
@@ -895,9 +886,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         const float2* xr = xq + (uc & 1) * 512 + row;
         const float2 a0 = xr[0], a1 = xr[128], a2 = xr[256], a3 = xr[384];
-        const float qn = sqrtf((a0.x + a1.x) + (a2.x + a3.x));
-        const float probe = ((a0.y + a1.y) + (a2.y + a3.y)) * p.scale_log2;
-        m_ref = fminf(qn * kmax * p.scale_log2, probe + 100.f);
+        m_ref = ((a0.y + a1.y) + (a2.y + a3.y)) * p.scale_log2 + 64.f;
       }
       float l_run = 0.f;
       const int j0 = (pr - static_cast<int>(g & 1)) & 1;
@@ -926,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       g += n;
       // the next unit's Q goes to the other TMEM buffer now, so its first
       // QK^T overlaps this unit's epilogue
-      if (pos + gridDim.x < p.num_units) kmax = prep(pos + gridDim.x, uc + 1);
+      if (pos + gridDim.x < p.num_units) prep(pos + gridDim.x, uc + 1);
       // ---------------------------------------------- fused epilogue
       // l = the four warpgroups' partial sums; warpgroup q finalises output
       // columns [32q, 32q + 32) of its row
@@ -940,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l_all;
       // the reference m was too low (P, l and O headed for overflow) or too
       // high (every P flushed): hand the unit to the running-max kernel
-      const bool bad = rows_live && row < qrows && !(l_all >= 1e-30f && l_all <= 1.8e19f);
+      const bool bad = rows_live && row < qrows && !(l_all >= 7.9e-31f && l_all <= 1.29e33f);  // [2^-100, 2^110]
       if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag_count != nullptr) {
         if (atomicExch(p.unit_flag + u, 1) == 0) p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int32_t>(u);
       }
@@ -1001,37 +990,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-}
-
-// Per key block: the largest |k| over its real rows (fp32, rounded up by a
-// relative 2^-20 so the Cauchy-Schwarz product stays an upper bound).  One
-// warp per block, 16 lanes per row pair.
-__global__ void key_block_norm_kernel(const __nv_bfloat16* __restrict__ k, int64_t L, int block, int nb, int64_t BH,
-                                      float* __restrict__ out) {
-  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (wid >= BH * nb) return;
-  const int64_t bh = wid / nb;
-  const int b = static_cast<int>(wid % nb);
-  const int rows = block_size(L, block, b);
-  const __nv_bfloat16* base = k + (bh * L + static_cast<int64_t>(b) * block) * D;
-  float best = 0.f;
-  // lanes 0-15 take even rows, 16-31 odd rows; each lane 8 of the 128 columns
-  for (int r = lane >> 4; r < rows; r += 2) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + static_cast<int64_t>(r) * D) + (lane & 15));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-    float ss = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(h[e]);
-      ss = fmaf(f.x, f.x, fmaf(f.y, f.y, ss));
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    best = fmaxf(best, ss);
-  }
-  best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, 16));
-  if (lane == 0) out[wid] = sqrtf(best) * (1.f + 1.0f / (1 << 20));
 }
 
 // Longest-first unit schedule for variable per-row block counts (the `keep`
@@ -1140,24 +1098,17 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
   return launch_status();
 }
 
-// The fixed-reference kernel: key-block norms first (into kbnorm), then K2.
+// The fixed-reference kernel, then the running-max kernel over its flagged units.
 template <int BLK>
 static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
-                        float* kbnorm, int* fallback, cudaStream_t st) {
+                        int* fallback, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
   // fallback area: [unit_flag: num_units][count: 1][list: num_units]
   prm.unit_flag = fallback;
   prm.flag_count = fallback + prm.num_units;
   prm.flag_list = fallback + prm.num_units + 1;
   if (cudaMemsetAsync(fallback, 0, (prm.num_units + 1) * sizeof(int), st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-  {
-    const int64_t warps = BH * prm.nb;
-    key_block_norm_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), s->L, BLK, prm.nb, BH, kbnorm);
-    if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-  }
   prm.kmat = static_cast<const __nv_bfloat16*>(k);
-  prm.kbnorm = kbnorm;
   CUtensorMap mq, mk, mv;
   if (!make_map(&mq, q, BH, s->L, BLK) || !make_map(&mk, k, BH, s->L, BLK) || !make_map(&mv, v, BH, s->L, BLK))
     return ROPESLR_ERR_LAUNCH;
@@ -1212,13 +1163,12 @@ static int resolve_impl(const ropeslr_shape* s, int impl) {
   return impl;
 }
 
-// workspace of the fixed-reference path: [schedule: NU][kbnorm: NU][fallback: 2 NU + 1]
+// workspace of the fixed-reference path: [schedule: NU][fallback: 2 NU + 1]
 static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                                  const tc::Params& prm, void* ws, cudaStream_t st) {
-  float* kbnorm = static_cast<float*>(ws) + prm.num_units;
-  int* fallback = static_cast<int*>(ws) + 2 * prm.num_units;
-  return s->block == 128 ? tc::launch_fixed<128>(s, q, k, v, prm, kbnorm, fallback, st)
-                         : tc::launch_fixed<64>(s, q, k, v, prm, kbnorm, fallback, st);
+  int* fallback = static_cast<int*>(ws) + prm.num_units;
+  return s->block == 128 ? tc::launch_fixed<128>(s, q, k, v, prm, fallback, st)
+                         : tc::launch_fixed<64>(s, q, k, v, prm, fallback, st);
 }
 
 // K2 flavour for the tcgen05 path: the fixed-reference kernel unless
@@ -1246,7 +1196,6 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.perm = perm;
   prm.order = nullptr;
   prm.kmat = nullptr;
-  prm.kbnorm = nullptr;
   prm.unit_flag = nullptr;
   prm.flag_count = nullptr;
   prm.flag_list = nullptr;
@@ -1300,9 +1249,9 @@ extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t
   if (!s) return 0;
   const int which = resolve_impl(s, impl);
   if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
-  // tcgen05 path: the longest-first unit schedule, then the key-block norms
-  // and the fallback area of the fixed-reference kernel
-  return (4 * static_cast<size_t>(num_units_of(s)) + 1) * sizeof(int32_t);
+  // tcgen05 path: the longest-first unit schedule, then the fallback area of
+  // the fixed-reference kernel
+  return (3 * static_cast<size_t>(num_units_of(s)) + 1) * sizeof(int32_t);
 }
 
 namespace ropeslr {

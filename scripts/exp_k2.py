@@ -16,7 +16,7 @@ print("prepare done", flush=True)
 out = torch.empty((1, L, H, 128), dtype=torch.bfloat16, device='cuda')
 torch.cuda.synchronize()
 att = int(prep.sel.attended.sum())
-def timeit(n=5):
+def timeit(n=int(os.environ.get('EXP_ITERS', '5'))):
     for i in range(2):
         P.attend(prep, params, st, out=out)
         torch.cuda.synchronize()

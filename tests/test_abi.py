@@ -56,8 +56,8 @@ def test_host_functions():
     shp = _lib.Shape(1, 24, 118800, 128, 128, _lib.BF16)
     ws = lib.ropeslr_select_workspace_bytes(ctypes.byref(shp))
     assert ws >= (2 * 24 * 929 * 128 + 24 * 929 * 929) * 8
-    # tcgen05: unit schedule, key-block norms, fallback flags / list / count
-    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 0) == (4 * 24 * 929 + 1) * 4
+    # tcgen05: unit schedule, fallback flags / count / list
+    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 0) == (3 * 24 * 929 + 1) * 4
     assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 1) == 24 * 118800 * 128 * 4
 
 
