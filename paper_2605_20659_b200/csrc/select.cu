@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace ropeslr {
@@ -118,6 +120,72 @@ __global__ void __launch_bounds__(256) block_scores_kernel(const double* __restr
       int gj = j0 + tx + 16 * v;
       if (gj < nb) out[static_cast<int64_t>(gi) * nb + gj] = acc[u][v] / sqrt_d;
     }
+  }
+}
+
+// The same scores on the FP64 tensor cores (DMMA m8n8k4): 64x64 output tile
+// per CTA, four warps of 32x32 (4x4 DMMA tiles each), k-chunks of 32 staged
+// in shared memory.  Products and sums are IEEE float64 like the CUDA-core
+// kernel (only the summation order differs, ~1 ulp: the top-k margins at
+// configs 1-3 are >= 1e-9 relative).
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) block_scores_dmma_kernel(const double* __restrict__ pooled,
+                                                                double* __restrict__ scores, int nb, int d,
+                                                                int64_t BH, double sqrt_d) {
+  constexpr int KC = 32;
+  __shared__ double As[KC][64 + 1];
+  __shared__ double Bs[KC][64 + 1];
+  const int64_t bh = blockIdx.z;
+  const double* pq = pooled + bh * nb * d;
+  const double* pk = pooled + (BH + bh) * nb * d;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;  // warp tile origin
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int k0 = 0; k0 < d; k0 += KC) {
+    for (int e = tid; e < 64 * KC; e += 128) {
+      const int r = e / KC, c = e % KC;
+      const int gi = i0 + r, gj = j0 + r, gc = k0 + c;
+      As[c][r] = (gi < nb && gc < d) ? pq[static_cast<int64_t>(gi) * d + gc] : 0.0;
+      Bs[c][r] = (gj < nb && gc < d) ? pk[static_cast<int64_t>(gj) * d + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = As[kk + t4][wr + 8 * m + g];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) b[n] = Bs[kk + t4][wc + 8 * n + g];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n], a[m], b[n]);
+    }
+    __syncthreads();
+  }
+  double* out = scores + bh * nb * nb;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int gi = i0 + wr + 8 * m + g;
+    if (gi >= nb) continue;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gj = j0 + wc + 8 * n + 2 * t4 + e;
+        if (gj < nb) out[static_cast<int64_t>(gi) * nb + gj] = acc[m][n][e] / sqrt_d;
+      }
   }
 }
 
@@ -426,7 +494,12 @@ static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_param
   {
     dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
               static_cast<unsigned>(BH));
-    block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
+    // ROPESLR_SCORES=fma: the CUDA-core kernel (A/B timing)
+    const char* e = getenv("ROPESLR_SCORES");
+    if (e != nullptr && e[0] == 'f')
+      block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
+    else
+      block_scores_dmma_kernel<<<grid, 128, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
     if (launch_status()) return ROPESLR_ERR_LAUNCH;
   }
   if (sel->topk > 0 && nb <= 1024) {
