@@ -19,7 +19,8 @@ constexpr int TILE = BLK * 128 * 2;
 
 template <int NST>
 __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ CUtensorMap tm, const int* order,
-                                                      int tiles_per_cta, int nb, int heads, long long* cyc) {
+                                                      int tiles_per_cta, int nb, int heads, long long* cyc,
+                                                      int evict_last) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * TILE);
   uint64_t* empty = full + NST;
@@ -31,7 +32,7 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
     fence_mbar_init();
   }
   __syncthreads();
-  const uint64_t pol = policy_evict_last();
+  const uint64_t pol = evict_last ? policy_evict_last() : policy_evict_normal();
   long long t0 = clock64();
   if (threadIdx.x == 0) {
     for (int i = 0; i < tiles_per_cta; ++i) {
@@ -76,8 +77,13 @@ int main() {
   cuuint64_t dims[3] = {128, (cuuint64_t)L, (cuuint64_t)heads};
   cuuint64_t strides[2] = {256, (cuuint64_t)L * 256};
   cuuint32_t box[3] = {64, BLK, 1}, es[3] = {1, 1, 1};
-  enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  int evict_last = 1;
+  auto encode = [&]() {
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  };
+  encode();
   const int tiles = 4000;
   auto run = [&](auto kern, int nst) {
     const int smem = nst * TILE + 1024;
@@ -87,7 +93,7 @@ int main() {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0);
-      kern<<<148, 64, smem>>>(tm, order, tiles, nb, heads, cyc);
+      kern<<<148, 64, smem>>>(tm, order, tiles, nb, heads, cyc, evict_last);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -97,7 +103,7 @@ int main() {
       long long mx = 0;
       for (auto v : c) mx = v > mx ? v : mx;
       const double bytes = 148.0 * tiles * TILE;
-      printf("NST %d rep %d: %.3f ms  %.2f TB/s  %.0f B/clk (SM clk)  %.0f clk per 32 KiB tile per SM\n", nst, rep, ms,
+      printf("promo %d evict_last %d NST %d rep %d: %.3f ms  %.2f TB/s  %.0f B/clk (SM clk)  %.0f clk per 32 KiB tile per SM\n", (int)promo, evict_last, nst, rep, ms,
              bytes / ms / 1e9, bytes / mx, (double)mx / tiles);
     }
   };
@@ -105,5 +111,13 @@ int main() {
   run(stream_kernel<3>, 3);
   run(stream_kernel<4>, 4);
   run(stream_kernel<6>, 6);
+  evict_last = 0;
+  run(stream_kernel<4>, 4);
+  for (auto pr : {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B}) {
+    promo = pr;
+    encode();
+    evict_last = 1;
+    run(stream_kernel<4>, 4);
+  }
   return 0;
 }
