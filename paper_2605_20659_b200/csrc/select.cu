@@ -18,6 +18,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace ropeslr {
 
@@ -68,6 +69,60 @@ __global__ void __launch_bounds__(256) pool_blocks_kernel(const T* __restrict__ 
     double s = 0.0;
     for (int j = 0; j < lanes_r; ++j) s += sred[j * d + c];
     dst[c] = s / static_cast<double>(rows);
+  }
+}
+
+// The same pooling for bf16 rows of d = 128 and blocks of <= 128 rows: the
+// block's rows are one contiguous run of <= 32 KiB, fetched by a single bulk
+// copy into shared memory (so the bytes in flight do not depend on register
+// occupancy), then summed in float64 from there.  256 threads: column chunk
+// c = t % 16 (8 columns), rows t / 16 + 16 i.
+__global__ void __launch_bounds__(256) pool_blocks_bulk_kernel(const __nv_bfloat16* __restrict__ q,
+                                                               const __nv_bfloat16* __restrict__ k,
+                                                               double* __restrict__ pooled, int64_t L, int block,
+                                                               int nb, int64_t BH) {
+  constexpr int D = 128;
+  __shared__ __align__(128) uint8_t buf[128 * D * 2];  // the block's rows; then the f64 partial sums
+  __shared__ uint64_t bar;
+  const int64_t bh = blockIdx.y;
+  const __nv_bfloat16* src = (blockIdx.z == 0 ? q : k) + bh * L * D;
+  const int b = blockIdx.x;
+  const int rows = block_size(L, block, b);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(rows) * D * 2;
+    sm100::mbar_arrive_expect_tx(&bar, bytes);
+    sm100::bulk_load_1d(buf, src + static_cast<int64_t>(b) * block * D, bytes, &bar, sm100::policy_evict_first());
+  }
+  sm100::mbar_wait(&bar, 0);
+  const int ch = tid & 15, rr = tid >> 4;
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  for (int r = rr; r < rows; r += 16) {
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + (r * D + ch * 8) * 2);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      acc[2 * e] += static_cast<double>(f.x);
+      acc[2 * e + 1] += static_cast<double>(f.y);
+    }
+  }
+  __syncthreads();  // every row has been read: buf now holds the partial sums
+  double* sred = reinterpret_cast<double*>(buf);  // [16 row lanes][128]
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sred[rr * D + ch * 8 + i] = acc[i];
+  __syncthreads();
+  if (tid < D) {
+    double s = 0.0;
+    for (int j = 0; j < 16; ++j) s += sred[j * D + tid];
+    pooled[((static_cast<int64_t>(blockIdx.z) * BH + bh) * nb + b) * D + tid] = s / static_cast<double>(rows);
   }
 }
 
@@ -564,7 +619,11 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
     const int chunks = d / 8;
     const int lanes_r = 256 / chunks;
     size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
-    if (s->dtype == ROPESLR_BF16)
+    if (s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128 && aligned16(q) && aligned16(k))
+      pool_blocks_bulk_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                     static_cast<const __nv_bfloat16*>(k), pooled, s->L, s->block,
+                                                     nb, BH);
+    else if (s->dtype == ROPESLR_BF16)
       pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
                                                                 static_cast<const __nv_bfloat16*>(k), pooled, s->L,
                                                                 d, s->block, nb, BH);
