@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include "common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace ropeslr {
 namespace rp {
@@ -71,19 +72,39 @@ __device__ __forceinline__ __nv_bfloat16 cast_out<__nv_bfloat16>(double v) {
 
 // grid (nb, B*H, 2): z = 0 Q, z = 1 K; 256 threads; each thread owns 8
 // consecutive columns (4 pairs) of the rows r = rr, rr + lanes_r, ...
-template <typename T>
+// BULK (bf16, d = 128, block <= 128): the block's rows, one contiguous run of
+// <= 32 KiB, arrive by a single bulk copy into shared memory first, so the
+// loads in flight do not hang on one row load per thread at a time; the
+// staging buffer then holds the f64 partial sums.
+template <typename T, bool BULK>
 __global__ void __launch_bounds__(256) rope_pool_kernel(const T* __restrict__ q_in, const T* __restrict__ k_in,
                                                         T* __restrict__ q_out, T* __restrict__ k_out,
                                                         double* __restrict__ pooled, const Tables tab, int64_t L,
                                                         int d, int block, int nb, int64_t BH, int grid_h,
                                                         int grid_w) {
-  extern __shared__ double sred[];
+  extern __shared__ double sred_dyn[];
+  __shared__ __align__(128) uint8_t stage[BULK ? 128 * 128 * 2 : 16];
+  __shared__ uint64_t bar;
   const int64_t bh = blockIdx.y;
   const T* src = (blockIdx.z == 0 ? q_in : k_in) + bh * L * d;
   T* dst = (blockIdx.z == 0 ? q_out : k_out) + bh * L * d;
   const int b = blockIdx.x;
   const int rows = block_size(L, block, b);
   const int64_t r0 = static_cast<int64_t>(b) * block;
+  if (BULK) {
+    if (threadIdx.x == 0) {
+      sm100::mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(rows) * d * sizeof(T);
+      sm100::mbar_arrive_expect_tx(&bar, bytes);
+      sm100::bulk_load_1d(stage, src + r0 * d, bytes, &bar, sm100::policy_evict_first());
+    }
+    sm100::mbar_wait(&bar, 0);
+  }
+  double* sred = BULK ? reinterpret_cast<double*>(stage) : sred_dyn;
   const int chunks = d / 8;
   const int lanes_r = blockDim.x / chunks;
   const int tid = threadIdx.x;
@@ -114,7 +135,10 @@ __global__ void __launch_bounds__(256) rope_pool_kernel(const T* __restrict__ q_
     for (int r = rr; r < rows; r += lanes_r) {
       const int64_t pos = r0 + r;
       float v[8];
-      load8(src + pos * d + ch * 8, v);
+      if (BULK)
+        load8(reinterpret_cast<const T*>(stage) + static_cast<int64_t>(r) * d + ch * 8, v);
+      else
+        load8(src + pos * d + ch * 8, v);
       double out[8];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -148,6 +172,9 @@ __global__ void __launch_bounds__(256) rope_pool_kernel(const T* __restrict__ q_
         ++ct;
       }
     }
+  }
+  if (BULK) __syncthreads();  // every staged row has been read
+  if (rr < lanes_r) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) sred[rr * d + ch * 8 + i] = acc[i];
   }
@@ -225,13 +252,18 @@ extern "C" int ropeslr_rope_pool(const ropeslr_shape* s, const ropeslr_rope_args
   dim3 grid(nb, static_cast<unsigned>(BH), 2);
   const int lanes_r = 256 / (d / 8);
   const size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
-  if (s->dtype == ROPESLR_BF16)
-    rp::rope_pool_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(
+  if (s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128)
+    rp::rope_pool_kernel<__nv_bfloat16, true><<<grid, 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(q_in), static_cast<const __nv_bfloat16*>(k_in),
+        static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_out), pooled, tab, s->L, d, s->block, nb,
+        BH, r->grid_h, r->grid_w);
+  else if (s->dtype == ROPESLR_BF16)
+    rp::rope_pool_kernel<__nv_bfloat16, false><<<grid, 256, sm, st>>>(
         static_cast<const __nv_bfloat16*>(q_in), static_cast<const __nv_bfloat16*>(k_in),
         static_cast<__nv_bfloat16*>(q_out), static_cast<__nv_bfloat16*>(k_out), pooled, tab, s->L, d, s->block, nb,
         BH, r->grid_h, r->grid_w);
   else
-    rp::rope_pool_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q_in), static_cast<const float*>(k_in),
+    rp::rope_pool_kernel<float, false><<<grid, 256, sm, st>>>(static_cast<const float*>(q_in), static_cast<const float*>(k_in),
                                                        static_cast<float*>(q_out), static_cast<float*>(k_out), pooled,
                                                        tab, s->L, d, s->block, nb, BH, r->grid_h, r->grid_w);
   return launch_status();
