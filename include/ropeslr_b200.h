@@ -260,6 +260,19 @@ typedef struct ropeslr_host_forward {
 size_t ropeslr_forward_host_workspace_bytes(const ropeslr_host_forward* args);
 int ropeslr_forward_host(const ropeslr_host_forward* args, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------- caller helpers: the config-4 DiT block (dit.py)
+ * Fused token-wise ops around the op, bf16 rows of D columns (D % 8 == 0,
+ * D <= 2048), fp32 math, one launch each instead of PyTorch's 5-8:
+ *   ln_modulate:    y = LayerNorm(x) * (1 + scale) + shift   (scale, shift [D] fp32)
+ *   rms_heads:      RMSNorm(x) * weight (weight NULL: no norm), written
+ *                   head-major [H, N, D/H] when head_major, else [N, D]
+ *   gated_residual: x += bf16(y * gate)                      (gate [D] fp32) */
+int ropeslr_dit_ln_modulate(const void* x, const float* shift, const float* scale, float eps, int64_t N, int32_t D,
+                            void* y, void* stream);
+int ropeslr_dit_rms_heads(const void* x, const void* weight, float eps, int64_t N, int32_t D, int32_t H,
+                          int32_t head_major, void* out, void* stream);
+int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_t N, int32_t D, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,9 @@ _SIGNATURES = {
     "ropeslr_select_pooled_workspace_bytes": (c_sz, [P(Shape)]),
     "ropeslr_select_from_pooled": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
                                            c_vp, c_sz, c_vp]),
+    "ropeslr_dit_ln_modulate": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
+    "ropeslr_dit_rms_heads": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "ropeslr_dit_gated_residual": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "ropeslr_rope_pool_workspace_bytes": (c_sz, [P(RopeArgs)]),
     "ropeslr_rope_pool": (c_i32, [P(Shape), P(RopeArgs), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_forward_host_workspace_bytes": (c_sz, [P(HostForward)]),

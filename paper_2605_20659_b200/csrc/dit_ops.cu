@@ -1,0 +1,181 @@
+// Caller-side fused ops of the config-4 DiT (dit.py), the transformer block
+// around RoPeSLR: the token-wise normalisations and gated residuals that
+// PyTorch would otherwise run as 5-8 separate elementwise kernels each, and
+// the head-major re-layout the op's Q/K/V need.  All are HBM-bound row
+// kernels: one warp per token row of D = H * d bf16 values, fp32 math.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace ropeslr {
+namespace dit {
+
+constexpr int kMaxPerLane = 64;  // D <= 2048
+
+// Row r of x[N, D] into registers: lane holds columns [8 * (lane + 32 j), +8).
+template <int J>
+__device__ __forceinline__ void load_row(const __nv_bfloat16* row, int D, int lane, float (&v)[J * 8]) {
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int c = (lane + 32 * j) * 8;
+    if (c < D) {
+      load8(row + c, v + 8 * j);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[8 * j + e] = 0.f;
+    }
+  }
+}
+
+// y = LayerNorm(x) * (1 + scale) + shift (no affine; fp32 statistics).
+template <int J>
+__global__ void ln_modulate_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ shift,
+                                   const float* __restrict__ scale, float eps, int64_t N, int D,
+                                   __nv_bfloat16* __restrict__ y) {
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= N) return;
+  float v[J * 8];
+  load_row<J>(x + r * D, D, lane, v);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < J * 8; ++i) s += v[i];
+  const float mean = warp_sum(s) / static_cast<float>(D);
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    if ((lane + 32 * j) * 8 >= D) continue;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float t = v[8 * j + e] - mean;
+      q = fmaf(t, t, q);
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / static_cast<float>(D) + eps);
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int c = (lane + 32 * j) * 8;
+    if (c >= D) continue;
+    float sc[8], sh[8], o[8];
+    load8(scale + c, sc);
+    load8(shift + c, sh);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = fmaf((v[8 * j + e] - mean) * rstd, 1.f + sc[e], sh[e]);
+    store8(y + r * D + c, o);
+  }
+}
+
+// RMSNorm over the row (torch order: bf16(x * rsqrt(mean(x^2) + eps)) * w,
+// w == nullptr: no norm) written head-major out[H, N, d] (head_major) or in
+// place of the row layout out[N, D].
+template <int J>
+__global__ void rms_heads_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, float eps,
+                                 int64_t N, int D, int H, int head_major, __nv_bfloat16* __restrict__ out) {
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= N) return;
+  const int d = D / H;
+  float v[J * 8];
+  load_row<J>(x + r * D, D, lane, v);
+  float rs = 1.f;
+  if (w != nullptr) {
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < J * 8; ++i) q = fmaf(v[i], v[i], q);
+    rs = rsqrtf(warp_sum(q) / static_cast<float>(D) + eps);
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int c = (lane + 32 * j) * 8;
+    if (c >= D) continue;
+    float o[8], wv[8];
+    if (w != nullptr) load8(w + c, wv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float t = v[8 * j + e];
+      if (w != nullptr) t = __bfloat162float(__float2bfloat16_rn(t * rs)) * wv[e];
+      o[e] = t;
+    }
+    const int h = c / d, cc = c - h * d;  // 8 | d: a chunk never straddles two heads
+    __nv_bfloat16* dst = head_major ? out + (static_cast<int64_t>(h) * N + r) * d + cc : out + r * D + c;
+    store8(dst, o);
+  }
+}
+
+// x = x + bf16(y * gate), torch's `x + (y.float() * g).to(bf16)`.
+template <int J>
+__global__ void gated_residual_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
+                                      const float* __restrict__ gate, int64_t N, int D) {
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= N) return;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int c = (lane + 32 * j) * 8;
+    if (c >= D) continue;
+    float xv[8], yv[8], gv[8];
+    load8(x + r * D + c, xv);
+    load8(y + r * D + c, yv);
+    load8(gate + c, gv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xv[e] = xv[e] + __bfloat162float(__float2bfloat16_rn(yv[e] * gv[e]));
+    store8(x + r * D + c, xv);
+  }
+}
+
+static bool row_ok(int64_t N, int D) { return N >= 1 && D >= 8 && D % 8 == 0 && D <= 32 * 8 * kMaxPerLane / 8; }
+
+}  // namespace dit
+}  // namespace ropeslr
+
+using namespace ropeslr;
+
+#define ROPESLR_DIT_DISPATCH(KERNEL, ...)                                          \
+  do {                                                                             \
+    const unsigned grid_ = static_cast<unsigned>(ceil_div(N * 32, 256));           \
+    const int J_ = static_cast<int>(ceil_div(D, 256));                             \
+    if (J_ <= 2)                                                                   \
+      dit::KERNEL<2><<<grid_, 256, 0, st>>>(__VA_ARGS__);                          \
+    else if (J_ <= 4)                                                              \
+      dit::KERNEL<4><<<grid_, 256, 0, st>>>(__VA_ARGS__);                          \
+    else if (J_ <= 6)                                                              \
+      dit::KERNEL<6><<<grid_, 256, 0, st>>>(__VA_ARGS__);                          \
+    else                                                                           \
+      dit::KERNEL<8><<<grid_, 256, 0, st>>>(__VA_ARGS__);                          \
+  } while (0)
+
+extern "C" int ropeslr_dit_ln_modulate(const void* x, const float* shift, const float* scale, float eps, int64_t N,
+                                       int32_t D, void* y, void* stream) {
+  if (!x || !shift || !scale || !y) return ROPESLR_ERR_NULL;
+  if (!dit::row_ok(N, D)) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(y)) return ROPESLR_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ROPESLR_DIT_DISPATCH(ln_modulate_kernel, static_cast<const __nv_bfloat16*>(x), shift, scale, eps, N, D,
+                       static_cast<__nv_bfloat16*>(y));
+  return launch_status();
+}
+
+extern "C" int ropeslr_dit_rms_heads(const void* x, const void* weight, float eps, int64_t N, int32_t D, int32_t H,
+                                     int32_t head_major, void* out, void* stream) {
+  if (!x || !out) return ROPESLR_ERR_NULL;
+  if (!dit::row_ok(N, D) || H < 1 || D % H || (D / H) % 8) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(out)) return ROPESLR_ERR_ALIGN;
+  if (!head_major && x == out && weight == nullptr) return ROPESLR_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ROPESLR_DIT_DISPATCH(rms_heads_kernel, static_cast<const __nv_bfloat16*>(x),
+                       static_cast<const __nv_bfloat16*>(weight), eps, N, D, H, head_major,
+                       static_cast<__nv_bfloat16*>(out));
+  return launch_status();
+}
+
+extern "C" int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_t N, int32_t D,
+                                          void* stream) {
+  if (!x || !y || !gate) return ROPESLR_ERR_NULL;
+  if (!dit::row_ok(N, D)) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(y)) return ROPESLR_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ROPESLR_DIT_DISPATCH(gated_residual_kernel, static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(y),
+                       gate, N, D);
+  return launch_status();
+}

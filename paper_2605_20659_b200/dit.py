@@ -19,6 +19,7 @@ other layer is token-wise and needs no communication.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 from typing import Optional
@@ -27,6 +28,7 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from . import _lib
 from .mechanism import ForwardSettings, MechanismParams, PETables, SparseSettings, forward
 from .rope3d import GridShape, RopeConfig
 from .ulysses import seq_slice, ulysses_attention
@@ -65,6 +67,52 @@ class RMSNorm(nn.Module):
     def forward(self, x):
         xf = x.float()
         return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.eps)).to(x.dtype) * self.weight
+
+
+# ---- fused token-wise ops of the block (csrc/dit_ops.cu): one launch each
+# where the PyTorch composition runs 5-8 elementwise kernels, bf16 rows.
+# FUSED_OPS = False runs the plain PyTorch composition (tests compare both).
+FUSED_OPS = True
+def _stream(t):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def ln_modulate(x: torch.Tensor, shift: torch.Tensor, scale: torch.Tensor, eps: float) -> torch.Tensor:
+    """bf16(LayerNorm(x) * (1 + scale) + shift); x [B, L, D] bf16, shift /
+    scale broadcastable to [D] (float32)."""
+    D = x.shape[-1]
+    x = x.contiguous()
+    sh = shift.reshape(-1)[-D:].float().contiguous()
+    sc = scale.reshape(-1)[-D:].float().contiguous()
+    y = torch.empty_like(x)
+    _lib.call("ropeslr_dit_ln_modulate", x.data_ptr(), sh.data_ptr(), sc.data_ptr(), float(eps), x.numel() // D, D,
+              y.data_ptr(), _stream(x))
+    return y
+
+
+def rms_heads(x: torch.Tensor, weight: Optional[torch.Tensor], eps: float, H: int, head_major: bool = True):
+    """RMSNorm over the last dim (weight None: none) of x [1, L, D] bf16; out
+    [1, H, L, D/H] when head_major, else [1, L, H, D/H]."""
+    B, L, D = x.shape
+    if B != 1:
+        raise ValueError("rms_heads: batch 1 (the DiT step)")
+    x = x.contiguous()
+    out = torch.empty((1, H, L, D // H) if head_major else (1, L, H, D // H), dtype=x.dtype, device=x.device)
+    w = None if weight is None else weight.to(x.dtype).contiguous()
+    _lib.call("ropeslr_dit_rms_heads", x.data_ptr(), None if w is None else w.data_ptr(), float(eps), L, D, H,
+              int(head_major), out.data_ptr(), _stream(x))
+    return out
+
+
+def gated_residual_(x: torch.Tensor, y: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
+    """x += bf16(y * gate) in place; x, y [B, L, D] bf16, gate -> [D] float32."""
+    D = x.shape[-1]
+    if not x.is_contiguous():
+        raise ValueError("gated_residual_: x must be contiguous")
+    y = y.contiguous()
+    g = gate.reshape(-1)[-D:].float().contiguous()
+    _lib.call("ropeslr_dit_gated_residual", x.data_ptr(), y.data_ptr(), g.data_ptr(), x.numel() // D, D, _stream(x))
+    return x
 
 
 def sinusoidal(t: torch.Tensor, dim: int) -> torch.Tensor:
@@ -108,6 +156,8 @@ class WanBlock(nn.Module):
         B, Lr, D = x.shape
         H, d = cfg.heads, cfg.head_dim
         sh_a, sc_a, g_a, sh_f, sc_f, g_f = (self.modulation + e).chunk(6, dim=1)
+        if FUSED_OPS and B == 1 and x.dtype == torch.bfloat16 and x.is_cuda:
+            return self._forward_fused(x, (sh_a, sc_a, g_a, sh_f, sc_f, g_f), ctx, grid, pe, settings, rope, group)
         y = (self.norm1(x.float()) * (1 + sc_a) + sh_a).to(x.dtype)
         q = self.norm_q(self.q(y)).view(B, Lr, H, d)
         k = self.norm_k(self.k(y)).view(B, Lr, H, d)
@@ -128,6 +178,37 @@ class WanBlock(nn.Module):
         x = x + self.co(ca)
         y = (self.norm2(x.float()) * (1 + sc_f) + sh_f).to(x.dtype)
         x = x + (self.ffn2(F.gelu(self.ffn1(y), approximate="tanh")).float() * g_f).to(x.dtype)
+        return x
+
+    def _forward_fused(self, x, mods, ctx, grid, pe, settings, rope, group):
+        """The same block with the token-wise ops fused (csrc/dit_ops.cu):
+        modulated LayerNorms, Q/K RMSNorm written straight into the op's
+        head-major layout, gated residuals in place."""
+        cfg = self.cfg
+        B, Lr, D = x.shape
+        H, d = cfg.heads, cfg.head_dim
+        sh_a, sc_a, g_a, sh_f, sc_f, g_f = mods
+        x = x.contiguous().clone()
+        y = ln_modulate(x, sh_a, sc_a, cfg.eps)
+        params = self.ropeslr_params()
+        hm = group is None  # the Ulysses wrapper takes token-major [B, L_r, H, d]
+        q = rms_heads(self.q(y), self.norm_q.weight, self.norm_q.eps, H, head_major=hm)
+        k = rms_heads(self.k(y), self.norm_k.weight, self.norm_k.eps, H, head_major=hm)
+        v = rms_heads(self.v(y), None, 0.0, H, head_major=hm)
+        if group is not None:
+            a = ulysses_attention(q, k, v, y, grid, params, settings, pe, group=group, rope=rope)
+        else:
+            a = forward(q, k, v, y, grid, params, settings, pe, rope=rope)
+        gated_residual_(x, self.o(a), g_a)
+        # cross-attention to the text tokens
+        c = self.norm3(x)
+        cq = rms_heads(self.cq(c), self.norm_cq.weight, self.norm_cq.eps, H)
+        ck = self.norm_ck(self.ck(ctx)).view(B, -1, H, d).transpose(1, 2)
+        cv = self.cv(ctx).view(B, -1, H, d).transpose(1, 2)
+        ca = F.scaled_dot_product_attention(cq, ck, cv).transpose(1, 2).reshape(B, Lr, D)
+        x += self.co(ca)
+        y = ln_modulate(x, sh_f, sc_f, cfg.eps)
+        gated_residual_(x, self.ffn2(F.gelu(self.ffn1(y), approximate="tanh")), g_f)
         return x
 
 

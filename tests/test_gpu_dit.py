@@ -51,3 +51,57 @@ def test_ulysses_world1_equals_direct_forward():
                             v.permute(0, 2, 1, 3).contiguous(), x, grid, params, st, pe)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+def test_fused_block_ops_match_torch(monkeypatch):
+    """The fused token-wise ops (csrc/dit_ops.cu: modulated LayerNorm,
+    RMSNorm into the head-major layout, gated residual) give the plain
+    PyTorch composition's block output within bf16 rounding."""
+    import paper_2605_20659_b200.dit as dit
+
+    cfg = _small_cfg()
+    model = dit.make_model(cfg)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    latent = torch.randn((1, 16, 3, 8, 16), generator=g, device="cuda").to(torch.bfloat16)
+    text = torch.randn((1, cfg.text_len, cfg.text_dim), generator=g, device="cuda").to(torch.bfloat16)
+    t = torch.tensor([250.0], device="cuda")
+    outs = {}
+    for fused in (True, False):
+        monkeypatch.setattr(dit, "FUSED_OPS", fused)
+        with torch.no_grad():
+            outs[fused] = model(latent, t, text).float()
+    torch.cuda.synchronize()
+    a, b = outs[True], outs[False]
+    scale = b.abs().max().item()
+    assert torch.isfinite(a).all()
+    assert (a - b).abs().max().item() <= 3e-2 * scale
+    assert ((a - b).abs().mean() / b.abs().mean()).item() <= 1e-2
+
+
+def test_fused_ops_unit():
+    """Each fused op against its PyTorch definition on random rows."""
+    import torch.nn.functional as F
+
+    import paper_2605_20659_b200.dit as dit
+
+    g = torch.Generator(device="cuda").manual_seed(4)
+    L, D, H = 333, 1536, 12
+    x = torch.randn((1, L, D), generator=g, device="cuda").to(torch.bfloat16)
+    sh = torch.randn((1, 1, D), generator=g, device="cuda") * 0.1
+    sc = torch.randn((1, 1, D), generator=g, device="cuda") * 0.1
+    want = (F.layer_norm(x.float(), (D,), eps=1e-6) * (1 + sc) + sh).to(torch.bfloat16)
+    got = dit.ln_modulate(x, sh, sc, 1e-6)
+    assert (got.float() - want.float()).abs().max().item() <= 2e-2
+    w = (1 + 0.1 * torch.randn(D, generator=g, device="cuda")).to(torch.bfloat16)
+    xf = x.float()
+    rms = ((xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6)).to(torch.bfloat16) * w)
+    got_h = dit.rms_heads(x, w, 1e-6, H)
+    torch.testing.assert_close(got_h, rms.view(1, L, H, D // H).permute(0, 2, 1, 3), atol=2e-2, rtol=1e-2)
+    got_t = dit.rms_heads(x, w, 1e-6, H, head_major=False)
+    torch.testing.assert_close(got_t, rms.view(1, L, H, D // H), atol=2e-2, rtol=1e-2)
+    assert torch.equal(dit.rms_heads(x, None, 0.0, H), x.view(1, L, H, D // H).permute(0, 2, 1, 3))
+    y = torch.randn((1, L, D), generator=g, device="cuda").to(torch.bfloat16)
+    gate = torch.randn((1, 1, D), generator=g, device="cuda")
+    want_x = x + (y.float() * gate).to(torch.bfloat16)
+    got_x = dit.gated_residual_(x.clone(), y, gate)
+    assert torch.equal(got_x, want_x)
