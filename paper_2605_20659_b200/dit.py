@@ -208,7 +208,9 @@ class WanBlock(nn.Module):
         ca = F.scaled_dot_product_attention(cq, ck, cv).transpose(1, 2).reshape(B, Lr, D)
         x += self.co(ca)
         y = ln_modulate(x, sh_f, sc_f, cfg.eps)
-        gated_residual_(x, self.ffn2(F.gelu(self.ffn1(y), approximate="tanh")), g_f)
+        # FFN up-projection with the tanh-GELU in the cuBLASLt epilogue
+        h = torch._addmm_activation(self.ffn1.bias, y.view(-1, D), self.ffn1.weight.t(), use_gelu=True)
+        gated_residual_(x, self.ffn2(h.view(B, Lr, -1)), g_f)
         return x
 
 
