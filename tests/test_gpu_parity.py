@@ -305,3 +305,32 @@ def test_fixed_reference_extreme_logits(scale, block, monkeypatch):
     if scale >= 12.0:
         assert torch.equal(outs["fixed"][0], outs["online"][0])
         assert torch.equal(outs["fixed"][1], outs["online"][1])
+
+
+def test_fixed_reference_partial_fallback(monkeypatch):
+    """One head with extreme logits (every one of its units falls back to the
+    running-max kernel) next to normal heads (none does), in the same launch,
+    with and without the unit schedule: the fallen-back head equals the
+    running-max kernel bit for bit, and every head matches the oracle."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((4, 16, 64), H=3)
+    q, k = q.clone(), k.clone()
+    q[:, 1] = (q[:, 1].float() * 12.0).to(q.dtype)
+    k[:, 1] = (k[:, 1].float() * 12.0).to(k.dtype)
+    st = P.ForwardSettings(P.SparseSettings(block=128, topk=5))
+    prep = P.prepare(q, k, v, x, grid, params, st, pe)
+    ref_out, _ = _oracle_sparse(q, k, v, 128, topk=5)
+    res = {}
+    for mode, sched in (("fixed", "0"), ("fixed", "1"), ("online", "0")):
+        monkeypatch.setenv("ROPESLR_K2", mode)
+        monkeypatch.setenv("ROPESLR_SCHEDULE", sched)
+        _, o_sp = P.attend(prep, params, st, want_o_sparse=True)
+        torch.cuda.synchronize()
+        res[(mode, sched)] = o_sp.clone()
+    for key in (("fixed", "0"), ("fixed", "1")):
+        got = res[key][0].cpu().numpy()
+        for h in range(3):
+            G.assert_close(got[h], ref_out[h], "bf16", f"o_sparse head {h} {key}")
+        assert torch.equal(res[key][0, 1], res[("online", "0")][0, 1])
+    assert torch.equal(res[("fixed", "0")], res[("fixed", "1")])
