@@ -553,13 +553,73 @@ def run_sweep(args, local_rank):
                 "dtype": "bf16", "data": "synthetic (seeded N(0,1), 3D RoPE)"}), flush=True)
 
 
+def run_train(args, local_rank):
+    """SURVEY 8f next #3 measured: one Stage-I training step (training.py:
+    the compensator / gate / RMSNorm / PE forward + backward against the
+    cached sparse branch, then the gradient-descent update) at the config-1
+    shape, one sample, synthetic target.  The sparse branch is computed once
+    through the op and cached (mechanism.py:536-549); that cost is reported
+    separately."""
+    import torch
+
+    import paper_2605_20659_b200 as P
+    from paper_2605_20659_b200 import training as T
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS["cfg1"]
+    q, k, v, x, params, pe, grid = make_inputs(cfg, 0, cfg["H"], dev)
+    L = grid.size
+    settings = P.ForwardSettings(P.SparseSettings.for_sparsity(cfg["block"], L, cfg["sparsity"]))
+    gen = torch.Generator(device=dev).manual_seed(7)
+    target = torch.randn(x.shape, generator=gen, device=dev).to(x.dtype)
+    sample = T.Stage1Sample(q=q, k=k, v=v, x=x, target=target)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    prepared = T.prepare([sample], grid, params, settings, pe)
+    t1.record()
+    torch.cuda.synchronize()
+    cache_ms = t0.elapsed_time(t1)
+    pe_dense = pe.dense(grid).float()
+    lr = 1e-3
+
+    def step():
+        loss, grads = T.loss_and_grads(prepared, params, settings, pe_dense)
+        with torch.no_grad():
+            for name in T.PARAM_NAMES:
+                getattr(params, name).sub_(lr * grads[name].to(getattr(params, name).dtype))
+        params.b_g = float(params.b_g) - lr * grads["b_g"]
+        return loss
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    losses = []
+    e0.record()
+    for _ in range(args.steps):
+        losses.append(step())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    line = {"metric": "Stage-I training step (compensator/gate/RMSNorm/PE forward+backward+update), ms",
+            "value": ms, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded inputs of config 1, random target)",
+            "config": {"workload": cfg["name"] + "_stage1", "samples": 1, "lr": lr},
+            "sparse_branch_cache_ms": cache_ms, "loss_first": losses[0], "loss_last": losses[-1],
+            "note": "per-step math is float32 cuBLAS GEMMs + torch elementwise (training.py); the loss is read "
+                    "back every step, as the reference trainer does"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep"], default="cfg3")
+    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep", "train"], default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rope-pass", action="store_true", help="skip timing the fused RoPE + pooling pre-pass")
@@ -585,6 +645,8 @@ def main():
             run_dit(args, rank, world, local_rank)
         elif args.config == "cfg2_sweep":
             run_sweep(args, local_rank)
+        elif args.config == "train":
+            run_train(args, local_rank)
         else:
             run_ours(args, cfg, rank, world, local_rank)
     finally:
