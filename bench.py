@@ -580,7 +580,7 @@ def run_train(args, local_rank):
     t1.record()
     torch.cuda.synchronize()
     cache_ms = t0.elapsed_time(t1)
-    pe_dense = pe.dense(grid).float()
+    pe_dense = T.pe_head_major(pe, grid, params.n_heads, params.d_h)
     lr = 1e-3
 
     def step():

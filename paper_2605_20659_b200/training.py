@@ -41,8 +41,8 @@ class Stage1Sample:
 
 @dataclass
 class _Prepared:
-    x: torch.Tensor          # [L, D] float32
-    target: torch.Tensor     # [L, D] float32
+    x: torch.Tensor          # [H, L, d] float32, head-major (contiguous for the per-head GEMMs)
+    target: torch.Tensor     # [H, L, d] float32, head-major
     o_sparse: torch.Tensor   # [H, L, d] float32 (constant during training)
 
 
@@ -70,8 +70,28 @@ def prepare(samples: Sequence[Stage1Sample], grid: GridShape, params: MechanismP
         if s.q.shape[0] != 1:
             raise ValueError("samples are single sequences (B = 1)")
         tr = forward(s.q, s.k, s.v, s.x, grid, params, settings, pe, trace=True)
-        out.append(_Prepared(x=s.x[0].float(), target=s.target[0].float(), o_sparse=tr.o_sparse[0].float()))
+        H, d = s.q.shape[1], s.q.shape[3]
+        out.append(_Prepared(x=_head_major(s.x[0].float(), H, d), target=_head_major(s.target[0].float(), H, d),
+                             o_sparse=tr.o_sparse[0].float().contiguous()))
     return out
+
+
+def _head_major(t: torch.Tensor, H: int, d: int) -> torch.Tensor:
+    """[L, H*d] -> contiguous [H, L, d]."""
+    return t.view(t.shape[0], H, d).transpose(0, 1).contiguous()
+
+
+def _at_b(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Per head a^T b for a [H, L, m], b [H, L, n] -> [H, m, n], the long L
+    reduction split into S segments (batched GEMMs, then a sum): cuBLAS picks
+    a small-tile, single-split kernel for m, n << L otherwise."""
+    H, L, m = a.shape
+    S = next((c for c in range(32, 1, -1) if L % c == 0 and (L // c) % 4 == 0), 1)
+    if S == 1:
+        return torch.bmm(a.transpose(1, 2), b)
+    a2 = a.reshape(H * S, L // S, m)
+    b2 = b.reshape(H * S, L // S, b.shape[2])
+    return torch.bmm(a2.transpose(1, 2), b2).view(H, S, m, b.shape[2]).sum(1)
 
 
 def _rms(o, scale, eps):
@@ -102,39 +122,47 @@ def loss_and_grads(prepared: Sequence[_Prepared], params: MechanismParams, setti
     gb = torch.zeros((), dtype=torch.float64, device=w_a.device)
     total = 0.0
     n = len(prepared)
+    w_g_h = w_g.view(H, d)
+    alpha_h = alpha.view(H, d)
     for s in prepared:
-        L, D = s.x.shape
-        x_hat = s.x + alpha[None, :] * pe_dense if settings.use_pe else s.x
-        g = torch.sigmoid(x_hat @ w_g + params.b_g)                          # [L]
-        xh = x_hat.view(L, H, d).permute(1, 0, 2)                            # [H, L, d]
+        _, L, _ = s.x.shape
+        # everything head-major [H, L, d]: contiguous operands for the batched
+        # GEMMs and vectorised elementwise kernels (no strided permutes)
+        xh = s.x + alpha_h[:, None, :] * pe_dense if settings.use_pe else s.x
+        g = torch.sigmoid(torch.einsum("hld,hd->l", xh, w_g_h) + params.b_g)  # [L]
         h1 = torch.sigmoid(torch.bmm(xh, w_a))                               # [H, L, r]
         o_lr = torch.sigmoid(torch.bmm(h1, w_b))                             # [H, L, d]
         y_lr, inv_lr, u_lr = _rms(o_lr, rms_lr, eps)
         y_sp, inv_sp, u_sp = _rms(s.o_sparse, rms_sp, eps)
-        out = (y_sp + g[None, :, None] * y_lr).permute(1, 0, 2).reshape(L, D)
-        diff = out - s.target
+        diff = torch.addcmul(y_sp, g[None, :, None], y_lr) - s.target
         total += float((diff.double() ** 2).mean()) / n
         if not want_grads:
             continue
-        gh = (2.0 * diff / (diff.numel() * n)).view(L, H, d).permute(1, 0, 2)  # [H, L, d]
+        gh = diff * (2.0 / (diff.numel() * n))                                # [H, L, d]
         grads["rms_sparse"] += (gh * u_sp).reshape(-1, d).sum(0)
         d_g = (gh * y_lr).sum((0, 2))                                         # [L]
         d_o_lr, d_rl = _rms_backward(gh * g[None, :, None], o_lr, inv_lr, u_lr, rms_lr)
         grads["rms_lowrank"] += d_rl
         d_z2 = d_o_lr * o_lr * (1.0 - o_lr)
-        grads["w_b"] += torch.bmm(h1.transpose(1, 2), d_z2)
+        grads["w_b"] += _at_b(h1, d_z2)
         d_z1 = torch.bmm(d_z2, w_b.transpose(1, 2)) * h1 * (1.0 - h1)
-        grads["w_a"] += torch.bmm(xh.transpose(1, 2), d_z1)
-        d_xhat = torch.bmm(d_z1, w_a.transpose(1, 2)).permute(1, 0, 2).reshape(L, D)
+        grads["w_a"] += _at_b(xh, d_z1)
+        d_xh = torch.bmm(d_z1, w_a.transpose(1, 2))                          # [H, L, d]
         d_zg = d_g * g * (1.0 - g)
-        grads["w_g"] += x_hat.t() @ d_zg
+        grads["w_g"] += torch.einsum("hld,l->hd", xh, d_zg).reshape(-1)
         gb += d_zg.double().sum()
-        d_xhat = d_xhat + torch.outer(d_zg, w_g)
         if settings.use_pe:
-            grads["alpha"] += (d_xhat * pe_dense).sum(0)
+            d_xh = d_xh + d_zg[None, :, None] * w_g_h[:, None, :]
+            grads["alpha"] += (d_xh * pe_dense).sum(1).reshape(-1)
     if want_grads:
         grads["b_g"] = float(gb)
     return total, grads
+
+
+def pe_head_major(pe: PETables, grid: GridShape, H: int, d: int) -> torch.Tensor:
+    """The dense 3D PE [L, H*d] as the head-major float32 [H, L, d] that
+    loss_and_grads takes."""
+    return _head_major(pe.dense(grid).float(), H, d)
 
 
 def train_stage1(samples: Sequence[Stage1Sample], grid: GridShape, params: MechanismParams,
@@ -149,7 +177,7 @@ def train_stage1(samples: Sequence[Stage1Sample], grid: GridShape, params: Mecha
     if not samples:
         raise ValueError("dataset must be non-empty")
     prepared = prepare(samples, grid, params, settings, pe)
-    pe_dense = pe.dense(grid).float() if settings.use_pe else None
+    pe_dense = pe_head_major(pe, grid, params.n_heads, params.d_h) if settings.use_pe else None
     losses = []
     for step in range(steps + 1):
         loss, grads = loss_and_grads(prepared, params, settings, pe_dense, want_grads=step < steps)

@@ -37,7 +37,7 @@ def test_stage1_grads_match_oracle():
     P, T, q, k, v, x, params, pe, grid, target, st = _setup()
     prep = T.prepare([T.Stage1Sample(q, k, v, x, target)], grid, params, st, pe)
     pe_dense = pe.dense(grid).float()
-    loss, grads = T.loss_and_grads(prep, params, st, pe_dense)
+    loss, grads = T.loss_and_grads(prep, params, st, T.pe_head_major(pe, grid, params.n_heads, params.d_h))
     torch.cuda.synchronize()
     H = params.n_heads
     p_np = {n: getattr(params, n).double().cpu().numpy() for n in T.PARAM_NAMES}
