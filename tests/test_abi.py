@@ -82,6 +82,21 @@ def test_abi_rejects_bad_arguments_without_a_gpu():
     assert st == -9
 
 
+def test_dit_ops_reject_bad_arguments_without_a_gpu():
+    """The config-4 caller helpers validate before launching."""
+    import paper_2605_20659_b200 as P
+
+    lib = P.lib()
+    # NULL input, D not a multiple of 8, D beyond 2048, heads not dividing D,
+    # a misaligned pointer
+    assert lib.ropeslr_dit_ln_modulate(None, 16, 16, ctypes.c_float(1e-6), 4, 64, 16, None) == -9
+    assert lib.ropeslr_dit_ln_modulate(16, 16, 16, ctypes.c_float(1e-6), 4, 60, 16, None) == -1
+    assert lib.ropeslr_dit_ln_modulate(16, 16, 16, ctypes.c_float(1e-6), 4, 4096, 16, None) == -1
+    assert lib.ropeslr_dit_rms_heads(16, None, ctypes.c_float(0.0), 4, 1536, 7, 1, 16, None) == -1
+    assert lib.ropeslr_dit_rms_heads(18, None, ctypes.c_float(0.0), 4, 1536, 12, 1, 16, None) == -3
+    assert lib.ropeslr_dit_gated_residual(16, 16, None, 4, 1536, None) == -9
+
+
 def test_settings_validation_mirrors_reference():
     import paper_2605_20659_b200 as P
 
