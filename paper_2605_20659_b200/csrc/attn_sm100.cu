@@ -661,16 +661,24 @@ struct Layout {
 };
 }  // namespace fx
 
-template <int BLK>
+// BLK = keys per tile (the S tile width); KB = block size (query rows of a
+// unit, keys of a selected block).  KB == BLK: one selected block per tile.
+// KB = 64 with BLK = 128 ("paired" block 64): a tile is two consecutive
+// selected blocks stacked in one 128-row K / V slot (the second masked out
+// when the count is odd), so block 64 runs the 128-key pipeline with half
+// the per-tile barrier round trips.
+template <int BLK, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_fixed_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                              const __grid_constant__ CUtensorMap tmV, const Params p) {
   using Lay = fx::Layout<BLK>;
   using Bx = fx::FBars<BLK>;
   static_assert(Bx::COUNT <= Lay::NBAR, "barrier count");
+  static_assert(KB == BLK || (KB == 64 && BLK == 128), "tile shapes");
   constexpr int KST = Lay::KST, VST = Lay::VST;
   constexpr int HB = BLK / 2;   // keys per warpgroup of a pair
   constexpr int KK = BLK / 16;  // K steps of the PV MMA
+  constexpr int TPB = BLK / KB;  // selected blocks per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (smem_u32(smem_raw) & 1023u) __trap();
@@ -703,11 +711,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_alloc(tmem_holder, 512);
     tmem_relinquish();
   }
-  if (BLK < M && warp >= 4 && warp < 8) {
+  if (KB < M && warp >= 4 && warp < 8) {
     const int t = threadIdx.x - 128;
     for (int half = 0; half < 2; ++half) {
-      uint4* z = reinterpret_cast<uint4*>(sQ + half * (M * 128) + BLK * 128);
-      for (int i = t; i < (M - BLK) * 128 / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
+      uint4* z = reinterpret_cast<uint4*>(sQ + half * (M * 128) + KB * 128);
+      for (int i = t; i < (M - KB) * 128 / 16; i += 128) z[i] = make_uint4(0, 0, 0, 0);
     }
     fence_proxy_async_smem();
   }
@@ -734,23 +742,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int64_t u = p.order ? p.order[pos] : pos;
           const int bh = static_cast<int>(u / p.nb);
           const int n = p.cnt[u];
+          const int nt = (n + TPB - 1) / TPB;
           const int32_t* irow = p.idx + u * p.kmax;
           if (is_k) {
             const int qb = static_cast<int>(u % p.nb);
             mbar_wait(&bars[Bx::Q_EMPTY], (uc & 1) ^ 1);
-            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * BLK * 128);
-            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * BLK, bh, pol_q);
-            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * BLK, bh, pol_q);
+            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * KB * 128);
+            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * KB, bh, pol_q);
+            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * KB, bh, pol_q);
           }
-          for (int j = 0; j < n; ++j, ++g) {
-            const int kb = irow[j];
+          for (int j = 0; j < nt; ++j, ++g) {
             const int s = g % st;
             const uint32_t ph = (g / st) & 1;
             uint8_t* dst = ring + s * Lay::KV_BYTES;
             mbar_wait(&bars[empty + s], ph ^ 1);
             mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
-            tma_load_3d_hint(dst, map, &bars[full + s], 0, kb * BLK, bh, pol_kv);
-            tma_load_3d_hint(dst + BLK * 128, map, &bars[full + s], 64, kb * BLK, bh, pol_kv);
+#pragma unroll
+            for (int b = 0; b < TPB; ++b) {
+              // an odd count's missing partner block: reload the first one
+              // (its columns are masked) so the byte count stays fixed
+              const int kb = irow[TPB * j + b < n ? TPB * j + b : TPB * j];
+              tma_load_3d_hint(dst + b * KB * 128, map, &bars[full + s], 0, kb * KB, bh, pol_kv);
+              tma_load_3d_hint(dst + BLK * 128 + b * KB * 128, map, &bars[full + s], 64, kb * KB, bh, pol_kv);
+            }
           }
         }
       }
@@ -767,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t g = 0, uc = 0;
       for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
         const int64_t u = p.order ? p.order[pos] : pos;
-        const int n = p.cnt[u];
+        const int n = (p.cnt[u] + TPB - 1) / TPB;  // tiles
         const uint32_t tQ = tmem + fx::Q_COL + (uc & 1) * (D / 2);
         mbar_wait(&bars[Bx::QT_FULL], uc & 1);
         tc_fence_after();
@@ -827,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t tS = lane_addr + pr * 128 + w * HB;  // this warpgroup's S columns; its P over their first half
     const uint32_t tOq = lane_addr + fx::O_COL + q * (D / 4);
-    const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
+    const bool rows_live = KB >= M || (warp & 3) * 32 < KB;
     // this thread's quarter of its Q row in the 128B-swizzled tile: d in
     // [32q, 32q + 32) = 16-byte chunks 4(q&1) .. 4(q&1)+3 of half q>>1
     const uint8_t* qrow = sQ + (q >> 1) * (M * 128) + row * 128;
@@ -841,7 +855,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t* irow = p.idx + u * p.kmax;
       mbar_wait(&bars[Bx::Q_FULL], uc & 1);
       const __nv_bfloat16* krow =
-          p.kmat + (static_cast<int64_t>(bh) * p.L + static_cast<int64_t>(irow[0]) * BLK) * D + q * 32;
+          p.kmat + (static_cast<int64_t>(bh) * p.L + static_cast<int64_t>(irow[0]) * KB) * D + q * 32;
       float dot = 0.f;
       uint32_t qw[16];
 #pragma unroll
@@ -877,9 +891,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t u = p.order ? p.order[pos] : pos;
       const int bh = static_cast<int>(u / p.nb);
       const int qb = static_cast<int>(u % p.nb);
-      const int n = p.cnt[u];
+      const int nblk = p.cnt[u];
+      const int n = (nblk + TPB - 1) / TPB;  // tiles
       const int32_t* irow = p.idx + u * p.kmax;
-      const int qrows = block_size(p.L, BLK, qb);
+      const int qrows = block_size(p.L, KB, qb);
       // ---- the unit's exponent reference m (see the header)
       named_bar_sync(2, 512);
       float m_ref;
@@ -895,12 +910,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars[Bx::S_FULL + pr], (t >> 1) & 1);
         tc_fence_after();
         if (rows_live) {
-          const int kreal = block_size(p.L, BLK, irow[j]);
+          // real keys in this warpgroup's half of the tile
+          int valid;
+          if (TPB == 1) {
+            valid = block_size(p.L, BLK, irow[j]) - w * HB;
+          } else {
+            const int jb = TPB * j + w;  // the selected block this half holds
+            valid = jb < nblk ? block_size(p.L, KB, irow[jb]) : 0;
+          }
           uint32_t sr[HB];
 #pragma unroll
           for (int c = 0; c < HB / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
           tmem_wait_ld();
-          const int valid = kreal - w * HB;
           if (valid < HB) {
 #pragma unroll
             for (int c = 0; c < HB; ++c)
@@ -948,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ss = (xs[row] + xs[128 + row]) + (xs[256 + row] + xs[384 + row]);
       const bool live = row < qrows;
       if (!live) continue;
-      const int64_t flat = static_cast<int64_t>(qb) * BLK + row;
+      const int64_t flat = static_cast<int64_t>(qb) * KB + row;
       const int64_t tok = p.perm ? p.perm[flat] : flat;
       const int b = bh / p.H, h = bh % p.H;
       const float inv = 1.f / sqrtf(ss / static_cast<float>(D) + p.eps);
@@ -1099,7 +1120,7 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
 }
 
 // The fixed-reference kernel, then the running-max kernel over its flagged units.
-template <int BLK>
+template <int BLK, int KB>
 static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
                         int* fallback, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
@@ -1110,9 +1131,9 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   if (cudaMemsetAsync(fallback, 0, (prm.num_units + 1) * sizeof(int), st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
   prm.kmat = static_cast<const __nv_bfloat16*>(k);
   CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, q, BH, s->L, BLK) || !make_map(&mk, k, BH, s->L, BLK) || !make_map(&mv, v, BH, s->L, BLK))
+  if (!make_map(&mq, q, BH, s->L, KB) || !make_map(&mk, k, BH, s->L, KB) || !make_map(&mv, v, BH, s->L, KB))
     return ROPESLR_ERR_LAUNCH;
-  auto kfn = sparse_attn_fixed_kernel<BLK>;
+  auto kfn = sparse_attn_fixed_kernel<BLK, KB>;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, fx::Layout<BLK>::ALLOC) != cudaSuccess)
     return ROPESLR_ERR_LAUNCH;
   const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
@@ -1126,7 +1147,7 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   fb.unit_flag = nullptr;
   fb.flag_count = nullptr;
   fb.flag_list = nullptr;
-  return launch_tc<BLK>(s, q, k, v, fb, st);
+  return launch_tc<KB>(s, q, k, v, fb, st);
 }
 
 static bool tc_eligible(const ropeslr_shape* s) {
@@ -1167,8 +1188,11 @@ static int resolve_impl(const ropeslr_shape* s, int impl) {
 static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                                  const tc::Params& prm, void* ws, cudaStream_t st) {
   int* fallback = static_cast<int*>(ws) + prm.num_units;
-  return s->block == 128 ? tc::launch_fixed<128>(s, q, k, v, prm, fallback, st)
-                         : tc::launch_fixed<64>(s, q, k, v, prm, fallback, st);
+  if (s->block == 128) return tc::launch_fixed<128, 128>(s, q, k, v, prm, fallback, st);
+  // block 64: two selected blocks per 128-key tile unless ROPESLR_PAIR64=0
+  const char* e = getenv("ROPESLR_PAIR64");
+  if (e != nullptr && e[0] == '0') return tc::launch_fixed<64, 64>(s, q, k, v, prm, fallback, st);
+  return tc::launch_fixed<128, 64>(s, q, k, v, prm, fallback, st);
 }
 
 // K2 flavour for the tcgen05 path: the fixed-reference kernel unless
