@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace ropeslr {
@@ -431,6 +433,18 @@ extern "C" size_t ropeslr_linear_workspace_bytes(const ropeslr_shape* s) {
   return static_cast<size_t>(BH * (lin_nchunks(s->L) + 1) * n) * sizeof(float);
 }
 
+namespace ropeslr {
+int linear_branch_tc(const ropeslr_shape* s, const void* q_lin, const void* k_lin, const void* v_lin,
+                     const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* partial, float* state,
+                     int nchunks, cudaStream_t st);
+// Fixed-order chunk reduction of the linear state (also used by linear_tc.cu).
+int linear_reduce(const float* partial, int nchunks, int n, float* state, int64_t BH, cudaStream_t st) {
+  dim3 g2(static_cast<unsigned>(ceil_div(n, 256)), static_cast<unsigned>(BH));
+  linear_reduce_kernel<<<g2, 256, 0, st>>>(partial, nchunks, n, state);
+  return cudaGetLastError() == cudaSuccess ? ROPESLR_OK : ROPESLR_ERR_LAUNCH;
+}
+}  // namespace ropeslr
+
 extern "C" int ropeslr_linear_branch(const ropeslr_shape* s, const void* q_lin, const void* k_lin, const void* v_lin,
                                      const float* rms_lowrank, float eps, void* y_lr, float* o_lr, void* ws,
                                      size_t ws_bytes, void* stream) {
@@ -447,6 +461,11 @@ extern "C" int ropeslr_linear_branch(const ropeslr_shape* s, const void* q_lin, 
   float* partial = static_cast<float*>(ws);
   float* state = partial + BH * nch * static_cast<int64_t>(n);
   cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
+  // bf16, d = 128: the tensor-core passes (linear_tc.cu)
+  const char* lin_env = getenv("ROPESLR_LINEAR");
+  if (s->dtype == ROPESLR_BF16 && d == 128 && !(lin_env != nullptr && lin_env[0] == 's') && aligned16(q_lin) &&
+      aligned16(k_lin) && aligned16(v_lin) && aligned16(y_lr))
+    return linear_branch_tc(s, q_lin, k_lin, v_lin, rms_lowrank, eps, y_lr, o_lr, partial, state, nch, stream_);
   size_t sm1 = sizeof(float) * 2 * 32 * d;
   size_t sm3 = sizeof(float) * (static_cast<size_t>(n) + kTok * (d + 1));
   dim3 g1(nch, static_cast<unsigned>(BH));

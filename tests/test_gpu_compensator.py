@@ -87,3 +87,34 @@ def test_lowrank_generic_d64_vs_oracle():
     for h in range(H):
         o_ref = R.lowrank_compensator(x_hat, params.w_a.double().cpu().numpy(), params.w_b.double().cpu().numpy(), h)
         G.assert_close(o_lr[0, h].cpu().numpy(), o_ref, "f32", f"d64 h{h} o_lr")
+
+
+@pytest.mark.parametrize("L_grid", [(2, 25, 50), (1, 8, 16)])
+def test_linear_branch_tensor_cores_vs_oracle(L_grid, monkeypatch):
+    """K3 linear mode (mechanism.py:33-36, 347-362) on the tensor cores
+    (linear_tc.cu: bf16, d = 128) against the float64 oracle, with a token
+    count that is ragged for both the 1024-token state chunks and the
+    128-token apply tiles, batch 2; and against the CUDA-core kernels."""
+    import paper_2605_20659_b200 as P
+
+    B, H, d = 2, 2, 128
+    L = L_grid[0] * L_grid[1] * L_grid[2]
+    x, params, pe, grid = _inputs(B, H, d, 64, L_grid, seed=11)
+    rng = np.random.default_rng(12)
+    lin = [torch.from_numpy(rng.standard_normal((B, H, L, d)) * 0.5).to(torch.bfloat16).cuda() for _ in range(3)]
+    st = P.ForwardSettings(P.SparseSettings(block=64, topk=1), compensator="linear")
+    outs = {}
+    for mode in ("tc", "simt"):
+        monkeypatch.setenv("ROPESLR_LINEAR", mode)
+        y_lr, o_lr, _ = P.compensator_branch(x, grid, params, st, pe, lin_proj=lin, want_o_lr=True)
+        torch.cuda.synchronize()
+        outs[mode] = (y_lr.float().cpu().numpy(), o_lr.cpu().numpy())
+    rms = params.rms_lowrank.double().cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            qh, kh, vh = (t[b, h].double().cpu().numpy() for t in lin)
+            o = R.linear_apply(qh, *R.linear_state(kh, vh))
+            y = o / np.sqrt((o ** 2).mean(-1, keepdims=True) + st.rms_eps) * rms
+            for mode in ("tc", "simt"):
+                G.assert_close(outs[mode][1][b, h], o, "bf16", f"o_lr {mode} b{b} h{h}")
+                G.assert_close(outs[mode][0][b, :, h], y, "bf16", f"y_lr {mode} b{b} h{h}")
