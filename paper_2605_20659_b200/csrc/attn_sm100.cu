@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmV);
     for (int i = 0; i < Bx::COUNT; ++i) {
       uint32_t count = 1;
-      if (i == Bx::P_FULL || i == Bx::P_FULL + 1) count = 256;
+      if (i == Bx::P_FULL || i == Bx::P_FULL + 1) count = 8;  // one arrival per warp of the pair
       if (i == Bx::O_EMPTY) count = 512;
       if (i == Bx::Q_EMPTY || i == Bx::QT_FULL) count = 16;  // every softmax warp: Q read / stored to TMEM
       mbar_init(&bars[i], count);
@@ -931,7 +931,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_st();
         }
         tc_fence_before();
-        mbar_arrive(&bars[Bx::P_FULL + pr]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[Bx::P_FULL + pr]);
       }
       g += n;
       // the next unit's Q goes to the other TMEM buffer now, so its first
@@ -1096,8 +1097,8 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
       usleep(100000);
       if (hbuf[0]) {
         usleep(500000);
-        fprintf(stderr, "WATCHDOG %llu waiters (S_FULL=%d P_FULL=%d PV_DONE=%d O_FULL=%d O_EMPTY=%d V_FULL=%d K_FULL=%d)\n",
-                hbuf[0], Bars<BLK>::S_FULL, Bars<BLK>::P_FULL, Bars<BLK>::PV_DONE, Bars<BLK>::O_FULL,
+        fprintf(stderr, "WATCHDOG %llu waiters (S_FULL=%d P_FULL=%d O_FULL=%d O_EMPTY=%d V_FULL=%d K_FULL=%d)\n",
+                hbuf[0], Bars<BLK>::S_FULL, Bars<BLK>::P_FULL, Bars<BLK>::O_FULL,
                 Bars<BLK>::O_EMPTY, Bars<BLK>::V_FULL, Bars<BLK>::K_FULL);
         for (unsigned long long k = 0; k < hbuf[0] && k < 30; ++k)
           fprintf(stderr, "  block %llu thread %llu barrier %llu parity %llu line %llu\n", hbuf[2 + k * 4],
