@@ -210,10 +210,10 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
  * additionally receives the raw sparse-branch output.  Workspace: the
  * CUDA-core path keeps o_sparse there when o_sparse is NULL.  The tcgen05
  * path keeps the per-key-block maxima of |k| there that its fixed exponent
- * reference needs (without a workspace it runs the running-max kernel), and,
- * with the environment variable ROPESLR_SCHEDULE=1, a longest-first schedule
- * of the (head, query block) units (for rows with different block counts
- * under the `keep` rule). */
+ * reference needs (without a workspace it runs the running-max kernel) and a
+ * longest-first schedule of the (head, query block) units, which balances
+ * rows with different block counts under the `keep` rule (environment
+ * variable ROPESLR_SCHEDULE=0 turns the schedule off). */
 int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
                          const int32_t* idx, int32_t kmax, const int32_t* cnt,
                          const int32_t* row_perm, const void* y_lr, const float* g_logit, float b_g,

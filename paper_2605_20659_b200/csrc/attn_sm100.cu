@@ -1337,13 +1337,12 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
   prm.eps = eps;
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.o_sparse = o_sparse;
-  // ROPESLR_SCHEDULE=1 and a workspace: the longest-first unit schedule.
-  // Off by default: measured on skewed `keep` inputs (1 to 397 blocks per
-  // row, 1/2/12 heads of the Wan shape, scripts/exp_keep.py) it changes
-  // nothing, because K2 is L2-bandwidth bound and CTAs that finish early
-  // hand their bandwidth to the rest.
+  // With a workspace: the longest-first unit schedule (ROPESLR_SCHEDULE=0
+  // turns it off).  On skewed `keep` inputs (1 to 397 blocks per row, 12
+  // heads of the Wan shape, scripts/exp_keep.py) it is 19-20% faster with the
+  // fixed-reference kernel; on uniform top-k counts it is neutral.
   const char* sched_env = getenv("ROPESLR_SCHEDULE");
-  const bool sched = sched_env != nullptr && sched_env[0] == '1';
+  const bool sched = !(sched_env != nullptr && sched_env[0] == '0');
   if (sched && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl) && prm.nb <= kMaxScheduledBlocks) {
     const int64_t G = prm.num_units < num_sms() ? prm.num_units : num_sms();
     int32_t* order = static_cast<int32_t*>(ws);
