@@ -1268,6 +1268,23 @@ extern "C" int ropeslr_sparse_attention(const ropeslr_shape* s, const void* q, c
 namespace ropeslr {
 constexpr int kMaxScheduledBlocks = 8192;  // larger nb: identity order (the O(nb^2) ranking gets slow)
 static int64_t num_units_of(const ropeslr_shape* s) { return s->B * s->H * ceil_div(s->L, s->block); }
+
+// The longest-first unit schedule into the workspace's first num_units
+// int32 (ROPESLR_SCHEDULE=0 turns it off).  On skewed `keep` inputs (1 to
+// 397 blocks per row, 12 heads of the Wan shape, scripts/exp_keep.py) it is
+// 19-20% faster with the fixed-reference kernel; on uniform top-k counts it
+// is neutral.
+static int schedule_units(const ropeslr_shape* s, const int32_t* cnt, tc::Params& prm, void* ws, cudaStream_t cs) {
+  const char* sched_env = getenv("ROPESLR_SCHEDULE");
+  if ((sched_env != nullptr && sched_env[0] == '0') || prm.nb > kMaxScheduledBlocks) return ROPESLR_OK;
+  const int64_t G = prm.num_units < num_sms() ? prm.num_units : num_sms();
+  int32_t* order = static_cast<int32_t*>(ws);
+  tc::schedule_units_kernel<<<static_cast<unsigned>(s->B * s->H), 512, prm.nb * sizeof(int32_t), cs>>>(
+      cnt, prm.nb, prm.num_units, static_cast<int>(G), order);
+  if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  prm.order = order;
+  return ROPESLR_OK;
+}
 }  // namespace ropeslr
 
 extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t impl) {
@@ -1300,8 +1317,10 @@ int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.out_H = out_H;
   prm.out_h0 = out_h0;
-  if (use_fixed_reference() && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, ROPESLR_IMPL_TCGEN05))
-    return launch_fixed_dispatch(s, q, k, v, prm, ws, stream);
+  if (ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, ROPESLR_IMPL_TCGEN05)) {
+    if (int e = schedule_units(s, cnt, prm, ws, stream)) return e;
+    if (use_fixed_reference()) return launch_fixed_dispatch(s, q, k, v, prm, ws, stream);
+  }
   return launch_tc_dispatch(s, q, k, v, prm, stream);
 }
 bool attend_tc_eligible(const ropeslr_shape* s) { return tc::tc_eligible(s); }
@@ -1337,19 +1356,8 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
   prm.eps = eps;
   prm.out = static_cast<__nv_bfloat16*>(out);
   prm.o_sparse = o_sparse;
-  // With a workspace: the longest-first unit schedule (ROPESLR_SCHEDULE=0
-  // turns it off).  On skewed `keep` inputs (1 to 397 blocks per row, 12
-  // heads of the Wan shape, scripts/exp_keep.py) it is 19-20% faster with the
-  // fixed-reference kernel; on uniform top-k counts it is neutral.
-  const char* sched_env = getenv("ROPESLR_SCHEDULE");
-  const bool sched = !(sched_env != nullptr && sched_env[0] == '0');
-  if (sched && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl) && prm.nb <= kMaxScheduledBlocks) {
-    const int64_t G = prm.num_units < num_sms() ? prm.num_units : num_sms();
-    int32_t* order = static_cast<int32_t*>(ws);
-    tc::schedule_units_kernel<<<static_cast<unsigned>(s->B * s->H), 512, prm.nb * sizeof(int32_t), cs>>>(
-        cnt, prm.nb, prm.num_units, static_cast<int>(G), order);
-    if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-    prm.order = order;
+  if (ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl)) {
+    if (int e = schedule_units(s, cnt, prm, ws, cs)) return e;
   }
   if (use_fixed_reference() && ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl))
     return launch_fixed_dispatch(s, q, k, v, prm, ws, cs);
