@@ -244,6 +244,98 @@ __global__ void __launch_bounds__(128) block_scores_dmma_kernel(const double* __
   }
 }
 
+// The same DMMA tiling with the pooled rows staged row-major by cp.async in
+// a 3-stage ring of 16-wide k-chunks (d % 16 == 0), so the loads of chunk
+// c + 2 overlap the DMMAs of chunk c.  Row pitch 20 doubles (160 B): the
+// 8 rows x 4 k of one fragment load fall into two 128-byte wavefronts, the
+// minimum for 256 bytes.  Same products and per-k accumulation order as
+// block_scores_dmma_kernel.
+namespace sc {
+#ifndef ROPESLR_SC_ST
+#define ROPESLR_SC_ST 2
+#endif
+#ifndef ROPESLR_SC_KC
+#define ROPESLR_SC_KC 16
+#endif
+constexpr int KC = ROPESLR_SC_KC, PITCH = KC + 4, ST = ROPESLR_SC_ST, TILE = 64;
+constexpr int STAGE_DOUBLES = 2 * TILE * PITCH;  // A then B
+__device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+}  // namespace sc
+
+__global__ void __launch_bounds__(128) block_scores_dmma_pipe_kernel(const double* __restrict__ pooled,
+                                                                     double* __restrict__ scores, int nb, int d,
+                                                                     int64_t BH, double sqrt_d) {
+  using namespace sc;
+  extern __shared__ __align__(16) double sbuf[];  // ST stages of [A 64 x PITCH | B 64 x PITCH]
+  const int64_t bh = blockIdx.z;
+  const double* pq = pooled + bh * nb * d;
+  const double* pk = pooled + (BH + bh) * nb * d;
+  const int i0 = blockIdx.y * TILE, j0 = blockIdx.x * TILE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nchunks = d / KC;
+  auto load = [&](int c) {
+    double* st = sbuf + (c % ST) * STAGE_DOUBLES;
+    // 64 rows x KC/2 16-byte pieces per operand
+    constexpr int PR = KC / 2, PIECES = 2 * TILE * PR;
+#pragma unroll
+    for (int it = 0; it < PIECES / 128; ++it) {
+      const int e = tid + it * 128;
+      const int op = e / (TILE * PR), r = (e / PR) % TILE, piece = e % PR;
+      const int grow = (op == 0 ? i0 : j0) + r;
+      const bool valid = grow < nb;
+      const double* src = (op == 0 ? pq : pk) + static_cast<int64_t>(valid ? grow : 0) * d + c * KC + piece * 2;
+      cp16(st + op * TILE * PITCH + r * PITCH + piece * 2, src, valid);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int c = 0; c < ST - 1 && c < nchunks; ++c) load(c);
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + ST - 2 < nchunks - 1)
+      asm volatile("cp.async.wait_group %0;" ::"n"(ST - 2) : "memory");
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // chunk c landed for every thread; chunk c - 1's stage is free
+    if (c + ST - 1 < nchunks) load(c + ST - 1);
+    const double* As = sbuf + (c % ST) * STAGE_DOUBLES;
+    const double* Bs = As + TILE * PITCH;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) a[m] = As[(wr + 8 * m + g) * PITCH + kk + t4];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) b[n] = Bs[(wc + 8 * n + g) * PITCH + kk + t4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n], a[m], b[n]);
+    }
+  }
+  double* out = scores + bh * nb * nb;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int gi = i0 + wr + 8 * m + g;
+    if (gi >= nb) continue;
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gj = j0 + wc + 8 * n + 2 * t4 + e;
+        if (gj < nb) out[static_cast<int64_t>(gi) * nb + gj] = acc[m][n][e] / sqrt_d;
+      }
+  }
+}
+
 // Order-preserving map double -> uint64, inverted so that an ascending sort
 // yields descending scores.  +0 and -0 compare equal in the reference's
 // softmax, so -0 is folded onto +0 to keep the lower-index tie rule.
@@ -553,7 +645,17 @@ static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_param
     const char* e = getenv("ROPESLR_SCORES");
     if (e != nullptr && e[0] == 'f')
       block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
-    else
+    else if (d % sc::KC == 0 && !(e != nullptr && e[0] == 'd')) {  // ROPESLR_SCORES=dmma: the unpipelined kernel
+      static bool attr = false;  // opt in above 48 KiB of dynamic shared memory once
+      if (!attr) {
+        if (cudaFuncSetAttribute(block_scores_dmma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 sc::ST * sc::STAGE_DOUBLES * static_cast<int>(sizeof(double))) != cudaSuccess)
+          return ROPESLR_ERR_LAUNCH;
+        attr = true;
+      }
+      block_scores_dmma_pipe_kernel<<<grid, 128, sc::ST * sc::STAGE_DOUBLES * sizeof(double), st>>>(
+          pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
+    } else
       block_scores_dmma_kernel<<<grid, 128, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
     if (launch_status()) return ROPESLR_ERR_LAUNCH;
   }
