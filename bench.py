@@ -608,8 +608,8 @@ def run_train(args, local_rank):
             "data": "synthetic (seeded inputs of config 1, random target)",
             "config": {"workload": cfg["name"] + "_stage1", "samples": 1, "lr": lr},
             "sparse_branch_cache_ms": cache_ms, "loss_first": losses[0], "loss_last": losses[-1],
-            "note": "per-step math is float32 cuBLAS GEMMs + torch elementwise (training.py); the loss is read "
-                    "back every step, as the reference trainer does"}
+            "note": "per-step math is float32 cuBLAS GEMMs + the fused row kernels of csrc/stage1.cu (training.py); "
+                    "the loss is read back every step, as the reference trainer does"}
     print(json.dumps(line), flush=True)
 
 

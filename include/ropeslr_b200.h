@@ -273,6 +273,36 @@ int ropeslr_dit_rms_heads(const void* x, const void* weight, float eps, int64_t 
                           int32_t head_major, void* out, void* stream);
 int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_t N, int32_t D, void* stream);
 
+/* ------------------------- Stage-I training (training.py; mechanism.py:426-488, 519-614)
+ * The per-row chains of the fused forward / backward around the float32
+ * GEMMs, on head-major float32 rows [H, L, d] (d in {32, 64, 128, 256}):
+ *   pre:      xh = x + alpha_h * pe (pe NULL: no PE), gpart[h, l] = xh . w_g_h,
+ *             g[l] = sigmoid(sum_h gpart + b_g)
+ *   rows:     z2 (= H1 W_B) in, d z2 out in place; dgpart[h, l] = d loss / d g
+ *             per row; red[blocks][2][d] partial d rms_sparse / d rms_lowrank;
+ *             loss_part[blocks] = partial sum of diff^2 (float64);
+ *             gscale = 2 / (H * L * d * samples)
+ *   gate_bwd: dzg[l] = (sum_h dgpart) g (1 - g); bg_part[ceil(L/256)] its sums
+ *   dsig:     t *= h1 * (1 - h1)  (n floats, 16-byte aligned)
+ *   xgrad:    red[H][blocks][2][d] partial d alpha (needs pe; dxh = d xh) / d w_g
+ *   reduce:   out[o][j][c] += sum over parts, in part order (deterministic)
+ * *_blocks give the partial counts (grid sizes) of rows / xgrad. */
+int ropeslr_stage1_supported(int64_t d);
+int ropeslr_stage1_rows_blocks(int64_t H, int64_t L);
+int ropeslr_stage1_xgrad_blocks(int64_t H, int64_t L);
+int ropeslr_stage1_pre(int64_t H, int64_t L, int64_t d, const float* x, const float* pe, const float* alpha,
+                       const float* w_g, float b_g, float* xh, float* gpart, float* g, void* stream);
+int ropeslr_stage1_rows(int64_t H, int64_t L, int64_t d, float* z2, const float* o_sp, const float* target,
+                        const float* g, const float* rms_sp, const float* rms_lr, float eps, float gscale,
+                        float* dgpart, float* red, double* loss_part, void* stream);
+int ropeslr_stage1_gate_bwd(int64_t H, int64_t L, const float* dgpart, const float* g, float* dzg, double* bg_part,
+                            void* stream);
+int ropeslr_stage1_dsig(float* t, const float* h1, int64_t n, void* stream);
+int ropeslr_stage1_xgrad(int64_t H, int64_t L, int64_t d, const float* dxh, const float* xh, const float* pe,
+                         const float* dzg, const float* w_g, float* red, void* stream);
+int ropeslr_stage1_reduce(const float* parts, int32_t outer, int32_t nparts, int32_t groups, int32_t width, float* out,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

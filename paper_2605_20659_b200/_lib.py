@@ -79,6 +79,16 @@ _SIGNATURES = {
     "ropeslr_dit_ln_modulate": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_rms_heads": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "ropeslr_dit_gated_residual": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "ropeslr_stage1_supported": (c_i32, [c_i64]),
+    "ropeslr_stage1_rows_blocks": (c_i32, [c_i64, c_i64]),
+    "ropeslr_stage1_xgrad_blocks": (c_i32, [c_i64, c_i64]),
+    "ropeslr_stage1_pre": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp, c_vp, c_vp, c_vp]),
+    "ropeslr_stage1_rows": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f32, c_f32, c_vp,
+                                    c_vp, c_vp, c_vp]),
+    "ropeslr_stage1_gate_bwd": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ropeslr_stage1_dsig": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
+    "ropeslr_stage1_xgrad": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ropeslr_stage1_reduce": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "ropeslr_rope_pool_workspace_bytes": (c_sz, [P(RopeArgs)]),
     "ropeslr_rope_pool": (c_i32, [P(Shape), P(RopeArgs), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_forward_host_workspace_bytes": (c_sz, [P(HostForward)]),

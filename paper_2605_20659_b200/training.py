@@ -21,6 +21,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 import torch
 
+from . import _lib
 from .mechanism import ForwardSettings, MechanismParams, PETables, forward
 from .rope3d import GridShape
 
@@ -112,7 +113,78 @@ def _rms_backward(d_y, o, inv, u, scale):
 def loss_and_grads(prepared: Sequence[_Prepared], params: MechanismParams, settings: ForwardSettings,
                    pe_dense: Optional[torch.Tensor], want_grads: bool = True):
     """mechanism._loss_and_grads (mechanism.py:552-565) over the prepared
-    samples; returns (loss, {name: gradient}) with float32 gradients."""
+    samples; returns (loss, {name: gradient}) with float32 gradients.
+
+    The per-row chains run as the fused kernels of csrc/stage1.cu between
+    the float32 GEMMs (head dims 32 / 64 / 128 / 256); other head dims use
+    the same math composed from torch ops (_loss_and_grads_composed)."""
+    d = params.d_h
+    if want_grads and prepared and prepared[0].x.is_cuda and _lib.lib().ropeslr_stage1_supported(d):
+        return _loss_and_grads_fused(prepared, params, settings, pe_dense)
+    return _loss_and_grads_composed(prepared, params, settings, pe_dense, want_grads)
+
+
+def _loss_and_grads_fused(prepared, params, settings, pe_dense):
+    eps = settings.rms_eps
+    H, d, r = params.n_heads, params.d_h, params.rank
+    dev = prepared[0].x.device
+    st = torch.cuda.current_stream(dev).cuda_stream
+    lib = _lib.lib()
+    w_a, w_b = params.w_a.float().contiguous(), params.w_b.float().contiguous()
+    alpha, w_g = params.alpha.float().contiguous(), params.w_g.float().contiguous()
+    rms_sp, rms_lr = params.rms_sparse.float().contiguous(), params.rms_lowrank.float().contiguous()
+    grads = {n: torch.zeros_like(getattr(params, n), dtype=torch.float32) for n in PARAM_NAMES}
+    n = len(prepared)
+    use_pe = settings.use_pe
+    acc = torch.zeros(2, dtype=torch.float64, device=dev)  # loss, d b_g
+    rms_acc = torch.zeros((2, d), dtype=torch.float32, device=dev)
+    x_acc = torch.zeros((H, 2, d), dtype=torch.float32, device=dev)
+    for s in prepared:
+        _, L, _ = s.x.shape
+        xh = torch.empty_like(s.x)
+        gpart = torch.empty((H, L), dtype=torch.float32, device=dev)
+        g = torch.empty((L,), dtype=torch.float32, device=dev)
+        pe_ptr = pe_dense.data_ptr() if use_pe else None
+        _lib.call("ropeslr_stage1_pre", H, L, d, s.x.data_ptr(), pe_ptr, alpha.data_ptr(), w_g.data_ptr(),
+                  float(params.b_g), xh.data_ptr(), gpart.data_ptr(), g.data_ptr(), st)
+        h1 = torch.sigmoid_(torch.bmm(xh, w_a))                      # [H, L, r]
+        dz2 = torch.bmm(h1, w_b)                                      # z2 in, d z2 out (in place)
+        nb_rows = lib.ropeslr_stage1_rows_blocks(H, L)
+        red = torch.empty((nb_rows, 2, d), dtype=torch.float32, device=dev)
+        loss_part = torch.empty((nb_rows,), dtype=torch.float64, device=dev)
+        dgpart = torch.empty((H, L), dtype=torch.float32, device=dev)
+        _lib.call("ropeslr_stage1_rows", H, L, d, dz2.data_ptr(), s.o_sparse.data_ptr(), s.target.data_ptr(),
+                  g.data_ptr(), rms_sp.data_ptr(), rms_lr.data_ptr(), float(eps), 2.0 / (H * L * d * n),
+                  dgpart.data_ptr(), red.data_ptr(), loss_part.data_ptr(), st)
+        _lib.call("ropeslr_stage1_reduce", red.data_ptr(), 1, nb_rows, 2, d, rms_acc.data_ptr(), st)
+        dzg = torch.empty((L,), dtype=torch.float32, device=dev)
+        bg_part = torch.empty((-(-L // 256),), dtype=torch.float64, device=dev)
+        _lib.call("ropeslr_stage1_gate_bwd", H, L, dgpart.data_ptr(), g.data_ptr(), dzg.data_ptr(),
+                  bg_part.data_ptr(), st)
+        acc[0] += loss_part.sum() / (H * L * d * n)
+        acc[1] += bg_part.sum()
+        grads["w_b"] += _at_b(h1, dz2)
+        dz1 = torch.bmm(dz2, w_b.transpose(1, 2))                     # [H, L, r]
+        _lib.call("ropeslr_stage1_dsig", dz1.data_ptr(), h1.data_ptr(), dz1.numel(), st)
+        grads["w_a"] += _at_b(xh, dz1)
+        dxh = torch.bmm(dz1, w_a.transpose(1, 2)) if use_pe else xh   # [H, L, d] (read only with PE)
+        nb_x = lib.ropeslr_stage1_xgrad_blocks(H, L)
+        xred = torch.empty((H, nb_x, 2, d), dtype=torch.float32, device=dev)
+        _lib.call("ropeslr_stage1_xgrad", H, L, d, dxh.data_ptr(), xh.data_ptr(), pe_ptr, dzg.data_ptr(),
+                  w_g.data_ptr(), xred.data_ptr(), st)
+        _lib.call("ropeslr_stage1_reduce", xred.data_ptr(), H, nb_x, 2, d, x_acc.data_ptr(), st)
+    grads["rms_sparse"] += rms_acc[0]
+    grads["rms_lowrank"] += rms_acc[1]
+    if use_pe:
+        grads["alpha"] += x_acc[:, 0].reshape(-1)
+    grads["w_g"] += x_acc[:, 1].reshape(-1)
+    loss, gb = acc.tolist()  # the one host read of the step (the reference trainer reads the loss too)
+    grads["b_g"] = float(gb)
+    return float(loss), grads
+
+
+def _loss_and_grads_composed(prepared: Sequence[_Prepared], params: MechanismParams, settings: ForwardSettings,
+                             pe_dense: Optional[torch.Tensor], want_grads: bool = True):
     eps = settings.rms_eps
     H, d, r = params.n_heads, params.d_h, params.rank
     w_a, w_b = params.w_a.float(), params.w_b.float()

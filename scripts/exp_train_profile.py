@@ -21,5 +21,5 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
 rows = sorted(((e.key, e.device_time_total / 1e3, e.count) for e in prof.key_averages() if e.device_time_total > 0),
               key=lambda r: -r[1])
 print(f"total {sum(r[1] for r in rows):.2f} ms")
-for key, ms, n in rows[:25]:
+for key, ms, n in rows[:int(sys.argv[1]) if len(sys.argv) > 1 else 25]:
     print(f"{ms:7.3f} ms {n:4d}x {key[:100]}")

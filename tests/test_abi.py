@@ -174,3 +174,19 @@ def test_flops_model():
     assert flops.c_full(1, 24, 118800, 128) == pytest.approx(1.734e14, rel=1e-3)
     assert flops.c_lowrank(1, 24, 118800, 128, 64) == pytest.approx(9.34e10, rel=1e-3)
     assert flops.overhead_eta(118800, 0.9, 64) == pytest.approx(5.43e-3, rel=1e-3)
+
+
+def test_stage1_ops_reject_bad_arguments_without_a_gpu():
+    """The Stage-I row kernels validate before launching (no device needed)."""
+    import paper_2605_20659_b200 as P
+
+    lib = P.lib()
+    assert [lib.ropeslr_stage1_supported(d) for d in (32, 48, 64, 128, 256, 512)] == [1, 0, 1, 1, 1, 0]
+    f = ctypes.c_float
+    # unsupported head dim, NULL output, PE without alpha
+    assert lib.ropeslr_stage1_pre(2, 8, 48, 16, None, None, 16, f(0.0), 16, 16, 16, None) == -1
+    assert lib.ropeslr_stage1_pre(2, 8, 64, 16, None, None, 16, f(0.0), None, 16, 16, None) == -9
+    assert lib.ropeslr_stage1_pre(2, 8, 64, 16, 16, None, 16, f(0.0), 16, 16, 16, None) == -9
+    assert lib.ropeslr_stage1_rows(2, 0, 64, 16, 16, 16, 16, 16, 16, f(1e-6), f(1.0), 16, 16, 16, None) == -1
+    assert lib.ropeslr_stage1_dsig(18, 16, 8, None) == -3
+    assert lib.ropeslr_stage1_reduce(16, 1, 0, 2, 64, 16, None) == -1

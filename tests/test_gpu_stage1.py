@@ -33,11 +33,13 @@ def _setup(dtype=torch.float32, seed=2):
     return P, T, q, k, v, x, params, pe, grid, target, st
 
 
-def test_stage1_grads_match_oracle():
+@pytest.mark.parametrize("path", ["fused", "composed"])
+def test_stage1_grads_match_oracle(path):
     P, T, q, k, v, x, params, pe, grid, target, st = _setup()
     prep = T.prepare([T.Stage1Sample(q, k, v, x, target)], grid, params, st, pe)
     pe_dense = pe.dense(grid).float()
-    loss, grads = T.loss_and_grads(prep, params, st, T.pe_head_major(pe, grid, params.n_heads, params.d_h))
+    fn = T.loss_and_grads if path == "fused" else T._loss_and_grads_composed
+    loss, grads = fn(prep, params, st, T.pe_head_major(pe, grid, params.n_heads, params.d_h))
     torch.cuda.synchronize()
     H = params.n_heads
     p_np = {n: getattr(params, n).double().cpu().numpy() for n in T.PARAM_NAMES}
@@ -59,3 +61,32 @@ def test_stage1_training_reduces_loss():
     res = T.train_stage1([T.Stage1Sample(q, k, v, x, target)], grid, params, st, pe, lr=0.5, steps=5)
     assert not res.diverged
     assert res.final_loss < res.initial_loss
+
+
+@pytest.mark.parametrize("use_pe", [True, False])
+def test_stage1_fused_equals_composed_d128(use_pe):
+    """The fused row kernels (csrc/stage1.cu, 4 values per lane at d = 128,
+    the bench shape) against the torch composition of the same math, two
+    samples (gradients accumulate over samples)."""
+    import paper_2605_20659_b200 as P
+    from paper_2605_20659_b200 import training as T
+
+    grid_s, split = (2, 6, 20), (16, 56, 56)
+    H, d, r = 3, 128, 32
+    q, k, v, x, params, pe, grid = G.make_full_inputs(grid_s, H, d, split, r, seed=6, dtype=torch.float32)
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    samples = [T.Stage1Sample(q, k, v, x, torch.randn((1, grid.size, H * d), generator=gen, device="cuda") * 0.5)
+               for _ in range(2)]
+    st = P.ForwardSettings(P.SparseSettings(block=64, topk=2), use_pe=use_pe)
+    prep = T.prepare(samples, grid, params, st, pe)
+    pe_hm = T.pe_head_major(pe, grid, H, d) if use_pe else None
+    loss_f, gf = T.loss_and_grads(prep, params, st, pe_hm)
+    loss_c, gc = T._loss_and_grads_composed(prep, params, st, pe_hm)
+    assert abs(loss_f - loss_c) <= 1e-6 * abs(loss_c)
+    for name in T.PARAM_NAMES:
+        if name == "alpha" and not use_pe:
+            assert torch.count_nonzero(gf[name]) == 0
+            continue
+        scale = float(gc[name].abs().max()) or 1.0
+        assert float((gf[name] - gc[name]).abs().max()) <= 2e-5 * scale, name
+    assert abs(gf["b_g"] - gc["b_g"]) <= 2e-5 * max(abs(gc["b_g"]), 1e-9)
