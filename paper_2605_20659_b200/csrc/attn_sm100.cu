@@ -132,7 +132,8 @@ struct Params {
   int out_H;   // heads per token row of out / y_lr (>= H when a head chunk writes into a wider row)
   int out_h0;  // first head of this call inside that row
   int kv_evict_last;
-  int debug_mode;  // 0 normal; 1 no softmax math; 2 every K/V load hits block 0; 3 no K/V TMA
+  int debug_mode;  // measurement only: 0 normal; 2 every K/V load reads block 0; 3 no K/V TMA;
+                   // 4 no MMAs (fixed-reference kernel)
   long long* trace;  // TRACE
 };
 
@@ -756,12 +757,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (g / st) & 1;
             uint8_t* dst = ring + s * Lay::KV_BYTES;
             mbar_wait(&bars[empty + s], ph ^ 1);
+            if (p.debug_mode == 3) {  // measurement only: no K/V bytes at all
+              mbar_arrive(&bars[full + s]);
+              continue;
+            }
             mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
 #pragma unroll
             for (int b = 0; b < TPB; ++b) {
               // an odd count's missing partner block: reload the first one
               // (its columns are masked) so the byte count stays fixed
-              const int kb = irow[TPB * j + b < n ? TPB * j + b : TPB * j];
+              const int kb = p.debug_mode == 2 ? 0 : irow[TPB * j + b < n ? TPB * j + b : TPB * j];
               tma_load_3d_hint(dst + b * KB * 128, map, &bars[full + s], 0, kb * KB, bh, pol_kv);
               tma_load_3d_hint(dst + BLK * 128 + b * KB * 128, map, &bars[full + s], 64, kb * KB, bh, pol_kv);
             }
@@ -796,11 +801,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (leader) {
               const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+              if (p.debug_mode != 4) {  // mode 4 (measurement only): no MMAs, same barriers
 #pragma unroll
-              for (int kk = 0; kk < KK; ++kk) {
-                const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
-                const uint32_t a = tmem + pr * 128 + (kk / (KK / 2)) * HB + (kk % (KK / 2)) * 8;
-                mma_bf16_ts(tmem + fx::O_COL, a, db, idesc_pv, (j > 2 || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < KK; ++kk) {
+                  const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
+                  const uint32_t a = tmem + pr * 128 + (kk / (KK / 2)) * HB + (kk % (KK / 2)) * 8;
+                  mma_bf16_ts(tmem + fx::O_COL, a, db, idesc_pv, (j > 2 || kk > 0) ? 1u : 0u);
+                }
               }
               mma_commit(&bars[Bx::V_EMPTY + s]);
             }
@@ -814,11 +821,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (leader) {
               const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
+              if (p.debug_mode != 4) {
 #pragma unroll
-              for (int kk = 0; kk < D / 16; ++kk) {
-                // A = Q from TMEM (TS-MMA): only K is read from shared memory
-                const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
-                mma_bf16_ts(tmem + pr * 128, tQ + kk * 8, db, idesc_qk, kk > 0 ? 1u : 0u);
+                for (int kk = 0; kk < D / 16; ++kk) {
+                  // A = Q from TMEM (TS-MMA): only K is read from shared memory
+                  const uint64_t db = dK + static_cast<uint64_t>(((kk >> 2) * (BLK * 128) + (kk & 3) * 32) >> 4);
+                  mma_bf16_ts(tmem + pr * 128, tQ + kk * 8, db, idesc_qk, kk > 0 ? 1u : 0u);
+                }
               }
               mma_commit(&bars[Bx::K_EMPTY + s]);
               mma_commit(&bars[Bx::S_FULL + pr]);
@@ -1140,6 +1149,7 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
   kfn<<<static_cast<unsigned>(grid), kThreads, fx::Layout<BLK>::ALLOC, st>>>(mq, mk, mv, prm);
   if (int e = launch_status()) return e;
+  if (prm.debug_mode >= 2) return ROPESLR_OK;  // measurement modes: the fixed kernel alone
   // the running-max kernel over the flagged units (usually none: its CTAs
   // read a zero count and retire)
   Params fb = prm;
