@@ -47,6 +47,13 @@
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 
+// -DROPESLR_K2_MEASURE=1 (scripts/build_variant.sh) compiles the
+// measurement switches into the fixed-reference kernel; the product build
+// leaves them out (their branches cost 1.6% at config 3).
+#ifndef ROPESLR_K2_MEASURE
+#define ROPESLR_K2_MEASURE 0
+#endif
+
 namespace ropeslr {
 
 int launch_sparse_attention_simt(const ropeslr_shape* s, const void* q, const void* k, const void* v,
@@ -133,7 +140,7 @@ struct Params {
   int out_h0;  // first head of this call inside that row
   int kv_evict_last;
   int debug_mode;  // measurement only: 0 normal; 2 every K/V load reads block 0; 3 no K/V TMA;
-                   // 4 no MMAs (fixed-reference kernel)
+                   // 4 no MMAs (fixed-reference kernel: only in a build with -DROPESLR_K2_MEASURE=1)
   long long* trace;  // TRACE
 };
 
@@ -757,16 +764,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (g / st) & 1;
             uint8_t* dst = ring + s * Lay::KV_BYTES;
             mbar_wait(&bars[empty + s], ph ^ 1);
-            if (p.debug_mode == 3) {  // measurement only: no K/V bytes at all
+#if ROPESLR_K2_MEASURE
+            if (p.debug_mode == 3) {  // measurement build only: no K/V bytes at all
               mbar_arrive(&bars[full + s]);
               continue;
             }
+#endif
             mbar_arrive_expect_tx(&bars[full + s], Lay::KV_BYTES);
 #pragma unroll
             for (int b = 0; b < TPB; ++b) {
               // an odd count's missing partner block: reload the first one
               // (its columns are masked) so the byte count stays fixed
+#if ROPESLR_K2_MEASURE
               const int kb = p.debug_mode == 2 ? 0 : irow[TPB * j + b < n ? TPB * j + b : TPB * j];
+#else
+              const int kb = irow[TPB * j + b < n ? TPB * j + b : TPB * j];
+#endif
               tma_load_3d_hint(dst + b * KB * 128, map, &bars[full + s], 0, kb * KB, bh, pol_kv);
               tma_load_3d_hint(dst + BLK * 128 + b * KB * 128, map, &bars[full + s], 64, kb * KB, bh, pol_kv);
             }
@@ -801,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (leader) {
               const uint64_t dV = dV0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
-              if (p.debug_mode != 4) {  // mode 4 (measurement only): no MMAs, same barriers
+              if (!ROPESLR_K2_MEASURE || p.debug_mode != 4) {  // mode 4 (measurement build): no MMAs
 #pragma unroll
                 for (int kk = 0; kk < KK; ++kk) {
                   const uint64_t db = dV + static_cast<uint64_t>((kk * 2048) >> 4);
@@ -821,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             if (leader) {
               const uint64_t dK = dK0 + static_cast<uint64_t>((s * Lay::KV_BYTES) >> 4);
-              if (p.debug_mode != 4) {
+              if (!ROPESLR_K2_MEASURE || p.debug_mode != 4) {
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                   // A = Q from TMEM (TS-MMA): only K is read from shared memory
@@ -1149,7 +1162,7 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
   kfn<<<static_cast<unsigned>(grid), kThreads, fx::Layout<BLK>::ALLOC, st>>>(mq, mk, mv, prm);
   if (int e = launch_status()) return e;
-  if (prm.debug_mode >= 2) return ROPESLR_OK;  // measurement modes: the fixed kernel alone
+  if (ROPESLR_K2_MEASURE && prm.debug_mode >= 2) return ROPESLR_OK;  // measurement modes: the fixed kernel alone
   // the running-max kernel over the flagged units (usually none: its CTAs
   // read a zero count and retire)
   Params fb = prm;

@@ -1,5 +1,7 @@
 """K2 experiments: time the fused attention alone at cfg3 shape (a head
-subset), under the ROPESLR_DEBUG_MODE variants, plus a clock64 trace."""
+subset), under the ROPESLR_DEBUG_MODE variants (modes 2-4 need the measurement
+build: scripts/build_variant.sh measure attn_sm100 csrc/attn_sm100.cu -DROPESLR_K2_MEASURE=1,
+then ROPESLR_LIBRARY=paper_2605_20659_b200/_variants/measure.so), plus a clock64 trace."""
 import os, sys
 sys.path[:0] = ['.', 'tests', 'oracle']
 import torch
