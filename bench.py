@@ -308,6 +308,22 @@ def run_ours(args, cfg, rank, world, local_rank):
     k2_ms_local = statistics.mean(a.elapsed_time(b) for a, b in zip(k2_start, k2_end))
     clock_summary = clocks.summary()
 
+    # ---- K1 (selection) and K3 (compensator + gate) alone, CUDA events on the
+    # launching stream: the HBM roofline of the two bandwidth-bound stages
+    def stage_ms(fn, n=20):
+        for _ in range(2):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    k1_ms = stage_ms(lambda: P.select_blocks(q, k, settings.sparse, grid, want_mask=False))
+    k3_ms = stage_ms(lambda: P.compensator_branch(x, grid, params, settings, pe, head_offset=h0, H_local=Hl))
+
     # ---- the fused RoPE + pooling pre-pass, measured
     # alone on this rank's Q/K taken as the un-rotated projections
     rope_ms = None
@@ -398,6 +414,21 @@ def run_ours(args, cfg, rank, world, local_rank):
             "GB_per_s": 4 * q.numel() * q.element_size() / (rope_ms * 1e-3) / 1e9,
             "frac_of_hbm": 4 * q.numel() * q.element_size() / (rope_ms * 1e-3) / 1e9 / load_peaks().get("hbm_gbs", 6650.0),
             "note": "rank 0: read un-rotated Q,K + write rotated Q,K (pooled means ride along)"},
+        "stages": {
+            "note": "rank 0, each stage alone (20 launches after 2 warm-up), CUDA events; algorithmic bytes; "
+                    "peak = measured HBM copy rate",
+            "K1_select": {"ms": k1_ms, "bytes": 2 * q.numel() * q.element_size(),
+                          "GB_per_s": 2 * q.numel() * q.element_size() / (k1_ms * 1e-3) / 1e9,
+                          "frac_of_hbm": 2 * q.numel() * q.element_size() / (k1_ms * 1e-3) / 1e9
+                          / load_peaks().get("hbm_gbs", 6650.0),
+                          "kernels": "pool (f64 block means) + DMMA f64 scores + radix top-k",
+                          "unit": "read Q and K once"},
+            "K3_compensator": {"ms": k3_ms, "bytes": 2 * x.numel() * x.element_size(),
+                               "GB_per_s": 2 * x.numel() * x.element_size() / (k3_ms * 1e-3) / 1e9,
+                               "frac_of_hbm": 2 * x.numel() * x.element_size() / (k3_ms * 1e-3) / 1e9
+                               / load_peaks().get("hbm_gbs", 6650.0),
+                               "kernels": "PE fold + tcgen05 low-rank / gate + fixed-order gate sum",
+                               "unit": "read X once, write y_lr once"}},
         "attended_pairs": attended_total,
         "sparsity": 1.0 - attended_total / (H * float(L) ** 2),
         "roofline": {"bound": "tensor", "kernel": "sparse_attn_fixed_kernel (K2+K4 fused)",
@@ -405,9 +436,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "peak_source": peaks["source"] + ", bf16 dense sustained (kernel timed inside a long step)",
                      "peak_burst": peaks.get("bf16_tflops"), "frac_of_burst": achieved / peaks.get("bf16_tflops", 1),
                      # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the
-                     # committed ncu --set full capture (profiles/r01m_ncu_summary.md)
-                     "traffic": 11.98e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
-                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01m_ncu_summary.md",
+                     # committed ncu --set full capture (profiles/r01n_ncu_summary.md)
+                     "traffic": 12.10e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
+                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01n_ncu_summary.md",
                      "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)",
                      # what actually bounds K2: every (query block, key block) tile streams
                      # its K and V block (2 * block * d * 2 B) from L2 into shared memory.
