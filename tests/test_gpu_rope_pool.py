@@ -39,7 +39,9 @@ def _pool_torch(t, block):
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("grid_s,split,block", [((3, 8, 16), (16, 56, 56), 128), ((2, 5, 9), (44, 42, 42), 64),
-                                                ((4, 7, 7), (16, 24, 24), 32)])
+                                                ((4, 7, 7), (16, 24, 24), 32),
+                                                # TMA-tiled kernel edges: 5-row ragged last blocks, 8-row blocks
+                                                ((1, 7, 19), (16, 56, 56), 128), ((1, 7, 19), (16, 56, 56), 8)])
 def test_rope_pool_matches_torch_rotation(dtype, grid_s, split, block):
     import paper_2605_20659_b200 as P
 
