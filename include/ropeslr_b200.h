@@ -275,7 +275,7 @@ int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_
 
 /* ------------------------- Stage-I training (training.py; mechanism.py:426-488, 519-614)
  * The per-row chains of the fused forward / backward around the float32
- * GEMMs, on head-major float32 rows [H, L, d] (d in {32, 64, 128, 256}):
+ * GEMMs, on head-major float32 rows [H, L, d] (d in {32, 64, 128}):
  *   pre:      xh = x + alpha_h * pe (pe NULL: no PE), gpart[h, l] = xh . w_g_h,
  *             g[l] = sigmoid(sum_h gpart + b_g)
  *   rows:     z2 (= H1 W_B) in, d z2 out in place; dgpart[h, l] = d loss / d g

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const float* __restrict__ p
   }
 }
 
-int vec_of(int64_t d) { return d == 32 ? 1 : d == 64 ? 2 : d == 128 ? 4 : d == 256 ? 8 : 0; }
+int vec_of(int64_t d) { return d == 32 ? 1 : d == 64 ? 2 : d == 128 ? 4 : 0; }  // the op's head dims
 
 }  // namespace s1
 }  // namespace ropeslr
@@ -334,10 +334,8 @@ using namespace ropeslr;
       constexpr int V = 4;   \
       CALL;                  \
     } break;                 \
-    default: {               \
-      constexpr int V = 8;   \
-      CALL;                  \
-    } break;                 \
+    default:                 \
+      break;                 \
   }
 
 static unsigned row_grid(int64_t rows) {

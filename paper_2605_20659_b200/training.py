@@ -116,7 +116,7 @@ def loss_and_grads(prepared: Sequence[_Prepared], params: MechanismParams, setti
     samples; returns (loss, {name: gradient}) with float32 gradients.
 
     The per-row chains run as the fused kernels of csrc/stage1.cu between
-    the float32 GEMMs (head dims 32 / 64 / 128 / 256); other head dims use
+    the float32 GEMMs (head dims 32 / 64 / 128); other head dims use
     the same math composed from torch ops (_loss_and_grads_composed)."""
     d = params.d_h
     if want_grads and prepared and prepared[0].x.is_cuda and _lib.lib().ropeslr_stage1_supported(d):

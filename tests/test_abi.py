@@ -181,7 +181,7 @@ def test_stage1_ops_reject_bad_arguments_without_a_gpu():
     import paper_2605_20659_b200 as P
 
     lib = P.lib()
-    assert [lib.ropeslr_stage1_supported(d) for d in (32, 48, 64, 128, 256, 512)] == [1, 0, 1, 1, 1, 0]
+    assert [lib.ropeslr_stage1_supported(d) for d in (32, 48, 64, 128, 256, 512)] == [1, 0, 1, 1, 0, 0]
     f = ctypes.c_float
     # unsupported head dim, NULL output, PE without alpha
     assert lib.ropeslr_stage1_pre(2, 8, 48, 16, None, None, 16, f(0.0), 16, 16, 16, None) == -1

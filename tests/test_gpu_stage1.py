@@ -64,15 +64,15 @@ def test_stage1_training_reduces_loss():
 
 
 @pytest.mark.parametrize("use_pe", [True, False])
-def test_stage1_fused_equals_composed_d128(use_pe):
-    """The fused row kernels (csrc/stage1.cu, 4 values per lane at d = 128,
-    the bench shape) against the torch composition of the same math, two
-    samples (gradients accumulate over samples)."""
+@pytest.mark.parametrize("d,split,r", [(128, (16, 56, 56), 32), (32, (8, 12, 12), 16)])
+def test_stage1_fused_equals_composed(use_pe, d, split, r):
+    """The fused row kernels (csrc/stage1.cu: 1 and 4 values per lane;
+    d = 128 is the bench shape) against the torch composition of the same
+    math, two samples (gradients accumulate over samples)."""
     import paper_2605_20659_b200 as P
     from paper_2605_20659_b200 import training as T
 
-    grid_s, split = (2, 6, 20), (16, 56, 56)
-    H, d, r = 3, 128, 32
+    grid_s, H = (2, 6, 20), 3
     q, k, v, x, params, pe, grid = G.make_full_inputs(grid_s, H, d, split, r, seed=6, dtype=torch.float32)
     gen = torch.Generator(device="cuda").manual_seed(8)
     samples = [T.Stage1Sample(q, k, v, x, torch.randn((1, grid.size, H * d), generator=gen, device="cuda") * 0.5)
