@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
       const float inv = rsqrtf(ss * (1.f / D) + a.eps);
       const int64_t yrow = ((static_cast<int64_t>(b) * a.L + tt) * a.H + h) * D;
       uint4* dst = reinterpret_cast<uint4*>(a.y_lr + yrow);
+      uint32_t packed[8];  // 16 columns: one 256-bit store (a full 32-byte sector per thread)
 #pragma unroll
       for (int e = 0; e < D / 8; ++e) {
         const float4 w0 = *reinterpret_cast<const float4*>(sRms + 8 * e);
@@ -426,8 +427,16 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
         __nv_bfloat162 p1 = __floats2bfloat162_rn(f1.x * inv * w0.z, f1.y * inv * w0.w);
         __nv_bfloat162 p2 = __floats2bfloat162_rn(f2.x * inv * w1.x, f2.y * inv * w1.y);
         __nv_bfloat162 p3 = __floats2bfloat162_rn(f3.x * inv * w1.z, f3.y * inv * w1.w);
-        __stcs(dst + e, make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
-                                   *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3)));
+        const int o4 = (e & 1) * 4;
+        packed[o4 + 0] = *reinterpret_cast<uint32_t*>(&p0);
+        packed[o4 + 1] = *reinterpret_cast<uint32_t*>(&p1);
+        packed[o4 + 2] = *reinterpret_cast<uint32_t*>(&p2);
+        packed[o4 + 3] = *reinterpret_cast<uint32_t*>(&p3);
+        if (e & 1)
+          asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + e - 1),
+                       "r"(packed[0]), "r"(packed[1]), "r"(packed[2]), "r"(packed[3]), "r"(packed[4]),
+                       "r"(packed[5]), "r"(packed[6]), "r"(packed[7])
+                       : "memory");
         if (a.o_lr) {
           float* od = a.o_lr + ((static_cast<int64_t>(b) * a.H + h) * a.L + tok) * D + 8 * e;
           *reinterpret_cast<float4*>(od) = make_float4(f0.x, f0.y, f1.x, f1.y);
