@@ -589,19 +589,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const __nv_bfloat16* y = p.y_lr + orow;
         __nv_bfloat16* dst = p.out + orow;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
-          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
-          uint4 uo;
-          __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
+        for (int i = 0; i < 32; i += 16) {
+          // 16 columns = 32 bytes: one 256-bit load of y_lr and one 256-bit
+          // store of out per step (a full sector per thread)
+          uint32_t uy[8], uo[8];
+          asm volatile("ld.global.cs.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                       : "=r"(uy[0]), "=r"(uy[1]), "=r"(uy[2]), "=r"(uy[3]), "=r"(uy[4]), "=r"(uy[5]),
+                         "=r"(uy[6]), "=r"(uy[7])
+                       : "l"(y + i));
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 yv = __bfloat1622float2(hy[e]);
+          for (int e = 0; e < 8; ++e) {
+            const float2 yv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uy[e]));
             const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
             const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
-            ho[e] = __floats2bfloat162_rn(o0, o1);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(o0, o1);
+            uo[e] = *reinterpret_cast<uint32_t*>(&h2);
           }
-          __stcs(reinterpret_cast<uint4*>(dst + i), uo);
+          asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + i), "r"(uo[0]),
+                       "r"(uo[1]), "r"(uo[2]), "r"(uo[3]), "r"(uo[4]), "r"(uo[5]), "r"(uo[6]), "r"(uo[7])
+                       : "memory");
         }
       }
     }
@@ -1010,19 +1016,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const __nv_bfloat16* y = p.y_lr + orow;
         __nv_bfloat16* dst = p.out + orow;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          const uint4 uy = __ldcs(reinterpret_cast<const uint4*>(y + i));
-          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&uy);
-          uint4 uo;
-          __nv_bfloat162* ho = reinterpret_cast<__nv_bfloat162*>(&uo);
+        for (int i = 0; i < 32; i += 16) {
+          // 16 columns = 32 bytes: one 256-bit load of y_lr and one 256-bit
+          // store of out per step (a full sector per thread)
+          uint32_t uy[8], uo[8];
+          asm volatile("ld.global.cs.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                       : "=r"(uy[0]), "=r"(uy[1]), "=r"(uy[2]), "=r"(uy[3]), "=r"(uy[4]), "=r"(uy[5]),
+                         "=r"(uy[6]), "=r"(uy[7])
+                       : "l"(y + i));
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 yv = __bfloat1622float2(hy[e]);
+          for (int e = 0; e < 8; ++e) {
+            const float2 yv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uy[e]));
             const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
             const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
-            ho[e] = __floats2bfloat162_rn(o0, o1);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(o0, o1);
+            uo[e] = *reinterpret_cast<uint32_t*>(&h2);
           }
-          __stcs(reinterpret_cast<uint4*>(dst + i), uo);
+          asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + i), "r"(uo[0]),
+                       "r"(uo[1]), "r"(uo[2]), "r"(uo[3]), "r"(uo[4]), "r"(uo[5]), "r"(uo[6]), "r"(uo[7])
+                       : "memory");
         }
       }
     }
