@@ -436,9 +436,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "peak_source": peaks["source"] + ", bf16 dense sustained (kernel timed inside a long step)",
                      "peak_burst": peaks.get("bf16_tflops"), "frac_of_burst": achieved / peaks.get("bf16_tflops", 1),
                      # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the
-                     # committed ncu --set full capture (profiles/r01n_ncu_summary.md)
-                     "traffic": 12.10e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
-                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01n_ncu_summary.md",
+                     # committed ncu --set full capture (profiles/r01o_ncu_summary.md)
+                     "traffic": 9.87e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
+                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01o_ncu_summary.md",
                      "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)",
                      # what actually bounds K2: every (query block, key block) tile streams
                      # its K and V block (2 * block * d * 2 B) from L2 into shared memory.
