@@ -45,7 +45,7 @@ METRIC = "RoPeSLR attn fwd ms & effective TFLOPS/GPU, L=118800, 90% sparse, 1/2/
 # our launches per step: pool_blocks, block_scores, select_topk_warp (K1);
 # lowrank_fold, lowrank_umma, gate_sum (K3); sparse_attn_fixed and the
 # running-max sparse_attn_tc over the fixed kernel's flagged units (K2+K4)
-KERNELS_PER_STEP = 8
+KERNELS_PER_STEP = 8  # pool, scores, select, fold, lowrank, gate_sum, fixed K2, K2 fallback (top-k: no unit ranking)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 

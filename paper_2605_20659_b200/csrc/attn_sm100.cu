@@ -1312,6 +1312,9 @@ static int64_t num_units_of(const ropeslr_shape* s) { return s->B * s->H * ceil_
 static int schedule_units(const ropeslr_shape* s, const int32_t* cnt, tc::Params& prm, void* ws, cudaStream_t cs) {
   const char* sched_env = getenv("ROPESLR_SCHEDULE");
   if ((sched_env != nullptr && sched_env[0] == '0') || prm.nb > kMaxScheduledBlocks) return ROPESLR_OK;
+  // top-k rows (index rows narrower than nb) all hold k blocks: balanced by
+  // construction, so the identity order is as good and the ranking is skipped
+  if (prm.kmax < prm.nb) return ROPESLR_OK;
   const int64_t G = prm.num_units < num_sms() ? prm.num_units : num_sms();
   int32_t* order = static_cast<int32_t*>(ws);
   tc::schedule_units_kernel<<<static_cast<unsigned>(s->B * s->H), 512, prm.nb * sizeof(int32_t), cs>>>(

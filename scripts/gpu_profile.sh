@@ -4,7 +4,7 @@
 # usage: gpurun --timeout 1800 -- bash scripts/gpu_profile.sh [tag] [bench args...]
 tag=${1:-prof}; shift
 mkdir -p gpurun_out
-KRE=${KRE:-'regex:pool_blocks|block_scores|select_|lowrank|gate_|sparse_attn|key_block_norm|fuse_output|linear_|rope_pool'}
+KRE=${KRE:-'regex:pool_blocks|block_scores|select_|lowrank|gate_|schedule_units|sparse_attn|key_block_norm|fuse_output|linear_|rope_pool'}
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" --csv \
   --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline "$@" \
   > gpurun_out/${tag}_launches.log 2>&1
