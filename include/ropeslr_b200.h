@@ -53,7 +53,7 @@ typedef enum ropeslr_status {
   ROPESLR_OK = 0,
   ROPESLR_ERR_SHAPE = -1,      /* inconsistent or unsupported sizes */
   ROPESLR_ERR_DTYPE = -2,      /* unsupported dtype code */
-  ROPESLR_ERR_ALIGN = -3,      /* pointer not 16-byte aligned */
+  ROPESLR_ERR_ALIGN = -3,      /* pointer not 16-byte aligned (32 bytes for out / y_lr on the tcgen05 paths) */
   ROPESLR_ERR_DIVIS = -4,      /* 3D block does not divide the grid */
   ROPESLR_ERR_LAUNCH = -5,     /* CUDA launch / runtime error */
   ROPESLR_ERR_VALUE = -6,      /* out-of-range scalar (keep, eps, topk, ...) */
@@ -207,13 +207,20 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
 /* K2 + K4 in one launch where the tcgen05 path applies (else K2 then K4):
  * attention, normalisation by the softmax denominator, RMSNorm, gated
  * combination with y_lr and the bf16/f32 store of out.  o_sparse (nullable)
- * additionally receives the raw sparse-branch output.  Workspace: the
- * CUDA-core path keeps o_sparse there when o_sparse is NULL.  The tcgen05
- * path keeps the per-key-block maxima of |k| there that its fixed exponent
- * reference needs (without a workspace it runs the running-max kernel) and a
- * longest-first schedule of the (head, query block) units, which balances
- * rows with different block counts under the `keep` rule (environment
- * variable ROPESLR_SCHEDULE=0 turns the schedule off). */
+ * additionally receives the raw sparse-branch output.  On the tcgen05 path
+ * y_lr and out must be 32-byte aligned (256-bit row accesses), else
+ * ROPESLR_ERR_ALIGN.  Workspace: the CUDA-core path keeps o_sparse there when
+ * o_sparse is NULL.  The tcgen05 path keeps there, as int32:
+ *   [0, NU)          a longest-first schedule of the NU = B*H*nb
+ *                    (head, query block) units (`keep` rule only; top-k rows
+ *                    are balanced by construction; ROPESLR_SCHEDULE=0 turns
+ *                    it off),
+ *   [NU, 2 NU)       per-unit flags of the fixed-exponent kernel,
+ *   [2 NU]           the number of units whose exponent reference failed and
+ *                    that the running-max kernel recomputed (the fallback
+ *                    count; readable after the call),
+ *   [2 NU + 1, ...)  their list.
+ * Without a workspace the tcgen05 path runs the running-max kernel alone. */
 int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
                          const int32_t* idx, int32_t kmax, const int32_t* cnt,
                          const int32_t* row_perm, const void* y_lr, const float* g_logit, float b_g,

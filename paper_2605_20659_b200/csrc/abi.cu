@@ -1,6 +1,8 @@
 // Miscellaneous C-ABI entry points and the per-device attribute cache.
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "common.cuh"
@@ -21,6 +23,29 @@ int num_sms() {
   return cache[dev];
 }
 
+static bool env_off(const char* name) {
+  const char* e = getenv(name);
+  return e != nullptr && e[0] == '0';
+}
+
+const Tuning& tuning() {
+  static const Tuning t = [] {
+    Tuning r{};
+    const char* k2 = getenv("ROPESLR_K2");
+    r.k2_online = k2 != nullptr && k2[0] == 'o';
+    r.pair64 = !env_off("ROPESLR_PAIR64");
+    r.schedule = !env_off("ROPESLR_SCHEDULE");
+    r.kv_evict_last = !env_off("ROPESLR_KV_EVICT_LAST");
+    const char* sc = getenv("ROPESLR_SCORES");
+    r.scores = sc != nullptr ? sc[0] : 0;
+    r.rope_tma = !env_off("ROPESLR_ROPE_TMA");
+    const char* lin = getenv("ROPESLR_LINEAR");
+    r.linear_simt = lin != nullptr && lin[0] == 's';
+    return r;
+  }();
+  return t;
+}
+
 }  // namespace ropeslr
 
 extern "C" int ropeslr_abi_version(void) { return ROPESLR_ABI_VERSION; }
@@ -30,7 +55,7 @@ extern "C" const char* ropeslr_status_string(int status) {
     case ROPESLR_OK: return "ok";
     case ROPESLR_ERR_SHAPE: return "inconsistent or unsupported shape";
     case ROPESLR_ERR_DTYPE: return "unsupported dtype";
-    case ROPESLR_ERR_ALIGN: return "pointer is not 16-byte aligned";
+    case ROPESLR_ERR_ALIGN: return "pointer is misaligned (16 bytes; 32 for out / y_lr on the tensor-core path)";
     case ROPESLR_ERR_DIVIS: return "block dims do not divide the grid";
     case ROPESLR_ERR_LAUNCH: return "CUDA launch or runtime error";
     case ROPESLR_ERR_VALUE: return "scalar argument out of range";

@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kreal = block_size(p.L, BLK, irow[j]);
         mbar_wait(&bars[Bx::S_FULL + pr], (t >> 1) & 1);
         tc_fence_after();
-        const bool trc = p.trace && blockIdx.x == 0 && row == 0 && t < 64;
+        const bool trc = ROPESLR_K2_MEASURE && p.trace && blockIdx.x == 0 && row == 0 && t < 64;
         if (trc) p.trace[(w * 64 + t) * 4 + 0] = clock64();
         float* xm = xch + (pr * 2 + ((t >> 1) & 1)) * 256;  // [pair][tile parity][wg][row]
         if (!rows_live) {
@@ -1143,14 +1143,21 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
     }
   }
 #endif
-  if (prm.trace) {
+#if ROPESLR_K2_MEASURE
+  if (prm.trace) {  // measurement build only: clock64 trace of CTA 0 (scripts/exp_k2.py)
     long long h[2 * 64 * 4];
-    cudaMemcpy(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost);
-    FILE* f = fopen(getenv("ROPESLR_K2_TRACE"), "w");
-    for (int i = 0; i < 128; ++i) fprintf(f, "%d %d %lld %lld %lld\n", i / 64, i % 64, h[i * 4] ? h[i * 4] - h[0] : -1,
-                                          h[i * 4 + 1] ? h[i * 4 + 1] - h[0] : -1, h[i * 4 + 2] ? h[i * 4 + 2] - h[0] : -1);
-    fclose(f);
+    if (cudaMemcpyAsync(h, prm.trace, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
+    const char* path = getenv("ROPESLR_K2_TRACE");
+    if (FILE* f = path ? fopen(path, "w") : nullptr) {
+      for (int i = 0; i < 128; ++i)
+        fprintf(f, "%d %d %lld %lld %lld\n", i / 64, i % 64, h[i * 4] ? h[i * 4] - h[0] : -1,
+                h[i * 4 + 1] ? h[i * 4 + 1] - h[0] : -1, h[i * 4 + 2] ? h[i * 4 + 2] - h[0] : -1);
+      fclose(f);
+    }
   }
+#endif
   return launch_status();
 }
 
@@ -1226,17 +1233,13 @@ static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const vo
   int* fallback = static_cast<int*>(ws) + prm.num_units;
   if (s->block == 128) return tc::launch_fixed<128, 128>(s, q, k, v, prm, fallback, st);
   // block 64: two selected blocks per 128-key tile unless ROPESLR_PAIR64=0
-  const char* e = getenv("ROPESLR_PAIR64");
-  if (e != nullptr && e[0] == '0') return tc::launch_fixed<64, 64>(s, q, k, v, prm, fallback, st);
+  if (!tuning().pair64) return tc::launch_fixed<64, 64>(s, q, k, v, prm, fallback, st);
   return tc::launch_fixed<128, 64>(s, q, k, v, prm, fallback, st);
 }
 
 // K2 flavour for the tcgen05 path: the fixed-reference kernel unless
 // ROPESLR_K2=online asks for the running-max (v7) kernel.
-static bool use_fixed_reference() {
-  const char* e = getenv("ROPESLR_K2");
-  return !(e != nullptr && e[0] == 'o');
-}
+static bool use_fixed_reference() { return !tuning().k2_online; }
 
 static int launch_tc_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                               const tc::Params& prm, cudaStream_t st) {
@@ -1244,7 +1247,7 @@ static int launch_tc_dispatch(const ropeslr_shape* s, const void* q, const void*
 }
 
 static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int kmax, const int32_t* cnt,
-                              const int32_t* perm) {
+                              const int32_t* perm, cudaStream_t st) {
   tc::Params prm{};
   prm.idx = idx;
   prm.cnt = cnt;
@@ -1266,17 +1269,19 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   // K/V tiles are re-read by many query blocks of the head: keep them in L2
   // (evict_last) ahead of the streamed Q / y_lr / out; ROPESLR_KV_EVICT_LAST=0
   // turns the hint off
-  const char* pol = getenv("ROPESLR_KV_EVICT_LAST");
-  prm.kv_evict_last = (pol != nullptr && pol[0] == '0') ? 0 : 1;
+  prm.kv_evict_last = tuning().kv_evict_last ? 1 : 0;
+  prm.debug_mode = 0;
+  prm.trace = nullptr;
+#if ROPESLR_K2_MEASURE
+  // measurement build only (scripts/build_variant.sh): K2 mode switches and the clock64 trace
   const char* dbg = getenv("ROPESLR_DEBUG_MODE");
   prm.debug_mode = dbg ? atoi(dbg) : 0;
-  prm.trace = nullptr;
   static long long* tbuf = nullptr;
   if (getenv("ROPESLR_K2_TRACE")) {
-    if (!tbuf) cudaMalloc(&tbuf, 2 * 64 * 4 * 8);
-    cudaMemset(tbuf, 0, 2 * 64 * 4 * 8);
-    prm.trace = tbuf;
+    if (!tbuf && cudaMalloc(&tbuf, 2 * 64 * 4 * 8) != cudaSuccess) tbuf = nullptr;
+    if (tbuf && cudaMemsetAsync(tbuf, 0, 2 * 64 * 4 * 8, st) == cudaSuccess) prm.trace = tbuf;
   }
+#endif
   return prm;
 }
 
@@ -1295,7 +1300,7 @@ extern "C" int ropeslr_sparse_attention(const ropeslr_shape* s, const void* q, c
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   if (which == ROPESLR_IMPL_SIMT)
     return launch_sparse_attention_simt(s, q, k, v, idx, kmax, cnt, row_perm, o_sparse, cs);
-  tc::Params prm = base_params(s, idx, kmax, cnt, row_perm);
+  tc::Params prm = base_params(s, idx, kmax, cnt, row_perm, cs);
   prm.o_sparse = o_sparse;
   return launch_tc_dispatch(s, q, k, v, prm, cs);
 }
@@ -1310,8 +1315,7 @@ static int64_t num_units_of(const ropeslr_shape* s) { return s->B * s->H * ceil_
 // 19-20% faster with the fixed-reference kernel; on uniform top-k counts it
 // is neutral.
 static int schedule_units(const ropeslr_shape* s, const int32_t* cnt, tc::Params& prm, void* ws, cudaStream_t cs) {
-  const char* sched_env = getenv("ROPESLR_SCHEDULE");
-  if ((sched_env != nullptr && sched_env[0] == '0') || prm.nb > kMaxScheduledBlocks) return ROPESLR_OK;
+  if (!tuning().schedule || prm.nb > kMaxScheduledBlocks) return ROPESLR_OK;
   // top-k rows (index rows narrower than nb) all hold k blocks: balanced by
   // construction, so the identity order is as good and the ranking is skipped
   if (prm.kmax < prm.nb) return ROPESLR_OK;
@@ -1346,7 +1350,10 @@ int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k
   if (st) return st;
   if (!tc::tc_eligible(s)) return ROPESLR_ERR_VALUE;
   if (out_h0 < 0 || out_h0 + s->H > out_H) return ROPESLR_ERR_SHAPE;
-  tc::Params prm = base_params(s, idx, kmax, cnt, nullptr);
+  if (!y_lr || !g_logit || !rms_sparse || !out) return ROPESLR_ERR_NULL;
+  // the fused epilogue moves y_lr / out rows with 256-bit accesses
+  if (!aligned32(y_lr) || !aligned32(out)) return ROPESLR_ERR_ALIGN;
+  tc::Params prm = base_params(s, idx, kmax, cnt, nullptr, stream);
   prm.y_lr = static_cast<const __nv_bfloat16*>(y_lr);
   prm.g_logit = g_logit;
   prm.b_g = b_g;
@@ -1376,7 +1383,9 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
   const int which = resolve_impl(s, impl);
   if (which < 0) return ROPESLR_ERR_VALUE;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  if (o_sparse && !aligned16(o_sparse)) return ROPESLR_ERR_ALIGN;
   if (which == ROPESLR_IMPL_SIMT) {
+    if (!aligned16(y_lr) || !aligned16(out)) return ROPESLR_ERR_ALIGN;
     float* osp = o_sparse;
     if (osp == nullptr) {
       if (!ws || ws_bytes < ropeslr_attend_workspace_bytes(s, impl)) return ROPESLR_ERR_WORKSPACE;
@@ -1386,7 +1395,9 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
     if (st) return st;
     return ropeslr_fuse_output(s, osp, y_lr, g_logit, b_g, rms_sparse, eps, out, stream);
   }
-  tc::Params prm = base_params(s, idx, kmax, cnt, row_perm);
+  // the fused epilogue moves y_lr / out rows with 256-bit accesses
+  if (!aligned32(y_lr) || !aligned32(out)) return ROPESLR_ERR_ALIGN;
+  tc::Params prm = base_params(s, idx, kmax, cnt, row_perm, cs);
   prm.y_lr = static_cast<const __nv_bfloat16*>(y_lr);
   prm.g_logit = g_logit;
   prm.b_g = b_g;

@@ -86,4 +86,19 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 int num_sms();  // cached per device (abi.cu)
 
+// The A/B switches of the kernel experiments, read
+// from the environment once per process (abi.cu), not on every call.
+struct Tuning {
+  bool k2_online;      // ROPESLR_K2=online: the running-max K2 kernel
+  bool pair64;         // ROPESLR_PAIR64=0 turns the paired block-64 tiles off
+  bool schedule;       // ROPESLR_SCHEDULE=0 turns the longest-first unit schedule off
+  bool kv_evict_last;  // ROPESLR_KV_EVICT_LAST=0 drops the K/V L2 evict-last hint
+  char scores;         // ROPESLR_SCORES: 'f' CUDA-core f64, 'd' unpipelined DMMA, 0 default
+  bool rope_tma;       // ROPESLR_ROPE_TMA=0: the row-bulk-copy RoPE kernel
+  bool linear_simt;    // ROPESLR_LINEAR=simt: the CUDA-core linear compensator
+};
+const Tuning& tuning();
+
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+
 }  // namespace ropeslr

@@ -374,8 +374,9 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
   if (rank < 1 || rank > 256) return ROPESLR_ERR_SHAPE;
   if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
   if (lowrank_umma_eligible(s, t, rank)) {
-    // tcgen05 / TMA path (bf16, d = 128, r in {16, 32, 48, 64})
-    if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned16(y_lr)) return ROPESLR_ERR_ALIGN;
+    // tcgen05 / TMA path (bf16, d = 128, r in {16, 32, 48, 64}); y_lr rows leave by 256-bit stores
+    if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned32(y_lr)) return ROPESLR_ERR_ALIGN;
+    if (o_lr && !aligned16(o_lr)) return ROPESLR_ERR_ALIGN;
     if (!ws || ws_bytes < ropeslr_lowrank_workspace_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
     return launch_lowrank_umma(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
                                static_cast<cudaStream_t>(stream));
@@ -462,8 +463,7 @@ extern "C" int ropeslr_linear_branch(const ropeslr_shape* s, const void* q_lin, 
   float* state = partial + BH * nch * static_cast<int64_t>(n);
   cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
   // bf16, d = 128: the tensor-core passes (linear_tc.cu)
-  const char* lin_env = getenv("ROPESLR_LINEAR");
-  if (s->dtype == ROPESLR_BF16 && d == 128 && !(lin_env != nullptr && lin_env[0] == 's') && aligned16(q_lin) &&
+  if (s->dtype == ROPESLR_BF16 && d == 128 && !tuning().linear_simt && aligned16(q_lin) &&
       aligned16(k_lin) && aligned16(v_lin) && aligned16(y_lr))
     return linear_branch_tc(s, q_lin, k_lin, v_lin, rms_lowrank, eps, y_lr, o_lr, partial, state, nch, stream_);
   size_t sm1 = sizeof(float) * 2 * 32 * d;

@@ -376,10 +376,7 @@ int table_rows(const ropeslr_rope_args* r) {
 using namespace ropeslr;
 
 // ROPESLR_ROPE_TMA=0 selects the row-bulk-copy kernel (rope_pool_kernel) for A/B runs.
-static bool rp_tma_disabled() {
-  const char* e = getenv("ROPESLR_ROPE_TMA");
-  return e != nullptr && e[0] == '0';
-}
+static bool rp_tma_disabled() { return !tuning().rope_tma; }
 
 extern "C" size_t ropeslr_rope_pool_workspace_bytes(const ropeslr_rope_args* r) {
   if (!r) return 0;
@@ -458,13 +455,10 @@ extern "C" int ropeslr_rope_pool(const ropeslr_shape* s, const ropeslr_rope_args
     if (!rp::make_map(&mqi, q_in, BH, s->L, s->block) || !rp::make_map(&mki, k_in, BH, s->L, s->block) ||
         !rp::make_map(&mqo, q_out, BH, s->L, s->block) || !rp::make_map(&mko, k_out, BH, s->L, s->block))
       return ROPESLR_ERR_LAUNCH;
-    static bool attr = false;  // one-time opt-in above 48 KiB
-    if (!attr) {
-      if (cudaFuncSetAttribute(rp::rope_pool_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rp::kTmaSmem) !=
-          cudaSuccess)
-        return ROPESLR_ERR_LAUNCH;
-      attr = true;
-    }
+    // opt in above 48 KiB on every call: the attribute is per device
+    if (cudaFuncSetAttribute(rp::rope_pool_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rp::kTmaSmem) !=
+        cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
     rp::rope_pool_tma_kernel<<<grid, 256, rp::kTmaSmem, st>>>(mqi, mki, mqo, mko, pooled, tt, s->L, s->block, nb, BH, r->grid_h,
                                                    r->grid_w);
   } else if (s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128)

@@ -641,18 +641,15 @@ static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_param
   {
     dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
               static_cast<unsigned>(BH));
-    // ROPESLR_SCORES=fma: the CUDA-core kernel (A/B timing)
-    const char* e = getenv("ROPESLR_SCORES");
-    if (e != nullptr && e[0] == 'f')
+    // ROPESLR_SCORES=fma: the CUDA-core kernel, =dmma: the unpipelined DMMA kernel (A/B timing)
+    const char e = tuning().scores;
+    if (e == 'f')
       block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
-    else if (d % sc::KC == 0 && !(e != nullptr && e[0] == 'd')) {  // ROPESLR_SCORES=dmma: the unpipelined kernel
-      static bool attr = false;  // opt in above 48 KiB of dynamic shared memory once
-      if (!attr) {
-        if (cudaFuncSetAttribute(block_scores_dmma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 sc::ST * sc::STAGE_DOUBLES * static_cast<int>(sizeof(double))) != cudaSuccess)
-          return ROPESLR_ERR_LAUNCH;
-        attr = true;
-      }
+    else if (d % sc::KC == 0 && e != 'd') {
+      // opt in above 48 KiB of dynamic shared memory on every call (per-device attribute)
+      if (cudaFuncSetAttribute(block_scores_dmma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               sc::ST * sc::STAGE_DOUBLES * static_cast<int>(sizeof(double))) != cudaSuccess)
+        return ROPESLR_ERR_LAUNCH;
       block_scores_dmma_pipe_kernel<<<grid, 128, sc::ST * sc::STAGE_DOUBLES * sizeof(double), st>>>(
           pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
     } else

@@ -588,6 +588,11 @@ def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *
     dev = q.device
     if out is None:
         out = torch.empty((B, L, H, d), dtype=q.dtype, device=dev)
+    else:
+        if tuple(out.shape) not in ((B, L, H, d), (B, L, H * d)):
+            raise ValueError(f"out must have shape {(B, L, H, d)} or {(B, L, H * d)}, got {tuple(out.shape)}")
+        if out.dtype != q.dtype or out.device != dev or not out.is_contiguous():
+            raise ValueError("out must be a contiguous tensor of Q's dtype on Q's device")
     o_sparse = torch.empty((B, H, L, d), dtype=torch.float32, device=dev) if want_o_sparse else None
     shp = _shape(q, prep.block)
     impl_code = _lib.IMPL[impl]
