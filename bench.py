@@ -149,6 +149,20 @@ def cpu_oracle_sample(q0, k0, v0, x_np, pe_np, params_np, cfg, topk, qblocks):
     return dt, flops
 
 
+def cpu_info():
+    """Host CPU model and logical core count (the CPU baseline's machine)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count()}
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -192,6 +206,27 @@ def make_inputs(cfg, h0, h1, dev, seed=0):
     x_local = x_full[:, :, h0 * d:h1 * d].contiguous()
     del x_full
     return q, k, v, x_local, params.heads(h0, h1), pe, grid
+
+
+# ---------------------------------------------------------------- ranks
+def reduce_over_ranks(times_ms, attended_local, device, world):
+    """Max over ranks of each time (the job finishes with its slowest rank),
+    sum over ranks of the attended pairs.  Returns (times, attended_total)."""
+    import torch
+    import torch.distributed as dist
+
+    vals = torch.tensor([float(t) for t in times_ms], dtype=torch.float64, device=device)
+    att = torch.tensor([int(attended_local)], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(att, op=dist.ReduceOp.SUM)
+    return [float(a) for a in vals.tolist()], int(att.item())
+
+
+def heads_per_rank(H, world):
+    from paper_2605_20659_b200.distributed import head_slice
+
+    return [b - a for a, b in (head_slice(H, world, r) for r in range(world))]
 
 
 # ---------------------------------------------------------------- arms
@@ -241,7 +276,8 @@ def run_reference(args, cfg, rank, world):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1), 3D RoPE, bf16-rounded)",
         "config": {"workload": cfg["name"], "sample": "bounded CPU sample", "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **cpu_info(),
+                         "cores_note": "cores = OpenBLAS threads used by the float64 NumPy port"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -381,13 +417,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e = dict(ms=e2e_ms_local, bi=bi, bo=bo, h2d_gbps=h2d_gbps)
 
     # ---- reduce over ranks
-    vals = torch.tensor([ms_local, k2_ms_local, (e2e or {}).get("ms", 0.0)], dtype=torch.float64, device=dev)
-    att = torch.tensor([attended_local], dtype=torch.int64, device=dev)
-    if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        dist.all_reduce(att, op=dist.ReduceOp.SUM)
-    ms, k2_ms, e2e_ms = (float(a) for a in vals.tolist())
-    attended_total = int(att.item())
+    (ms, k2_ms, e2e_ms), attended_total = reduce_over_ranks(
+        [ms_local, k2_ms_local, (e2e or {}).get("ms", 0.0)], attended_local, dev, world)
 
     if rank != 0:
         return
@@ -405,7 +436,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded N(0,1) Q/K/V with 3D RoPE, X, PE tables; random-init params)",
         "config": {"workload": cfg["name"], "B": B, "L": L, "H": H, "d_h": d, "block": cfg["block"],
                    "n_blocks": nb, "topk": settings.sparse.topk, "rank_r": r,
-                   "heads_per_gpu": Hl, "parallelism": f"head-parallel x{world}",
+                   "heads_per_gpu": Hl, "heads_per_rank": heads_per_rank(H, world),
+                   "parallelism": f"head-parallel x{world}",
                    "l2": "inputs (2.9 GB) larger than L2; no explicit flush"},
         "tflops_per_gpu": value / world,
         "sparse_attn_ms": k2_ms,
@@ -470,7 +502,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         qbs = list(range(args.cpu_qblocks))
         dt, fl = cpu_oracle_sample(q0, k0, v0, x_np, pe_np, params_np, cfg, settings.sparse.topk, qbs)
         line["cpu_baseline"] = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": blas_threads(),
-                                "kind": "port", "seconds": dt,
+                                "kind": "port", "seconds": dt, **cpu_info(),
+                                "cores_note": "cores = OpenBLAS threads used by the float64 NumPy port",
                                 "sample": f"head 0, selection over all {nb} blocks + attention/compensator/fusion "
                                           f"of query blocks 0..{args.cpu_qblocks - 1} (float64 NumPy oracle)"}
     print(json.dumps(line), flush=True)
@@ -644,6 +677,30 @@ def run_train(args, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-run this command under
+    torch.distributed.run with one process per GPU (rendezvous on
+    127.0.0.1), forward its output and exit with its status."""
+    import torch
+
+    if not args.same_device and torch.cuda.device_count() < args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} needs {args.gpus} GPUs, found {torch.cuda.device_count()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -657,11 +714,21 @@ def main():
     ap.add_argument("--cpu-qblocks", type=int, default=300)
     ap.add_argument("--ref-qblocks", type=int, default=100)
     ap.add_argument("--chunk-heads", type=int, default=0, help="heads per H2D/compute chunk of the e2e path (0 = auto)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N > 1 (gloo: a host-side stand-in for rank-logic runs)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (exercises the N > 1 host logic on one GPU; not a scaling number)")
     args = ap.parse_args()
     cfg = CONFIGS.get(args.config)
+    if args.gpus < 1:
+        raise SystemExit("bench: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args, cfg or CONFIGS["cfg1"], rank, world)
         return
@@ -670,7 +737,10 @@ def main():
 
     if world > 1:
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     try:
         if args.config == "cfg4":
             run_dit(args, rank, world, local_rank)

@@ -84,7 +84,16 @@ typedef struct ropeslr_shape {
 typedef struct ropeslr_select_params {
   int32_t topk;
   double keep;
+  /* Nullable device word.  The reference rejects non-finite inputs
+   * (linalg.py:17-20 via as_matrix, mechanism.py:494): when set, the
+   * selection ORs in ROPESLR_NONFINITE_QK (stream-ordered) if a Q or K value
+   * is NaN or infinite.  Detected on the float64 block means, which any
+   * non-finite member makes non-finite (a bf16/f32 sum cannot overflow f64). */
+  uint32_t* nonfinite;
 } ropeslr_select_params;
+
+#define ROPESLR_NONFINITE_QK 1u
+#define ROPESLR_NONFINITE_X 2u
 
 /* Token-side inputs of the compensator / gate (mechanism.py:426-447). */
 typedef struct ropeslr_token_args {
@@ -99,6 +108,10 @@ typedef struct ropeslr_token_args {
   const float* pe_y;       /* [grid_w, D_total] */
   const float* alpha;      /* [D_total] */
   const float* w_g;        /* [D_total] */
+  /* Nullable device word: ORs in ROPESLR_NONFINITE_X when an X value of the
+   * local columns is NaN or infinite (detected on the gate logits, whose
+   * sums every value enters; needs g_logit). */
+  uint32_t* nonfinite;
 } ropeslr_token_args;
 
 /* ---------------------------------------------------------------- misc */
@@ -108,6 +121,19 @@ const char* ropeslr_status_string(int status);
 int ropeslr_device_check(int device);
 /* Number of flat blocks: ceil(L / block). */
 int64_t ropeslr_num_blocks(int64_t L, int32_t block);
+/* Kernel-variant switches for A/B tests and benchmarks, process-wide,
+ * initialised once from the ROPESLR_* environment:
+ *   "k2_online"     1: the running-max K2 kernel instead of the fixed-exponent one
+ *   "pair64"        0: unpaired block-64 K/V tiles
+ *   "schedule"      0: no longest-first unit schedule under the keep rule
+ *   "kv_evict_last" 0: no L2 evict-last hint on K/V tiles
+ *   "scores"        'f' / 'd': CUDA-core / unpipelined DMMA block scores
+ *   "rope_tma"      0: the row-bulk-copy RoPE pre-pass
+ *   "linear_simt"   1: the CUDA-core linear compensator
+ * Not synchronised with calls in flight on other threads.  Unknown name:
+ * ROPESLR_ERR_VALUE.  ropeslr_get_option returns the current value. */
+int ropeslr_set_option(const char* name, int value);
+int ropeslr_get_option(const char* name);
 
 /* ------------------------------------------------ K1: block selection
  * Replaces the routing half of block_sparse_attention (mechanism.py:305-320,

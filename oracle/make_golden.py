@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE ONLY.  Run in the build container (where the read-only
 reference lives at /root/reference):
 
-    python oracle/make_golden.py            # writes tests/golden/*.npz
+    python oracle/make_golden.py [case ...]  # writes tests/golden/*.npz (all cases, or the named ones)
 
 Each fixture stores the exact (post-RoPE, post-cast) inputs the GPU op
 consumes and the reference's outputs on those same values:
@@ -181,6 +181,18 @@ CASES = {
     # bf16, d=128, flat 128-token blocks == tile (1,8,16), top-1 via keep->0
     "bf16_d128_b128": dict(inputs=dict(seed=3, H=1, d=128, grid=(3, 8, 16), split=(16, 56, 56), r=64, dtype="bf16"),
                            ref=dict(block3=(1, 8, 16), keep=1e-12, compensator="lowrank")),
+    # bf16, d=128, TRUE 3D tiles (not whole grid rows): the tcgen05 kernel's
+    # row_perm path, tile-major token order; 64-token tiles (2,4,8) and
+    # 128-token tiles (2,4,16) on a (4,8,16) grid, keep rule, learnable PE
+    "bf16_3d_tile64": dict(inputs=dict(seed=6, H=2, d=128, grid=(4, 8, 16), split=(44, 42, 42), r=64, dtype="bf16"),
+                           ref=dict(block3=(2, 4, 8), keep=0.5, compensator="lowrank")),
+    "bf16_3d_tile128": dict(inputs=dict(seed=7, H=2, d=128, grid=(4, 8, 16), split=(16, 56, 56), r=64,
+                                        dtype="bf16"),
+                            ref=dict(block3=(2, 4, 16), keep=0.4, compensator="lowrank")),
+    # bf16, d=128 linear compensator (the tensor-core linear path) from the reference
+    "bf16_d128_linear": dict(inputs=dict(seed=8, H=2, d=128, grid=(2, 8, 16), split=(44, 42, 42), r=64,
+                                         dtype="bf16"),
+                             ref=dict(block3=(1, 4, 16), keep=0.35, compensator="linear")),
     # ragged flat blocks + fixed top-k (restated; L = 196, block 64 -> last block 4 tokens)
     "ragged_topk_bf16": dict(inputs=dict(seed=4, H=2, d=128, grid=(4, 7, 7), split=(44, 42, 42), r=64, dtype="bf16"),
                              restated=dict(block=64, topk=2, compensator="lowrank")),
@@ -189,9 +201,52 @@ CASES = {
 }
 
 
-def main():
+# Cases run through the reference's real mechanism.forward(x, grid, cfg,
+# backbone, params, settings) (mechanism.py:491-512) -- projections and 3D
+# RoPE inside the reference -- plus the analysis calls the CLI makes on its
+# trace (cli.py:432-433 gram_spectral(trace.o_lowrank[0]), cli.py:463-464
+# gate_map(trace.g)).  They pin reference_api.forward end to end.
+FORWARD_CASES = {
+    "fwd_ref_lowrank": dict(seed=20, H=2, d=64, grid=(4, 8, 8), split=(16, 24, 24), r=16, block3=(1, 8, 8),
+                            keep=0.5, compensator="lowrank", use_pe=True),
+    "fwd_ref_linear_3d": dict(seed=21, H=2, d=64, grid=(4, 8, 8), split=(16, 24, 24), r=16, block3=(2, 4, 4),
+                              keep=0.6, compensator="linear", use_pe=True),
+}
+
+
+def run_reference_forward(seed, H, d, grid, split, r, block3, keep, compensator, use_pe):
+    M, GridShape, RopeConfig = _import_reference()
+    import ropeslr.analysis as A  # noqa: E402
+    g = GridShape(*grid)
+    cfg = RopeConfig(*split)
+    rng = np.random.default_rng(seed)
+    D = H * d
+    x = rng.standard_normal((g.size, D))
+    backbone = M.random_backbone(H, d, seed + 1)
+    params = M.init_params(H, d, r, seed + 2)
+    params.w_g = rng.standard_normal(D) * 0.05  # non-zero so the gate path is exercised
+    fs = M.ForwardSettings(sparse=M.SparseSettings(block=tuple(block3), keep=keep), compensator=compensator,
+                           use_pe=use_pe)
+    tr = M.forward(x, g, cfg, backbone, params, fs)
+    spec = A.gram_spectral(tr.o_lowrank[0], g, 4)
+    gmap = A.gate_map(tr.g, g)
+    out = dict(x=x, w_q=backbone.w_q, w_k=backbone.w_k, w_v=backbone.w_v,
+               **{f"p_{n}": np.asarray(getattr(params, n)) for n in (
+                   "w_a", "w_b", "alpha", "w_g", "b_g", "rms_sparse", "rms_lowrank")},
+               grid=np.array(grid), split=np.array(split), block3=np.array(block3), keep=np.float64(keep),
+               compensator=np.array(compensator), use_pe=np.bool_(use_pe), source=np.array("reference_forward"))
+    for f in ("x_hat", "o_sparse", "o_lowrank", "norm_sparse", "norm_lowrank", "g", "output", "sparsity"):
+        out[f"ref_{f}"] = np.asarray(getattr(tr, f))
+    out.update(ref_gram_sigma=spec.sigma, ref_gram_modes=spec.modes, ref_gate_values=gmap.values,
+               ref_gate_frame_means=gmap.frame_means)
+    return out
+
+
+def main(only=None):
     os.makedirs(OUT_DIR, exist_ok=True)
     for name, spec in CASES.items():
+        if only and name not in only:
+            continue
         inp = make_inputs(**spec["inputs"])
         if "ref" in spec:
             outs = run_reference(inp, **spec["ref"])
@@ -212,7 +267,16 @@ def main():
         np.savez_compressed(path, **inp, **meta, **{f"ref_{k}": v for k, v in outs.items()})
         print(f"{name}: {os.path.getsize(path) / 1024:.0f} KiB, source={meta['source']}, "
               f"sparsity={outs['sparsity']}")
+    os.makedirs(os.path.join(OUT_DIR, "forward"), exist_ok=True)
+    for name, spec in FORWARD_CASES.items():
+        if only and name not in only:
+            continue
+        path = os.path.join(OUT_DIR, "forward", f"{name}.npz")
+        out = run_reference_forward(**spec)
+        np.savez_compressed(path, **out)
+        print(f"{name}: {os.path.getsize(path) / 1024:.0f} KiB, source=reference_forward, "
+              f"sparsity={out['ref_sparsity']}")
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("ROPESLR_LIBRARY") or os.path.join(PKG, "libropeslr_b2
 
 F32, BF16 = 0, 1
 LOWRANK, LINEAR = 0, 1
+NONFINITE_QK, NONFINITE_X = 1, 2
 IMPL = {"auto": 0, "simt": 1, "tcgen05": 2}
 
 c_i32, c_i64, c_f32, c_f64, c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double, ctypes.c_size_t
@@ -29,13 +30,13 @@ class Shape(ctypes.Structure):
 
 
 class SelectParams(ctypes.Structure):
-    _fields_ = [("topk", c_i32), ("keep", c_f64)]
+    _fields_ = [("topk", c_i32), ("keep", c_f64), ("nonfinite", c_vp)]
 
 
 class TokenArgs(ctypes.Structure):
     _fields_ = [("x", c_vp), ("x_row_stride", c_i64), ("head_offset", c_i64), ("d_model", c_i64),
                 ("grid_t", c_i32), ("grid_h", c_i32), ("grid_w", c_i32), ("use_pe", c_i32),
-                ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp)]
+                ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp), ("nonfinite", c_vp)]
 
 
 class RopeArgs(ctypes.Structure):
@@ -59,6 +60,8 @@ _SIGNATURES = {
     "ropeslr_status_string": (ctypes.c_char_p, [c_i32]),
     "ropeslr_device_check": (c_i32, [c_i32]),
     "ropeslr_num_blocks": (c_i64, [c_i64, c_i32]),
+    "ropeslr_set_option": (c_i32, [ctypes.c_char_p, c_i32]),
+    "ropeslr_get_option": (c_i32, [ctypes.c_char_p]),
     "ropeslr_select_workspace_bytes": (c_sz, [P(Shape)]),
     "ropeslr_select_blocks": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
                                       c_vp, c_sz, c_vp]),
@@ -138,3 +141,33 @@ def check(fn: str, status: int) -> None:
 
 def call(fn: str, *args) -> None:
     check(fn, getattr(lib(), fn)(*args))
+
+
+def set_option(name: str, value) -> None:
+    """Process-wide kernel-variant switch (include/ropeslr_b200.h
+    ropeslr_set_option); ``value`` may be a one-character string ('f', 'd')."""
+    v = ord(value) if isinstance(value, str) else int(value)
+    check("ropeslr_set_option", lib().ropeslr_set_option(name.encode(), v))
+
+
+def get_option(name: str) -> int:
+    v = lib().ropeslr_get_option(name.encode())
+    if v < 0:
+        check("ropeslr_get_option", v)
+    return v
+
+
+class option:
+    """Context manager: ``with option("k2_online", 1): ...`` restores the
+    previous value on exit."""
+
+    def __init__(self, name: str, value):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        self.prev = get_option(self.name)
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.prev)

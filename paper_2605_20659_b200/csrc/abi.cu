@@ -4,6 +4,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -28,8 +29,8 @@ static bool env_off(const char* name) {
   return e != nullptr && e[0] == '0';
 }
 
-const Tuning& tuning() {
-  static const Tuning t = [] {
+static Tuning& tuning_mut() {
+  static Tuning t = [] {
     Tuning r{};
     const char* k2 = getenv("ROPESLR_K2");
     r.k2_online = k2 != nullptr && k2[0] == 'o';
@@ -44,6 +45,28 @@ const Tuning& tuning() {
     return r;
   }();
   return t;
+}
+
+const Tuning& tuning() { return tuning_mut(); }
+
+template <typename T>
+__global__ void nonfinite_scan_kernel(const T* __restrict__ a, int64_t n, uint32_t* flag, uint32_t bit) {
+  bool bad = false;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= !isfinite(a[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, bit);
+}
+
+int scan_nonfinite(const void* a, bool f64, int64_t n, uint32_t* flag, uint32_t bit, cudaStream_t st) {
+  if (flag == nullptr || n <= 0) return ROPESLR_OK;
+  const int64_t blocks = ceil_div(n, 256 * 8);
+  const unsigned grid = static_cast<unsigned>(blocks < 8 * num_sms() ? blocks : 8 * num_sms());
+  if (f64)
+    nonfinite_scan_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(a), n, flag, bit);
+  else
+    nonfinite_scan_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(a), n, flag, bit);
+  return launch_status();
 }
 
 }  // namespace ropeslr
@@ -78,4 +101,31 @@ extern "C" int ropeslr_device_check(int device) {
 extern "C" int64_t ropeslr_num_blocks(int64_t L, int32_t block) {
   if (L < 1 || block < 1) return 0;
   return ropeslr::ceil_div(L, block);
+}
+
+extern "C" int ropeslr_set_option(const char* name, int value) {
+  if (name == nullptr) return ROPESLR_ERR_NULL;
+  ropeslr::Tuning& t = ropeslr::tuning_mut();
+  if (!strcmp(name, "k2_online")) t.k2_online = value != 0;
+  else if (!strcmp(name, "pair64")) t.pair64 = value != 0;
+  else if (!strcmp(name, "schedule")) t.schedule = value != 0;
+  else if (!strcmp(name, "kv_evict_last")) t.kv_evict_last = value != 0;
+  else if (!strcmp(name, "scores")) t.scores = static_cast<char>(value);
+  else if (!strcmp(name, "rope_tma")) t.rope_tma = value != 0;
+  else if (!strcmp(name, "linear_simt")) t.linear_simt = value != 0;
+  else return ROPESLR_ERR_VALUE;
+  return ROPESLR_OK;
+}
+
+extern "C" int ropeslr_get_option(const char* name) {
+  if (name == nullptr) return ROPESLR_ERR_NULL;
+  const ropeslr::Tuning& t = ropeslr::tuning();
+  if (!strcmp(name, "k2_online")) return t.k2_online;
+  if (!strcmp(name, "pair64")) return t.pair64;
+  if (!strcmp(name, "schedule")) return t.schedule;
+  if (!strcmp(name, "kv_evict_last")) return t.kv_evict_last;
+  if (!strcmp(name, "scores")) return t.scores;
+  if (!strcmp(name, "rope_tma")) return t.rope_tma;
+  if (!strcmp(name, "linear_simt")) return t.linear_simt;
+  return ROPESLR_ERR_VALUE;
 }

@@ -86,6 +86,10 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 int num_sms();  // cached per device (abi.cu)
 
+// ORs `bit` into *flag (stream-ordered) when any of the n values is NaN or
+// infinite; no-op for a NULL flag (abi.cu).
+int scan_nonfinite(const void* a, bool f64, int64_t n, uint32_t* flag, uint32_t bit, cudaStream_t st);
+
 // The A/B switches of the kernel experiments, read
 // from the environment once per process (abi.cu), not on every call.
 struct Tuning {

@@ -378,14 +378,20 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
     if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned32(y_lr)) return ROPESLR_ERR_ALIGN;
     if (o_lr && !aligned16(o_lr)) return ROPESLR_ERR_ALIGN;
     if (!ws || ws_bytes < ropeslr_lowrank_workspace_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
-    return launch_lowrank_umma(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
-                               static_cast<cudaStream_t>(stream));
+    if (int e = launch_lowrank_umma(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
+                                    static_cast<cudaStream_t>(stream)))
+      return e;
+    return scan_nonfinite(g_logit, false, g_logit ? s->B * s->L : 0, t->nonfinite, ROPESLR_NONFINITE_X,
+                          static_cast<cudaStream_t>(stream));
   }
   if (lowrank_tc_eligible(s, rank)) {
     if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned16(y_lr)) return ROPESLR_ERR_ALIGN;
     if (!ws || ws_bytes < ropeslr_lowrank_workspace_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
-    return launch_lowrank_tc(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
-                             static_cast<cudaStream_t>(stream));
+    if (int e = launch_lowrank_tc(s, t, w_a, w_b, rank, rms_lowrank, eps, y_lr, o_lr, g_logit, ws,
+                                  static_cast<cudaStream_t>(stream)))
+      return e;
+    return scan_nonfinite(g_logit, false, g_logit ? s->B * s->L : 0, t->nonfinite, ROPESLR_NONFINITE_X,
+                          static_cast<cudaStream_t>(stream));
   }
   const int d = static_cast<int>(s->d), r = rank;
   size_t sm = sizeof(float) * (static_cast<size_t>(kTok) * (d + 1) + d * r + kTok * (r + 1) + r * d + kTok);
@@ -403,7 +409,8 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
     kfn<<<grid, 256, sm, stream_>>>(c, static_cast<const float*>(t->x), static_cast<int>(s->H), d, r, w_a, w_b,
                                     rms_lowrank, eps, static_cast<float*>(y_lr), o_lr, g_logit);
   }
-  return launch_status();
+  if (int e = launch_status()) return e;
+  return scan_nonfinite(g_logit, false, g_logit ? s->B * s->L : 0, t->nonfinite, ROPESLR_NONFINITE_X, stream_);
 }
 
 extern "C" int ropeslr_gate_logits(const ropeslr_shape* s, const ropeslr_token_args* t, float* g_logit,
@@ -422,7 +429,8 @@ extern "C" int ropeslr_gate_logits(const ropeslr_shape* s, const ropeslr_token_a
   else
     gate_kernel<float><<<grid, 256, 0, stream_>>>(c, static_cast<const float*>(t->x), static_cast<int>(s->H),
                                                   static_cast<int>(s->d), g_logit);
-  return launch_status();
+  if (int e = launch_status()) return e;
+  return scan_nonfinite(g_logit, false, s->B * s->L, t->nonfinite, ROPESLR_NONFINITE_X, stream_);
 }
 
 static int64_t lin_nchunks(int64_t L) { return ceil_div(L, kLinChunk); }

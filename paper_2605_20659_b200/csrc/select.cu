@@ -638,6 +638,7 @@ static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_param
   const int d = static_cast<int>(s->d);
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
   if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  if (int e = scan_nonfinite(pooled, true, 2 * BH * nb * d, sel->nonfinite, ROPESLR_NONFINITE_QK, st)) return e;
   {
     dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
               static_cast<unsigned>(BH));

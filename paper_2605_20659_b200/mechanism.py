@@ -339,7 +339,7 @@ def block_layout(L: int, settings: SparseSettings, grid: Optional[GridShape], de
 
 def select_blocks(q: torch.Tensor, k: torch.Tensor, settings: SparseSettings, grid: Optional[GridShape] = None,
                   *, want_mask: bool = True, want_scores: bool = False, _layout=None,
-                  pooled: Optional[torch.Tensor] = None) -> Selection:
+                  pooled: Optional[torch.Tensor] = None, nonfinite: Optional[torch.Tensor] = None) -> Selection:
     """Block routing of block_sparse_attention (mechanism.py:305-320).
     ``pooled`` ([2, B*H, nb, d] float64 block means, e.g. from ``rope_pool``)
     skips the pooling stage."""
@@ -359,7 +359,7 @@ def select_blocks(q: torch.Tensor, k: torch.Tensor, settings: SparseSettings, gr
     attended = torch.empty((B, H), dtype=torch.int64, device=dev)
     scores = torch.empty((B, H, nb, nb), dtype=torch.float64, device=dev) if want_scores else None
     shp = _shape(q, block)
-    sel = _lib.SelectParams(int(settings.topk), float(settings.keep))
+    sel = _lib.SelectParams(int(settings.topk), float(settings.keep), _ptr(nonfinite))
     if pooled is not None:
         if pooled.shape != (2, B * H, nb, d) or pooled.dtype != torch.float64 or not pooled.is_contiguous():
             raise ValueError(f"pooled must be contiguous float64 [2, {B * H}, {nb}, {d}]")
@@ -440,7 +440,7 @@ def block_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, se
 
 
 def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: Optional[PETables], use_pe: bool,
-                head_offset: int, H_local: int, d: int) -> _lib.TokenArgs:
+                head_offset: int, H_local: int, d: int, nonfinite: Optional[torch.Tensor] = None) -> _lib.TokenArgs:
     if x.dim() != 3:
         raise ValueError(f"expected X of shape [B, L, H*d], got {tuple(x.shape)}")
     B, L, W = x.shape
@@ -460,13 +460,14 @@ def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: O
                 raise ValueError("PE tables must be contiguous float32 [grid axis, d_model]")
     return _lib.TokenArgs(x.data_ptr(), x.stride(1), head_offset, params.d_model, grid.t, grid.h, grid.w,
                           int(bool(use_pe)), _ptr(pe.pe_t) if use_pe else None, _ptr(pe.pe_x) if use_pe else None,
-                          _ptr(pe.pe_y) if use_pe else None, params.alpha.data_ptr(), params.w_g.data_ptr())
+                          _ptr(pe.pe_y) if use_pe else None, params.alpha.data_ptr(), params.w_g.data_ptr(),
+                          _ptr(nonfinite))
 
 
 def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams, settings: ForwardSettings,
                        pe: Optional[PETables] = None, *, head_offset: int = 0,
                        lin_proj: Optional[Sequence[torch.Tensor]] = None, want_o_lr: bool = False,
-                       H_local: Optional[int] = None):
+                       H_local: Optional[int] = None, nonfinite: Optional[torch.Tensor] = None):
     """Low-rank (mechanism.py:225-235, 441-446) or linear (mechanism.py:350-362)
     compensator of the local heads, RMS-normalised with rms_lowrank, plus the
     gate logits over the local columns (mechanism.py:434).
@@ -477,7 +478,7 @@ def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams
     d = params.d_h
     B, L, _ = x.shape
     dev = x.device
-    tok = _token_args(x, grid, params, pe, settings.use_pe, head_offset, H, d)
+    tok = _token_args(x, grid, params, pe, settings.use_pe, head_offset, H, d, nonfinite)
     shp = _lib.Shape(B, H, L, d, 1, _dtype_code(x))
     y_lr = torch.empty((B, L, H, d), dtype=x.dtype, device=dev)
     o_lr = torch.empty((B, H, L, d), dtype=torch.float32, device=dev) if want_o_lr else None
@@ -550,7 +551,8 @@ class Prepared:
 def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, grid: GridShape,
             params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False,
-            head_offset: int = 0, rope: Optional[RopeConfig] = None) -> Prepared:
+            head_offset: int = 0, rope: Optional[RopeConfig] = None,
+            nonfinite: Optional[torch.Tensor] = None) -> Prepared:
     """K1 (routing, mechanism.py:305-320) and K3 (compensator + partial gate
     logits, mechanism.py:429-447) for the local heads.  With ``rope`` the
     given Q/K are un-rotated: the fused RoPE + pooling pre-pass rotates them
@@ -572,9 +574,9 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
         pl = perm.long()
         q, k, v = q.index_select(2, pl), k.index_select(2, pl), v.index_select(2, pl)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    sel = select_blocks(q, k, settings.sparse, want_mask=trace, _layout=layout, pooled=pooled)
+    sel = select_blocks(q, k, settings.sparse, want_mask=trace, _layout=layout, pooled=pooled, nonfinite=nonfinite)
     y_lr, o_lr, g_logit = compensator_branch(x, grid, params, settings, pe, head_offset=head_offset,
-                                             lin_proj=lin_proj, want_o_lr=trace, H_local=H)
+                                             lin_proj=lin_proj, want_o_lr=trace, H_local=H, nonfinite=nonfinite)
     return Prepared(q=q, k=k, v=v, sel=sel, y_lr=y_lr, o_lr=o_lr, g_logit=g_logit, block=block, perm=perm)
 
 
@@ -608,7 +610,7 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
             params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False, impl: str = "auto",
             head_offset: int = 0, gate_reduce: Optional[Callable[[torch.Tensor], None]] = None,
-            rope: Optional[RopeConfig] = None):
+            rope: Optional[RopeConfig] = None, check_finite: bool = False):
     """RoPeSLR forward (mechanism.py:491-512, Algorithm 1).
 
     q, k, v: post-RoPE [B, H, L, d] (bf16 or f32); x: token features
@@ -618,10 +620,18 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     With ``rope`` (a RopeConfig), q and k are the un-rotated projections and
     the fused RoPE + pooling pre-pass rotates them on the way in.
 
+    With ``check_finite`` a NaN or infinite value in Q, K or X raises
+    ValueError like the reference (linalg.py:17-20); the kernels flag it on
+    values they already reduce (block means, gate logits), and the check
+    costs one 4-byte read-back (a stream synchronisation).
+
     Returns the output [B, L, H*d] (x's dtype), or a ForwardTrace when
     ``trace`` (adds the float32 branch outputs, the gate and the masks)."""
+    flag = torch.zeros(1, dtype=torch.int32, device=q.device) if check_finite else None
     prep = prepare(q, k, v, x, grid, params, settings, pe, lin_proj=lin_proj, trace=trace, head_offset=head_offset,
-                   rope=rope)
+                   rope=rope, nonfinite=flag)
+    if flag is not None:
+        raise_nonfinite(flag)
     if gate_reduce is not None:
         gate_reduce(prep.g_logit)
     out, o_sparse = attend(prep, params, settings, impl=impl, want_o_sparse=trace)
@@ -631,6 +641,14 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     sparsity = 1.0 - prep.sel.attended.to(torch.float64) / float(L) ** 2
     return ForwardTrace(output=out, o_sparse=o_sparse, o_lowrank=prep.o_lr, g=torch.sigmoid(prep.g_logit + params.b_g),
                         sparsity=sparsity, selected=prep.sel.mask, attended=prep.sel.attended)
+
+
+def raise_nonfinite(flag: torch.Tensor) -> None:
+    """ValueError when a kernel flagged non-finite inputs (linalg.py:17-20)."""
+    bits = int(flag.item())
+    if bits:
+        what = [n for b, n in ((_lib.NONFINITE_QK, "Q/K"), (_lib.NONFINITE_X, "X")) if bits & b]
+        raise ValueError(f"input contains non-finite values ({', '.join(what)})")
 
 
 def project_and_rotate(x: torch.Tensor, grid: GridShape, cfg: RopeConfig, backbone: Backbone,
@@ -709,10 +727,11 @@ def forward_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Ten
     if out.is_cuda or out.shape[:2] != (B, L) or out.shape[2] < H * d or out.stride(2) != 1 or out.dtype != q.dtype:
         raise ValueError("out must be a host tensor [B, L, >= H*d] of the input dtype")
     attended = torch.zeros((B, H), dtype=torch.int64) if want_attended else None
-    tok = _token_args(x, grid, params, pe, settings.use_pe, head_offset, H, d)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)  # non-finite inputs (linalg.py:17-20)
+    tok = _token_args(x, grid, params, pe, settings.use_pe, head_offset, H, d, flag)
     args = _lib.HostForward()
     args.shape = _lib.Shape(B, H, L, d, settings.sparse.block, _dtype_code(q))
-    args.sel = _lib.SelectParams(int(settings.sparse.topk), float(settings.sparse.keep))
+    args.sel = _lib.SelectParams(int(settings.sparse.topk), float(settings.sparse.keep), flag.data_ptr())
     args.q, args.k, args.v = q.data_ptr(), k.data_ptr(), v.data_ptr()
     args.tok = tok
     args.w_a, args.w_b, args.rank = params.w_a.data_ptr(), params.w_b.data_ptr(), params.rank
@@ -748,6 +767,7 @@ def forward_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Ten
             raise hook_error[0]
         if sync:
             torch.cuda.current_stream(dev).synchronize()
+            raise_nonfinite(flag)
         else:
             # keep the workspace alive until the stream reaches this point
             ws.record_stream(torch.cuda.current_stream(dev))

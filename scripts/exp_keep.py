@@ -31,7 +31,6 @@ run(P.ForwardSettings(P.SparseSettings.for_sparsity(64, L, 0.9)), "top-51 (90%)"
 from test_gpu_parity import _skew_blocks
 q, k = _skew_blocks(q, k, 64, spread=float(os.environ.get("EXP_SPREAD", "2.0")))
 for keep in (0.5, 0.8):
-    for sched in ("1", "0"):
-        os.environ["ROPESLR_SCHEDULE"] = sched
-        run(P.ForwardSettings(P.SparseSettings(64, keep=keep)), f"skew keep {keep} sched {sched}")
-os.environ["ROPESLR_SCHEDULE"] = "1"
+    for sched in (1, 0):
+        with P._lib.option("schedule", sched):
+            run(P.ForwardSettings(P.SparseSettings(64, keep=keep)), f"skew keep {keep} sched {sched}")

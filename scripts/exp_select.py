@@ -12,7 +12,7 @@ L = grid.size
 sp = P.SparseSettings.for_sparsity(128, L, 0.9)
 res = {}
 for mode in ("fma", "dmma", "fma", "dmma"):
-    os.environ["ROPESLR_SCORES"] = mode
+    P._lib.set_option("scores", mode[0])
     for _ in range(2):
         sel = P.select_blocks(q, k, sp)
     torch.cuda.synchronize()

@@ -4,11 +4,14 @@ seeded full-size inputs, tolerance metrics."""
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
 
 import restated as R
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # BASELINE north star: masks bit-exact; bf16 outputs within max-abs 2e-2 and
 # mean-relative 1e-2 of the float64 reference.  float32 runs get 1e-4.

@@ -90,7 +90,7 @@ def test_lowrank_generic_d64_vs_oracle():
 
 
 @pytest.mark.parametrize("L_grid", [(2, 25, 50), (1, 8, 16)])
-def test_linear_branch_tensor_cores_vs_oracle(L_grid, monkeypatch):
+def test_linear_branch_tensor_cores_vs_oracle(L_grid):
     """K3 linear mode (mechanism.py:33-36, 347-362) on the tensor cores
     (linear_tc.cu: bf16, d = 128) against the float64 oracle, with a token
     count that is ragged for both the 1024-token state chunks and the
@@ -105,9 +105,9 @@ def test_linear_branch_tensor_cores_vs_oracle(L_grid, monkeypatch):
     st = P.ForwardSettings(P.SparseSettings(block=64, topk=1), compensator="linear")
     outs = {}
     for mode in ("tc", "simt"):
-        monkeypatch.setenv("ROPESLR_LINEAR", mode)
-        y_lr, o_lr, _ = P.compensator_branch(x, grid, params, st, pe, lin_proj=lin, want_o_lr=True)
-        torch.cuda.synchronize()
+        with P._lib.option("linear_simt", int(mode == "simt")):
+            y_lr, o_lr, _ = P.compensator_branch(x, grid, params, st, pe, lin_proj=lin, want_o_lr=True)
+            torch.cuda.synchronize()
         outs[mode] = (y_lr.float().cpu().numpy(), o_lr.cpu().numpy())
     rms = params.rms_lowrank.double().cpu().numpy()
     for b in range(B):

@@ -250,7 +250,7 @@ def _skew_blocks(q, k, block, seed=1, strength=4.0, spread=2.0):
 
 
 @pytest.mark.parametrize("block", [64, 128])
-def test_keep_schedule_bit_identical(block, monkeypatch):
+def test_keep_schedule_bit_identical(block):
     """The longest-first unit schedule (schedule_units_kernel) only changes
     which CTA runs a (head, query block): the output is bit-identical to the
     unscheduled launch, every row is written, and the counts really vary."""
@@ -264,11 +264,11 @@ def test_keep_schedule_bit_identical(block, monkeypatch):
     assert cnt.max() > 2 * cnt.min(), "skewed inputs should give uneven block counts"
     B, H, L, d = q.shape
     outs = []
-    for sched in ("1", "0"):
-        monkeypatch.setenv("ROPESLR_SCHEDULE", sched)
-        out = torch.full((B, L, H, d), float("nan"), dtype=q.dtype, device=q.device)
-        P.attend(prep, params, st, out=out)
-        torch.cuda.synchronize()
+    for sched in (1, 0):
+        with P._lib.option("schedule", sched):
+            out = torch.full((B, L, H, d), float("nan"), dtype=q.dtype, device=q.device)
+            P.attend(prep, params, st, out=out)
+            torch.cuda.synchronize()
         outs.append(out)
     assert torch.isfinite(outs[0].float()).all()
     assert torch.equal(outs[0], outs[1])
@@ -276,7 +276,7 @@ def test_keep_schedule_bit_identical(block, monkeypatch):
 
 @pytest.mark.parametrize("scale", [1.0, 4.0, 12.0])
 @pytest.mark.parametrize("block", [64, 128])
-def test_fixed_reference_extreme_logits(scale, block, monkeypatch):
+def test_fixed_reference_extreme_logits(scale, block):
     """The fixed-reference K2 (sparse_attn_fixed_kernel) picks one exponent
     reference per row and unit; rows whose scores span too many binary
     orders for it are recomputed by the running-max kernel.  Q and K scaled
@@ -293,9 +293,9 @@ def test_fixed_reference_extreme_logits(scale, block, monkeypatch):
     prep = P.prepare(q, k, v, x, grid, params, st, pe)
     outs = {}
     for mode in ("fixed", "online"):
-        monkeypatch.setenv("ROPESLR_K2", mode)
-        out, o_sp = P.attend(prep, params, st, want_o_sparse=True)
-        torch.cuda.synchronize()
+        with P._lib.option("k2_online", int(mode == "online")):
+            out, o_sp = P.attend(prep, params, st, want_o_sparse=True)
+            torch.cuda.synchronize()
         outs[mode] = (out.clone(), o_sp.clone())
     ref_out, ref_sel = _oracle_sparse(q, k, v, block, topk=6)
     got = outs["fixed"][1][0].cpu().numpy()
@@ -307,7 +307,7 @@ def test_fixed_reference_extreme_logits(scale, block, monkeypatch):
         assert torch.equal(outs["fixed"][1], outs["online"][1])
 
 
-def test_fixed_reference_partial_fallback(monkeypatch):
+def test_fixed_reference_partial_fallback():
     """One head with extreme logits (every one of its units falls back to the
     running-max kernel) next to normal heads (none does), in the same launch,
     with and without the unit schedule: the fallen-back head equals the
@@ -323,10 +323,9 @@ def test_fixed_reference_partial_fallback(monkeypatch):
     ref_out, _ = _oracle_sparse(q, k, v, 128, topk=5)
     res = {}
     for mode, sched in (("fixed", "0"), ("fixed", "1"), ("online", "0")):
-        monkeypatch.setenv("ROPESLR_K2", mode)
-        monkeypatch.setenv("ROPESLR_SCHEDULE", sched)
-        _, o_sp = P.attend(prep, params, st, want_o_sparse=True)
-        torch.cuda.synchronize()
+        with P._lib.option("k2_online", int(mode == "online")), P._lib.option("schedule", int(sched)):
+            _, o_sp = P.attend(prep, params, st, want_o_sparse=True)
+            torch.cuda.synchronize()
         res[(mode, sched)] = o_sp.clone()
     for key in (("fixed", "0"), ("fixed", "1")):
         got = res[key][0].cpu().numpy()
