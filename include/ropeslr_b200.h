@@ -130,6 +130,8 @@ int64_t ropeslr_num_blocks(int64_t L, int32_t block);
  *   "scores"        'f' / 'd': CUDA-core / unpipelined DMMA block scores
  *   "rope_tma"      0: the row-bulk-copy RoPE pre-pass
  *   "linear_simt"   1: the CUDA-core linear compensator
+ *   "select"        'r': the radix-select top-k kernel instead of the value-bin one
+ *   "k1_pipeline"   0: K1's pooling / scores / selection in sequence, not head-group pipelined
  * Not synchronised with calls in flight on other threads.  Unknown name:
  * ROPESLR_ERR_VALUE.  ropeslr_get_option returns the current value. */
 int ropeslr_set_option(const char* name, int value);
@@ -141,7 +143,10 @@ int ropeslr_get_option(const char* name);
  * stable descending order (ties to the lower block index), top-k or
  * cumulative-mass count, ascending index list.  `mask` and `scores`
  * ([B,H,nb,nb] float64) may be NULL.  kmax must be >= min(topk, nb) in top-k
- * mode and >= nb in keep mode. */
+ * mode and >= nb in keep mode.  Large problems are pipelined by head groups:
+ * the pooling of one group runs on `stream` while the scores and selection
+ * of the previous group run on an internal side stream (one per device,
+ * forked from and joined back to `stream` with events, capture-safe). */
 size_t ropeslr_select_workspace_bytes(const ropeslr_shape* shape);
 int ropeslr_select_blocks(const ropeslr_shape* shape, const ropeslr_select_params* sel,
                           const void* q, const void* k,

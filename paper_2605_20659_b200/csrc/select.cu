@@ -22,13 +22,18 @@
 
 namespace ropeslr {
 
+// exp(x) of a float64 is 0 below this: a block whose score is that far below
+// the row max has probability 0 in the reference (mechanism.py:310-311), and
+// all such blocks tie in its stable order (mechanism.py:317)
+constexpr double kProbUnderflow = -745.1332191019412;
+
 // grid (nb, B*H, 2): z = 0 pools Q, z = 1 pools K.  pooled: [2][BH][nb][d].
 template <typename T>
 __global__ void __launch_bounds__(256) pool_blocks_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                           double* __restrict__ pooled, int64_t L, int d, int block,
-                                                          int nb, int64_t BH) {
+                                                          int nb, int64_t BH, int64_t bh0) {
   extern __shared__ double sred[];
-  const int64_t bh = blockIdx.y;
+  const int64_t bh = bh0 + blockIdx.y;
   const T* src = (blockIdx.z == 0 ? q : k) + bh * L * d;
   const int b = blockIdx.x;
   const int rows = block_size(L, block, b);
@@ -80,11 +85,11 @@ __global__ void __launch_bounds__(256) pool_blocks_kernel(const T* __restrict__ 
 __global__ void __launch_bounds__(256) pool_blocks_bulk_kernel(const __nv_bfloat16* __restrict__ q,
                                                                const __nv_bfloat16* __restrict__ k,
                                                                double* __restrict__ pooled, int64_t L, int block,
-                                                               int nb, int64_t BH) {
+                                                               int nb, int64_t BH, int64_t bh0) {
   constexpr int D = 128;
   __shared__ __align__(128) uint8_t buf[128 * D * 2];  // the block's rows; then the f64 partial sums
   __shared__ uint64_t bar;
-  const int64_t bh = blockIdx.y;
+  const int64_t bh = bh0 + blockIdx.y;
   const __nv_bfloat16* src = (blockIdx.z == 0 ? q : k) + bh * L * D;
   const int b = blockIdx.x;
   const int rows = block_size(L, block, b);
@@ -129,10 +134,10 @@ __global__ void __launch_bounds__(256) pool_blocks_bulk_kernel(const __nv_bfloat
 // scores[bh, i, j] = dot(pooled_q[bh, i], pooled_k[bh, j]) / sqrt(d), float64.
 // 64x64 output tile per CTA, 4x4 per thread, k-chunks of 16 staged in smem.
 __global__ void __launch_bounds__(256) block_scores_kernel(const double* __restrict__ pooled, double* __restrict__ scores,
-                                                           int nb, int d, int64_t BH, double sqrt_d) {
+                                                           int nb, int d, int64_t BH, double sqrt_d, int64_t bh0) {
   __shared__ double As[16][64 + 1];
   __shared__ double Bs[16][64 + 1];
-  const int64_t bh = blockIdx.z;
+  const int64_t bh = bh0 + blockIdx.z;
   const double* pq = pooled + bh * nb * d;
   const double* pk = pooled + (BH + bh) * nb * d;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
@@ -191,11 +196,11 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 
 __global__ void __launch_bounds__(128) block_scores_dmma_kernel(const double* __restrict__ pooled,
                                                                 double* __restrict__ scores, int nb, int d,
-                                                                int64_t BH, double sqrt_d) {
+                                                                int64_t BH, double sqrt_d, int64_t bh0) {
   constexpr int KC = 32;
   __shared__ double As[KC][64 + 1];
   __shared__ double Bs[KC][64 + 1];
-  const int64_t bh = blockIdx.z;
+  const int64_t bh = bh0 + blockIdx.z;
   const double* pq = pooled + bh * nb * d;
   const double* pk = pooled + (BH + bh) * nb * d;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
@@ -267,10 +272,10 @@ __device__ __forceinline__ void cp16(double* dst, const double* src, bool valid)
 
 __global__ void __launch_bounds__(128) block_scores_dmma_pipe_kernel(const double* __restrict__ pooled,
                                                                      double* __restrict__ scores, int nb, int d,
-                                                                     int64_t BH, double sqrt_d) {
+                                                                     int64_t BH, double sqrt_d, int64_t bh0) {
   using namespace sc;
   extern __shared__ __align__(16) double sbuf[];  // ST stages of [A 64 x PITCH | B 64 x PITCH]
-  const int64_t bh = blockIdx.z;
+  const int64_t bh = bh0 + blockIdx.z;
   const double* pq = pooled + bh * nb * d;
   const double* pk = pooled + (BH + bh) * nb * d;
   const int i0 = blockIdx.y * TILE, j0 = blockIdx.x * TILE;
@@ -366,9 +371,27 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 
+  // row max: scores below max + kProbUnderflow have probability 0 and tie
+  __shared__ double s_max;
+  {
+    double m = -INFINITY;
+    for (int i = tid; i < nb; i += blockDim.x) m = fmax(m, srow[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_red[warp] = m;
+    __syncthreads();
+    if (tid == 0) {
+      double t = s_red[0];
+      for (int w = 1; w < (int)(blockDim.x / 32); ++w) t = fmax(t, s_red[w]);
+      s_max = t;
+    }
+    __syncthreads();
+  }
+  const double row_max = s_max;
   for (int i = tid; i < n2; i += blockDim.x) {
     if (i < nb) {
-      keys[i] = desc_key(srow[i]);
+      const double v = srow[i];
+      keys[i] = desc_key(v - row_max < kProbUnderflow ? -INFINITY : v);
       ids[i] = static_cast<uint32_t>(i);
     } else {
       keys[i] = ~0ull;
@@ -593,6 +616,221 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
   }
 }
 
+// Top-k rows by value bins, one warp per (bh, query block) row, nb <= 32 * NPER.
+//
+// The radix select above spends most of its time in the first digits: block
+// scores of one row share sign / exponent bits, so its shared-memory
+// histogram atomics all hit a few bins and serialise.  Here the bins are
+// linear in the VALUE over the row's [min, max] instead (256 bins; random
+// rows spread evenly), the bucket holding the k-th best score is found by a
+// descending scan, every key in a higher bin is kept, and the bucket is
+// refined the same way over its own range until it is small (<= kCand
+// keys), when an exact rank -- score descending, block index ascending on
+// equal scores, the stable order of mechanism.py:317 -- picks the rest.
+// The bin map floor((s/2 - lo/2) / span * 256) is monotone non-decreasing in
+// s, so a higher bin always holds strictly larger scores; exactness never
+// depends on the bin arithmetic, only on the float64 compares of the final
+// rank.  A bucket whose keys are all equal keeps its lowest block indices.
+namespace tb {
+constexpr int kWarps = 8;
+constexpr int kCand = 128;
+}  // namespace tb
+
+__device__ __forceinline__ double warp_min_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int NPER>
+__global__ void __launch_bounds__(256) select_topk_bins_kernel(const double* __restrict__ scores, int nb,
+                                                               int64_t row0, int64_t row1, int64_t L, int block,
+                                                               int topk, int kmax, int32_t* __restrict__ idx,
+                                                               int32_t* __restrict__ cnt, uint8_t* __restrict__ mask,
+                                                               unsigned long long* __restrict__ attended) {
+  __shared__ int hist_all[tb::kWarps][256];
+  __shared__ double cs_all[tb::kWarps][tb::kCand];
+  __shared__ int ci_all[tb::kWarps][tb::kCand];
+  __shared__ uint8_t pick_all[tb::kWarps][32 * NPER];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = row0 + static_cast<int64_t>(blockIdx.x) * tb::kWarps + warp;
+  if (row >= row1) return;
+  int* hist = hist_all[warp];
+  double* cs = cs_all[warp];
+  int* ci = ci_all[warp];
+  uint8_t* pick = pick_all[warp];
+  const int64_t bh = row / nb;
+  const int qb = static_cast<int>(row % nb);
+  const double* srow = scores + row * nb;
+  double s[NPER];
+  uint32_t active = 0, sel = 0;  // bit i: key lane + 32 i
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    double v = c < nb ? srow[c] : 0.0;
+    if (v != v) v = -INFINITY;  // NaN (non-finite inputs, flagged elsewhere) ranks last
+    s[i] = v;
+    if (c < nb) active |= 1u << i;
+  }
+  // the reference orders blocks by their softmax probability (mechanism.py:
+  // 310-317): scores more than ~745 below the row max give exp() == 0 in
+  // float64, so they all tie (and go by block index); clamp them to -inf
+  {
+    double mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (active >> i & 1) mx = fmax(mx, s[i]);
+    mx = warp_max_d(mx);
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (s[i] - mx < kProbUnderflow) s[i] = -INFINITY;
+  }
+  int need = topk < nb ? topk : nb;
+#pragma unroll 1
+  while (need > 0) {
+    double lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (active >> i & 1) {
+        lo = fmin(lo, s[i]);
+        hi = fmax(hi, s[i]);
+      }
+    lo = warp_min_d(lo);
+    hi = warp_max_d(hi);
+    const int count = __reduce_add_sync(0xffffffffu, __popc(active));
+    if (count == need) {  // the rest of the bucket, whole
+      sel |= active;
+      break;
+    }
+    if (!(hi > lo)) {  // every remaining key is equal (or -inf): lowest block indices
+      int taken = 0;
+#pragma unroll
+      for (int i = 0; i < NPER; ++i) {
+        const bool a = active >> i & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, a);
+        if (a && taken + __popc(bal & ((1u << lane) - 1u)) < need) sel |= 1u << i;
+        taken += __popc(bal);
+      }
+      break;
+    }
+    if (count <= tb::kCand) {  // exact rank among the candidates
+      int base = 0;
+#pragma unroll
+      for (int i = 0; i < NPER; ++i) {
+        const bool a = active >> i & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, a);
+        if (a) {
+          const int pos = base + __popc(bal & ((1u << lane) - 1u));
+          cs[pos] = s[i];
+          ci[pos] = lane + 32 * i;
+        }
+        base += __popc(bal);
+      }
+      __syncwarp();
+      for (int j = lane; j < count; j += 32) {
+        const double v = cs[j];
+        const int id = ci[j];
+        int rank = 0;
+        for (int m = 0; m < count; ++m) {
+          const double w = cs[m];
+          rank += (w > v) || (w == v && ci[m] < id);
+        }
+        pick[id] = rank < need;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NPER; ++i)
+        if ((active >> i & 1) && pick[lane + 32 * i]) sel |= 1u << i;
+      break;
+    }
+    // one level of value bins over [lo, hi]
+    const double half_lo = 0.5 * lo, span = 0.5 * hi - half_lo;
+    const double scale = 256.0 / span;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (active >> i & 1) {
+        const double t = (0.5 * s[i] - half_lo) * scale;
+        const int bin = t >= 255.0 ? 255 : static_cast<int>(t);
+        atomicAdd(&hist[bin], 1);
+      }
+    __syncwarp();
+    int h8[8];
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      h8[i] = hist[lane * 8 + i];
+      tot += h8[i];
+    }
+    // descending order of bins: inclusive suffix sum over lanes
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_down_sync(0xffffffffu, incl, o);
+      if (lane + o < 32) incl += t;
+    }
+    const int excl = incl - tot;
+    const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
+    const int src = 31 - __clz(owner);  // the unique owner (suffix sums are monotone)
+    int bucket = 0, above = 0;
+    if (lane == src) {
+      int run = excl;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        if (run + h8[i] >= need) {
+          bucket = lane * 8 + i;
+          above = run;
+          break;
+        }
+        run += h8[i];
+      }
+    }
+    bucket = __shfl_sync(0xffffffffu, bucket, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    need -= above;
+    uint32_t next = 0;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (active >> i & 1) {
+        const double t = (0.5 * s[i] - half_lo) * scale;
+        const int bin = t >= 255.0 ? 255 : static_cast<int>(t);
+        if (bin > bucket) sel |= 1u << i;
+        else if (bin == bucket) next |= 1u << i;
+      }
+    active = next;
+    __syncwarp();
+  }
+  int32_t* irow = idx + row * kmax;
+  uint8_t* mrow = mask ? mask + row * nb : nullptr;
+  int carry = 0;
+  long long ksum = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    const bool si = sel >> i & 1;
+    const unsigned bal = __ballot_sync(0xffffffffu, si);
+    if (si) {
+      irow[carry + __popc(bal & ((1u << lane) - 1u))] = c;
+      ksum += block_size(L, block, c);
+    }
+    if (mrow && c < nb) mrow[c] = si ? 1 : 0;
+    carry += __popc(bal);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+  if (lane == 0) {
+    cnt[row] = carry;
+    atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
+  }
+}
+
 }  // namespace ropeslr
 
 using namespace ropeslr;
@@ -630,40 +868,59 @@ static size_t scores_bytes(const ropeslr_shape* s) {
   return ((static_cast<size_t>(s->B * s->H * nb * nb) * sizeof(double) + 255) / 256) * 256;
 }
 
-// Scores from the pooled means, then top-k / cumulative-mass selection.
-static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
-                              int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
-                              double* scores, cudaStream_t st) {
-  const int64_t BH = s->B * s->H;
-  const int d = static_cast<int>(s->d);
+// Scores of heads [bh0, bh1) from the pooled means.
+static int launch_scores(const double* pooled, double* scores, int nb, int d, int64_t BH, int64_t bh0, int64_t bh1,
+                         cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
+            static_cast<unsigned>(bh1 - bh0));
+  const double sq = sqrt(static_cast<double>(d));
+  // scores = 'f': the CUDA-core kernel, 'd': the unpipelined DMMA kernel (A/B timing)
+  const char e = tuning().scores;
+  if (e == 'f') {
+    block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sq, bh0);
+  } else if (d % sc::KC == 0 && e != 'd') {
+    // opt in above 48 KiB of dynamic shared memory on every call (per-device attribute)
+    if (cudaFuncSetAttribute(block_scores_dmma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             sc::ST * sc::STAGE_DOUBLES * static_cast<int>(sizeof(double))) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
+    block_scores_dmma_pipe_kernel<<<grid, 128, sc::ST * sc::STAGE_DOUBLES * sizeof(double), st>>>(
+        pooled, scores, nb, d, BH, sq, bh0);
+  } else {
+    block_scores_dmma_kernel<<<grid, 128, 0, st>>>(pooled, scores, nb, d, BH, sq, bh0);
+  }
+  return launch_status();
+}
+
+// Selection of the rows of heads [bh0, bh1).
+static int launch_select(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* scores, int32_t* idx,
+                         int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended, int64_t bh0, int64_t bh1,
+                         cudaStream_t st) {
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
-  if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-  if (int e = scan_nonfinite(pooled, true, 2 * BH * nb * d, sel->nonfinite, ROPESLR_NONFINITE_QK, st)) return e;
-  {
-    dim3 grid(static_cast<unsigned>(ceil_div(nb, 64)), static_cast<unsigned>(ceil_div(nb, 64)),
-              static_cast<unsigned>(BH));
-    // ROPESLR_SCORES=fma: the CUDA-core kernel, =dmma: the unpipelined DMMA kernel (A/B timing)
-    const char e = tuning().scores;
-    if (e == 'f')
-      block_scores_kernel<<<grid, 256, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
-    else if (d % sc::KC == 0 && e != 'd') {
-      // opt in above 48 KiB of dynamic shared memory on every call (per-device attribute)
-      if (cudaFuncSetAttribute(block_scores_dmma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               sc::ST * sc::STAGE_DOUBLES * static_cast<int>(sizeof(double))) != cudaSuccess)
-        return ROPESLR_ERR_LAUNCH;
-      block_scores_dmma_pipe_kernel<<<grid, 128, sc::ST * sc::STAGE_DOUBLES * sizeof(double), st>>>(
-          pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
-    } else
-      block_scores_dmma_kernel<<<grid, 128, 0, st>>>(pooled, scores, nb, d, BH, sqrt(static_cast<double>(d)));
-    if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  auto* att = reinterpret_cast<unsigned long long*>(attended);
+  const int64_t row0 = bh0 * nb, row1 = bh1 * nb;
+  if (sel->topk > 0 && nb <= 1024 && tuning().select == 'r') {  // the radix-select kernel (A/B timing)
+    const int64_t off = row0, rows = row1 - row0;
+    const unsigned grid = static_cast<unsigned>(ceil_div(rows, 8));
+#define ROPESLR_SEL_CASE(NPER_)                                                                            \
+  select_topk_warp_kernel<NPER_><<<grid, 256, 0, st>>>(scores + off * nb, nb, rows, s->L, s->block, sel->topk, \
+                                                        kmax, idx + off * kmax, cnt + off,                    \
+                                                        mask ? mask + off * nb : nullptr, att + bh0)
+    if (nb <= 128)
+      ROPESLR_SEL_CASE(4);
+    else if (nb <= 256)
+      ROPESLR_SEL_CASE(8);
+    else if (nb <= 512)
+      ROPESLR_SEL_CASE(16);
+    else
+      ROPESLR_SEL_CASE(32);
+#undef ROPESLR_SEL_CASE
+    return launch_status();
   }
   if (sel->topk > 0 && nb <= 1024) {
-    const int64_t rows = BH * nb;
-    const unsigned grid = static_cast<unsigned>(ceil_div(rows, 8));
-    auto* att = reinterpret_cast<unsigned long long*>(attended);
-#define ROPESLR_SEL_CASE(NPER_)                                                                                 \
-  select_topk_warp_kernel<NPER_><<<grid, 256, 0, st>>>(scores, nb, rows, s->L, s->block, sel->topk, kmax, idx, \
-                                                        cnt, mask, att)
+    const unsigned grid = static_cast<unsigned>(ceil_div(row1 - row0, tb::kWarps));
+#define ROPESLR_SEL_CASE(NPER_)                                                                              \
+  select_topk_bins_kernel<NPER_><<<grid, 32 * tb::kWarps, 0, st>>>(scores, nb, row0, row1, s->L, s->block,   \
+                                                                   sel->topk, kmax, idx, cnt, mask, att)
     if (nb <= 128)
       ROPESLR_SEL_CASE(4);
     else if (nb <= 256)
@@ -683,9 +940,47 @@ static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_param
                              static_cast<int>(sm)) != cudaSuccess)
       return ROPESLR_ERR_LAUNCH;
   }
-  select_rows_kernel<<<static_cast<unsigned>(BH * nb), 256, sm, st>>>(
-      scores, nb, n2, s->L, s->block, sel->topk, sel->keep, kmax, idx, cnt, mask,
-      reinterpret_cast<unsigned long long*>(attended));
+  // select_rows_kernel takes the absolute row from blockIdx.x: offset the pointers of the head range instead
+  const int64_t off = row0;
+  select_rows_kernel<<<static_cast<unsigned>(row1 - row0), 256, sm, st>>>(
+      scores + off * nb, nb, n2, s->L, s->block, sel->topk, sel->keep, kmax, idx + off * kmax, cnt + off,
+      mask ? mask + off * nb : nullptr, att + bh0);
+  return launch_status();
+}
+
+// Scores from the pooled means, then top-k / cumulative-mass selection.
+static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
+                              int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
+                              double* scores, cudaStream_t st) {
+  const int64_t BH = s->B * s->H;
+  const int d = static_cast<int>(s->d);
+  const int nb = static_cast<int>(ceil_div(s->L, s->block));
+  if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  if (int e = scan_nonfinite(pooled, true, 2 * BH * nb * d, sel->nonfinite, ROPESLR_NONFINITE_QK, st)) return e;
+  if (int e = launch_scores(pooled, scores, nb, d, BH, 0, BH, st)) return e;
+  return launch_select(s, sel, scores, idx, kmax, cnt, mask, attended, 0, BH, st);
+}
+
+static int launch_pool(const ropeslr_shape* s, const void* q, const void* k, double* pooled, int64_t bh0, int64_t bh1,
+                       cudaStream_t st) {
+  const int64_t BH = s->B * s->H;
+  const int d = static_cast<int>(s->d);
+  const int nb = static_cast<int>(ceil_div(s->L, s->block));
+  dim3 grid(nb, static_cast<unsigned>(bh1 - bh0), 2);
+  const int chunks = d / 8;
+  const int lanes_r = 256 / chunks;
+  size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
+  if (s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128 && aligned16(q) && aligned16(k))
+    pool_blocks_bulk_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                   static_cast<const __nv_bfloat16*>(k), pooled, s->L, s->block, nb,
+                                                   BH, bh0);
+  else if (s->dtype == ROPESLR_BF16)
+    pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
+                                                              static_cast<const __nv_bfloat16*>(k), pooled, s->L, d,
+                                                              s->block, nb, BH, bh0);
+  else
+    pool_blocks_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q), static_cast<const float*>(k),
+                                                      pooled, s->L, d, s->block, nb, BH, bh0);
   return launch_status();
 }
 
@@ -697,6 +992,15 @@ extern "C" size_t ropeslr_select_workspace_bytes(const ropeslr_shape* s) {
 extern "C" size_t ropeslr_select_pooled_workspace_bytes(const ropeslr_shape* s) {
   if (s == nullptr || s->block <= 0) return 0;
   return scores_bytes(s);
+}
+
+// Head groups of the pipelined selection: the pooling (HBM-bound) of group
+// g + 1 runs on the caller's stream while the scores (FP64 tensor pipe) and
+// the selection (integer pipe) of group g run on a side stream, so the
+// three bounds overlap instead of adding up.  Small problems run unsplit.
+static int pipeline_groups(int64_t BH, int nb) {
+  if (!tuning().k1_pipeline || BH < 4 || static_cast<int64_t>(nb) * nb < 128 * 128) return 1;
+  return BH >= 8 ? 4 : 2;
 }
 
 extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_select_params* sel, const void* q,
@@ -714,25 +1018,31 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
   double* pooled = static_cast<double*>(ws);
   double* scores = scores_out ? scores_out : reinterpret_cast<double*>(static_cast<char*>(ws) + pooled_bytes(s));
-  {
-    dim3 grid(nb, static_cast<unsigned>(BH), 2);
-    const int chunks = d / 8;
-    const int lanes_r = 256 / chunks;
-    size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
-    if (s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128 && aligned16(q) && aligned16(k))
-      pool_blocks_bulk_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                                     static_cast<const __nv_bfloat16*>(k), pooled, s->L, s->block,
-                                                     nb, BH);
-    else if (s->dtype == ROPESLR_BF16)
-      pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
-                                                                static_cast<const __nv_bfloat16*>(k), pooled, s->L,
-                                                                d, s->block, nb, BH);
-    else
-      pool_blocks_kernel<float><<<grid, 256, sm, st>>>(static_cast<const float*>(q), static_cast<const float*>(k),
-                                                        pooled, s->L, d, s->block, nb, BH);
-    if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  const int G = pipeline_groups(BH, nb);
+  if (G == 1) {
+    if (int e = launch_pool(s, q, k, pooled, 0, BH, st)) return e;
+    return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores, st);
   }
-  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores, st);
+  if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  AuxStream aux;
+  if (int e = aux.fork(st)) return e;
+  for (int g = 0; g < G; ++g) {
+    const int64_t b0 = BH * g / G, b1 = BH * (g + 1) / G;
+    if (int e = launch_pool(s, q, k, pooled, b0, b1, st)) return e;
+    if (int e = aux.wait_main()) return e;  // pool of group g (and the memset) done
+    // the non-finite scan over this group's Q and K means (both halves of pooled)
+    if (sel->nonfinite) {
+      if (int e = scan_nonfinite(pooled + b0 * nb * d, true, (b1 - b0) * nb * d, sel->nonfinite,
+                                 ROPESLR_NONFINITE_QK, aux.stream))
+        return e;
+      if (int e = scan_nonfinite(pooled + (BH + b0) * nb * d, true, (b1 - b0) * nb * d, sel->nonfinite,
+                                 ROPESLR_NONFINITE_QK, aux.stream))
+        return e;
+    }
+    if (int e = launch_scores(pooled, scores, nb, d, BH, b0, b1, aux.stream)) return e;
+    if (int e = launch_select(s, sel, scores, idx, kmax, cnt, mask, attended, b0, b1, aux.stream)) return e;
+  }
+  return aux.join();
 }
 
 extern "C" int ropeslr_select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel,

@@ -1,6 +1,6 @@
-"""K1 experiments: time the selection (pool + scores + top-k) at the config-3
-shape, CUDA-core vs DMMA block scores (ROPESLR_SCORES), and check that both
-give the same index lists."""
+"""K1 experiments at the config-3 shape: time the selection (pool + scores +
+top-k) with the value-bin vs radix top-k kernel and with / without the
+head-group pipeline, and check every variant gives the same index lists."""
 import os, sys
 sys.path[:0] = ['.', 'tests', 'oracle']
 import torch
@@ -11,17 +11,32 @@ q, k, v, x, params, pe, grid = G.make_full_inputs((33, 45, 80), H, 128, (16, 56,
 L = grid.size
 sp = P.SparseSettings.for_sparsity(128, L, 0.9)
 res = {}
-for mode in ("fma", "dmma", "fma", "dmma"):
-    P._lib.set_option("scores", mode[0])
-    for _ in range(2):
-        sel = P.select_blocks(q, k, sp)
+
+
+def timed(fn, n=20):
+    for _ in range(3):
+        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(10):
-        sel = P.select_blocks(q, k, sp)
+    for _ in range(n):
+        fn()
     e1.record()
     torch.cuda.synchronize()
-    print(f"{mode:5s} select_blocks {e0.elapsed_time(e1) / 10:.3f} ms", flush=True)
-    res[mode] = sel.idx.clone()
-print("identical index lists:", torch.equal(res["fma"], res["dmma"]))
+    return e0.elapsed_time(e1) / n
+
+
+for rep in range(2):
+    for sel in ("bins", "radix"):
+        for pipe in (1, 0):
+            with P._lib.option("select", "r" if sel == "radix" else 0), P._lib.option("k1_pipeline", pipe):
+                ms = timed(lambda: P.select_blocks(q, k, sp, want_mask=False))
+                out = P.select_blocks(q, k, sp, want_mask=False)
+            torch.cuda.synchronize()
+            print(f"select={sel:5s} pipeline={pipe} select_blocks {ms:.3f} ms", flush=True)
+            res[(sel, pipe)] = out.idx.clone()
+ref = res[("radix", 0)]
+print("identical index lists:", all(torch.equal(ref, t) for t in res.values()))
+# the stages alone
+pooled = torch.empty((2, H, -(-L // 128), 128), dtype=torch.float64, device=q.device)
+print(f"scores+select from pooled {timed(lambda: P.select_blocks(q, k, sp, want_mask=False, pooled=P.rope_pool(q, k, grid, P.RopeConfig(16, 56, 56), 128)[2])):.3f} ms (incl. rope_pool)")

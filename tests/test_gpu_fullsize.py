@@ -34,13 +34,13 @@ HUNYUAN = ((33, 45, 80), 24, 128, (16, 56, 56), 64)
 
 TOPK_CASES = {
     # name: (shape, block, sparsity, query blocks sampled per head)
-    "cfg2_wan_b64_s80": (WAN, 64, 0.80, 2),
-    "cfg1_cfg2_wan_b64_s90": (WAN, 64, 0.90, 3),
-    "cfg2_wan_b64_s95": (WAN, 64, 0.95, 2),
-    "cfg2_wan_b128_s80": (WAN, 128, 0.80, 2),
-    "cfg2_wan_b128_s90": (WAN, 128, 0.90, 2),
-    "cfg2_wan_b128_s95": (WAN, 128, 0.95, 2),
-    "cfg3_hunyuan_b128_s90": (HUNYUAN, 128, 0.90, 2),
+    "cfg2_wan_b64_s80": (WAN, 64, 0.80, 6),
+    "cfg1_cfg2_wan_b64_s90": (WAN, 64, 0.90, 16),
+    "cfg2_wan_b64_s95": (WAN, 64, 0.95, 6),
+    "cfg2_wan_b128_s80": (WAN, 128, 0.80, 6),
+    "cfg2_wan_b128_s90": (WAN, 128, 0.90, 6),
+    "cfg2_wan_b128_s95": (WAN, 128, 0.95, 6),
+    "cfg3_hunyuan_b128_s90": (HUNYUAN, 128, 0.90, 12),
 }
 
 KEEP_CASES = {
@@ -89,7 +89,7 @@ def keep_margin(probs_row: np.ndarray, order: np.ndarray, n_keep: int, keep: flo
     return float(m)
 
 
-def _check(name, shape, block, sel_kw, n_qb, q, k, v, x, params, pe, grid):
+def _check(name, shape, block, sel_kw, n_qb, q, k, v, x, params, pe, grid, skew=False):
     import paper_2605_20659_b200 as P
 
     grid_s, H, d, split, r = shape
@@ -136,8 +136,12 @@ def _check(name, shape, block, sel_kw, n_qb, q, k, v, x, params, pe, grid):
         ref_o = G.oracle_rows(qh, kh, vh, members, ref_sel, qbs)
         rows = np.concatenate([members[b] for b in qbs])
         o_gpu = o_sp[h].double().cpu().numpy()[rows]
-        scale = float(np.sqrt(np.mean(ref_o[rows] ** 2)))
-        G.assert_close(o_gpu / scale, ref_o[rows] / scale, "bf16", f"{name} h{h} o_sparse/rms")
+        # the raw branch relative to its own scale: rms for the flat block
+        # softmax of N(0,1) inputs; on skewed (peaked) rows a few keys carry
+        # the row and the bf16 P of the P.V MMA (2^-9 relative) scales with
+        # their |v|, so the bar is taken relative to max |o| there
+        scale = float(np.sqrt(np.mean(ref_o[rows] ** 2))) if not skew else float(np.max(np.abs(ref_o[rows])))
+        G.assert_close(o_gpu / scale, ref_o[rows] / scale, "bf16", f"{name} h{h} o_sparse/scale")
         y_ref, _, _ = G.oracle_fused_rows(rows, ref_o[rows], x_np, pe_np, params_np, grid_s, h, d)
         y_gpu = out_np[rows, h * d:(h + 1) * d]
         ma, mr = G.assert_close(y_gpu, y_ref, "bf16", f"{name} h{h} output")
@@ -150,7 +154,7 @@ def _check(name, shape, block, sel_kw, n_qb, q, k, v, x, params, pe, grid):
                "|cumulative mass - (keep - 1e-12)| at the decision",
                blocks_per_row=dict(min=int(counts_all.min()), max=int(counts_all.max()),
                                    mean=float(counts_all.mean())),
-               output_rows_checked_per_head=int(len(rows)), output_worst=worst,
+               output_rows_checked_per_head=int(len(rows)), output_worst=worst, skewed_inputs=skew,
                oracle_seconds=round(time.time() - t0, 1))
     _record(name, rec)
     print(json.dumps(rec))
@@ -177,4 +181,4 @@ def test_fullsize_keep_all_heads(name):
     q, k, v, x, params, pe, grid = _inputs(WAN)
     if skew:
         q, k = _skew_blocks(q, k, 64)
-    _check(name, WAN, 64, dict(keep=keep), 2, q, k, v, x, params, pe, grid)
+    _check(name, WAN, 64, dict(keep=keep), 4, q, k, v, x, params, pe, grid, skew=skew)

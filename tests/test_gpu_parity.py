@@ -333,3 +333,62 @@ def test_fixed_reference_partial_fallback():
             G.assert_close(got[h], ref_out[h], "bf16", f"o_sparse head {h} {key}")
         assert torch.equal(res[key][0, 1], res[("online", "0")][0, 1])
     assert torch.equal(res[("fixed", "0")], res[("fixed", "1")])
+
+
+def _crafted_scores_inputs(b_vals, a_vals, block=32, d=64):
+    """f32 Q/K whose block means are a_i * e0 and b_j * e0 exactly (constant
+    rows), so every block score a_i * b_j / sqrt(d) is one exact product on
+    both sides and the selection rule itself is what is compared."""
+    nb = len(b_vals)
+    L = nb * block
+    q = torch.zeros((1, 1, L, d), dtype=torch.float32)
+    k = torch.zeros((1, 1, L, d), dtype=torch.float32)
+    for i in range(nb):
+        q[0, 0, i * block:(i + 1) * block, 0] = float(a_vals[i])
+        k[0, 0, i * block:(i + 1) * block, 0] = float(b_vals[i])
+    return q.cuda(), k.cuda(), torch.zeros_like(q).cuda()
+
+
+@pytest.mark.parametrize("rule", [dict(topk=7), dict(topk=1), dict(keep=0.5), dict(keep=0.999)])
+@pytest.mark.parametrize("pattern", ["wide", "powers", "dups", "signed_zero"])
+def test_selection_extreme_and_tied_scores(pattern, rule):
+    """Selection on block scores with spreads far beyond the float64 exp
+    range (the reference's block probabilities underflow to 0 and tie, so
+    those blocks go by index), exact duplicates, powers of two and signed
+    zeros: masks bit-exact against the oracle (mechanism.py:309-320)."""
+    import paper_2605_20659_b200 as P
+
+    rng = np.random.default_rng(5)
+    nb = 40
+    if pattern == "wide":
+        b = rng.standard_normal(nb) * 3000.0
+    elif pattern == "powers":
+        b = np.array([(-1) ** j * 2.0 ** (j - 10) for j in range(nb)])
+    elif pattern == "dups":
+        b = rng.choice([-1.0, 0.0, 1.0, 2.0], size=nb)
+    else:
+        b = np.where(np.arange(nb) % 2 == 0, -0.0, 0.0)
+        b[[5, 17, 30]] = [1.0, 1.0, 0.5]
+    a = rng.standard_normal(nb) * 4.0
+    a[[3, 11]] = 0.0
+    q, k, v = _crafted_scores_inputs(b, a)
+    sp = P.SparseSettings(block=32, **rule)
+    sel = P.select_blocks(q, k, sp)
+    members = R.flat_block_members(q.shape[2], 32)
+    scores = R.block_scores(q[0, 0].double().cpu().numpy(), k[0, 0].double().cpu().numpy(), members)
+    ref_sel, _ = R.select_blocks(scores, **rule)
+    np.testing.assert_array_equal(sel.mask[0, 0].cpu().numpy(), ref_sel, err_msg=f"{pattern} {rule}")
+
+
+@pytest.mark.parametrize("kind", ["bins", "radix"])
+def test_topk_kernels_agree(kind):
+    """The value-bin top-k kernel (default) and the radix-select kernel give
+    identical index lists at a BASELINE-like shape."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((4, 32, 64), H=3)
+    sp = P.SparseSettings(block=64, topk=13)
+    with P._lib.option("select", "r" if kind == "radix" else 0):
+        a = P.select_blocks(q, k, sp)
+    b = P.select_blocks(q, k, sp)
+    assert torch.equal(a.idx, b.idx) and torch.equal(a.cnt, b.cnt) and torch.equal(a.attended, b.attended)
