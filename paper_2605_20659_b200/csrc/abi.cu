@@ -59,8 +59,13 @@ static cudaStream_t aux_stream_of_current_device() {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
   if (cache[dev] == nullptr) {
+    // highest priority: the side stream carries the compute-bound stages
+    // (K1 scores / selection), whose CTAs should be dispatched ahead of the
+    // HBM-bound kernel filling the rest of the SMs on the caller's stream
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
     cudaStream_t st = nullptr;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
     cache[dev] = st;
   }
   return cache[dev];

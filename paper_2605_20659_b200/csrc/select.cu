@@ -618,37 +618,122 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
 
 // Top-k rows by value bins, one warp per (bh, query block) row, nb <= 32 * NPER.
 //
-// The radix select above spends most of its time in the first digits: block
-// scores of one row share sign / exponent bits, so its shared-memory
-// histogram atomics all hit a few bins and serialise.  Here the bins are
-// linear in the VALUE over the row's [min, max] instead (256 bins; random
-// rows spread evenly), the bucket holding the k-th best score is found by a
-// descending scan, every key in a higher bin is kept, and the bucket is
-// refined the same way over its own range until it is small (<= kCand
-// keys), when an exact rank -- score descending, block index ascending on
-// equal scores, the stable order of mechanism.py:317 -- picks the rest.
-// The bin map floor((s/2 - lo/2) / span * 256) is monotone non-decreasing in
-// s, so a higher bin always holds strictly larger scores; exactness never
-// depends on the bin arithmetic, only on the float64 compares of the final
-// rank.  A bucket whose keys are all equal keeps its lowest block indices.
+// The radix select above spends most of its time in its first digits: the
+// block scores of a row share sign / exponent bits, so its histogram atomics
+// hit a few shared-memory bins and serialise.  Here the bins are linear in
+// the VALUE over the row's current [min, max] (256 bins; random rows spread
+// evenly), computed in float32: the float64 -> float32 rounding and the bin
+// map are both monotone non-decreasing, so a higher bin always holds
+// strictly larger float64 scores and exactness never depends on them.  Every
+// key in a bin above the one holding the k-th best is kept, and that bin is
+// refined over its own range until at most kCand keys remain; an exact rank
+// of those in float64 -- score descending, block index ascending on equal
+// scores, the stable order of mechanism.py:317 -- picks the rest.  Rows the
+// float32 map cannot separate (values beyond float32 range, or a bucket of
+// more than kCand keys that are equal in float32) finish with a radix select
+// on the order-preserving 64-bit keys, reloaded from the row.
 namespace tb {
 constexpr int kWarps = 8;
 constexpr int kCand = 128;
 }  // namespace tb
 
-__device__ __forceinline__ double warp_min_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 __device__ __forceinline__ double warp_max_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
+// Score of column c as the selection sees it: NaN (non-finite inputs, flagged
+// elsewhere) ranks last; a probability that underflows ties at -inf.
+__device__ __forceinline__ double sel_score(const double* srow, int c, double row_max) {
+  double v = srow[c];
+  if (v != v) v = -INFINITY;
+  return v - row_max < kProbUnderflow ? -INFINITY : v;
+}
+
+// Radix select of the `need` best of the active columns (bit i of `active`:
+// column lane + 32 i) on desc_key of sel_score, keys reloaded per pass.
 template <int NPER>
-__global__ void __launch_bounds__(256) select_topk_bins_kernel(const double* __restrict__ scores, int nb,
+__device__ __noinline__ uint32_t radix_select_active(const double* srow, double row_max, uint32_t active, int need, int* hist,
+                                        int lane) {
+  uint64_t prefix = 0, pmask = 0;
+  bool exact = false;
+#pragma unroll 1
+  for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (active >> i & 1) {
+        const uint64_t key = desc_key(sel_score(srow, lane + 32 * i, row_max));
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      }
+    __syncwarp();
+    int h8[8];
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      h8[i] = hist[lane * 8 + i];
+      tot += h8[i];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int excl = incl - tot;
+    const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
+    const int src = __ffs(owner) - 1;
+    int bucket = 0, before = 0, cnt_b = 0;
+    if (lane == src) {
+      int run = excl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (run + h8[i] >= need) {
+          bucket = lane * 8 + i;
+          before = run;
+          cnt_b = h8[i];
+          break;
+        }
+        run += h8[i];
+      }
+    }
+    bucket = __shfl_sync(0xffffffffu, bucket, src);
+    before = __shfl_sync(0xffffffffu, before, src);
+    cnt_b = __shfl_sync(0xffffffffu, cnt_b, src);
+    need -= before;
+    prefix |= static_cast<uint64_t>(bucket) << shift;
+    pmask |= 255ull << shift;
+    __syncwarp();
+    if (cnt_b == need) {
+      exact = true;
+      break;
+    }
+  }
+  uint32_t sel = 0;
+  int taken = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const bool a = active >> i & 1;
+    const uint64_t km = a ? desc_key(sel_score(srow, lane + 32 * i, row_max)) & pmask : ~0ull;
+    bool si = a && km < prefix;
+    const bool tie = a && km == prefix;
+    if (exact) {
+      si = si || tie;
+    } else {
+      const unsigned bal = __ballot_sync(0xffffffffu, tie);
+      si = si || (tie && taken + __popc(bal & ((1u << lane) - 1u)) < need);
+      taken += __popc(bal);
+    }
+    if (si) sel |= 1u << i;
+  }
+  return sel;
+}
+
+template <int NPER>
+__global__ void __launch_bounds__(256, 3) select_topk_bins_kernel(const double* __restrict__ scores, int nb,
                                                                int64_t row0, int64_t row1, int64_t L, int block,
                                                                int topk, int kmax, int32_t* __restrict__ idx,
                                                                int32_t* __restrict__ cnt, uint8_t* __restrict__ mask,
@@ -667,145 +752,160 @@ __global__ void __launch_bounds__(256) select_topk_bins_kernel(const double* __r
   const int64_t bh = row / nb;
   const int qb = static_cast<int>(row % nb);
   const double* srow = scores + row * nb;
-  double s[NPER];
-  uint32_t active = 0, sel = 0;  // bit i: key lane + 32 i
+  // row max (the probability-underflow reference), then float32 images
+  double row_max = -INFINITY;
 #pragma unroll
   for (int i = 0; i < NPER; ++i) {
     const int c = lane + 32 * i;
-    double v = c < nb ? srow[c] : 0.0;
-    if (v != v) v = -INFINITY;  // NaN (non-finite inputs, flagged elsewhere) ranks last
-    s[i] = v;
-    if (c < nb) active |= 1u << i;
+    if (c < nb) {
+      const double v = srow[c];
+      if (v == v) row_max = fmax(row_max, v);
+    }
   }
-  // the reference orders blocks by their softmax probability (mechanism.py:
-  // 310-317): scores more than ~745 below the row max give exp() == 0 in
-  // float64, so they all tie (and go by block index); clamp them to -inf
-  {
-    double mx = -INFINITY;
+  row_max = warp_max_d(row_max);
+  float f[NPER];
+  uint32_t fin = 0, ninf = 0;  // finite in float32 / tied at -inf (probability 0)
+  bool f32_safe = true;
 #pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (active >> i & 1) mx = fmax(mx, s[i]);
-    mx = warp_max_d(mx);
-#pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (s[i] - mx < kProbUnderflow) s[i] = -INFINITY;
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    f[i] = 0.f;
+    if (c < nb) {
+      const double v = sel_score(srow, c, row_max);
+      if (v == -INFINITY) {
+        ninf |= 1u << i;
+      } else {
+        f32_safe &= fabs(v) < 1e38;
+        f[i] = static_cast<float>(v);
+        fin |= 1u << i;
+      }
+    }
   }
+  f32_safe = __all_sync(0xffffffffu, f32_safe);
   int need = topk < nb ? topk : nb;
+  uint32_t sel = 0;
+  const int n_fin = __reduce_add_sync(0xffffffffu, __popc(fin));
+  if (need >= n_fin) {  // every finite key, then the -inf ties by block index
+    sel = fin;
+    need -= n_fin;
+    int taken = 0;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {
+      const bool a = ninf >> i & 1;
+      const unsigned bal = __ballot_sync(0xffffffffu, a);
+      if (a && taken + __popc(bal & ((1u << lane) - 1u)) < need) sel |= 1u << i;
+      taken += __popc(bal);
+    }
+  } else if (!f32_safe) {
+    sel = radix_select_active<NPER>(srow, row_max, fin, need, hist, lane);
+  } else {
+    uint32_t active = fin;
 #pragma unroll 1
-  while (need > 0) {
-    double lo = INFINITY, hi = -INFINITY;
+    while (true) {
+      float lo = INFINITY, hi = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (active >> i & 1) {
-        lo = fmin(lo, s[i]);
-        hi = fmax(hi, s[i]);
-      }
-    lo = warp_min_d(lo);
-    hi = warp_max_d(hi);
-    const int count = __reduce_add_sync(0xffffffffu, __popc(active));
-    if (count == need) {  // the rest of the bucket, whole
-      sel |= active;
-      break;
-    }
-    if (!(hi > lo)) {  // every remaining key is equal (or -inf): lowest block indices
-      int taken = 0;
-#pragma unroll
-      for (int i = 0; i < NPER; ++i) {
-        const bool a = active >> i & 1;
-        const unsigned bal = __ballot_sync(0xffffffffu, a);
-        if (a && taken + __popc(bal & ((1u << lane) - 1u)) < need) sel |= 1u << i;
-        taken += __popc(bal);
-      }
-      break;
-    }
-    if (count <= tb::kCand) {  // exact rank among the candidates
-      int base = 0;
-#pragma unroll
-      for (int i = 0; i < NPER; ++i) {
-        const bool a = active >> i & 1;
-        const unsigned bal = __ballot_sync(0xffffffffu, a);
-        if (a) {
-          const int pos = base + __popc(bal & ((1u << lane) - 1u));
-          cs[pos] = s[i];
-          ci[pos] = lane + 32 * i;
+      for (int i = 0; i < NPER; ++i)
+        if (active >> i & 1) {
+          lo = fminf(lo, f[i]);
+          hi = fmaxf(hi, f[i]);
         }
-        base += __popc(bal);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
       }
-      __syncwarp();
-      for (int j = lane; j < count; j += 32) {
-        const double v = cs[j];
-        const int id = ci[j];
-        int rank = 0;
-        for (int m = 0; m < count; ++m) {
-          const double w = cs[m];
-          rank += (w > v) || (w == v && ci[m] < id);
+      const int count = __reduce_add_sync(0xffffffffu, __popc(active));
+      if (count == need) {
+        sel |= active;
+        break;
+      }
+      if (count <= tb::kCand) {  // exact float64 rank among the candidates
+        int base = 0;
+#pragma unroll
+        for (int i = 0; i < NPER; ++i) {
+          const bool a = active >> i & 1;
+          const unsigned bal = __ballot_sync(0xffffffffu, a);
+          if (a) {
+            const int pos = base + __popc(bal & ((1u << lane) - 1u));
+            cs[pos] = srow[lane + 32 * i];
+            ci[pos] = lane + 32 * i;
+          }
+          base += __popc(bal);
         }
-        pick[id] = rank < need;
+        __syncwarp();
+        for (int j = lane; j < count; j += 32) {
+          const double v = cs[j];
+          const int id = ci[j];
+          int rank = 0;
+          for (int m = 0; m < count; ++m) {
+            const double w = cs[m];
+            rank += (w > v) || (w == v && ci[m] < id);
+          }
+          pick[id] = rank < need;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < NPER; ++i)
+          if ((active >> i & 1) && pick[lane + 32 * i]) sel |= 1u << i;
+        break;
       }
+      if (!(hi > lo)) {  // > kCand keys equal in float32: finish on the float64 keys
+        sel |= radix_select_active<NPER>(srow, row_max, active, need, hist, lane);
+        break;
+      }
+      // one level of value bins over [lo, hi]; f / 2 keeps the span finite
+      const float half_lo = 0.5f * lo, scale = 256.f / (0.5f * hi - half_lo);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < NPER; ++i)
-        if ((active >> i & 1) && pick[lane + 32 * i]) sel |= 1u << i;
-      break;
-    }
-    // one level of value bins over [lo, hi]
-    const double half_lo = 0.5 * lo, span = 0.5 * hi - half_lo;
-    const double scale = 256.0 / span;
+        if (active >> i & 1) atomicAdd(&hist[min(255, static_cast<int>((0.5f * f[i] - half_lo) * scale))], 1);
+      __syncwarp();
+      int h8[8];
+      int tot = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (active >> i & 1) {
-        const double t = (0.5 * s[i] - half_lo) * scale;
-        const int bin = t >= 255.0 ? 255 : static_cast<int>(t);
-        atomicAdd(&hist[bin], 1);
+      for (int i = 0; i < 8; ++i) {
+        h8[i] = hist[lane * 8 + i];
+        tot += h8[i];
       }
-    __syncwarp();
-    int h8[8];
-    int tot = 0;
+      // bins in descending order: inclusive suffix sums over the lanes
+      int incl = tot;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      h8[i] = hist[lane * 8 + i];
-      tot += h8[i];
-    }
-    // descending order of bins: inclusive suffix sum over lanes
-    int incl = tot;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl += t;
+      }
+      const int excl = incl - tot;
+      const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
+      const int src = 31 - __clz(owner);
+      int bucket = 0, above = 0;
+      if (lane == src) {
+        int run = excl;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_down_sync(0xffffffffu, incl, o);
-      if (lane + o < 32) incl += t;
-    }
-    const int excl = incl - tot;
-    const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
-    const int src = 31 - __clz(owner);  // the unique owner (suffix sums are monotone)
-    int bucket = 0, above = 0;
-    if (lane == src) {
-      int run = excl;
-#pragma unroll
-      for (int i = 7; i >= 0; --i) {
-        if (run + h8[i] >= need) {
-          bucket = lane * 8 + i;
-          above = run;
-          break;
+        for (int i = 7; i >= 0; --i) {
+          if (run + h8[i] >= need) {
+            bucket = lane * 8 + i;
+            above = run;
+            break;
+          }
+          run += h8[i];
         }
-        run += h8[i];
       }
-    }
-    bucket = __shfl_sync(0xffffffffu, bucket, src);
-    above = __shfl_sync(0xffffffffu, above, src);
-    need -= above;
-    uint32_t next = 0;
+      bucket = __shfl_sync(0xffffffffu, bucket, src);
+      above = __shfl_sync(0xffffffffu, above, src);
+      need -= above;
+      uint32_t next = 0;
 #pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (active >> i & 1) {
-        const double t = (0.5 * s[i] - half_lo) * scale;
-        const int bin = t >= 255.0 ? 255 : static_cast<int>(t);
-        if (bin > bucket) sel |= 1u << i;
-        else if (bin == bucket) next |= 1u << i;
-      }
-    active = next;
-    __syncwarp();
+      for (int i = 0; i < NPER; ++i)
+        if (active >> i & 1) {
+          const int bin = min(255, static_cast<int>((0.5f * f[i] - half_lo) * scale));
+          if (bin > bucket) sel |= 1u << i;
+          else if (bin == bucket) next |= 1u << i;
+        }
+      active = next;
+      __syncwarp();
+    }
   }
   int32_t* irow = idx + row * kmax;
   uint8_t* mrow = mask ? mask + row * nb : nullptr;

@@ -13,7 +13,7 @@ sp = P.SparseSettings.for_sparsity(128, L, 0.9)
 res = {}
 
 
-def timed(fn, n=20):
+def timed(fn, n=int(os.environ.get("EXP_ITERS", "20"))):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -26,7 +26,7 @@ def timed(fn, n=20):
     return e0.elapsed_time(e1) / n
 
 
-for rep in range(2):
+for rep in range(int(os.environ.get("EXP_REPS", "2"))):
     for sel in ("bins", "radix"):
         for pipe in (1, 0):
             with P._lib.option("select", "r" if sel == "radix" else 0), P._lib.option("k1_pipeline", pipe):

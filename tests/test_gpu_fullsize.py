@@ -34,13 +34,13 @@ HUNYUAN = ((33, 45, 80), 24, 128, (16, 56, 56), 64)
 
 TOPK_CASES = {
     # name: (shape, block, sparsity, query blocks sampled per head)
-    "cfg2_wan_b64_s80": (WAN, 64, 0.80, 6),
-    "cfg1_cfg2_wan_b64_s90": (WAN, 64, 0.90, 16),
-    "cfg2_wan_b64_s95": (WAN, 64, 0.95, 6),
-    "cfg2_wan_b128_s80": (WAN, 128, 0.80, 6),
-    "cfg2_wan_b128_s90": (WAN, 128, 0.90, 6),
-    "cfg2_wan_b128_s95": (WAN, 128, 0.95, 6),
-    "cfg3_hunyuan_b128_s90": (HUNYUAN, 128, 0.90, 12),
+    "cfg2_wan_b64_s80": (WAN, 64, 0.80, 4),
+    "cfg1_cfg2_wan_b64_s90": (WAN, 64, 0.90, 8),
+    "cfg2_wan_b64_s95": (WAN, 64, 0.95, 4),
+    "cfg2_wan_b128_s80": (WAN, 128, 0.80, 4),
+    "cfg2_wan_b128_s90": (WAN, 128, 0.90, 4),
+    "cfg2_wan_b128_s95": (WAN, 128, 0.95, 4),
+    "cfg3_hunyuan_b128_s90": (HUNYUAN, 128, 0.90, 4),
 }
 
 KEEP_CASES = {
