@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define ROPESLR_ABI_VERSION 1
+#define ROPESLR_ABI_VERSION 2
 
 typedef enum ropeslr_status {
   ROPESLR_OK = 0,
@@ -130,8 +130,6 @@ int64_t ropeslr_num_blocks(int64_t L, int32_t block);
  *   "scores"        'f' / 'd': CUDA-core / unpipelined DMMA block scores
  *   "rope_tma"      0: the row-bulk-copy RoPE pre-pass
  *   "linear_simt"   1: the CUDA-core linear compensator
- *   "select"        'r': the radix-select top-k kernel instead of the value-bin one
- *   "k1_pipeline"   0: K1's pooling / scores / selection in sequence, not head-group pipelined
  * Not synchronised with calls in flight on other threads.  Unknown name:
  * ROPESLR_ERR_VALUE.  ropeslr_get_option returns the current value. */
 int ropeslr_set_option(const char* name, int value);
@@ -143,10 +141,7 @@ int ropeslr_get_option(const char* name);
  * stable descending order (ties to the lower block index), top-k or
  * cumulative-mass count, ascending index list.  `mask` and `scores`
  * ([B,H,nb,nb] float64) may be NULL.  kmax must be >= min(topk, nb) in top-k
- * mode and >= nb in keep mode.  Large problems are pipelined by head groups:
- * the pooling of one group runs on `stream` while the scores and selection
- * of the previous group run on an internal side stream (one per device,
- * forked from and joined back to `stream` with events, capture-safe). */
+ * mode and >= nb in keep mode. */
 size_t ropeslr_select_workspace_bytes(const ropeslr_shape* shape);
 int ropeslr_select_blocks(const ropeslr_shape* shape, const ropeslr_select_params* sel,
                           const void* q, const void* k,
@@ -237,7 +232,9 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
 
 /* K2 + K4 in one launch where the tcgen05 path applies (else K2 then K4):
  * attention, normalisation by the softmax denominator, RMSNorm, gated
- * combination with y_lr and the bf16/f32 store of out.  o_sparse (nullable)
+ * combination with y_lr and the store of out, in out_dtype: shape.dtype, or
+ * ROPESLR_F32 for a float32 output from bf16 inputs (the fused result before
+ * any bf16 rounding; [B,L,H,d] float32).  o_sparse (nullable)
  * additionally receives the raw sparse-branch output.  On the tcgen05 path
  * y_lr and out must be 32-byte aligned (256-bit row accesses), else
  * ROPESLR_ERR_ALIGN.  Workspace: the CUDA-core path keeps o_sparse there when
@@ -255,7 +252,7 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
 int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
                          const int32_t* idx, int32_t kmax, const int32_t* cnt,
                          const int32_t* row_perm, const void* y_lr, const float* g_logit, float b_g,
-                         const float* rms_sparse, float eps, void* out, float* o_sparse,
+                         const float* rms_sparse, float eps, void* out, int32_t out_dtype, float* o_sparse,
                          int32_t impl, void* workspace, size_t workspace_bytes, void* stream);
 size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* shape, int32_t impl);
 

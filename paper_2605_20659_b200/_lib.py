@@ -16,6 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # variant experiments); the default is the in-tree build.
 LIB_PATH = os.environ.get("ROPESLR_LIBRARY") or os.path.join(PKG, "libropeslr_b200.so")
 
+ABI_VERSION = 2  # include/ropeslr_b200.h ROPESLR_ABI_VERSION
 F32, BF16 = 0, 1
 LOWRANK, LINEAR = 0, 1
 NONFINITE_QK, NONFINITE_X = 1, 2
@@ -74,7 +75,7 @@ _SIGNATURES = {
     "ropeslr_linear_branch": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_f32, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_fuse_output": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_f32, c_vp, c_f32, c_vp, c_vp]),
     "ropeslr_attend_fused": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp,
-                                     c_f32, c_vp, c_vp, c_i32, c_vp, c_sz, c_vp]),
+                                     c_f32, c_vp, c_i32, c_vp, c_i32, c_vp, c_sz, c_vp]),
     "ropeslr_attend_workspace_bytes": (c_sz, [P(Shape), c_i32]),
     "ropeslr_select_pooled_workspace_bytes": (c_sz, [P(Shape)]),
     "ropeslr_select_from_pooled": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
@@ -127,7 +128,7 @@ def lib() -> ctypes.CDLL:
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args
-            if handle.ropeslr_abi_version() != 1:
+            if handle.ropeslr_abi_version() != ABI_VERSION:
                 raise RuntimeError("libropeslr_b200.so ABI version mismatch")
             _lib = handle
     return _lib

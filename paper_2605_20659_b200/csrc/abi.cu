@@ -42,58 +42,12 @@ static Tuning& tuning_mut() {
     r.rope_tma = !env_off("ROPESLR_ROPE_TMA");
     const char* lin = getenv("ROPESLR_LINEAR");
     r.linear_simt = lin != nullptr && lin[0] == 's';
-    const char* sl = getenv("ROPESLR_SELECT");
-    r.select = sl != nullptr ? sl[0] : 0;
-    r.k1_pipeline = !env_off("ROPESLR_K1_PIPELINE");
     return r;
   }();
   return t;
 }
 
 const Tuning& tuning() { return tuning_mut(); }
-
-static cudaStream_t aux_stream_of_current_device() {
-  static std::mutex mu;
-  static cudaStream_t cache[64] = {nullptr};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (cache[dev] == nullptr) {
-    // highest priority: the side stream carries the compute-bound stages
-    // (K1 scores / selection), whose CTAs should be dispatched ahead of the
-    // HBM-bound kernel filling the rest of the SMs on the caller's stream
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStream_t st = nullptr;
-    if (cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
-    cache[dev] = st;
-  }
-  return cache[dev];
-}
-
-int AuxStream::fork(cudaStream_t caller) {
-  main = caller;
-  stream = aux_stream_of_current_device();
-  if (stream == nullptr) return ROPESLR_ERR_LAUNCH;
-  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-  return wait_main();
-}
-
-int AuxStream::wait_main() {
-  if (cudaEventRecord(ev, main) != cudaSuccess || cudaStreamWaitEvent(stream, ev, 0) != cudaSuccess)
-    return ROPESLR_ERR_LAUNCH;
-  return ROPESLR_OK;
-}
-
-int AuxStream::join() {
-  if (cudaEventRecord(ev, stream) != cudaSuccess || cudaStreamWaitEvent(main, ev, 0) != cudaSuccess)
-    return ROPESLR_ERR_LAUNCH;
-  return ROPESLR_OK;
-}
-
-AuxStream::~AuxStream() {
-  if (ev != nullptr) cudaEventDestroy(ev);  // released once the pending records complete
-}
 
 template <typename T>
 __global__ void nonfinite_scan_kernel(const T* __restrict__ a, int64_t n, uint32_t* flag, uint32_t bit) {
@@ -159,8 +113,6 @@ extern "C" int ropeslr_set_option(const char* name, int value) {
   else if (!strcmp(name, "scores")) t.scores = static_cast<char>(value);
   else if (!strcmp(name, "rope_tma")) t.rope_tma = value != 0;
   else if (!strcmp(name, "linear_simt")) t.linear_simt = value != 0;
-  else if (!strcmp(name, "select")) t.select = static_cast<char>(value);
-  else if (!strcmp(name, "k1_pipeline")) t.k1_pipeline = value != 0;
   else return ROPESLR_ERR_VALUE;
   return ROPESLR_OK;
 }
@@ -175,7 +127,5 @@ extern "C" int ropeslr_get_option(const char* name) {
   if (!strcmp(name, "scores")) return t.scores;
   if (!strcmp(name, "rope_tma")) return t.rope_tma;
   if (!strcmp(name, "linear_simt")) return t.linear_simt;
-  if (!strcmp(name, "select")) return t.select;
-  if (!strcmp(name, "k1_pipeline")) return t.k1_pipeline;
   return ROPESLR_ERR_VALUE;
 }

@@ -135,6 +135,7 @@ struct Params {
   const float* rms_sp;
   float eps;
   __nv_bfloat16* out;
+  float* out_f32;  // when set, the fused output is stored as float32 here instead of bf16 into out
   float* o_sparse;
   int out_H;   // heads per token row of out / y_lr (>= H when a head chunk writes into a wider row)
   int out_h0;  // first head of this call inside that row
@@ -143,6 +144,53 @@ struct Params {
                    // 4 no MMAs (fixed-reference kernel: only in a build with -DROPESLR_K2_MEASURE=1)
   long long* trace;  // TRACE
 };
+
+// Fused output of one row's 32 columns [col0, col0 + 32): the normalised
+// sparse branch O/l * rsqrt(mean + eps) * rms_sparse (ob holds O/l, inv the
+// rsqrt) plus sigmoid(g_logit + b_g) * y_lr (mechanism.py:437-451), stored
+// as bf16 into out or as float32 into out_f32.  16 columns per step: one
+// 256-bit load of y_lr and one (bf16) or two (f32) 256-bit stores, a full
+// sector per access.
+__device__ __forceinline__ void store_fused_row(const Params& p, int64_t orow, const uint32_t (&ob)[32], float inv,
+                                                float gate, int col0) {
+  const __nv_bfloat16* y = p.y_lr + orow;
+#pragma unroll
+  for (int i = 0; i < 32; i += 16) {
+    uint32_t uy[8];
+    asm volatile("ld.global.cs.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(uy[0]), "=r"(uy[1]), "=r"(uy[2]), "=r"(uy[3]), "=r"(uy[4]), "=r"(uy[5]), "=r"(uy[6]),
+                   "=r"(uy[7])
+                 : "l"(y + i));
+    float o[16];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float2 yv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uy[e]));
+      o[2 * e] = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
+      o[2 * e + 1] = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
+    }
+    if (p.out_f32 != nullptr) {
+      float* dst = p.out_f32 + orow + i;
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf)
+        asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 8 * hlf),
+                     "r"(__float_as_uint(o[8 * hlf])), "r"(__float_as_uint(o[8 * hlf + 1])),
+                     "r"(__float_as_uint(o[8 * hlf + 2])), "r"(__float_as_uint(o[8 * hlf + 3])),
+                     "r"(__float_as_uint(o[8 * hlf + 4])), "r"(__float_as_uint(o[8 * hlf + 5])),
+                     "r"(__float_as_uint(o[8 * hlf + 6])), "r"(__float_as_uint(o[8 * hlf + 7]))
+                     : "memory");
+    } else {
+      uint32_t uo[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+        uo[e] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p.out + orow + i), "r"(uo[0]),
+                   "r"(uo[1]), "r"(uo[2]), "r"(uo[3]), "r"(uo[4]), "r"(uo[5]), "r"(uo[6]), "r"(uo[7])
+                   : "memory");
+    }
+  }
+}
 
 #ifdef ROPESLR_WATCHDOG
 __device__ volatile unsigned long long* g_watchdog;  // host-mapped
@@ -286,7 +334,7 @@ __device__ __forceinline__ float half_exp(const uint32_t (&sr)[BLK / 2], uint32_
 template <int BLK>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                          const __grid_constant__ CUtensorMap tmV, const Params p) {
+                          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ Params p) {
   using Lay = Layout<BLK>;
   using Bx = Bars<BLK>;
   constexpr int KST = Lay::KST, VST = Lay::VST;
@@ -583,32 +631,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
                                                             __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
       }
-      if (p.out) {
+      if (p.out || p.out_f32) {
         const float gate = sigmoidf_stable(p.g_logit[static_cast<int64_t>(b) * p.L + tok] + p.b_g);
         const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
-        const __nv_bfloat16* y = p.y_lr + orow;
-        __nv_bfloat16* dst = p.out + orow;
-#pragma unroll
-        for (int i = 0; i < 32; i += 16) {
-          // 16 columns = 32 bytes: one 256-bit load of y_lr and one 256-bit
-          // store of out per step (a full sector per thread)
-          uint32_t uy[8], uo[8];
-          asm volatile("ld.global.cs.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                       : "=r"(uy[0]), "=r"(uy[1]), "=r"(uy[2]), "=r"(uy[3]), "=r"(uy[4]), "=r"(uy[5]),
-                         "=r"(uy[6]), "=r"(uy[7])
-                       : "l"(y + i));
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float2 yv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uy[e]));
-            const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
-            const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(o0, o1);
-            uo[e] = *reinterpret_cast<uint32_t*>(&h2);
-          }
-          asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + i), "r"(uo[0]),
-                       "r"(uo[1]), "r"(uo[2]), "r"(uo[3]), "r"(uo[4]), "r"(uo[5]), "r"(uo[6]), "r"(uo[7])
-                       : "memory");
-        }
+        store_fused_row(p, orow, ob, inv, gate, col0);
       }
     }
   }
@@ -684,7 +710,7 @@ struct Layout {
 template <int BLK, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_fixed_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                             const __grid_constant__ CUtensorMap tmV, const Params p) {
+                             const __grid_constant__ CUtensorMap tmV, const __grid_constant__ Params p) {
   using Lay = fx::Layout<BLK>;
   using Bx = fx::FBars<BLK>;
   static_assert(Bx::COUNT <= Lay::NBAR, "barrier count");
@@ -1010,32 +1036,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(ob[i]), __uint_as_float(ob[i + 1]),
                                                             __uint_as_float(ob[i + 2]), __uint_as_float(ob[i + 3]));
       }
-      if (p.out) {
+      if (p.out || p.out_f32) {
         const float gate = sigmoidf_stable(p.g_logit[static_cast<int64_t>(b) * p.L + tok] + p.b_g);
         const int64_t orow = ((static_cast<int64_t>(b) * p.L + tok) * p.out_H + p.out_h0 + h) * D + col0;
-        const __nv_bfloat16* y = p.y_lr + orow;
-        __nv_bfloat16* dst = p.out + orow;
-#pragma unroll
-        for (int i = 0; i < 32; i += 16) {
-          // 16 columns = 32 bytes: one 256-bit load of y_lr and one 256-bit
-          // store of out per step (a full sector per thread)
-          uint32_t uy[8], uo[8];
-          asm volatile("ld.global.cs.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                       : "=r"(uy[0]), "=r"(uy[1]), "=r"(uy[2]), "=r"(uy[3]), "=r"(uy[4]), "=r"(uy[5]),
-                         "=r"(uy[6]), "=r"(uy[7])
-                       : "l"(y + i));
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float2 yv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&uy[e]));
-            const float o0 = fmaf(gate, yv.x, __uint_as_float(ob[i + 2 * e]) * inv * p.rms_sp[col0 + i + 2 * e]);
-            const float o1 = fmaf(gate, yv.y, __uint_as_float(ob[i + 2 * e + 1]) * inv * p.rms_sp[col0 + i + 2 * e + 1]);
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(o0, o1);
-            uo[e] = *reinterpret_cast<uint32_t*>(&h2);
-          }
-          asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + i), "r"(uo[0]),
-                       "r"(uo[1]), "r"(uo[2]), "r"(uo[3]), "r"(uo[4]), "r"(uo[5]), "r"(uo[6]), "r"(uo[7])
-                       : "memory");
-        }
+        store_fused_row(p, orow, ob, inv, gate, col0);
       }
     }
   }
@@ -1371,15 +1375,21 @@ int attend_fused_tc_strided(const ropeslr_shape* s, const void* q, const void* k
 bool attend_tc_eligible(const ropeslr_shape* s) { return tc::tc_eligible(s); }
 }  // namespace ropeslr
 
+namespace ropeslr {
+int fuse_output(const ropeslr_shape* s, const float* o_sparse, const void* y_lr, const float* g_logit, float b_g,
+                const float* rms_sparse, float eps, void* out, int out_dtype, cudaStream_t stream_);
+}
+
 extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                                     const int32_t* idx, int32_t kmax, const int32_t* cnt, const int32_t* row_perm,
                                     const void* y_lr, const float* g_logit, float b_g, const float* rms_sparse,
-                                    float eps, void* out, float* o_sparse, int32_t impl, void* ws, size_t ws_bytes,
-                                    void* stream) {
+                                    float eps, void* out, int32_t out_dtype, float* o_sparse, int32_t impl, void* ws,
+                                    size_t ws_bytes, void* stream) {
   int st = check_attn_args(s, q, k, v, idx, kmax, cnt);
   if (st) return st;
   if (!y_lr || !g_logit || !rms_sparse || !out) return ROPESLR_ERR_NULL;
   if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  if (out_dtype != s->dtype && out_dtype != ROPESLR_F32) return ROPESLR_ERR_DTYPE;
   const int which = resolve_impl(s, impl);
   if (which < 0) return ROPESLR_ERR_VALUE;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
@@ -1393,7 +1403,7 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
     }
     st = launch_sparse_attention_simt(s, q, k, v, idx, kmax, cnt, row_perm, osp, cs);
     if (st) return st;
-    return ropeslr_fuse_output(s, osp, y_lr, g_logit, b_g, rms_sparse, eps, out, stream);
+    return fuse_output(s, osp, y_lr, g_logit, b_g, rms_sparse, eps, out, out_dtype, cs);
   }
   // the fused epilogue moves y_lr / out rows with 256-bit accesses
   if (!aligned32(y_lr) || !aligned32(out)) return ROPESLR_ERR_ALIGN;
@@ -1403,7 +1413,10 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
   prm.b_g = b_g;
   prm.rms_sp = rms_sparse;
   prm.eps = eps;
-  prm.out = static_cast<__nv_bfloat16*>(out);
+  if (out_dtype == ROPESLR_F32)
+    prm.out_f32 = static_cast<float*>(out);
+  else
+    prm.out = static_cast<__nv_bfloat16*>(out);
   prm.o_sparse = o_sparse;
   if (ws && ws_bytes >= ropeslr_attend_workspace_bytes(s, impl)) {
     if (int e = schedule_units(s, cnt, prm, ws, cs)) return e;

@@ -86,20 +86,6 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 int num_sms();  // cached per device (abi.cu)
 
-// A side stream of the current device (created once per device, abi.cu),
-// forked from the caller's stream and joined back with per-call events:
-// work on `stream` between fork() and join() overlaps the caller's stream
-// and is ordered before everything the caller enqueues after join().
-// Capture-safe (the fork/join pattern of CUDA graphs).
-struct AuxStream {
-  cudaStream_t main = nullptr, stream = nullptr;
-  cudaEvent_t ev = nullptr;
-  int fork(cudaStream_t caller);  // aux waits for the caller's work so far
-  int wait_main();                // aux waits for the caller's work so far (again)
-  int join();                     // the caller waits for the aux work so far
-  ~AuxStream();
-};
-
 // ORs `bit` into *flag (stream-ordered) when any of the n values is NaN or
 // infinite; no-op for a NULL flag (abi.cu).
 int scan_nonfinite(const void* a, bool f64, int64_t n, uint32_t* flag, uint32_t bit, cudaStream_t st);
@@ -114,8 +100,6 @@ struct Tuning {
   char scores;         // ROPESLR_SCORES: 'f' CUDA-core f64, 'd' unpipelined DMMA, 0 default
   bool rope_tma;       // ROPESLR_ROPE_TMA=0: the row-bulk-copy RoPE kernel
   bool linear_simt;    // ROPESLR_LINEAR=simt: the CUDA-core linear compensator
-  char select;         // ROPESLR_SELECT=radix ('r'): the radix-select top-k kernel
-  bool k1_pipeline;    // ROPESLR_K1_PIPELINE=0: pool / scores / select unpipelined
 };
 const Tuning& tuning();
 

@@ -276,11 +276,11 @@ __global__ void __launch_bounds__(256) linear_apply_kernel(const T* __restrict__
 }
 
 // One warp per (b, token, head) row.
-template <typename T>
+template <typename T, typename TO = T>
 __global__ void __launch_bounds__(256) fuse_output_kernel(const float* __restrict__ o_sparse, const T* __restrict__ y_lr,
                                                           const float* __restrict__ g_logit, float b_g,
                                                           const float* __restrict__ rms_sp, float eps, int64_t B,
-                                                          int64_t L, int H, int d, T* __restrict__ out) {
+                                                          int64_t L, int H, int d, TO* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);  // (b*L + tok)*H + h
   if (row >= B * L * H) return;
@@ -299,10 +299,10 @@ __global__ void __launch_bounds__(256) fuse_output_kernel(const float* __restric
   const float inv = 1.f / sqrtf(ss / static_cast<float>(d) + eps);
   const float g = sigmoidf_stable(g_logit[bt] + b_g);
   const T* y = y_lr + row * d;
-  T* dst = out + row * d;
+  TO* dst = out + row * d;
   for (int m = 0; m < nm; ++m) {
     const int j = lane + 32 * m;
-    dst[j] = from_f<T>(fmaf(g, to_f(y[j]), ov[m] * inv * rms_sp[j]));
+    dst[j] = from_f<TO>(fmaf(g, to_f(y[j]), ov[m] * inv * rms_sp[j]));
   }
 }
 
@@ -501,24 +501,38 @@ extern "C" int ropeslr_linear_branch(const ropeslr_shape* s, const void* q_lin, 
   return launch_status();
 }
 
-extern "C" int ropeslr_fuse_output(const ropeslr_shape* s, const float* o_sparse, const void* y_lr,
-                                   const float* g_logit, float b_g, const float* rms_sparse, float eps, void* out,
-                                   void* stream) {
+namespace ropeslr {
+// K4 with the output in `out_dtype` (the shape's dtype, or float32).
+int fuse_output(const ropeslr_shape* s, const float* o_sparse, const void* y_lr, const float* g_logit, float b_g,
+                const float* rms_sparse, float eps, void* out, int out_dtype, cudaStream_t stream_) {
   int st = check_shape(s);
   if (st) return st;
   if (!o_sparse || !y_lr || !g_logit || !rms_sparse || !out) return ROPESLR_ERR_NULL;
   if (s->d < 32 || s->d > 256 || s->d % 32) return ROPESLR_ERR_SHAPE;
   if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  if (out_dtype != s->dtype && out_dtype != ROPESLR_F32) return ROPESLR_ERR_DTYPE;
   const int64_t rows = s->B * s->L * s->H;
   dim3 grid(static_cast<unsigned>(ceil_div(rows, 8)));
-  cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
-  if (s->dtype == ROPESLR_BF16)
+  const int H = static_cast<int>(s->H), d = static_cast<int>(s->d);
+  if (s->dtype == ROPESLR_BF16 && out_dtype == ROPESLR_BF16)
     fuse_output_kernel<__nv_bfloat16><<<grid, 256, 0, stream_>>>(
-        o_sparse, static_cast<const __nv_bfloat16*>(y_lr), g_logit, b_g, rms_sparse, eps, s->B, s->L,
-        static_cast<int>(s->H), static_cast<int>(s->d), static_cast<__nv_bfloat16*>(out));
+        o_sparse, static_cast<const __nv_bfloat16*>(y_lr), g_logit, b_g, rms_sparse, eps, s->B, s->L, H, d,
+        static_cast<__nv_bfloat16*>(out));
+  else if (s->dtype == ROPESLR_BF16)
+    fuse_output_kernel<__nv_bfloat16, float><<<grid, 256, 0, stream_>>>(
+        o_sparse, static_cast<const __nv_bfloat16*>(y_lr), g_logit, b_g, rms_sparse, eps, s->B, s->L, H, d,
+        static_cast<float*>(out));
   else
     fuse_output_kernel<float><<<grid, 256, 0, stream_>>>(o_sparse, static_cast<const float*>(y_lr), g_logit, b_g,
-                                                         rms_sparse, eps, s->B, s->L, static_cast<int>(s->H),
-                                                         static_cast<int>(s->d), static_cast<float*>(out));
+                                                         rms_sparse, eps, s->B, s->L, H, d, static_cast<float*>(out));
   return launch_status();
+}
+}  // namespace ropeslr
+
+extern "C" int ropeslr_fuse_output(const ropeslr_shape* s, const float* o_sparse, const void* y_lr,
+                                   const float* g_logit, float b_g, const float* rms_sparse, float eps, void* out,
+                                   void* stream) {
+  if (!s) return ROPESLR_ERR_NULL;
+  return ropeslr::fuse_output(s, o_sparse, y_lr, g_logit, b_g, rms_sparse, eps, out, s->dtype,
+                              static_cast<cudaStream_t>(stream));
 }

@@ -306,7 +306,7 @@ extern "C" int ropeslr_forward_host(const ropeslr_host_forward* a, void* workspa
                                       nullptr, base + p.sel_ws, p.sel_ws_bytes, S));
     if (p.nchunks == 1) {
       ROPESLR_TRY(ropeslr_attend_fused(&sc, q, k, v, idx, static_cast<int32_t>(p.kmax), cnt, nullptr, y_lr, g_logit,
-                                       a->b_g, rms_sp, a->eps, dout, nullptr, ROPESLR_IMPL_AUTO, base + p.osp,
+                                       a->b_g, rms_sp, a->eps, dout, sc.dtype, nullptr, ROPESLR_IMPL_AUTO, base + p.osp,
                                        p.osp_bytes, S));
     } else {
       ROPESLR_TRY(attend_fused_tc_strided(&sc, q, k, v, idx, static_cast<int32_t>(p.kmax), cnt, y_lr, g_logit,

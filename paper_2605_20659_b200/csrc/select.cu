@@ -512,11 +512,29 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
   const int64_t bh = row / nb;
   const int qb = static_cast<int>(row % nb);
   const double* srow = scores + row * nb;
+  // the reference orders blocks by their softmax probability (mechanism.py:
+  // 310-317): scores more than kProbUnderflow below the row max have
+  // probability 0 and tie (lower block index first), so they key as -inf
   uint64_t key[NPER];
+  uint64_t kmax_key = 0;  // the row max, as an ascending key
 #pragma unroll
   for (int i = 0; i < NPER; ++i) {
     const int c = lane + 32 * i;
     key[i] = c < nb ? desc_key(srow[c]) : ~0ull;
+    if (c < nb) kmax_key = max(kmax_key, ~key[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) kmax_key = max(kmax_key, __shfl_xor_sync(0xffffffffu, kmax_key, o));
+  // invert the ascending map of desc_key
+  const double row_max = __longlong_as_double(
+      static_cast<long long>((kmax_key >> 63) ? (kmax_key & ~(1ull << 63)) : ~kmax_key));
+  if (row_max > -INFINITY) {
+    const uint64_t ninf_key = desc_key(-INFINITY);
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {
+      const int c = lane + 32 * i;
+      if (c < nb && srow[c] - row_max < kProbUnderflow) key[i] = ninf_key;
+    }
   }
   int need = topk < nb ? topk : nb;
   uint64_t prefix = 0, pmask = 0;
@@ -616,321 +634,6 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
   }
 }
 
-// Top-k rows by value bins, one warp per (bh, query block) row, nb <= 32 * NPER.
-//
-// The radix select above spends most of its time in its first digits: the
-// block scores of a row share sign / exponent bits, so its histogram atomics
-// hit a few shared-memory bins and serialise.  Here the bins are linear in
-// the VALUE over the row's current [min, max] (256 bins; random rows spread
-// evenly), computed in float32: the float64 -> float32 rounding and the bin
-// map are both monotone non-decreasing, so a higher bin always holds
-// strictly larger float64 scores and exactness never depends on them.  Every
-// key in a bin above the one holding the k-th best is kept, and that bin is
-// refined over its own range until at most kCand keys remain; an exact rank
-// of those in float64 -- score descending, block index ascending on equal
-// scores, the stable order of mechanism.py:317 -- picks the rest.  Rows the
-// float32 map cannot separate (values beyond float32 range, or a bucket of
-// more than kCand keys that are equal in float32) finish with a radix select
-// on the order-preserving 64-bit keys, reloaded from the row.
-namespace tb {
-constexpr int kWarps = 8;
-constexpr int kCand = 128;
-}  // namespace tb
-
-__device__ __forceinline__ double warp_max_d(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Score of column c as the selection sees it: NaN (non-finite inputs, flagged
-// elsewhere) ranks last; a probability that underflows ties at -inf.
-__device__ __forceinline__ double sel_score(const double* srow, int c, double row_max) {
-  double v = srow[c];
-  if (v != v) v = -INFINITY;
-  return v - row_max < kProbUnderflow ? -INFINITY : v;
-}
-
-// Radix select of the `need` best of the active columns (bit i of `active`:
-// column lane + 32 i) on desc_key of sel_score, keys reloaded per pass.
-template <int NPER>
-__device__ __noinline__ uint32_t radix_select_active(const double* srow, double row_max, uint32_t active, int need, int* hist,
-                                        int lane) {
-  uint64_t prefix = 0, pmask = 0;
-  bool exact = false;
-#pragma unroll 1
-  for (int shift = 56; shift >= 0; shift -= 8) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (active >> i & 1) {
-        const uint64_t key = desc_key(sel_score(srow, lane + 32 * i, row_max));
-        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
-      }
-    __syncwarp();
-    int h8[8];
-    int tot = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      h8[i] = hist[lane * 8 + i];
-      tot += h8[i];
-    }
-    int incl = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const int excl = incl - tot;
-    const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
-    const int src = __ffs(owner) - 1;
-    int bucket = 0, before = 0, cnt_b = 0;
-    if (lane == src) {
-      int run = excl;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (run + h8[i] >= need) {
-          bucket = lane * 8 + i;
-          before = run;
-          cnt_b = h8[i];
-          break;
-        }
-        run += h8[i];
-      }
-    }
-    bucket = __shfl_sync(0xffffffffu, bucket, src);
-    before = __shfl_sync(0xffffffffu, before, src);
-    cnt_b = __shfl_sync(0xffffffffu, cnt_b, src);
-    need -= before;
-    prefix |= static_cast<uint64_t>(bucket) << shift;
-    pmask |= 255ull << shift;
-    __syncwarp();
-    if (cnt_b == need) {
-      exact = true;
-      break;
-    }
-  }
-  uint32_t sel = 0;
-  int taken = 0;
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const bool a = active >> i & 1;
-    const uint64_t km = a ? desc_key(sel_score(srow, lane + 32 * i, row_max)) & pmask : ~0ull;
-    bool si = a && km < prefix;
-    const bool tie = a && km == prefix;
-    if (exact) {
-      si = si || tie;
-    } else {
-      const unsigned bal = __ballot_sync(0xffffffffu, tie);
-      si = si || (tie && taken + __popc(bal & ((1u << lane) - 1u)) < need);
-      taken += __popc(bal);
-    }
-    if (si) sel |= 1u << i;
-  }
-  return sel;
-}
-
-template <int NPER>
-__global__ void __launch_bounds__(256, 3) select_topk_bins_kernel(const double* __restrict__ scores, int nb,
-                                                               int64_t row0, int64_t row1, int64_t L, int block,
-                                                               int topk, int kmax, int32_t* __restrict__ idx,
-                                                               int32_t* __restrict__ cnt, uint8_t* __restrict__ mask,
-                                                               unsigned long long* __restrict__ attended) {
-  __shared__ int hist_all[tb::kWarps][256];
-  __shared__ double cs_all[tb::kWarps][tb::kCand];
-  __shared__ int ci_all[tb::kWarps][tb::kCand];
-  __shared__ uint8_t pick_all[tb::kWarps][32 * NPER];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row = row0 + static_cast<int64_t>(blockIdx.x) * tb::kWarps + warp;
-  if (row >= row1) return;
-  int* hist = hist_all[warp];
-  double* cs = cs_all[warp];
-  int* ci = ci_all[warp];
-  uint8_t* pick = pick_all[warp];
-  const int64_t bh = row / nb;
-  const int qb = static_cast<int>(row % nb);
-  const double* srow = scores + row * nb;
-  // row max (the probability-underflow reference), then float32 images
-  double row_max = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const int c = lane + 32 * i;
-    if (c < nb) {
-      const double v = srow[c];
-      if (v == v) row_max = fmax(row_max, v);
-    }
-  }
-  row_max = warp_max_d(row_max);
-  float f[NPER];
-  uint32_t fin = 0, ninf = 0;  // finite in float32 / tied at -inf (probability 0)
-  bool f32_safe = true;
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const int c = lane + 32 * i;
-    f[i] = 0.f;
-    if (c < nb) {
-      const double v = sel_score(srow, c, row_max);
-      if (v == -INFINITY) {
-        ninf |= 1u << i;
-      } else {
-        f32_safe &= fabs(v) < 1e38;
-        f[i] = static_cast<float>(v);
-        fin |= 1u << i;
-      }
-    }
-  }
-  f32_safe = __all_sync(0xffffffffu, f32_safe);
-  int need = topk < nb ? topk : nb;
-  uint32_t sel = 0;
-  const int n_fin = __reduce_add_sync(0xffffffffu, __popc(fin));
-  if (need >= n_fin) {  // every finite key, then the -inf ties by block index
-    sel = fin;
-    need -= n_fin;
-    int taken = 0;
-#pragma unroll
-    for (int i = 0; i < NPER; ++i) {
-      const bool a = ninf >> i & 1;
-      const unsigned bal = __ballot_sync(0xffffffffu, a);
-      if (a && taken + __popc(bal & ((1u << lane) - 1u)) < need) sel |= 1u << i;
-      taken += __popc(bal);
-    }
-  } else if (!f32_safe) {
-    sel = radix_select_active<NPER>(srow, row_max, fin, need, hist, lane);
-  } else {
-    uint32_t active = fin;
-#pragma unroll 1
-    while (true) {
-      float lo = INFINITY, hi = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < NPER; ++i)
-        if (active >> i & 1) {
-          lo = fminf(lo, f[i]);
-          hi = fmaxf(hi, f[i]);
-        }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      const int count = __reduce_add_sync(0xffffffffu, __popc(active));
-      if (count == need) {
-        sel |= active;
-        break;
-      }
-      if (count <= tb::kCand) {  // exact float64 rank among the candidates
-        int base = 0;
-#pragma unroll
-        for (int i = 0; i < NPER; ++i) {
-          const bool a = active >> i & 1;
-          const unsigned bal = __ballot_sync(0xffffffffu, a);
-          if (a) {
-            const int pos = base + __popc(bal & ((1u << lane) - 1u));
-            cs[pos] = srow[lane + 32 * i];
-            ci[pos] = lane + 32 * i;
-          }
-          base += __popc(bal);
-        }
-        __syncwarp();
-        for (int j = lane; j < count; j += 32) {
-          const double v = cs[j];
-          const int id = ci[j];
-          int rank = 0;
-          for (int m = 0; m < count; ++m) {
-            const double w = cs[m];
-            rank += (w > v) || (w == v && ci[m] < id);
-          }
-          pick[id] = rank < need;
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < NPER; ++i)
-          if ((active >> i & 1) && pick[lane + 32 * i]) sel |= 1u << i;
-        break;
-      }
-      if (!(hi > lo)) {  // > kCand keys equal in float32: finish on the float64 keys
-        sel |= radix_select_active<NPER>(srow, row_max, active, need, hist, lane);
-        break;
-      }
-      // one level of value bins over [lo, hi]; f / 2 keeps the span finite
-      const float half_lo = 0.5f * lo, scale = 256.f / (0.5f * hi - half_lo);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < NPER; ++i)
-        if (active >> i & 1) atomicAdd(&hist[min(255, static_cast<int>((0.5f * f[i] - half_lo) * scale))], 1);
-      __syncwarp();
-      int h8[8];
-      int tot = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        h8[i] = hist[lane * 8 + i];
-        tot += h8[i];
-      }
-      // bins in descending order: inclusive suffix sums over the lanes
-      int incl = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_down_sync(0xffffffffu, incl, o);
-        if (lane + o < 32) incl += t;
-      }
-      const int excl = incl - tot;
-      const unsigned owner = __ballot_sync(0xffffffffu, excl < need && incl >= need);
-      const int src = 31 - __clz(owner);
-      int bucket = 0, above = 0;
-      if (lane == src) {
-        int run = excl;
-#pragma unroll
-        for (int i = 7; i >= 0; --i) {
-          if (run + h8[i] >= need) {
-            bucket = lane * 8 + i;
-            above = run;
-            break;
-          }
-          run += h8[i];
-        }
-      }
-      bucket = __shfl_sync(0xffffffffu, bucket, src);
-      above = __shfl_sync(0xffffffffu, above, src);
-      need -= above;
-      uint32_t next = 0;
-#pragma unroll
-      for (int i = 0; i < NPER; ++i)
-        if (active >> i & 1) {
-          const int bin = min(255, static_cast<int>((0.5f * f[i] - half_lo) * scale));
-          if (bin > bucket) sel |= 1u << i;
-          else if (bin == bucket) next |= 1u << i;
-        }
-      active = next;
-      __syncwarp();
-    }
-  }
-  int32_t* irow = idx + row * kmax;
-  uint8_t* mrow = mask ? mask + row * nb : nullptr;
-  int carry = 0;
-  long long ksum = 0;
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const int c = lane + 32 * i;
-    const bool si = sel >> i & 1;
-    const unsigned bal = __ballot_sync(0xffffffffu, si);
-    if (si) {
-      irow[carry + __popc(bal & ((1u << lane) - 1u))] = c;
-      ksum += block_size(L, block, c);
-    }
-    if (mrow && c < nb) mrow[c] = si ? 1 : 0;
-    carry += __popc(bal);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
-  if (lane == 0) {
-    cnt[row] = carry;
-    atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
-  }
-}
-
 }  // namespace ropeslr
 
 using namespace ropeslr;
@@ -998,29 +701,13 @@ static int launch_select(const ropeslr_shape* s, const ropeslr_select_params* se
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
   auto* att = reinterpret_cast<unsigned long long*>(attended);
   const int64_t row0 = bh0 * nb, row1 = bh1 * nb;
-  if (sel->topk > 0 && nb <= 1024 && tuning().select == 'r') {  // the radix-select kernel (A/B timing)
+  if (sel->topk > 0 && nb <= 1024) {
     const int64_t off = row0, rows = row1 - row0;
     const unsigned grid = static_cast<unsigned>(ceil_div(rows, 8));
 #define ROPESLR_SEL_CASE(NPER_)                                                                            \
   select_topk_warp_kernel<NPER_><<<grid, 256, 0, st>>>(scores + off * nb, nb, rows, s->L, s->block, sel->topk, \
                                                         kmax, idx + off * kmax, cnt + off,                    \
                                                         mask ? mask + off * nb : nullptr, att + bh0)
-    if (nb <= 128)
-      ROPESLR_SEL_CASE(4);
-    else if (nb <= 256)
-      ROPESLR_SEL_CASE(8);
-    else if (nb <= 512)
-      ROPESLR_SEL_CASE(16);
-    else
-      ROPESLR_SEL_CASE(32);
-#undef ROPESLR_SEL_CASE
-    return launch_status();
-  }
-  if (sel->topk > 0 && nb <= 1024) {
-    const unsigned grid = static_cast<unsigned>(ceil_div(row1 - row0, tb::kWarps));
-#define ROPESLR_SEL_CASE(NPER_)                                                                              \
-  select_topk_bins_kernel<NPER_><<<grid, 32 * tb::kWarps, 0, st>>>(scores, nb, row0, row1, s->L, s->block,   \
-                                                                   sel->topk, kmax, idx, cnt, mask, att)
     if (nb <= 128)
       ROPESLR_SEL_CASE(4);
     else if (nb <= 256)
@@ -1094,15 +781,6 @@ extern "C" size_t ropeslr_select_pooled_workspace_bytes(const ropeslr_shape* s) 
   return scores_bytes(s);
 }
 
-// Head groups of the pipelined selection: the pooling (HBM-bound) of group
-// g + 1 runs on the caller's stream while the scores (FP64 tensor pipe) and
-// the selection (integer pipe) of group g run on a side stream, so the
-// three bounds overlap instead of adding up.  Small problems run unsplit.
-static int pipeline_groups(int64_t BH, int nb) {
-  if (!tuning().k1_pipeline || BH < 4 || static_cast<int64_t>(nb) * nb < 128 * 128) return 1;
-  return BH >= 8 ? 4 : 2;
-}
-
 extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_select_params* sel, const void* q,
                                      const void* k, int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask,
                                      int64_t* attended, double* scores_out, void* ws, size_t ws_bytes,
@@ -1113,36 +791,10 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
   if (!aligned16(q) || !aligned16(k)) return ROPESLR_ERR_ALIGN;
   if (ws == nullptr || ws_bytes < ropeslr_select_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
-  const int64_t BH = s->B * s->H;
-  const int d = static_cast<int>(s->d);
-  const int nb = static_cast<int>(ceil_div(s->L, s->block));
   double* pooled = static_cast<double*>(ws);
   double* scores = scores_out ? scores_out : reinterpret_cast<double*>(static_cast<char*>(ws) + pooled_bytes(s));
-  const int G = pipeline_groups(BH, nb);
-  if (G == 1) {
-    if (int e = launch_pool(s, q, k, pooled, 0, BH, st)) return e;
-    return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores, st);
-  }
-  if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
-  AuxStream aux;
-  if (int e = aux.fork(st)) return e;
-  for (int g = 0; g < G; ++g) {
-    const int64_t b0 = BH * g / G, b1 = BH * (g + 1) / G;
-    if (int e = launch_pool(s, q, k, pooled, b0, b1, st)) return e;
-    if (int e = aux.wait_main()) return e;  // pool of group g (and the memset) done
-    // the non-finite scan over this group's Q and K means (both halves of pooled)
-    if (sel->nonfinite) {
-      if (int e = scan_nonfinite(pooled + b0 * nb * d, true, (b1 - b0) * nb * d, sel->nonfinite,
-                                 ROPESLR_NONFINITE_QK, aux.stream))
-        return e;
-      if (int e = scan_nonfinite(pooled + (BH + b0) * nb * d, true, (b1 - b0) * nb * d, sel->nonfinite,
-                                 ROPESLR_NONFINITE_QK, aux.stream))
-        return e;
-    }
-    if (int e = launch_scores(pooled, scores, nb, d, BH, b0, b1, aux.stream)) return e;
-    if (int e = launch_select(s, sel, scores, idx, kmax, cnt, mask, attended, b0, b1, aux.stream)) return e;
-  }
-  return aux.join();
+  if (int e = launch_pool(s, q, k, pooled, 0, s->B * s->H, st)) return e;
+  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores, st);
 }
 
 extern "C" int ropeslr_select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel,

@@ -581,20 +581,25 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
 
 
 def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *, impl: str = "auto",
-           want_o_sparse: bool = False, out: Optional[torch.Tensor] = None):
+           want_o_sparse: bool = False, out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None):
     """K2 + K4: block-sparse attention with the fused RMSNorm / gate / combine
     epilogue (mechanism.py:321-326, 435-451).  Returns (out [B, L, H*d],
-    o_sparse [B, H, L, d] float32 or None)."""
+    o_sparse [B, H, L, d] float32 or None).  out_dtype: Q's dtype (default)
+    or torch.float32 (the fused result before any bf16 rounding)."""
     q = prep.q
     B, H, L, d = q.shape
     dev = q.device
+    if out_dtype is None:
+        out_dtype = out.dtype if out is not None else q.dtype
+    if out_dtype not in (q.dtype, torch.float32):
+        raise ValueError(f"out_dtype must be {q.dtype} or torch.float32, got {out_dtype}")
     if out is None:
-        out = torch.empty((B, L, H, d), dtype=q.dtype, device=dev)
+        out = torch.empty((B, L, H, d), dtype=out_dtype, device=dev)
     else:
         if tuple(out.shape) not in ((B, L, H, d), (B, L, H * d)):
             raise ValueError(f"out must have shape {(B, L, H, d)} or {(B, L, H * d)}, got {tuple(out.shape)}")
-        if out.dtype != q.dtype or out.device != dev or not out.is_contiguous():
-            raise ValueError("out must be a contiguous tensor of Q's dtype on Q's device")
+        if out.dtype != out_dtype or out.device != dev or not out.is_contiguous():
+            raise ValueError("out must be a contiguous tensor of out_dtype on Q's device")
     o_sparse = torch.empty((B, H, L, d), dtype=torch.float32, device=dev) if want_o_sparse else None
     shp = _shape(q, prep.block)
     impl_code = _lib.IMPL[impl]
@@ -602,7 +607,7 @@ def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *
     _lib.call("ropeslr_attend_fused", ctypes_ref(shp), q.data_ptr(), prep.k.data_ptr(), prep.v.data_ptr(),
               prep.sel.idx.data_ptr(), prep.sel.kmax, prep.sel.cnt.data_ptr(), _ptr(prep.perm), prep.y_lr.data_ptr(),
               prep.g_logit.data_ptr(), float(params.b_g), params.rms_sparse.data_ptr(), float(settings.rms_eps),
-              out.data_ptr(), _ptr(o_sparse), impl_code, ws.data_ptr(), ws.numel(), _stream(dev))
+              out.data_ptr(), _dtype_code(out), _ptr(o_sparse), impl_code, ws.data_ptr(), ws.numel(), _stream(dev))
     return out.view(B, L, H * d), o_sparse
 
 
@@ -610,7 +615,8 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
             params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False, impl: str = "auto",
             head_offset: int = 0, gate_reduce: Optional[Callable[[torch.Tensor], None]] = None,
-            rope: Optional[RopeConfig] = None, check_finite: bool = False):
+            rope: Optional[RopeConfig] = None, check_finite: bool = False,
+            out_dtype: Optional[torch.dtype] = None):
     """RoPeSLR forward (mechanism.py:491-512, Algorithm 1).
 
     q, k, v: post-RoPE [B, H, L, d] (bf16 or f32); x: token features
@@ -625,6 +631,9 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     values they already reduce (block means, gate logits), and the check
     costs one 4-byte read-back (a stream synchronisation).
 
+    ``out_dtype=torch.float32`` returns the fused output in float32 (the
+    epilogue's result before the bf16 rounding of a bf16 output).
+
     Returns the output [B, L, H*d] (x's dtype), or a ForwardTrace when
     ``trace`` (adds the float32 branch outputs, the gate and the masks)."""
     flag = torch.zeros(1, dtype=torch.int32, device=q.device) if check_finite else None
@@ -634,7 +643,7 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
         raise_nonfinite(flag)
     if gate_reduce is not None:
         gate_reduce(prep.g_logit)
-    out, o_sparse = attend(prep, params, settings, impl=impl, want_o_sparse=trace)
+    out, o_sparse = attend(prep, params, settings, impl=impl, want_o_sparse=trace, out_dtype=out_dtype)
     if not trace:
         return out
     L = q.shape[2]

@@ -1,6 +1,6 @@
 """K1 experiments at the config-3 shape: time the selection (pool + scores +
-top-k) with the value-bin vs radix top-k kernel and with / without the
-head-group pipeline, and check every variant gives the same index lists."""
+top-k) with the DMMA vs CUDA-core block scores, and check both give the
+same index lists."""
 import os, sys
 sys.path[:0] = ['.', 'tests', 'oracle']
 import torch
@@ -27,15 +27,14 @@ def timed(fn, n=int(os.environ.get("EXP_ITERS", "20"))):
 
 
 for rep in range(int(os.environ.get("EXP_REPS", "2"))):
-    for sel in ("bins", "radix"):
-        for pipe in (1, 0):
-            with P._lib.option("select", "r" if sel == "radix" else 0), P._lib.option("k1_pipeline", pipe):
-                ms = timed(lambda: P.select_blocks(q, k, sp, want_mask=False))
-                out = P.select_blocks(q, k, sp, want_mask=False)
-            torch.cuda.synchronize()
-            print(f"select={sel:5s} pipeline={pipe} select_blocks {ms:.3f} ms", flush=True)
-            res[(sel, pipe)] = out.idx.clone()
-ref = res[("radix", 0)]
+    for sc in ("dmma-pipe", "fma"):
+        with P._lib.option("scores", "f" if sc == "fma" else 0):
+            ms = timed(lambda: P.select_blocks(q, k, sp, want_mask=False))
+            out = P.select_blocks(q, k, sp, want_mask=False)
+        torch.cuda.synchronize()
+        print(f"scores={sc:9s} select_blocks {ms:.3f} ms", flush=True)
+        res[sc] = out.idx.clone()
+ref = res["dmma-pipe"]
 print("identical index lists:", all(torch.equal(ref, t) for t in res.values()))
 # the stages alone
 pooled = torch.empty((2, H, -(-L // 128), 128), dtype=torch.float64, device=q.device)

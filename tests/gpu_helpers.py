@@ -34,6 +34,31 @@ def assert_close(got, want, dtype: str, what: str = "", scale: float = 1.0):
     return err, mr
 
 
+def bf16_half_ulp(x) -> np.ndarray:
+    """Half a bf16 ulp at |x| (8 significant bits): the rounding error of
+    storing x in bf16."""
+    a = np.abs(np.asarray(x, np.float64))
+    e = np.floor(np.log2(np.maximum(a, 2.0 ** -126)))
+    return 2.0 ** (e - 8)
+
+
+def assert_close_bf16_store(got, want, what: str = ""):
+    """A bf16-stored output against the float64 reference: the north-star
+    bar (max-abs 2e-2, mean-rel 1e-2) on top of the rounding of the stored
+    value itself (half a bf16 ulp of the reference value: 0.0078 at |x| in
+    [2, 4), 0.0156 in [4, 8)).  The op's float32 output (out_dtype) is held to
+    the bar alone."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    tol = TOL["bf16"]
+    excess = np.abs(got - want) - bf16_half_ulp(want)
+    err = float(np.max(excess)) if got.size else 0.0
+    mr = mean_rel(got, want)
+    assert err <= tol["max_abs"], f"{what}: max-abs beyond the bf16 store {err:.3e} > {tol['max_abs']:.1e}"
+    assert mr <= tol["mean_rel"], f"{what}: mean-rel {mr:.3e} > {tol['mean_rel']:.1e}"
+    return float(np.max(np.abs(got - want))) if got.size else 0.0, mr
+
+
 def torch_dtype(name: str):
     return torch.bfloat16 if name == "bf16" else torch.float32
 
