@@ -222,6 +222,32 @@ int ropeslr_linear_branch(const ropeslr_shape* shape, const void* q_lin, const v
                           void* y_lr, float* o_lr, void* workspace, size_t workspace_bytes,
                           void* stream);
 
+/* Linear compensator with the PE injection in the kernels (bf16, d = 128;
+ * csrc/linear_umma.cu).  The caller supplies the frozen projections of the
+ * PLAIN token features, q_lin/k_lin/v_lin = x W_{q,k,v}[h] ([B,H,L,d] bf16,
+ * no PE, no RoPE).  x_hat W = x W + (alpha * PE) W, and the second term is
+ * parameter-only and axis-separable: ropeslr_linear_tables folds it into
+ * per-axis tables T_axis = (alpha * P_axis) W_z[h] ([n_axis, d] per local
+ * head and z in {q, k, v}, bf16) plus the gate's per-axis scalars
+ * G_axis = (alpha * P_axis) . w_g over the local columns (float32), from
+ * w_q/w_k/w_v float32 [H, D_total, d] (the local heads' backbone weights).
+ * Cache the tables while the parameters do not change.  Then
+ * ropeslr_linear_branch_pe runs the tcgen05 state pass (phi(K)^T V and
+ * sum phi(K), fixed-order reduction), the apply pass (phi(Q) S / max(phi(Q) z,
+ * 1e-8), RMSNorm * rms_lowrank -> y_lr, o_lr nullable) and the gate logits
+ * (x . w_g + G rows; g_logit nullable).  `state` (nullable) receives S and z
+ * as float32 [B*H, d, 144] (column 128 = z).  Both return ROPESLR_ERR_SHAPE
+ * for shapes outside the path (then pass x_hat projections to
+ * ropeslr_linear_branch). */
+size_t ropeslr_linear_tables_bytes(const ropeslr_shape* shape, const ropeslr_token_args* tok);
+int ropeslr_linear_tables(const ropeslr_shape* shape, const ropeslr_token_args* tok, const float* w_q,
+                          const float* w_k, const float* w_v, void* tables, size_t tables_bytes, void* stream);
+size_t ropeslr_linear_pe_workspace_bytes(const ropeslr_shape* shape, const ropeslr_token_args* tok);
+int ropeslr_linear_branch_pe(const ropeslr_shape* shape, const ropeslr_token_args* tok, const void* q_lin,
+                             const void* k_lin, const void* v_lin, const void* tables, const float* rms_lowrank,
+                             float eps, void* y_lr, float* o_lr, float* g_logit, float* state, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------ K4: fused epilogue
  * out = RMS(o_sparse) * rms_sparse + sigmoid(g_logit + b_g) * y_lr
  * (mechanism.py:437-451).  Standalone form used after the CUDA-core

@@ -73,6 +73,11 @@ _SIGNATURES = {
     "ropeslr_gate_logits": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp]),
     "ropeslr_linear_workspace_bytes": (c_sz, [P(Shape)]),
     "ropeslr_linear_branch": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_f32, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "ropeslr_linear_tables_bytes": (c_sz, [P(Shape), P(TokenArgs)]),
+    "ropeslr_linear_tables": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "ropeslr_linear_pe_workspace_bytes": (c_sz, [P(Shape), P(TokenArgs)]),
+    "ropeslr_linear_branch_pe": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp, c_vp,
+                                         c_vp, c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_fuse_output": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_f32, c_vp, c_f32, c_vp, c_vp]),
     "ropeslr_attend_fused": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp,
                                      c_f32, c_vp, c_i32, c_vp, c_i32, c_vp, c_sz, c_vp]),

@@ -1,0 +1,793 @@
+// K3 `linear` mode on tcgen05 with the 3D absolute-PE injection inside the
+// kernels: the linear compensator of mechanism.py:33-36, 347-362, fed by the
+// backbone projections of x_hat = x + alpha * PE (mechanism.py:429-432).
+//
+// The caller supplies the frozen projections of the plain token features,
+// q_lin / k_lin / v_lin = x W_{q,k,v}[h] ([B, H, L, d] bf16; a DiT computes
+// them for its own attention anyway).  The PE part of x_hat W is
+// parameter-only and axis-separable,
+//
+//   (alpha * PE[p]) W = T[t] + T[x] + T[y],  T_axis = (alpha * P_axis) W,
+//
+// so ropeslr_linear_tables folds it once into per-axis [n_axis, d] tables
+// per head and tensor (and the gate into per-axis scalars); the kernels add
+// three table rows per token on the way through:
+//
+//   state   (one CTA per (head, token chunk))  TMA K, V tiles -> k + T_k, phi,
+//           v + T_v in place in shared memory -> tcgen05 S += phi(K)^T V
+//           (M = d, N = d, K = 128 tokens, both operands MN-major) and
+//           z += phi(K)^T 1 (N = 16) into TMEM; the chunk's [d, d | z]
+//           partial goes to the workspace;
+//   reduce  partials summed in fixed chunk order (float64), written as the
+//           apply GEMM's B operand image [S | z] (K-major, 128B-swizzled),
+//           split into bf16 hi + lo (~16 mantissa bits);
+//   apply   (one CTA per (head, token chunk))  TMA Q tiles -> phi(q + T_q)
+//           in place -> tcgen05 [phi(Q) S | phi(Q) z] (N = 144) as hi + lo
+//           MMAs into a double-buffered TMEM accumulator; the epilogue
+//           warps divide by max(phi(q) . z, 1e-8), RMS-normalise with
+//           rms_lowrank and store y_lr (bf16) and optionally o_lr (f32);
+//   gate    g_logit = x . w_g over the local columns + G[t] + G[x] + G[y]
+//           (one warp per token: X is read once, no per-element PE gather).
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace ropeslr {
+namespace lnu {
+
+using namespace sm100;
+
+constexpr int D = 128;                  // head dim
+constexpr int M = 128;                  // tokens per tile
+constexpr int HALF = M * 128;           // 16 KiB: one 64-column half of a tile (TMA box)
+constexpr int TILE = 2 * HALF;          // 32 KiB
+constexpr int TAB_PITCH = 272;          // bytes per bf16 table row: 128 values + 16 B (conflict-free rows)
+constexpr int NB = 144;                 // apply GEMM N: 128 numerators + the denominator column + pad
+constexpr int BHALF = NB * 128;         // 18 KiB: one 64-wide K half of the B image
+constexpr int BIMG = 2 * BHALF;         // 36 KiB: the hi (or lo) image
+constexpr int NPART = NB;               // columns of a state partial: S row (128) | z | pad
+constexpr int ONES_BYTES = 16 * 128 * 2;  // K-major [16 rows][128 tokens] bf16: row 0 ones
+constexpr float kFloor = 1e-8f;         // mechanism.py:347
+
+__device__ __forceinline__ float elu1(float v) { return v > 0.f ? v + 1.f : __expf(v); }
+
+// Chunk c (0..15: 8 bf16 each) of row r of a TMA-loaded [128 x 128] tile,
+// two 64-column halves in the 128B-swizzled layout.
+__device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int r, int c) {
+  return reinterpret_cast<uint4*>(tile + (c >> 3) * HALF + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+// In place on row r of a tile: v + T[rt] + T[rx] + T[ry] (tables optional),
+// then phi when PHI; rows of tokens beyond L become zero.
+template <bool PHI>
+__device__ __forceinline__ void transform_row(uint8_t* tile, int r, bool valid, const uint8_t* tab, int rt, int rx,
+                                              int ry) {
+#pragma unroll 4
+  for (int c = 0; c < 16; ++c) {
+    uint4* p = tile_chunk(tile, r, c);
+    if (!valid) {
+      *p = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    float f[8];
+    bf16x8_to_f32(*p, f);
+    if (tab != nullptr) {
+      float a[8], b[8], e[8];
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(tab + rt * TAB_PITCH + c * 16), a);
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(tab + rx * TAB_PITCH + c * 16), b);
+      bf16x8_to_f32(*reinterpret_cast<const uint4*>(tab + ry * TAB_PITCH + c * 16), e);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] += (a[i] + b[i]) + e[i];
+    }
+    if (PHI) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = elu1(f[i]);
+    }
+    *p = f32_to_bf16x8(f);
+  }
+}
+
+struct Grid3 {
+  int T, Hg, Wg;
+  __device__ __forceinline__ void rows(int64_t l, int& rt, int& rx, int& ry) const {
+    const int64_t hw = static_cast<int64_t>(Hg) * Wg;
+    rt = static_cast<int>(l / hw);
+    rx = T + static_cast<int>((l / Wg) % Hg);
+    ry = T + Hg + static_cast<int>(l % Wg);
+  }
+};
+
+struct StateArgs {
+  int64_t L;
+  int H;
+  Grid3 g;
+  int use_pe;
+  int nrows;
+  int ntiles;           // ceil(L / 128)
+  int tiles_per_cta;
+  int nchunks;
+  const uint8_t* tables;  // [H][3][nrows][TAB_PITCH] bf16 (q, k, v)
+  float* partial;       // [BH][nchunks][128][NPART]
+};
+
+// smem: K ring (2 x 32 KiB) | V ring (2 x 32 KiB) | ones (4 KiB) | T_k | T_v | barriers
+struct StateLay {
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + 2 * TILE;
+  static constexpr int OFF_ONES = OFF_V + 2 * TILE;
+  static constexpr int OFF_TAB = OFF_ONES + ONES_BYTES;
+  __host__ __device__ static int off_bar(int nrows) { return OFF_TAB + ((2 * nrows * TAB_PITCH + 127) / 128) * 128; }
+  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 8 * 8 + 16; }
+};
+
+constexpr int kStateThreads = 192;  // warps 0-3 transform, 4 TMA, 5 MMA + TMEM
+
+__global__ void __launch_bounds__(kStateThreads, 1)
+    linear_state_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ StateArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.y, chunk = blockIdx.x;
+  const int h = bh % a.H;
+  const int t0 = chunk * a.tiles_per_cta;
+  const int t1 = min(a.ntiles, t0 + a.tiles_per_cta);
+  const int n = max(0, t1 - t0);
+  uint8_t* sK = smem + StateLay::OFF_K;
+  uint8_t* sV = smem + StateLay::OFF_V;
+  uint8_t* sOnes = smem + StateLay::OFF_ONES;
+  uint8_t* sTab = smem + StateLay::OFF_TAB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(a.nrows));
+  uint64_t* full = bars;       // [2] TMA -> transform
+  uint64_t* ready = bars + 2;  // [2] transform -> MMA
+  uint64_t* empty = bars + 4;  // [2] MMA -> TMA
+  uint64_t* done = bars + 6;   // MMA -> readout
+  uint64_t* tabf = bars + 7;   // tables landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * a.nrows * TAB_PITCH;
+  const int tab_bytes = a.nrows * TAB_PITCH;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&ready[i], 128);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(tabf, 1);
+    fence_mbar_init();
+  }
+  // the constant B operand of z: K-major [16 rows][128 tokens], row 0 ones;
+  // every row is constant, so the 128B swizzle leaves it as is
+  for (int i = threadIdx.x; i < ONES_BYTES / 16; i += blockDim.x) {
+    const int row = (i * 16 % 2048) / 128;  // two 2 KiB K-halves of 16 rows x 128 B
+    const uint32_t one2 = 0x3F803F80u;
+    reinterpret_cast<uint4*>(sOnes)[i] = row == 0 ? make_uint4(one2, one2, one2, one2) : make_uint4(0, 0, 0, 0);
+  }
+  fence_proxy_async_smem();
+  if (warp == 5) {
+    tmem_alloc(tmem_slot, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    if (elect_one()) {
+      if (a.use_pe) {
+        mbar_arrive_expect_tx(tabf, 2 * tab_bytes);
+        bulk_load_1d(sTab, gtab + 1 * tab_bytes, tab_bytes, tabf, policy_evict_last());
+        bulk_load_1d(sTab + tab_bytes, gtab + 2 * tab_bytes, tab_bytes, tabf, policy_evict_last());
+      }
+      const uint64_t pol = policy_evict_first();
+      for (int i = 0; i < n; ++i) {
+        const int s = i & 1;
+        if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], 2 * TILE);
+        const int row = (t0 + i) * M;
+        uint8_t* k = sK + s * TILE;
+        uint8_t* v = sV + s * TILE;
+        tma_load_3d_hint(k, &tmK, &full[s], 0, row, bh, pol);
+        tma_load_3d_hint(k + HALF, &tmK, &full[s], 64, row, bh, pol);
+        tma_load_3d_hint(v, &tmV, &full[s], 0, row, bh, pol);
+        tma_load_3d_hint(v + HALF, &tmV, &full[s], 64, row, bh, pol);
+      }
+    }
+  } else if (warp == 5) {
+    constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
+    constexpr uint32_t idesc_z = idesc_bf16_f32(M, 16, true, false);
+    const bool leader = elect_one();
+    for (int i = 0; i < n; ++i) {
+      const int s = i & 1;
+      mbar_wait(&ready[s], (i >> 1) & 1);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t dA = desc_sw128(smem_u32(sK + s * TILE), HALF, 1024);
+        const uint64_t dB = desc_sw128(smem_u32(sV + s * TILE), HALF, 1024);
+        const uint64_t dO = desc_sw128(smem_u32(sOnes), 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < M / 16; ++kk) {
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          const uint64_t da = dA + static_cast<uint64_t>((kk * 2048) >> 4);
+          mma_bf16_ss(tmem, da, dB + static_cast<uint64_t>((kk * 2048) >> 4), idesc_s, acc);
+          mma_bf16_ss(tmem + 128, da, dO + static_cast<uint64_t>(((kk & 3) * 32 + (kk >> 2) * 2048) >> 4), idesc_z,
+                      acc);
+        }
+        mma_commit(&empty[s]);
+        if (i == n - 1) mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // transform warps: one token row per thread
+    const int r = threadIdx.x;
+    const uint8_t* tk = nullptr;
+    const uint8_t* tv = nullptr;
+    if (a.use_pe) {
+      mbar_wait(tabf, 0);
+      tk = sTab;
+      tv = sTab + tab_bytes;
+    }
+    for (int i = 0; i < n; ++i) {
+      const int s = i & 1;
+      mbar_wait(&full[s], (i >> 1) & 1);
+      const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
+      const bool valid = l < a.L;
+      int rt = 0, rx = 0, ry = 0;
+      if (valid) a.g.rows(l, rt, rx, ry);
+      transform_row<true>(sK + s * TILE, r, valid, tk, rt, rx, ry);
+      transform_row<false>(sV + s * TILE, r, valid, tv, rt, rx, ry);
+      fence_proxy_async_smem();
+      mbar_arrive(&ready[s]);
+    }
+    // the chunk's partial [S | z]: TMEM lane r = row r (d_k) of S
+    float* dst = a.partial + ((static_cast<int64_t>(bh) * a.nchunks + chunk) * D + r) * NPART;
+    if (n > 0) {
+      mbar_wait(done, 0);
+      tc_fence_after();
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(lane_base + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(
+              __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+      }
+      uint32_t v[16];
+      tmem_ld16(lane_base + 128, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(dst + 128 + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+    } else {
+      for (int j = 0; j < NPART; ++j) dst[j] = 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+// Sum the chunk partials (fixed order, float64) and write the apply GEMM's B
+// operand: B[n][k] = S[k][n] for n < 128, B[128][k] = z[k], zero rows above;
+// K-major, two 64-wide K halves of [144 rows x 128 B], 128B-swizzled as a
+// 1024-aligned shared-memory copy expects; bf16 hi image then lo image.
+// Also S and z in float32 (state [BH][128][NPART]) for inspection.
+__global__ void __launch_bounds__(256) linear_reduce_image_kernel(const float* __restrict__ partial, int nchunks,
+                                                                  uint8_t* __restrict__ bimg,
+                                                                  float* __restrict__ state) {
+  const int bh = blockIdx.x;
+  const float* src = partial + static_cast<int64_t>(bh) * nchunks * D * NPART;
+  uint8_t* img = bimg + static_cast<int64_t>(bh) * 2 * BIMG;
+  for (int e = threadIdx.x; e < NB * D; e += blockDim.x) {
+    const int n = e / D, k = e % D;
+    double acc = 0.0;
+    if (n <= 128)
+      for (int c = 0; c < nchunks; ++c) acc += src[(static_cast<int64_t>(c) * D + k) * NPART + n];
+    if (state != nullptr && n <= 128) state[(static_cast<int64_t>(bh) * D + k) * NPART + n] = static_cast<float>(acc);
+    const __nv_bfloat16 hi = __double2bfloat16(acc);
+    const __nv_bfloat16 lo = __double2bfloat16(acc - static_cast<double>(__bfloat162float(hi)));
+    const int half = k >> 6, ch = (k & 63) >> 3, el = k & 7;
+    const int off = half * BHALF + n * 128 + ((ch ^ (n & 7)) << 4) + el * 2;
+    *reinterpret_cast<__nv_bfloat16*>(img + off) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(img + BIMG + off) = lo;
+  }
+}
+
+struct ApplyArgs {
+  int64_t L;
+  int H;
+  Grid3 g;
+  int use_pe;
+  int nrows;
+  int ntiles;
+  int tiles_per_cta;
+  const uint8_t* tables;  // [H][3][nrows][TAB_PITCH]
+  const uint8_t* bimg;    // [BH][2][BIMG]
+  const float* rms_lr;
+  float eps;
+  __nv_bfloat16* y_lr;    // [B, L, H, d]
+  float* o_lr;            // [B, H, L, d] nullable
+};
+
+// smem: Q ring (2 x 32 KiB) | B image hi | lo (2 x 36 KiB) | T_q | rms | barriers
+struct ApplyLay {
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_B = OFF_Q + 2 * TILE;
+  static constexpr int OFF_TAB = OFF_B + 2 * BIMG;
+  __host__ __device__ static int off_rms(int nrows) { return OFF_TAB + ((nrows * TAB_PITCH + 127) / 128) * 128; }
+  __host__ __device__ static int off_bar(int nrows) { return off_rms(nrows) + D * 4; }
+  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 12 * 8 + 16; }
+};
+
+constexpr int kApplyThreads = 320;  // warps 0-3 transform, 4-7 epilogue, 8 TMA, 9 MMA + TMEM
+
+__global__ void __launch_bounds__(kApplyThreads, 1)
+    linear_apply_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ ApplyArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int bh = blockIdx.y;
+  const int h = bh % a.H, b = bh / a.H;
+  const int t0 = blockIdx.x * a.tiles_per_cta;
+  const int t1 = min(a.ntiles, t0 + a.tiles_per_cta);
+  const int n = max(0, t1 - t0);
+  uint8_t* sQ = smem + ApplyLay::OFF_Q;
+  uint8_t* sB = smem + ApplyLay::OFF_B;
+  uint8_t* sTab = smem + ApplyLay::OFF_TAB;
+  float* sRms = reinterpret_cast<float*>(smem + ApplyLay::off_rms(a.nrows));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ApplyLay::off_bar(a.nrows));
+  uint64_t* full = bars;        // [2]
+  uint64_t* ready = bars + 2;   // [2]
+  uint64_t* empty = bars + 4;   // [2]
+  uint64_t* accf = bars + 6;    // [2] MMA -> epilogue
+  uint64_t* acce = bars + 8;    // [2] epilogue -> MMA
+  uint64_t* init = bars + 10;   // B image + table landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  const int tab_bytes = a.nrows * TAB_PITCH;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&ready[i], 128);
+      mbar_init(&empty[i], 1);
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 128);
+    }
+    mbar_init(init, 1);
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < D; i += blockDim.x) sRms[i] = a.rms_lr[i];
+  if (warp == 9) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (elect_one()) {
+      const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * tab_bytes;
+      mbar_arrive_expect_tx(init, 2 * BIMG + (a.use_pe ? tab_bytes : 0));
+      bulk_load_1d(sB, a.bimg + static_cast<int64_t>(bh) * 2 * BIMG, 2 * BIMG, init, policy_evict_last());
+      if (a.use_pe) bulk_load_1d(sTab, gtab, tab_bytes, init, policy_evict_last());
+      const uint64_t pol = policy_evict_first();
+      for (int i = 0; i < n; ++i) {
+        const int s = i & 1;
+        if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], TILE);
+        const int row = (t0 + i) * M;
+        tma_load_3d_hint(sQ + s * TILE, &tmQ, &full[s], 0, row, bh, pol);
+        tma_load_3d_hint(sQ + s * TILE + HALF, &tmQ, &full[s], 64, row, bh, pol);
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idesc = idesc_bf16_f32(M, NB, false, false);
+    const bool leader = elect_one();
+    mbar_wait(init, 0);
+    const uint64_t dBh = desc_sw128(smem_u32(sB), 16, 1024);
+    const uint64_t dBl = desc_sw128(smem_u32(sB + BIMG), 16, 1024);
+    for (int i = 0; i < n; ++i) {
+      const int s = i & 1, ab = i & 1;
+      mbar_wait(&ready[s], (i >> 1) & 1);
+      if (i >= 2) mbar_wait(&acce[ab], ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t dA = desc_sw128(smem_u32(sQ + s * TILE), 16, 1024);
+        const uint32_t acc_t = tmem + ab * 256;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = ((kk & 3) * 32 + (kk >> 2) * HALF) >> 4;
+          const uint32_t kb = ((kk & 3) * 32 + (kk >> 2) * BHALF) >> 4;
+          mma_bf16_ss(acc_t, dA + ka, dBh + kb, idesc, kk > 0 ? 1u : 0u);
+          mma_bf16_ss(acc_t, dA + ka, dBl + kb, idesc, 1u);
+        }
+        mma_commit(&empty[s]);
+        mma_commit(&accf[ab]);
+      }
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    const int r = threadIdx.x;
+    const uint8_t* tq = nullptr;
+    if (a.use_pe) {
+      mbar_wait(init, 0);
+      tq = sTab;
+    }
+    for (int i = 0; i < n; ++i) {
+      const int s = i & 1;
+      mbar_wait(&full[s], (i >> 1) & 1);
+      const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
+      const bool valid = l < a.L;
+      int rt = 0, rx = 0, ry = 0;
+      if (valid) a.g.rows(l, rt, rx, ry);
+      transform_row<true>(sQ + s * TILE, r, valid, tq, rt, rx, ry);
+      fence_proxy_async_smem();
+      mbar_arrive(&ready[s]);
+    }
+  } else {
+    // epilogue warps 4-7: TMEM lane quarter warp % 4, token row r
+    const int q4 = warp - 4;
+    const int r = q4 * 32 + (threadIdx.x & 31);
+    for (int i = 0; i < n; ++i) {
+      const int ab = i & 1;
+      mbar_wait(&accf[ab], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + ab * 256 + (static_cast<uint32_t>(q4 * 32) << 16);
+      uint32_t den_u[16];
+      tmem_ld16(base + 128, den_u);
+      tmem_wait_ld();
+      const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
+      float o[D];
+      float ss = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(base + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          o[c * 32 + j] = __uint_as_float(v[j]) * inv_den;
+          ss = fmaf(o[c * 32 + j], o[c * 32 + j], ss);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acce[ab]);
+      const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
+      if (l >= a.L) continue;
+      const float inv = rsqrtf(ss / static_cast<float>(D) + a.eps);
+      if (a.o_lr != nullptr) {
+        float* dst = a.o_lr + (static_cast<int64_t>(bh) * a.L + l) * D;
+#pragma unroll
+        for (int j = 0; j < D; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+      }
+      __nv_bfloat16* dst = a.y_lr + ((static_cast<int64_t>(b) * a.L + l) * a.H + h) * D;
+#pragma unroll
+      for (int j = 0; j < D; j += 16) {
+        uint32_t u[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(o[j + 2 * e] * inv * sRms[j + 2 * e],
+                                                    o[j + 2 * e + 1] * inv * sRms[j + 2 * e + 1]);
+          u[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + j), "r"(u[0]),
+                     "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
+                     : "memory");
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- tables
+// T[h][z][row][j] = sum_c alpha[c] P_axis[row][c] W_z[h][c][j] over all
+// D_total columns (x_hat W with x_hat the full token row), rounded to bf16
+// into padded rows.  grid (ceil(nrows / 16), 3 H), 128 threads (column j).
+__global__ void __launch_bounds__(128) linear_fold_kernel(const float* __restrict__ pe_t, const float* __restrict__ pe_x,
+                                                          const float* __restrict__ pe_y,
+                                                          const float* __restrict__ alpha,
+                                                          const float* __restrict__ wq, const float* __restrict__ wk,
+                                                          const float* __restrict__ wv, int64_t Dt, int T, int Hg,
+                                                          int Wg, uint8_t* __restrict__ tables) {
+  constexpr int RT = 16, CK = 32;
+  __shared__ float sp[RT][CK];
+  const int nrows = T + Hg + Wg;
+  const int r0 = blockIdx.x * RT;
+  const int h = blockIdx.y / 3, z = blockIdx.y % 3;
+  const float* W = (z == 0 ? wq : z == 1 ? wk : wv) + static_cast<int64_t>(h) * Dt * D;
+  const int j = threadIdx.x;
+  float acc[RT];
+#pragma unroll
+  for (int i = 0; i < RT; ++i) acc[i] = 0.f;
+  for (int64_t c0 = 0; c0 < Dt; c0 += CK) {
+    for (int e = threadIdx.x; e < RT * CK; e += blockDim.x) {
+      const int rr = e / CK, cc = e % CK;
+      const int row = r0 + rr;
+      const int64_t c = c0 + cc;
+      float v = 0.f;
+      if (row < nrows && c < Dt) {
+        const float* src = row < T ? pe_t + static_cast<int64_t>(row) * Dt
+                         : row < T + Hg ? pe_x + static_cast<int64_t>(row - T) * Dt
+                                        : pe_y + static_cast<int64_t>(row - T - Hg) * Dt;
+        v = alpha[c] * src[c];
+      }
+      sp[rr][cc] = v;
+    }
+    __syncthreads();
+    const int ck = static_cast<int>(Dt - c0 < CK ? Dt - c0 : CK);
+    for (int cc = 0; cc < ck; ++cc) {
+      const float w = W[(c0 + cc) * D + j];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) acc[i] = fmaf(sp[i][cc], w, acc[i]);
+    }
+    __syncthreads();
+  }
+  uint8_t* out = tables + (static_cast<int64_t>(h) * 3 + z) * nrows * TAB_PITCH;
+#pragma unroll
+  for (int i = 0; i < RT; ++i) {
+    const int row = r0 + i;
+    if (row < nrows) reinterpret_cast<__nv_bfloat16*>(out + row * TAB_PITCH)[j] = __float2bfloat16_rn(acc[i]);
+  }
+}
+
+// G[row] = sum over the local columns of alpha P_axis[row] w_g (float32).
+__global__ void __launch_bounds__(256) linear_gate_fold_kernel(const float* __restrict__ pe_t,
+                                                               const float* __restrict__ pe_x,
+                                                               const float* __restrict__ pe_y,
+                                                               const float* __restrict__ alpha,
+                                                               const float* __restrict__ w_g, int64_t Dt, int64_t c0,
+                                                               int64_t ncols, int T, int Hg, float* __restrict__ G) {
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  const float* src = row < T ? pe_t + static_cast<int64_t>(row) * Dt
+                   : row < T + Hg ? pe_x + static_cast<int64_t>(row - T) * Dt
+                                  : pe_y + static_cast<int64_t>(row - T - Hg) * Dt;
+  float s = 0.f;
+  for (int64_t c = c0 + threadIdx.x; c < c0 + ncols; c += blockDim.x) s = fmaf(alpha[c] * src[c], w_g[c], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    G[row] = t;
+  }
+}
+
+// g_logit[b, l] = x[b, l, local cols] . w_g[local cols] + G[t] + G[x] + G[y]
+// (no bias: the fused epilogue adds it after any head-parallel all-reduce).
+// One warp per token; 16-byte loads of X.
+__global__ void __launch_bounds__(256) linear_gate_kernel(const __nv_bfloat16* __restrict__ x, int64_t row_stride,
+                                                          const float* __restrict__ w_g, int64_t ncols, int64_t BL,
+                                                          int64_t L, Grid3 g, const float* __restrict__ G,
+                                                          float* __restrict__ g_logit) {
+  const int64_t tok = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (tok >= BL) return;
+  const __nv_bfloat16* row = x + tok * row_stride;
+  float s = 0.f;
+  for (int64_t c = lane * 8; c < ncols; c += 256) {
+    float f[8];
+    bf16x8_to_f32(*reinterpret_cast<const uint4*>(row + c), f);
+    const float4 wa = *reinterpret_cast<const float4*>(w_g + c);
+    const float4 wb = *reinterpret_cast<const float4*>(w_g + c + 4);
+    s = fmaf(f[0], wa.x, s);
+    s = fmaf(f[1], wa.y, s);
+    s = fmaf(f[2], wa.z, s);
+    s = fmaf(f[3], wa.w, s);
+    s = fmaf(f[4], wb.x, s);
+    s = fmaf(f[5], wb.y, s);
+    s = fmaf(f[6], wb.z, s);
+    s = fmaf(f[7], wb.w, s);
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    if (G != nullptr) {
+      int rt, rx, ry;
+      g.rows(tok % L, rt, rx, ry);
+      s += (G[rt] + G[rx]) + G[ry];
+    }
+    g_logit[tok] = s;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// [BH, L, 128] bf16 as a 3-D tensor, box [64 cols, 128 rows, 1], 128B swizzle;
+// rows past L read as zero.
+static bool make_map(CUtensorMap* m, const void* base, int64_t BH, int64_t L) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(BH)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(L) * D * 2};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(M), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int nrows_of(const ropeslr_token_args* t) { return t->grid_t + t->grid_h + t->grid_w; }
+
+// CTAs per head: about two waves of the persistent-size grid over all heads.
+static int chunks_per_head(int64_t BH, int ntiles) {
+  int64_t c = (2 * static_cast<int64_t>(num_sms()) + BH - 1) / BH;
+  if (c > ntiles) c = ntiles;
+  return static_cast<int>(c < 1 ? 1 : c);
+}
+
+static size_t up256(size_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace lnu
+}  // namespace ropeslr
+
+using namespace ropeslr;
+
+static bool linear_pe_eligible(const ropeslr_shape* s, const ropeslr_token_args* t) {
+  if (!s || !t || s->dtype != ROPESLR_BF16 || s->d != lnu::D) return false;
+  const int nr = lnu::nrows_of(t);
+  return lnu::StateLay::bytes(nr) <= 227 * 1024 && lnu::ApplyLay::bytes(nr) <= 227 * 1024;
+}
+
+extern "C" size_t ropeslr_linear_tables_bytes(const ropeslr_shape* s, const ropeslr_token_args* t) {
+  if (!linear_pe_eligible(s, t)) return 0;
+  const int nr = lnu::nrows_of(t);
+  return lnu::up256(static_cast<size_t>(s->H) * 3 * nr * lnu::TAB_PITCH) + lnu::up256(static_cast<size_t>(nr) * 4);
+}
+
+extern "C" int ropeslr_linear_tables(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_q,
+                                     const float* w_k, const float* w_v, void* tables, size_t tables_bytes,
+                                     void* stream) {
+  if (!s || !t || !tables) return ROPESLR_ERR_NULL;
+  if (!linear_pe_eligible(s, t)) return ROPESLR_ERR_SHAPE;
+  if (tables_bytes < ropeslr_linear_tables_bytes(s, t)) return ROPESLR_ERR_WORKSPACE;
+  if (!t->use_pe) return ROPESLR_OK;  // no PE: the tables are not read
+  if (!w_q || !w_k || !w_v || !t->pe_t || !t->pe_x || !t->pe_y || !t->alpha || !t->w_g) return ROPESLR_ERR_NULL;
+  if (t->d_model < (t->head_offset + s->H) * s->d) return ROPESLR_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nr = lnu::nrows_of(t);
+  uint8_t* tab = static_cast<uint8_t*>(tables);
+  lnu::linear_fold_kernel<<<dim3(static_cast<unsigned>(ceil_div(nr, 16)), static_cast<unsigned>(3 * s->H)), 128, 0,
+                            st>>>(t->pe_t, t->pe_x, t->pe_y, t->alpha, w_q, w_k, w_v, t->d_model, t->grid_t,
+                                  t->grid_h, t->grid_w, tab);
+  if (int e = launch_status()) return e;
+  float* G = reinterpret_cast<float*>(tab + lnu::up256(static_cast<size_t>(s->H) * 3 * nr * lnu::TAB_PITCH));
+  lnu::linear_gate_fold_kernel<<<nr, 256, 0, st>>>(t->pe_t, t->pe_x, t->pe_y, t->alpha, t->w_g, t->d_model,
+                                                   t->head_offset * s->d, s->H * s->d, t->grid_t, t->grid_h, G);
+  return launch_status();
+}
+
+extern "C" size_t ropeslr_linear_pe_workspace_bytes(const ropeslr_shape* s, const ropeslr_token_args* t) {
+  if (!linear_pe_eligible(s, t)) return 0;
+  const int64_t BH = s->B * s->H;
+  const int ntiles = static_cast<int>(ceil_div(s->L, lnu::M));
+  const int nch = lnu::chunks_per_head(BH, ntiles);
+  return lnu::up256(static_cast<size_t>(BH) * nch * lnu::D * lnu::NPART * 4) +
+         lnu::up256(static_cast<size_t>(BH) * 2 * lnu::BIMG);
+}
+
+extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_token_args* t, const void* q_lin,
+                                        const void* k_lin, const void* v_lin, const void* tables,
+                                        const float* rms_lowrank, float eps, void* y_lr, float* o_lr,
+                                        float* g_logit, float* state, void* ws, size_t ws_bytes, void* stream) {
+  if (!s || !t || !q_lin || !k_lin || !v_lin || !tables || !rms_lowrank || !y_lr || !t->x || !t->w_g)
+    return ROPESLR_ERR_NULL;
+  if (s->B < 1 || s->H < 1 || s->L < 1) return ROPESLR_ERR_SHAPE;
+  if (!linear_pe_eligible(s, t)) return ROPESLR_ERR_SHAPE;
+  if (static_cast<int64_t>(t->grid_t) * t->grid_h * t->grid_w != s->L) return ROPESLR_ERR_SHAPE;
+  if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  if (!aligned16(q_lin) || !aligned16(k_lin) || !aligned16(v_lin) || !aligned16(tables) || !aligned32(y_lr) ||
+      !aligned16(t->x) || t->x_row_stride % 8 || (o_lr && !aligned16(o_lr)) || (state && !aligned16(state)))
+    return ROPESLR_ERR_ALIGN;
+  if (!ws || ws_bytes < ropeslr_linear_pe_workspace_bytes(s, t)) return ROPESLR_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t BH = s->B * s->H;
+  const int nr = lnu::nrows_of(t);
+  const int ntiles = static_cast<int>(ceil_div(s->L, lnu::M));
+  const int nch = lnu::chunks_per_head(BH, ntiles);
+  const int tpc = static_cast<int>(ceil_div(ntiles, nch));
+  float* partial = static_cast<float*>(ws);
+  uint8_t* bimg = static_cast<uint8_t*>(ws) + lnu::up256(static_cast<size_t>(BH) * nch * lnu::D * lnu::NPART * 4);
+  const uint8_t* tab = static_cast<const uint8_t*>(tables);
+  const float* G = reinterpret_cast<const float*>(tab + lnu::up256(static_cast<size_t>(s->H) * 3 * nr * lnu::TAB_PITCH));
+  lnu::Grid3 g{t->grid_t, t->grid_h, t->grid_w};
+
+  CUtensorMap mq, mk, mv;
+  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mk, k_lin, BH, s->L) ||
+      !lnu::make_map(&mv, v_lin, BH, s->L))
+    return ROPESLR_ERR_LAUNCH;
+  // state
+  lnu::StateArgs sa{};
+  sa.L = s->L;
+  sa.H = static_cast<int>(s->H);
+  sa.g = g;
+  sa.use_pe = t->use_pe;
+  sa.nrows = nr;
+  sa.ntiles = ntiles;
+  sa.tiles_per_cta = tpc;
+  sa.nchunks = nch;
+  sa.tables = tab;
+  sa.partial = partial;
+  const int ssm = lnu::StateLay::bytes(nr);
+  if (cudaFuncSetAttribute(lnu::linear_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm) != cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, sa);
+  if (int e = launch_status()) return e;
+  lnu::linear_reduce_image_kernel<<<static_cast<unsigned>(BH), 256, 0, st>>>(partial, nch, bimg, state);
+  if (int e = launch_status()) return e;
+  // apply
+  lnu::ApplyArgs aa{};
+  aa.L = s->L;
+  aa.H = static_cast<int>(s->H);
+  aa.g = g;
+  aa.use_pe = t->use_pe;
+  aa.nrows = nr;
+  aa.ntiles = ntiles;
+  aa.tiles_per_cta = tpc;
+  aa.tables = tab;
+  aa.bimg = bimg;
+  aa.rms_lr = rms_lowrank;
+  aa.eps = eps;
+  aa.y_lr = static_cast<__nv_bfloat16*>(y_lr);
+  aa.o_lr = o_lr;
+  const int asm_ = lnu::ApplyLay::bytes(nr);
+  if (cudaFuncSetAttribute(lnu::linear_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_) != cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  lnu::linear_apply_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kApplyThreads, asm_, st>>>(mq, aa);
+  if (int e = launch_status()) return e;
+  // gate
+  if (g_logit != nullptr) {
+    const int64_t BL = s->B * s->L;
+    lnu::linear_gate_kernel<<<static_cast<unsigned>(ceil_div(BL, 8)), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(t->x), t->x_row_stride, t->w_g + t->head_offset * s->d, s->H * s->d, BL,
+        s->L, g, t->use_pe ? G : nullptr, g_logit);
+    if (int e = launch_status()) return e;
+    return scan_nonfinite(g_logit, false, BL, t->nonfinite, ROPESLR_NONFINITE_X, st);
+  }
+  return ROPESLR_OK;
+}

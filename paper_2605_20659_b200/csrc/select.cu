@@ -516,19 +516,28 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
   // 310-317): scores more than kProbUnderflow below the row max have
   // probability 0 and tie (lower block index first), so they key as -inf
   uint64_t key[NPER];
-  uint64_t kmax_key = 0;  // the row max, as an ascending key
+  // the row max and min as ascending keys (~desc_key); invalid columns hold
+  // ~0 descending keys = ascending 0, which never wins the max
+  uint64_t kmax_key = 0, kmin_key = ~0ull;
 #pragma unroll
   for (int i = 0; i < NPER; ++i) {
     const int c = lane + 32 * i;
     key[i] = c < nb ? desc_key(srow[c]) : ~0ull;
-    if (c < nb) kmax_key = max(kmax_key, ~key[i]);
+    kmax_key = max(kmax_key, ~key[i]);
+    if (c < nb) kmin_key = min(kmin_key, ~key[i]);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) kmax_key = max(kmax_key, __shfl_xor_sync(0xffffffffu, kmax_key, o));
+  for (int o = 16; o > 0; o >>= 1) {
+    kmax_key = max(kmax_key, __shfl_xor_sync(0xffffffffu, kmax_key, o));
+    kmin_key = min(kmin_key, __shfl_xor_sync(0xffffffffu, kmin_key, o));
+  }
   // invert the ascending map of desc_key
-  const double row_max = __longlong_as_double(
-      static_cast<long long>((kmax_key >> 63) ? (kmax_key & ~(1ull << 63)) : ~kmax_key));
-  if (row_max > -INFINITY) {
+  auto value_of = [](uint64_t a) {
+    return __longlong_as_double(static_cast<long long>((a >> 63) ? (a & ~(1ull << 63)) : ~a));
+  };
+  const double row_max = value_of(kmax_key);
+  // only a row spanning more than the float64 exp range has underflowed probabilities
+  if (row_max > -INFINITY && value_of(kmin_key) - row_max < kProbUnderflow) {
     const uint64_t ninf_key = desc_key(-INFINITY);
 #pragma unroll
     for (int i = 0; i < NPER; ++i) {

@@ -23,6 +23,7 @@ Bad shapes, ranges and dtypes raise ``ValueError`` like the reference.
 from __future__ import annotations
 
 import math
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence, Tuple, Union
 
@@ -464,16 +465,63 @@ def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: O
                           _ptr(nonfinite))
 
 
+_TABLES: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+
+
+def linear_tables(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: Optional[PETables], use_pe: bool,
+                  lin_weights: Sequence[torch.Tensor], head_offset: int = 0, H_local: Optional[int] = None
+                  ) -> torch.Tensor:
+    """The parameter-only PE fold of the linear compensator (x_hat W = x W +
+    (alpha * PE) W as per-axis tables, include/ropeslr_b200.h
+    ropeslr_linear_tables), cached while alpha / the PE tables / the backbone
+    weights / w_g are unchanged (keyed on storage and version counters)."""
+    H = params.n_heads if H_local is None else H_local
+    d = params.d_h
+    B, L, _ = x.shape
+    tok = _token_args(x, grid, params, pe, use_pe, head_offset, H, d)
+    shp = _lib.Shape(B, H, L, d, 1, _dtype_code(x))
+    nbytes = _lib.lib().ropeslr_linear_tables_bytes(ctypes_ref(shp), ctypes_ref(tok))
+    if nbytes == 0:
+        raise ValueError("the PE-injecting linear compensator runs bf16 with d_h = 128 on grids whose "
+                         "T + H + W tables fit in shared memory; pass x_hat projections instead")
+    wq, wk, wv = (w.contiguous() for w in lin_weights)
+    for w in (wq, wk, wv):
+        if w.shape != (H, params.d_model, d) or w.dtype != torch.float32 or w.device != x.device:
+            raise ValueError(f"linear backbone weights must be float32 [{H}, {params.d_model}, {d}] on X's device")
+    deps = [params.alpha, params.w_g, wq, wk, wv] + ([pe.pe_t, pe.pe_x, pe.pe_y] if use_pe else [])
+    key = (tuple((t.data_ptr(), t._version) for t in deps), head_offset, H, grid.as_tuple(), bool(use_pe), x.device)
+    tab = _TABLES.get(key)
+    if tab is None:
+        tab = _workspace(nbytes, x.device)
+        _lib.call("ropeslr_linear_tables", ctypes_ref(shp), ctypes_ref(tok), wq.data_ptr(), wk.data_ptr(),
+                  wv.data_ptr(), tab.data_ptr(), tab.numel(), _stream(x.device))
+        _TABLES[key] = tab
+        while len(_TABLES) > 8:
+            _TABLES.popitem(last=False)
+    else:
+        _TABLES.move_to_end(key)
+    return tab
+
+
 def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams, settings: ForwardSettings,
                        pe: Optional[PETables] = None, *, head_offset: int = 0,
                        lin_proj: Optional[Sequence[torch.Tensor]] = None, want_o_lr: bool = False,
-                       H_local: Optional[int] = None, nonfinite: Optional[torch.Tensor] = None):
+                       H_local: Optional[int] = None, nonfinite: Optional[torch.Tensor] = None,
+                       lin_weights: Optional[Sequence[torch.Tensor]] = None,
+                       want_state: bool = False):
     """Low-rank (mechanism.py:225-235, 441-446) or linear (mechanism.py:350-362)
     compensator of the local heads, RMS-normalised with rms_lowrank, plus the
     gate logits over the local columns (mechanism.py:434).
 
+    Linear mode takes the backbone projections in ``lin_proj`` (q, k, v
+    [B, H, L, d]).  With ``lin_weights`` (the local heads' W_q, W_k, W_v,
+    float32 [H, D_total, d]) they are the projections of the plain X
+    (x W, no PE) and the kernels add the PE part from folded tables (the
+    tcgen05 path, bf16 with d = 128); without, they are the caller's x_hat W.
+
     Returns (y_lr [B, L, H, d] in X's dtype, o_lr [B, H, L, d] float32 or None,
-    g_logit [B, L] float32 without bias)."""
+    g_logit [B, L] float32 without bias), plus the linear state (S | z,
+    float32 [B*H, d, 144]) when ``want_state``."""
     H = params.n_heads if H_local is None else H_local
     d = params.d_h
     B, L, _ = x.shape
@@ -483,6 +531,7 @@ def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams
     y_lr = torch.empty((B, L, H, d), dtype=x.dtype, device=dev)
     o_lr = torch.empty((B, H, L, d), dtype=torch.float32, device=dev) if want_o_lr else None
     g_logit = torch.empty((B, L), dtype=torch.float32, device=dev)
+    state = None
     st = _stream(dev)
     if settings.compensator == "lowrank":
         if params.w_a.shape[0] != H or params.w_b.shape != (H, params.rank, d):
@@ -497,13 +546,24 @@ def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams
             raise ValueError("the linear compensator needs the projections (q_lin, k_lin, v_lin)")
         ql, kl, vl = (t.contiguous() for t in lin_proj)
         for t in (ql, kl, vl):
-            if t.shape != (B, H, L, d) or t.dtype != x.dtype:
-                raise ValueError("linear projections must be [B, H, L, d] in X's dtype")
-        _lib.call("ropeslr_gate_logits", ctypes_ref(shp), ctypes_ref(tok), g_logit.data_ptr(), st)
-        ws = _workspace(_lib.lib().ropeslr_linear_workspace_bytes(ctypes_ref(shp)), dev)
-        _lib.call("ropeslr_linear_branch", ctypes_ref(shp), ql.data_ptr(), kl.data_ptr(), vl.data_ptr(),
-                  params.rms_lowrank.data_ptr(), float(settings.rms_eps), y_lr.data_ptr(), _ptr(o_lr),
-                  ws.data_ptr(), ws.numel(), st)
+            if t.shape != (B, H, L, d) or t.dtype != x.dtype or t.device != dev:
+                raise ValueError("linear projections must be [B, H, L, d] in X's dtype on X's device")
+        if lin_weights is not None:
+            tab = linear_tables(x, grid, params, pe, settings.use_pe, lin_weights, head_offset, H)
+            if want_state:
+                state = torch.empty((B * H, d, 144), dtype=torch.float32, device=dev)
+            ws = _workspace(_lib.lib().ropeslr_linear_pe_workspace_bytes(ctypes_ref(shp), ctypes_ref(tok)), dev)
+            _lib.call("ropeslr_linear_branch_pe", ctypes_ref(shp), ctypes_ref(tok), ql.data_ptr(), kl.data_ptr(),
+                      vl.data_ptr(), tab.data_ptr(), params.rms_lowrank.data_ptr(), float(settings.rms_eps),
+                      y_lr.data_ptr(), _ptr(o_lr), g_logit.data_ptr(), _ptr(state), ws.data_ptr(), ws.numel(), st)
+        else:
+            _lib.call("ropeslr_gate_logits", ctypes_ref(shp), ctypes_ref(tok), g_logit.data_ptr(), st)
+            ws = _workspace(_lib.lib().ropeslr_linear_workspace_bytes(ctypes_ref(shp)), dev)
+            _lib.call("ropeslr_linear_branch", ctypes_ref(shp), ql.data_ptr(), kl.data_ptr(), vl.data_ptr(),
+                      params.rms_lowrank.data_ptr(), float(settings.rms_eps), y_lr.data_ptr(), _ptr(o_lr),
+                      ws.data_ptr(), ws.numel(), st)
+    if want_state:
+        return y_lr, o_lr, g_logit, state
     return y_lr, o_lr, g_logit
 
 
@@ -552,7 +612,8 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
             params: MechanismParams, settings: ForwardSettings, pe: Optional[PETables] = None, *,
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False,
             head_offset: int = 0, rope: Optional[RopeConfig] = None,
-            nonfinite: Optional[torch.Tensor] = None) -> Prepared:
+            nonfinite: Optional[torch.Tensor] = None,
+            lin_weights: Optional[Sequence[torch.Tensor]] = None) -> Prepared:
     """K1 (routing, mechanism.py:305-320) and K3 (compensator + partial gate
     logits, mechanism.py:429-447) for the local heads.  With ``rope`` the
     given Q/K are un-rotated: the fused RoPE + pooling pre-pass rotates them
@@ -576,7 +637,8 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     sel = select_blocks(q, k, settings.sparse, want_mask=trace, _layout=layout, pooled=pooled, nonfinite=nonfinite)
     y_lr, o_lr, g_logit = compensator_branch(x, grid, params, settings, pe, head_offset=head_offset,
-                                             lin_proj=lin_proj, want_o_lr=trace, H_local=H, nonfinite=nonfinite)
+                                             lin_proj=lin_proj, want_o_lr=trace, H_local=H, nonfinite=nonfinite,
+                                             lin_weights=lin_weights)
     return Prepared(q=q, k=k, v=v, sel=sel, y_lr=y_lr, o_lr=o_lr, g_logit=g_logit, block=block, perm=perm)
 
 
@@ -616,7 +678,7 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False, impl: str = "auto",
             head_offset: int = 0, gate_reduce: Optional[Callable[[torch.Tensor], None]] = None,
             rope: Optional[RopeConfig] = None, check_finite: bool = False,
-            out_dtype: Optional[torch.dtype] = None):
+            out_dtype: Optional[torch.dtype] = None, lin_weights: Optional[Sequence[torch.Tensor]] = None):
     """RoPeSLR forward (mechanism.py:491-512, Algorithm 1).
 
     q, k, v: post-RoPE [B, H, L, d] (bf16 or f32); x: token features
@@ -631,6 +693,11 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     values they already reduce (block means, gate logits), and the check
     costs one 4-byte read-back (a stream synchronisation).
 
+    Linear compensator: ``lin_proj`` holds the backbone projections (q, k, v);
+    with ``lin_weights`` (W_q, W_k, W_v of the local heads, float32
+    [H, D_total, d]) they are x W and the PE part is added in the kernels
+    (see compensator_branch), else they are x_hat W.
+
     ``out_dtype=torch.float32`` returns the fused output in float32 (the
     epilogue's result before the bf16 rounding of a bf16 output).
 
@@ -638,7 +705,7 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     ``trace`` (adds the float32 branch outputs, the gate and the masks)."""
     flag = torch.zeros(1, dtype=torch.int32, device=q.device) if check_finite else None
     prep = prepare(q, k, v, x, grid, params, settings, pe, lin_proj=lin_proj, trace=trace, head_offset=head_offset,
-                   rope=rope, nonfinite=flag)
+                   rope=rope, nonfinite=flag, lin_weights=lin_weights)
     if flag is not None:
         raise_nonfinite(flag)
     if gate_reduce is not None:
@@ -688,14 +755,20 @@ def forward_from_x(x: torch.Tensor, grid: GridShape, cfg: RopeConfig, backbone: 
         pe = PETables.sinusoidal(grid, backbone.d_model, cfg, device=xb.device)
     q, k, v = project_and_rotate(xb, grid, cfg, backbone, dtype)
     xd = xb.to(dtype).contiguous()
-    lin = None
+    lin, lin_w = None, None
     if settings.compensator == "linear":
-        x_hat = xb.to(torch.float64)
-        if settings.use_pe:
-            x_hat = x_hat + params.alpha.to(torch.float64)[None, None, :] * pe.dense(grid).to(torch.float64)[None]
-        lin = tuple(torch.einsum("bld,hde->bhle", x_hat, w.to(torch.float64)).to(dtype)
+        # the backbone projections are the caller-side step (like Q/K/V):
+        # on the tensor-core path x W of the stored X, and the kernels add
+        # the PE part (alpha * PE) W from folded tables; otherwise x_hat W
+        tc_path = dtype == torch.bfloat16 and backbone.d_h == 128
+        x_src = xd.to(torch.float64) if tc_path else xb.to(torch.float64)
+        if settings.use_pe and not tc_path:
+            x_src = x_src + params.alpha.to(torch.float64)[None, None, :] * pe.dense(grid).to(torch.float64)[None]
+        lin = tuple(torch.einsum("bld,hde->bhle", x_src, w.to(torch.float64)).to(dtype)
                     for w in (backbone.w_q, backbone.w_k, backbone.w_v))
-    return forward(q, k, v, xd, grid, params, settings, pe, lin_proj=lin, trace=trace, impl=impl)
+        if tc_path:
+            lin_w = tuple(w.to(torch.float32).contiguous() for w in (backbone.w_q, backbone.w_k, backbone.w_v))
+    return forward(q, k, v, xd, grid, params, settings, pe, lin_proj=lin, trace=trace, impl=impl, lin_weights=lin_w)
 
 
 def forward_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, grid: GridShape,

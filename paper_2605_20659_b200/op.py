@@ -7,7 +7,7 @@ stream, fake kernels for tracing):
 
 from __future__ import annotations
 
-from typing import List
+from typing import List, Optional
 
 import torch
 
@@ -20,18 +20,36 @@ from .rope3d import GridShape
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, pe_t: torch.Tensor,
              pe_x: torch.Tensor, pe_y: torch.Tensor, alpha: torch.Tensor, w_a: torch.Tensor, w_b: torch.Tensor,
              w_g: torch.Tensor, b_g: float, rms_sparse: torch.Tensor, rms_lowrank: torch.Tensor, grid: List[int],
-             block: int, topk: int, keep: float, use_pe: bool, eps: float) -> torch.Tensor:
+             block: int, topk: int, keep: float, use_pe: bool, eps: float, compensator: str = "lowrank",
+             q_lin: Optional[torch.Tensor] = None, k_lin: Optional[torch.Tensor] = None,
+             v_lin: Optional[torch.Tensor] = None, w_lin_q: Optional[torch.Tensor] = None,
+             w_lin_k: Optional[torch.Tensor] = None, w_lin_v: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The whole forward.  compensator "linear" takes the backbone projections
+    q_lin/k_lin/v_lin [B, H, L, d]: of the plain X when w_lin_q/k/v (float32
+    [H, D, d]) are given (the PE part is added in the kernels), else of x_hat."""
     params = MechanismParams(w_a=w_a.contiguous(), w_b=w_b.contiguous(), alpha=alpha.contiguous(),
                              w_g=w_g.contiguous(), b_g=b_g, rms_sparse=rms_sparse.contiguous(),
                              rms_lowrank=rms_lowrank.contiguous())
-    st = ForwardSettings(SparseSettings(block=block, keep=keep, topk=topk), use_pe=use_pe, rms_eps=eps)
+    st = ForwardSettings(SparseSettings(block=block, keep=keep, topk=topk), compensator=compensator, use_pe=use_pe,
+                         rms_eps=eps)
     pe = PETables(pe_t.contiguous(), pe_x.contiguous(), pe_y.contiguous())
-    return forward(q, k, v, x, GridShape(*grid), params, st, pe)
+    lin = None
+    lin_w = None
+    if compensator == "linear":
+        if q_lin is None or k_lin is None or v_lin is None:
+            raise ValueError("the linear compensator needs q_lin, k_lin and v_lin")
+        lin = (q_lin, k_lin, v_lin)
+        if w_lin_q is not None:
+            if w_lin_k is None or w_lin_v is None:
+                raise ValueError("w_lin_q, w_lin_k and w_lin_v go together")
+            lin_w = (w_lin_q, w_lin_k, w_lin_v)
+    return forward(q, k, v, x, GridShape(*grid), params, st, pe, lin_proj=lin, lin_weights=lin_w)
 
 
 @attn_fwd.register_fake
 def _(q, k, v, x, pe_t, pe_x, pe_y, alpha, w_a, w_b, w_g, b_g, rms_sparse, rms_lowrank, grid, block, topk, keep,
-      use_pe, eps):
+      use_pe, eps, compensator="lowrank", q_lin=None, k_lin=None, v_lin=None, w_lin_q=None, w_lin_k=None,
+      w_lin_v=None):
     B, H, L, d = q.shape
     return q.new_empty((B, L, H * d))
 

@@ -396,3 +396,22 @@ def test_float32_output(name, impl):
     assert o32.dtype == torch.float32 and o32.shape == o16.shape
     assert torch.equal(o32.to(torch.bfloat16), o16)
     G.assert_close(o32[0].cpu().numpy(), g["ref_output"], "bf16", f"{name} float32 output")
+
+
+def test_golden_linear_pe_in_kernel():
+    """The reference's linear compensator (bf16_d128_linear, mechanism.py:350-362
+    on x_hat = x + alpha PE) through the PE-injecting tensor-core path: the
+    caller passes x W and the backbone weights, the kernels add (alpha PE) W."""
+    import paper_2605_20659_b200 as P
+
+    g = golden_io.load("bf16_d128_linear")
+    q, k, v, x, params, pe, st, grid, _ = G.golden_to_device(g)
+    W = [torch.from_numpy(np.ascontiguousarray(g[n])).float().cuda() for n in
+         ("ref_w_lin_q", "ref_w_lin_k", "ref_w_lin_v")]
+    lin = tuple(torch.einsum("bld,hde->bhle", x.double(), w.double()).to(torch.bfloat16).contiguous() for w in W)
+    tr = P.forward(q, k, v, x, grid, params, st, pe, lin_proj=lin, lin_weights=W, trace=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(tr.selected[0].cpu().numpy(), g["ref_selected"])
+    G.assert_close(tr.o_lowrank[0].cpu().numpy(), g["ref_o_lowrank"], "bf16", "linear pe o_lowrank")
+    G.assert_close(tr.g[0].cpu().numpy(), g["ref_g"], "bf16", "linear pe gate")
+    G.assert_close_bf16_store(tr.output[0].float().cpu().numpy(), g["ref_output"], "linear pe output")
