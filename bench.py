@@ -617,6 +617,74 @@ def run_sweep(args, local_rank):
                 "dtype": "bf16", "data": "synthetic (seeded N(0,1), 3D RoPE)"}), flush=True)
 
 
+def run_linear(args, local_rank):
+    """Linear-compensator mode (mechanism.py:350-362, the north star's "K^T.V
+    state reduction followed by a Q.state contraction") at the config-3
+    shape: the branch alone (state + apply on tcgen05 with the PE added in
+    the kernels, plus the gate; its algorithmic bytes are q_lin, k_lin,
+    v_lin and X read once and y_lr written once) and the whole forward step
+    in linear mode.  The backbone projections x W are the caller's
+    (computed once before timing, like Q/K/V)."""
+    import torch
+
+    import paper_2605_20659_b200 as P
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS["cfg3"]
+    H, d = cfg["H"], cfg["d"]
+    q, k, v, x, params, pe, grid = make_inputs(cfg, 0, H, dev)
+    L, D = grid.size, H * d
+    gen = torch.Generator(device=dev).manual_seed(11)
+    W = [torch.randn((H, D, d), generator=gen, device=dev) / math.sqrt(D) for _ in range(3)]
+    lin = tuple(torch.einsum("bld,hde->bhle", x, w.to(torch.bfloat16)).contiguous() for w in W)
+    st = P.ForwardSettings(P.SparseSettings.for_sparsity(cfg["block"], L, cfg["sparsity"]), compensator="linear")
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, n):
+        for _ in range(max(2, args.warmup)):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clocks:
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n, clocks.summary()
+
+    branch_ms, _ = timed(lambda: P.compensator_branch(x, grid, params, st, pe, lin_proj=lin, lin_weights=W),
+                         max(5, args.steps))
+    out = torch.empty((1, L, H, d), dtype=torch.bfloat16, device=dev)
+
+    def step():
+        prep = P.prepare(q, k, v, x, grid, params, st, pe, lin_proj=lin, lin_weights=W)
+        P.attend(prep, params, st, out=out)
+        return prep
+
+    step_ms, clocks = timed(step, args.steps)
+    prep = step()
+    torch.cuda.synchronize()
+    att = int(prep.sel.attended.sum())
+    peaks = load_peaks()
+    bytes_branch = 5 * x.numel() * x.element_size()  # q_lin, k_lin, v_lin, X in; y_lr out
+    gbs = bytes_branch / (branch_ms * 1e-3) / 1e9
+    flops = P.flops.total_ropeslr(att, 1, H, L, d, cfg["r"]) - P.flops.c_lowrank(1, H, L, d, cfg["r"]) \
+        + P.flops.c_linear_branch(1, H, L, d)
+    print(json.dumps({
+        "metric": "RoPeSLR attn fwd, linear compensator (config-3 shape), ms", "value": step_ms, "unit": "ms",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) Q/K/V with 3D RoPE, X, PE tables, backbone weights; random-init params)",
+        "config": {"workload": cfg["name"] + "_linear", "compensator": "linear", "topk": st.sparse.topk},
+        "tflops_effective": flops / (step_ms * 1e-3) / 1e12,
+        "linear_branch": {"ms": branch_ms, "bytes": bytes_branch, "GB_per_s": gbs, "frac_of_hbm": gbs / peaks["hbm_gbs"],
+                          "unit": "read q_lin, k_lin, v_lin, X once; write y_lr once",
+                          "kernels": "linear_state (tcgen05) + reduce + linear_apply (tcgen05) + gate"},
+        "clocks": clocks}), flush=True)
+
+
 def run_train(args, local_rank):
     """SURVEY 8f next #3 measured: one Stage-I training step (training.py:
     the compensator / gate / RMSNorm / PE forward + backward against the
@@ -707,7 +775,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep", "train"], default="cfg3")
+    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep", "train", "linear"], default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rope-pass", action="store_true", help="skip timing the fused RoPE + pooling pre-pass")
@@ -748,6 +816,8 @@ def main():
             run_sweep(args, local_rank)
         elif args.config == "train":
             run_train(args, local_rank)
+        elif args.config == "linear":
+            run_linear(args, local_rank)
         else:
             run_ours(args, cfg, rank, world, local_rank)
     finally:
