@@ -77,13 +77,16 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
   return u;
 }
 
-// In place on row r of a tile: v + T[rt] + T[rx] + T[ry] (tables optional),
-// then phi when PHI; rows of tokens beyond L become zero.
-template <bool PHI>
-__device__ __forceinline__ void transform_row(uint8_t* tile, int r, bool valid, const uint8_t* tab, int rt, int rx,
-                                              int ry) {
-#pragma unroll 4
-  for (int c = 0; c < 16; ++c) {
+// In place on chunks [c0, c0 + NC) of row r of a tile: v + T[rt] + T[rx] +
+// T[ry] (tables optional), then phi when PHI; rows of tokens beyond L become
+// zero.  Several threads share a row (each its own chunk range), so the
+// CUDA-core work of a tile spreads over many warps.
+template <bool PHI, int NC>
+__device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt,
+                                              int rx, int ry) {
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int c = c0 + cc;
     uint4* p = tile_chunk(tile, r, c);
     if (!valid) {
       *p = make_uint4(0, 0, 0, 0);
@@ -140,7 +143,9 @@ struct StateLay {
   __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 8 * 8 + 16; }
 };
 
-constexpr int kStateThreads = 192;  // warps 0-3 transform, 4 TMA, 5 MMA + TMEM
+constexpr int kStateXf = 512;                 // transform threads: 4 per token row, 4 chunks of K and of V each
+constexpr int kStateThreads = kStateXf + 64;  // + warp 16 TMA, warp 17 MMA + TMEM
+constexpr int kStateTma = kStateXf / 32, kStateMma = kStateTma + 1;
 
 __global__ void __launch_bounds__(kStateThreads, 1)
     linear_state_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&ready[i], 128);
+      mbar_init(&ready[i], kStateXf);
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     reinterpret_cast<uint4*>(sOnes)[i] = row == 0 ? make_uint4(one2, one2, one2, one2) : make_uint4(0, 0, 0, 0);
   }
   fence_proxy_async_smem();
-  if (warp == 5) {
+  if (warp == kStateMma) {
     tmem_alloc(tmem_slot, 256);
     tmem_relinquish();
   }
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == kStateTma) {
     if (elect_one()) {
       if (a.use_pe) {
         mbar_arrive_expect_tx(tabf, 2 * tab_bytes);
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
         tma_load_3d_hint(v + HALF, &tmV, &full[s], 64, row, bh, pol);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kStateMma) {
     constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
     constexpr uint32_t idesc_z = idesc_bf16_f32(M, 16, true, false);
     const bool leader = elect_one();
@@ -240,8 +245,8 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       __syncwarp();
     }
   } else {
-    // transform warps: one token row per thread
-    const int r = threadIdx.x;
+    // transform warps: 4 threads per token row, 4 of its 16 chunks each
+    const int r = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 4;
     const uint8_t* tk = nullptr;
     const uint8_t* tv = nullptr;
     if (a.use_pe) {
@@ -256,11 +261,14 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true>(sK + s * TILE, r, valid, tk, rt, rx, ry);
-      transform_row<false>(sV + s * TILE, r, valid, tv, rt, rx, ry);
+      transform_row<true, 4>(sK + s * TILE, r, c0, valid, tk, rt, rx, ry);
+      transform_row<false, 4>(sV + s * TILE, r, c0, valid, tv, rt, rx, ry);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
     }
+  }
+  if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out
+    const int r = threadIdx.x;
     // the chunk's partial [S | z]: TMEM lane r = row r (d_k) of S
     float* dst = a.partial + ((static_cast<int64_t>(bh) * a.nchunks + chunk) * D + r) * NPART;
     if (n > 0) {
@@ -290,7 +298,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kStateMma) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
   }
@@ -307,8 +315,10 @@ __global__ void __launch_bounds__(256) linear_reduce_image_kernel(const float* _
   const int bh = blockIdx.x;
   const float* src = partial + static_cast<int64_t>(bh) * nchunks * D * NPART;
   uint8_t* img = bimg + static_cast<int64_t>(bh) * 2 * BIMG;
-  for (int e = threadIdx.x; e < NB * D; e += blockDim.x) {
-    const int n = e / D, k = e % D;
+  // blockIdx.y: 16 of the 144 image rows; thread: (row, k) with k fastest so
+  // the partial reads (k-major rows of NPART) are spread, the image writes local
+  for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) {
+    const int n = blockIdx.y * 16 + e / D, k = e % D;
     double acc = 0.0;
     if (n <= 128)
       for (int c = 0; c < nchunks; ++c) acc += src[(static_cast<int64_t>(c) * D + k) * NPART + n];
@@ -338,17 +348,21 @@ struct ApplyArgs {
   float* o_lr;            // [B, H, L, d] nullable
 };
 
-// smem: Q ring (2 x 32 KiB) | B image hi | lo (2 x 36 KiB) | T_q | rms | barriers
+// smem: Q ring (2 x 32 KiB) | B image hi | lo (2 x 36 KiB) | T_q | rms | row sums | barriers
 struct ApplyLay {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_B = OFF_Q + 2 * TILE;
   static constexpr int OFF_TAB = OFF_B + 2 * BIMG;
   __host__ __device__ static int off_rms(int nrows) { return OFF_TAB + ((nrows * TAB_PITCH + 127) / 128) * 128; }
-  __host__ __device__ static int off_bar(int nrows) { return off_rms(nrows) + D * 4; }
+  __host__ __device__ static int off_xs(int nrows) { return off_rms(nrows) + D * 4; }
+  __host__ __device__ static int off_bar(int nrows) { return off_xs(nrows) + 2 * M * 4; }
   __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 12 * 8 + 16; }
 };
 
-constexpr int kApplyThreads = 320;  // warps 0-3 transform, 4-7 epilogue, 8 TMA, 9 MMA + TMEM
+constexpr int kApplyXf = 256;   // transform threads: 2 per token row, 8 chunks each (warps 0-7)
+constexpr int kApplyEpi = 256;  // epilogue threads (warps 8-15): lane quarter warp % 4, column half (warp - 8) / 4
+constexpr int kApplyTma = (kApplyXf + kApplyEpi) / 32, kApplyMma = kApplyTma + 1;
+constexpr int kApplyThreads = kApplyXf + kApplyEpi + 64;
 
 __global__ void __launch_bounds__(kApplyThreads, 1)
     linear_apply_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ ApplyArgs a) {
@@ -363,6 +377,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   uint8_t* sB = smem + ApplyLay::OFF_B;
   uint8_t* sTab = smem + ApplyLay::OFF_TAB;
   float* sRms = reinterpret_cast<float*>(smem + ApplyLay::off_rms(a.nrows));
+  float(*xs)[M] = reinterpret_cast<float(*)[M]>(smem + ApplyLay::off_xs(a.nrows));  // per-half row sums of squares
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ApplyLay::off_bar(a.nrows));
   uint64_t* full = bars;        // [2]
   uint64_t* ready = bars + 2;   // [2]
@@ -376,16 +391,16 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&ready[i], 128);
+      mbar_init(&ready[i], kApplyXf);
       mbar_init(&empty[i], 1);
       mbar_init(&accf[i], 1);
-      mbar_init(&acce[i], 128);
+      mbar_init(&acce[i], kApplyEpi);
     }
     mbar_init(init, 1);
     fence_mbar_init();
   }
   for (int i = threadIdx.x; i < D; i += blockDim.x) sRms[i] = a.rms_lr[i];
-  if (warp == 9) {
+  if (warp == kApplyMma) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
   }
@@ -394,7 +409,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == kApplyTma) {
     if (elect_one()) {
       const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * tab_bytes;
       mbar_arrive_expect_tx(init, 2 * BIMG + (a.use_pe ? tab_bytes : 0));
@@ -410,7 +425,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
         tma_load_3d_hint(sQ + s * TILE + HALF, &tmQ, &full[s], 64, row, bh, pol);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kApplyMma) {
     constexpr uint32_t idesc = idesc_bf16_f32(M, NB, false, false);
     const bool leader = elect_one();
     mbar_wait(init, 0);
@@ -436,8 +451,9 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       }
       __syncwarp();
     }
-  } else if (warp < 4) {
-    const int r = threadIdx.x;
+  } else if (warp < kApplyXf / 32) {
+    // transform: 2 threads per token row, 8 of its 16 chunks each
+    const int r = threadIdx.x >> 1, c0 = (threadIdx.x & 1) * 8;
     const uint8_t* tq = nullptr;
     if (a.use_pe) {
       mbar_wait(init, 0);
@@ -450,13 +466,13 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true>(sQ + s * TILE, r, valid, tq, rt, rx, ry);
+      transform_row<true, 8>(sQ + s * TILE, r, c0, valid, tq, rt, rx, ry);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
     }
   } else {
-    // epilogue warps 4-7: TMEM lane quarter warp % 4, token row r
-    const int q4 = warp - 4;
+    // epilogue: row r = TMEM lane (warp % 4) * 32 + lane; columns [64 hf, 64 hf + 64)
+    const int q4 = warp & 3, hf = (warp - kApplyXf / 32) >> 2;
     const int r = q4 * 32 + (threadIdx.x & 31);
     for (int i = 0; i < n; ++i) {
       const int ab = i & 1;
@@ -465,39 +481,45 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       const uint32_t base = tmem + ab * 256 + (static_cast<uint32_t>(q4 * 32) << 16);
       uint32_t den_u[16];
       tmem_ld16(base + 128, den_u);
-      tmem_wait_ld();
-      const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
-      float o[D];
-      float ss = 0.f;
+      float o[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld32(base + c * 32, v);
+        tmem_ld32(base + hf * 64 + c * 32, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          o[c * 32 + j] = __uint_as_float(v[j]) * inv_den;
-          ss = fmaf(o[c * 32 + j], o[c * 32 + j], ss);
-        }
+        for (int j = 0; j < 32; ++j) o[c * 32 + j] = __uint_as_float(v[j]);
       }
       tc_fence_before();
       mbar_arrive(&acce[ab]);
+      const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        o[j] *= inv_den;
+        ss = fmaf(o[j], o[j], ss);
+      }
+      xs[hf][r] = ss;
+      asm volatile("bar.sync 1, %0;" ::"n"(kApplyEpi) : "memory");
+      ss = xs[0][r] + xs[1][r];
+      asm volatile("bar.sync 1, %0;" ::"n"(kApplyEpi) : "memory");  // xs is reused by the next tile
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
       if (l >= a.L) continue;
       const float inv = rsqrtf(ss / static_cast<float>(D) + a.eps);
+      const int col0 = hf * 64;
       if (a.o_lr != nullptr) {
-        float* dst = a.o_lr + (static_cast<int64_t>(bh) * a.L + l) * D;
+        float* dst = a.o_lr + (static_cast<int64_t>(bh) * a.L + l) * D + col0;
 #pragma unroll
-        for (int j = 0; j < D; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+        for (int j = 0; j < 64; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
       }
-      __nv_bfloat16* dst = a.y_lr + ((static_cast<int64_t>(b) * a.L + l) * a.H + h) * D;
+      __nv_bfloat16* dst = a.y_lr + ((static_cast<int64_t>(b) * a.L + l) * a.H + h) * D + col0;
 #pragma unroll
-      for (int j = 0; j < D; j += 16) {
+      for (int j = 0; j < 64; j += 16) {
         uint32_t u[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(o[j + 2 * e] * inv * sRms[j + 2 * e],
-                                                    o[j + 2 * e + 1] * inv * sRms[j + 2 * e + 1]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(o[j + 2 * e] * inv * sRms[col0 + j + 2 * e],
+                                                    o[j + 2 * e + 1] * inv * sRms[col0 + j + 2 * e + 1]);
           u[e] = *reinterpret_cast<uint32_t*>(&h2);
         }
         asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + j), "r"(u[0]),
@@ -508,7 +530,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kApplyMma) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -654,9 +676,10 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t BH, int64_t L) {
 
 static int nrows_of(const ropeslr_token_args* t) { return t->grid_t + t->grid_h + t->grid_w; }
 
-// CTAs per head: about two waves of the persistent-size grid over all heads.
+// CTAs per head: one wave over all heads (one CTA per SM; BH * chunks <= SMs
+// when BH <= SMs, so no tail wave).
 static int chunks_per_head(int64_t BH, int ntiles) {
-  int64_t c = (2 * static_cast<int64_t>(num_sms()) + BH - 1) / BH;
+  int64_t c = num_sms() / BH;
   if (c > ntiles) c = ntiles;
   return static_cast<int>(c < 1 ? 1 : c);
 }
@@ -758,7 +781,8 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
     return ROPESLR_ERR_LAUNCH;
   lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, sa);
   if (int e = launch_status()) return e;
-  lnu::linear_reduce_image_kernel<<<static_cast<unsigned>(BH), 256, 0, st>>>(partial, nch, bimg, state);
+  lnu::linear_reduce_image_kernel<<<dim3(static_cast<unsigned>(BH), lnu::NB / 16), 256, 0, st>>>(partial, nch, bimg,
+                                                                                                state);
   if (int e = launch_status()) return e;
   // apply
   lnu::ApplyArgs aa{};

@@ -498,53 +498,11 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
 // the k-th best key T; rows keep every key < T and, on exact ties at T, the
 // lowest block indices (the stable order of mechanism.py:317).  The keys
 // stay in registers; each warp owns a 256-bin histogram in shared memory.
+// The radix select and the outputs of one row, from its keys (registers).
 template <int NPER>
-__global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __restrict__ scores, int nb,
-                                                               int64_t rows, int64_t L, int block, int topk, int kmax,
-                                                               int32_t* __restrict__ idx, int32_t* __restrict__ cnt,
-                                                               uint8_t* __restrict__ mask,
-                                                               unsigned long long* __restrict__ attended) {
-  __shared__ int hist_all[8][256];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-  if (row >= rows) return;
-  int* hist = hist_all[warp];
+__device__ __forceinline__ void topk_row(uint64_t (&key)[NPER], int* hist, int lane, int nb, int64_t row, int64_t L, int block, int topk, int kmax, int32_t* __restrict__ idx, int32_t* __restrict__ cnt, uint8_t* __restrict__ mask, unsigned long long* __restrict__ attended) {
   const int64_t bh = row / nb;
   const int qb = static_cast<int>(row % nb);
-  const double* srow = scores + row * nb;
-  // the reference orders blocks by their softmax probability (mechanism.py:
-  // 310-317): scores more than kProbUnderflow below the row max have
-  // probability 0 and tie (lower block index first), so they key as -inf
-  uint64_t key[NPER];
-  // the row max and min as ascending keys (~desc_key); invalid columns hold
-  // ~0 descending keys = ascending 0, which never wins the max
-  uint64_t kmax_key = 0, kmin_key = ~0ull;
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const int c = lane + 32 * i;
-    key[i] = c < nb ? desc_key(srow[c]) : ~0ull;
-    kmax_key = max(kmax_key, ~key[i]);
-    if (c < nb) kmin_key = min(kmin_key, ~key[i]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    kmax_key = max(kmax_key, __shfl_xor_sync(0xffffffffu, kmax_key, o));
-    kmin_key = min(kmin_key, __shfl_xor_sync(0xffffffffu, kmin_key, o));
-  }
-  // invert the ascending map of desc_key
-  auto value_of = [](uint64_t a) {
-    return __longlong_as_double(static_cast<long long>((a >> 63) ? (a & ~(1ull << 63)) : ~a));
-  };
-  const double row_max = value_of(kmax_key);
-  // only a row spanning more than the float64 exp range has underflowed probabilities
-  if (row_max > -INFINITY && value_of(kmin_key) - row_max < kProbUnderflow) {
-    const uint64_t ninf_key = desc_key(-INFINITY);
-#pragma unroll
-    for (int i = 0; i < NPER; ++i) {
-      const int c = lane + 32 * i;
-      if (c < nb && srow[c] - row_max < kProbUnderflow) key[i] = ninf_key;
-    }
-  }
   int need = topk < nb ? topk : nb;
   uint64_t prefix = 0, pmask = 0;
   bool exact = false;  // the remaining bucket is taken whole
@@ -641,6 +599,66 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
     cnt[row] = carry;
     atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
   }
+}
+
+// A row spanning more than the float64 exp range: keys of columns whose block
+// probability underflows (score more than kProbUnderflow below the row max)
+// become the key of -inf, so they tie and go by block index.  Out of line:
+// such rows are rare, and the common path keeps its registers.
+template <int NPER>
+__device__ __noinline__ void topk_row_clamped(const double* srow, double row_max, int* hist, int lane, int nb, int64_t row, int64_t L, int block, int topk, int kmax, int32_t* __restrict__ idx, int32_t* __restrict__ cnt, uint8_t* __restrict__ mask, unsigned long long* __restrict__ attended) {
+  uint64_t key[NPER];
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    const double v = c < nb ? srow[c] : 0.0;
+    key[i] = c < nb ? desc_key(v - row_max < kProbUnderflow ? -INFINITY : v) : ~0ull;
+  }
+  topk_row<NPER>(key, hist, lane, nb, row, L, block, topk, kmax, idx, cnt, mask, attended);
+}
+
+template <int NPER>
+__global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __restrict__ scores, int nb,
+                                                               int64_t rows, int64_t L, int block, int topk, int kmax,
+                                                               int32_t* __restrict__ idx, int32_t* __restrict__ cnt,
+                                                               uint8_t* __restrict__ mask,
+                                                               unsigned long long* __restrict__ attended) {
+  __shared__ int hist_all[8][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (row >= rows) return;
+  int* hist = hist_all[warp];
+  const double* srow = scores + row * nb;
+  // the reference orders blocks by their softmax probability (mechanism.py:
+  // 310-317): scores more than kProbUnderflow below the row max have
+  // probability 0 and tie (lower block index first), so they key as -inf
+  uint64_t key[NPER];
+  // the row max and min as ascending keys (~desc_key); invalid columns hold
+  // ~0 descending keys = ascending 0, which never wins the max
+  uint64_t kmax_key = 0, kmin_key = ~0ull;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    key[i] = c < nb ? desc_key(srow[c]) : ~0ull;
+    kmax_key = max(kmax_key, ~key[i]);
+    if (c < nb) kmin_key = min(kmin_key, ~key[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmax_key = max(kmax_key, __shfl_xor_sync(0xffffffffu, kmax_key, o));
+    kmin_key = min(kmin_key, __shfl_xor_sync(0xffffffffu, kmin_key, o));
+  }
+  // invert the ascending map of desc_key
+  auto value_of = [](uint64_t a) {
+    return __longlong_as_double(static_cast<long long>((a >> 63) ? (a & ~(1ull << 63)) : ~a));
+  };
+  const double row_max = value_of(kmax_key);
+  // only a row spanning more than the float64 exp range has underflowed probabilities
+  if (row_max > -INFINITY && value_of(kmin_key) - row_max < kProbUnderflow) {
+    topk_row_clamped<NPER>(srow, row_max, hist, lane, nb, row, L, block, topk, kmax, idx, cnt, mask, attended);
+    return;
+  }
+  topk_row<NPER>(key, hist, lane, nb, row, L, block, topk, kmax, idx, cnt, mask, attended);
 }
 
 }  // namespace ropeslr
