@@ -15,9 +15,10 @@
 //
 //   state   (one CTA per (head, token chunk))  TMA K, V tiles -> k + T_k, phi,
 //           v + T_v in place in shared memory -> tcgen05 S += phi(K)^T V
-//           (M = d, N = d, K = 128 tokens, both operands MN-major) and
-//           z += phi(K)^T 1 (N = 16) into TMEM; the chunk's [d, d | z]
-//           partial goes to the workspace;
+//           (M = d, N = d, K = 128 tokens, both operands MN-major) into
+//           TMEM, z = sum phi(k) in registers (fixed-order reduction over
+//           the token slots at the end); the chunk's [d, d | z] partial
+//           goes to the workspace;
 //   reduce  partials summed in fixed chunk order (float64), written as the
 //           apply GEMM's B operand image [S | z] (K-major, 128B-swizzled),
 //           split into bf16 hi + lo (~16 mantissa bits);
@@ -49,7 +50,6 @@ constexpr int NB = 144;                 // apply GEMM N: 128 numerators + the de
 constexpr int BHALF = NB * 128;         // 18 KiB: one 64-wide K half of the B image
 constexpr int BIMG = 2 * BHALF;         // 36 KiB: the hi (or lo) image
 constexpr int NPART = NB;               // columns of a state partial: S row (128) | z | pad
-constexpr int ONES_BYTES = 16 * 128 * 2;  // K-major [16 rows][128 tokens] bf16: row 0 ones
 constexpr float kFloor = 1e-8f;         // mechanism.py:347
 
 __device__ __forceinline__ float elu1(float v) { return v > 0.f ? v + 1.f : __expf(v); }
@@ -81,9 +81,9 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 // T[ry] (tables optional), then phi when PHI; rows of tokens beyond L become
 // zero.  Several threads share a row (each its own chunk range), so the
 // CUDA-core work of a tile spreads over many warps.
-template <bool PHI, int NC>
+template <bool PHI, int NC, bool ACC = false>
 __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt,
-                                              int rx, int ry) {
+                                              int rx, int ry, float (*acc)[NC * 8] = nullptr) {
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) {
     const int c = c0 + cc;
@@ -105,6 +105,10 @@ __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool
     if (PHI) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) f[i] = elu1(f[i]);
+    }
+    if (ACC) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) (*acc)[cc * 8 + i] += f[i];
     }
     *p = f32_to_bf16x8(f);
   }
@@ -133,12 +137,11 @@ struct StateArgs {
   float* partial;       // [BH][nchunks][128][NPART]
 };
 
-// smem: K ring (2 x 32 KiB) | V ring (2 x 32 KiB) | ones (4 KiB) | T_k | T_v | barriers
+// smem: K ring (2 x 32 KiB) | V ring (2 x 32 KiB) | T_k | T_v | barriers
 struct StateLay {
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + 2 * TILE;
-  static constexpr int OFF_ONES = OFF_V + 2 * TILE;
-  static constexpr int OFF_TAB = OFF_ONES + ONES_BYTES;
+  static constexpr int OFF_TAB = OFF_V + 2 * TILE;
   __host__ __device__ static int off_bar(int nrows) { return OFF_TAB + ((2 * nrows * TAB_PITCH + 127) / 128) * 128; }
   __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 8 * 8 + 16; }
 };
@@ -159,7 +162,6 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   const int n = max(0, t1 - t0);
   uint8_t* sK = smem + StateLay::OFF_K;
   uint8_t* sV = smem + StateLay::OFF_V;
-  uint8_t* sOnes = smem + StateLay::OFF_ONES;
   uint8_t* sTab = smem + StateLay::OFF_TAB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(a.nrows));
   uint64_t* full = bars;       // [2] TMA -> transform
@@ -181,14 +183,6 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     mbar_init(tabf, 1);
     fence_mbar_init();
   }
-  // the constant B operand of z: K-major [16 rows][128 tokens], row 0 ones;
-  // every row is constant, so the 128B swizzle leaves it as is
-  for (int i = threadIdx.x; i < ONES_BYTES / 16; i += blockDim.x) {
-    const int row = (i * 16 % 2048) / 128;  // two 2 KiB K-halves of 16 rows x 128 B
-    const uint32_t one2 = 0x3F803F80u;
-    reinterpret_cast<uint4*>(sOnes)[i] = row == 0 ? make_uint4(one2, one2, one2, one2) : make_uint4(0, 0, 0, 0);
-  }
-  fence_proxy_async_smem();
   if (warp == kStateMma) {
     tmem_alloc(tmem_slot, 256);
     tmem_relinquish();
@@ -221,7 +215,6 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     }
   } else if (warp == kStateMma) {
     constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
-    constexpr uint32_t idesc_z = idesc_bf16_f32(M, 16, true, false);
     const bool leader = elect_one();
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
@@ -230,22 +223,18 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       if (leader) {
         const uint64_t dA = desc_sw128(smem_u32(sK + s * TILE), HALF, 1024);
         const uint64_t dB = desc_sw128(smem_u32(sV + s * TILE), HALF, 1024);
-        const uint64_t dO = desc_sw128(smem_u32(sOnes), 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < M / 16; ++kk) {
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          const uint64_t da = dA + static_cast<uint64_t>((kk * 2048) >> 4);
-          mma_bf16_ss(tmem, da, dB + static_cast<uint64_t>((kk * 2048) >> 4), idesc_s, acc);
-          mma_bf16_ss(tmem + 128, da, dO + static_cast<uint64_t>(((kk & 3) * 32 + (kk >> 2) * 2048) >> 4), idesc_z,
-                      acc);
-        }
+        for (int kk = 0; kk < M / 16; ++kk)
+          mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
+                      idesc_s, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&empty[s]);
         if (i == n - 1) mma_commit(done);
       }
       __syncwarp();
     }
   } else {
-    // transform warps: 4 threads per token row, 4 of its 16 chunks each
+    // transform warps: 4 threads per token row, 4 of its 16 chunks each;
+    // z = sum phi(k) accumulates in registers over the CTA's tiles
     const int r = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 4;
     const uint8_t* tk = nullptr;
     const uint8_t* tv = nullptr;
@@ -254,6 +243,9 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       tk = sTab;
       tv = sTab + tab_bytes;
     }
+    float zacc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) zacc[j] = 0.f;
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
       mbar_wait(&full[s], (i >> 1) & 1);
@@ -261,18 +253,29 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true, 4>(sK + s * TILE, r, c0, valid, tk, rt, rx, ry);
+      transform_row<true, 4, true>(sK + s * TILE, r, c0, valid, tk, rt, rx, ry, &zacc);
       transform_row<false, 4>(sV + s * TILE, r, c0, valid, tv, rt, rx, ry);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
     }
+    // every MMA has read the K ring: reuse it for the z partials
+    // zbuf[thread][32] (thread = 4 r + q holds columns [32 q, 32 q + 32))
+    if (n > 0) mbar_wait(done, 0);
+    float* zbuf = reinterpret_cast<float*>(sK);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(zbuf + threadIdx.x * 32 + j) = make_float4(zacc[j], zacc[j + 1], zacc[j + 2], zacc[j + 3]);
+    asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
   }
   if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out
     const int r = threadIdx.x;
     // the chunk's partial [S | z]: TMEM lane r = row r (d_k) of S
     float* dst = a.partial + ((static_cast<int64_t>(bh) * a.nchunks + chunk) * D + r) * NPART;
+    // z[r] over the 128 token slots in fixed order
+    const float* zbuf = reinterpret_cast<const float*>(sK);
+    float zsum = 0.f;
+    for (int slot = 0; slot < M; ++slot) zsum += zbuf[(slot * 4 + (r >> 5)) * 32 + (r & 31)];
     if (n > 0) {
-      mbar_wait(done, 0);
       tc_fence_after();
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
 #pragma unroll 1
@@ -285,13 +288,9 @@ __global__ void __launch_bounds__(kStateThreads, 1)
           *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(
               __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
       }
-      uint32_t v[16];
-      tmem_ld16(lane_base + 128, v);
-      tmem_wait_ld();
+      dst[128] = zsum;
 #pragma unroll
-      for (int j = 0; j < 16; j += 4)
-        *reinterpret_cast<float4*>(dst + 128 + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
-                                                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+      for (int j = 129; j < NPART; ++j) dst[j] = 0.f;
     } else {
       for (int j = 0; j < NPART; ++j) dst[j] = 0.f;
     }
@@ -348,15 +347,16 @@ struct ApplyArgs {
   float* o_lr;            // [B, H, L, d] nullable
 };
 
-// smem: Q ring (2 x 32 KiB) | B image hi | lo (2 x 36 KiB) | T_q | rms | row sums | barriers
+// smem: Q ring (3 x 32 KiB) | B image hi | lo (2 x 36 KiB) | T_q | rms | row sums | barriers
+constexpr int QST = 3;  // Q ring depth
 struct ApplyLay {
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_B = OFF_Q + 2 * TILE;
+  static constexpr int OFF_B = OFF_Q + QST * TILE;
   static constexpr int OFF_TAB = OFF_B + 2 * BIMG;
   __host__ __device__ static int off_rms(int nrows) { return OFF_TAB + ((nrows * TAB_PITCH + 127) / 128) * 128; }
   __host__ __device__ static int off_xs(int nrows) { return off_rms(nrows) + D * 4; }
   __host__ __device__ static int off_bar(int nrows) { return off_xs(nrows) + 2 * M * 4; }
-  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 12 * 8 + 16; }
+  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + (3 * QST + 5) * 8 + 16; }
 };
 
 constexpr int kApplyXf = 256;   // transform threads: 2 per token row, 8 chunks each (warps 0-7)
@@ -379,20 +379,22 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   float* sRms = reinterpret_cast<float*>(smem + ApplyLay::off_rms(a.nrows));
   float(*xs)[M] = reinterpret_cast<float(*)[M]>(smem + ApplyLay::off_xs(a.nrows));  // per-half row sums of squares
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ApplyLay::off_bar(a.nrows));
-  uint64_t* full = bars;        // [2]
-  uint64_t* ready = bars + 2;   // [2]
-  uint64_t* empty = bars + 4;   // [2]
-  uint64_t* accf = bars + 6;    // [2] MMA -> epilogue
-  uint64_t* acce = bars + 8;    // [2] epilogue -> MMA
-  uint64_t* init = bars + 10;   // B image + table landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* full = bars;              // [QST] TMA -> transform
+  uint64_t* ready = bars + QST;       // [QST] transform -> MMA
+  uint64_t* empty = bars + 2 * QST;   // [QST] MMA -> TMA
+  uint64_t* accf = bars + 3 * QST;    // [2] MMA -> epilogue
+  uint64_t* acce = accf + 2;          // [2] epilogue -> MMA
+  uint64_t* init = acce + 2;          // B image + table landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(init + 1);
   const int tab_bytes = a.nrows * TAB_PITCH;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < QST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&ready[i], kApplyXf);
       mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&accf[i], 1);
       mbar_init(&acce[i], kApplyEpi);
     }
@@ -417,8 +419,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       if (a.use_pe) bulk_load_1d(sTab, gtab, tab_bytes, init, policy_evict_last());
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < n; ++i) {
-        const int s = i & 1;
-        if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        const int s = i % QST;
+        if (i >= QST) mbar_wait(&empty[s], ((i / QST) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], TILE);
         const int row = (t0 + i) * M;
         tma_load_3d_hint(sQ + s * TILE, &tmQ, &full[s], 0, row, bh, pol);
@@ -432,8 +434,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
     const uint64_t dBh = desc_sw128(smem_u32(sB), 16, 1024);
     const uint64_t dBl = desc_sw128(smem_u32(sB + BIMG), 16, 1024);
     for (int i = 0; i < n; ++i) {
-      const int s = i & 1, ab = i & 1;
-      mbar_wait(&ready[s], (i >> 1) & 1);
+      const int s = i % QST, ab = i & 1;
+      mbar_wait(&ready[s], (i / QST) & 1);
       if (i >= 2) mbar_wait(&acce[ab], ((i >> 1) - 1) & 1);
       tc_fence_after();
       if (leader) {
@@ -460,8 +462,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       tq = sTab;
     }
     for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
-      mbar_wait(&full[s], (i >> 1) & 1);
+      const int s = i % QST;
+      mbar_wait(&full[s], (i / QST) & 1);
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
