@@ -81,6 +81,27 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 // T[ry] (tables optional), then phi when PHI; rows of tokens beyond L become
 // zero.  Several threads share a row (each its own chunk range), so the
 // CUDA-core work of a tile spreads over many warps.
+__device__ __forceinline__ float2 bf16x2_to_f32x2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
+// phi(k) = elu(k) + 1 = exp(min(k, 0)) + max(k, 0) (mechanism.py:33-36),
+// branch-free: exp(0) = 1 supplies the +1 of the positive side.
+__device__ __forceinline__ float2 phi2(float2 k) {
+  const float2 e = __fmul2_rn(make_float2(fminf(k.x, 0.f), fminf(k.y, 0.f)),
+                              make_float2(1.4426950408889634f, 1.4426950408889634f));
+  float2 r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(e.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(e.y));
+  return __fadd2_rn(r, make_float2(fmaxf(k.x, 0.f), fmaxf(k.y, 0.f)));
+}
+
+// In place on chunks [c0, c0 + NC) of row r of a tile: v + (T[rt] + T[rx] +
+// T[ry]) (tables optional; the three table rows are summed in bf16x2, their
+// sum is small against v and is rounded once more with v to bf16 anyway),
+// then phi when PHI; rows of tokens beyond L become zero.  Several threads
+// share a row (each its own chunk range), so the CUDA-core work of a tile
+// spreads over many warps.  ACC: add the phi values to acc (z = sum phi(k)).
 template <bool PHI, int NC, bool ACC = false>
 __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt,
                                               int rx, int ry, float (*acc)[NC * 8] = nullptr) {
@@ -92,35 +113,48 @@ __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool
       *p = make_uint4(0, 0, 0, 0);
       continue;
     }
-    float f[8];
-    bf16x8_to_f32(*p, f);
+    uint4 u = *p;
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t t[4] = {0u, 0u, 0u, 0u};
     if (tab != nullptr) {
-      float a[8], b[8], e[8];
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(tab + rt * TAB_PITCH + c * 16), a);
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(tab + rx * TAB_PITCH + c * 16), b);
-      bf16x8_to_f32(*reinterpret_cast<const uint4*>(tab + ry * TAB_PITCH + c * 16), e);
+      const uint4 a = *reinterpret_cast<const uint4*>(tab + rt * TAB_PITCH + c * 16);
+      const uint4 b = *reinterpret_cast<const uint4*>(tab + rx * TAB_PITCH + c * 16);
+      const uint4 e = *reinterpret_cast<const uint4*>(tab + ry * TAB_PITCH + c * 16);
+      const uint32_t aa[4] = {a.x, a.y, a.z, a.w}, bb[4] = {b.x, b.y, b.z, b.w}, ee[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] += (a[i] + b[i]) + e[i];
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 s2 = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&aa[i]),
+                                    *reinterpret_cast<const __nv_bfloat162*>(&bb[i]));
+        s2 = __hadd2(s2, *reinterpret_cast<const __nv_bfloat162*>(&ee[i]));
+        t[i] = *reinterpret_cast<uint32_t*>(&s2);
+      }
     }
-    if (PHI) {
+    uint32_t o[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] = elu1(f[i]);
+    for (int i = 0; i < 4; ++i) {
+      float2 f = bf16x2_to_f32x2(w[i]);
+      if (tab != nullptr) f = __fadd2_rn(f, bf16x2_to_f32x2(t[i]));
+      if (PHI) f = phi2(f);
+      if (ACC) {
+        (*acc)[cc * 8 + 2 * i] += f.x;
+        (*acc)[cc * 8 + 2 * i + 1] += f.y;
+      }
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
+      o[i] = *reinterpret_cast<uint32_t*>(&h2);
     }
-    if (ACC) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) (*acc)[cc * 8 + i] += f[i];
-    }
-    *p = f32_to_bf16x8(f);
+    *p = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
 struct Grid3 {
   int T, Hg, Wg;
+  // table rows of token l: t, T + x, T + Hg + y (32-bit: L < 2^31 on this path)
   __device__ __forceinline__ void rows(int64_t l, int& rt, int& rx, int& ry) const {
-    const int64_t hw = static_cast<int64_t>(Hg) * Wg;
-    rt = static_cast<int>(l / hw);
-    rx = T + static_cast<int>((l / Wg) % Hg);
-    ry = T + Hg + static_cast<int>(l % Wg);
+    const uint32_t u = static_cast<uint32_t>(l);
+    const uint32_t row = u / static_cast<uint32_t>(Wg);
+    rt = static_cast<int>(row / static_cast<uint32_t>(Hg));
+    rx = T + static_cast<int>(row - static_cast<uint32_t>(rt) * Hg);
+    ry = T + Hg + static_cast<int>(u - row * static_cast<uint32_t>(Wg));
   }
 };
 
@@ -202,7 +236,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < n; ++i) {
         const int s = i & 1;
-        if (i >= 2) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        if (i >= 2) mbar_wait_sleep(&empty[s], ((i >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], 2 * TILE);
         const int row = (t0 + i) * M;
         uint8_t* k = sK + s * TILE;
@@ -218,7 +252,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     const bool leader = elect_one();
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
-      mbar_wait(&ready[s], (i >> 1) & 1);
+      mbar_wait_sleep(&ready[s], (i >> 1) & 1);
       tc_fence_after();
       if (leader) {
         const uint64_t dA = desc_sw128(smem_u32(sK + s * TILE), HALF, 1024);
@@ -239,7 +273,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     const uint8_t* tk = nullptr;
     const uint8_t* tv = nullptr;
     if (a.use_pe) {
-      mbar_wait(tabf, 0);
+      mbar_wait_sleep(tabf, 0);
       tk = sTab;
       tv = sTab + tab_bytes;
     }
@@ -248,7 +282,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     for (int j = 0; j < 32; ++j) zacc[j] = 0.f;
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
-      mbar_wait(&full[s], (i >> 1) & 1);
+      mbar_wait_sleep(&full[s], (i >> 1) & 1);
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
@@ -260,7 +294,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     }
     // every MMA has read the K ring: reuse it for the z partials
     // zbuf[thread][32] (thread = 4 r + q holds columns [32 q, 32 q + 32))
-    if (n > 0) mbar_wait(done, 0);
+    if (n > 0) mbar_wait_sleep(done, 0);
     float* zbuf = reinterpret_cast<float*>(sK);
 #pragma unroll
     for (int j = 0; j < 32; j += 4)
@@ -420,7 +454,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < n; ++i) {
         const int s = i % QST;
-        if (i >= QST) mbar_wait(&empty[s], ((i / QST) - 1) & 1);
+        if (i >= QST) mbar_wait_sleep(&empty[s], ((i / QST) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], TILE);
         const int row = (t0 + i) * M;
         tma_load_3d_hint(sQ + s * TILE, &tmQ, &full[s], 0, row, bh, pol);
@@ -430,13 +464,13 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   } else if (warp == kApplyMma) {
     constexpr uint32_t idesc = idesc_bf16_f32(M, NB, false, false);
     const bool leader = elect_one();
-    mbar_wait(init, 0);
+    mbar_wait_sleep(init, 0);
     const uint64_t dBh = desc_sw128(smem_u32(sB), 16, 1024);
     const uint64_t dBl = desc_sw128(smem_u32(sB + BIMG), 16, 1024);
     for (int i = 0; i < n; ++i) {
       const int s = i % QST, ab = i & 1;
-      mbar_wait(&ready[s], (i / QST) & 1);
-      if (i >= 2) mbar_wait(&acce[ab], ((i >> 1) - 1) & 1);
+      mbar_wait_sleep(&ready[s], (i / QST) & 1);
+      if (i >= 2) mbar_wait_sleep(&acce[ab], ((i >> 1) - 1) & 1);
       tc_fence_after();
       if (leader) {
         const uint64_t dA = desc_sw128(smem_u32(sQ + s * TILE), 16, 1024);
@@ -458,12 +492,12 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
     const int r = threadIdx.x >> 1, c0 = (threadIdx.x & 1) * 8;
     const uint8_t* tq = nullptr;
     if (a.use_pe) {
-      mbar_wait(init, 0);
+      mbar_wait_sleep(init, 0);
       tq = sTab;
     }
     for (int i = 0; i < n; ++i) {
       const int s = i % QST;
-      mbar_wait(&full[s], (i / QST) & 1);
+      mbar_wait_sleep(&full[s], (i / QST) & 1);
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
@@ -478,7 +512,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
     const int r = q4 * 32 + (threadIdx.x & 31);
     for (int i = 0; i < n; ++i) {
       const int ab = i & 1;
-      mbar_wait(&accf[ab], (i >> 1) & 1);
+      mbar_wait_sleep(&accf[ab], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t base = tmem + ab * 256 + (static_cast<uint32_t>(q4 * 32) << 16);
       uint32_t den_u[16];
@@ -694,7 +728,7 @@ static size_t up256(size_t x) { return (x + 255) / 256 * 256; }
 using namespace ropeslr;
 
 static bool linear_pe_eligible(const ropeslr_shape* s, const ropeslr_token_args* t) {
-  if (!s || !t || s->dtype != ROPESLR_BF16 || s->d != lnu::D) return false;
+  if (!s || !t || s->dtype != ROPESLR_BF16 || s->d != lnu::D || s->L >= (1LL << 31)) return false;
   const int nr = lnu::nrows_of(t);
   return lnu::StateLay::bytes(nr) <= 227 * 1024 && lnu::ApplyLay::bytes(nr) <= 227 * 1024;
 }
