@@ -13,8 +13,11 @@
 // per head and tensor (and the gate into per-axis scalars); the kernels add
 // three table rows per token on the way through:
 //
-//   state   (one CTA per (head, token chunk))  TMA K, V tiles -> k + T_k, phi,
-//           v + T_v in place in shared memory -> tcgen05 S += phi(K)^T V
+//   state   (one CTA per (head, token chunk))  TMA K, V tiles -> phi(k + T_k)
+//           in place in shared memory -> tcgen05 S += phi(K)^T V, then the
+//           PE part of V (T_v rows, written into V's buffer once that MMA
+//           is done; adding it to the bf16 v would round it away) -> S +=
+//           phi(K)^T T_v
 //           (M = d, N = d, K = 128 tokens, both operands MN-major) into
 //           TMEM, z = sum phi(k) in registers (fixed-order reduction over
 //           the token slots at the end); the chunk's [d, d | z] partial
@@ -146,6 +149,37 @@ __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool
   }
 }
 
+// Chunks [c0, c0 + NC) of row r of a tile := T[rt] + T[rx] + T[ry] (bf16x2
+// sums), zero for tokens beyond L: the PE part of V as its own MMA operand.
+// V itself stays the exact bf16 input: adding a table value much smaller than
+// v's bf16 spacing and rounding again would drop it systematically.
+template <int NC>
+__device__ __forceinline__ void table_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt, int rx,
+                                          int ry) {
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int c = c0 + cc;
+    uint4* p = tile_chunk(tile, r, c);
+    if (!valid) {
+      *p = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4 a = *reinterpret_cast<const uint4*>(tab + rt * TAB_PITCH + c * 16);
+    const uint4 b = *reinterpret_cast<const uint4*>(tab + rx * TAB_PITCH + c * 16);
+    const uint4 e = *reinterpret_cast<const uint4*>(tab + ry * TAB_PITCH + c * 16);
+    const uint32_t aa[4] = {a.x, a.y, a.z, a.w}, bb[4] = {b.x, b.y, b.z, b.w}, ee[4] = {e.x, e.y, e.z, e.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 s2 = __hadd2(*reinterpret_cast<const __nv_bfloat162*>(&aa[i]),
+                                  *reinterpret_cast<const __nv_bfloat162*>(&bb[i]));
+      s2 = __hadd2(s2, *reinterpret_cast<const __nv_bfloat162*>(&ee[i]));
+      o[i] = *reinterpret_cast<uint32_t*>(&s2);
+    }
+    *p = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 struct Grid3 {
   int T, Hg, Wg;
   // table rows of token l: t, T + x, T + Hg + y (32-bit: L < 2^31 on this path)
@@ -177,7 +211,7 @@ struct StateLay {
   static constexpr int OFF_V = OFF_K + 2 * TILE;
   static constexpr int OFF_TAB = OFF_V + 2 * TILE;
   __host__ __device__ static int off_bar(int nrows) { return OFF_TAB + ((2 * nrows * TAB_PITCH + 127) / 128) * 128; }
-  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 8 * 8 + 16; }
+  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 12 * 8 + 16; }
 };
 
 constexpr int kStateXf = 512;                 // transform threads: 4 per token row, 4 chunks of K and of V each
@@ -198,19 +232,24 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   uint8_t* sV = smem + StateLay::OFF_V;
   uint8_t* sTab = smem + StateLay::OFF_TAB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(a.nrows));
-  uint64_t* full = bars;       // [2] TMA -> transform
-  uint64_t* ready = bars + 2;  // [2] transform -> MMA
-  uint64_t* empty = bars + 4;  // [2] MMA -> TMA
-  uint64_t* done = bars + 6;   // MMA -> readout
-  uint64_t* tabf = bars + 7;   // tables landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* full = bars;        // [2] TMA -> transform
+  uint64_t* ready = bars + 2;   // [2] phi(K) written -> MMA (phi(K)^T V)
+  uint64_t* vdone = bars + 4;   // [2] that MMA done -> transform (V buffer free for the PE tile)
+  uint64_t* tvready = bars + 6; // [2] PE tile written -> MMA (phi(K)^T T_v)
+  uint64_t* empty = bars + 8;   // [2] MMA -> TMA
+  uint64_t* done = bars + 10;   // MMA -> readout
+  uint64_t* tabf = bars + 11;   // tables landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * a.nrows * TAB_PITCH;
   const int tab_bytes = a.nrows * TAB_PITCH;
+  const bool pe = a.use_pe != 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&ready[i], kStateXf);
+      mbar_init(&vdone[i], 1);
+      mbar_init(&tvready[i], kStateXf);
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
@@ -248,31 +287,54 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       }
     }
   } else if (warp == kStateMma) {
+    // per tile i: S += phi(K_i)^T V_i, then (with PE) S += phi(K_i)^T Tv_i once
+    // the transform has put the PE tile into V_i's buffer; the second MMA of
+    // tile i - 1 goes after the first of tile i so the transform overlaps both
     constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
     const bool leader = elect_one();
+    auto mma = [&](int s, uint32_t first) {
+      const uint64_t dA = desc_sw128(smem_u32(sK + s * TILE), HALF, 1024);
+      const uint64_t dB = desc_sw128(smem_u32(sV + s * TILE), HALF, 1024);
+#pragma unroll
+      for (int kk = 0; kk < M / 16; ++kk)
+        mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
+                    idesc_s, (first == 0 || kk > 0) ? 1u : 0u);
+    };
+    auto second = [&](int j) {  // the PE tile of tile j
+      const int s = j & 1;
+      mbar_wait_sleep(&tvready[s], (j >> 1) & 1);
+      tc_fence_after();
+      if (leader) {
+        mma(s, 1u);
+        mma_commit(&empty[s]);
+        if (j == n - 1) mma_commit(done);
+      }
+      __syncwarp();
+    };
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
       mbar_wait_sleep(&ready[s], (i >> 1) & 1);
       tc_fence_after();
       if (leader) {
-        const uint64_t dA = desc_sw128(smem_u32(sK + s * TILE), HALF, 1024);
-        const uint64_t dB = desc_sw128(smem_u32(sV + s * TILE), HALF, 1024);
-#pragma unroll
-        for (int kk = 0; kk < M / 16; ++kk)
-          mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
-                      idesc_s, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&empty[s]);
-        if (i == n - 1) mma_commit(done);
+        mma(s, i > 0 ? 1u : 0u);
+        if (pe) {
+          mma_commit(&vdone[s]);
+        } else {
+          mma_commit(&empty[s]);
+          if (i == n - 1) mma_commit(done);
+        }
       }
       __syncwarp();
+      if (pe && i > 0) second(i - 1);
     }
+    if (pe && n > 0) second(n - 1);
   } else {
     // transform warps: 4 threads per token row, 4 of its 16 chunks each;
     // z = sum phi(k) accumulates in registers over the CTA's tiles
     const int r = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 4;
     const uint8_t* tk = nullptr;
     const uint8_t* tv = nullptr;
-    if (a.use_pe) {
+    if (pe) {
       mbar_wait_sleep(tabf, 0);
       tk = sTab;
       tv = sTab + tab_bytes;
@@ -280,6 +342,17 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     float zacc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) zacc[j] = 0.f;
+    auto pe_tile = [&](int j) {  // the PE part of V_j into V_j's buffer once phi(K_j)^T V_j is done
+      const int s = j & 1;
+      mbar_wait_sleep(&vdone[s], (j >> 1) & 1);
+      const int64_t l = static_cast<int64_t>(t0 + j) * M + r;
+      const bool valid = l < a.L;
+      int rt = 0, rx = 0, ry = 0;
+      if (valid) a.g.rows(l, rt, rx, ry);
+      table_row<4>(sV + s * TILE, r, c0, valid, tv, rt, rx, ry);
+      fence_proxy_async_smem();
+      mbar_arrive(&tvready[s]);
+    };
     for (int i = 0; i < n; ++i) {
       const int s = i & 1;
       mbar_wait_sleep(&full[s], (i >> 1) & 1);
@@ -288,10 +361,11 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
       transform_row<true, 4, true>(sK + s * TILE, r, c0, valid, tk, rt, rx, ry, &zacc);
-      transform_row<false, 4>(sV + s * TILE, r, c0, valid, tv, rt, rx, ry);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
+      if (pe && i > 0) pe_tile(i - 1);
     }
+    if (pe && n > 0) pe_tile(n - 1);
     // every MMA has read the K ring: reuse it for the z partials
     // zbuf[thread][32] (thread = 4 r + q holds columns [32 q, 32 q + 32))
     if (n > 0) mbar_wait_sleep(done, 0);
