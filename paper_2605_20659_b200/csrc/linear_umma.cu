@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kStateThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < M / 16; ++kk)
         mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
-                    idesc_s, (first == 0 || kk > 0) ? 1u : 0u);
+                    idesc_s, (first != 0 || kk > 0) ? 1u : 0u);
     };
     auto second = [&](int j) {  // the PE tile of tile j
       const int s = j & 1;
