@@ -23,16 +23,17 @@
 //           the token slots at the end); the chunk's [d, d | z] partial
 //           goes to the workspace;
 //   reduce  partials summed in fixed chunk order (float64), written as the
-//           apply GEMM's B operand image [S | z] (K-major, 128B-swizzled),
-//           split into bf16 hi + lo (~16 mantissa bits);
+//           apply GEMM's B operand image [S | z] / L (K-major,
+//           128B-swizzled, fp16);
 //   apply   (one CTA per (head, token chunk))  TMA Q tiles -> phi(q + T_q)
-//           in place -> tcgen05 [phi(Q) S | phi(Q) z] (N = 144) as hi + lo
-//           MMAs into a double-buffered TMEM accumulator; the epilogue
+//           in place as fp16 -> tcgen05 [phi(Q) S | phi(Q) z] (fp16 x fp16,
+//           N = 144) into a double-buffered TMEM accumulator; the epilogue
 //           warps divide by max(phi(q) . z, 1e-8), RMS-normalise with
 //           rms_lowrank and store y_lr (bf16) and optionally o_lr (f32);
 //   gate    g_logit = x . w_g over the local columns + G[t] + G[x] + G[y]
 //           (one warp per token: X is read once, no per-element PE gather).
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -51,7 +52,7 @@ constexpr int TILE = 2 * HALF;          // 32 KiB
 constexpr int TAB_PITCH = 272;          // bytes per bf16 table row: 128 values + 16 B (conflict-free rows)
 constexpr int NB = 144;                 // apply GEMM N: 128 numerators + the denominator column + pad
 constexpr int BHALF = NB * 128;         // 18 KiB: one 64-wide K half of the B image
-constexpr int BIMG = 2 * BHALF;         // 36 KiB: the hi (or lo) image
+constexpr int BIMG = 2 * BHALF;         // 36 KiB: the fp16 image
 constexpr int NPART = NB;               // columns of a state partial: S row (128) | z | pad
 constexpr float kFloor = 1e-8f;         // mechanism.py:347
 
@@ -105,7 +106,8 @@ __device__ __forceinline__ float2 phi2(float2 k) {
 // then phi when PHI; rows of tokens beyond L become zero.  Several threads
 // share a row (each its own chunk range), so the CUDA-core work of a tile
 // spreads over many warps.  ACC: add the phi values to acc (z = sum phi(k)).
-template <bool PHI, int NC, bool ACC = false>
+// F16OUT: store fp16 instead of bf16 (the apply GEMM runs fp16 x fp16).
+template <bool PHI, int NC, bool ACC = false, bool F16OUT = false>
 __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt,
                                               int rx, int ry, float (*acc)[NC * 8] = nullptr) {
 #pragma unroll
@@ -142,8 +144,13 @@ __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool
         (*acc)[cc * 8 + 2 * i] += f.x;
         (*acc)[cc * 8 + 2 * i + 1] += f.y;
       }
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
-      o[i] = *reinterpret_cast<uint32_t*>(&h2);
+      if (F16OUT) {
+        __half2 h2 = __floats2half2_rn(f.x, f.y);
+        o[i] = *reinterpret_cast<uint32_t*>(&h2);
+      } else {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
+        o[i] = *reinterpret_cast<uint32_t*>(&h2);
+      }
     }
     *p = make_uint4(o[0], o[1], o[2], o[3]);
   }
@@ -412,30 +419,29 @@ __global__ void __launch_bounds__(kStateThreads, 1)
 }
 
 // Sum the chunk partials (fixed order, float64) and write the apply GEMM's B
-// operand: B[n][k] = S[k][n] for n < 128, B[128][k] = z[k], zero rows above;
-// K-major, two 64-wide K halves of [144 rows x 128 B], 128B-swizzled as a
-// 1024-aligned shared-memory copy expects; bf16 hi image then lo image.
-// Also S and z in float32 (state [BH][128][NPART]) for inspection.
+// operand: B[n][k] = S[k][n] / L for n < 128, B[128][k] = z[k] / L, zero rows
+// above; K-major, two 64-wide K halves of [144 rows x 128 B], 128B-swizzled
+// as a 1024-aligned shared-memory copy expects, in fp16.  The common 1/L
+// cancels in phi(q) S / phi(q) z and keeps z (a sum of L positive terms)
+// inside fp16's range; fp16's 11-bit significand keeps S and z to ~5e-4,
+// against bf16's 2^-9 for the phi(q) operand it meets in the MMA.  Also S
+// and z in float32, unscaled (state [BH][128][NPART]), for inspection.
 __global__ void __launch_bounds__(256) linear_reduce_image_kernel(const float* __restrict__ partial, int nchunks,
-                                                                  uint8_t* __restrict__ bimg,
+                                                                  double inv_L, uint8_t* __restrict__ bimg,
                                                                   float* __restrict__ state) {
   const int bh = blockIdx.x;
   const float* src = partial + static_cast<int64_t>(bh) * nchunks * D * NPART;
-  uint8_t* img = bimg + static_cast<int64_t>(bh) * 2 * BIMG;
-  // blockIdx.y: 16 of the 144 image rows; thread: (row, k) with k fastest so
-  // the partial reads (k-major rows of NPART) are spread, the image writes local
+  uint8_t* img = bimg + static_cast<int64_t>(bh) * BIMG;
+  // blockIdx.y: 16 of the 144 image rows; thread: (row, k)
   for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) {
     const int n = blockIdx.y * 16 + e / D, k = e % D;
     double acc = 0.0;
     if (n <= 128)
       for (int c = 0; c < nchunks; ++c) acc += src[(static_cast<int64_t>(c) * D + k) * NPART + n];
     if (state != nullptr && n <= 128) state[(static_cast<int64_t>(bh) * D + k) * NPART + n] = static_cast<float>(acc);
-    const __nv_bfloat16 hi = __double2bfloat16(acc);
-    const __nv_bfloat16 lo = __double2bfloat16(acc - static_cast<double>(__bfloat162float(hi)));
     const int half = k >> 6, ch = (k & 63) >> 3, el = k & 7;
     const int off = half * BHALF + n * 128 + ((ch ^ (n & 7)) << 4) + el * 2;
-    *reinterpret_cast<__nv_bfloat16*>(img + off) = hi;
-    *reinterpret_cast<__nv_bfloat16*>(img + BIMG + off) = lo;
+    *reinterpret_cast<__half*>(img + off) = __float2half_rn(static_cast<float>(acc * inv_L));
   }
 }
 
@@ -448,19 +454,19 @@ struct ApplyArgs {
   int ntiles;
   int tiles_per_cta;
   const uint8_t* tables;  // [H][3][nrows][TAB_PITCH]
-  const uint8_t* bimg;    // [BH][2][BIMG]
+  const uint8_t* bimg;    // [BH][BIMG] fp16
   const float* rms_lr;
   float eps;
   __nv_bfloat16* y_lr;    // [B, L, H, d]
   float* o_lr;            // [B, H, L, d] nullable
 };
 
-// smem: Q ring (3 x 32 KiB) | B image hi | lo (2 x 36 KiB) | T_q | rms | row sums | barriers
-constexpr int QST = 3;  // Q ring depth
+// smem: Q ring (4 x 32 KiB) | B image (36 KiB) | T_q | rms | row sums | barriers
+constexpr int QST = 4;  // Q ring depth
 struct ApplyLay {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_B = OFF_Q + QST * TILE;
-  static constexpr int OFF_TAB = OFF_B + 2 * BIMG;
+  static constexpr int OFF_TAB = OFF_B + BIMG;
   __host__ __device__ static int off_rms(int nrows) { return OFF_TAB + ((nrows * TAB_PITCH + 127) / 128) * 128; }
   __host__ __device__ static int off_xs(int nrows) { return off_rms(nrows) + D * 4; }
   __host__ __device__ static int off_bar(int nrows) { return off_xs(nrows) + 2 * M * 4; }
@@ -472,7 +478,7 @@ constexpr int kApplyEpi = 256;  // epilogue threads (warps 8-15): lane quarter w
 constexpr int kApplyTma = (kApplyXf + kApplyEpi) / 32, kApplyMma = kApplyTma + 1;
 constexpr int kApplyThreads = kApplyXf + kApplyEpi + 64;
 
-__global__ void __launch_bounds__(kApplyThreads, 1)
+__global__ void __maxnreg__(112)
     linear_apply_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ ApplyArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
@@ -522,8 +528,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
   if (warp == kApplyTma) {
     if (elect_one()) {
       const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * tab_bytes;
-      mbar_arrive_expect_tx(init, 2 * BIMG + (a.use_pe ? tab_bytes : 0));
-      bulk_load_1d(sB, a.bimg + static_cast<int64_t>(bh) * 2 * BIMG, 2 * BIMG, init, policy_evict_last());
+      mbar_arrive_expect_tx(init, BIMG + (a.use_pe ? tab_bytes : 0));
+      bulk_load_1d(sB, a.bimg + static_cast<int64_t>(bh) * BIMG, BIMG, init, policy_evict_last());
       if (a.use_pe) bulk_load_1d(sTab, gtab, tab_bytes, init, policy_evict_last());
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < n; ++i) {
@@ -536,11 +542,10 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       }
     }
   } else if (warp == kApplyMma) {
-    constexpr uint32_t idesc = idesc_bf16_f32(M, NB, false, false);
+    constexpr uint32_t idesc = idesc_f16_f32(M, NB, false, false);
     const bool leader = elect_one();
     mbar_wait_sleep(init, 0);
-    const uint64_t dBh = desc_sw128(smem_u32(sB), 16, 1024);
-    const uint64_t dBl = desc_sw128(smem_u32(sB + BIMG), 16, 1024);
+    const uint64_t dB = desc_sw128(smem_u32(sB), 16, 1024);
     for (int i = 0; i < n; ++i) {
       const int s = i % QST, ab = i & 1;
       mbar_wait_sleep(&ready[s], (i / QST) & 1);
@@ -553,8 +558,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t ka = ((kk & 3) * 32 + (kk >> 2) * HALF) >> 4;
           const uint32_t kb = ((kk & 3) * 32 + (kk >> 2) * BHALF) >> 4;
-          mma_bf16_ss(acc_t, dA + ka, dBh + kb, idesc, kk > 0 ? 1u : 0u);
-          mma_bf16_ss(acc_t, dA + ka, dBl + kb, idesc, 1u);
+          mma_f16_ss(acc_t, dA + ka, dB + kb, idesc, kk > 0 ? 1u : 0u);
         }
         mma_commit(&empty[s]);
         mma_commit(&accf[ab]);
@@ -576,7 +580,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true, 8>(sQ + s * TILE, r, c0, valid, tq, rt, rx, ry);
+      transform_row<true, 8, false, true>(sQ + s * TILE, r, c0, valid, tq, rt, rx, ry);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
     }
@@ -841,7 +845,7 @@ extern "C" size_t ropeslr_linear_pe_workspace_bytes(const ropeslr_shape* s, cons
   const int ntiles = static_cast<int>(ceil_div(s->L, lnu::M));
   const int nch = lnu::chunks_per_head(BH, ntiles);
   return lnu::up256(static_cast<size_t>(BH) * nch * lnu::D * lnu::NPART * 4) +
-         lnu::up256(static_cast<size_t>(BH) * 2 * lnu::BIMG);
+         lnu::up256(static_cast<size_t>(BH) * lnu::BIMG);
 }
 
 extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_token_args* t, const void* q_lin,
@@ -891,8 +895,8 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
     return ROPESLR_ERR_LAUNCH;
   lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, sa);
   if (int e = launch_status()) return e;
-  lnu::linear_reduce_image_kernel<<<dim3(static_cast<unsigned>(BH), lnu::NB / 16), 256, 0, st>>>(partial, nch, bimg,
-                                                                                                state);
+  lnu::linear_reduce_image_kernel<<<dim3(static_cast<unsigned>(BH), lnu::NB / 16), 256, 0, st>>>(
+      partial, nch, 1.0 / static_cast<double>(s->L), bimg, state);
   if (int e = launch_status()) return e;
   // apply
   lnu::ApplyArgs aa{};
