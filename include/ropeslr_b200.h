@@ -117,6 +117,9 @@ typedef struct ropeslr_token_args {
 /* ---------------------------------------------------------------- misc */
 int ropeslr_abi_version(void);
 const char* ropeslr_status_string(int status);
+/* The CUDA runtime's message for the last error behind a ROPESLR_ERR_LAUNCH
+ * on the calling thread ("no error" if none). */
+const char* ropeslr_last_cuda_error(void);
 /* ROPESLR_OK when `device` is an sm_100 part the kernels were built for. */
 int ropeslr_device_check(int device);
 /* Number of flat blocks: ceil(L / block). */

@@ -59,6 +59,7 @@ P = ctypes.POINTER
 _SIGNATURES = {
     "ropeslr_abi_version": (c_i32, []),
     "ropeslr_status_string": (ctypes.c_char_p, [c_i32]),
+    "ropeslr_last_cuda_error": (ctypes.c_char_p, []),
     "ropeslr_device_check": (c_i32, [c_i32]),
     "ropeslr_num_blocks": (c_i64, [c_i64, c_i32]),
     "ropeslr_set_option": (c_i32, [ctypes.c_char_p, c_i32]),
@@ -142,6 +143,8 @@ def lib() -> ctypes.CDLL:
 def check(fn: str, status: int) -> None:
     if status != 0:
         msg = lib().ropeslr_status_string(status).decode()
+        if status == -5:  # ROPESLR_ERR_LAUNCH: add the CUDA runtime's message
+            msg += f" [{lib().ropeslr_last_cuda_error().decode()}]"
         raise RopeSLRError(fn, status, msg)
 
 

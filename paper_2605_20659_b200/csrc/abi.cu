@@ -10,6 +10,9 @@
 
 namespace ropeslr {
 
+static thread_local cudaError_t t_last_error = cudaSuccess;
+void note_cuda_error(cudaError_t e) { t_last_error = e; }
+
 int num_sms() {
   static std::mutex mu;
   static int cache[64] = {0};
@@ -128,4 +131,8 @@ extern "C" int ropeslr_get_option(const char* name) {
   if (!strcmp(name, "rope_tma")) return t.rope_tma;
   if (!strcmp(name, "linear_simt")) return t.linear_simt;
   return ROPESLR_ERR_VALUE;
+}
+
+extern "C" const char* ropeslr_last_cuda_error(void) {
+  return cudaGetErrorString(ropeslr::t_last_error);
 }

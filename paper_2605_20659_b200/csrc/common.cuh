@@ -76,9 +76,12 @@ __device__ __forceinline__ float warp_sum(T v) {
   return v;
 }
 
-// Host: map a CUDA error to a status.
+// Host: map a CUDA error to a status; the error is kept per thread for
+// ropeslr_last_cuda_error().
+void note_cuda_error(cudaError_t e);  // abi.cu
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) note_cuda_error(e);
   return e == cudaSuccess ? ROPESLR_OK : ROPESLR_ERR_LAUNCH;
 }
 
