@@ -478,7 +478,7 @@ constexpr int kApplyEpi = 256;  // epilogue threads (warps 8-15): lane quarter w
 constexpr int kApplyTma = (kApplyXf + kApplyEpi) / 32, kApplyMma = kApplyTma + 1;
 constexpr int kApplyThreads = kApplyXf + kApplyEpi + 64;
 
-__global__ void __maxnreg__(104)
+__global__ void __launch_bounds__(kApplyThreads, 1)
     linear_apply_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ ApplyArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
