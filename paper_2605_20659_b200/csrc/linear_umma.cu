@@ -60,8 +60,9 @@ __device__ __forceinline__ float elu1(float v) { return v > 0.f ? v + 1.f : __ex
 
 // Chunk c (0..15: 8 bf16 each) of row r of a TMA-loaded [128 x 128] tile,
 // two 64-column halves in the 128B-swizzled layout.
+template <int ROWS = M>
 __device__ __forceinline__ uint4* tile_chunk(uint8_t* tile, int r, int c) {
-  return reinterpret_cast<uint4*>(tile + (c >> 3) * HALF + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+  return reinterpret_cast<uint4*>(tile + (c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
@@ -107,13 +108,13 @@ __device__ __forceinline__ float2 phi2(float2 k) {
 // share a row (each its own chunk range), so the CUDA-core work of a tile
 // spreads over many warps.  ACC: add the phi values to acc (z = sum phi(k)).
 // F16OUT: store fp16 instead of bf16 (the apply GEMM runs fp16 x fp16).
-template <bool PHI, int NC, bool ACC = false, bool F16OUT = false>
+template <bool PHI, int NC, bool ACC = false, bool F16OUT = false, int ROWS = M>
 __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt,
                                               int rx, int ry, float (*acc)[NC * 8] = nullptr) {
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) {
     const int c = c0 + cc;
-    uint4* p = tile_chunk(tile, r, c);
+    uint4* p = tile_chunk<ROWS>(tile, r, c);
     if (!valid) {
       *p = make_uint4(0, 0, 0, 0);
       continue;
@@ -160,13 +161,13 @@ __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool
 // sums), zero for tokens beyond L: the PE part of V as its own MMA operand.
 // V itself stays the exact bf16 input: adding a table value much smaller than
 // v's bf16 spacing and rounding again would drop it systematically.
-template <int NC>
+template <int NC, int ROWS = M>
 __device__ __forceinline__ void table_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt, int rx,
                                           int ry) {
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) {
     const int c = c0 + cc;
-    uint4* p = tile_chunk(tile, r, c);
+    uint4* p = tile_chunk<ROWS>(tile, r, c);
     if (!valid) {
       *p = make_uint4(0, 0, 0, 0);
       continue;
@@ -205,23 +206,29 @@ struct StateArgs {
   Grid3 g;
   int use_pe;
   int nrows;
-  int ntiles;           // ceil(L / 128)
+  int ntiles;           // ceil(L / SR)
   int tiles_per_cta;
   int nchunks;
   const uint8_t* tables;  // [H][3][nrows][TAB_PITCH] bf16 (q, k, v)
   float* partial;       // [BH][nchunks][128][NPART]
 };
 
-// smem: K ring (2 x 32 KiB) | V ring (2 x 32 KiB) | T_k | T_v | barriers
+// The state pass streams 64-token stages, four deep (more bytes in flight per
+// SM than two 128-token ones in the same space).
+constexpr int SR = 64;                 // tokens per state stage
+constexpr int SHALF = SR * 128;        // 8 KiB: one 64-column half of a stage tile
+constexpr int STILE = 2 * SHALF;       // 16 KiB
+constexpr int SST = 4;                 // state ring depth
+// smem: K ring (4 x 16 KiB) | V ring (4 x 16 KiB) | T_k | T_v | barriers
 struct StateLay {
   static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + 2 * TILE;
-  static constexpr int OFF_TAB = OFF_V + 2 * TILE;
+  static constexpr int OFF_V = OFF_K + SST * STILE;
+  static constexpr int OFF_TAB = OFF_V + SST * STILE;
   __host__ __device__ static int off_bar(int nrows) { return OFF_TAB + ((2 * nrows * TAB_PITCH + 127) / 128) * 128; }
-  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + 12 * 8 + 16; }
+  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + (5 * SST + 2) * 8 + 16; }
 };
 
-constexpr int kStateXf = 512;                 // transform threads: 4 per token row, 4 chunks of K and of V each
+constexpr int kStateXf = 512;                 // transform threads: 8 per token row, 2 chunks of K and of V each
 constexpr int kStateThreads = kStateXf + 64;  // + warp 16 TMA, warp 17 MMA + TMEM
 constexpr int kStateTma = kStateXf / 32, kStateMma = kStateTma + 1;
 
@@ -239,20 +246,20 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   uint8_t* sV = smem + StateLay::OFF_V;
   uint8_t* sTab = smem + StateLay::OFF_TAB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(a.nrows));
-  uint64_t* full = bars;        // [2] TMA -> transform
-  uint64_t* ready = bars + 2;   // [2] phi(K) written -> MMA (phi(K)^T V)
-  uint64_t* vdone = bars + 4;   // [2] that MMA done -> transform (V buffer free for the PE tile)
-  uint64_t* tvready = bars + 6; // [2] PE tile written -> MMA (phi(K)^T T_v)
-  uint64_t* empty = bars + 8;   // [2] MMA -> TMA
-  uint64_t* done = bars + 10;   // MMA -> readout
-  uint64_t* tabf = bars + 11;   // tables landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* full = bars;                 // [SST] TMA -> transform
+  uint64_t* ready = bars + SST;          // [SST] phi(K) written -> MMA (phi(K)^T V)
+  uint64_t* vdone = bars + 2 * SST;      // [SST] that MMA done -> transform (V buffer free for the PE tile)
+  uint64_t* tvready = bars + 3 * SST;    // [SST] PE tile written -> MMA (phi(K)^T T_v)
+  uint64_t* empty = bars + 4 * SST;      // [SST] MMA -> TMA
+  uint64_t* done = bars + 5 * SST;       // MMA -> readout
+  uint64_t* tabf = done + 1;             // tables landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tabf + 1);
   const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * a.nrows * TAB_PITCH;
   const int tab_bytes = a.nrows * TAB_PITCH;
   const bool pe = a.use_pe != 0;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < SST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&ready[i], kStateXf);
       mbar_init(&vdone[i], 1);
@@ -281,16 +288,16 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       }
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < n; ++i) {
-        const int s = i & 1;
-        if (i >= 2) mbar_wait_sleep(&empty[s], ((i >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], 2 * TILE);
-        const int row = (t0 + i) * M;
-        uint8_t* k = sK + s * TILE;
-        uint8_t* v = sV + s * TILE;
+        const int s = i % SST;
+        if (i >= SST) mbar_wait_sleep(&empty[s], ((i / SST) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], 2 * STILE);
+        const int row = (t0 + i) * SR;
+        uint8_t* k = sK + s * STILE;
+        uint8_t* v = sV + s * STILE;
         tma_load_3d_hint(k, &tmK, &full[s], 0, row, bh, pol);
-        tma_load_3d_hint(k + HALF, &tmK, &full[s], 64, row, bh, pol);
+        tma_load_3d_hint(k + SHALF, &tmK, &full[s], 64, row, bh, pol);
         tma_load_3d_hint(v, &tmV, &full[s], 0, row, bh, pol);
-        tma_load_3d_hint(v + HALF, &tmV, &full[s], 64, row, bh, pol);
+        tma_load_3d_hint(v + SHALF, &tmV, &full[s], 64, row, bh, pol);
       }
     }
   } else if (warp == kStateMma) {
@@ -300,16 +307,16 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
     const bool leader = elect_one();
     auto mma = [&](int s, uint32_t first) {
-      const uint64_t dA = desc_sw128(smem_u32(sK + s * TILE), HALF, 1024);
-      const uint64_t dB = desc_sw128(smem_u32(sV + s * TILE), HALF, 1024);
+      const uint64_t dA = desc_sw128(smem_u32(sK + s * STILE), SHALF, 1024);
+      const uint64_t dB = desc_sw128(smem_u32(sV + s * STILE), SHALF, 1024);
 #pragma unroll
-      for (int kk = 0; kk < M / 16; ++kk)
+      for (int kk = 0; kk < SR / 16; ++kk)
         mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
                     idesc_s, (first != 0 || kk > 0) ? 1u : 0u);
     };
     auto second = [&](int j) {  // the PE tile of tile j
-      const int s = j & 1;
-      mbar_wait_sleep(&tvready[s], (j >> 1) & 1);
+      const int s = j % SST;
+      mbar_wait_sleep(&tvready[s], (j / SST) & 1);
       tc_fence_after();
       if (leader) {
         mma(s, 1u);
@@ -319,8 +326,8 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       __syncwarp();
     };
     for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
-      mbar_wait_sleep(&ready[s], (i >> 1) & 1);
+      const int s = i % SST;
+      mbar_wait_sleep(&ready[s], (i / SST) & 1);
       tc_fence_after();
       if (leader) {
         mma(s, i > 0 ? 1u : 0u);
@@ -336,9 +343,9 @@ __global__ void __launch_bounds__(kStateThreads, 1)
     }
     if (pe && n > 0) second(n - 1);
   } else {
-    // transform warps: 4 threads per token row, 4 of its 16 chunks each;
+    // transform warps: 8 threads per token row, 2 of its 16 chunks each;
     // z = sum phi(k) accumulates in registers over the CTA's tiles
-    const int r = threadIdx.x >> 2, c0 = (threadIdx.x & 3) * 4;
+    const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 2;
     const uint8_t* tk = nullptr;
     const uint8_t* tv = nullptr;
     if (pe) {
@@ -346,50 +353,50 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       tk = sTab;
       tv = sTab + tab_bytes;
     }
-    float zacc[32];
+    float zacc[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) zacc[j] = 0.f;
+    for (int j = 0; j < 16; ++j) zacc[j] = 0.f;
     auto pe_tile = [&](int j) {  // the PE part of V_j into V_j's buffer once phi(K_j)^T V_j is done
-      const int s = j & 1;
-      mbar_wait_sleep(&vdone[s], (j >> 1) & 1);
-      const int64_t l = static_cast<int64_t>(t0 + j) * M + r;
+      const int s = j % SST;
+      mbar_wait_sleep(&vdone[s], (j / SST) & 1);
+      const int64_t l = static_cast<int64_t>(t0 + j) * SR + r;
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      table_row<4>(sV + s * TILE, r, c0, valid, tv, rt, rx, ry);
+      table_row<2, SR>(sV + s * STILE, r, c0, valid, tv, rt, rx, ry);
       fence_proxy_async_smem();
       mbar_arrive(&tvready[s]);
     };
     for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
-      mbar_wait_sleep(&full[s], (i >> 1) & 1);
-      const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
+      const int s = i % SST;
+      mbar_wait_sleep(&full[s], (i / SST) & 1);
+      const int64_t l = static_cast<int64_t>(t0 + i) * SR + r;
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true, 4, true>(sK + s * TILE, r, c0, valid, tk, rt, rx, ry, &zacc);
+      transform_row<true, 2, true, false, SR>(sK + s * STILE, r, c0, valid, tk, rt, rx, ry, &zacc);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
       if (pe && i > 0) pe_tile(i - 1);
     }
     if (pe && n > 0) pe_tile(n - 1);
     // every MMA has read the K ring: reuse it for the z partials
-    // zbuf[thread][32] (thread = 4 r + q holds columns [32 q, 32 q + 32))
+    // zbuf[thread][16] (thread = 8 r + q holds columns [16 q, 16 q + 16))
     if (n > 0) mbar_wait_sleep(done, 0);
     float* zbuf = reinterpret_cast<float*>(sK);
 #pragma unroll
-    for (int j = 0; j < 32; j += 4)
-      *reinterpret_cast<float4*>(zbuf + threadIdx.x * 32 + j) = make_float4(zacc[j], zacc[j + 1], zacc[j + 2], zacc[j + 3]);
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(zbuf + threadIdx.x * 16 + j) = make_float4(zacc[j], zacc[j + 1], zacc[j + 2], zacc[j + 3]);
     asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
   }
   if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out
     const int r = threadIdx.x;
     // the chunk's partial [S | z]: TMEM lane r = row r (d_k) of S
     float* dst = a.partial + ((static_cast<int64_t>(bh) * a.nchunks + chunk) * D + r) * NPART;
-    // z[r] over the 128 token slots in fixed order
+    // z[r] over the 64 token slots in fixed order
     const float* zbuf = reinterpret_cast<const float*>(sK);
     float zsum = 0.f;
-    for (int slot = 0; slot < M; ++slot) zsum += zbuf[(slot * 4 + (r >> 5)) * 32 + (r & 31)];
+    for (int slot = 0; slot < SR; ++slot) zsum += zbuf[(slot * 8 + (r >> 4)) * 16 + (r & 15)];
     if (n > 0) {
       tc_fence_after();
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
@@ -776,12 +783,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // [BH, L, 128] bf16 as a 3-D tensor, box [64 cols, 128 rows, 1], 128B swizzle;
 // rows past L read as zero.
-static bool make_map(CUtensorMap* m, const void* base, int64_t BH, int64_t L) {
+static bool make_map(CUtensorMap* m, const void* base, int64_t BH, int64_t L, int rows = M) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(BH)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(L) * D * 2};
-  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(M), 1};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), 1};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -875,8 +882,8 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   lnu::Grid3 g{t->grid_t, t->grid_h, t->grid_w};
 
   CUtensorMap mq, mk, mv;
-  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mk, k_lin, BH, s->L) ||
-      !lnu::make_map(&mv, v_lin, BH, s->L))
+  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mk, k_lin, BH, s->L, lnu::SR) ||
+      !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR))
     return ROPESLR_ERR_LAUNCH;
   // state
   lnu::StateArgs sa{};
@@ -885,8 +892,9 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   sa.g = g;
   sa.use_pe = t->use_pe;
   sa.nrows = nr;
-  sa.ntiles = ntiles;
-  sa.tiles_per_cta = tpc;
+  // the state pass walks the same token chunks in 64-token stages
+  sa.ntiles = static_cast<int>(ceil_div(s->L, lnu::SR));
+  sa.tiles_per_cta = tpc * (lnu::M / lnu::SR);
   sa.nchunks = nch;
   sa.tables = tab;
   sa.partial = partial;
