@@ -744,9 +744,14 @@ __global__ void __launch_bounds__(256) linear_gate_kernel(const __nv_bfloat16* _
   if (tok >= BL) return;
   const __nv_bfloat16* row = x + tok * row_stride;
   float s = 0.f;
+#pragma unroll 4
   for (int64_t c = lane * 8; c < ncols; c += 256) {
     float f[8];
-    bf16x8_to_f32(*reinterpret_cast<const uint4*>(row + c), f);
+    uint4 u;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+        : "l"(row + c));
+    bf16x8_to_f32(u, f);
     const float4 wa = *reinterpret_cast<const float4*>(w_g + c);
     const float4 wb = *reinterpret_cast<const float4*>(w_g + c + 4);
     s = fmaf(f[0], wa.x, s);
