@@ -55,6 +55,16 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 L2_TMA_TBPS = 10.85
 
 
+def k2_traffic(workload, world):
+    """DRAM bytes (read + write) per launch of the K2 kernel for this workload,
+    from the committed ncu capture (profiles/k2_traffic.json), or None."""
+    path = os.path.join(REPO, "profiles", "k2_traffic.json")
+    if world != 1 or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f).get(workload, {}).get("dram_bytes_per_launch")
+
+
 def load_peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -312,14 +322,17 @@ def run_ours(args, cfg, rank, world, local_rank):
     k2_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k2_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     out_buf = torch.empty((1, L, Hl, d), dtype=torch.bfloat16, device=dev)
+    k2_ws = []
 
     def step(i=None):
         prep = P.prepare(q, k, v, x, grid, params, settings, pe, head_offset=h0)
         if reduce_ is not None:
             reduce_(prep.g_logit)
+        if not k2_ws:
+            k2_ws.append(P.attend_workspace(prep))
         if i is not None:
             k2_start[i].record(stream)
-        out, _ = P.attend(prep, params, settings, out=out_buf)
+        out, _ = P.attend(prep, params, settings, out=out_buf, workspace=k2_ws[0])
         if i is not None:
             k2_end[i].record(stream)
         return prep
@@ -330,6 +343,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     attended_local = int(prep.sel.attended.sum())
     tiles_local = int(prep.sel.cnt.sum())  # (query block, selected key block) pairs = K/V tiles K2 streams
+    fallback_local = P.fallback_units(prep, k2_ws[0])  # units the running-max kernel recomputed
     barrier()
     torch.cuda.synchronize()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -462,15 +476,18 @@ def run_ours(args, cfg, rank, world, local_rank):
                                "kernels": "PE fold + tcgen05 low-rank / gate + fixed-order gate sum",
                                "unit": "read X once, write y_lr once"}},
         "attended_pairs": attended_total,
+        "k2_fallback_units": {"rank0": fallback_local, "of_units": Hl * nb,
+                              "note": "(head, query block) units whose fixed exponent reference failed and that the "
+                                      "running-max kernel recomputed (0 on N(0,1) inputs; see --config skew)"},
         "sparsity": 1.0 - attended_total / (H * float(L) ** 2),
         "roofline": {"bound": "tensor", "kernel": "sparse_attn_fixed_kernel (K2+K4 fused)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": peaks["source"] + ", bf16 dense sustained (kernel timed inside a long step)",
                      "peak_burst": peaks.get("bf16_tflops"), "frac_of_burst": achieved / peaks.get("bf16_tflops", 1),
-                     # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the
-                     # committed ncu --set full capture (profiles/r01o_ncu_summary.md)
-                     "traffic": 9.87e9 if cfg["name"].startswith("hunyuan") and world == 1 else None,
-                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/r01o_ncu_summary.md",
+                     # dram__bytes_read.sum + dram__bytes_write.sum of this kernel per launch, from the
+                     # committed ncu --set full capture of this command (profiles/k2_traffic.json)
+                     "traffic": k2_traffic(cfg["name"], world),
+                     "traffic_unit": "bytes per launch", "traffic_source": "profiles/k2_traffic.json (ncu --set full)",
                      "algorithmic_unit": "4*d*attended pairs per launch (flops.c_sparse)",
                      # what actually bounds K2: every (query block, key block) tile streams
                      # its K and V block (2 * block * d * 2 B) from L2 into shared memory.
@@ -685,6 +702,77 @@ def run_linear(args, local_rank):
         "clocks": clocks}), flush=True)
 
 
+def skew_blocks(q, k, block, seed=1, strength=4.0, spread=2.0):
+    """Block scores with structure, as real attention has (tests/test_gpu_parity
+    ._skew_blocks): a shared unit direction u, key block b shifted by
+    strength * c_b * u (c_b ~ N(0, 1)), query block j by strength * a_j * u
+    with a_j = exp(U(-spread, spread)); rows with large a_j get a peaked
+    block softmax and a wide score spread."""
+    import torch
+
+    B, H, L, d = q.shape
+    nb = -(-L // block)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    u = torch.randn(d, generator=g, dtype=torch.float64)
+    u = u / u.norm()
+    c = torch.randn((B, H, nb), generator=g, dtype=torch.float64)
+    a = torch.exp((torch.rand((B, H, nb), generator=g, dtype=torch.float64) * 2 - 1) * spread)
+
+    def shift(t, w):
+        w = w.repeat_interleave(block, dim=-1)[..., :L].to(t.device)
+        return (t.double() + strength * w[..., None] * u.to(t.device)).to(t.dtype)
+
+    return shift(q, a), shift(k, c)
+
+
+def run_skew(args, local_rank):
+    """K2 on realistic (skewed) block scores at the config-3 shape: the step
+    time and the share of (head, query block) units the fixed-exponent
+    kernel hands to the running-max kernel, top-k (the BASELINE rule) and
+    keep 0.9, next to the N(0,1) inputs."""
+    import torch
+
+    import paper_2605_20659_b200 as P
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = CONFIGS["cfg3"]
+    q0, k0, v, x, params, pe, grid = make_inputs(cfg, 0, cfg["H"], dev)
+    L = grid.size
+    nb = -(-L // cfg["block"])
+    stream = torch.cuda.current_stream(dev)
+    for strength in (0.0, 4.0, 8.0):
+        q, k = (q0, k0) if strength == 0.0 else skew_blocks(q0, k0, cfg["block"], strength=strength)
+        for rule in ("topk", "keep0.9"):
+            sp = (P.SparseSettings.for_sparsity(cfg["block"], L, cfg["sparsity"]) if rule == "topk"
+                  else P.SparseSettings(cfg["block"], keep=0.9))
+            st = P.ForwardSettings(sp)
+            prep = P.prepare(q, k, v, x, grid, params, st, pe)
+            ws = P.attend_workspace(prep)
+            out = torch.empty((1, L, cfg["H"], cfg["d"]), dtype=torch.bfloat16, device=dev)
+            for _ in range(max(2, args.warmup)):
+                P.attend(prep, params, st, out=out, workspace=ws)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = max(3, args.steps // 2)
+            e0.record(stream)
+            for _ in range(n):
+                P.attend(prep, params, st, out=out, workspace=ws)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / n
+            att = int(prep.sel.attended.sum())
+            fb = P.fallback_units(prep, ws)
+            cnt = prep.sel.cnt.float()
+            print(json.dumps({
+                "metric": "K2+K4 on skewed block scores (config-3 shape)", "config": {
+                    "workload": cfg["name"] + f"_skew{strength:g}_{rule}", "skew_strength": strength, "rule": rule},
+                "k2_ms": ms, "sparse_TFLOP_per_s": 4.0 * cfg["d"] * att / (ms * 1e-3) / 1e12,
+                "fallback_units": fb, "units": cfg["H"] * nb, "fallback_rate": fb / (cfg["H"] * nb),
+                "blocks_per_row": {"min": int(cnt.min()), "max": int(cnt.max()), "mean": float(cnt.mean())},
+                "dtype": "bf16", "data": "synthetic: seeded N(0,1) + skew_blocks structure"}), flush=True)
+
+
 def run_train(args, local_rank):
     """SURVEY 8f next #3 measured: one Stage-I training step (training.py:
     the compensator / gate / RMSNorm / PE forward + backward against the
@@ -775,7 +863,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep", "train", "linear"], default="cfg3")
+    ap.add_argument("--config", choices=list(CONFIGS) + ["cfg4", "cfg2_sweep", "train", "linear", "skew"],
+                    default="cfg3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rope-pass", action="store_true", help="skip timing the fused RoPE + pooling pre-pass")
@@ -818,6 +907,8 @@ def main():
             run_train(args, local_rank)
         elif args.config == "linear":
             run_linear(args, local_rank)
+        elif args.config == "skew":
+            run_skew(args, local_rank)
         else:
             run_ours(args, cfg, rank, world, local_rank)
     finally:

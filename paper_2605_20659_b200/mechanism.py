@@ -642,8 +642,26 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     return Prepared(q=q, k=k, v=v, sel=sel, y_lr=y_lr, o_lr=o_lr, g_logit=g_logit, block=block, perm=perm)
 
 
+def attend_workspace(prep: Prepared, impl: str = "auto") -> torch.Tensor:
+    """A workspace for attend() (include/ropeslr_b200.h ropeslr_attend_fused);
+    pass it as ``workspace`` to reuse it and to read fallback_units()."""
+    shp = _shape(prep.q, prep.block)
+    return _workspace(_lib.lib().ropeslr_attend_workspace_bytes(ctypes_ref(shp), _lib.IMPL[impl]), prep.q.device)
+
+
+def fallback_units(prep: Prepared, workspace: torch.Tensor) -> int:
+    """(head, query block) units of the last attend() on `workspace` whose
+    fixed exponent reference failed and which the running-max kernel
+    recomputed (the workspace's int32 at [2 NU], NU = B * H * nb; tcgen05
+    path).  Synchronises."""
+    B, H, L, d = prep.q.shape
+    nu = B * H * (-(-L // prep.block))
+    return int(workspace[:4 * (2 * nu + 1)].view(torch.int32)[2 * nu].item())
+
+
 def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *, impl: str = "auto",
-           want_o_sparse: bool = False, out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None):
+           want_o_sparse: bool = False, out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None,
+           workspace: Optional[torch.Tensor] = None):
     """K2 + K4: block-sparse attention with the fused RMSNorm / gate / combine
     epilogue (mechanism.py:321-326, 435-451).  Returns (out [B, L, H*d],
     o_sparse [B, H, L, d] float32 or None).  out_dtype: Q's dtype (default)
@@ -665,7 +683,9 @@ def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *
     o_sparse = torch.empty((B, H, L, d), dtype=torch.float32, device=dev) if want_o_sparse else None
     shp = _shape(q, prep.block)
     impl_code = _lib.IMPL[impl]
-    ws = _workspace(_lib.lib().ropeslr_attend_workspace_bytes(ctypes_ref(shp), impl_code), dev)
+    ws = workspace
+    if ws is None or ws.numel() < _lib.lib().ropeslr_attend_workspace_bytes(ctypes_ref(shp), impl_code):
+        ws = _workspace(_lib.lib().ropeslr_attend_workspace_bytes(ctypes_ref(shp), impl_code), dev)
     _lib.call("ropeslr_attend_fused", ctypes_ref(shp), q.data_ptr(), prep.k.data_ptr(), prep.v.data_ptr(),
               prep.sel.idx.data_ptr(), prep.sel.kmax, prep.sel.cnt.data_ptr(), _ptr(prep.perm), prep.y_lr.data_ptr(),
               prep.g_logit.data_ptr(), float(params.b_g), params.rms_sparse.data_ptr(), float(settings.rms_eps),
