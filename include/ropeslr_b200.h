@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define ROPESLR_ABI_VERSION 2
+#define ROPESLR_ABI_VERSION 3
 
 typedef enum ropeslr_status {
   ROPESLR_OK = 0,
@@ -75,6 +75,14 @@ typedef struct ropeslr_shape {
   int64_t d;      /* head dim */
   int32_t block;  /* flat block size in tokens (query blocks == key blocks) */
   int32_t dtype;  /* ropeslr_dtype of Q/K/V/X/out/y_lr */
+  /* Query-block range [qb_begin, qb_end) of this call; 0, 0 = every block.
+   * Honoured by the sparse attention (ropeslr_attend_fused, ropeslr_sparse_
+   * attention; tcgen05 path): only the units (head, query block) of the range
+   * run and only their output rows are written, the tensors keeping their
+   * full-length layouts (a rank that shares a head with another rank computes
+   * its half of the query blocks).  The other entry points ignore it. */
+  int32_t qb_begin;
+  int32_t qb_end;
 } ropeslr_shape;
 
 /* Selection rule.  topk > 0: keep the k best blocks (BASELINE configs);
@@ -112,6 +120,10 @@ typedef struct ropeslr_token_args {
    * local columns is NaN or infinite (detected on the gate logits, whose
    * sums every value enters; needs g_logit). */
   uint32_t* nonfinite;
+  /* Grid index of X's row 0.  Nonzero only for ropeslr_gate_logits on a
+   * sequence shard (rows [token_offset, token_offset + L) of the grid, for
+   * the PE coordinates); every other entry point requires 0 and L = the grid. */
+  int64_t token_offset;
 } ropeslr_token_args;
 
 /* ---------------------------------------------------------------- misc */
@@ -210,7 +222,9 @@ int ropeslr_lowrank_branch(const ropeslr_shape* shape, const ropeslr_token_args*
 /* Gate logits alone: g_logit[b,l] = sum over the local columns of
  * x_hat[b,l,c] * w_g[c] (mechanism.py:249-255, 434; bias and sigmoid are
  * applied in the fused epilogue so that head-sharded ranks can all-reduce
- * the partial logits first). */
+ * the partial logits first).  With tok->token_offset the rows are the grid
+ * tokens [token_offset, token_offset + L): a sequence shard's own gate over
+ * all columns (ulysses.py). */
 int ropeslr_gate_logits(const ropeslr_shape* shape, const ropeslr_token_args* tok,
                         float* g_logit, void* stream);
 
@@ -323,6 +337,24 @@ typedef struct ropeslr_host_forward {
 
 size_t ropeslr_forward_host_workspace_bytes(const ropeslr_host_forward* args);
 int ropeslr_forward_host(const ropeslr_host_forward* args, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------- caller helper: segmented row copy (ulysses.py)
+ * The pack and unpack around the sequence <-> head all-to-alls of BASELINE
+ * config 4, one launch each.  segs: DEVICE array of nseg segments, row0
+ * ascending; segment k copies its `rows` rows (row_bytes each, a multiple of
+ * 16, pointers and strides 16-byte aligned) from src to dst and covers the
+ * launch's global rows [row0, row0 + rows); total_rows = the sum. */
+typedef struct ropeslr_row_segment {
+  const void* src;
+  void* dst;
+  int64_t src_stride;  /* bytes between rows */
+  int64_t dst_stride;
+  int64_t rows;
+  int64_t row0;
+  int32_t row_bytes;
+  int32_t pad;
+} ropeslr_row_segment;
+int ropeslr_copy_rows(const ropeslr_row_segment* segs, int32_t nseg, int64_t total_rows, void* stream);
 
 /* ------------------------- caller helpers: the config-4 DiT block (dit.py)
  * Fused token-wise ops around the op, bf16 rows of D columns (D % 8 == 0,

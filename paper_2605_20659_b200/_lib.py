@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 # variant experiments); the default is the in-tree build.
 LIB_PATH = os.environ.get("ROPESLR_LIBRARY") or os.path.join(PKG, "libropeslr_b200.so")
 
-ABI_VERSION = 2  # include/ropeslr_b200.h ROPESLR_ABI_VERSION
+ABI_VERSION = 3  # include/ropeslr_b200.h ROPESLR_ABI_VERSION
 F32, BF16 = 0, 1
 LOWRANK, LINEAR = 0, 1
 NONFINITE_QK, NONFINITE_X = 1, 2
@@ -27,7 +27,8 @@ c_vp = ctypes.c_void_p
 
 
 class Shape(ctypes.Structure):
-    _fields_ = [("B", c_i64), ("H", c_i64), ("L", c_i64), ("d", c_i64), ("block", c_i32), ("dtype", c_i32)]
+    _fields_ = [("B", c_i64), ("H", c_i64), ("L", c_i64), ("d", c_i64), ("block", c_i32), ("dtype", c_i32),
+                ("qb_begin", c_i32), ("qb_end", c_i32)]
 
 
 class SelectParams(ctypes.Structure):
@@ -37,7 +38,8 @@ class SelectParams(ctypes.Structure):
 class TokenArgs(ctypes.Structure):
     _fields_ = [("x", c_vp), ("x_row_stride", c_i64), ("head_offset", c_i64), ("d_model", c_i64),
                 ("grid_t", c_i32), ("grid_h", c_i32), ("grid_w", c_i32), ("use_pe", c_i32),
-                ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp), ("nonfinite", c_vp)]
+                ("pe_t", c_vp), ("pe_x", c_vp), ("pe_y", c_vp), ("alpha", c_vp), ("w_g", c_vp), ("nonfinite", c_vp),
+                ("token_offset", c_i64)]
 
 
 class RopeArgs(ctypes.Structure):
@@ -86,6 +88,7 @@ _SIGNATURES = {
     "ropeslr_select_pooled_workspace_bytes": (c_sz, [P(Shape)]),
     "ropeslr_select_from_pooled": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
                                            c_vp, c_sz, c_vp]),
+    "ropeslr_copy_rows": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "ropeslr_dit_ln_modulate": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_rms_heads": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "ropeslr_dit_gated_residual": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),

@@ -139,11 +139,21 @@ struct Params {
   float* o_sparse;
   int out_H;   // heads per token row of out / y_lr (>= H when a head chunk writes into a wider row)
   int out_h0;  // first head of this call inside that row
+  int qb0;  // query-block range of this call (nq > 0): positions map to units
+  int nq;   // (bh, qb0 + pos % nq), bh = pos / nq; nq == 0: every query block
   int kv_evict_last;
   int debug_mode;  // measurement only: 0 normal; 2 every K/V load reads block 0; 3 no K/V TMA;
                    // 4 no MMAs (fixed-reference kernel: only in a build with -DROPESLR_K2_MEASURE=1)
   long long* trace;  // TRACE
 };
+
+// Unit (bh * nb + qb) at schedule position pos: the longest-first order or a
+// fallback list when given, else the query-block range of the call.
+__device__ __forceinline__ int64_t unit_at(const Params& p, int64_t pos) {
+  if (p.order != nullptr) return p.order[pos];
+  if (p.nq > 0) return (pos / p.nq) * p.nb + p.qb0 + pos % p.nq;
+  return pos;
+}
 
 // Fused output of one row's 32 columns [col0, col0 + 32): the normalised
 // sparse branch O/l * rsqrt(mean + eps) * rms_sparse (ob holds O/l, inv the
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
         uint32_t g = 0, uc = 0;
         for (int64_t pos = blockIdx.x; pos < nunits; pos += gridDim.x, ++uc) {
-          const int64_t u = p.order ? p.order[pos] : pos;
+          const int64_t u = unit_at(p, pos);
           const int bh = static_cast<int>(u / p.nb);
           const int n = p.cnt[u];
           const int32_t* irow = p.idx + u * p.kmax;
@@ -445,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool leader = elect_one_sync();
       uint32_t g = 0, uc = 0;
       for (int64_t pos = blockIdx.x; pos < nunits; pos += gridDim.x, ++uc) {
-        const int64_t u = p.order ? p.order[pos] : pos;
+        const int64_t u = unit_at(p, pos);
         const int n = p.cnt[u];
         mbar_wait(&bars[Bx::Q_FULL], uc & 1);
         tc_fence_after();
@@ -510,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool rows_live = BLK >= M || (warp & 3) * 32 < BLK;
     uint32_t g = 0, uc = 0;
     for (int64_t pos = blockIdx.x; pos < nunits; pos += gridDim.x, ++uc) {
-      const int64_t u = p.order ? p.order[pos] : pos;
+      const int64_t u = unit_at(p, pos);
       const int bh = static_cast<int>(u / p.nb);
       const int qb = static_cast<int>(u % p.nb);
       const int n = p.cnt[u];
@@ -779,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int empty = is_k ? Bx::K_EMPTY : Bx::V_EMPTY;
         uint32_t g = 0, uc = 0;
         for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
-          const int64_t u = p.order ? p.order[pos] : pos;
+          const int64_t u = unit_at(p, pos);
           const int bh = static_cast<int>(u / p.nb);
           const int n = p.cnt[u];
           const int nt = (n + TPB - 1) / TPB;
@@ -830,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool leader = elect_one_sync();
       uint32_t g = 0, uc = 0;
       for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
-        const int64_t u = p.order ? p.order[pos] : pos;
+        const int64_t u = unit_at(p, pos);
         const int n = (p.cnt[u] + TPB - 1) / TPB;  // tiles
         const uint32_t tQ = tmem + fx::Q_COL + (uc & 1) * (D / 2);
         mbar_wait(&bars[Bx::QT_FULL], uc & 1);
@@ -904,7 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // QK^T: column c holds d = 2c, 2c+1), publish its part of the probe dot
     // product, free the shared-memory tile
     auto prep = [&](int64_t pos, uint32_t uc) {
-      const int64_t u = p.order ? p.order[pos] : pos;
+      const int64_t u = unit_at(p, pos);
       const int bh = static_cast<int>(u / p.nb);
       const int32_t* irow = p.idx + u * p.kmax;
       mbar_wait(&bars[Bx::Q_FULL], uc & 1);
@@ -942,7 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t g = 0, uc = 0;
     if (blockIdx.x < p.num_units) prep(blockIdx.x, 0);
     for (int64_t pos = blockIdx.x; pos < p.num_units; pos += gridDim.x, ++uc) {
-      const int64_t u = p.order ? p.order[pos] : pos;
+      const int64_t u = unit_at(p, pos);
       const int bh = static_cast<int>(u / p.nb);
       const int qb = static_cast<int>(u % p.nb);
       const int nblk = p.cnt[u];
@@ -1170,11 +1180,13 @@ template <int BLK, int KB>
 static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
                         int* fallback, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
-  // fallback area: [unit_flag: num_units][count: 1][list: num_units]
+  // fallback area: [unit_flag: all B*H*nb units][count: 1][list]; flags are
+  // indexed by unit, which a query-block range does not renumber
+  const int64_t nu_all = BH * prm.nb;
   prm.unit_flag = fallback;
-  prm.flag_count = fallback + prm.num_units;
-  prm.flag_list = fallback + prm.num_units + 1;
-  if (cudaMemsetAsync(fallback, 0, (prm.num_units + 1) * sizeof(int), st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+  prm.flag_count = fallback + nu_all;
+  prm.flag_list = fallback + nu_all + 1;
+  if (cudaMemsetAsync(fallback, 0, (nu_all + 1) * sizeof(int), st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
   prm.kmat = static_cast<const __nv_bfloat16*>(k);
   CUtensorMap mq, mk, mv;
   if (!make_map(&mq, q, BH, s->L, KB) || !make_map(&mk, k, BH, s->L, KB) || !make_map(&mv, v, BH, s->L, KB))
@@ -1189,6 +1201,7 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   // the running-max kernel over the flagged units (usually none: its CTAs
   // read a zero count and retire)
   Params fb = prm;
+  fb.nq = 0;
   fb.order = prm.flag_list;
   fb.num_units_dev = prm.flag_count;
   fb.unit_flag = nullptr;
@@ -1220,6 +1233,10 @@ static int check_attn_args(const ropeslr_shape* s, const void* q, const void* k,
   if (!q || !k || !v || !idx || !cnt) return ROPESLR_ERR_NULL;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v)) return ROPESLR_ERR_ALIGN;
   if (kmax < 1) return ROPESLR_ERR_SHAPE;
+  if (s->qb_begin != 0 || s->qb_end != 0) {
+    const int64_t nb = ceil_div(s->L, s->block);
+    if (s->qb_begin < 0 || s->qb_end <= s->qb_begin || s->qb_end > nb) return ROPESLR_ERR_SHAPE;
+  }
   if (!device_is_sm100()) return ROPESLR_ERR_ARCH;
   return ROPESLR_OK;
 }
@@ -1234,7 +1251,7 @@ static int resolve_impl(const ropeslr_shape* s, int impl) {
 // workspace of the fixed-reference path: [schedule: NU][fallback: 2 NU + 1]
 static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                                  const tc::Params& prm, void* ws, cudaStream_t st) {
-  int* fallback = static_cast<int*>(ws) + prm.num_units;
+  int* fallback = static_cast<int*>(ws) + s->B * s->H * prm.nb;
   if (s->block == 128) return tc::launch_fixed<128, 128>(s, q, k, v, prm, fallback, st);
   // block 64: two selected blocks per 128-key tile unless ROPESLR_PAIR64=0
   if (!tuning().pair64) return tc::launch_fixed<64, 64>(s, q, k, v, prm, fallback, st);
@@ -1260,6 +1277,11 @@ static tc::Params base_params(const ropeslr_shape* s, const int32_t* idx, int km
   prm.H = static_cast<int>(s->H);
   prm.L = s->L;
   prm.num_units = s->B * s->H * prm.nb;
+  if (s->qb_end > s->qb_begin) {  // a query-block range (validated by check_attn_args)
+    prm.qb0 = s->qb_begin;
+    prm.nq = s->qb_end - s->qb_begin;
+    prm.num_units = s->B * s->H * prm.nq;
+  }
   prm.perm = perm;
   prm.order = nullptr;
   prm.kmat = nullptr;
@@ -1302,8 +1324,10 @@ extern "C" int ropeslr_sparse_attention(const ropeslr_shape* s, const void* q, c
   const int which = resolve_impl(s, impl);
   if (which < 0) return ROPESLR_ERR_VALUE;
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  if (which == ROPESLR_IMPL_SIMT)
+  if (which == ROPESLR_IMPL_SIMT) {
+    if (s->qb_end > s->qb_begin) return ROPESLR_ERR_SHAPE;  // query-block ranges: tcgen05 path only
     return launch_sparse_attention_simt(s, q, k, v, idx, kmax, cnt, row_perm, o_sparse, cs);
+  }
   tc::Params prm = base_params(s, idx, kmax, cnt, row_perm, cs);
   prm.o_sparse = o_sparse;
   return launch_tc_dispatch(s, q, k, v, prm, cs);
@@ -1319,7 +1343,7 @@ static int64_t num_units_of(const ropeslr_shape* s) { return s->B * s->H * ceil_
 // 19-20% faster with the fixed-reference kernel; on uniform top-k counts it
 // is neutral.
 static int schedule_units(const ropeslr_shape* s, const int32_t* cnt, tc::Params& prm, void* ws, cudaStream_t cs) {
-  if (!tuning().schedule || prm.nb > kMaxScheduledBlocks) return ROPESLR_OK;
+  if (!tuning().schedule || prm.nq > 0 || prm.nb > kMaxScheduledBlocks) return ROPESLR_OK;
   // top-k rows (index rows narrower than nb) all hold k blocks: balanced by
   // construction, so the identity order is as good and the ranking is skipped
   if (prm.kmax < prm.nb) return ROPESLR_OK;
@@ -1395,6 +1419,7 @@ extern "C" int ropeslr_attend_fused(const ropeslr_shape* s, const void* q, const
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   if (o_sparse && !aligned16(o_sparse)) return ROPESLR_ERR_ALIGN;
   if (which == ROPESLR_IMPL_SIMT) {
+    if (s->qb_end > s->qb_begin) return ROPESLR_ERR_SHAPE;  // query-block ranges: tcgen05 path only
     if (!aligned16(y_lr) || !aligned16(out)) return ROPESLR_ERR_ALIGN;
     float* osp = o_sparse;
     if (osp == nullptr) {

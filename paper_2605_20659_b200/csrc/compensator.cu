@@ -22,6 +22,7 @@ namespace ropeslr {
 
 struct TokenCtx {
   int64_t L, x_row_stride, head_offset, d_model;
+  int64_t tok0;  // grid index of local token 0 (the PE coordinates)
   int grid_h, grid_w, use_pe;
   const float *pe_t, *pe_x, *pe_y, *alpha, *w_g;
 };
@@ -33,7 +34,8 @@ __device__ __forceinline__ void xhat4(const TokenCtx& c, const T* xrow, int64_t 
   for (int i = 0; i < 4; ++i) o[i] = to_f(xrow[lc + i]);
   if (c.use_pe) {
     const int64_t hw = static_cast<int64_t>(c.grid_h) * c.grid_w;
-    const int64_t tt = tok / hw, rem = tok % hw, xx = rem / c.grid_w, yy = rem % c.grid_w;
+    const int64_t gt = tok + c.tok0;
+    const int64_t tt = gt / hw, rem = gt % hw, xx = rem / c.grid_w, yy = rem % c.grid_w;
     const float* pt = c.pe_t + tt * c.d_model + gc;
     const float* px = c.pe_x + xx * c.d_model + gc;
     const float* py = c.pe_y + yy * c.d_model + gc;
@@ -320,6 +322,7 @@ int launch_lowrank_tc(const ropeslr_shape* s, const ropeslr_token_args* t, const
 static TokenCtx make_ctx(const ropeslr_shape* s, const ropeslr_token_args* t) {
   TokenCtx c;
   c.L = s->L;
+  c.tok0 = t->token_offset;
   c.x_row_stride = t->x_row_stride;
   c.head_offset = t->head_offset;
   c.d_model = t->d_model;
@@ -334,10 +337,17 @@ static TokenCtx make_ctx(const ropeslr_shape* s, const ropeslr_token_args* t) {
   return c;
 }
 
-static int check_token_args(const ropeslr_shape* s, const ropeslr_token_args* t) {
+// token_range: the call covers grid tokens [token_offset, token_offset + L)
+// (the gate of a sequence shard); otherwise the whole grid, offset 0.
+static int check_token_args(const ropeslr_shape* s, const ropeslr_token_args* t, bool token_range = false) {
   if (!t || !t->x || !t->w_g) return ROPESLR_ERR_NULL;
   if (t->use_pe && (!t->pe_t || !t->pe_x || !t->pe_y || !t->alpha)) return ROPESLR_ERR_NULL;
-  if (static_cast<int64_t>(t->grid_t) * t->grid_h * t->grid_w != s->L) return ROPESLR_ERR_SHAPE;
+  const int64_t gsize = static_cast<int64_t>(t->grid_t) * t->grid_h * t->grid_w;
+  if (token_range) {
+    if (t->token_offset < 0 || t->token_offset + s->L > gsize) return ROPESLR_ERR_SHAPE;
+  } else if (gsize != s->L || t->token_offset != 0) {
+    return ROPESLR_ERR_SHAPE;
+  }
   if (t->grid_t < 1 || t->grid_h < 1 || t->grid_w < 1) return ROPESLR_ERR_SHAPE;
   if (t->head_offset < 0 || (t->head_offset + s->H) * s->d > t->d_model) return ROPESLR_ERR_SHAPE;
   if (t->x_row_stride < s->H * s->d || t->x_row_stride % 4) return ROPESLR_ERR_SHAPE;
@@ -417,7 +427,7 @@ extern "C" int ropeslr_gate_logits(const ropeslr_shape* s, const ropeslr_token_a
                                    void* stream) {
   int st = check_shape(s);
   if (st) return st;
-  if ((st = check_token_args(s, t))) return st;
+  if ((st = check_token_args(s, t, true))) return st;
   if (!g_logit) return ROPESLR_ERR_NULL;
   if (s->d % 4) return ROPESLR_ERR_SHAPE;
   dim3 grid(static_cast<unsigned>(ceil_div(s->L, 8)), static_cast<unsigned>(s->B));

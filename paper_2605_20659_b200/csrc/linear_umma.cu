@@ -834,6 +834,7 @@ extern "C" int ropeslr_linear_tables(const ropeslr_shape* s, const ropeslr_token
                                      void* stream) {
   if (!s || !t || !tables) return ROPESLR_ERR_NULL;
   if (!linear_pe_eligible(s, t)) return ROPESLR_ERR_SHAPE;
+  if (t->token_offset != 0) return ROPESLR_ERR_SHAPE;
   if (tables_bytes < ropeslr_linear_tables_bytes(s, t)) return ROPESLR_ERR_WORKSPACE;
   if (!t->use_pe) return ROPESLR_OK;  // no PE: the tables are not read
   if (!w_q || !w_k || !w_v || !t->pe_t || !t->pe_x || !t->pe_y || !t->alpha || !t->w_g) return ROPESLR_ERR_NULL;
@@ -868,7 +869,8 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
     return ROPESLR_ERR_NULL;
   if (s->B < 1 || s->H < 1 || s->L < 1) return ROPESLR_ERR_SHAPE;
   if (!linear_pe_eligible(s, t)) return ROPESLR_ERR_SHAPE;
-  if (static_cast<int64_t>(t->grid_t) * t->grid_h * t->grid_w != s->L) return ROPESLR_ERR_SHAPE;
+  if (static_cast<int64_t>(t->grid_t) * t->grid_h * t->grid_w != s->L || t->token_offset != 0)
+    return ROPESLR_ERR_SHAPE;
   if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
   if (!aligned16(q_lin) || !aligned16(k_lin) || !aligned16(v_lin) || !aligned16(tables) || !aligned32(y_lr) ||
       !aligned16(t->x) || t->x_row_stride % 8 || (o_lr && !aligned16(o_lr)) || (state && !aligned16(state)))

@@ -441,7 +441,8 @@ def block_sparse_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, se
 
 
 def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: Optional[PETables], use_pe: bool,
-                head_offset: int, H_local: int, d: int, nonfinite: Optional[torch.Tensor] = None) -> _lib.TokenArgs:
+                head_offset: int, H_local: int, d: int, nonfinite: Optional[torch.Tensor] = None,
+                check_grid: bool = True) -> _lib.TokenArgs:
     if x.dim() != 3:
         raise ValueError(f"expected X of shape [B, L, H*d], got {tuple(x.shape)}")
     B, L, W = x.shape
@@ -449,7 +450,7 @@ def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: O
         raise ValueError(f"X has {W} columns, expected {H_local * d}")
     if x.stride(2) != 1 or x.stride(0) != L * x.stride(1):
         raise ValueError("X rows must be unit-stride with batch stride L * row stride")
-    if grid.size != L:
+    if check_grid and grid.size != L:
         raise ValueError(f"grid size {grid.size} != sequence length {L}")
     if params.d_model < (head_offset + H_local) * d:
         raise ValueError("alpha / w_g are narrower than the head slice")
@@ -661,11 +662,14 @@ def fallback_units(prep: Prepared, workspace: torch.Tensor) -> int:
 
 def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *, impl: str = "auto",
            want_o_sparse: bool = False, out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None,
-           workspace: Optional[torch.Tensor] = None):
+           workspace: Optional[torch.Tensor] = None, q_blocks: Optional[Tuple[int, int]] = None):
     """K2 + K4: block-sparse attention with the fused RMSNorm / gate / combine
     epilogue (mechanism.py:321-326, 435-451).  Returns (out [B, L, H*d],
     o_sparse [B, H, L, d] float32 or None).  out_dtype: Q's dtype (default)
-    or torch.float32 (the fused result before any bf16 rounding)."""
+    or torch.float32 (the fused result before any bf16 rounding).
+    ``q_blocks=(qb0, qb1)`` computes only those query blocks of every head
+    (their output rows; the rest of ``out`` is left as it was): a share of a
+    head for a sequence-parallel rank (ulysses.py)."""
     q = prep.q
     B, H, L, d = q.shape
     dev = q.device
@@ -682,6 +686,14 @@ def attend(prep: Prepared, params: MechanismParams, settings: ForwardSettings, *
             raise ValueError("out must be a contiguous tensor of out_dtype on Q's device")
     o_sparse = torch.empty((B, H, L, d), dtype=torch.float32, device=dev) if want_o_sparse else None
     shp = _shape(q, prep.block)
+    if q_blocks is not None:
+        nb = -(-L // prep.block)
+        qb0, qb1 = (int(b) for b in q_blocks)
+        if not (0 <= qb0 < qb1 <= nb):
+            raise ValueError(f"q_blocks must satisfy 0 <= qb0 < qb1 <= {nb}, got {q_blocks}")
+        if prep.perm is not None:
+            raise ValueError("q_blocks takes flat blocks")
+        shp.qb_begin, shp.qb_end = qb0, qb1
     impl_code = _lib.IMPL[impl]
     ws = workspace
     if ws is None or ws.numel() < _lib.lib().ropeslr_attend_workspace_bytes(ctypes_ref(shp), impl_code):
@@ -698,7 +710,8 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
             lin_proj: Optional[Sequence[torch.Tensor]] = None, trace: bool = False, impl: str = "auto",
             head_offset: int = 0, gate_reduce: Optional[Callable[[torch.Tensor], None]] = None,
             rope: Optional[RopeConfig] = None, check_finite: bool = False,
-            out_dtype: Optional[torch.dtype] = None, lin_weights: Optional[Sequence[torch.Tensor]] = None):
+            out_dtype: Optional[torch.dtype] = None, lin_weights: Optional[Sequence[torch.Tensor]] = None,
+            q_blocks: Optional[Tuple[int, int]] = None, out: Optional[torch.Tensor] = None):
     """RoPeSLR forward (mechanism.py:491-512, Algorithm 1).
 
     q, k, v: post-RoPE [B, H, L, d] (bf16 or f32); x: token features
@@ -718,6 +731,9 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
     [H, D_total, d]) they are x W and the PE part is added in the kernels
     (see compensator_branch), else they are x_hat W.
 
+    ``q_blocks=(qb0, qb1)`` runs the sparse attention for those query
+    blocks only (rows outside are left as ``out`` holds them).
+
     ``out_dtype=torch.float32`` returns the fused output in float32 (the
     epilogue's result before the bf16 rounding of a bf16 output).
 
@@ -730,7 +746,8 @@ def forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Tensor, 
         raise_nonfinite(flag)
     if gate_reduce is not None:
         gate_reduce(prep.g_logit)
-    out, o_sparse = attend(prep, params, settings, impl=impl, want_o_sparse=trace, out_dtype=out_dtype)
+    out, o_sparse = attend(prep, params, settings, impl=impl, want_o_sparse=trace, out_dtype=out_dtype,
+                           q_blocks=q_blocks, out=out)
     if not trace:
         return out
     L = q.shape[2]

@@ -48,7 +48,7 @@ def test_host_functions():
     from paper_2605_20659_b200 import _lib
 
     lib = P.lib()
-    assert lib.ropeslr_abi_version() == 2
+    assert lib.ropeslr_abi_version() == 3
     assert lib.ropeslr_num_blocks(118800, 128) == 929
     assert lib.ropeslr_num_blocks(32760, 64) == 512
     assert lib.ropeslr_num_blocks(0, 64) == 0

@@ -415,3 +415,26 @@ def test_golden_linear_pe_in_kernel():
     G.assert_close(tr.o_lowrank[0].cpu().numpy(), g["ref_o_lowrank"], "bf16", "linear pe o_lowrank")
     G.assert_close(tr.g[0].cpu().numpy(), g["ref_g"], "bf16", "linear pe gate")
     G.assert_close_bf16_store(tr.output[0].float().cpu().numpy(), g["ref_output"], "linear pe output")
+
+
+@pytest.mark.parametrize("block,rule", [(64, dict(topk=5)), (128, dict(topk=3)), (64, dict(keep=0.6))])
+def test_query_block_range(block, rule):
+    """q_blocks=(qb0, qb1): only those query blocks run (the share of a head a
+    sequence-parallel rank computes); their rows equal the full call's bit for
+    bit, every other row keeps the caller's contents."""
+    import paper_2605_20659_b200 as P
+
+    q, k, v, x, params, pe, grid = _small((3, 16, 40), H=3)  # L = 1920, ragged at block 128
+    st = P.ForwardSettings(P.SparseSettings(block=block, **rule))
+    full = P.forward(q, k, v, x, grid, params, st, pe)
+    B, H, L, d = q.shape
+    nb = -(-L // block)
+    for qb0, qb1 in ((0, 1), (3, nb), (nb // 3, 2 * nb // 3)):
+        out = torch.full((B, L, H * d), 7.0, dtype=q.dtype, device=q.device)
+        got = P.forward(q, k, v, x, grid, params, st, pe, q_blocks=(qb0, qb1), out=out)
+        torch.cuda.synchronize()
+        r0, r1 = qb0 * block, min(L, qb1 * block)
+        assert torch.equal(got[:, r0:r1], full[:, r0:r1])
+        assert bool((got[:, :r0] == 7.0).all()) and bool((got[:, r1:] == 7.0).all())
+    with pytest.raises(ValueError):
+        P.forward(q, k, v, x, grid, params, st, pe, q_blocks=(2, 2))
