@@ -399,6 +399,21 @@ int ropeslr_stage1_xgrad(int64_t H, int64_t L, int64_t d, const float* dxh, cons
 int ropeslr_stage1_reduce(const float* parts, int32_t outer, int32_t nparts, int32_t groups, int32_t width, float* out,
                           void* stream);
 
+/* The step's float32 GEMMs on the tcgen05 tensor cores, float32-grade (each
+ * operand split into bf16 hi + lo, three MMAs per product; csrc/stage1_gemm.cu):
+ *   gemm_rows: C[h] = epi(A[h] B[h]), A [H, L, K], B [H, K, N] ([H, N, K] when
+ *              b_trans), C [H, L, N], K, N in {64, 128}; epi 0 none,
+ *              1 sigmoid, 2 times aux (1 - aux) with aux [H, L, N];
+ *   gemm_gram: out[h] (+)= A[h]^T B[h] summed over L, A [H, L, 128],
+ *              B [H, L, N], N in {64, 128}; out [H, 128, N], or [H, N, 128]
+ *              when transpose; fixed-order reduction over token chunks. */
+int ropeslr_stage1_gemm_rows(int64_t H, int64_t L, int32_t K, int32_t N, const float* A, const float* B,
+                             int32_t b_trans, int32_t epi, const float* aux, float* C, void* stream);
+size_t ropeslr_stage1_gram_workspace_bytes(int64_t H, int64_t L, int32_t N);
+int ropeslr_stage1_gemm_gram(int64_t H, int64_t L, int32_t N, const float* A, const float* B, float* out,
+                             int32_t transpose, int32_t accumulate, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

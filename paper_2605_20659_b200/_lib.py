@@ -102,6 +102,9 @@ _SIGNATURES = {
     "ropeslr_stage1_dsig": (c_i32, [c_vp, c_vp, c_i64, c_vp]),
     "ropeslr_stage1_xgrad": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ropeslr_stage1_reduce": (c_i32, [c_vp, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "ropeslr_stage1_gemm_rows": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "ropeslr_stage1_gram_workspace_bytes": (c_sz, [c_i64, c_i64, c_i32]),
+    "ropeslr_stage1_gemm_gram": (c_i32, [c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_sz, c_vp]),
     "ropeslr_rope_pool_workspace_bytes": (c_sz, [P(RopeArgs)]),
     "ropeslr_rope_pool": (c_i32, [P(Shape), P(RopeArgs), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_forward_host_workspace_bytes": (c_sz, [P(HostForward)]),

@@ -448,7 +448,7 @@ def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: O
     B, L, W = x.shape
     if W != H_local * d:
         raise ValueError(f"X has {W} columns, expected {H_local * d}")
-    if x.stride(2) != 1 or x.stride(0) != L * x.stride(1):
+    if x.stride(2) != 1 or (B > 1 and x.stride(0) != L * x.stride(1)):
         raise ValueError("X rows must be unit-stride with batch stride L * row stride")
     if check_grid and grid.size != L:
         raise ValueError(f"grid size {grid.size} != sequence length {L}")
@@ -836,7 +836,7 @@ def forward_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, x: torch.Ten
     B, H, L, d = q.shape
     if x.dim() != 3 or x.shape[:2] != (B, L) or x.shape[2] < H * d or x.stride(2) != 1:
         raise ValueError(f"expected host X [B, L, >= H*d] with unit column stride, got {tuple(x.shape)}")
-    if x.stride(0) != L * x.stride(1):
+    if B > 1 and x.stride(0) != L * x.stride(1):
         raise ValueError("X rows must have batch stride L * row stride")
     if params.d_h != d or params.w_a.shape[0] != H:
         raise ValueError("parameters do not match the head count / head dim")

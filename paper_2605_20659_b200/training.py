@@ -95,6 +95,34 @@ def _at_b(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return torch.bmm(a2.transpose(1, 2), b2).view(H, S, m, b.shape[2]).sum(1)
 
 
+def _tc_gemms(d: int, r: int) -> bool:
+    """The tcgen05 float32-grade GEMMs (csrc/stage1_gemm.cu) cover d = 128
+    with r in {64, 128}; other shapes use cuBLAS float32."""
+    return d == 128 and r in (64, 128)
+
+
+def _rows(A: torch.Tensor, B: torch.Tensor, *, b_trans: bool = False, epi: int = 0,
+          aux: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """C[h] = epi(A[h] B[h]) on the tensor cores (ropeslr_stage1_gemm_rows)."""
+    H, L, K = A.shape
+    N = B.shape[1] if b_trans else B.shape[2]
+    C = torch.empty((H, L, N), dtype=torch.float32, device=A.device)
+    _lib.call("ropeslr_stage1_gemm_rows", H, L, K, N, A.data_ptr(), B.contiguous().data_ptr(), int(b_trans), epi,
+              None if aux is None else aux.data_ptr(), C.data_ptr(), torch.cuda.current_stream(A.device).cuda_stream)
+    return C
+
+
+def _gram_into(out: torch.Tensor, A: torch.Tensor, B: torch.Tensor, transpose: bool) -> None:
+    """out[h] += A[h]^T B[h] (or its transpose) on the tensor cores
+    (ropeslr_stage1_gemm_gram)."""
+    H, L, _ = A.shape
+    N = B.shape[2]
+    ws = torch.empty(max(16, _lib.lib().ropeslr_stage1_gram_workspace_bytes(H, L, N)), dtype=torch.uint8,
+                     device=A.device)
+    _lib.call("ropeslr_stage1_gemm_gram", H, L, N, A.data_ptr(), B.data_ptr(), out.data_ptr(), int(transpose), 1,
+              ws.data_ptr(), ws.numel(), torch.cuda.current_stream(A.device).cuda_stream)
+
+
 def _rms(o, scale, eps):
     inv = torch.rsqrt((o * o).mean(-1, keepdim=True) + eps)
     u = o * inv
@@ -147,8 +175,13 @@ def _loss_and_grads_fused(prepared, params, settings, pe_dense):
         pe_ptr = pe_dense.data_ptr() if use_pe else None
         _lib.call("ropeslr_stage1_pre", H, L, d, s.x.data_ptr(), pe_ptr, alpha.data_ptr(), w_g.data_ptr(),
                   float(params.b_g), xh.data_ptr(), gpart.data_ptr(), g.data_ptr(), st)
-        h1 = torch.sigmoid_(torch.bmm(xh, w_a))                      # [H, L, r]
-        dz2 = torch.bmm(h1, w_b)                                      # z2 in, d z2 out (in place)
+        tc = _tc_gemms(d, r)
+        if tc:
+            h1 = _rows(xh, w_a, epi=1)                                    # sigma(x_hat W_A) [H, L, r]
+            dz2 = _rows(h1, w_b)                                          # z2 in, d z2 out (in place)
+        else:
+            h1 = torch.sigmoid_(torch.bmm(xh, w_a))
+            dz2 = torch.bmm(h1, w_b)
         nb_rows = lib.ropeslr_stage1_rows_blocks(H, L)
         red = torch.empty((nb_rows, 2, d), dtype=torch.float32, device=dev)
         loss_part = torch.empty((nb_rows,), dtype=torch.float64, device=dev)
@@ -163,11 +196,17 @@ def _loss_and_grads_fused(prepared, params, settings, pe_dense):
                   bg_part.data_ptr(), st)
         acc[0] += loss_part.sum() / (H * L * d * n)
         acc[1] += bg_part.sum()
-        grads["w_b"] += _at_b(h1, dz2)
-        dz1 = torch.bmm(dz2, w_b.transpose(1, 2))                     # [H, L, r]
-        _lib.call("ropeslr_stage1_dsig", dz1.data_ptr(), h1.data_ptr(), dz1.numel(), st)
-        grads["w_a"] += _at_b(xh, dz1)
-        dxh = torch.bmm(dz1, w_a.transpose(1, 2)) if use_pe else xh   # [H, L, d] (read only with PE)
+        if tc:
+            _gram_into(grads["w_b"], dz2, h1, transpose=True)            # (dz2^T h1)^T = h1^T dz2
+            dz1 = _rows(dz2, w_b, b_trans=True, epi=2, aux=h1)            # (dz2 W_B^T) h1 (1 - h1)
+            _gram_into(grads["w_a"], xh, dz1, transpose=False)            # x_hat^T dz1
+            dxh = _rows(dz1, w_a, b_trans=True) if use_pe else xh         # dz1 W_A^T (read only with PE)
+        else:
+            grads["w_b"] += _at_b(h1, dz2)
+            dz1 = torch.bmm(dz2, w_b.transpose(1, 2))
+            _lib.call("ropeslr_stage1_dsig", dz1.data_ptr(), h1.data_ptr(), dz1.numel(), st)
+            grads["w_a"] += _at_b(xh, dz1)
+            dxh = torch.bmm(dz1, w_a.transpose(1, 2)) if use_pe else xh
         nb_x = lib.ropeslr_stage1_xgrad_blocks(H, L)
         xred = torch.empty((H, nb_x, 2, d), dtype=torch.float32, device=dev)
         _lib.call("ropeslr_stage1_xgrad", H, L, d, dxh.data_ptr(), xh.data_ptr(), pe_ptr, dzg.data_ptr(),

@@ -113,7 +113,7 @@ class Segments:
         from . import _lib
 
         dev = self.views[0][0].device
-        rows = torch.empty((len(self.views), 8), dtype=torch.int64)
+        rows = torch.empty((len(self.views), 7), dtype=torch.int64)  # ropeslr_row_segment: 56 bytes
         row0 = 0
         for i, (s, d) in enumerate(self.views):
             es = s.element_size()
@@ -130,7 +130,6 @@ class Segments:
             rows[i, 4] = s.shape[0]
             rows[i, 5] = row0
             rows[i, 6] = row_bytes  # int32 row_bytes, int32 pad (little endian)
-            rows[i, 7] = 0
             row0 += s.shape[0]
         table = rows.pin_memory().to(dev, non_blocking=True)
         stream = torch.cuda.current_stream(dev)

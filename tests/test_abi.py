@@ -190,3 +190,18 @@ def test_stage1_ops_reject_bad_arguments_without_a_gpu():
     assert lib.ropeslr_stage1_rows(2, 0, 64, 16, 16, 16, 16, 16, 16, f(1e-6), f(1.0), 16, 16, 16, None) == -1
     assert lib.ropeslr_stage1_dsig(18, 16, 8, None) == -3
     assert lib.ropeslr_stage1_reduce(16, 1, 0, 2, 64, 16, None) == -1
+
+
+def test_row_segment_struct_layout():
+    """ulysses.Segments packs ropeslr_row_segment as seven int64 words: the
+    header's struct is 56 bytes with row_bytes in the low half of word 6."""
+    import ctypes
+
+    class Seg(ctypes.Structure):
+        _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("src_stride", ctypes.c_int64),
+                    ("dst_stride", ctypes.c_int64), ("rows", ctypes.c_int64), ("row0", ctypes.c_int64),
+                    ("row_bytes", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+    assert ctypes.sizeof(Seg) == 56 and Seg.row_bytes.offset == 48
+    src = open(os.path.join(REPO, "paper_2605_20659_b200", "ulysses.py")).read()
+    assert "dtype=torch.int64)  # ropeslr_row_segment: 56 bytes" in src and "(len(self.views), 7)" in src

@@ -90,3 +90,38 @@ def test_stage1_fused_equals_composed(use_pe, d, split, r):
         scale = float(gc[name].abs().max()) or 1.0
         assert float((gf[name] - gc[name]).abs().max()) <= 2e-5 * scale, name
     assert abs(gf["b_g"] - gc["b_g"]) <= 2e-5 * max(abs(gc["b_g"]), 1e-9)
+
+
+@pytest.mark.parametrize("K,N", [(128, 64), (64, 128), (128, 128)])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_stage1_tensor_core_gemms_float32_grade(K, N, epi):
+    """The tcgen05 GEMMs of the step (bf16 hi + lo split, three MMAs): rows
+    C = epi(A B) and gram A^T B against float64, within 2e-5 relative (float32
+    grade, far inside the 2e-4 gradient bar); ragged L."""
+    from paper_2605_20659_b200 import training as T
+
+    g = torch.Generator(device="cuda").manual_seed(K + N + epi)
+    H, L = 3, 1000
+    A = torch.randn((H, L, K), generator=g, device="cuda")
+    B = torch.randn((H, K, N), generator=g, device="cuda") / K ** 0.5
+    aux = torch.rand((H, L, N), generator=g, device="cuda")
+    got = T._rows(A, B, epi=epi, aux=aux if epi == 2 else None)
+    want = torch.bmm(A.double(), B.double())
+    if epi == 1:
+        want = torch.sigmoid(want)
+    elif epi == 2:
+        want = want * aux.double() * (1 - aux.double())
+    rel = ((got.double() - want).abs().max() / want.abs().max()).item()
+    assert rel < 2e-5, rel
+    got_t = T._rows(A, B.transpose(1, 2).contiguous(), b_trans=True)
+    rel = ((got_t.double() - torch.bmm(A.double(), B.double())).abs().max() / want.abs().max()).item()
+    assert rel < 2e-5, rel
+    if K == 128:
+        Bt = torch.randn((H, L, N), generator=g, device="cuda")
+        out = torch.zeros((H, 128, N), device="cuda")
+        T._gram_into(out, A, Bt, transpose=False)
+        ref = torch.bmm(A.double().transpose(1, 2), Bt.double())
+        assert ((out.double() - ref).abs().max() / ref.abs().max()).item() < 2e-5
+        out_t = torch.ones((H, N, 128), device="cuda")
+        T._gram_into(out_t, A, Bt, transpose=True)
+        assert ((out_t.double() - 1 - ref.transpose(1, 2)).abs().max() / ref.abs().max()).item() < 2e-5
