@@ -828,7 +828,8 @@ def run_train(args, local_rank):
             "data": "synthetic (seeded inputs of config 1, random target)",
             "config": {"workload": cfg["name"] + "_stage1", "samples": 1, "lr": lr},
             "sparse_branch_cache_ms": cache_ms, "loss_first": losses[0], "loss_last": losses[-1],
-            "note": "per-step math is float32 cuBLAS GEMMs + the fused row kernels of csrc/stage1.cu (training.py); "
+            "note": "per-step math: the six GEMMs on tcgen05 with float32-grade bf16 hi+lo splits "
+                    "(csrc/stage1_gemm.cu) + the fused row kernels of csrc/stage1.cu (training.py), no cuBLAS; "
                     "the loss is read back every step, as the reference trainer does"}
     print(json.dumps(line), flush=True)
 

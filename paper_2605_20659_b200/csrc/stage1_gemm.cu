@@ -65,17 +65,28 @@ __device__ __forceinline__ void load8(const float* p, bool valid, float* f) {
 }
 
 // Convert a [128 x C] float32 tile (rows row0.., row stride C, rows >= nrows
-// zero) into swizzled bf16 hi / lo tiles; `nthr` threads, thread t.
-template <int C>
+// zero) into swizzled bf16 hi / lo tiles; NT threads, thread t.  All of a
+// thread's loads are issued before the conversions, so a tile's bytes are in
+// flight at once.
+template <int C, int NT>
 __device__ __forceinline__ void convert_tile(const float* src, int64_t row0, int64_t nrows, uint8_t* hi, uint8_t* lo,
-                                             int t, int nthr) {
-  constexpr int CH = C / 8;  // chunks per row
-  for (int e = t; e < M * CH; e += nthr) {
+                                             int t) {
+  constexpr int CH = C / 8;             // chunks per row
+  constexpr int PER = M * CH / NT;      // chunks per thread
+  static_assert(M * CH % NT == 0, "tile chunks split evenly");
+  float f[PER][8];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = t + i * NT;
     const int r = e / CH, c = e % CH;
-    float f[8];
-    load8(src + (row0 + r) * C + c * 8, row0 + r < nrows, f);
+    load8(src + (row0 + r) * C + c * 8, row0 + r < nrows, f[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int e = t + i * NT;
+    const int r = e / CH, c = e % CH;
     uint4 h, l;
-    split8(f, h, l);
+    split8(f[i], h, l);
     const uint32_t off = sw_off(M, r, c);
     *reinterpret_cast<uint4*>(hi + off) = h;
     *reinterpret_cast<uint4*>(lo + off) = l;
@@ -174,8 +185,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
         }
         cur_h = h;
       }
-      convert_tile<K>(a.A + static_cast<int64_t>(h) * a.L * K, static_cast<int64_t>(tile) * M, a.L,
-                      sA + s * 2 * Lay::A_BYTES, sA + s * 2 * Lay::A_BYTES + Lay::A_BYTES, threadIdx.x, kConv);
+      convert_tile<K, kConv>(a.A + static_cast<int64_t>(h) * a.L * K, static_cast<int64_t>(tile) * M, a.L,
+                             sA + s * 2 * Lay::A_BYTES, sA + s * 2 * Lay::A_BYTES + Lay::A_BYTES, threadIdx.x);
       fence_proxy_async_smem();
       mbar_arrive(&afull[s]);
     }
@@ -279,7 +290,8 @@ struct GramLay {
   static constexpr int A_BYTES = M * 128 * 2;  // one of hi / lo: [128 tok][128 cols]
   static constexpr int B_BYTES = M * N * 2;
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int OFF_BAR = 2 * STAGE;
+  static constexpr int ST = N == 128 ? 1 : 2;  // stages that fit in 227 KiB
+  static constexpr int OFF_BAR = ST * STAGE;
   static constexpr int BYTES = OFF_BAR + 8 * 8;
 };
 
@@ -319,13 +331,13 @@ __global__ void __launch_bounds__(kGramThreads, 1) stage1_gram_kernel(const __gr
   const float* B = a.B + static_cast<int64_t>(h) * a.L * N;
   if (warp < 8) {
     for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
-      if (i >= 2) mbar_wait_sleep(&empty[s], ((i >> 1) - 1) & 1);
+      const int s = i % Lay::ST;
+      if (i >= Lay::ST) mbar_wait_sleep(&empty[s], ((i / Lay::ST) - 1) & 1);
       uint8_t* st = smem + s * Lay::STAGE;
       const int64_t row0 = static_cast<int64_t>(t0 + i) * M;
-      convert_tile<128>(A, row0, a.L, st, st + Lay::A_BYTES, threadIdx.x, kGramConv);
-      convert_tile<N>(B, row0, a.L, st + 2 * Lay::A_BYTES, st + 2 * Lay::A_BYTES + Lay::B_BYTES, threadIdx.x,
-                      kGramConv);
+      convert_tile<128, kGramConv>(A, row0, a.L, st, st + Lay::A_BYTES, threadIdx.x);
+      convert_tile<N, kGramConv>(B, row0, a.L, st + 2 * Lay::A_BYTES, st + 2 * Lay::A_BYTES + Lay::B_BYTES,
+                                 threadIdx.x);
       fence_proxy_async_smem();
       mbar_arrive(&full[s]);
     }
@@ -334,8 +346,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) stage1_gram_kernel(const __gr
     constexpr uint32_t idesc = idesc_bf16_f32(M, N, true, true);
     const bool leader = elect_one();
     for (int i = 0; i < n; ++i) {
-      const int s = i & 1;
-      mbar_wait_sleep(&full[s], (i >> 1) & 1);
+      const int s = i % Lay::ST;
+      mbar_wait_sleep(&full[s], (i / Lay::ST) & 1);
       tc_fence_after();
       if (leader) {
         uint8_t* st = smem + s * Lay::STAGE;

