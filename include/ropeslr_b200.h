@@ -145,6 +145,9 @@ int64_t ropeslr_num_blocks(int64_t L, int32_t block);
  *   "scores"        'f' / 'd': CUDA-core / unpipelined DMMA block scores
  *   "rope_tma"      0: the row-bulk-copy RoPE pre-pass
  *   "linear_simt"   1: the CUDA-core linear compensator
+ *   "screen"        0: K1 top-k from float64 scores of every block pair
+ *                   (default 1: float32-grade tensor-core screening, float64
+ *                   only where the decision can depend on it)
  * Not synchronised with calls in flight on other threads.  Unknown name:
  * ROPESLR_ERR_VALUE.  ropeslr_get_option returns the current value. */
 int ropeslr_set_option(const char* name, int value);
@@ -156,7 +159,12 @@ int ropeslr_get_option(const char* name);
  * stable descending order (ties to the lower block index), top-k or
  * cumulative-mass count, ascending index list.  `mask` and `scores`
  * ([B,H,nb,nb] float64) may be NULL.  kmax must be >= min(topk, nb) in top-k
- * mode and >= nb in keep mode. */
+ * mode and >= nb in keep mode.
+ *
+ * Top-k with d = 128 and `scores` NULL takes the screening path: float32-
+ * grade scores on the tensor cores with a proven per-row error bound E, then
+ * float64 scores only for the blocks within 2E of the k-th (the result is
+ * the float64 selection, K1). */
 size_t ropeslr_select_workspace_bytes(const ropeslr_shape* shape);
 int ropeslr_select_blocks(const ropeslr_shape* shape, const ropeslr_select_params* sel,
                           const void* q, const void* k,
@@ -172,6 +180,20 @@ size_t ropeslr_select_pooled_workspace_bytes(const ropeslr_shape* shape);
 int ropeslr_select_from_pooled(const ropeslr_shape* shape, const ropeslr_select_params* sel, const double* pooled,
                                int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
                                double* scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Where the screening path keeps its state inside the `scores` area of the
+ * selection workspace (the workspace of ropeslr_select_from_pooled, or the
+ * select workspace past the pooled means, ropeslr_select_pooled_workspace_
+ * bytes): the float32 approximate scores [B*H, nb, nbs] at *approx_offset
+ * (row stride nbs: the first of 128, 256, 512, 1024 that is >= nb),
+ * at *stats_offset an int32 count of rows decided wholly in float64 (rows
+ * whose band held more than 64 blocks, or non-finite / very wide rows), and
+ * at *diag_offset (may be NULL) an int32 per row: band size | bisection
+ * steps << 16, or -1 for a row decided wholly in float64.  For tests and
+ * measurement.  Returns ROPESLR_ERR_VALUE when this shape does not take the
+ * screening path. */
+int ropeslr_select_screen_offsets(const ropeslr_shape* shape, int32_t topk, size_t* approx_offset,
+                                  size_t* stats_offset, size_t* diag_offset);
 
 /* ------------------------------- fused 3D RoPE + block pooling (pre-pass)
  * The caller-side rotation of the reference (rope3d.rotate_rows,

@@ -86,6 +86,7 @@ _SIGNATURES = {
                                      c_f32, c_vp, c_i32, c_vp, c_i32, c_vp, c_sz, c_vp]),
     "ropeslr_attend_workspace_bytes": (c_sz, [P(Shape), c_i32]),
     "ropeslr_select_pooled_workspace_bytes": (c_sz, [P(Shape)]),
+    "ropeslr_select_screen_offsets": (c_i32, [P(Shape), c_i32, P(c_sz), P(c_sz), P(c_sz)]),
     "ropeslr_select_from_pooled": (c_i32, [P(Shape), P(SelectParams), c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp,
                                            c_vp, c_sz, c_vp]),
     "ropeslr_copy_rows": (c_i32, [c_vp, c_i32, c_i64, c_vp]),

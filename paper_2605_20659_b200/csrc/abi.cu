@@ -45,6 +45,7 @@ static Tuning& tuning_mut() {
     r.rope_tma = !env_off("ROPESLR_ROPE_TMA");
     const char* lin = getenv("ROPESLR_LINEAR");
     r.linear_simt = lin != nullptr && lin[0] == 's';
+    r.screen = !env_off("ROPESLR_SCREEN");
     return r;
   }();
   return t;
@@ -116,6 +117,7 @@ extern "C" int ropeslr_set_option(const char* name, int value) {
   else if (!strcmp(name, "scores")) t.scores = static_cast<char>(value);
   else if (!strcmp(name, "rope_tma")) t.rope_tma = value != 0;
   else if (!strcmp(name, "linear_simt")) t.linear_simt = value != 0;
+  else if (!strcmp(name, "screen")) t.screen = value != 0;
   else return ROPESLR_ERR_VALUE;
   return ROPESLR_OK;
 }
@@ -130,6 +132,7 @@ extern "C" int ropeslr_get_option(const char* name) {
   if (!strcmp(name, "scores")) return t.scores;
   if (!strcmp(name, "rope_tma")) return t.rope_tma;
   if (!strcmp(name, "linear_simt")) return t.linear_simt;
+  if (!strcmp(name, "screen")) return t.screen;
   return ROPESLR_ERR_VALUE;
 }
 

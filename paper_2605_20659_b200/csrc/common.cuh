@@ -103,6 +103,7 @@ struct Tuning {
   char scores;         // ROPESLR_SCORES: 'f' CUDA-core f64, 'd' unpipelined DMMA, 0 default
   bool rope_tma;       // ROPESLR_ROPE_TMA=0: the row-bulk-copy RoPE kernel
   bool linear_simt;    // ROPESLR_LINEAR=simt: the CUDA-core linear compensator
+  bool screen;         // ROPESLR_SCREEN=0: K1 top-k from float64 scores of every pair (no screening)
 };
 const Tuning& tuning();
 

@@ -12,6 +12,8 @@
 //             (decomposition.py:105-111); emits the ascending index list the
 //             attention kernel walks (mechanism.py:321 `sorted(chosen)`).
 // All three are HBM/L2-bound; see DESIGN.md for the byte counts.
+#include <algorithm>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -499,10 +501,47 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
 // lowest block indices (the stable order of mechanism.py:317).  The keys
 // stay in registers; each warp owns a 256-bin histogram in shared memory.
 // The radix select and the outputs of one row, from its keys (registers).
+// The outputs of one row from its selection bits (bit i: column lane +
+// 32 i): ascending index list, count, optional mask, attended pairs of the
+// head.
 template <int NPER>
-__device__ __forceinline__ void topk_row(uint64_t (&key)[NPER], int* hist, int lane, int nb, int64_t row, int64_t L, int block, int topk, int kmax, int32_t* __restrict__ idx, int32_t* __restrict__ cnt, uint8_t* __restrict__ mask, unsigned long long* __restrict__ attended) {
+__device__ __forceinline__ void emit_bits(uint32_t bits, int lane, int nb, int64_t row, int64_t L, int block, int kmax, int32_t* __restrict__ idx, int32_t* __restrict__ cnt, uint8_t* __restrict__ mask, unsigned long long* __restrict__ attended) {
   const int64_t bh = row / nb;
   const int qb = static_cast<int>(row % nb);
+  int32_t* irow = idx + row * kmax;
+  uint8_t* mrow = mask ? mask + row * nb : nullptr;
+  int carry = 0;
+  long long ksum = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    const bool s = (bits >> i) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, s);
+    if (s) {
+      irow[carry + __popc(bal & ((1u << lane) - 1u))] = c;
+      ksum += block_size(L, block, c);
+    }
+    if (mrow && c < nb) mrow[c] = s ? 1 : 0;
+    carry += __popc(bal);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+  if (lane == 0) {
+    cnt[row] = carry;
+    atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
+  }
+}
+
+template <int NPER>
+__device__ __forceinline__ void emit_row(const bool (&sel)[NPER], int lane, int nb, int64_t row, int64_t L, int block, int kmax, int32_t* __restrict__ idx, int32_t* __restrict__ cnt, uint8_t* __restrict__ mask, unsigned long long* __restrict__ attended) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) bits |= static_cast<uint32_t>(sel[i]) << i;
+  emit_bits<NPER>(bits, lane, nb, row, L, block, kmax, idx, cnt, mask, attended);
+}
+
+template <int NPER>
+__device__ __forceinline__ void topk_row(uint64_t (&key)[NPER], int* hist, int lane, int nb, int64_t row, int64_t L, int block, int topk, int kmax, int32_t* __restrict__ idx, int32_t* __restrict__ cnt, uint8_t* __restrict__ mask, unsigned long long* __restrict__ attended) {
   int need = topk < nb ? topk : nb;
   uint64_t prefix = 0, pmask = 0;
   bool exact = false;  // the remaining bucket is taken whole
@@ -578,27 +617,7 @@ __device__ __forceinline__ void topk_row(uint64_t (&key)[NPER], int* hist, int l
     }
     sel[i] = s;
   }
-  int32_t* irow = idx + row * kmax;
-  uint8_t* mrow = mask ? mask + row * nb : nullptr;
-  int carry = 0;
-  long long ksum = 0;
-#pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const int c = lane + 32 * i;
-    const unsigned bal = __ballot_sync(0xffffffffu, sel[i]);
-    if (sel[i]) {
-      irow[carry + __popc(bal & ((1u << lane) - 1u))] = c;
-      ksum += block_size(L, block, c);
-    }
-    if (mrow && c < nb) mrow[c] = sel[i] ? 1 : 0;
-    carry += __popc(bal);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
-  if (lane == 0) {
-    cnt[row] = carry;
-    atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
-  }
+  emit_row<NPER>(sel, lane, nb, row, L, block, kmax, idx, cnt, mask, attended);
 }
 
 // A row spanning more than the float64 exp range: keys of columns whose block
@@ -661,6 +680,535 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
   topk_row<NPER>(key, hist, lane, nb, row, L, block, topk, kmax, idx, cnt, mask, attended);
 }
 
+
+// ---------------------------------------------------------------- screening
+// Top-k with d = 128: the decision of mechanism.py:316-320 only depends on
+// which blocks score above the k-th, so most of the nb^2 float64 dot
+// products never matter.  The path:
+//   screen_image_kernel   pooled float64 rows -> bf16 hi/lo splits (x = hi
+//                         + lo + r, |r| <= 2^-16 |x|), written as the
+//                         128B-swizzled K-major tiles the tensor cores read,
+//                         plus an upward-rounded float norm per row
+//   screen_scores_kernel  s~ = (Qhi Khi^T + Qhi Klo^T + Qlo Khi^T) / sqrt(d)
+//                         on tcgen05 (float32 accumulation in TMEM)
+//   screen_select_kernel  per row: [lo, hi] around the k-th best s~, t_k,
+//                         by bisection on the value (hi - lo <= E); with
+//                         |s~ - s| <= E for every block of the row, blocks
+//                         with s~ > hi + 2E are in, blocks with s~ < lo - 2E
+//                         are out, and the few in between get float64 scores
+//                         and the exact stable order.
+// E = kScreenBound |q_i| max_j |k_j| / sqrt(d).  Derivation (DESIGN.md,
+// K1): the dropped split terms are <= 3.1 * 2^-16 sum |q||k|; the float32
+// accumulation of 3 d = 384 exact bf16 products, allowing each addition a
+// relative error of 2^-22 (twice a truncating adder's), adds <= 383 *
+// 2^-22 * 1.02 sum |q||k|; together 1.4e-4 |q||k| (Cauchy-Schwarz), under
+// kScreenBound = 2^-12.  Proof that the band decides exactly: the k-th best
+// exact score tau lies in [t_k - E, t_k + E], since k blocks have s >= s~ -
+// E >= t_k - E and nb - k + 1 blocks have s <= t_k + E; so tau is in
+// [lo - E, hi + E], a block with s~ > hi + 2E has s > hi + E >= tau and a
+// block with s~ < lo - 2E has s < lo - E <= tau.  Every block with s >= tau
+// outside the top set is therefore in the band, where the float64 order
+// (ties to the lower block) picks the remaining k - |in|.
+// Rows that are non-finite, span more than 700 (the probability underflow
+// of mechanism.py:310-311 needs the float64 path) or hold more than
+// kScreenBand blocks in the band are decided wholly in float64.
+namespace scr {
+constexpr int D = 128;
+constexpr int ROWS = 128;              // rows of a tile
+constexpr int ATOM = ROWS * 128;       // 16 KiB: 128 rows x 64 bf16, 128B-swizzled
+constexpr int TILE = 2 * ATOM;         // 128 rows x 128 bf16 (one split)
+constexpr double kScreenBound = 1.0 / 4096.0;
+constexpr int kScreenBand = 64;
+constexpr int EPI_WARPS = 8;
+constexpr int SMEM = 1024 + 2 * TILE + 2 * 2 * TILE + EPI_WARPS * 32 * 33 * 4 + 16 * 8;
+}  // namespace scr
+
+
+// grid (ntile * 16, BH, 2), 256 threads: one warp per pooled row (z = 0: Q,
+// 1: K); rows nb .. ntile*128 - 1 are written as zeros.  img:
+// [z][hi/lo][BH][ntile][TILE].
+__global__ void __launch_bounds__(256) screen_image_kernel(const double* __restrict__ pooled, int nb, int ntile,
+                                                           int64_t BH, uint8_t* __restrict__ img,
+                                                           float* __restrict__ norms, int* __restrict__ stats) {
+  using namespace scr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (stats != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) stats[0] = 0;
+  const int z = blockIdx.z;
+  const int64_t bh = blockIdx.y;
+  const int r = blockIdx.x * 8 + warp;
+  if (r >= ntile * ROWS) return;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  if (r < nb) {
+    const double* src = pooled + ((z * BH + bh) * nb + r) * D + lane * 4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = src[e];
+  }
+  __nv_bfloat16 hi[4], lo[4];
+  double ss = 0.0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    hi[e] = __double2bfloat16(v[e]);
+    lo[e] = __double2bfloat16(v[e] - static_cast<double>(__bfloat162float(hi[e])));
+    ss = fma(v[e], v[e], ss);
+  }
+  const int c0 = lane * 4, atom = c0 >> 6, ch = (c0 & 63) >> 3, el = c0 & 7;
+  const int rr = r & (ROWS - 1), tile = r / ROWS;
+  const int64_t off = static_cast<int64_t>(atom) * ATOM + rr * 128 + ((ch ^ (rr & 7)) << 4) + el * 2;
+  uint8_t* base_hi = img + (((z * 2 + 0) * BH + bh) * ntile + tile) * TILE;
+  uint8_t* base_lo = img + (((z * 2 + 1) * BH + bh) * ntile + tile) * TILE;
+  *reinterpret_cast<uint2*>(base_hi + off) = *reinterpret_cast<const uint2*>(hi);
+  *reinterpret_cast<uint2*>(base_lo + off) = *reinterpret_cast<const uint2*>(lo);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0 && r < nb) norms[(z * BH + bh) * nb + r] = __double2float_ru(__dsqrt_ru(ss));
+}
+
+// grid (ntile, BH), 384 threads, one CTA per SM.  Warp 0: bulk copies (the
+// CTA's 128 Q rows once, then K tiles through a 2-stage ring); warp 1: the
+// MMAs, 3 per 16-wide k-step into one of four 128-column TMEM
+// accumulators; warp 3 of tile 0: max_j |k_j| of the head; warps 4-11: the
+// epilogue, two warps per TMEM lane quarter with 64 columns each (scale,
+// transpose through shared memory, coalesced row stores of approx
+// [BH][nb][nb]).
+__global__ void __launch_bounds__(384, 1) screen_scores_kernel(const uint8_t* __restrict__ img,
+                                                                const float* __restrict__ norms, int nb, int nbs,
+                                                                int ntile, int64_t BH, float scale,
+                                                                float* __restrict__ approx,
+                                                                float* __restrict__ kmaxn) {
+  using namespace scr;
+  using namespace sm100;
+  extern __shared__ uint8_t scr_smem[];
+  uint8_t* sm = scr_smem + ((1024u - (smem_u32(scr_smem) & 1023u)) & 1023u);
+  uint8_t* sA = sm;                 // [hi tile | lo tile]
+  uint8_t* sB = sm + 2 * TILE;      // 2 stages of [hi tile | lo tile]
+  float* sT = reinterpret_cast<float*>(sB + 4 * TILE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + EPI_WARPS * 32 * 33);
+  uint64_t* afull = bars;
+  uint64_t* bfull = bars + 1;   // [2]
+  uint64_t* bempty = bars + 3;  // [2]
+  uint64_t* tfull = bars + 5;   // [4]
+  uint64_t* tempty = bars + 9;  // [4]
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int64_t bh = blockIdx.y;
+  // blockIdx.z: which part of the key tiles (more CTAs than SMs' worth of rows)
+  const int per = (ntile + gridDim.z - 1) / gridDim.z;
+  const int n0 = blockIdx.z * per, nn = min(ntile, n0 + per) - n0;
+  if (threadIdx.x == 0) {
+    mbar_init(afull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI_WARPS);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(&tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint8_t* qh = img + ((0 * BH + bh) * ntile + tile) * TILE;
+      const uint8_t* ql = img + ((1 * BH + bh) * ntile + tile) * TILE;
+      const uint8_t* kh = img + ((2 * BH + bh) * ntile) * TILE;
+      const uint8_t* kl = img + ((3 * BH + bh) * ntile) * TILE;
+      mbar_arrive_expect_tx(afull, 2 * TILE);
+      bulk_load_1d(sA, qh, TILE, afull, policy_evict_first());
+      bulk_load_1d(sA + TILE, ql, TILE, afull, policy_evict_first());
+      for (int n = 0; n < nn; ++n) {
+        const int s = n & 1;
+        if (n >= 2) mbar_wait(&bempty[s], ((n >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&bfull[s], 2 * TILE);
+        bulk_load_1d(sB + s * 2 * TILE, kh + static_cast<int64_t>(n0 + n) * TILE, TILE, &bfull[s],
+                     policy_evict_last());
+        bulk_load_1d(sB + s * 2 * TILE + TILE, kl + static_cast<int64_t>(n0 + n) * TILE, TILE, &bfull[s],
+                     policy_evict_last());
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16_f32(ROWS, ROWS, false, false);
+    const bool leader = elect_one();
+    mbar_wait(afull, 0);
+    const uint64_t dAh = desc_sw128(smem_u32(sA), 16, 1024), dAl = desc_sw128(smem_u32(sA + TILE), 16, 1024);
+    for (int n = 0; n < nn; ++n) {
+      const int s = n & 1, a = n & 3;
+      mbar_wait(&bfull[s], (n >> 1) & 1);
+      if (n >= 4) mbar_wait(&tempty[a], ((n >> 2) - 1) & 1);
+      tc_fence_after();
+      if (leader) {
+        const uint64_t dBh = desc_sw128(smem_u32(sB + s * 2 * TILE), 16, 1024);
+        const uint64_t dBl = desc_sw128(smem_u32(sB + s * 2 * TILE + TILE), 16, 1024);
+        const uint32_t acc = tmem + a * ROWS;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ko = ((kk & 3) * 32 + (kk >> 2) * ATOM) >> 4;
+          mma_bf16_ss(acc, dAl + ko, dBh + ko, idesc, kk > 0 ? 1u : 0u);
+          mma_bf16_ss(acc, dAh + ko, dBl + ko, idesc, 1u);
+          mma_bf16_ss(acc, dAh + ko, dBh + ko, idesc, 1u);
+        }
+        mma_commit(&bempty[s]);
+        mma_commit(&tfull[a]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 3) {
+    if (tile == 0 && blockIdx.z == 0) {
+      const float* kn = norms + (BH + bh) * nb;
+      float m = 0.f;
+      for (int j = lane; j < nb; j += 32) m = fmaxf(m, kn[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) kmaxn[bh] = m;
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4, q4 = warp & 3, half = ew >> 2;
+    float* T = sT + ew * 32 * 33;
+    float* out = approx + bh * nb * static_cast<int64_t>(nbs);
+    const int row0 = tile * ROWS + q4 * 32;
+    const int rmax = min(32, nb - row0);
+    for (int n = 0; n < nn; ++n) {
+      const int a = n & 3;
+      mbar_wait(&tfull[a], (n >> 2) & 1);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + a * ROWS + half * 64;
+      tmem_ld32(taddr, r0);
+      tmem_ld32(taddr + 32, r1);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(g ? r1[j] : r0[j]) * scale;
+        __syncwarp();
+        const int col = (n0 + n) * ROWS + half * 64 + g * 32 + lane;
+        if (col < nb)
+          for (int rr = 0; rr < rmax; ++rr) out[static_cast<int64_t>(row0 + rr) * nbs + col] = T[rr * 33 + lane];
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+struct ScreenArgs {
+  const float* approx;
+  const double* pooled;
+  const float* norms;
+  const float* kmaxn;
+  int* full_count;  // rows decided wholly in float64 ...
+  int* full_list;   // ... and which
+  int* diag;        // per row: band size | bisection steps << 16 (-1: deferred)
+  int nb;
+  int64_t BH, rows, L;
+  int block, topk, kmax;
+  double sqrt_d, inv_sqrt_d;
+  int nbs;  // row stride of approx (floats)
+  int32_t* idx;
+  int32_t* cnt;
+  uint8_t* mask;
+  unsigned long long* attended;
+};
+
+// One warp per row: a bracket [lo, hi] of the k-th best approximate score,
+// the band, float64 scores of the band, the exact decision.  Rows that
+// cannot be decided this way go to a list for screen_exact_kernel.  Lane l
+// holds the NPER consecutive columns [l NPER, l NPER + NPER) (the approx
+// rows are padded to 32 NPER floats), so every compaction -- the band, the
+// ascending index list -- is one prefix sum over the lanes.
+template <int NPER>
+__global__ void __launch_bounds__(256, 4) screen_select_kernel(const ScreenArgs a) {
+  using namespace scr;
+  __shared__ int listA[8][kScreenBand];
+  __shared__ uint64_t keyA[8][kScreenBand];
+  __shared__ uint8_t selA[8][kScreenBand];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+  if (row >= a.rows) return;
+  const int nb = a.nb;
+  const int64_t bh = row / nb;
+  const int c0 = lane * NPER;
+  const float4* arow = reinterpret_cast<const float4*>(a.approx + row * (32 * NPER)) + lane * (NPER / 4);
+  float v[NPER];
+#pragma unroll
+  for (int j = 0; j < NPER / 4; ++j) {
+    const float4 t = arow[j];
+    v[4 * j] = t.x;
+    v[4 * j + 1] = t.y;
+    v[4 * j + 2] = t.z;
+    v[4 * j + 3] = t.w;
+  }
+  float vmax = -INFINITY, vmin = INFINITY, vsum = 0.f, vsq = 0.f;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    // padding is NaN: ignored by fmaxf / fminf, above nothing, in no band
+    if (c0 + i >= nb) v[i] = __int_as_float(0x7fffffff);
+    const float u = c0 + i < nb ? v[i] : 0.f;
+    vmax = fmaxf(vmax, v[i]);
+    vmin = fminf(vmin, v[i]);
+    vsum += u;  // a NaN / inf score anywhere makes this non-finite
+    vsq = fmaf(u, u, vsq);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+    vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+    vsq += __shfl_xor_sync(0xffffffffu, vsq, o);
+  }
+  const bool bad = !isfinite(vsum) || !isfinite(vsq);
+  const int need = a.topk < nb ? a.topk : nb;
+  const double E = kScreenBound * static_cast<double>(a.norms[row]) * static_cast<double>(a.kmaxn[bh]) * a.inv_sqrt_d *
+                       (1.0 + 1e-6) + 1e-300;
+  uint32_t bits = 0;
+  if (need < nb) {
+    if (bad || !(E < 1e300) || static_cast<double>(vmax) - static_cast<double>(vmin) > 700.0) {
+      if (lane == 0) {
+        a.full_list[atomicAdd(a.full_count, 1)] = static_cast<int>(row);
+        a.diag[row] = -1;
+      }
+      return;
+    }
+    // count(v > x): the sign of x - v (exact: x - v is 0 only for x == v,
+    // and never -0 for x != -0), one FADD and one shifted add per value; the
+    // NaN padding gives a positive NaN
+    auto count_gt = [&](float x) {
+      x += 0.f;  // -0 -> +0
+      unsigned c = 0;
+#pragma unroll
+      for (int i = 0; i < NPER; ++i) c += __float_as_uint(__fsub_rn(x, v[i])) >> 31;
+      return static_cast<int>(__reduce_add_sync(0xffffffffu, c));
+    };
+    // Bracket t_k, the need-th best approximate score: count(v >= lo) >=
+    // need and count(v > hi) < need, until count(v > lo) == need exactly
+    // (then t_k = min{v > lo}) or hi - lo <= E.  Probes: the normal quantile
+    // of the row's mean and spread, one Newton step with the normal density
+    // there, then interpolation of the count inside the bracket.  The probes
+    // only steer; the bracket is kept by the exact counts.
+    float lo = vmin, hi = vmax;
+    int clo = nb, chi = 0;
+    bool lo_exact = false;
+    int it = 0;
+    const float mean = vsum / nb, sd = sqrtf(fmaxf(vsq / nb - mean * mean, 0.f));
+    const float z = 1.41421356f * erfinvf(1.f - 2.f * (static_cast<float>(need) - 0.5f) / static_cast<float>(nb));
+    const float dens = static_cast<float>(nb) * 0.39894228f * __expf(-0.5f * z * z) / fmaxf(sd, 1e-30f);
+    float x = mean + z * sd;
+    int c = 0;
+    for (; it < 48 && static_cast<double>(hi) - static_cast<double>(lo) > E; ++it) {
+      const float w = hi - lo;
+      if (it == 1) {
+        x = x + (static_cast<float>(c - need) + 0.5f) / dens;
+      } else if (it > 1) {
+        const float f = (static_cast<float>(clo - need) + 0.5f) / static_cast<float>(clo - chi);
+        x = lo + fminf(fmaxf(f, 0.125f), 0.875f) * w;
+      }
+      x = fminf(fmaxf(x, lo + w * (1.f / 64.f)), hi - w * (1.f / 64.f));
+      if (!(x > lo && x < hi)) break;
+      c = count_gt(x);
+      if (c >= need) {
+        lo = x;
+        clo = c;
+        if (c == need) {
+          lo_exact = true;
+          break;
+        }
+      } else {
+        hi = x;
+        chi = c;
+      }
+    }
+    if (lo_exact) {
+      float m = INFINITY;
+#pragma unroll
+      for (int i = 0; i < NPER; ++i) m = fminf(m, __fsub_rn(v[i], lo) > 0.f ? v[i] : INFINITY);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      lo = hi = m;
+    }
+    // tau (the k-th best float64 score) lies in [lo - E, hi + E]: in above
+    // hi + 2E, out below lo - 2E (thresholds rounded outward to float)
+    const float hiB = __double2float_ru(static_cast<double>(hi) + 2.0 * E);
+    const float loB = __double2float_rd(static_cast<double>(lo) - 2.0 * E);
+    uint32_t abits = 0;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {
+      const bool inD = v[i] > hiB;
+      bits |= static_cast<uint32_t>(inD) << i;
+      abits |= static_cast<uint32_t>(!inD && v[i] >= loB) << i;
+    }
+    const int nD = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(__popc(bits))));
+    const int myA = __popc(abits);
+    int incl = myA;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int nA = __shfl_sync(0xffffffffu, incl, 31);
+    if (nA > kScreenBand) {
+      if (lane == 0) {
+        a.full_list[atomicAdd(a.full_count, 1)] = static_cast<int>(row);
+        a.diag[row] = -1;
+      }
+      return;
+    }
+    if (lane == 0) a.diag[row] = nA | (it << 16);
+    {
+      int p = incl - myA;
+      for (uint32_t m = abits; m; m &= m - 1) listA[warp][p++] = c0 + __ffs(m) - 1;
+    }
+    __syncwarp();
+    // float64 scores of the band, two rows of K in flight
+    const double* qrow = a.pooled + row * D;
+    const double* kbase = a.pooled + (a.BH + bh) * nb * D;
+    const double2 q01 = reinterpret_cast<const double2*>(qrow)[lane * 2];
+    const double2 q23 = reinterpret_cast<const double2*>(qrow)[lane * 2 + 1];
+    for (int b = 0; b < nA; b += 2) {
+      const int j0 = listA[warp][b], j1 = listA[warp][b + 1 < nA ? b + 1 : b];
+      const double2* k0 = reinterpret_cast<const double2*>(kbase + static_cast<int64_t>(j0) * D) + lane * 2;
+      const double2* k1 = reinterpret_cast<const double2*>(kbase + static_cast<int64_t>(j1) * D) + lane * 2;
+      const double2 a0 = k0[0], a1 = k0[1], b0 = k1[0], b1 = k1[1];
+      double p0 = q01.x * a0.x, p1 = q01.x * b0.x;
+      p0 = fma(q01.y, a0.y, p0);
+      p1 = fma(q01.y, b0.y, p1);
+      p0 = fma(q23.x, a1.x, p0);
+      p1 = fma(q23.x, b1.x, p1);
+      p0 = fma(q23.y, a1.y, p0);
+      p1 = fma(q23.y, b1.y, p1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+      }
+      if (lane == 0) {
+        keyA[warp][b] = desc_key(p0 / a.sqrt_d);
+        if (b + 1 < nA) keyA[warp][b + 1] = desc_key(p1 / a.sqrt_d);
+      }
+    }
+    __syncwarp();
+    // the band's best need - nD by (float64 score, then lower block)
+    const int needA = need - nD;
+    for (int xx = lane; xx < nA; xx += 32) {
+      const uint64_t kx = keyA[warp][xx];
+      const int cx = listA[warp][xx];
+      int rank = 0;
+      for (int y = 0; y < nA; ++y) {
+        const uint64_t ky = keyA[warp][y];
+        rank += (ky < kx) || (ky == kx && listA[warp][y] < cx);
+      }
+      selA[warp][xx] = rank < needA;
+    }
+    __syncwarp();
+    {
+      int p = incl - myA;
+      for (uint32_t m = abits; m; m &= m - 1, ++p)
+        if (selA[warp][p]) bits |= 1u << (__ffs(m) - 1);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) bits |= static_cast<uint32_t>(c0 + i < nb) << i;
+  }
+  // outputs: ascending index list (lane-major = column order), count,
+  // mask, attended pairs
+  const int mine = __popc(bits);
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int32_t* irow = a.idx + row * a.kmax + (incl - mine);
+  for (uint32_t m = bits; m; m &= m - 1) *irow++ = c0 + __ffs(m) - 1;
+  if (a.mask != nullptr) {
+    uint8_t* mrow = a.mask + row * nb;
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (c0 + i < nb) mrow[c0 + i] = (bits >> i) & 1u;
+  }
+  // every selected block has `block` keys except a selected ragged last one
+  const int last = nb - 1;
+  const bool last_sel = __any_sync(0xffffffffu, last / NPER == lane && ((bits >> (last % NPER)) & 1u));
+  if (lane == 0) {
+    const int qb = static_cast<int>(row % nb);
+    const long long ksum = static_cast<long long>(need) * a.block -
+                           (last_sel ? static_cast<long long>(nb) * a.block - a.L : 0);
+    a.cnt[row] = need;
+    atomicAdd(a.attended + bh, static_cast<unsigned long long>(ksum * block_size(a.L, a.block, qb)));
+  }
+}
+
+// The listed rows, decided wholly in float64: every score (lane = column,
+// the 128 products in order, Q row from shared memory), the probability-
+// underflow clamp of mechanism.py:310-317 and topk_row.  A grid-stride loop
+// over the list; the count is read once.
+template <int NPER>
+__global__ void __launch_bounds__(256) screen_exact_kernel(const ScreenArgs a) {
+  using namespace scr;
+  __shared__ int hist_all[8][256];
+  __shared__ double qs_all[8][D];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = *a.full_count;
+  const int nb = a.nb;
+  for (int w = blockIdx.x * 8 + warp; w < n; w += gridDim.x * 8) {
+    const int64_t row = a.full_list[w];
+    const int64_t bh = row / nb;
+    const double* qrow = a.pooled + row * D;
+    const double* kbase = a.pooled + (a.BH + bh) * nb * D;
+    double* qs = qs_all[warp];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) qs[lane * 4 + e] = qrow[lane * 4 + e];
+    __syncwarp();
+    uint64_t key[NPER];
+    uint64_t amax = 0, amin = ~0ull;  // ascending keys of the row max / min
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {
+      const int c = lane + 32 * i;
+      key[i] = ~0ull;
+      if (c < nb) {
+        const double2* kr = reinterpret_cast<const double2*>(kbase + static_cast<int64_t>(c) * D);
+        double p = 0.0;
+#pragma unroll 8
+        for (int e = 0; e < D / 2; ++e) {
+          const double2 kk = kr[e];
+          p = fma(qs[2 * e], kk.x, p);
+          p = fma(qs[2 * e + 1], kk.y, p);
+        }
+        key[i] = desc_key(p / a.sqrt_d);
+        amax = max(amax, ~key[i]);
+        amin = min(amin, ~key[i]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      amin = min(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+    }
+    auto value_of = [](uint64_t asc) {
+      return __longlong_as_double(static_cast<long long>((asc >> 63) ? (asc & ~(1ull << 63)) : ~asc));
+    };
+    const double row_max = value_of(amax);
+    if (row_max > -INFINITY && value_of(amin) - row_max < kProbUnderflow) {
+#pragma unroll
+      for (int i = 0; i < NPER; ++i)
+        if (lane + 32 * i < nb && value_of(~key[i]) - row_max < kProbUnderflow) key[i] = desc_key(-INFINITY);
+    }
+    topk_row<NPER>(key, hist_all[warp], lane, nb, row, a.L, a.block, a.topk, a.kmax, a.idx, a.cnt, a.mask,
+                   a.attended);
+    __syncwarp();
+  }
+}
+
 }  // namespace ropeslr
 
 using namespace ropeslr;
@@ -693,9 +1241,113 @@ static size_t pooled_bytes(const ropeslr_shape* s) {
   return ((static_cast<size_t>(2 * s->B * s->H * nb * s->d) * sizeof(double) + 255) / 256) * 256;
 }
 
+// The screening path's state inside the scores area (select.cu, K1 screening).
+struct ScreenLayout {
+  size_t approx, img, norms, kmaxn, stats, list, diag, total;
+};
+
+// Values per lane of screen_select_kernel, and the approx row stride 32 * that.
+static int screen_nper(int64_t nb) { return nb <= 128 ? 4 : nb <= 256 ? 8 : nb <= 512 ? 16 : 32; }
+
+static ScreenLayout screen_layout(int64_t BH, int64_t nb) {
+  const int64_t ntile = ceil_div(nb, scr::ROWS);
+  const int64_t nbs = 32 * screen_nper(nb);
+  ScreenLayout y{};
+  size_t off = 0;
+  auto take = [&off](size_t b) {
+    const size_t o = off;
+    off += (b + 255) / 256 * 256;
+    return o;
+  };
+  y.approx = take(static_cast<size_t>(BH * nb * nbs) * sizeof(float));
+  y.img = take(static_cast<size_t>(4 * BH * ntile) * scr::TILE);
+  y.norms = take(static_cast<size_t>(2 * BH * nb) * sizeof(float));
+  y.kmaxn = take(static_cast<size_t>(BH) * sizeof(float));
+  y.stats = take(16);
+  y.list = take(static_cast<size_t>(BH * nb) * sizeof(int));
+  y.diag = take(static_cast<size_t>(BH * nb) * sizeof(int));
+  y.total = off;
+  return y;
+}
+
+static bool screen_eligible(const ropeslr_shape* s, int32_t topk) {
+  const int64_t nb = ceil_div(s->L, s->block);
+  return tuning().screen && topk > 0 && s->d == scr::D && nb <= 1024;
+}
+
 static size_t scores_bytes(const ropeslr_shape* s) {
   const int64_t nb = ceil_div(s->L, s->block);
-  return ((static_cast<size_t>(s->B * s->H * nb * nb) * sizeof(double) + 255) / 256) * 256;
+  const size_t f64 = ((static_cast<size_t>(s->B * s->H * nb * nb) * sizeof(double) + 255) / 256) * 256;
+  const size_t scr_bytes = s->d == scr::D ? screen_layout(s->B * s->H, nb).total : 0;
+  return f64 > scr_bytes ? f64 : scr_bytes;
+}
+
+// Top-k of every row through the screening kernels (area: the scores area).
+static int launch_screen(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
+                         int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended, uint8_t* area,
+                         cudaStream_t st) {
+  const int64_t BH = s->B * s->H;
+  const int nb = static_cast<int>(ceil_div(s->L, s->block));
+  const int ntile = static_cast<int>(ceil_div(nb, scr::ROWS));
+  const int nbs = 32 * screen_nper(nb);
+  const ScreenLayout y = screen_layout(BH, nb);
+  float* approx = reinterpret_cast<float*>(area + y.approx);
+  uint8_t* img = area + y.img;
+  float* norms = reinterpret_cast<float*>(area + y.norms);
+  float* kmaxn = reinterpret_cast<float*>(area + y.kmaxn);
+  int* stats = reinterpret_cast<int*>(area + y.stats);
+  screen_image_kernel<<<dim3(static_cast<unsigned>(ntile * 16), static_cast<unsigned>(BH), 2), 256, 0, st>>>(
+      pooled, nb, ntile, BH, img, norms, stats);
+  if (cudaFuncSetAttribute(screen_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, scr::SMEM) !=
+      cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  // split the key tiles when the (row tile, head) CTAs alone would leave a
+  // partial second wave
+  const unsigned nsplit = ntile >= 4 && ntile * BH < 4 * num_sms() ? 2u : 1u;
+  screen_scores_kernel<<<dim3(static_cast<unsigned>(ntile), static_cast<unsigned>(BH), nsplit),
+                         128 + 32 * scr::EPI_WARPS,
+                         scr::SMEM, st>>>(
+      img, norms, nb, nbs, ntile, BH, static_cast<float>(1.0 / sqrt(static_cast<double>(scr::D))), approx, kmaxn);
+  ScreenArgs a{};
+  a.approx = approx;
+  a.pooled = pooled;
+  a.norms = norms;
+  a.kmaxn = kmaxn;
+  a.full_count = stats;
+  a.full_list = reinterpret_cast<int*>(area + y.list);
+  a.diag = reinterpret_cast<int*>(area + y.diag);
+  a.nb = nb;
+  a.BH = BH;
+  a.rows = BH * nb;
+  a.L = s->L;
+  a.block = s->block;
+  a.topk = sel->topk;
+  a.kmax = kmax;
+  a.sqrt_d = sqrt(static_cast<double>(scr::D));
+  a.inv_sqrt_d = 1.0 / a.sqrt_d;
+  a.nbs = nbs;
+  a.idx = idx;
+  a.cnt = cnt;
+  a.mask = mask;
+  a.attended = reinterpret_cast<unsigned long long*>(attended);
+  const unsigned grid = static_cast<unsigned>(ceil_div(a.rows, 8));
+  // the exact pass: enough warps for a list of every row, at most 4 CTAs per SM
+  const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(ceil_div(a.rows, 8), 4 * num_sms()));
+#define ROPESLR_SCREEN_CASE(NPER_)                                  \
+  do {                                                              \
+    screen_select_kernel<NPER_><<<grid, 256, 0, st>>>(a);           \
+    screen_exact_kernel<NPER_><<<grid_x, 256, 0, st>>>(a);          \
+  } while (0)
+  if (nb <= 128)
+    ROPESLR_SCREEN_CASE(4);
+  else if (nb <= 256)
+    ROPESLR_SCREEN_CASE(8);
+  else if (nb <= 512)
+    ROPESLR_SCREEN_CASE(16);
+  else
+    ROPESLR_SCREEN_CASE(32);
+#undef ROPESLR_SCREEN_CASE
+  return launch_status();
 }
 
 // Scores of heads [bh0, bh1) from the pooled means.
@@ -763,14 +1415,19 @@ static int launch_select(const ropeslr_shape* s, const ropeslr_select_params* se
 }
 
 // Scores from the pooled means, then top-k / cumulative-mass selection.
+// scores_out: the caller's float64 scores (then every pair is scored in
+// float64), else NULL; area: the workspace's scores area.
 static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
                               int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
-                              double* scores, cudaStream_t st) {
+                              double* scores_out, uint8_t* area, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
   const int d = static_cast<int>(s->d);
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
   if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
   if (int e = scan_nonfinite(pooled, true, 2 * BH * nb * d, sel->nonfinite, ROPESLR_NONFINITE_QK, st)) return e;
+  if (scores_out == nullptr && screen_eligible(s, sel->topk))
+    return launch_screen(s, sel, pooled, idx, kmax, cnt, mask, attended, area, st);
+  double* scores = scores_out ? scores_out : reinterpret_cast<double*>(area);
   if (int e = launch_scores(pooled, scores, nb, d, BH, 0, BH, st)) return e;
   return launch_select(s, sel, scores, idx, kmax, cnt, mask, attended, 0, BH, st);
 }
@@ -819,9 +1476,9 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
   if (ws == nullptr || ws_bytes < ropeslr_select_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   double* pooled = static_cast<double*>(ws);
-  double* scores = scores_out ? scores_out : reinterpret_cast<double*>(static_cast<char*>(ws) + pooled_bytes(s));
+  uint8_t* area = static_cast<uint8_t*>(ws) + pooled_bytes(s);
   if (int e = launch_pool(s, q, k, pooled, 0, s->B * s->H, st)) return e;
-  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores, st);
+  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores_out, area, st);
 }
 
 extern "C" int ropeslr_select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel,
@@ -831,11 +1488,20 @@ extern "C" int ropeslr_select_from_pooled(const ropeslr_shape* s, const ropeslr_
   int stt = check_select(s, sel, kmax, idx, cnt, attended);
   if (stt) return stt;
   if (!pooled) return ROPESLR_ERR_NULL;
-  double* scores = scores_out;
-  if (scores == nullptr) {
-    if (ws == nullptr || ws_bytes < ropeslr_select_pooled_workspace_bytes(s)) return ROPESLR_ERR_WORKSPACE;
-    scores = static_cast<double*>(ws);
-  }
-  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores,
+  if (scores_out == nullptr && (ws == nullptr || ws_bytes < ropeslr_select_pooled_workspace_bytes(s)))
+    return ROPESLR_ERR_WORKSPACE;
+  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores_out, static_cast<uint8_t*>(ws),
                             static_cast<cudaStream_t>(stream_));
+}
+
+extern "C" int ropeslr_select_screen_offsets(const ropeslr_shape* s, int32_t topk, size_t* approx_offset,
+                                             size_t* stats_offset, size_t* diag_offset) {
+  if (s == nullptr || approx_offset == nullptr || stats_offset == nullptr) return ROPESLR_ERR_NULL;
+  if (s->block < 1 || s->L < 1 || s->B < 1 || s->H < 1) return ROPESLR_ERR_SHAPE;
+  if (!screen_eligible(s, topk)) return ROPESLR_ERR_VALUE;
+  const ScreenLayout y = screen_layout(s->B * s->H, ceil_div(s->L, s->block));
+  *approx_offset = y.approx;
+  *stats_offset = y.stats;
+  if (diag_offset != nullptr) *diag_offset = y.diag;
+  return ROPESLR_OK;
 }

@@ -349,13 +349,15 @@ def _crafted_scores_inputs(b_vals, a_vals, block=32, d=64):
     return q.cuda(), k.cuda(), torch.zeros_like(q).cuda()
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("rule", [dict(topk=7), dict(topk=1), dict(keep=0.5), dict(keep=0.999)])
 @pytest.mark.parametrize("pattern", ["wide", "powers", "dups", "signed_zero"])
-def test_selection_extreme_and_tied_scores(pattern, rule):
+def test_selection_extreme_and_tied_scores(pattern, rule, d):
     """Selection on block scores with spreads far beyond the float64 exp
     range (the reference's block probabilities underflow to 0 and tie, so
     those blocks go by index), exact duplicates, powers of two and signed
-    zeros: masks bit-exact against the oracle (mechanism.py:309-320)."""
+    zeros: masks bit-exact against the oracle (mechanism.py:309-320).  With
+    d = 128 top-k takes the screening path (test_gpu_screen.py)."""
     import paper_2605_20659_b200 as P
 
     rng = np.random.default_rng(5)
@@ -371,7 +373,7 @@ def test_selection_extreme_and_tied_scores(pattern, rule):
         b[[5, 17, 30]] = [1.0, 1.0, 0.5]
     a = rng.standard_normal(nb) * 4.0
     a[[3, 11]] = 0.0
-    q, k, v = _crafted_scores_inputs(b, a)
+    q, k, v = _crafted_scores_inputs(b, a, d=d)
     sp = P.SparseSettings(block=32, **rule)
     sel = P.select_blocks(q, k, sp)
     members = R.flat_block_members(q.shape[2], 32)

@@ -1,0 +1,170 @@
+"""K1 screening path (csrc/select.cu, screen_*): top-k with d = 128 decided
+from float32-grade tensor-core block scores, with float64 scores only for
+the blocks within 2E of the k-th.  It must select exactly what the
+float64-everywhere path selects (mechanism.py:309-320), on random, clustered
+(near-tied), duplicated and very wide score rows, and the measured score
+error must sit far inside the bound E the kernel assumes."""
+
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import gpu_helpers as G
+
+pytestmark = pytest.mark.gpu
+
+BOUND = 2.0 ** -12  # scr::kScreenBound
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _both(q, k, topk, block):
+    import paper_2605_20659_b200 as P
+    from paper_2605_20659_b200 import _lib
+
+    sp = P.SparseSettings(block=block, topk=topk)
+    with _lib.option("screen", 1):
+        a = P.select_blocks(q, k, sp)
+    with _lib.option("screen", 0):
+        b = P.select_blocks(q, k, sp, want_scores=True)
+    torch.cuda.synchronize()
+    for f in ("idx", "cnt", "attended", "mask"):
+        assert torch.equal(getattr(a, f), getattr(b, f)), f"screened selection differs from float64 in {f}"
+    return a, b
+
+
+def _raw_screen(q, k, topk, block):
+    """The screening call through the C ABI, returning (pooled, approx,
+    full-row count) read back from its workspace."""
+    from paper_2605_20659_b200 import _lib, mechanism as M
+
+    B, H, L, d = q.shape
+    nb = -(-L // block)
+    shp = M._shape(q, block)
+    lib = _lib.lib()
+    ws_bytes = lib.ropeslr_select_workspace_bytes(ctypes.byref(shp))
+    area0 = ws_bytes - lib.ropeslr_select_pooled_workspace_bytes(ctypes.byref(shp))
+    a_off, s_off, d_off = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.call("ropeslr_select_screen_offsets", ctypes.byref(shp), topk, ctypes.byref(a_off), ctypes.byref(s_off),
+              ctypes.byref(d_off))
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=q.device)
+    idx = torch.empty((B, H, nb, min(topk, nb)), dtype=torch.int32, device=q.device)
+    cnt = torch.empty((B, H, nb), dtype=torch.int32, device=q.device)
+    att = torch.empty((B, H), dtype=torch.int64, device=q.device)
+    sel = _lib.SelectParams(topk, 0.0, None)
+    with _lib.option("screen", 1):
+        _lib.call("ropeslr_select_blocks", ctypes.byref(shp), ctypes.byref(sel), q.data_ptr(), k.data_ptr(),
+                  idx.data_ptr(), idx.shape[-1], cnt.data_ptr(), None, att.data_ptr(), None, ws.data_ptr(), ws_bytes,
+                  None)
+    torch.cuda.synchronize()
+    pooled = ws[:2 * B * H * nb * d * 8].view(torch.float64).view(2, B * H, nb, d)
+    o = area0 + a_off.value
+    nbs = next(w for w in (128, 256, 512, 1024) if w >= nb)
+    approx = ws[o:o + B * H * nb * nbs * 4].view(torch.float32).view(B, H, nb, nbs)[..., :nb]
+    o = area0 + s_off.value
+    full = int(ws[o:o + 4].view(torch.int32)[0])
+    o = area0 + d_off.value
+    _raw_screen.diag = ws[o:o + B * H * nb * 4].view(torch.int32).clone()
+    return pooled, approx, full
+
+
+@pytest.mark.parametrize("nb,block,ragged", [(100, 64, 0), (200, 32, 7), (400, 64, 0), (929, 32, 13)])
+def test_screen_equals_float64_random(nb, block, ragged):
+    g = torch.Generator(device="cuda").manual_seed(nb)
+    L = nb * block - ragged
+    q = torch.randn((2, 3, L, 128), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((2, 3, L, 128), generator=g, device="cuda").to(torch.bfloat16)
+    for frac in (0.05, 0.1, 0.2, 0.5):
+        _both(q, k, max(1, int(nb * frac)), block)
+
+
+def test_screen_error_inside_bound():
+    """|s~ - s| / (|q_i| max_j |k_j| / sqrt(d)) over every block pair of a
+    config-3-sized head set, against the float64 scores: the kernel assumes
+    <= 2^-12; the measured worst case must be at least 8x below."""
+    nb, block, H = 929, 128, 4
+    L = 118800
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = torch.randn((1, H, L, 128), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, H, L, 128), generator=g, device="cuda").to(torch.bfloat16)
+    topk = 93
+    a, b = _both(q, k, topk, block)
+    pooled, approx, full = _raw_screen(q, k, topk, block)
+    s = b.scores.double()
+    qn = pooled[0].norm(dim=-1)  # [BH, nb]
+    kmax = pooled[1].norm(dim=-1).max(dim=-1).values  # [BH]
+    scale = (qn * kmax[:, None] / np.sqrt(128.0)).view(1, H, nb, 1)
+    ratio = float(((approx.double() - s).abs() / scale).max())
+    diag = _raw_screen.diag
+    band, steps = (diag & 0xffff).float(), (diag >> 16).float()
+    rec = dict(test="screen_error", worst_ratio=ratio, bound=BOUND, full_rows=full, rows=H * nb,
+               band_mean=float(band.mean()), band_max=int(band.max()), steps_mean=float(steps.mean()),
+               steps_max=int(steps.max()))
+    out_dir = os.path.join(G.REPO, "gpurun_out", "parity")
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "k1_screen_error.json"), "w") as f:
+        json.dump(rec, f)
+    print(json.dumps(rec))
+    assert ratio < BOUND / 8, rec
+    assert full == 0, rec
+
+
+def test_screen_clusters_and_duplicates():
+    """Blocks in tight clusters (pooled K within 1e-9 of a centre) and exact
+    duplicates: the band holds whole clusters and the float64 scores decide
+    inside them; ties of duplicates go to the lower block."""
+    nb, block, d = 320, 32, 128
+    rng = np.random.default_rng(11)
+    centres = rng.standard_normal((32, d))
+    kb = np.repeat(centres, 10, axis=0) + 1e-9 * rng.standard_normal((nb, d))
+    kb[::7] = kb[1]  # exact duplicates
+    qb = rng.standard_normal((nb, d))
+    q = torch.from_numpy(np.repeat(qb, block, axis=0)).float().view(1, 1, nb * block, d).cuda()
+    k = torch.from_numpy(np.repeat(kb, block, axis=0)).float().view(1, 1, nb * block, d).cuda()
+    for topk in (5, 32, 100, 319):
+        _both(q, k, topk, block)
+
+
+def test_screen_defers_undecidable_rows():
+    """Rows the band cannot decide go to the float64 pass: one cluster of
+    300 near-identical blocks (band > 64), and rows spanning more than 700
+    (the probability-underflow clamp, mechanism.py:310-317)."""
+    nb, block, d = 300, 32, 128
+    rng = np.random.default_rng(12)
+    kb = rng.standard_normal(d)[None, :] + 1e-7 * rng.standard_normal((nb, d))
+    qb = rng.standard_normal((nb, d))
+    q = torch.from_numpy(np.repeat(qb, block, axis=0)).float().view(1, 1, nb * block, d).cuda()
+    k = torch.from_numpy(np.repeat(kb, block, axis=0)).float().view(1, 1, nb * block, d).cuda()
+    _both(q, k, 30, block)
+    _, _, full = _raw_screen(q, k, 30, block)
+    assert full == nb
+    # wide rows: scores up to ~ +-1e4
+    kb = 40.0 * rng.standard_normal((nb, d))
+    qb = 40.0 * rng.standard_normal((nb, d))
+    q = torch.from_numpy(np.repeat(qb, block, axis=0)).float().view(1, 1, nb * block, d).cuda()
+    k = torch.from_numpy(np.repeat(kb, block, axis=0)).float().view(1, 1, nb * block, d).cuda()
+    for topk in (3, 150, 290):
+        _both(q, k, topk, block)
+    _, _, full = _raw_screen(q, k, 150, block)
+    assert full == nb
+
+
+def test_screen_offsets_abi():
+    from paper_2605_20659_b200 import _lib
+
+    a, s = ctypes.c_size_t(), ctypes.c_size_t()
+    shp = _lib.Shape(1, 2, 4096, 128, 64, 1)
+    f = _lib.lib().ropeslr_select_screen_offsets
+    assert f(ctypes.byref(shp), 8, ctypes.byref(a), ctypes.byref(s), None) == 0
+    assert a.value == 0 and s.value > 0
+    shp64 = _lib.Shape(1, 2, 4096, 64, 64, 1)
+    assert f(ctypes.byref(shp64), 8, ctypes.byref(a), ctypes.byref(s), None) != 0
+    assert f(ctypes.byref(shp), 0, ctypes.byref(a), ctypes.byref(s), None) != 0
