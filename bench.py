@@ -42,10 +42,12 @@ CONFIGS = {
                       split=(44, 42, 42), block=128, sparsity=0.9, r=64),
 }
 METRIC = "RoPeSLR attn fwd ms & effective TFLOPS/GPU, L=118800, 90% sparse, 1/2/4/8 B200"
-# our launches per step: pool_blocks, block_scores, select_topk_warp (K1);
-# lowrank_fold, lowrank_umma, gate_sum (K3); sparse_attn_fixed and the
-# running-max sparse_attn_tc over the fixed kernel's flagged units (K2+K4)
-KERNELS_PER_STEP = 8  # pool, scores, select, fold, lowrank, gate_sum, fixed K2, K2 fallback (top-k: no unit ranking)
+# our launches per step: pool_blocks_bulk (+ the screening image rows),
+# screen_scores, screen_select, screen_exact (K1); lowrank_umma, gate_sum
+# (K3; the parameter-only PE fold is cached across steps); sparse_attn_fixed
+# and the running-max sparse_attn_tc over the fixed kernel's flagged units
+# (K2+K4)
+KERNELS_PER_STEP = 8  # pool, scores, select, exact, lowrank, gate_sum, fixed K2, K2 fallback
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -467,13 +469,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                           "GB_per_s": 2 * q.numel() * q.element_size() / (k1_ms * 1e-3) / 1e9,
                           "frac_of_hbm": 2 * q.numel() * q.element_size() / (k1_ms * 1e-3) / 1e9
                           / load_peaks().get("hbm_gbs", 6650.0),
-                          "kernels": "pool (f64 block means) + DMMA f64 scores + radix top-k",
+                          "kernels": "pool (f64 block means + bf16 hi/lo image) + tcgen05 screening scores + band select (float64 in the band) + float64 pass over deferred rows",
                           "unit": "read Q and K once"},
             "K3_compensator": {"ms": k3_ms, "bytes": 2 * x.numel() * x.element_size(),
                                "GB_per_s": 2 * x.numel() * x.element_size() / (k3_ms * 1e-3) / 1e9,
                                "frac_of_hbm": 2 * x.numel() * x.element_size() / (k3_ms * 1e-3) / 1e9
                                / load_peaks().get("hbm_gbs", 6650.0),
-                               "kernels": "PE fold + tcgen05 low-rank / gate + fixed-order gate sum",
+                               "kernels": "tcgen05 low-rank / gate (PE fold cached) + fixed-order gate sum",
                                "unit": "read X once, write y_lr once"}},
         "attended_pairs": attended_total,
         "k2_fallback_units": {"rank0": fallback_local, "of_units": Hl * nb,

@@ -187,7 +187,7 @@ int ropeslr_select_from_pooled(const ropeslr_shape* shape, const ropeslr_select_
  * bytes): the float32 approximate scores [B*H, nb, nbs] at *approx_offset
  * (row stride nbs: the first of 128, 256, 512, 1024 that is >= nb),
  * at *stats_offset an int32 count of rows decided wholly in float64 (rows
- * whose band held more than 64 blocks, or non-finite / very wide rows), and
+ * whose band held more than 32 blocks, or non-finite / very wide rows), and
  * at *diag_offset (may be NULL) an int32 per row: band size | bisection
  * steps << 16, or -1 for a row decided wholly in float64.  For tests and
  * measurement.  Returns ROPESLR_ERR_VALUE when this shape does not take the
@@ -240,6 +240,21 @@ int ropeslr_lowrank_branch(const ropeslr_shape* shape, const ropeslr_token_args*
                            const float* rms_lowrank, float eps,
                            void* y_lr, float* o_lr, float* g_logit,
                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* The same branch with its parameter-only tables built once: the W_A^T /
+ * W_B^T operand images and the per-axis PE folds Z_axis = (alpha P_axis)_h
+ * W_A and G_axis (what ropeslr_lowrank_branch rebuilds on every call).  They
+ * depend on w_a, w_b, alpha, w_g, the PE tables, the grid and the head slice
+ * only.  tcgen05 path only (bf16, d = 128, rank 16/32/48/64); _bytes
+ * returns 0 otherwise.  The folded call's workspace holds the gate partials,
+ * B*H*L floats (ropeslr_lowrank_workspace_bytes suffices). */
+size_t ropeslr_lowrank_tables_bytes(const ropeslr_shape* shape, const ropeslr_token_args* tok, int32_t rank);
+int ropeslr_lowrank_tables(const ropeslr_shape* shape, const ropeslr_token_args* tok, const float* w_a,
+                           const float* w_b, int32_t rank, void* tables, size_t tables_bytes, void* stream);
+int ropeslr_lowrank_branch_folded(const ropeslr_shape* shape, const ropeslr_token_args* tok, int32_t rank,
+                                  const void* tables, size_t tables_bytes, const float* rms_lowrank, float eps,
+                                  void* y_lr, float* o_lr, float* g_logit, void* workspace, size_t workspace_bytes,
+                                  void* stream);
 
 /* Gate logits alone: g_logit[b,l] = sum over the local columns of
  * x_hat[b,l,c] * w_g[c] (mechanism.py:249-255, 434; bias and sigmoid are

@@ -71,6 +71,10 @@ _SIGNATURES = {
                                       c_vp, c_sz, c_vp]),
     "ropeslr_sparse_attention": (c_i32, [P(Shape), c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "ropeslr_lowrank_workspace_bytes": (c_sz, [P(Shape), P(TokenArgs), c_i32]),
+    "ropeslr_lowrank_tables_bytes": (c_sz, [P(Shape), P(TokenArgs), c_i32]),
+    "ropeslr_lowrank_tables": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp, c_i32, c_vp, c_sz, c_vp]),
+    "ropeslr_lowrank_branch_folded": (c_i32, [P(Shape), P(TokenArgs), c_i32, c_vp, c_sz, c_vp, c_f32, c_vp, c_vp,
+                                              c_vp, c_vp, c_sz, c_vp]),
     "ropeslr_lowrank_branch": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp, c_i32, c_vp, c_f32, c_vp, c_vp, c_vp,
                                        c_vp, c_sz, c_vp]),
     "ropeslr_gate_logits": (c_i32, [P(Shape), P(TokenArgs), c_vp, c_vp]),

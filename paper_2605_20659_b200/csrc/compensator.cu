@@ -312,6 +312,12 @@ size_t lowrank_tc_workspace_bytes(int64_t B, int64_t H, int64_t L, int r, int T,
 bool lowrank_tc_eligible(const ropeslr_shape* s, int r);
 bool lowrank_umma_eligible(const ropeslr_shape* s, const ropeslr_token_args* t, int r);
 size_t lowrank_umma_workspace_bytes(const ropeslr_shape* s, const ropeslr_token_args* t, int r);
+size_t lowrank_umma_tables_bytes(const ropeslr_shape* s, const ropeslr_token_args* t, int r);
+int lowrank_umma_fold(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b, int r,
+                      void* tables, cudaStream_t st);
+int lowrank_umma_folded(const ropeslr_shape* s, const ropeslr_token_args* t, int r, const void* tables,
+                        const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, float* g_part,
+                        cudaStream_t st);
 int launch_lowrank_umma(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
                         int r, const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit,
                         void* ws, cudaStream_t st);
@@ -420,6 +426,46 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
                                     rms_lowrank, eps, static_cast<float*>(y_lr), o_lr, g_logit);
   }
   if (int e = launch_status()) return e;
+  return scan_nonfinite(g_logit, false, g_logit ? s->B * s->L : 0, t->nonfinite, ROPESLR_NONFINITE_X, stream_);
+}
+
+extern "C" size_t ropeslr_lowrank_tables_bytes(const ropeslr_shape* s, const ropeslr_token_args* t, int32_t rank) {
+  if (!s || !t || !lowrank_umma_eligible(s, t, rank)) return 0;
+  return lowrank_umma_tables_bytes(s, t, rank);
+}
+
+extern "C" int ropeslr_lowrank_tables(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a,
+                                      const float* w_b, int32_t rank, void* tables, size_t tables_bytes,
+                                      void* stream) {
+  int st = check_shape(s);
+  if (st) return st;
+  if ((st = check_token_args(s, t))) return st;
+  if (!w_a || !w_b || !tables) return ROPESLR_ERR_NULL;
+  if (!lowrank_umma_eligible(s, t, rank)) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(tables)) return ROPESLR_ERR_ALIGN;
+  if (tables_bytes < lowrank_umma_tables_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
+  return lowrank_umma_fold(s, t, w_a, w_b, rank, tables, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int ropeslr_lowrank_branch_folded(const ropeslr_shape* s, const ropeslr_token_args* t, int32_t rank,
+                                             const void* tables, size_t tables_bytes, const float* rms_lowrank,
+                                             float eps, void* y_lr, float* o_lr, float* g_logit, void* ws,
+                                             size_t ws_bytes, void* stream) {
+  int st = check_shape(s);
+  if (st) return st;
+  if ((st = check_token_args(s, t))) return st;
+  if (!tables || !rms_lowrank || !y_lr) return ROPESLR_ERR_NULL;
+  if (!(eps > 0.f)) return ROPESLR_ERR_VALUE;
+  if (!lowrank_umma_eligible(s, t, rank)) return ROPESLR_ERR_SHAPE;
+  if (t->x_row_stride % 8 || !aligned16(t->x) || !aligned32(y_lr) || !aligned16(tables)) return ROPESLR_ERR_ALIGN;
+  if (o_lr && !aligned16(o_lr)) return ROPESLR_ERR_ALIGN;
+  if (tables_bytes < lowrank_umma_tables_bytes(s, t, rank)) return ROPESLR_ERR_WORKSPACE;
+  const size_t need = static_cast<size_t>(s->B * s->H * s->L) * sizeof(float);
+  if (g_logit != nullptr && (!ws || ws_bytes < need)) return ROPESLR_ERR_WORKSPACE;
+  cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
+  if (int e = lowrank_umma_folded(s, t, rank, tables, rms_lowrank, eps, y_lr, o_lr, g_logit,
+                                  static_cast<float*>(ws), stream_))
+    return e;
   return scan_nonfinite(g_logit, false, g_logit ? s->B * s->L : 0, t->nonfinite, ROPESLR_NONFINITE_X, stream_);
 }
 

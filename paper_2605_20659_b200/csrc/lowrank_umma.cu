@@ -479,19 +479,26 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 size_t up(size_t x) { return (x + 255) / 256 * 256; }
 
+// The parameter-only part of the workspace (W_A^T / W_B^T images, Z, G),
+// then the gate partials.
 template <int R>
-size_t ws_bytes(int64_t B, int64_t H, int64_t L, int nrows) {
+size_t tables_bytes(int64_t H, int nrows) {
   return up(static_cast<size_t>(H) * Lay<R>::WA_BYTES) + up(static_cast<size_t>(H) * Lay<R>::WB_BYTES) +
-         up(static_cast<size_t>(H) * nrows * R * 4) + up(static_cast<size_t>(H) * nrows * 4) +
-         up(static_cast<size_t>(B * H * L) * 4);
+         up(static_cast<size_t>(H) * nrows * R * 4) + up(static_cast<size_t>(H) * nrows * 4);
 }
 
 template <int R>
-int launch(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
-           const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, void* ws, cudaStream_t st) {
+size_t ws_bytes(int64_t B, int64_t H, int64_t L, int nrows) {
+  return tables_bytes<R>(H, nrows) + up(static_cast<size_t>(B * H * L) * 4);
+}
+
+// The fold kernel's outputs inside a tables buffer.
+template <int R>
+FoldArgs fold_args(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
+                   void* tables) {
   const int H = static_cast<int>(s->H);
   const int nrows = t->grid_t + t->grid_h + t->grid_w;
-  uint8_t* p = static_cast<uint8_t*>(ws);
+  uint8_t* p = static_cast<uint8_t*>(tables);
   FoldArgs f;
   f.w_a = w_a;
   f.w_b = w_b;
@@ -515,11 +522,25 @@ int launch(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a
   f.Z = reinterpret_cast<float*>(p);
   p += up(static_cast<size_t>(H) * nrows * R * 4);
   f.G = reinterpret_cast<float*>(p);
-  p += up(static_cast<size_t>(H) * nrows * 4);
-  float* g_part = reinterpret_cast<float*>(p);
-  lowrank_fold_umma_kernel<R><<<dim3(nrows + 2, H), 128, 0, st>>>(f);
-  if (launch_status()) return ROPESLR_ERR_LAUNCH;
+  return f;
+}
 
+template <int R>
+int fold(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b, void* tables,
+         cudaStream_t st) {
+  const FoldArgs f = fold_args<R>(s, t, w_a, w_b, tables);
+  const int nrows = t->grid_t + t->grid_h + t->grid_w;
+  lowrank_fold_umma_kernel<R><<<dim3(nrows + 2, f.H), 128, 0, st>>>(f);
+  return launch_status();
+}
+
+// The main kernel (+ the gate sum) from folded tables; g_part: B*H*L floats.
+template <int R>
+int run_main(const ropeslr_shape* s, const ropeslr_token_args* t, const void* tables, const float* rms_lowrank,
+             float eps, void* y_lr, float* o_lr, float* g_logit, float* g_part, cudaStream_t st) {
+  const int H = static_cast<int>(s->H);
+  const int nrows = t->grid_t + t->grid_h + t->grid_w;
+  const FoldArgs f = fold_args<R>(s, t, nullptr, nullptr, const_cast<void*>(tables));
   auto enc = encode_fn();
   if (enc == nullptr) return ROPESLR_ERR_LAUNCH;
   CUtensorMap mx;
@@ -566,6 +587,15 @@ int launch(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a
   return launch_status();
 }
 
+template <int R>
+int launch(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
+           const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, void* ws, cudaStream_t st) {
+  const int nrows = t->grid_t + t->grid_h + t->grid_w;
+  if (int e = fold<R>(s, t, w_a, w_b, ws, st)) return e;
+  float* g_part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + tables_bytes<R>(s->H, nrows));
+  return run_main<R>(s, t, ws, rms_lowrank, eps, y_lr, o_lr, g_logit, g_part, st);
+}
+
 }  // namespace lu
 
 // r % 16 == 0, r <= 112 keeps GEMM1's N (r + 16) within one 128-column TMEM
@@ -587,6 +617,39 @@ size_t lowrank_umma_workspace_bytes(const ropeslr_shape* s, const ropeslr_token_
     case 32: return lu::ws_bytes<32>(s->B, s->H, s->L, nrows);
     case 48: return lu::ws_bytes<48>(s->B, s->H, s->L, nrows);
     default: return lu::ws_bytes<64>(s->B, s->H, s->L, nrows);
+  }
+}
+
+size_t lowrank_umma_tables_bytes(const ropeslr_shape* s, const ropeslr_token_args* t, int r) {
+  const int nrows = t->grid_t + t->grid_h + t->grid_w;
+  switch (r) {
+    case 16: return lu::tables_bytes<16>(s->H, nrows);
+    case 32: return lu::tables_bytes<32>(s->H, nrows);
+    case 48: return lu::tables_bytes<48>(s->H, nrows);
+    default: return lu::tables_bytes<64>(s->H, nrows);
+  }
+}
+
+int lowrank_umma_fold(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b, int r,
+                      void* tables, cudaStream_t st) {
+  switch (r) {
+    case 16: return lu::fold<16>(s, t, w_a, w_b, tables, st);
+    case 32: return lu::fold<32>(s, t, w_a, w_b, tables, st);
+    case 48: return lu::fold<48>(s, t, w_a, w_b, tables, st);
+    case 64: return lu::fold<64>(s, t, w_a, w_b, tables, st);
+    default: return ROPESLR_ERR_SHAPE;
+  }
+}
+
+int lowrank_umma_folded(const ropeslr_shape* s, const ropeslr_token_args* t, int r, const void* tables,
+                        const float* rms_lowrank, float eps, void* y_lr, float* o_lr, float* g_logit, float* g_part,
+                        cudaStream_t st) {
+  switch (r) {
+    case 16: return lu::run_main<16>(s, t, tables, rms_lowrank, eps, y_lr, o_lr, g_logit, g_part, st);
+    case 32: return lu::run_main<32>(s, t, tables, rms_lowrank, eps, y_lr, o_lr, g_logit, g_part, st);
+    case 48: return lu::run_main<48>(s, t, tables, rms_lowrank, eps, y_lr, o_lr, g_logit, g_part, st);
+    case 64: return lu::run_main<64>(s, t, tables, rms_lowrank, eps, y_lr, o_lr, g_logit, g_part, st);
+    default: return ROPESLR_ERR_SHAPE;
   }
 }
 

@@ -84,10 +84,15 @@ __global__ void __launch_bounds__(256) pool_blocks_kernel(const T* __restrict__ 
 // copy into shared memory (so the bytes in flight do not depend on register
 // occupancy), then summed in float64 from there.  256 threads: column chunk
 // c = t % 16 (8 columns), rows t / 16 + 16 i.
+// With img != NULL it also writes the screening path's bf16 hi / lo image
+// rows and the row norm (what screen_image_kernel does, without re-reading
+// the means).
 __global__ void __launch_bounds__(256) pool_blocks_bulk_kernel(const __nv_bfloat16* __restrict__ q,
                                                                const __nv_bfloat16* __restrict__ k,
                                                                double* __restrict__ pooled, int64_t L, int block,
-                                                               int nb, int64_t BH, int64_t bh0) {
+                                                               int nb, int64_t BH, int64_t bh0,
+                                                               uint8_t* __restrict__ img, float* __restrict__ norms,
+                                                               int ntile) {
   constexpr int D = 128;
   __shared__ __align__(128) uint8_t buf[128 * D * 2];  // the block's rows; then the f64 partial sums
   __shared__ uint64_t bar;
@@ -126,10 +131,32 @@ __global__ void __launch_bounds__(256) pool_blocks_bulk_kernel(const __nv_bfloat
 #pragma unroll
   for (int i = 0; i < 8; ++i) sred[rr * D + ch * 8 + i] = acc[i];
   __syncthreads();
+  __shared__ double nsq[4];
   if (tid < D) {
     double s = 0.0;
     for (int j = 0; j < 16; ++j) s += sred[j * D + tid];
-    pooled[((static_cast<int64_t>(blockIdx.z) * BH + bh) * nb + b) * D + tid] = s / static_cast<double>(rows);
+    const double m = s / static_cast<double>(rows);
+    pooled[((static_cast<int64_t>(blockIdx.z) * BH + bh) * nb + b) * D + tid] = m;
+    if (img != nullptr) {
+      constexpr int ATOM = 128 * 128, TILE = 2 * ATOM;
+      const __nv_bfloat16 hi = __double2bfloat16(m);
+      const __nv_bfloat16 lo = __double2bfloat16(m - static_cast<double>(__bfloat162float(hi)));
+      const int atom = tid >> 6, ch = (tid & 63) >> 3, el = tid & 7, rr = b & 127, tile = b >> 7;
+      const int64_t off = atom * ATOM + rr * 128 + ((ch ^ (rr & 7)) << 4) + el * 2;
+      const int z = blockIdx.z;
+      *reinterpret_cast<__nv_bfloat16*>(img + (((z * 2 + 0) * BH + bh) * ntile + tile) * TILE + off) = hi;
+      *reinterpret_cast<__nv_bfloat16*>(img + (((z * 2 + 1) * BH + bh) * ntile + tile) * TILE + off) = lo;
+      double q2 = m * m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+      if ((tid & 31) == 0) nsq[tid >> 5] = q2;
+    }
+  }
+  if (img != nullptr) {
+    __syncthreads();
+    if (tid == 0)
+      norms[(static_cast<int64_t>(blockIdx.z) * BH + bh) * nb + b] =
+          __double2float_ru(__dsqrt_ru(nsq[0] + nsq[1] + nsq[2] + nsq[3]));
   }
 }
 
@@ -718,9 +745,9 @@ constexpr int ROWS = 128;              // rows of a tile
 constexpr int ATOM = ROWS * 128;       // 16 KiB: 128 rows x 64 bf16, 128B-swizzled
 constexpr int TILE = 2 * ATOM;         // 128 rows x 128 bf16 (one split)
 constexpr double kScreenBound = 1.0 / 4096.0;
-constexpr int kScreenBand = 64;
+constexpr int kScreenBand = 32;
 constexpr int EPI_WARPS = 8;
-constexpr int SMEM = 1024 + 2 * TILE + 2 * 2 * TILE + EPI_WARPS * 32 * 33 * 4 + 16 * 8;
+constexpr int SMEM = 1024 + 2 * TILE + 2 * 2 * TILE + EPI_WARPS * 32 * 33 * 4 + 16 * 8;  // 226.1 KiB
 }  // namespace scr
 
 
@@ -729,10 +756,9 @@ constexpr int SMEM = 1024 + 2 * TILE + 2 * 2 * TILE + EPI_WARPS * 32 * 33 * 4 + 
 // [z][hi/lo][BH][ntile][TILE].
 __global__ void __launch_bounds__(256) screen_image_kernel(const double* __restrict__ pooled, int nb, int ntile,
                                                            int64_t BH, uint8_t* __restrict__ img,
-                                                           float* __restrict__ norms, int* __restrict__ stats) {
+                                                           float* __restrict__ norms) {
   using namespace scr;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (stats != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) stats[0] = 0;
   const int z = blockIdx.z;
   const int64_t bh = blockIdx.y;
   const int r = blockIdx.x * 8 + warp;
@@ -763,20 +789,23 @@ __global__ void __launch_bounds__(256) screen_image_kernel(const double* __restr
   if (lane == 0 && r < nb) norms[(z * BH + bh) * nb + r] = __double2float_ru(__dsqrt_ru(ss));
 }
 
-// grid (ntile, BH), 384 threads, one CTA per SM.  Warp 0: bulk copies (the
-// CTA's 128 Q rows once, then K tiles through a 2-stage ring); warp 1: the
-// MMAs, 3 per 16-wide k-step into one of four 128-column TMEM
-// accumulators; warp 3 of tile 0: max_j |k_j| of the head; warps 4-11: the
-// epilogue, two warps per TMEM lane quarter with 64 columns each (scale,
-// transpose through shared memory, coalesced row stores of approx
-// [BH][nb][nb]).
+// Persistent: grid = min(SMs, items), 384 threads, one CTA per SM; CTA c
+// takes a contiguous range of the items (head, row tile, key tile), so the
+// 128 Q rows (A operand, hi | lo) are reloaded only when (head, row tile)
+// changes.  Warp 0: bulk copies (A when it changes, after the MMAs of the
+// previous A; K tiles through a 2-stage ring); warp 1: the MMAs, 3 per
+// 16-wide k-step into one of four 128-column TMEM accumulators; warp 3:
+// max_j |k_j| of each head it meets; warps 4-11: the epilogue, two warps per
+// TMEM lane quarter with 64 columns each (scale, transpose through shared
+// memory, coalesced row stores of approx [BH][nb][nbs]).
 __global__ void __launch_bounds__(384, 1) screen_scores_kernel(const uint8_t* __restrict__ img,
                                                                 const float* __restrict__ norms, int nb, int nbs,
                                                                 int ntile, int64_t BH, float scale,
                                                                 float* __restrict__ approx,
-                                                                float* __restrict__ kmaxn) {
+                                                                float* __restrict__ kmaxn, int* __restrict__ stats) {
   using namespace scr;
   using namespace sm100;
+  if (blockIdx.x == 0 && threadIdx.x == 0) stats[0] = 0;  // rows deferred by screen_select_kernel
   extern __shared__ uint8_t scr_smem[];
   uint8_t* sm = scr_smem + ((1024u - (smem_u32(scr_smem) & 1023u)) & 1023u);
   uint8_t* sA = sm;                 // [hi tile | lo tile]
@@ -784,19 +813,23 @@ __global__ void __launch_bounds__(384, 1) screen_scores_kernel(const uint8_t* __
   float* sT = reinterpret_cast<float*>(sB + 4 * TILE);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sT + EPI_WARPS * 32 * 33);
   uint64_t* afull = bars;
-  uint64_t* bfull = bars + 1;   // [2]
-  uint64_t* bempty = bars + 3;  // [2]
-  uint64_t* tfull = bars + 5;   // [4]
-  uint64_t* tempty = bars + 9;  // [4]
+  uint64_t* aempty = bars + 1;
+  uint64_t* bfull = bars + 2;   // [2]
+  uint64_t* bempty = bars + 4;  // [2]
+  uint64_t* tfull = bars + 6;   // [4]
+  uint64_t* tempty = bars + 10;  // [4]
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int64_t bh = blockIdx.y;
-  // blockIdx.z: which part of the key tiles (more CTAs than SMs' worth of rows)
-  const int per = (ntile + gridDim.z - 1) / gridDim.z;
-  const int n0 = blockIdx.z * per, nn = min(ntile, n0 + per) - n0;
+  const int64_t items = BH * ntile * ntile;
+  const int64_t per = (items + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * per;
+  const int64_t i1 = items < i0 + per ? items : i0 + per;
+  const int nn = i1 > i0 ? static_cast<int>(i1 - i0) : 0;
+  // item i: head bh, row tile rt, key tile kt; the A group of an item
+  auto group = [&](int64_t it) { return it / ntile; };
   if (threadIdx.x == 0) {
     mbar_init(afull, 1);
+    mbar_init(aempty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
@@ -814,30 +847,37 @@ __global__ void __launch_bounds__(384, 1) screen_scores_kernel(const uint8_t* __
   const uint32_t tmem = tmem_slot;
   if (warp == 0) {
     if (elect_one()) {
-      const uint8_t* qh = img + ((0 * BH + bh) * ntile + tile) * TILE;
-      const uint8_t* ql = img + ((1 * BH + bh) * ntile + tile) * TILE;
-      const uint8_t* kh = img + ((2 * BH + bh) * ntile) * TILE;
-      const uint8_t* kl = img + ((3 * BH + bh) * ntile) * TILE;
-      mbar_arrive_expect_tx(afull, 2 * TILE);
-      bulk_load_1d(sA, qh, TILE, afull, policy_evict_first());
-      bulk_load_1d(sA + TILE, ql, TILE, afull, policy_evict_first());
+      int na = 0;
       for (int n = 0; n < nn; ++n) {
+        const int64_t it = i0 + n, g = group(it);
+        const int64_t bh = g / ntile;
+        const int kt = static_cast<int>(it % ntile);
+        if (n == 0 || g != group(it - 1)) {
+          if (na > 0) mbar_wait(aempty, (na - 1) & 1);
+          const int rt = static_cast<int>(g % ntile);
+          mbar_arrive_expect_tx(afull, 2 * TILE);
+          bulk_load_1d(sA, img + ((0 * BH + bh) * ntile + rt) * TILE, TILE, afull, policy_evict_first());
+          bulk_load_1d(sA + TILE, img + ((1 * BH + bh) * ntile + rt) * TILE, TILE, afull, policy_evict_first());
+          ++na;
+        }
         const int s = n & 1;
         if (n >= 2) mbar_wait(&bempty[s], ((n >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&bfull[s], 2 * TILE);
-        bulk_load_1d(sB + s * 2 * TILE, kh + static_cast<int64_t>(n0 + n) * TILE, TILE, &bfull[s],
+        bulk_load_1d(sB + s * 2 * TILE, img + ((2 * BH + bh) * ntile + kt) * TILE, TILE, &bfull[s],
                      policy_evict_last());
-        bulk_load_1d(sB + s * 2 * TILE + TILE, kl + static_cast<int64_t>(n0 + n) * TILE, TILE, &bfull[s],
+        bulk_load_1d(sB + s * 2 * TILE + TILE, img + ((3 * BH + bh) * ntile + kt) * TILE, TILE, &bfull[s],
                      policy_evict_last());
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = idesc_bf16_f32(ROWS, ROWS, false, false);
     const bool leader = elect_one();
-    mbar_wait(afull, 0);
     const uint64_t dAh = desc_sw128(smem_u32(sA), 16, 1024), dAl = desc_sw128(smem_u32(sA + TILE), 16, 1024);
+    int na = 0;
     for (int n = 0; n < nn; ++n) {
+      const int64_t it = i0 + n, g = group(it);
       const int s = n & 1, a = n & 3;
+      if (n == 0 || g != group(it - 1)) mbar_wait(afull, (na++) & 1);
       mbar_wait(&bfull[s], (n >> 1) & 1);
       if (n >= 4) mbar_wait(&tempty[a], ((n >> 2) - 1) & 1);
       tc_fence_after();
@@ -854,25 +894,34 @@ __global__ void __launch_bounds__(384, 1) screen_scores_kernel(const uint8_t* __
         }
         mma_commit(&bempty[s]);
         mma_commit(&tfull[a]);
+        // the A of this group is done with after its last item
+        if (n + 1 == nn || group(it + 1) != g) mma_commit(aempty);
       }
       __syncwarp();
     }
   } else if (warp == 3) {
-    if (tile == 0 && blockIdx.z == 0) {
+    int64_t last_bh = -1;
+    for (int n = 0; n < nn; ++n) {
+      const int64_t bh = group(i0 + n) / ntile;
+      if (bh == last_bh) continue;
+      last_bh = bh;
       const float* kn = norms + (BH + bh) * nb;
       float m = 0.f;
       for (int j = lane; j < nb; j += 32) m = fmaxf(m, kn[j]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) kmaxn[bh] = m;
+      if (lane == 0) kmaxn[bh] = m;  // every CTA meeting this head writes the same value
     }
   } else if (warp >= 4) {
     const int ew = warp - 4, q4 = warp & 3, half = ew >> 2;
     float* T = sT + ew * 32 * 33;
-    float* out = approx + bh * nb * static_cast<int64_t>(nbs);
-    const int row0 = tile * ROWS + q4 * 32;
-    const int rmax = min(32, nb - row0);
     for (int n = 0; n < nn; ++n) {
+      const int64_t it = i0 + n, g = group(it);
+      const int64_t bh = g / ntile;
+      const int rt = static_cast<int>(g % ntile), kt = static_cast<int>(it % ntile);
+      float* out = approx + bh * nb * static_cast<int64_t>(nbs);
+      const int row0 = rt * ROWS + q4 * 32;
+      const int rmax = min(32, nb - row0);
       const int a = n & 3;
       mbar_wait(&tfull[a], (n >> 2) & 1);
       tc_fence_after();
@@ -885,11 +934,11 @@ __global__ void __launch_bounds__(384, 1) screen_scores_kernel(const uint8_t* __
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
+      for (int gg = 0; gg < 2; ++gg) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(g ? r1[j] : r0[j]) * scale;
+        for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(gg ? r1[j] : r0[j]) * scale;
         __syncwarp();
-        const int col = (n0 + n) * ROWS + half * 64 + g * 32 + lane;
+        const int col = kt * ROWS + half * 64 + gg * 32 + lane;
         if (col < nb)
           for (int rr = 0; rr < rmax; ++rr) out[static_cast<int64_t>(row0 + rr) * nbs + col] = T[rr * 33 + lane];
         __syncwarp();
@@ -924,37 +973,43 @@ struct ScreenArgs {
 // One warp per row: a bracket [lo, hi] of the k-th best approximate score,
 // the band, float64 scores of the band, the exact decision.  Rows that
 // cannot be decided this way go to a list for screen_exact_kernel.  Lane l
-// holds the NPER consecutive columns [l NPER, l NPER + NPER) (the approx
-// rows are padded to 32 NPER floats), so every compaction -- the band, the
-// ascending index list -- is one prefix sum over the lanes.
+// loads float4 j of its row at 32 j + l (coalesced; the approx rows are
+// padded to 32 NPER floats), so value b is column 128 (b / 4) + 4 l + b % 4;
+// the band is compacted by one prefix sum over the lanes (any order), the
+// selection is regrouped into 32-column words (one per lane) for the
+// ascending index list.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <int NPER>
-__global__ void __launch_bounds__(256, 4) screen_select_kernel(const ScreenArgs a) {
+__device__ __forceinline__ void screen_one_row(const ScreenArgs& a, int64_t row, int lane, int* listA) {
   using namespace scr;
-  __shared__ int listA[8][kScreenBand];
-  __shared__ uint64_t keyA[8][kScreenBand];
-  __shared__ uint8_t selA[8][kScreenBand];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-  if (row >= a.rows) return;
   const int nb = a.nb;
   const int64_t bh = row / nb;
-  const int c0 = lane * NPER;
-  const float4* arow = reinterpret_cast<const float4*>(a.approx + row * (32 * NPER)) + lane * (NPER / 4);
+  // value b of a lane: column 128 (b / 4) + 4 lane + b % 4 (coalesced float4 loads)
+  auto col = [&](int b) { return 128 * (b >> 2) + 4 * lane + (b & 3); };
+  // every load of the row up front: its approximate scores, its Q mean
+  // (4 columns per lane, for the float64 scores of the band), its bound
+  const float4* arow = reinterpret_cast<const float4*>(a.approx + row * (32 * NPER)) + lane;
   float v[NPER];
 #pragma unroll
   for (int j = 0; j < NPER / 4; ++j) {
-    const float4 t = arow[j];
+    const float4 t = arow[32 * j];
     v[4 * j] = t.x;
     v[4 * j + 1] = t.y;
     v[4 * j + 2] = t.z;
     v[4 * j + 3] = t.w;
   }
+  const double2 q01 = reinterpret_cast<const double2*>(a.pooled + row * D)[lane * 2];
+  const double2 q23 = reinterpret_cast<const double2*>(a.pooled + row * D)[lane * 2 + 1];
+  const float qn = a.norms[row], kn = a.kmaxn[bh];
   float vmax = -INFINITY, vmin = INFINITY, vsum = 0.f, vsq = 0.f;
 #pragma unroll
   for (int i = 0; i < NPER; ++i) {
     // padding is NaN: ignored by fmaxf / fminf, above nothing, in no band
-    if (c0 + i >= nb) v[i] = __int_as_float(0x7fffffff);
-    const float u = c0 + i < nb ? v[i] : 0.f;
+    if (col(i) >= nb) v[i] = __int_as_float(0x7fffffff);
+    const float u = col(i) < nb ? v[i] : 0.f;
     vmax = fmaxf(vmax, v[i]);
     vmin = fminf(vmin, v[i]);
     vsum += u;  // a NaN / inf score anywhere makes this non-finite
@@ -969,15 +1024,18 @@ __global__ void __launch_bounds__(256, 4) screen_select_kernel(const ScreenArgs 
   }
   const bool bad = !isfinite(vsum) || !isfinite(vsq);
   const int need = a.topk < nb ? a.topk : nb;
-  const double E = kScreenBound * static_cast<double>(a.norms[row]) * static_cast<double>(a.kmaxn[bh]) * a.inv_sqrt_d *
-                       (1.0 + 1e-6) + 1e-300;
+  const double E = kScreenBound * static_cast<double>(qn) * static_cast<double>(kn) * a.inv_sqrt_d * (1.0 + 1e-6) +
+                   1e-300;
   uint32_t bits = 0;
   if (need < nb) {
-    if (bad || !(E < 1e300) || static_cast<double>(vmax) - static_cast<double>(vmin) > 700.0) {
+    auto defer = [&]() {
       if (lane == 0) {
         a.full_list[atomicAdd(a.full_count, 1)] = static_cast<int>(row);
         a.diag[row] = -1;
       }
+    };
+    if (bad || !(E < 1e300) || static_cast<double>(vmax) - static_cast<double>(vmin) > 700.0) {
+      defer();
       return;
     }
     // count(v > x): the sign of x - v (exact: x - v is 0 only for x == v,
@@ -1057,25 +1115,27 @@ __global__ void __launch_bounds__(256, 4) screen_select_kernel(const ScreenArgs 
     }
     const int nA = __shfl_sync(0xffffffffu, incl, 31);
     if (nA > kScreenBand) {
-      if (lane == 0) {
-        a.full_list[atomicAdd(a.full_count, 1)] = static_cast<int>(row);
-        a.diag[row] = -1;
-      }
+      defer();
       return;
     }
     if (lane == 0) a.diag[row] = nA | (it << 16);
     {
       int p = incl - myA;
-      for (uint32_t m = abits; m; m &= m - 1) listA[warp][p++] = c0 + __ffs(m) - 1;
+      for (uint32_t m = abits; m; m &= m - 1) listA[p++] = col(__ffs(m) - 1);
     }
     __syncwarp();
-    // float64 scores of the band, two rows of K in flight
-    const double* qrow = a.pooled + row * D;
     const double* kbase = a.pooled + (a.BH + bh) * nb * D;
-    const double2 q01 = reinterpret_cast<const double2*>(qrow)[lane * 2];
-    const double2 q23 = reinterpret_cast<const double2*>(qrow)[lane * 2 + 1];
+    // the band's K means into L1 at once (lane: one 128-byte line of one
+    // entry, four entries per pass), so the dot products below do not pay
+    // one L2 round trip per pair
+    for (int b0 = 0; b0 < nA; b0 += 4)
+      if (b0 + (lane >> 3) < nA) prefetch_l1(kbase + static_cast<int64_t>(listA[b0 + (lane >> 3)]) * D + (lane & 7) * 16);
+    // float64 scores of the band (warp dot products, two K rows in flight);
+    // lane b keeps band entry b
+    const int cb = lane < nA ? listA[lane] : 0;
+    double pm = 0.0;
     for (int b = 0; b < nA; b += 2) {
-      const int j0 = listA[warp][b], j1 = listA[warp][b + 1 < nA ? b + 1 : b];
+      const int j0 = listA[b], j1 = listA[b + 1 < nA ? b + 1 : b];
       const double2* k0 = reinterpret_cast<const double2*>(kbase + static_cast<int64_t>(j0) * D) + lane * 2;
       const double2* k1 = reinterpret_cast<const double2*>(kbase + static_cast<int64_t>(j1) * D) + lane * 2;
       const double2 a0 = k0[0], a1 = k0[1], b0 = k1[0], b1 = k1[1];
@@ -1091,37 +1151,44 @@ __global__ void __launch_bounds__(256, 4) screen_select_kernel(const ScreenArgs 
         p0 += __shfl_xor_sync(0xffffffffu, p0, o);
         p1 += __shfl_xor_sync(0xffffffffu, p1, o);
       }
-      if (lane == 0) {
-        keyA[warp][b] = desc_key(p0 / a.sqrt_d);
-        if (b + 1 < nA) keyA[warp][b + 1] = desc_key(p1 / a.sqrt_d);
-      }
+      if (lane == b) pm = p0;
+      if (lane == b + 1) pm = p1;
     }
-    __syncwarp();
+    const uint64_t key = lane < nA ? desc_key(pm / a.sqrt_d) : ~0ull;
     // the band's best need - nD by (float64 score, then lower block)
-    const int needA = need - nD;
-    for (int xx = lane; xx < nA; xx += 32) {
-      const uint64_t kx = keyA[warp][xx];
-      const int cx = listA[warp][xx];
-      int rank = 0;
-      for (int y = 0; y < nA; ++y) {
-        const uint64_t ky = keyA[warp][y];
-        rank += (ky < kx) || (ky == kx && listA[warp][y] < cx);
-      }
-      selA[warp][xx] = rank < needA;
+    int rank = 0;
+    for (int y = 0; y < nA; ++y) {
+      const uint64_t ky = __shfl_sync(0xffffffffu, key, y);
+      const int cy = __shfl_sync(0xffffffffu, cb, y);
+      rank += (ky < key) || (ky == key && cy < cb);
     }
-    __syncwarp();
+    const uint32_t won = __ballot_sync(0xffffffffu, lane < nA && rank < need - nD);
     {
       int p = incl - myA;
       for (uint32_t m = abits; m; m &= m - 1, ++p)
-        if (selA[warp][p]) bits |= 1u << (__ffs(m) - 1);
+        if ((won >> p) & 1u) bits |= 1u << (__ffs(m) - 1);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < NPER; ++i) bits |= static_cast<uint32_t>(c0 + i < nb) << i;
+    for (int i = 0; i < NPER; ++i) bits |= static_cast<uint32_t>(col(i) < nb) << i;
+  }
+  // the selection as 32-column words, lane w holding columns [32 w, 32 w +
+  // 32): nibble j of lane l is columns 128 j + 4 l .. + 3, i.e. word 4 j +
+  // l / 8, bits 4 (l % 8) ..; OR them across each 8-lane group, then lane w
+  // takes word w from group w % 4 of nibble w / 4
+  uint32_t word = 0;
+#pragma unroll
+  for (int j = 0; j < NPER / 4; ++j) {
+    uint32_t x = ((bits >> (4 * j)) & 15u) << (4 * (lane & 7));
+    x |= __shfl_xor_sync(0xffffffffu, x, 1);
+    x |= __shfl_xor_sync(0xffffffffu, x, 2);
+    x |= __shfl_xor_sync(0xffffffffu, x, 4);
+    const uint32_t y = __shfl_sync(0xffffffffu, x, 8 * (lane & 3));
+    if ((lane >> 2) == j) word = y;
   }
   // outputs: ascending index list (lane-major = column order), count,
   // mask, attended pairs
-  const int mine = __popc(bits);
+  const int mine = __popc(word);
   int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1129,22 +1196,38 @@ __global__ void __launch_bounds__(256, 4) screen_select_kernel(const ScreenArgs 
     if (lane >= o) incl += t;
   }
   int32_t* irow = a.idx + row * a.kmax + (incl - mine);
-  for (uint32_t m = bits; m; m &= m - 1) *irow++ = c0 + __ffs(m) - 1;
+  for (uint32_t m = word; m; m &= m - 1) *irow++ = 32 * lane + __ffs(m) - 1;
   if (a.mask != nullptr) {
     uint8_t* mrow = a.mask + row * nb;
-#pragma unroll
-    for (int i = 0; i < NPER; ++i)
-      if (c0 + i < nb) mrow[c0 + i] = (bits >> i) & 1u;
+    for (int i = 0; i < 32 && 32 * lane + i < nb; ++i) mrow[32 * lane + i] = (word >> i) & 1u;
   }
   // every selected block has `block` keys except a selected ragged last one
   const int last = nb - 1;
-  const bool last_sel = __any_sync(0xffffffffu, last / NPER == lane && ((bits >> (last % NPER)) & 1u));
+  const bool last_sel = __any_sync(0xffffffffu, last / 32 == lane && ((word >> (last % 32)) & 1u));
   if (lane == 0) {
     const int qb = static_cast<int>(row % nb);
     const long long ksum = static_cast<long long>(need) * a.block -
                            (last_sel ? static_cast<long long>(nb) * a.block - a.L : 0);
     a.cnt[row] = need;
     atomicAdd(a.attended + bh, static_cast<unsigned long long>(ksum * block_size(a.L, a.block, qb)));
+  }
+}
+
+// Persistent warps over the rows; each warp prefetches its next row's
+// approximate scores and Q mean into L1 before deciding the current one.
+template <int NPER>
+__global__ void __launch_bounds__(256, NPER >= 32 ? 3 : 4) screen_select_kernel(const ScreenArgs a) {
+  __shared__ int listA[8][scr::kScreenBand];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * 8;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp; row < a.rows; row += stride) {
+    const int64_t next = row + stride;
+    if (next < a.rows) {
+      if (lane < NPER) prefetch_l1(a.approx + next * (32 * NPER) + lane * 32);
+      if (lane < 8) prefetch_l1(a.pooled + next * scr::D + lane * 16);
+    }
+    screen_one_row<NPER>(a, row, lane, listA[warp]);
+    __syncwarp();
   }
 }
 
@@ -1285,7 +1368,7 @@ static size_t scores_bytes(const ropeslr_shape* s) {
 // Top-k of every row through the screening kernels (area: the scores area).
 static int launch_screen(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
                          int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended, uint8_t* area,
-                         cudaStream_t st) {
+                         bool have_img, cudaStream_t st) {
   const int64_t BH = s->B * s->H;
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
   const int ntile = static_cast<int>(ceil_div(nb, scr::ROWS));
@@ -1296,18 +1379,17 @@ static int launch_screen(const ropeslr_shape* s, const ropeslr_select_params* se
   float* norms = reinterpret_cast<float*>(area + y.norms);
   float* kmaxn = reinterpret_cast<float*>(area + y.kmaxn);
   int* stats = reinterpret_cast<int*>(area + y.stats);
-  screen_image_kernel<<<dim3(static_cast<unsigned>(ntile * 16), static_cast<unsigned>(BH), 2), 256, 0, st>>>(
-      pooled, nb, ntile, BH, img, norms, stats);
+  if (!have_img)
+    screen_image_kernel<<<dim3(static_cast<unsigned>(ntile * 16), static_cast<unsigned>(BH), 2), 256, 0, st>>>(
+        pooled, nb, ntile, BH, img, norms);
   if (cudaFuncSetAttribute(screen_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, scr::SMEM) !=
       cudaSuccess)
     return ROPESLR_ERR_LAUNCH;
-  // split the key tiles when the (row tile, head) CTAs alone would leave a
-  // partial second wave
-  const unsigned nsplit = ntile >= 4 && ntile * BH < 4 * num_sms() ? 2u : 1u;
-  screen_scores_kernel<<<dim3(static_cast<unsigned>(ntile), static_cast<unsigned>(BH), nsplit),
-                         128 + 32 * scr::EPI_WARPS,
-                         scr::SMEM, st>>>(
-      img, norms, nb, nbs, ntile, BH, static_cast<float>(1.0 / sqrt(static_cast<double>(scr::D))), approx, kmaxn);
+  const int64_t items = BH * ntile * static_cast<int64_t>(ntile);
+  const unsigned grid_s = static_cast<unsigned>(std::min<int64_t>(items, num_sms()));
+  screen_scores_kernel<<<grid_s, 128 + 32 * scr::EPI_WARPS, scr::SMEM, st>>>(
+      img, norms, nb, nbs, ntile, BH, static_cast<float>(1.0 / sqrt(static_cast<double>(scr::D))), approx, kmaxn,
+      stats);
   ScreenArgs a{};
   a.approx = approx;
   a.pooled = pooled;
@@ -1330,13 +1412,16 @@ static int launch_screen(const ropeslr_shape* s, const ropeslr_select_params* se
   a.cnt = cnt;
   a.mask = mask;
   a.attended = reinterpret_cast<unsigned long long*>(attended);
-  const unsigned grid = static_cast<unsigned>(ceil_div(a.rows, 8));
-  // the exact pass: enough warps for a list of every row, at most 4 CTAs per SM
+  // the selection: persistent warps, as many CTAs of 8 as fit per SM (3 for
+  // NPER 32: 78 registers, no spills; 4 below); the exact pass: enough warps
+  // for a list of every row
   const unsigned grid_x = static_cast<unsigned>(std::min<int64_t>(ceil_div(a.rows, 8), 4 * num_sms()));
-#define ROPESLR_SCREEN_CASE(NPER_)                                  \
-  do {                                                              \
-    screen_select_kernel<NPER_><<<grid, 256, 0, st>>>(a);           \
-    screen_exact_kernel<NPER_><<<grid_x, 256, 0, st>>>(a);          \
+#define ROPESLR_SCREEN_CASE(NPER_)                                                                        \
+  do {                                                                                                    \
+    const unsigned grid = static_cast<unsigned>(                                                          \
+        std::min<int64_t>(ceil_div(a.rows, 8), ((NPER_) >= 32 ? 3 : 4) * static_cast<int64_t>(num_sms()))); \
+    screen_select_kernel<NPER_><<<grid, 256, 0, st>>>(a);                                                 \
+    screen_exact_kernel<NPER_><<<grid_x, 256, 0, st>>>(a);                                                \
   } while (0)
   if (nb <= 128)
     ROPESLR_SCREEN_CASE(4);
@@ -1419,21 +1504,21 @@ static int launch_select(const ropeslr_shape* s, const ropeslr_select_params* se
 // float64), else NULL; area: the workspace's scores area.
 static int select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel, const double* pooled,
                               int32_t* idx, int32_t kmax, int32_t* cnt, uint8_t* mask, int64_t* attended,
-                              double* scores_out, uint8_t* area, cudaStream_t st) {
+                              double* scores_out, uint8_t* area, cudaStream_t st, bool have_img = false) {
   const int64_t BH = s->B * s->H;
   const int d = static_cast<int>(s->d);
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
   if (cudaMemsetAsync(attended, 0, sizeof(int64_t) * BH, st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
   if (int e = scan_nonfinite(pooled, true, 2 * BH * nb * d, sel->nonfinite, ROPESLR_NONFINITE_QK, st)) return e;
   if (scores_out == nullptr && screen_eligible(s, sel->topk))
-    return launch_screen(s, sel, pooled, idx, kmax, cnt, mask, attended, area, st);
+    return launch_screen(s, sel, pooled, idx, kmax, cnt, mask, attended, area, have_img, st);
   double* scores = scores_out ? scores_out : reinterpret_cast<double*>(area);
   if (int e = launch_scores(pooled, scores, nb, d, BH, 0, BH, st)) return e;
   return launch_select(s, sel, scores, idx, kmax, cnt, mask, attended, 0, BH, st);
 }
 
 static int launch_pool(const ropeslr_shape* s, const void* q, const void* k, double* pooled, int64_t bh0, int64_t bh1,
-                       cudaStream_t st) {
+                       cudaStream_t st, uint8_t* img = nullptr, float* norms = nullptr, bool* wrote_img = nullptr) {
   const int64_t BH = s->B * s->H;
   const int d = static_cast<int>(s->d);
   const int nb = static_cast<int>(ceil_div(s->L, s->block));
@@ -1441,10 +1526,12 @@ static int launch_pool(const ropeslr_shape* s, const void* q, const void* k, dou
   const int chunks = d / 8;
   const int lanes_r = 256 / chunks;
   size_t sm = static_cast<size_t>(lanes_r) * d * sizeof(double);
-  if (s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128 && aligned16(q) && aligned16(k))
+  const bool bulk = s->dtype == ROPESLR_BF16 && d == 128 && s->block <= 128 && aligned16(q) && aligned16(k);
+  if (wrote_img != nullptr) *wrote_img = bulk && img != nullptr;
+  if (bulk)
     pool_blocks_bulk_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q),
                                                    static_cast<const __nv_bfloat16*>(k), pooled, s->L, s->block, nb,
-                                                   BH, bh0);
+                                                   BH, bh0, img, norms, static_cast<int>(ceil_div(nb, 128)));
   else if (s->dtype == ROPESLR_BF16)
     pool_blocks_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(static_cast<const __nv_bfloat16*>(q),
                                                               static_cast<const __nv_bfloat16*>(k), pooled, s->L, d,
@@ -1477,8 +1564,17 @@ extern "C" int ropeslr_select_blocks(const ropeslr_shape* s, const ropeslr_selec
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
   double* pooled = static_cast<double*>(ws);
   uint8_t* area = static_cast<uint8_t*>(ws) + pooled_bytes(s);
-  if (int e = launch_pool(s, q, k, pooled, 0, s->B * s->H, st)) return e;
-  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores_out, area, st);
+  // the screening path's image rows and norms come from the pooling kernel
+  uint8_t* img = nullptr;
+  float* norms = nullptr;
+  if (scores_out == nullptr && screen_eligible(s, sel->topk)) {
+    const ScreenLayout y = screen_layout(s->B * s->H, ceil_div(s->L, s->block));
+    img = area + y.img;
+    norms = reinterpret_cast<float*>(area + y.norms);
+  }
+  bool have_img = false;
+  if (int e = launch_pool(s, q, k, pooled, 0, s->B * s->H, st, img, norms, &have_img)) return e;
+  return select_from_pooled(s, sel, pooled, idx, kmax, cnt, mask, attended, scores_out, area, st, have_img);
 }
 
 extern "C" int ropeslr_select_from_pooled(const ropeslr_shape* s, const ropeslr_select_params* sel,

@@ -466,7 +466,7 @@ def _token_args(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: O
                           _ptr(nonfinite))
 
 
-_TABLES: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+_TABLES: "OrderedDict[tuple, tuple]" = OrderedDict()  # key -> (tables, dependencies)
 
 
 def linear_tables(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: Optional[PETables], use_pe: bool,
@@ -490,18 +490,55 @@ def linear_tables(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe:
         if w.shape != (H, params.d_model, d) or w.dtype != torch.float32 or w.device != x.device:
             raise ValueError(f"linear backbone weights must be float32 [{H}, {params.d_model}, {d}] on X's device")
     deps = [params.alpha, params.w_g, wq, wk, wv] + ([pe.pe_t, pe.pe_x, pe.pe_y] if use_pe else [])
-    key = (tuple((t.data_ptr(), t._version) for t in deps), head_offset, H, grid.as_tuple(), bool(use_pe), x.device)
-    tab = _TABLES.get(key)
-    if tab is None:
-        tab = _workspace(nbytes, x.device)
+
+    def build(tab):
         _lib.call("ropeslr_linear_tables", ctypes_ref(shp), ctypes_ref(tok), wq.data_ptr(), wk.data_ptr(),
                   wv.data_ptr(), tab.data_ptr(), tab.numel(), _stream(x.device))
-        _TABLES[key] = tab
-        while len(_TABLES) > 8:
-            _TABLES.popitem(last=False)
-    else:
+
+    return _cached_tables(("linear", head_offset, H, grid.as_tuple(), bool(use_pe), x.device), deps, nbytes,
+                          x.device, build)
+
+
+def _cached_tables(tag, deps, nbytes, device, build) -> torch.Tensor:
+    """Parameter-only device tables, rebuilt only when a dependency changes.
+    The key is each dependency's storage address and version counter; the
+    entry holds the dependencies themselves, so a cached address cannot be
+    freed and reused by another tensor while the entry lives (8 entries)."""
+    key = (tag, tuple((t.data_ptr(), t._version) for t in deps))
+    hit = _TABLES.get(key)
+    if hit is not None:
         _TABLES.move_to_end(key)
+        return hit[0]
+    tab = _workspace(nbytes, device)
+    build(tab)
+    _TABLES[key] = (tab, list(deps))
+    while len(_TABLES) > 8:
+        _TABLES.popitem(last=False)
     return tab
+
+
+def lowrank_tables(x: torch.Tensor, grid: GridShape, params: MechanismParams, pe: Optional[PETables], use_pe: bool,
+                   head_offset: int = 0, H_local: Optional[int] = None) -> Optional[torch.Tensor]:
+    """The low-rank branch's parameter-only tables (operand images of W_A /
+    W_B and the per-axis PE folds, include/ropeslr_b200.h
+    ropeslr_lowrank_tables), cached while w_a / w_b / alpha / w_g / the PE
+    tables are unchanged; None where the tcgen05 path does not apply."""
+    H = params.n_heads if H_local is None else H_local
+    d = params.d_h
+    B, L, _ = x.shape
+    tok = _token_args(x, grid, params, pe, use_pe, head_offset, H, d)
+    shp = _lib.Shape(B, H, L, d, 1, _dtype_code(x))
+    nbytes = _lib.lib().ropeslr_lowrank_tables_bytes(ctypes_ref(shp), ctypes_ref(tok), params.rank)
+    if nbytes == 0:
+        return None
+    deps = [params.w_a, params.w_b, params.alpha, params.w_g] + ([pe.pe_t, pe.pe_x, pe.pe_y] if use_pe else [])
+
+    def build(tab):
+        _lib.call("ropeslr_lowrank_tables", ctypes_ref(shp), ctypes_ref(tok), params.w_a.data_ptr(),
+                  params.w_b.data_ptr(), params.rank, tab.data_ptr(), tab.numel(), _stream(x.device))
+
+    return _cached_tables(("lowrank", head_offset, H, grid.as_tuple(), bool(use_pe), x.device), deps, nbytes,
+                          x.device, build)
 
 
 def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams, settings: ForwardSettings,
@@ -537,11 +574,19 @@ def compensator_branch(x: torch.Tensor, grid: GridShape, params: MechanismParams
     if settings.compensator == "lowrank":
         if params.w_a.shape[0] != H or params.w_b.shape != (H, params.rank, d):
             raise ValueError("compensator weights do not match the head slice")
-        ws = _workspace(_lib.lib().ropeslr_lowrank_workspace_bytes(ctypes_ref(shp), ctypes_ref(tok), params.rank),
-                        dev)
-        _lib.call("ropeslr_lowrank_branch", ctypes_ref(shp), ctypes_ref(tok), params.w_a.data_ptr(),
-                  params.w_b.data_ptr(), params.rank, params.rms_lowrank.data_ptr(), float(settings.rms_eps),
-                  y_lr.data_ptr(), _ptr(o_lr), g_logit.data_ptr(), ws.data_ptr(), ws.numel(), st)
+        tab = lowrank_tables(x, grid, params, pe, settings.use_pe, head_offset, H)
+        if tab is not None:
+            # parameter-only folds cached across calls: one kernel (+ the gate sum) per call
+            ws = _workspace(B * H * L * 4, dev)
+            _lib.call("ropeslr_lowrank_branch_folded", ctypes_ref(shp), ctypes_ref(tok), params.rank,
+                      tab.data_ptr(), tab.numel(), params.rms_lowrank.data_ptr(), float(settings.rms_eps),
+                      y_lr.data_ptr(), _ptr(o_lr), g_logit.data_ptr(), ws.data_ptr(), ws.numel(), st)
+        else:
+            ws = _workspace(_lib.lib().ropeslr_lowrank_workspace_bytes(ctypes_ref(shp), ctypes_ref(tok),
+                                                                       params.rank), dev)
+            _lib.call("ropeslr_lowrank_branch", ctypes_ref(shp), ctypes_ref(tok), params.w_a.data_ptr(),
+                      params.w_b.data_ptr(), params.rank, params.rms_lowrank.data_ptr(), float(settings.rms_eps),
+                      y_lr.data_ptr(), _ptr(o_lr), g_logit.data_ptr(), ws.data_ptr(), ws.numel(), st)
     else:
         if lin_proj is None:
             raise ValueError("the linear compensator needs the projections (q_lin, k_lin, v_lin)")

@@ -204,6 +204,35 @@ def test_linear_pe_tables_are_cached():
 
 
 @pytest.mark.slow
+def test_lowrank_tables_are_cached(monkeypatch):
+    """The low-rank branch's parameter-only tables (W_A / W_B images, per-axis
+    PE folds) are built once and reused until a parameter changes; the folded
+    call equals the per-call fold bit for bit."""
+    import paper_2605_20659_b200 as P
+    from paper_2605_20659_b200 import mechanism as Mm
+
+    q, k, v, x, params, pe, grid = G.make_full_inputs((3, 8, 16), 2, 128, (44, 42, 42), 64, seed=6)
+    st = P.ForwardSettings(P.SparseSettings(64, topk=1))
+    t1 = Mm.lowrank_tables(x, grid, params, pe, True)
+    t2 = Mm.lowrank_tables(x, grid, params, pe, True)
+    assert t1 is not None and t1.data_ptr() == t2.data_ptr()
+    y1, _, g1 = P.compensator_branch(x, grid, params, st, pe)
+    with monkeypatch.context() as m:
+        m.setattr(Mm, "lowrank_tables", lambda *a, **kw: None)  # the per-call fold
+        y0, _, g0 = P.compensator_branch(x, grid, params, st, pe)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y0) and torch.equal(g1, g0)
+    params.w_a.mul_(0.5)
+    t3 = Mm.lowrank_tables(x, grid, params, pe, True)
+    assert t3.data_ptr() != t1.data_ptr()
+    y3, _, _ = P.compensator_branch(x, grid, params, st, pe)
+    with monkeypatch.context() as m:
+        m.setattr(Mm, "lowrank_tables", lambda *a, **kw: None)
+        y4, _, _ = P.compensator_branch(x, grid, params, st, pe)
+    torch.cuda.synchronize()
+    assert torch.equal(y3, y4) and not torch.equal(y3, y1)
+
+
 def test_linear_forward_config1_fullsize():
     """Linear mode through the whole forward at the config-1 shape (L = 32760,
     H = 12, d = 128, block 64, top-51, bf16): the compensator of three heads

@@ -135,7 +135,7 @@ def test_screen_clusters_and_duplicates():
 
 def test_screen_defers_undecidable_rows():
     """Rows the band cannot decide go to the float64 pass: one cluster of
-    300 near-identical blocks (band > 64), and rows spanning more than 700
+    300 near-identical blocks (band > 32), and rows spanning more than 700
     (the probability-underflow clamp, mechanism.py:310-317)."""
     nb, block, d = 300, 32, 128
     rng = np.random.default_rng(12)
