@@ -805,13 +805,12 @@ def run_train(args, local_rank):
     pe_dense = T.pe_head_major(pe, grid, params.n_heads, params.d_h)
     lr = 1e-3
 
+    # the step as train_stage1 runs it: captured once (CUDA graphs), replayed;
+    # the loss is read back every step
+    runner = T.Stage1Step(prepared, params, settings, pe_dense, lr)
+
     def step():
-        loss, grads = T.loss_and_grads(prepared, params, settings, pe_dense)
-        with torch.no_grad():
-            for name in T.PARAM_NAMES:
-                getattr(params, name).sub_(lr * grads[name].to(getattr(params, name).dtype))
-        params.b_g = float(params.b_g) - lr * grads["b_g"]
-        return loss
+        return runner.step()
 
     for _ in range(args.warmup):
         step()
@@ -832,7 +831,8 @@ def run_train(args, local_rank):
             "sparse_branch_cache_ms": cache_ms, "loss_first": losses[0], "loss_last": losses[-1],
             "note": "per-step math: the six GEMMs on tcgen05 with float32-grade bf16 hi+lo splits "
                     "(csrc/stage1_gemm.cu) + the fused row kernels of csrc/stage1.cu (training.py), no cuBLAS; "
-                    "the loss is read back every step, as the reference trainer does"}
+                    "the step (loss, gradients, guarded update) is one CUDA graph replay "
+                    "(training.Stage1Step); the loss is read back every step, as the reference trainer does"}
     print(json.dumps(line), flush=True)
 
 

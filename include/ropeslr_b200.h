@@ -425,6 +425,10 @@ int ropeslr_stage1_rows_blocks(int64_t H, int64_t L);
 int ropeslr_stage1_xgrad_blocks(int64_t H, int64_t L);
 int ropeslr_stage1_pre(int64_t H, int64_t L, int64_t d, const float* x, const float* pe, const float* alpha,
                        const float* w_g, float b_g, float* xh, float* gpart, float* g, void* stream);
+/* The same with b_g read from device memory (float64), for a training step
+ * captured once in a CUDA graph and replayed while b_g changes. */
+int ropeslr_stage1_pre_dev(int64_t H, int64_t L, int64_t d, const float* x, const float* pe, const float* alpha,
+                           const float* w_g, const double* b_g, float* xh, float* gpart, float* g, void* stream);
 int ropeslr_stage1_rows(int64_t H, int64_t L, int64_t d, float* z2, const float* o_sp, const float* target,
                         const float* g, const float* rms_sp, const float* rms_lr, float eps, float gscale,
                         float* dgpart, float* red, double* loss_part, void* stream);

@@ -101,6 +101,7 @@ _SIGNATURES = {
     "ropeslr_stage1_rows_blocks": (c_i32, [c_i64, c_i64]),
     "ropeslr_stage1_xgrad_blocks": (c_i32, [c_i64, c_i64]),
     "ropeslr_stage1_pre": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_f32, c_vp, c_vp, c_vp, c_vp]),
+    "ropeslr_stage1_pre_dev": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ropeslr_stage1_rows": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f32, c_f32, c_vp,
                                     c_vp, c_vp, c_vp]),
     "ropeslr_stage1_gate_bwd": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),

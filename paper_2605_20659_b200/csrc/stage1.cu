@@ -65,12 +65,16 @@ __global__ void __launch_bounds__(kWarps * 32) pre_kernel(const float* __restric
   }
 }
 
-__global__ void gate_kernel(const float* __restrict__ gpart, int H, int64_t L, float b_g, float* __restrict__ g) {
+// b_g from the argument, or from device memory when b_g_dev is set (a
+// captured training step reads the current bias).
+__global__ void gate_kernel(const float* __restrict__ gpart, int H, int64_t L, float b_g,
+                            const double* __restrict__ b_g_dev, float* __restrict__ g) {
   const int64_t l = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (l >= L) return;
+  const float b = b_g_dev != nullptr ? static_cast<float>(*b_g_dev) : b_g;
   float s = 0.f;
   for (int h = 0; h < H; ++h) s += gpart[h * L + l];
-  g[l] = sigm(s + b_g);
+  g[l] = sigm(s + b);
 }
 
 // Per-CTA partials: red[blockIdx][0][d] = sum gh * u_sp (d rms_sparse),
@@ -348,9 +352,9 @@ extern "C" int ropeslr_stage1_supported(int64_t d) { return s1::vec_of(d) != 0; 
 
 extern "C" int ropeslr_stage1_rows_blocks(int64_t H, int64_t L) { return static_cast<int>(row_grid(H * L)); }
 
-extern "C" int ropeslr_stage1_pre(int64_t H, int64_t L, int64_t d, const float* x, const float* pe,
-                                  const float* alpha, const float* w_g, float b_g, float* xh, float* gpart,
-                                  float* g, void* stream) {
+static int stage1_pre(int64_t H, int64_t L, int64_t d, const float* x, const float* pe, const float* alpha,
+                      const float* w_g, float b_g, const double* b_g_dev, float* xh, float* gpart, float* g,
+                      void* stream) {
   const int V = s1::vec_of(d);
   if (V == 0 || H < 1 || L < 1) return ROPESLR_ERR_SHAPE;
   if (!x || !w_g || !xh || !gpart || !g || (pe && !alpha)) return ROPESLR_ERR_NULL;
@@ -358,8 +362,22 @@ extern "C" int ropeslr_stage1_pre(int64_t H, int64_t L, int64_t d, const float* 
   const int64_t rows = H * L;
   S1_SWITCH(V, (s1::pre_kernel<V><<<row_grid(rows), s1::kWarps * 32, 0, st>>>(x, pe, alpha, w_g, L, rows, xh,
                                                                                 gpart)));
-  s1::gate_kernel<<<static_cast<unsigned>(ceil_div(L, 256)), 256, 0, st>>>(gpart, static_cast<int>(H), L, b_g, g);
+  s1::gate_kernel<<<static_cast<unsigned>(ceil_div(L, 256)), 256, 0, st>>>(gpart, static_cast<int>(H), L, b_g,
+                                                                            b_g_dev, g);
   return launch_status();
+}
+
+extern "C" int ropeslr_stage1_pre(int64_t H, int64_t L, int64_t d, const float* x, const float* pe,
+                                  const float* alpha, const float* w_g, float b_g, float* xh, float* gpart,
+                                  float* g, void* stream) {
+  return stage1_pre(H, L, d, x, pe, alpha, w_g, b_g, nullptr, xh, gpart, g, stream);
+}
+
+extern "C" int ropeslr_stage1_pre_dev(int64_t H, int64_t L, int64_t d, const float* x, const float* pe,
+                                      const float* alpha, const float* w_g, const double* b_g, float* xh,
+                                      float* gpart, float* g, void* stream) {
+  if (!b_g) return ROPESLR_ERR_NULL;
+  return stage1_pre(H, L, d, x, pe, alpha, w_g, 0.f, b_g, xh, gpart, g, stream);
 }
 
 extern "C" int ropeslr_stage1_rows(int64_t H, int64_t L, int64_t d, float* z2, const float* o_sp,

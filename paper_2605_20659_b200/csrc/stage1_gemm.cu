@@ -21,6 +21,8 @@
 //
 // Operands are loaded as float32 by the converter warps (16-byte loads),
 // split and written in the 128B-swizzled layout the UMMA descriptors read.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -96,6 +98,7 @@ __device__ __forceinline__ void convert_tile(const float* src, int64_t row0, int
 enum Epi { EPI_NONE = 0, EPI_SIGMOID = 1, EPI_DSIG = 2 };
 
 struct RowsArgs {
+  CUtensorMap mC;    // C as [H][L][N] float32, box [32 columns, 32 rows, 1], 128-byte swizzle
   const float* A;    // [H, L, K]
   const float* B;    // [H, K, N], or [H, N, K] when b_trans (B^T given)
   const float* aux;  // EPI_DSIG: h1 [H, L, N]
@@ -109,37 +112,54 @@ struct RowsArgs {
 
 template <int K, int N>
 struct RowsLay {
+  static constexpr int F_BYTES = M * K * 4;   // one float32 staging tile (bulk copy target)
   static constexpr int A_BYTES = M * K * 2;   // one of hi / lo
   static constexpr int B_BYTES = N * K * 2;
-  static constexpr int OFF_A = 0;                       // [2 stages][hi, lo]
-  static constexpr int OFF_B = OFF_A + 4 * A_BYTES;     // [hi, lo] K-major [N rows][K]
-  static constexpr int OFF_BAR = OFF_B + 2 * B_BYTES;
+  static constexpr int FST = K == 128 ? 1 : 2;  // staging stages
+  static constexpr int AST = K == 128 ? 1 : 2;  // converted A stages
+  static constexpr int O_BYTES = 32 * 128;      // an epilogue warp's [32 rows x 32 columns] float32 store box
+  static constexpr int OFF_F = 0;
+  static constexpr int OFF_A = OFF_F + FST * F_BYTES;          // [AST][hi, lo]
+  static constexpr int OFF_B = OFF_A + AST * 2 * A_BYTES;      // [hi, lo] K-major [N rows][K]
+  static constexpr int OFF_O = OFF_B + 2 * B_BYTES;            // [4 warps][2 buffers] store boxes
+  static constexpr int OFF_BAR = OFF_O + 8 * O_BYTES;
   static constexpr int BYTES = OFF_BAR + 16 * 8;
+  static_assert(BYTES <= 227 * 1024, "shared memory");
 };
 
 constexpr int kConv = 256;  // converter threads (warps 0-7)
 constexpr int kEpi = 128;   // epilogue threads (warps 8-11)
-constexpr int kRowsThreads = kConv + kEpi + 32;  // + warp 12: MMA, TMEM
+constexpr int kRowsThreads = kConv + kEpi + 64;  // + warp 12: MMA, TMEM; warp 13: bulk copies
 
+// A float32 A tile is one contiguous run of rows (row stride K): warp 13
+// moves it into a staging ring with one bulk copy, so the bytes in flight do
+// not depend on registers; the converter warps split it from shared memory
+// into the swizzled bf16 hi / lo operand tiles.
 template <int K, int N>
 __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __grid_constant__ RowsArgs a) {
   using Lay = RowsLay<K, N>;
+  constexpr int FST = Lay::FST, AST = Lay::AST;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
+  uint8_t* sF = smem + Lay::OFF_F;
   uint8_t* sA = smem + Lay::OFF_A;
   uint8_t* sB = smem + Lay::OFF_B;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
-  uint64_t* afull = bars;       // [2]
-  uint64_t* aempty = bars + 2;  // [2]
-  uint64_t* accf = bars + 4;    // [2]
-  uint64_t* acce = bars + 6;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* ffull = bars;        // [2]
+  uint64_t* fempty = bars + 2;   // [2]
+  uint64_t* afull = bars + 4;    // [2]
+  uint64_t* aempty = bars + 6;   // [2]
+  uint64_t* accf = bars + 8;     // [2]
+  uint64_t* acce = bars + 10;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
   // the CTA's tiles: one contiguous range, so B (per head) changes at most
   // a couple of times
   const int64_t total = static_cast<int64_t>(a.H) * a.ntiles;
   const int64_t beg = total * blockIdx.x / gridDim.x, end = total * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&ffull[i], 1);
+      mbar_init(&fempty[i], kConv);
       mbar_init(&afull[i], kConv);
       mbar_init(&aempty[i], 1);
       mbar_init(&accf[i], 1);
@@ -155,18 +175,36 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp < kConv / 32) {
+  if (warp == 13) {
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t it = 0;
+      for (int64_t pos = beg; pos < end; ++pos, ++it) {
+        const int h = static_cast<int>(pos / a.ntiles);
+        const int tile = static_cast<int>(pos % a.ntiles);
+        const int s = it % FST;
+        if (it >= FST) mbar_wait_sleep(&fempty[s], ((it / FST) - 1) & 1);
+        const int64_t row0 = static_cast<int64_t>(tile) * M;
+        const int rows = static_cast<int>(a.L - row0 < M ? a.L - row0 : M);
+        const uint32_t bytes = static_cast<uint32_t>(rows) * K * 4;
+        mbar_arrive_expect_tx(&ffull[s], bytes);
+        bulk_load_1d(sF + s * Lay::F_BYTES, a.A + (static_cast<int64_t>(h) * a.L + row0) * K, bytes, &ffull[s],
+                     pol);
+      }
+    }
+  } else if (warp < kConv / 32) {
+    constexpr int CH = K / 8, PER = M * CH / kConv;
     int cur_h = -1;
     uint32_t it = 0;
     for (int64_t pos = beg; pos < end; ++pos, ++it) {
       const int h = static_cast<int>(pos / a.ntiles);
       const int tile = static_cast<int>(pos % a.ntiles);
-      const int s = it & 1;
-      if (it >= 2) mbar_wait_sleep(&aempty[s], ((it >> 1) - 1) & 1);
+      const int sf = it % FST, sa = it % AST;
+      if (it >= AST) mbar_wait_sleep(&aempty[sa], ((it / AST) - 1) & 1);
       if (h != cur_h) {
         // B of head h as K-major [N rows][K] hi / lo images; every MMA on the
-        // previous head's B has completed (aempty of the last two tiles)
-        if (it >= 1) mbar_wait_sleep(&aempty[s ^ 1], ((it - 1) >> 1) & 1);
+        // previous head's B has completed (aempty of the previous tile)
+        if (it >= 1) mbar_wait_sleep(&aempty[(it - 1) % AST], ((it - 1) / AST) & 1);
         asm volatile("bar.sync 2, %0;" ::"n"(kConv) : "memory");
         const float* B = a.B + static_cast<int64_t>(h) * K * N;
         for (int e = threadIdx.x; e < N * (K / 8); e += kConv) {
@@ -185,23 +223,46 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
         }
         cur_h = h;
       }
-      convert_tile<K, kConv>(a.A + static_cast<int64_t>(h) * a.L * K, static_cast<int64_t>(tile) * M, a.L,
-                             sA + s * 2 * Lay::A_BYTES, sA + s * 2 * Lay::A_BYTES + Lay::A_BYTES, threadIdx.x);
+      mbar_wait_sleep(&ffull[sf], (it / FST) & 1);
+      const int64_t nrows = a.L - static_cast<int64_t>(tile) * M;
+      const float* src = reinterpret_cast<const float*>(sF + sf * Lay::F_BYTES);
+      uint8_t* hi = sA + sa * 2 * Lay::A_BYTES;
+      uint8_t* lo = hi + Lay::A_BYTES;
+#pragma unroll 4
+      for (int i = 0; i < PER; ++i) {
+        const int e = threadIdx.x + i * kConv;
+        const int r = e / CH, c = e % CH;
+        float f[8];
+        if (r < nrows) {
+          const float4 x0 = *reinterpret_cast<const float4*>(src + r * K + c * 8);
+          const float4 x1 = *reinterpret_cast<const float4*>(src + r * K + c * 8 + 4);
+          f[0] = x0.x; f[1] = x0.y; f[2] = x0.z; f[3] = x0.w; f[4] = x1.x; f[5] = x1.y; f[6] = x1.z; f[7] = x1.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) f[j] = 0.f;
+        }
+        uint4 hv, lv;
+        split8(f, hv, lv);
+        const uint32_t off = sw_off(M, r, c);
+        *reinterpret_cast<uint4*>(hi + off) = hv;
+        *reinterpret_cast<uint4*>(lo + off) = lv;
+      }
+      mbar_arrive(&fempty[sf]);
       fence_proxy_async_smem();
-      mbar_arrive(&afull[s]);
+      mbar_arrive(&afull[sa]);
     }
   } else if (warp == 12) {
     constexpr uint32_t idesc = idesc_bf16_f32(M, N, false, false);
     const bool leader = elect_one();
     uint32_t it = 0;
     for (int64_t pos = beg; pos < end; ++pos, ++it) {
-      const int s = it & 1, ab = it & 1;
-      mbar_wait_sleep(&afull[s], (it >> 1) & 1);
+      const int sa = it % AST, ab = it & 1;
+      mbar_wait_sleep(&afull[sa], (it / AST) & 1);
       if (it >= 2) mbar_wait_sleep(&acce[ab], ((it >> 1) - 1) & 1);
       tc_fence_after();
       if (leader) {
-        const uint64_t dAh = desc_sw128(smem_u32(sA + s * 2 * Lay::A_BYTES), 16, 1024);
-        const uint64_t dAl = desc_sw128(smem_u32(sA + s * 2 * Lay::A_BYTES + Lay::A_BYTES), 16, 1024);
+        const uint64_t dAh = desc_sw128(smem_u32(sA + sa * 2 * Lay::A_BYTES), 16, 1024);
+        const uint64_t dAl = desc_sw128(smem_u32(sA + sa * 2 * Lay::A_BYTES + Lay::A_BYTES), 16, 1024);
         const uint64_t dBh = desc_sw128(smem_u32(sB), 16, 1024);
         const uint64_t dBl = desc_sw128(smem_u32(sB + Lay::B_BYTES), 16, 1024);
         const uint32_t acc = tmem + ab * 128;
@@ -213,16 +274,20 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
           mma_bf16_ss(acc, dAh + ka, dBl + kb, idesc, 1u);
           mma_bf16_ss(acc, dAl + ka, dBh + kb, idesc, 1u);
         }
-        mma_commit(&aempty[s]);
+        mma_commit(&aempty[sa]);
         mma_commit(&accf[ab]);
       }
       __syncwarp();
     }
   } else {
-    // epilogue warps 8-11: TMEM lane quarter warp % 4 = token row
-    const int q4 = warp & 3;
-    const int r = q4 * 32 + (threadIdx.x & 31);
-    uint32_t it = 0;
+    // epilogue warps 8-11: TMEM lane quarter warp % 4 = token row.  Each
+    // 32-column chunk goes TMEM -> registers -> (epilogue) -> a swizzled
+    // [32 rows x 128 B] box in shared memory -> one TMA store (coalesced;
+    // rows past L are clipped by the tensor map), two boxes in flight.
+    const int q4 = warp & 3, lane = threadIdx.x & 31;
+    const int r = q4 * 32 + lane;
+    uint8_t* obuf = smem + Lay::OFF_O + q4 * 2 * Lay::O_BYTES;
+    uint32_t it = 0, nst = 0;
     for (int64_t pos = beg; pos < end; ++pos, ++it) {
       const int h = static_cast<int>(pos / a.ntiles);
       const int tile = static_cast<int>(pos % a.ntiles);
@@ -232,9 +297,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
       const int64_t l = static_cast<int64_t>(tile) * M + r;
       const bool live = l < a.L;
       const int64_t row = (static_cast<int64_t>(h) * a.L + (live ? l : 0)) * N;
-      // 32 columns at a time: TMEM -> epilogue -> 128-byte store
 #pragma unroll 1
-      for (int c = 0; c < N / 32; ++c) {
+      for (int c = 0; c < N / 32; ++c, ++nst) {
         uint32_t u[32];
         tmem_ld32(tmem + ab * 128 + (static_cast<uint32_t>(q4 * 32) << 16) + c * 32, u);
         tmem_wait_ld();
@@ -242,14 +306,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
           tc_fence_before();
           mbar_arrive(&acce[ab]);
         }
-        if (!live) continue;
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(u[j]);
         if (a.epi == EPI_SIGMOID) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 1.f / (1.f + __expf(-v[j]));
-        } else if (a.epi == EPI_DSIG) {
+        } else if (a.epi == EPI_DSIG && live) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 g = __ldg(reinterpret_cast<const float4*>(a.aux + row + c * 32 + j));
@@ -259,11 +322,26 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
             v[j + 3] *= g.w * (1.f - g.w);
           }
         }
+        // the box written two stores ago has been read out
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint8_t* box = obuf + (nst & 1) * Lay::O_BYTES;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(a.C + row + c * 32 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                           reinterpret_cast<uint64_t>(&a.mC)),
+                       "r"(smem_u32(box)), "r"(c * 32), "r"(tile * M + q4 * 32), "r"(h)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -427,6 +505,22 @@ static int gram_chunks(int H, int ntiles) {
 
 using namespace ropeslr;
 
+namespace ropeslr {
+namespace s1g {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+}  // namespace s1g
+}  // namespace ropeslr
+
 extern "C" int ropeslr_stage1_gemm_rows(int64_t H, int64_t L, int32_t K, int32_t N, const float* A, const float* B,
                                         int32_t b_trans, int32_t epi, const float* aux, float* C, void* stream) {
   if (!A || !B || !C || (epi == s1g::EPI_DSIG && !aux)) return ROPESLR_ERR_NULL;
@@ -443,6 +537,18 @@ extern "C" int ropeslr_stage1_gemm_rows(int64_t H, int64_t L, int32_t K, int32_t
   a.b_trans = b_trans;
   a.epi = epi;
   a.ntiles = static_cast<int>(ceil_div(L, s1g::M));
+  {
+    auto enc = s1g::encode_fn();
+    if (enc == nullptr) return ROPESLR_ERR_LAUNCH;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(H)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(N) * 4, static_cast<cuuint64_t>(L) * N * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&a.mC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return ROPESLR_ERR_LAUNCH;
+  }
   const int64_t total = H * a.ntiles;
   const unsigned grid = static_cast<unsigned>(total < num_sms() ? total : num_sms());
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -153,6 +153,17 @@ def loss_and_grads(prepared: Sequence[_Prepared], params: MechanismParams, setti
 
 
 def _loss_and_grads_fused(prepared, params, settings, pe_dense):
+    acc, grads = _fused_device(prepared, params, settings, pe_dense)
+    loss, gb = acc.tolist()  # the one host read of the step (the reference trainer reads the loss too)
+    grads["b_g"] = float(gb)
+    return float(loss), grads
+
+
+def _fused_device(prepared, params, settings, pe_dense, b_g_dev: Optional[torch.Tensor] = None):
+    """The fused loss and gradients with no host read: (acc = float64 [loss,
+    d b_g] on the device, {name: float32 gradient} without b_g).  With
+    ``b_g_dev`` (float64 [1]) the gate bias is read from the device, so the
+    sequence can be captured in a CUDA graph and replayed (Stage1Step)."""
     eps = settings.rms_eps
     H, d, r = params.n_heads, params.d_h, params.rank
     dev = prepared[0].x.device
@@ -173,8 +184,12 @@ def _loss_and_grads_fused(prepared, params, settings, pe_dense):
         gpart = torch.empty((H, L), dtype=torch.float32, device=dev)
         g = torch.empty((L,), dtype=torch.float32, device=dev)
         pe_ptr = pe_dense.data_ptr() if use_pe else None
-        _lib.call("ropeslr_stage1_pre", H, L, d, s.x.data_ptr(), pe_ptr, alpha.data_ptr(), w_g.data_ptr(),
-                  float(params.b_g), xh.data_ptr(), gpart.data_ptr(), g.data_ptr(), st)
+        if b_g_dev is None:
+            _lib.call("ropeslr_stage1_pre", H, L, d, s.x.data_ptr(), pe_ptr, alpha.data_ptr(), w_g.data_ptr(),
+                      float(params.b_g), xh.data_ptr(), gpart.data_ptr(), g.data_ptr(), st)
+        else:
+            _lib.call("ropeslr_stage1_pre_dev", H, L, d, s.x.data_ptr(), pe_ptr, alpha.data_ptr(), w_g.data_ptr(),
+                      b_g_dev.data_ptr(), xh.data_ptr(), gpart.data_ptr(), g.data_ptr(), st)
         tc = _tc_gemms(d, r)
         if tc:
             h1 = _rows(xh, w_a, epi=1)                                    # sigma(x_hat W_A) [H, L, r]
@@ -217,9 +232,69 @@ def _loss_and_grads_fused(prepared, params, settings, pe_dense):
     if use_pe:
         grads["alpha"] += x_acc[:, 0].reshape(-1)
     grads["w_g"] += x_acc[:, 1].reshape(-1)
-    loss, gb = acc.tolist()  # the one host read of the step (the reference trainer reads the loss too)
-    grads["b_g"] = float(gb)
-    return float(loss), grads
+    return acc, grads
+
+
+class Stage1Step:
+    """The fused Stage-I step (loss, gradients, the gradient-descent update)
+    captured once in a CUDA graph per phase and replayed: no host work and
+    no launch gaps between the kernels, one host read of the loss per step
+    (mechanism.py:582-614 reads it too).  The update runs only when the step's
+    loss is finite, on the device, so a diverging step leaves the parameters
+    as the reference leaves them.  ``params`` are updated in place; b_g lives
+    on the device during training and is written back by ``sync_bias``."""
+
+    def __init__(self, prepared, params: MechanismParams, settings: ForwardSettings,
+                 pe_dense: Optional[torch.Tensor], lr: float):
+        if not (prepared and prepared[0].x.is_cuda and _lib.lib().ropeslr_stage1_supported(params.d_h)):
+            raise ValueError("the captured Stage-I step needs CUDA samples with a fused head dim (32 / 64 / 128)")
+        self.params = params
+        dev = prepared[0].x.device
+        self.b_g = torch.full((1,), float(params.b_g), dtype=torch.float64, device=dev)
+        lr_t = torch.full((), lr, dtype=torch.float64, device=dev)
+        zero_t = torch.zeros((), dtype=torch.float64, device=dev)
+        names = [n for n in PARAM_NAMES if n != "b_g"]
+        consts = {getattr(params, n).dtype: (lr_t.to(getattr(params, n).dtype), zero_t.to(getattr(params, n).dtype))
+                  for n in names}
+        # the graphs read these by address: they must live as long as the graphs
+        self._keep = (lr_t, zero_t, consts, prepared, pe_dense)
+
+        def body(update: bool):
+            acc, grads = _fused_device(prepared, params, settings, pe_dense, self.b_g)
+            if update:
+                ok = torch.isfinite(acc[0])
+                with torch.no_grad():
+                    for name in names:
+                        p = getattr(params, name)
+                        lr_p, zero_p = consts[p.dtype]
+                        p.sub_(torch.where(ok, grads[name].to(p.dtype) * lr_p, zero_p))
+                    self.b_g.sub_(torch.where(ok, acc[1] * lr_t, zero_t))
+            return acc
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            body(False)  # warm-up outside the capture (workspaces, attributes)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.g_loss = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g_loss):
+            self.acc_loss = body(False)
+        self.g_step = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g_step, pool=self.g_loss.pool()):
+            self.acc_step = body(True)
+
+    def step(self) -> float:
+        """Loss at the current parameters, then the update (if finite)."""
+        self.g_step.replay()
+        return float(self.acc_step[0].item())
+
+    def loss(self) -> float:
+        """Loss at the current parameters, no update."""
+        self.g_loss.replay()
+        return float(self.acc_loss[0].item())
+
+    def sync_bias(self) -> None:
+        self.params.b_g = float(self.b_g.item())
 
 
 def _loss_and_grads_composed(prepared: Sequence[_Prepared], params: MechanismParams, settings: ForwardSettings,
@@ -290,6 +365,18 @@ def train_stage1(samples: Sequence[Stage1Sample], grid: GridShape, params: Mecha
     prepared = prepare(samples, grid, params, settings, pe)
     pe_dense = pe_head_major(pe, grid, params.n_heads, params.d_h) if settings.use_pe else None
     losses = []
+    if steps > 0 and prepared[0].x.is_cuda and _lib.lib().ropeslr_stage1_supported(params.d_h):
+        # the captured step: loss, gradients and the guarded update per replay
+        runner = Stage1Step(prepared, params, settings, pe_dense, lr)
+        try:
+            for step in range(steps + 1):
+                loss = runner.step() if step < steps else runner.loss()
+                losses.append(loss)
+                if not np.isfinite(loss):
+                    return TrainResult(losses=np.asarray(losses), diverged=True)
+        finally:
+            runner.sync_bias()
+        return TrainResult(losses=np.asarray(losses), diverged=False)
     for step in range(steps + 1):
         loss, grads = loss_and_grads(prepared, params, settings, pe_dense, want_grads=step < steps)
         losses.append(loss)

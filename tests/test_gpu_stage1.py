@@ -63,6 +63,49 @@ def test_stage1_training_reduces_loss():
     assert res.final_loss < res.initial_loss
 
 
+@pytest.mark.parametrize("d,split,r", [(128, (16, 56, 56), 64), (64, (16, 24, 24), 16)])
+def test_stage1_captured_step_equals_eager(d, split, r):
+    """The CUDA-graph step (training.Stage1Step: loss, gradients and the
+    device-side update) against the eager loop of the same kernels: the
+    same losses and bit-identical parameters after three steps; a diverging
+    step leaves the parameters untouched."""
+    import copy
+
+    import paper_2605_20659_b200 as P
+    from paper_2605_20659_b200 import training as T
+
+    grid_s, H = (2, 6, 20), 2
+    q, k, v, x, params, pe, grid = G.make_full_inputs(grid_s, H, d, split, r, seed=9, dtype=torch.bfloat16)
+    gen = torch.Generator(device="cuda").manual_seed(10)
+    target = torch.randn((1, grid.size, H * d), generator=gen, device="cuda").to(torch.bfloat16)
+    st = P.ForwardSettings(P.SparseSettings(block=64, topk=2))
+    prep = T.prepare([T.Stage1Sample(q, k, v, x, target)], grid, params, st, pe)
+    pe_hm = T.pe_head_major(pe, grid, H, d)
+    lr = 0.05
+    p_eager = copy.deepcopy(params)
+    eager = []
+    for _ in range(3):
+        loss, grads = T.loss_and_grads(prep, p_eager, st, pe_hm)
+        eager.append(loss)
+        with torch.no_grad():
+            for name in T.PARAM_NAMES:
+                getattr(p_eager, name).sub_(lr * grads[name].to(getattr(p_eager, name).dtype))
+        p_eager.b_g = float(p_eager.b_g) - lr * grads["b_g"]
+    runner = T.Stage1Step(prep, params, st, pe_hm, lr)
+    captured = [runner.step() for _ in range(3)]
+    runner.sync_bias()
+    assert captured == eager
+    for name in T.PARAM_NAMES:
+        assert torch.equal(getattr(params, name), getattr(p_eager, name)), name
+    assert params.b_g == p_eager.b_g
+    # a non-finite loss: no update
+    before = {n: getattr(params, n).clone() for n in T.PARAM_NAMES}
+    prep[0].target.fill_(float("nan"))
+    assert not math.isfinite(runner.step())
+    for name in T.PARAM_NAMES:
+        assert torch.equal(getattr(params, name), before[name]), name
+
+
 @pytest.mark.parametrize("use_pe", [True, False])
 @pytest.mark.parametrize("d,split,r", [(128, (16, 56, 56), 32), (32, (8, 12, 12), 16)])
 def test_stage1_fused_equals_composed(use_pe, d, split, r):
