@@ -99,6 +99,7 @@ enum Epi { EPI_NONE = 0, EPI_SIGMOID = 1, EPI_DSIG = 2 };
 
 struct RowsArgs {
   CUtensorMap mC;    // C as [H][L][N] float32, box [32 columns, 32 rows, 1], 128-byte swizzle
+  CUtensorMap mAux;  // aux, the same way (EPI_DSIG)
   const float* A;    // [H, L, K]
   const float* B;    // [H, K, N], or [H, N, K] when b_trans (B^T given)
   const float* aux;  // EPI_DSIG: h1 [H, L, N]
@@ -112,31 +113,32 @@ struct RowsArgs {
 
 template <int K, int N>
 struct RowsLay {
-  static constexpr int F_BYTES = M * K * 4;   // one float32 staging tile (bulk copy target)
+  static constexpr int F_BYTES = M / 2 * K * 4;  // one float32 staging half tile (64 rows, bulk copy target)
   static constexpr int A_BYTES = M * K * 2;   // one of hi / lo
   static constexpr int B_BYTES = N * K * 2;
-  static constexpr int FST = K == 128 ? 1 : 2;  // staging stages
-  static constexpr int AST = K == 128 ? 1 : 2;  // converted A stages
+  static constexpr int EW = (K == 128 && N == 128) ? 4 : 8;       // epilogue warps (two per TMEM lane quarter)
+  static constexpr int FST = K == 128 ? 2 : 4;                    // staging half-tile stages
+  static constexpr int AST = K == 128 ? 1 : 2;                   // converted A stages
   static constexpr int O_BYTES = 32 * 128;      // an epilogue warp's [32 rows x 32 columns] float32 store box
   static constexpr int OFF_F = 0;
   static constexpr int OFF_A = OFF_F + FST * F_BYTES;          // [AST][hi, lo]
   static constexpr int OFF_B = OFF_A + AST * 2 * A_BYTES;      // [hi, lo] K-major [N rows][K]
-  static constexpr int OFF_O = OFF_B + 2 * B_BYTES;            // [4 warps][2 buffers] store boxes
-  static constexpr int OFF_BAR = OFF_O + 8 * O_BYTES;
-  static constexpr int BYTES = OFF_BAR + 16 * 8;
+  static constexpr int OFF_O = OFF_B + 2 * B_BYTES;            // [EW warps][2 buffers] store boxes
+  static constexpr int OFF_BAR = OFF_O + 2 * EW * O_BYTES;
+  static constexpr int THREADS = 256 + EW * 32 + 64;           // converters, epilogue, MMA, bulk copies
+  static constexpr int W_MMA = 8 + EW, W_LOAD = 9 + EW;
+  static constexpr int BYTES = OFF_BAR + 34 * 8;
   static_assert(BYTES <= 227 * 1024, "shared memory");
 };
 
 constexpr int kConv = 256;  // converter threads (warps 0-7)
-constexpr int kEpi = 128;   // epilogue threads (warps 8-11)
-constexpr int kRowsThreads = kConv + kEpi + 64;  // + warp 12: MMA, TMEM; warp 13: bulk copies
 
 // A float32 A tile is one contiguous run of rows (row stride K): warp 13
-// moves it into a staging ring with one bulk copy, so the bytes in flight do
-// not depend on registers; the converter warps split it from shared memory
-// into the swizzled bf16 hi / lo operand tiles.
+// moves it into a staging ring in two 64-row bulk copies, so the bytes in
+// flight do not depend on registers; the converter warps split it from
+// shared memory into the swizzled bf16 hi / lo operand tiles.
 template <int K, int N>
-__global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __grid_constant__ RowsArgs a) {
+__global__ void __launch_bounds__(RowsLay<K, N>::THREADS, 1) stage1_rows_kernel(const __grid_constant__ RowsArgs a) {
   using Lay = RowsLay<K, N>;
   constexpr int FST = Lay::FST, AST = Lay::AST;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -145,29 +147,33 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
   uint8_t* sA = smem + Lay::OFF_A;
   uint8_t* sB = smem + Lay::OFF_B;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
-  uint64_t* ffull = bars;        // [2]
-  uint64_t* fempty = bars + 2;   // [2]
-  uint64_t* afull = bars + 4;    // [2]
-  uint64_t* aempty = bars + 6;   // [2]
-  uint64_t* accf = bars + 8;     // [2]
-  uint64_t* acce = bars + 10;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* ffull = bars;        // [4]
+  uint64_t* fempty = bars + 4;   // [4]
+  uint64_t* afull = bars + 8;    // [2]
+  uint64_t* aempty = bars + 10;  // [2]
+  uint64_t* accf = bars + 12;    // [2]
+  uint64_t* acce = bars + 14;    // [2]
+  uint64_t* obar = bars + 16;    // [EW warps][2 boxes]: the aux box landed (EPI_DSIG)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
   // the CTA's tiles: one contiguous range, so B (per head) changes at most
   // a couple of times
   const int64_t total = static_cast<int64_t>(a.H) * a.ntiles;
   const int64_t beg = total * blockIdx.x / gridDim.x, end = total * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&ffull[i], 1);
       mbar_init(&fempty[i], kConv);
+    }
+    for (int i = 0; i < 2 * Lay::EW; ++i) mbar_init(&obar[i], 1);
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], kConv);
       mbar_init(&aempty[i], 1);
       mbar_init(&accf[i], 1);
-      mbar_init(&acce[i], kEpi);
+      mbar_init(&acce[i], Lay::EW * 32);
     }
     fence_mbar_init();
   }
-  if (warp == 12) {
+  if (warp == Lay::W_MMA) {
     tmem_alloc(tmem_slot, 256);
     tmem_relinquish();
   }
@@ -175,21 +181,25 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp == 13) {
+  if (warp == Lay::W_LOAD) {
     if (elect_one()) {
       const uint64_t pol = policy_evict_first();
-      uint32_t it = 0;
-      for (int64_t pos = beg; pos < end; ++pos, ++it) {
+      uint32_t hc = 0;  // half tiles issued
+      for (int64_t pos = beg; pos < end; ++pos) {
         const int h = static_cast<int>(pos / a.ntiles);
         const int tile = static_cast<int>(pos % a.ntiles);
-        const int s = it % FST;
-        if (it >= FST) mbar_wait_sleep(&fempty[s], ((it / FST) - 1) & 1);
-        const int64_t row0 = static_cast<int64_t>(tile) * M;
-        const int rows = static_cast<int>(a.L - row0 < M ? a.L - row0 : M);
-        const uint32_t bytes = static_cast<uint32_t>(rows) * K * 4;
-        mbar_arrive_expect_tx(&ffull[s], bytes);
-        bulk_load_1d(sF + s * Lay::F_BYTES, a.A + (static_cast<int64_t>(h) * a.L + row0) * K, bytes, &ffull[s],
-                     pol);
+        for (int hf = 0; hf < 2; ++hf, ++hc) {
+          const int s = hc % FST;
+          if (hc >= FST) mbar_wait_sleep(&fempty[s], ((hc / FST) - 1) & 1);
+          const int64_t row0 = static_cast<int64_t>(tile) * M + hf * (M / 2);
+          const int64_t left = a.L - row0;
+          const int rows = static_cast<int>(left <= 0 ? 0 : left < M / 2 ? left : M / 2);
+          const uint32_t bytes = static_cast<uint32_t>(rows) * K * 4;
+          mbar_arrive_expect_tx(&ffull[s], bytes);
+          if (rows > 0)
+            bulk_load_1d(sF + s * Lay::F_BYTES, a.A + (static_cast<int64_t>(h) * a.L + row0) * K, bytes, &ffull[s],
+                         pol);
+        }
       }
     }
   } else if (warp < kConv / 32) {
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
     for (int64_t pos = beg; pos < end; ++pos, ++it) {
       const int h = static_cast<int>(pos / a.ntiles);
       const int tile = static_cast<int>(pos % a.ntiles);
-      const int sf = it % FST, sa = it % AST;
+      const int sa = it % AST;
       if (it >= AST) mbar_wait_sleep(&aempty[sa], ((it / AST) - 1) & 1);
       if (h != cur_h) {
         // B of head h as K-major [N rows][K] hi / lo images; every MMA on the
@@ -223,35 +233,40 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
         }
         cur_h = h;
       }
-      mbar_wait_sleep(&ffull[sf], (it / FST) & 1);
       const int64_t nrows = a.L - static_cast<int64_t>(tile) * M;
-      const float* src = reinterpret_cast<const float*>(sF + sf * Lay::F_BYTES);
       uint8_t* hi = sA + sa * 2 * Lay::A_BYTES;
       uint8_t* lo = hi + Lay::A_BYTES;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        const uint32_t hc = 2 * it + hf;
+        const int sf = hc % FST;
+        mbar_wait_sleep(&ffull[sf], (hc / FST) & 1);
+        const float* src = reinterpret_cast<const float*>(sF + sf * Lay::F_BYTES);
 #pragma unroll 4
-      for (int i = 0; i < PER; ++i) {
-        const int e = threadIdx.x + i * kConv;
-        const int r = e / CH, c = e % CH;
-        float f[8];
-        if (r < nrows) {
-          const float4 x0 = *reinterpret_cast<const float4*>(src + r * K + c * 8);
-          const float4 x1 = *reinterpret_cast<const float4*>(src + r * K + c * 8 + 4);
-          f[0] = x0.x; f[1] = x0.y; f[2] = x0.z; f[3] = x0.w; f[4] = x1.x; f[5] = x1.y; f[6] = x1.z; f[7] = x1.w;
-        } else {
+        for (int i = 0; i < PER / 2; ++i) {
+          const int e = threadIdx.x + i * kConv;
+          const int rh = e / CH, c = e % CH, r = hf * (M / 2) + rh;
+          float f[8];
+          if (r < nrows) {
+            const float4 x0 = *reinterpret_cast<const float4*>(src + rh * K + c * 8);
+            const float4 x1 = *reinterpret_cast<const float4*>(src + rh * K + c * 8 + 4);
+            f[0] = x0.x; f[1] = x0.y; f[2] = x0.z; f[3] = x0.w; f[4] = x1.x; f[5] = x1.y; f[6] = x1.z; f[7] = x1.w;
+          } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) f[j] = 0.f;
+            for (int j = 0; j < 8; ++j) f[j] = 0.f;
+          }
+          uint4 hv, lv;
+          split8(f, hv, lv);
+          const uint32_t off = sw_off(M, r, c);
+          *reinterpret_cast<uint4*>(hi + off) = hv;
+          *reinterpret_cast<uint4*>(lo + off) = lv;
         }
-        uint4 hv, lv;
-        split8(f, hv, lv);
-        const uint32_t off = sw_off(M, r, c);
-        *reinterpret_cast<uint4*>(hi + off) = hv;
-        *reinterpret_cast<uint4*>(lo + off) = lv;
+        mbar_arrive(&fempty[sf]);
       }
-      mbar_arrive(&fempty[sf]);
       fence_proxy_async_smem();
       mbar_arrive(&afull[sa]);
     }
-  } else if (warp == 12) {
+  } else if (warp == Lay::W_MMA) {
     constexpr uint32_t idesc = idesc_bf16_f32(M, N, false, false);
     const bool leader = elect_one();
     uint32_t it = 0;
@@ -280,29 +295,45 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
       __syncwarp();
     }
   } else {
-    // epilogue warps 8-11: TMEM lane quarter warp % 4 = token row.  Each
+    // epilogue warps 8 ..: TMEM lane quarter warp % 4 = token row; with 8
+    // warps, warp 8 + q and 12 + q share a quarter (even / odd chunks).  Each
     // 32-column chunk goes TMEM -> registers -> (epilogue) -> a swizzled
     // [32 rows x 128 B] box in shared memory -> one TMA store (coalesced;
     // rows past L are clipped by the tensor map), two boxes in flight.
-    const int q4 = warp & 3, lane = threadIdx.x & 31;
-    const int r = q4 * 32 + lane;
-    uint8_t* obuf = smem + Lay::OFF_O + q4 * 2 * Lay::O_BYTES;
+    // EPI_DSIG's h1 box arrives in the same buffer by a TMA load.
+    const int q4 = warp & 3, lane = threadIdx.x & 31, ew = warp - 8;
+    constexpr int CSTEP = Lay::EW / 4;  // chunks of a warp: c0, c0 + CSTEP, ...
+    const int c0 = ew >> 2;
+    uint8_t* obuf = smem + Lay::OFF_O + ew * 2 * Lay::O_BYTES;
+    const bool dsig = a.epi == EPI_DSIG;
     uint32_t it = 0, nst = 0;
     for (int64_t pos = beg; pos < end; ++pos, ++it) {
       const int h = static_cast<int>(pos / a.ntiles);
       const int tile = static_cast<int>(pos % a.ntiles);
       const int ab = it & 1;
+      const int row0 = tile * M + q4 * 32;
       mbar_wait_sleep(&accf[ab], (it >> 1) & 1);
       tc_fence_after();
-      const int64_t l = static_cast<int64_t>(tile) * M + r;
-      const bool live = l < a.L;
-      const int64_t row = (static_cast<int64_t>(h) * a.L + (live ? l : 0)) * N;
 #pragma unroll 1
-      for (int c = 0; c < N / 32; ++c, ++nst) {
+      for (int c = c0; c < N / 32; c += CSTEP, ++nst) {
+        uint8_t* box = obuf + (nst & 1) * Lay::O_BYTES;
+        uint64_t* ob = &obar[ew * 2 + (nst & 1)];
+        // the box written two stores ago has been read out
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if (dsig) {
+            mbar_arrive_expect_tx(ob, Lay::O_BYTES);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+                "%5}], [%2];" ::"r"(smem_u32(box)),
+                "l"(reinterpret_cast<uint64_t>(&a.mAux)), "r"(smem_u32(ob)), "r"(c * 32), "r"(row0), "r"(h)
+                : "memory");
+          }
+        }
         uint32_t u[32];
         tmem_ld32(tmem + ab * 128 + (static_cast<uint32_t>(q4 * 32) << 16) + c * 32, u);
         tmem_wait_ld();
-        if (c == N / 32 - 1) {
+        if (c + CSTEP >= N / 32) {
           tc_fence_before();
           mbar_arrive(&acce[ab]);
         }
@@ -311,21 +342,19 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(u[j]);
         if (a.epi == EPI_SIGMOID) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 1.f / (1.f + __expf(-v[j]));
-        } else if (a.epi == EPI_DSIG && live) {
+          for (int j = 0; j < 32; ++j) v[j] = __frcp_rn(1.f + __expf(-v[j]));
+        } else if (dsig) {
+          mbar_wait(ob, (nst >> 1) & 1);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 g = __ldg(reinterpret_cast<const float4*>(a.aux + row + c * 32 + j));
-            v[j] *= g.x * (1.f - g.x);
-            v[j + 1] *= g.y * (1.f - g.y);
-            v[j + 2] *= g.z * (1.f - g.z);
-            v[j + 3] *= g.w * (1.f - g.w);
+          for (int j = 0; j < 8; ++j) {
+            const float4 g = *reinterpret_cast<const float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4));
+            v[4 * j] *= g.x * (1.f - g.x);
+            v[4 * j + 1] *= g.y * (1.f - g.y);
+            v[4 * j + 2] *= g.z * (1.f - g.z);
+            v[4 * j + 3] *= g.w * (1.f - g.w);
           }
         }
-        // the box written two stores ago has been read out
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
-        uint8_t* box = obuf + (nst & 1) * Lay::O_BYTES;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<float4*>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
@@ -335,7 +364,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
         if (lane == 0) {
           asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                            reinterpret_cast<uint64_t>(&a.mC)),
-                       "r"(smem_u32(box)), "r"(c * 32), "r"(tile * M + q4 * 32), "r"(h)
+                       "r"(smem_u32(box)), "r"(c * 32), "r"(row0), "r"(h)
                        : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -345,7 +374,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1) stage1_rows_kernel(const __gr
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == Lay::W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
   }
@@ -548,6 +577,11 @@ extern "C" int ropeslr_stage1_gemm_rows(int64_t H, int64_t L, int32_t K, int32_t
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
         CUDA_SUCCESS)
       return ROPESLR_ERR_LAUNCH;
+    if (aux != nullptr &&
+        enc(&a.mAux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(aux), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return ROPESLR_ERR_LAUNCH;
   }
   const int64_t total = H * a.ntiles;
   const unsigned grid = static_cast<unsigned>(total < num_sms() ? total : num_sms());
@@ -558,7 +592,7 @@ extern "C" int ropeslr_stage1_gemm_rows(int64_t H, int64_t L, int32_t K, int32_t
     if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, s1g::RowsLay<K_, N_>::BYTES) != \
         cudaSuccess)                                                                                         \
       return ROPESLR_ERR_LAUNCH;                                                                             \
-    kfn<<<grid, s1g::kRowsThreads, s1g::RowsLay<K_, N_>::BYTES, st>>>(a);                                    \
+    kfn<<<grid, s1g::RowsLay<K_, N_>::THREADS, s1g::RowsLay<K_, N_>::BYTES, st>>>(a);                                    \
   }
   if (K == 128 && N == 64) ROPESLR_ROWS(128, 64)
   else if (K == 64 && N == 128) ROPESLR_ROWS(64, 128)
