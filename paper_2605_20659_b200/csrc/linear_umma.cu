@@ -209,61 +209,100 @@ struct StateArgs {
   int ntiles;           // ceil(L / SR)
   int tiles_per_cta;
   int nchunks;
-  const uint8_t* tables;  // [H][3][nrows][TAB_PITCH] bf16 (q, k, v)
-  float* partial;       // [BH][nchunks][128][NPART]
+  const uint8_t* tables;  // [H][3][nrows][TAB_PITCH] bf16 (q, k, v): the rows of t read here
+  float* partial;       // [BH][nchunks][128][NPART]: phi(K)^T (V + T_xy,v) per chunk
+  float* phi_t;         // [BH][nchunks][T][128]: sum of phi(k) over the chunk's tokens of each t
 };
 
-// The state pass streams 64-token stages, four deep (more bytes in flight per
-// SM than two 128-token ones in the same space).
+// The state pass streams 64-token stages, three deep: per stage K, V and the
+// stage's 64 rows of the (x, y) tables of k and v (T_xy[x W + y] = T_x[x] +
+// T_y[y], rows repeated past H W so a stage never wraps).  The t part of the
+// PE is per-t: phi(k + T_k) takes T_t,k[t] from shared memory, and the V side
+// of it, sum_l phi(k_l) T_t,v[t(l)], is (sum over the tokens of each t of
+// phi(k)) x T_t,v[t]: the per-t sums go out with the chunk (phi_t) and the
+// reduce kernel adds their products with T_t,v (float32 tables).
 constexpr int SR = 64;                 // tokens per state stage
 constexpr int SHALF = SR * 128;        // 8 KiB: one 64-column half of a stage tile
 constexpr int STILE = 2 * SHALF;       // 16 KiB
-constexpr int SST = 4;                 // state ring depth
-// smem: K ring (4 x 16 KiB) | V ring (4 x 16 KiB) | T_k | T_v | barriers
+constexpr int SST = 3;                 // state ring depth
+// smem: [SST][K | V | Txy_k | Txy_v] | T_t,k rows | phi_t sums [T][128] | barriers
 struct StateLay {
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + SST * STILE;
-  static constexpr int OFF_TAB = OFF_V + SST * STILE;
-  __host__ __device__ static int off_bar(int nrows) { return OFF_TAB + ((2 * nrows * TAB_PITCH + 127) / 128) * 128; }
-  __host__ __device__ static int bytes(int nrows) { return off_bar(nrows) + (5 * SST + 2) * 8 + 16; }
+  static constexpr int STAGE = 4 * STILE;
+  static constexpr int OFF_TAB = SST * STAGE;
+  __host__ __device__ static int off_phi(int T) { return OFF_TAB + ((T * TAB_PITCH + 127) / 128) * 128; }
+  __host__ __device__ static int off_bar(int T) { return off_phi(T) + T * D * 4; }
+  __host__ __device__ static int bytes(int T) { return off_bar(T) + (3 * SST + 2) * 8 + 16; }
 };
 
-constexpr int kStateXf = 512;                 // transform threads: 8 per token row, 2 chunks of K and of V each
+constexpr int kStateXf = 512;                 // transform threads: 8 per token row, 2 chunks each
 constexpr int kStateThreads = kStateXf + 64;  // + warp 16 TMA, warp 17 MMA + TMEM
 constexpr int kStateTma = kStateXf / 32, kStateMma = kStateTma + 1;
 
+// phi(k + T_t[t] + T_xy) in place on chunks [c0, c0 + NC) of row r of the K
+// stage tile (T_xy from the stage's table tile, same swizzled position),
+// added into acc; rows of tokens beyond L become zero.
+template <int NC>
+__device__ __forceinline__ void state_row(uint8_t* tk, const uint8_t* txy, int r, int c0, bool valid,
+                                          const uint8_t* tt, float (&acc)[NC * 8]) {
+#pragma unroll
+  for (int cc = 0; cc < NC; ++cc) {
+    const int c = c0 + cc;
+    uint4* p = tile_chunk<SR>(tk, r, c);
+    if (!valid) {
+      *p = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4 u = *p;
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t a4[4] = {0u, 0u, 0u, 0u}, b4[4] = {0u, 0u, 0u, 0u};
+    if (tt != nullptr) {
+      const uint4 a = *tile_chunk<SR>(const_cast<uint8_t*>(txy), r, c);
+      const uint4 b = *reinterpret_cast<const uint4*>(tt + c * 16);
+      a4[0] = a.x; a4[1] = a.y; a4[2] = a.z; a4[3] = a.w;
+      b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = bf16x2_to_f32x2(w[i]);
+      if (tt != nullptr) f = __fadd2_rn(f, __fadd2_rn(bf16x2_to_f32x2(b4[i]), bf16x2_to_f32x2(a4[i])));
+      f = phi2(f);
+      acc[cc * 8 + 2 * i] += f.x;
+      acc[cc * 8 + 2 * i + 1] += f.y;
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
+      o[i] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    *p = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 __global__ void __launch_bounds__(kStateThreads, 1)
     linear_state_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ StateArgs a) {
+                        const __grid_constant__ CUtensorMap tmXY, const __grid_constant__ StateArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int bh = blockIdx.y, chunk = blockIdx.x;
   const int h = bh % a.H;
+  const int T = a.g.T, HW = a.g.Hg * a.g.Wg;
   const int t0 = chunk * a.tiles_per_cta;
   const int t1 = min(a.ntiles, t0 + a.tiles_per_cta);
   const int n = max(0, t1 - t0);
-  uint8_t* sK = smem + StateLay::OFF_K;
-  uint8_t* sV = smem + StateLay::OFF_V;
   uint8_t* sTab = smem + StateLay::OFF_TAB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(a.nrows));
+  float* sPhi = reinterpret_cast<float*>(smem + StateLay::off_phi(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(T));
   uint64_t* full = bars;                 // [SST] TMA -> transform
-  uint64_t* ready = bars + SST;          // [SST] phi(K) written -> MMA (phi(K)^T V)
-  uint64_t* vdone = bars + 2 * SST;      // [SST] that MMA done -> transform (V buffer free for the PE tile)
-  uint64_t* tvready = bars + 3 * SST;    // [SST] PE tile written -> MMA (phi(K)^T T_v)
-  uint64_t* empty = bars + 4 * SST;      // [SST] MMA -> TMA
-  uint64_t* done = bars + 5 * SST;       // MMA -> readout
-  uint64_t* tabf = done + 1;             // tables landed
+  uint64_t* ready = bars + SST;          // [SST] phi(K) written -> MMA
+  uint64_t* empty = bars + 2 * SST;      // [SST] MMA -> TMA
+  uint64_t* done = bars + 3 * SST;       // MMA -> readout
+  uint64_t* tabf = done + 1;             // T_t,k rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tabf + 1);
-  const uint8_t* gtab = a.tables + (static_cast<int64_t>(h) * 3) * a.nrows * TAB_PITCH;
-  const int tab_bytes = a.nrows * TAB_PITCH;
   const bool pe = a.use_pe != 0;
+  auto stage = [&](int s) { return smem + s * StateLay::STAGE; };  // K | V | Txy_k | Txy_v
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&ready[i], kStateXf);
-      mbar_init(&vdone[i], 1);
-      mbar_init(&tvready[i], kStateXf);
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
@@ -281,123 +320,105 @@ __global__ void __launch_bounds__(kStateThreads, 1)
 
   if (warp == kStateTma) {
     if (elect_one()) {
-      if (a.use_pe) {
-        mbar_arrive_expect_tx(tabf, 2 * tab_bytes);
-        bulk_load_1d(sTab, gtab + 1 * tab_bytes, tab_bytes, tabf, policy_evict_last());
-        bulk_load_1d(sTab + tab_bytes, gtab + 2 * tab_bytes, tab_bytes, tabf, policy_evict_last());
+      if (pe) {
+        const uint8_t* gk = a.tables + (static_cast<int64_t>(h) * 3 + 1) * a.nrows * TAB_PITCH;  // k, rows 0..T-1
+        mbar_arrive_expect_tx(tabf, T * TAB_PITCH);
+        bulk_load_1d(sTab, gk, T * TAB_PITCH, tabf, policy_evict_last());
       }
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = policy_evict_first(), pol_t = policy_evict_last();
       for (int i = 0; i < n; ++i) {
         const int s = i % SST;
         if (i >= SST) mbar_wait_sleep(&empty[s], ((i / SST) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], 2 * STILE);
+        mbar_arrive_expect_tx(&full[s], (pe ? 4 : 2) * STILE);
         const int row = (t0 + i) * SR;
-        uint8_t* k = sK + s * STILE;
-        uint8_t* v = sV + s * STILE;
-        tma_load_3d_hint(k, &tmK, &full[s], 0, row, bh, pol);
-        tma_load_3d_hint(k + SHALF, &tmK, &full[s], 64, row, bh, pol);
-        tma_load_3d_hint(v, &tmV, &full[s], 0, row, bh, pol);
-        tma_load_3d_hint(v + SHALF, &tmV, &full[s], 64, row, bh, pol);
+        uint8_t* st = stage(s);
+        tma_load_3d_hint(st, &tmK, &full[s], 0, row, bh, pol);
+        tma_load_3d_hint(st + SHALF, &tmK, &full[s], 64, row, bh, pol);
+        tma_load_3d_hint(st + STILE, &tmV, &full[s], 0, row, bh, pol);
+        tma_load_3d_hint(st + STILE + SHALF, &tmV, &full[s], 64, row, bh, pol);
+        if (pe) {
+          const int xy0 = row % HW;
+          tma_load_3d_hint(st + 2 * STILE, &tmXY, &full[s], 0, xy0, 2 * h, pol_t);
+          tma_load_3d_hint(st + 2 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h, pol_t);
+          tma_load_3d_hint(st + 3 * STILE, &tmXY, &full[s], 0, xy0, 2 * h + 1, pol_t);
+          tma_load_3d_hint(st + 3 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h + 1, pol_t);
+        }
       }
     }
   } else if (warp == kStateMma) {
-    // per tile i: S += phi(K_i)^T V_i, then (with PE) S += phi(K_i)^T Tv_i once
-    // the transform has put the PE tile into V_i's buffer; the second MMA of
-    // tile i - 1 goes after the first of tile i so the transform overlaps both
+    // per stage: S += phi(K)^T V, then (with PE) S += phi(K)^T T_xy,v
     constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
     const bool leader = elect_one();
-    auto mma = [&](int s, uint32_t first) {
-      const uint64_t dA = desc_sw128(smem_u32(sK + s * STILE), SHALF, 1024);
-      const uint64_t dB = desc_sw128(smem_u32(sV + s * STILE), SHALF, 1024);
-#pragma unroll
-      for (int kk = 0; kk < SR / 16; ++kk)
-        mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
-                    idesc_s, (first != 0 || kk > 0) ? 1u : 0u);
-    };
-    auto second = [&](int j) {  // the PE tile of tile j
-      const int s = j % SST;
-      mbar_wait_sleep(&tvready[s], (j / SST) & 1);
-      tc_fence_after();
-      if (leader) {
-        mma(s, 1u);
-        mma_commit(&empty[s]);
-        if (j == n - 1) mma_commit(done);
-      }
-      __syncwarp();
-    };
     for (int i = 0; i < n; ++i) {
       const int s = i % SST;
       mbar_wait_sleep(&ready[s], (i / SST) & 1);
       tc_fence_after();
       if (leader) {
-        mma(s, i > 0 ? 1u : 0u);
+        uint8_t* st = stage(s);
+        const uint64_t dA = desc_sw128(smem_u32(st), SHALF, 1024);
+        const uint64_t dV = desc_sw128(smem_u32(st + STILE), SHALF, 1024);
+        const uint64_t dT = desc_sw128(smem_u32(st + 3 * STILE), SHALF, 1024);
+#pragma unroll
+        for (int kk = 0; kk < SR / 16; ++kk)
+          mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dV + static_cast<uint64_t>((kk * 2048) >> 4),
+                      idesc_s, (i > 0 || kk > 0) ? 1u : 0u);
         if (pe) {
-          mma_commit(&vdone[s]);
-        } else {
-          mma_commit(&empty[s]);
-          if (i == n - 1) mma_commit(done);
+#pragma unroll
+          for (int kk = 0; kk < SR / 16; ++kk)
+            mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4),
+                        dT + static_cast<uint64_t>((kk * 2048) >> 4), idesc_s, 1u);
         }
+        mma_commit(&empty[s]);
+        if (i == n - 1) mma_commit(done);
       }
       __syncwarp();
-      if (pe && i > 0) second(i - 1);
     }
-    if (pe && n > 0) second(n - 1);
   } else {
-    // transform warps: 8 threads per token row, 2 of its 16 chunks each;
-    // z = sum phi(k) accumulates in registers over the CTA's tiles
+    // transform warps: 8 threads per token row, 2 of its 16 chunks each; the
+    // phi sums of the row slot accumulate in registers per t and go into
+    // sPhi[t] (shared-memory adds) when the slot's t changes
     const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 2;
-    const uint8_t* tk = nullptr;
-    const uint8_t* tv = nullptr;
-    if (pe) {
-      mbar_wait_sleep(tabf, 0);
-      tk = sTab;
-      tv = sTab + tab_bytes;
-    }
+    for (int e = threadIdx.x; e < T * D; e += kStateXf) sPhi[e] = 0.f;
+    asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
+    if (pe) mbar_wait_sleep(tabf, 0);
     float zacc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) zacc[j] = 0.f;
-    auto pe_tile = [&](int j) {  // the PE part of V_j into V_j's buffer once phi(K_j)^T V_j is done
-      const int s = j % SST;
-      mbar_wait_sleep(&vdone[s], (j / SST) & 1);
-      const int64_t l = static_cast<int64_t>(t0 + j) * SR + r;
-      const bool valid = l < a.L;
-      int rt = 0, rx = 0, ry = 0;
-      if (valid) a.g.rows(l, rt, rx, ry);
-      table_row<2, SR>(sV + s * STILE, r, c0, valid, tv, rt, rx, ry);
-      fence_proxy_async_smem();
-      mbar_arrive(&tvready[s]);
+    int cur_t = -1;
+    auto flush = [&]() {
+      if (cur_t < 0) return;
+      float* dst = sPhi + cur_t * D + c0 * 8;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        atomicAdd(dst + j, zacc[j]);
+        zacc[j] = 0.f;
+      }
     };
     for (int i = 0; i < n; ++i) {
       const int s = i % SST;
-      mbar_wait_sleep(&full[s], (i / SST) & 1);
       const int64_t l = static_cast<int64_t>(t0 + i) * SR + r;
       const bool valid = l < a.L;
-      int rt = 0, rx = 0, ry = 0;
-      if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true, 2, true, false, SR>(sK + s * STILE, r, c0, valid, tk, rt, rx, ry, &zacc);
+      const int t = valid ? static_cast<int>(l / HW) : cur_t;
+      if (t != cur_t) {
+        flush();
+        cur_t = t;
+      }
+      mbar_wait_sleep(&full[s], (i / SST) & 1);
+      uint8_t* st = stage(s);
+      state_row<2>(st, st + 2 * STILE, r, c0, valid, pe ? sTab + t * TAB_PITCH : nullptr, zacc);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
-      if (pe && i > 0) pe_tile(i - 1);
     }
-    if (pe && n > 0) pe_tile(n - 1);
-    // every MMA has read the K ring: reuse it for the z partials
-    // zbuf[thread][16] (thread = 8 r + q holds columns [16 q, 16 q + 16))
-    if (n > 0) mbar_wait_sleep(done, 0);
-    float* zbuf = reinterpret_cast<float*>(sK);
-#pragma unroll
-    for (int j = 0; j < 16; j += 4)
-      *reinterpret_cast<float4*>(zbuf + threadIdx.x * 16 + j) = make_float4(zacc[j], zacc[j + 1], zacc[j + 2], zacc[j + 3]);
+    flush();
     asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
+    float* gphi = a.phi_t + (static_cast<int64_t>(bh) * a.nchunks + chunk) * T * D;
+    for (int e = threadIdx.x; e < T * D; e += kStateXf) gphi[e] = sPhi[e];
   }
   if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out
     const int r = threadIdx.x;
-    // the chunk's partial [S | z]: TMEM lane r = row r (d_k) of S
     float* dst = a.partial + ((static_cast<int64_t>(bh) * a.nchunks + chunk) * D + r) * NPART;
-    // z[r] over the 64 token slots in fixed order
-    const float* zbuf = reinterpret_cast<const float*>(sK);
-    float zsum = 0.f;
-    for (int slot = 0; slot < SR; ++slot) zsum += zbuf[(slot * 8 + (r >> 4)) * 16 + (r & 15)];
     if (n > 0) {
+      mbar_wait_sleep(done, 0);
       tc_fence_after();
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
 #pragma unroll 1
@@ -410,11 +431,8 @@ __global__ void __launch_bounds__(kStateThreads, 1)
           *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(
               __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
       }
-      dst[128] = zsum;
-#pragma unroll
-      for (int j = 129; j < NPART; ++j) dst[j] = 0.f;
     } else {
-      for (int j = 0; j < NPART; ++j) dst[j] = 0.f;
+      for (int j = 0; j < D; ++j) dst[j] = 0.f;
     }
   }
   tc_fence_before();
@@ -427,24 +445,55 @@ __global__ void __launch_bounds__(kStateThreads, 1)
 
 // Sum the chunk partials (fixed order, float64) and write the apply GEMM's B
 // operand: B[n][k] = S[k][n] / L for n < 128, B[128][k] = z[k] / L, zero rows
-// above; K-major, two 64-wide K halves of [144 rows x 128 B], 128B-swizzled
-// as a 1024-aligned shared-memory copy expects, in fp16.  The common 1/L
-// cancels in phi(q) S / phi(q) z and keeps z (a sum of L positive terms)
-// inside fp16's range; fp16's 11-bit significand keeps S and z to ~5e-4,
-// against bf16's 2^-9 for the phi(q) operand it meets in the MMA.  Also S
-// and z in float32, unscaled (state [BH][128][NPART]), for inspection.
-__global__ void __launch_bounds__(256) linear_reduce_image_kernel(const float* __restrict__ partial, int nchunks,
+// above, with S = sum_chunks phi(K)^T (V + T_xy,v) + sum_t Phi[t]^T T_t,v[t]
+// (Phi[t] = the chunks' phi_t summed; float32 T_t,v) and z = sum_t Phi[t];
+// K-major, two 64-wide K halves of [144 rows x 128 B], 128B-swizzled as a
+// 1024-aligned shared-memory copy expects, in fp16.  The common 1/L cancels
+// in phi(q) S / phi(q) z and keeps z (a sum of L positive terms) inside
+// fp16's range; fp16's 11-bit significand keeps S and z to ~5e-4, against
+// bf16's 2^-9 for the phi(q) operand it meets in the MMA.  Also S and z in
+// float32, unscaled (state [BH][128][NPART]), for inspection.
+// phi_tot[bh][t][k] = sum over the chunks of phi_t (fixed order, float64).
+__global__ void __launch_bounds__(128) linear_phi_sum_kernel(const float* __restrict__ phi_t, int nchunks, int T,
+                                                             double* __restrict__ phi_tot) {
+  const int bh = blockIdx.x, t = blockIdx.y, k = threadIdx.x;
+  const float* p = phi_t + (static_cast<int64_t>(bh) * nchunks * T + t) * D + k;
+  double acc = 0.0;
+  for (int c = 0; c < nchunks; ++c) acc += p[static_cast<int64_t>(c) * T * D];
+  phi_tot[(static_cast<int64_t>(bh) * T + t) * D + k] = acc;
+}
+
+// grid (BH, D / 8): block = 8 rows k of S (one per warp), lanes over the
+// columns n (coalesced partial loads); T_t,v and the block's Phi rows are
+// staged in shared memory.
+__global__ void __launch_bounds__(256) linear_reduce_image_kernel(const float* __restrict__ partial,
+                                                                  const double* __restrict__ phi_tot, int nchunks, int T,
+                                                                  int H, const float* __restrict__ tf, int nrows,
                                                                   double inv_L, uint8_t* __restrict__ bimg,
                                                                   float* __restrict__ state) {
-  const int bh = blockIdx.x;
+  extern __shared__ double sRed[];  // T_t,v [T][128] | Phi [8][T]
+  double* sTv = sRed;
+  double* sPhi = sRed + T * D;
+  const int bh = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.y * 8 + warp;
+  // T_t,v rows (float32 tables [H][3][nrows][128], tensor 2 = v, rows 0..T-1)
+  const float* tv = tf != nullptr ? tf + (static_cast<int64_t>(bh % H) * 3 + 2) * nrows * D : nullptr;
+  for (int e = threadIdx.x; e < T * D; e += blockDim.x) sTv[e] = tv != nullptr ? static_cast<double>(tv[e]) : 0.0;
+  for (int e = threadIdx.x; e < 8 * T; e += blockDim.x)
+    sPhi[e] = phi_tot[(static_cast<int64_t>(bh) * T + e % T) * D + blockIdx.y * 8 + e / T];
+  __syncthreads();
   const float* src = partial + static_cast<int64_t>(bh) * nchunks * D * NPART;
   uint8_t* img = bimg + static_cast<int64_t>(bh) * BIMG;
-  // blockIdx.y: 16 of the 144 image rows; thread: (row, k)
-  for (int e = threadIdx.x; e < 16 * D; e += blockDim.x) {
-    const int n = blockIdx.y * 16 + e / D, k = e % D;
+  const double* ph = sPhi + warp * T;
+  for (int n = lane; n < NB; n += 32) {
     double acc = 0.0;
-    if (n <= 128)
+    if (n < 128) {
       for (int c = 0; c < nchunks; ++c) acc += src[(static_cast<int64_t>(c) * D + k) * NPART + n];
+      if (tv != nullptr)
+        for (int t = 0; t < T; ++t) acc += ph[t] * sTv[t * D + n];
+    } else if (n == 128) {
+      for (int t = 0; t < T; ++t) acc += ph[t];
+    }
     if (state != nullptr && n <= 128) state[(static_cast<int64_t>(bh) * D + k) * NPART + n] = static_cast<float>(acc);
     const int half = k >> 6, ch = (k & 63) >> 3, el = k & 7;
     const int off = half * BHALF + n * 128 + ((ch ^ (n & 7)) << 4) + el * 2;
@@ -666,7 +715,8 @@ __global__ void __launch_bounds__(128) linear_fold_kernel(const float* __restric
                                                           const float* __restrict__ alpha,
                                                           const float* __restrict__ wq, const float* __restrict__ wk,
                                                           const float* __restrict__ wv, int64_t Dt, int T, int Hg,
-                                                          int Wg, uint8_t* __restrict__ tables) {
+                                                          int Wg, uint8_t* __restrict__ tables,
+                                                          float* __restrict__ tf) {
   constexpr int RT = 16, CK = 32;
   __shared__ float sp[RT][CK];
   const int nrows = T + Hg + Wg;
@@ -701,10 +751,29 @@ __global__ void __launch_bounds__(128) linear_fold_kernel(const float* __restric
     __syncthreads();
   }
   uint8_t* out = tables + (static_cast<int64_t>(h) * 3 + z) * nrows * TAB_PITCH;
+  float* outf = tf + (static_cast<int64_t>(h) * 3 + z) * nrows * D;
 #pragma unroll
   for (int i = 0; i < RT; ++i) {
     const int row = r0 + i;
-    if (row < nrows) reinterpret_cast<__nv_bfloat16*>(out + row * TAB_PITCH)[j] = __float2bfloat16_rn(acc[i]);
+    if (row < nrows) {
+      reinterpret_cast<__nv_bfloat16*>(out + row * TAB_PITCH)[j] = __float2bfloat16_rn(acc[i]);
+      outf[row * D + j] = acc[i];
+    }
+  }
+}
+
+// The (x, y) tables of k and v: Txy[h][z - 1][i][j] = bf16(T_x[x] + T_y[y]) in
+// float32, x = (i mod HW) / W, y = i mod W, for i < HW + SR (a stage's 64
+// rows never wrap).  grid (ceil(rows / 8), 2 H), 128 threads (column j).
+__global__ void __launch_bounds__(128) linear_xy_kernel(const float* __restrict__ tf, int T, int Hg, int Wg, int nrows,
+                                                        int xye, __nv_bfloat16* __restrict__ xy) {
+  const int h = blockIdx.y >> 1, z = 1 + (blockIdx.y & 1);
+  const float* src = tf + (static_cast<int64_t>(h) * 3 + z) * nrows * D;
+  __nv_bfloat16* dst = xy + (static_cast<int64_t>(h) * 2 + (z - 1)) * xye * D;
+  const int HW = Hg * Wg, j = threadIdx.x;
+  for (int i = blockIdx.x * 8; i < min(xye, blockIdx.x * 8 + 8); ++i) {
+    const int u = i % HW, x = u / Wg, y = u % Wg;
+    dst[static_cast<int64_t>(i) * D + j] = __float2bfloat16_rn(src[(T + x) * D + j] + src[(T + Hg + y) * D + j]);
   }
 }
 
@@ -802,6 +871,26 @@ static bool make_map(CUtensorMap* m, const void* base, int64_t BH, int64_t L, in
 
 static int nrows_of(const ropeslr_token_args* t) { return t->grid_t + t->grid_h + t->grid_w; }
 
+// The tables buffer: per-axis bf16 rows [H][3][nrows][TAB_PITCH] | gate
+// scalars G [nrows] | per-axis float32 rows [H][3][nrows][128] | the (x, y)
+// tables of k and v [H][2][HW + SR][128] bf16.
+struct TabLay {
+  size_t ax, g, tf, xy, total;
+  int xye;
+};
+static size_t up256(size_t x);
+static TabLay tab_layout(int64_t H, const ropeslr_token_args* t) {
+  const int nr = nrows_of(t);
+  TabLay y{};
+  y.xye = t->grid_h * t->grid_w + SR;
+  y.ax = 0;
+  y.g = up256(static_cast<size_t>(H) * 3 * nr * TAB_PITCH);
+  y.tf = y.g + up256(static_cast<size_t>(nr) * 4);
+  y.xy = y.tf + up256(static_cast<size_t>(H) * 3 * nr * D * 4);
+  y.total = y.xy + up256(static_cast<size_t>(H) * 2 * y.xye * D * 2);
+  return y;
+}
+
 // CTAs per head: one wave over all heads (one CTA per SM; BH * chunks <= SMs
 // when BH <= SMs, so no tail wave).
 static int chunks_per_head(int64_t BH, int ntiles) {
@@ -820,13 +909,13 @@ using namespace ropeslr;
 static bool linear_pe_eligible(const ropeslr_shape* s, const ropeslr_token_args* t) {
   if (!s || !t || s->dtype != ROPESLR_BF16 || s->d != lnu::D || s->L >= (1LL << 31)) return false;
   const int nr = lnu::nrows_of(t);
-  return lnu::StateLay::bytes(nr) <= 227 * 1024 && lnu::ApplyLay::bytes(nr) <= 227 * 1024;
+  return lnu::StateLay::bytes(t->grid_t) <= 227 * 1024 && lnu::ApplyLay::bytes(nr) <= 227 * 1024 &&
+         t->grid_t * (lnu::D + 8) * 8 <= 200 * 1024;
 }
 
 extern "C" size_t ropeslr_linear_tables_bytes(const ropeslr_shape* s, const ropeslr_token_args* t) {
   if (!linear_pe_eligible(s, t)) return 0;
-  const int nr = lnu::nrows_of(t);
-  return lnu::up256(static_cast<size_t>(s->H) * 3 * nr * lnu::TAB_PITCH) + lnu::up256(static_cast<size_t>(nr) * 4);
+  return lnu::tab_layout(s->H, t).total;
 }
 
 extern "C" int ropeslr_linear_tables(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_q,
@@ -841,12 +930,18 @@ extern "C" int ropeslr_linear_tables(const ropeslr_shape* s, const ropeslr_token
   if (t->d_model < (t->head_offset + s->H) * s->d) return ROPESLR_ERR_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nr = lnu::nrows_of(t);
+  const lnu::TabLay ly = lnu::tab_layout(s->H, t);
   uint8_t* tab = static_cast<uint8_t*>(tables);
+  float* tf = reinterpret_cast<float*>(tab + ly.tf);
   lnu::linear_fold_kernel<<<dim3(static_cast<unsigned>(ceil_div(nr, 16)), static_cast<unsigned>(3 * s->H)), 128, 0,
                             st>>>(t->pe_t, t->pe_x, t->pe_y, t->alpha, w_q, w_k, w_v, t->d_model, t->grid_t,
-                                  t->grid_h, t->grid_w, tab);
+                                  t->grid_h, t->grid_w, tab, tf);
   if (int e = launch_status()) return e;
-  float* G = reinterpret_cast<float*>(tab + lnu::up256(static_cast<size_t>(s->H) * 3 * nr * lnu::TAB_PITCH));
+  lnu::linear_xy_kernel<<<dim3(static_cast<unsigned>(ceil_div(ly.xye, 8)), static_cast<unsigned>(2 * s->H)), 128, 0,
+                          st>>>(tf, t->grid_t, t->grid_h, t->grid_w, nr, ly.xye,
+                                reinterpret_cast<__nv_bfloat16*>(tab + ly.xy));
+  if (int e = launch_status()) return e;
+  float* G = reinterpret_cast<float*>(tab + ly.g);
   lnu::linear_gate_fold_kernel<<<nr, 256, 0, st>>>(t->pe_t, t->pe_x, t->pe_y, t->alpha, t->w_g, t->d_model,
                                                    t->head_offset * s->d, s->H * s->d, t->grid_t, t->grid_h, G);
   return launch_status();
@@ -858,7 +953,9 @@ extern "C" size_t ropeslr_linear_pe_workspace_bytes(const ropeslr_shape* s, cons
   const int ntiles = static_cast<int>(ceil_div(s->L, lnu::M));
   const int nch = lnu::chunks_per_head(BH, ntiles);
   return lnu::up256(static_cast<size_t>(BH) * nch * lnu::D * lnu::NPART * 4) +
-         lnu::up256(static_cast<size_t>(BH) * lnu::BIMG);
+         lnu::up256(static_cast<size_t>(BH) * lnu::BIMG) +
+         lnu::up256(static_cast<size_t>(BH) * nch * t->grid_t * lnu::D * 4) +
+         lnu::up256(static_cast<size_t>(BH) * t->grid_t * lnu::D * 8);
 }
 
 extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_token_args* t, const void* q_lin,
@@ -884,13 +981,18 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   const int tpc = static_cast<int>(ceil_div(ntiles, nch));
   float* partial = static_cast<float*>(ws);
   uint8_t* bimg = static_cast<uint8_t*>(ws) + lnu::up256(static_cast<size_t>(BH) * nch * lnu::D * lnu::NPART * 4);
+  float* phi_t = reinterpret_cast<float*>(bimg + lnu::up256(static_cast<size_t>(BH) * lnu::BIMG));
+  double* phi_tot = reinterpret_cast<double*>(reinterpret_cast<uint8_t*>(phi_t) +
+                                              lnu::up256(static_cast<size_t>(BH) * nch * t->grid_t * lnu::D * 4));
   const uint8_t* tab = static_cast<const uint8_t*>(tables);
-  const float* G = reinterpret_cast<const float*>(tab + lnu::up256(static_cast<size_t>(s->H) * 3 * nr * lnu::TAB_PITCH));
+  const lnu::TabLay ly = lnu::tab_layout(s->H, t);
+  const float* G = reinterpret_cast<const float*>(tab + ly.g);
   lnu::Grid3 g{t->grid_t, t->grid_h, t->grid_w};
 
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mxy;
   if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mk, k_lin, BH, s->L, lnu::SR) ||
-      !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR))
+      !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR) ||
+      !lnu::make_map(&mxy, tab + ly.xy, 2 * s->H, ly.xye, lnu::SR))
     return ROPESLR_ERR_LAUNCH;
   // state
   lnu::StateArgs sa{};
@@ -905,13 +1007,23 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   sa.nchunks = nch;
   sa.tables = tab;
   sa.partial = partial;
-  const int ssm = lnu::StateLay::bytes(nr);
+  sa.phi_t = phi_t;
+  const int ssm = lnu::StateLay::bytes(t->grid_t);
   if (cudaFuncSetAttribute(lnu::linear_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm) != cudaSuccess)
     return ROPESLR_ERR_LAUNCH;
-  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, sa);
+  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, mxy, sa);
   if (int e = launch_status()) return e;
-  lnu::linear_reduce_image_kernel<<<dim3(static_cast<unsigned>(BH), lnu::NB / 16), 256, 0, st>>>(
-      partial, nch, 1.0 / static_cast<double>(s->L), bimg, state);
+  const int rsm = t->grid_t * (lnu::D + 8) * 8;
+  if (rsm > 48 * 1024 && cudaFuncSetAttribute(lnu::linear_reduce_image_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, rsm) != cudaSuccess)
+    return ROPESLR_ERR_LAUNCH;
+  lnu::linear_phi_sum_kernel<<<dim3(static_cast<unsigned>(BH), static_cast<unsigned>(t->grid_t)), lnu::D, 0, st>>>(
+      phi_t, nch, t->grid_t, phi_tot);
+  if (int e = launch_status()) return e;
+  lnu::linear_reduce_image_kernel<<<dim3(static_cast<unsigned>(BH), lnu::D / 8), 256, rsm, st>>>(
+      partial, phi_tot, nch, t->grid_t, static_cast<int>(s->H), t->use_pe ? reinterpret_cast<const float*>(tab + ly.tf)
+                                                                        : nullptr,
+      nr, 1.0 / static_cast<double>(s->L), bimg, state);
   if (int e = launch_status()) return e;
   // apply
   lnu::ApplyArgs aa{};
