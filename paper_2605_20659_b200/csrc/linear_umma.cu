@@ -110,10 +110,12 @@ __device__ __forceinline__ float2 phi2(float2 k) {
 // F16OUT: store fp16 instead of bf16 (the apply GEMM runs fp16 x fp16).
 template <bool PHI, int NC, bool ACC = false, bool F16OUT = false, int ROWS = M>
 __device__ __forceinline__ void transform_row(uint8_t* tile, int r, int c0, bool valid, const uint8_t* tab, int rt,
-                                              int rx, int ry, float (*acc)[NC * 8] = nullptr) {
+                                              int rx, int ry, float (*acc)[NC * 8] = nullptr, int rot = 0) {
 #pragma unroll
   for (int cc = 0; cc < NC; ++cc) {
-    const int c = c0 + cc;
+    // rot: visit the chunks rotated (two threads of a row on the two halves
+    // then land in different bank groups of the swizzled tile)
+    const int c = c0 + ((cc + rot) & (NC - 1));
     uint4* p = tile_chunk<ROWS>(tile, r, c);
     if (!valid) {
       *p = make_uint4(0, 0, 0, 0);
@@ -209,76 +211,56 @@ struct StateArgs {
   int ntiles;           // ceil(L / SR)
   int tiles_per_cta;
   int nchunks;
-  const uint8_t* tables;  // [H][3][nrows][TAB_PITCH] bf16 (q, k, v): the rows of t read here
+  const __nv_bfloat16* k;   // [BH, L, 128] (x W_k, no PE)
+  const uint8_t* tables;    // [H][3][nrows][TAB_PITCH] bf16 (q, k, v): the rows of t read here
+  const __nv_bfloat16* xy;  // [H][2][xye][128] bf16: T_x + T_y of k (0) and v (1)
+  int xye;
   float* partial;       // [BH][nchunks][128][NPART]: phi(K)^T (V + T_xy,v) per chunk
   float* phi_t;         // [BH][nchunks][T][128]: sum of phi(k) over the chunk's tokens of each t
 };
 
-// The state pass streams 64-token stages, three deep: per stage K, V and the
-// stage's 64 rows of the (x, y) tables of k and v (T_xy[x W + y] = T_x[x] +
-// T_y[y], rows repeated past H W so a stage never wraps).  The t part of the
-// PE is per-t: phi(k + T_k) takes T_t,k[t] from shared memory, and the V side
-// of it, sum_l phi(k_l) T_t,v[t(l)], is (sum over the tokens of each t of
-// phi(k)) x T_t,v[t]: the per-t sums go out with the chunk (phi_t) and the
-// reduce kernel adds their products with T_t,v (float32 tables).
+// The state pass in 64-token stages.  K and its (x, y) table rows come
+// straight into the transform threads' registers (16-byte loads, the next
+// stage's in flight while the current one is transformed), and only
+// phi(k + T_k) is written to shared memory, as the MMA's A tile: the
+// tile never makes the TMA -> shared -> registers round trip, which with
+// the MMA's own reads made shared memory, not HBM, the binding rate.  V and
+// the stage's 64 rows of the (x, y) table of v (T_xy[x W + y] = T_x[x] +
+// T_y[y], rows repeated past H W so a stage never wraps) come by TMA and
+// sit side by side as one N = 256 B operand: S_v | S_xy = phi(K)^T [V |
+// T_xy,v] in one MMA per k-step.  The t part of the PE: phi(k + T_k) takes
+// T_t,k[t] from shared memory, and sum_l phi(k_l) T_t,v[t(l)] = sum_t (sum
+// over the tokens of t of phi(k)) T_t,v[t]: the per-t sums go out with the
+// chunk (phi_t) and the reduce kernel adds their products with T_t,v
+// (float32 tables).
 constexpr int SR = 64;                 // tokens per state stage
 constexpr int SHALF = SR * 128;        // 8 KiB: one 64-column half of a stage tile
 constexpr int STILE = 2 * SHALF;       // 16 KiB
-constexpr int SST = 3;                 // state ring depth
-// smem: [SST][K | V | Txy_k | Txy_v] | T_t,k rows | phi_t sums [T][128] | barriers
+constexpr int SST = 4;                 // state ring depth
+// smem: [SST][phi(K) | V | Txy_v] | T_t,k rows | phi_t sums [T][128] | barriers
 struct StateLay {
-  static constexpr int STAGE = 4 * STILE;
+  static constexpr int STAGE = 3 * STILE;
   static constexpr int OFF_TAB = SST * STAGE;
   __host__ __device__ static int off_phi(int T) { return OFF_TAB + ((T * TAB_PITCH + 127) / 128) * 128; }
   __host__ __device__ static int off_bar(int T) { return off_phi(T) + T * D * 4; }
-  __host__ __device__ static int bytes(int T) { return off_bar(T) + (3 * SST + 2) * 8 + 16; }
+  __host__ __device__ static int bytes(int T) { return off_bar(T) + (4 * SST + 2) * 8 + 16; }
 };
 
 constexpr int kStateXf = 512;                 // transform threads: 8 per token row, 2 chunks each
 constexpr int kStateThreads = kStateXf + 64;  // + warp 16 TMA, warp 17 MMA + TMEM
 constexpr int kStateTma = kStateXf / 32, kStateMma = kStateTma + 1;
 
-// phi(k + T_t[t] + T_xy) in place on chunks [c0, c0 + NC) of row r of the K
-// stage tile (T_xy from the stage's table tile, same swizzled position),
-// added into acc; rows of tokens beyond L become zero.
-template <int NC>
-__device__ __forceinline__ void state_row(uint8_t* tk, const uint8_t* txy, int r, int c0, bool valid,
-                                          const uint8_t* tt, float (&acc)[NC * 8]) {
-#pragma unroll
-  for (int cc = 0; cc < NC; ++cc) {
-    const int c = c0 + cc;
-    uint4* p = tile_chunk<SR>(tk, r, c);
-    if (!valid) {
-      *p = make_uint4(0, 0, 0, 0);
-      continue;
-    }
-    const uint4 u = *p;
-    uint32_t w[4] = {u.x, u.y, u.z, u.w};
-    uint32_t a4[4] = {0u, 0u, 0u, 0u}, b4[4] = {0u, 0u, 0u, 0u};
-    if (tt != nullptr) {
-      const uint4 a = *tile_chunk<SR>(const_cast<uint8_t*>(txy), r, c);
-      const uint4 b = *reinterpret_cast<const uint4*>(tt + c * 16);
-      a4[0] = a.x; a4[1] = a.y; a4[2] = a.z; a4[3] = a.w;
-      b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
-    }
-    uint32_t o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 f = bf16x2_to_f32x2(w[i]);
-      if (tt != nullptr) f = __fadd2_rn(f, __fadd2_rn(bf16x2_to_f32x2(b4[i]), bf16x2_to_f32x2(a4[i])));
-      f = phi2(f);
-      acc[cc * 8 + 2 * i] += f.x;
-      acc[cc * 8 + 2 * i + 1] += f.y;
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
-      o[i] = *reinterpret_cast<uint32_t*>(&h2);
-    }
-    *p = make_uint4(o[0], o[1], o[2], o[3]);
-  }
+__device__ __forceinline__ uint4 ldg_nc16(const void* p) {
+  uint4 u;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+               : "l"(p));
+  return u;
 }
 
 __global__ void __launch_bounds__(kStateThreads, 1)
-    linear_state_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                        const __grid_constant__ CUtensorMap tmXY, const __grid_constant__ StateArgs a) {
+    linear_state_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmXY,
+                        const __grid_constant__ StateArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int bh = blockIdx.y, chunk = blockIdx.x;
@@ -290,14 +272,14 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   uint8_t* sTab = smem + StateLay::OFF_TAB;
   float* sPhi = reinterpret_cast<float*>(smem + StateLay::off_phi(T));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(T));
-  uint64_t* full = bars;                 // [SST] TMA -> transform
-  uint64_t* ready = bars + SST;          // [SST] phi(K) written -> MMA
-  uint64_t* empty = bars + 2 * SST;      // [SST] MMA -> TMA
+  uint64_t* full = bars;                 // [SST] TMA (V, Txy_v) landed
+  uint64_t* ready = bars + SST;          // [SST] phi(K) written
+  uint64_t* empty = bars + 2 * SST;      // [SST] MMA done with the stage
   uint64_t* done = bars + 3 * SST;       // MMA -> readout
   uint64_t* tabf = done + 1;             // T_t,k rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tabf + 1);
   const bool pe = a.use_pe != 0;
-  auto stage = [&](int s) { return smem + s * StateLay::STAGE; };  // K | V | Txy_k | Txy_v
+  auto stage = [&](int s) { return smem + s * StateLay::STAGE; };  // phi(K) | V | Txy_v
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SST; ++i) {
@@ -329,55 +311,48 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       for (int i = 0; i < n; ++i) {
         const int s = i % SST;
         if (i >= SST) mbar_wait_sleep(&empty[s], ((i / SST) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], (pe ? 4 : 2) * STILE);
+        mbar_arrive_expect_tx(&full[s], (pe ? 2 : 1) * STILE);
         const int row = (t0 + i) * SR;
         uint8_t* st = stage(s);
-        tma_load_3d_hint(st, &tmK, &full[s], 0, row, bh, pol);
-        tma_load_3d_hint(st + SHALF, &tmK, &full[s], 64, row, bh, pol);
         tma_load_3d_hint(st + STILE, &tmV, &full[s], 0, row, bh, pol);
         tma_load_3d_hint(st + STILE + SHALF, &tmV, &full[s], 64, row, bh, pol);
         if (pe) {
           const int xy0 = row % HW;
-          tma_load_3d_hint(st + 2 * STILE, &tmXY, &full[s], 0, xy0, 2 * h, pol_t);
-          tma_load_3d_hint(st + 2 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h, pol_t);
-          tma_load_3d_hint(st + 3 * STILE, &tmXY, &full[s], 0, xy0, 2 * h + 1, pol_t);
-          tma_load_3d_hint(st + 3 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h + 1, pol_t);
+          tma_load_3d_hint(st + 2 * STILE, &tmXY, &full[s], 0, xy0, 2 * h + 1, pol_t);
+          tma_load_3d_hint(st + 2 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h + 1, pol_t);
         }
       }
     }
   } else if (warp == kStateMma) {
-    // per stage: S += phi(K)^T V, then (with PE) S += phi(K)^T T_xy,v
-    constexpr uint32_t idesc_s = idesc_bf16_f32(M, D, true, true);
+    // per stage: [S_v | S_xy] += phi(K)^T [V | T_xy,v] (N = 256 with PE)
+    const uint32_t idesc_s = pe ? idesc_bf16_f32(M, 2 * D, true, true) : idesc_bf16_f32(M, D, true, true);
     const bool leader = elect_one();
     for (int i = 0; i < n; ++i) {
       const int s = i % SST;
+      mbar_wait_sleep(&full[s], (i / SST) & 1);
       mbar_wait_sleep(&ready[s], (i / SST) & 1);
       tc_fence_after();
       if (leader) {
         uint8_t* st = stage(s);
         const uint64_t dA = desc_sw128(smem_u32(st), SHALF, 1024);
-        const uint64_t dV = desc_sw128(smem_u32(st + STILE), SHALF, 1024);
-        const uint64_t dT = desc_sw128(smem_u32(st + 3 * STILE), SHALF, 1024);
+        const uint64_t dB = desc_sw128(smem_u32(st + STILE), SHALF, 1024);
 #pragma unroll
         for (int kk = 0; kk < SR / 16; ++kk)
-          mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dV + static_cast<uint64_t>((kk * 2048) >> 4),
+          mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4), dB + static_cast<uint64_t>((kk * 2048) >> 4),
                       idesc_s, (i > 0 || kk > 0) ? 1u : 0u);
-        if (pe) {
-#pragma unroll
-          for (int kk = 0; kk < SR / 16; ++kk)
-            mma_bf16_ss(tmem, dA + static_cast<uint64_t>((kk * 2048) >> 4),
-                        dT + static_cast<uint64_t>((kk * 2048) >> 4), idesc_s, 1u);
-        }
         mma_commit(&empty[s]);
         if (i == n - 1) mma_commit(done);
       }
       __syncwarp();
     }
   } else {
-    // transform warps: 8 threads per token row, 2 of its 16 chunks each; the
-    // phi sums of the row slot accumulate in registers per t and go into
-    // sPhi[t] (shared-memory adds) when the slot's t changes
-    const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 2;
+    // transform warps: 8 threads per token row, 2 of its 16 chunks each.
+    // Registers hold this stage's K and T_xy,k chunks while the next
+    // stage's loads are in flight.  The phi sums of the row slot accumulate
+    // per t and go into sPhi[t] (shared-memory adds) when the slot's t changes.
+    // chunks c0 and c0 + 8: the 8 threads of a row (one shared-memory phase)
+    // touch 8 distinct 16-byte bank groups of the swizzled tile in each access
+    const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7;
     for (int e = threadIdx.x; e < T * D; e += kStateXf) sPhi[e] = 0.f;
     asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
     if (pe) mbar_wait_sleep(tabf, 0);
@@ -390,31 +365,104 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       float* dst = sPhi + cur_t * D + c0 * 8;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        atomicAdd(dst + j, zacc[j]);
+        atomicAdd(dst + (j < 8 ? j : 64 + j - 8), zacc[j]);
         zacc[j] = 0.f;
       }
     };
+    const __nv_bfloat16* kbase = a.k + static_cast<int64_t>(bh) * a.L * D + c0 * 8;
+    const __nv_bfloat16* xbase = a.xy + (static_cast<int64_t>(h) * 2) * a.xye * D + c0 * 8;
+    // token of this slot in stage i: l = (t0 + i) SR + r; its t and xy = l mod HW, stepped
+    int64_t l = static_cast<int64_t>(t0) * SR + r;
+    int tt = static_cast<int>(l / HW), xy = static_cast<int>(l - static_cast<int64_t>(tt) * HW);
+    auto load = [&](int64_t ll, int xyl, uint4 (&kv)[2], uint4 (&tv)[2]) {
+      if (ll < a.L) {
+        kv[0] = ldg_nc16(kbase + ll * D);
+        kv[1] = ldg_nc16(kbase + ll * D + 64);
+        if (pe) {
+          tv[0] = ldg_nc16(xbase + static_cast<int64_t>(xyl) * D);
+          tv[1] = ldg_nc16(xbase + static_cast<int64_t>(xyl) * D + 64);
+        }
+      }
+    };
+    // two stages ahead in flight: c (this stage), n (next), m (the one after)
+    uint4 kc[2] = {}, tc[2] = {}, kn[2] = {}, tn[2] = {}, km[2] = {}, tm[2] = {};
+    auto step = [&](int64_t& ll, int& xyl, int& tl) {
+      ll += SR;
+      xyl += SR;
+      while (xyl >= HW) {
+        xyl -= HW;
+        ++tl;
+      }
+    };
+    int64_t l1 = l;
+    int xy1 = xy, t1s = tt;
+    step(l1, xy1, t1s);  // stage 1's slot token
+    if (n > 0) load(l, xy, kc, tc);
+    if (n > 1) load(l1, xy1, kn, tn);
     for (int i = 0; i < n; ++i) {
       const int s = i % SST;
-      const int64_t l = static_cast<int64_t>(t0 + i) * SR + r;
       const bool valid = l < a.L;
-      const int t = valid ? static_cast<int>(l / HW) : cur_t;
-      if (t != cur_t) {
+      // the slot token two stages ahead
+      int64_t l2 = l1;
+      int xy2 = xy1, t2 = t1s;
+      step(l2, xy2, t2);
+      if (i + 2 < n) load(l2, xy2, km, tm);
+      if (valid && tt != cur_t) {
         flush();
-        cur_t = t;
+        cur_t = tt;
       }
-      mbar_wait_sleep(&full[s], (i / SST) & 1);
-      uint8_t* st = stage(s);
-      state_row<2>(st, st + 2 * STILE, r, c0, valid, pe ? sTab + t * TAB_PITCH : nullptr, zacc);
+      const uint8_t* trow = pe ? sTab + tt * TAB_PITCH : nullptr;
+      if (i >= SST) mbar_wait_sleep(&empty[s], ((i / SST) - 1) & 1);  // the MMA is done with this A tile
+      uint8_t* at = stage(s);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint4* p = tile_chunk<SR>(at, r, c0 + 8 * cc);
+        if (!valid) {
+          *p = make_uint4(0, 0, 0, 0);
+          continue;
+        }
+        const uint32_t w[4] = {kc[cc].x, kc[cc].y, kc[cc].z, kc[cc].w};
+        uint32_t a4[4] = {0u, 0u, 0u, 0u}, b4[4] = {0u, 0u, 0u, 0u};
+        if (pe) {
+          const uint4 b = *reinterpret_cast<const uint4*>(trow + (c0 + 8 * cc) * 16);
+          a4[0] = tc[cc].x; a4[1] = tc[cc].y; a4[2] = tc[cc].z; a4[3] = tc[cc].w;
+          b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 f = bf16x2_to_f32x2(w[e]);
+          if (pe) f = __fadd2_rn(f, __fadd2_rn(bf16x2_to_f32x2(b4[e]), bf16x2_to_f32x2(a4[e])));
+          f = phi2(f);
+          zacc[cc * 8 + 2 * e] += f.x;
+          zacc[cc * 8 + 2 * e + 1] += f.y;
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
+          o[e] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        *p = make_uint4(o[0], o[1], o[2], o[3]);
+      }
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
+      l = l1;
+      xy = xy1;
+      tt = t1s;
+      l1 = l2;
+      xy1 = xy2;
+      t1s = t2;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        kc[cc] = kn[cc];
+        tc[cc] = tn[cc];
+        kn[cc] = km[cc];
+        tn[cc] = tm[cc];
+      }
     }
     flush();
     asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
     float* gphi = a.phi_t + (static_cast<int64_t>(bh) * a.nchunks + chunk) * T * D;
     for (int e = threadIdx.x; e < T * D; e += kStateXf) gphi[e] = sPhi[e];
   }
-  if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out
+  if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out: S_v + S_xy
     const int r = threadIdx.x;
     float* dst = a.partial + ((static_cast<int64_t>(bh) * a.nchunks + chunk) * D + r) * NPART;
     if (n > 0) {
@@ -423,13 +471,22 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
+        uint32_t v[32], w[32];
         tmem_ld32(lane_base + c * 32, v);
+        if (pe) tmem_ld32(lane_base + 128 + c * 32, w);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(dst + c * 32 + j) = make_float4(
-              __uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        for (int j = 0; j < 32; j += 4) {
+          float4 o = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                 __uint_as_float(v[j + 3]));
+          if (pe) {
+            o.x += __uint_as_float(w[j]);
+            o.y += __uint_as_float(w[j + 1]);
+            o.z += __uint_as_float(w[j + 2]);
+            o.w += __uint_as_float(w[j + 3]);
+          }
+          *reinterpret_cast<float4*>(dst + c * 32 + j) = o;
+        }
       }
     } else {
       for (int j = 0; j < D; ++j) dst[j] = 0.f;
@@ -636,7 +693,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       const bool valid = l < a.L;
       int rt = 0, rx = 0, ry = 0;
       if (valid) a.g.rows(l, rt, rx, ry);
-      transform_row<true, 8, false, true>(sQ + s * TILE, r, c0, valid, tq, rt, rx, ry);
+      transform_row<true, 8, false, true>(sQ + s * TILE, r, c0, valid, tq, rt, rx, ry, nullptr, c0 >> 1);
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
     }
@@ -989,9 +1046,8 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   const float* G = reinterpret_cast<const float*>(tab + ly.g);
   lnu::Grid3 g{t->grid_t, t->grid_h, t->grid_w};
 
-  CUtensorMap mq, mk, mv, mxy;
-  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mk, k_lin, BH, s->L, lnu::SR) ||
-      !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR) ||
+  CUtensorMap mq, mv, mxy;
+  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR) ||
       !lnu::make_map(&mxy, tab + ly.xy, 2 * s->H, ly.xye, lnu::SR))
     return ROPESLR_ERR_LAUNCH;
   // state
@@ -1006,12 +1062,15 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   sa.tiles_per_cta = tpc * (lnu::M / lnu::SR);
   sa.nchunks = nch;
   sa.tables = tab;
+  sa.k = static_cast<const __nv_bfloat16*>(k_lin);
+  sa.xy = reinterpret_cast<const __nv_bfloat16*>(tab + ly.xy);
+  sa.xye = ly.xye;
   sa.partial = partial;
   sa.phi_t = phi_t;
   const int ssm = lnu::StateLay::bytes(t->grid_t);
   if (cudaFuncSetAttribute(lnu::linear_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm) != cudaSuccess)
     return ROPESLR_ERR_LAUNCH;
-  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, mxy, sa);
+  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mv, mxy, sa);
   if (int e = launch_status()) return e;
   const int rsm = t->grid_t * (lnu::D + 8) * 8;
   if (rsm > 48 * 1024 && cudaFuncSetAttribute(lnu::linear_reduce_image_kernel,
