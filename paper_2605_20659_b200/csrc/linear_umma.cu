@@ -706,52 +706,65 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       mbar_wait_sleep(&accf[ab], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t base = tmem + ab * 256 + (static_cast<uint32_t>(q4 * 32) << 16);
-      uint32_t den_u[16];
-      tmem_ld16(base + 128, den_u);
-      float o[64];
-#pragma unroll
+      // two passes over TMEM (the row's 64 columns are not held in
+      // registers): the sum of squares, then the normalised stores
+      uint32_t den_u[2];
+      tmem_ld2(base + 128, den_u);
+      tmem_wait_ld();
+      const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
+      float ss = 0.f;
+#pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
         tmem_ld32(base + hf * 64 + c * 32, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) o[c * 32 + j] = __uint_as_float(v[j]);
-      }
-      tc_fence_before();
-      mbar_arrive(&acce[ab]);
-      const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
-      float ss = 0.f;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        o[j] *= inv_den;
-        ss = fmaf(o[j], o[j], ss);
+        for (int j = 0; j < 32; ++j) {
+          const float x = __uint_as_float(v[j]) * inv_den;
+          ss = fmaf(x, x, ss);
+        }
       }
       xs[hf][r] = ss;
       asm volatile("bar.sync 1, %0;" ::"n"(kApplyEpi) : "memory");
       ss = xs[0][r] + xs[1][r];
       asm volatile("bar.sync 1, %0;" ::"n"(kApplyEpi) : "memory");  // xs is reused by the next tile
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
-      if (l >= a.L) continue;
+      const bool live = l < a.L;
       const float inv = rsqrtf(ss / static_cast<float>(D) + a.eps);
       const int col0 = hf * 64;
-      if (a.o_lr != nullptr) {
-        float* dst = a.o_lr + (static_cast<int64_t>(bh) * a.L + l) * D + col0;
-#pragma unroll
-        for (int j = 0; j < 64; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-      }
-      __nv_bfloat16* dst = a.y_lr + ((static_cast<int64_t>(b) * a.L + l) * a.H + h) * D + col0;
-#pragma unroll
-      for (int j = 0; j < 64; j += 16) {
-        uint32_t u[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(o[j + 2 * e] * inv * sRms[col0 + j + 2 * e],
-                                                    o[j + 2 * e + 1] * inv * sRms[col0 + j + 2 * e + 1]);
-          u[e] = *reinterpret_cast<uint32_t*>(&h2);
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(base + hf * 64 + c * 32, v);
+        tmem_wait_ld();
+        if (c == 1) {
+          tc_fence_before();
+          mbar_arrive(&acce[ab]);
         }
-        asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + j), "r"(u[0]),
-                     "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
-                     : "memory");
+        if (!live) continue;
+        const int cb = col0 + c * 32;
+        if (a.o_lr != nullptr) {
+          float* dst = a.o_lr + (static_cast<int64_t>(bh) * a.L + l) * D + cb;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) =
+                make_float4(__uint_as_float(v[j]) * inv_den, __uint_as_float(v[j + 1]) * inv_den,
+                            __uint_as_float(v[j + 2]) * inv_den, __uint_as_float(v[j + 3]) * inv_den);
+        }
+        __nv_bfloat16* dst = a.y_lr + ((static_cast<int64_t>(b) * a.L + l) * a.H + h) * D + cb;
+#pragma unroll
+        for (int j = 0; j < 32; j += 16) {
+          uint32_t u[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float x0 = __uint_as_float(v[j + 2 * e]) * inv_den, x1 = __uint_as_float(v[j + 2 * e + 1]) * inv_den;
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0 * inv * sRms[cb + j + 2 * e], x1 * inv * sRms[cb + j + 2 * e + 1]);
+            u[e] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+          asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + j), "r"(u[0]),
+                       "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
+                       : "memory");
+        }
       }
     }
   }
