@@ -236,13 +236,13 @@ struct StateArgs {
 constexpr int SR = 64;                 // tokens per state stage
 constexpr int SHALF = SR * 128;        // 8 KiB: one 64-column half of a stage tile
 constexpr int STILE = 2 * SHALF;       // 16 KiB
-constexpr int SST = 4;                 // state ring depth
-// smem: [SST][phi(K) | V | Txy_v] | T_t,k rows | phi_t sums [T][128] | barriers
+constexpr int SST = 3;                 // state ring depth
+// smem: [SST][K -> phi(K) | V | Txy_v | Txy_k] | T_t,k rows | flush buffer [16 warps][128] | barriers
 struct StateLay {
-  static constexpr int STAGE = 3 * STILE;
+  static constexpr int STAGE = 4 * STILE;
   static constexpr int OFF_TAB = SST * STAGE;
   __host__ __device__ static int off_phi(int T) { return OFF_TAB + ((T * TAB_PITCH + 127) / 128) * 128; }
-  __host__ __device__ static int off_bar(int T) { return off_phi(T) + T * D * 4; }
+  __host__ __device__ static int off_bar(int T) { return off_phi(T) + 16 * D * 4; }
   __host__ __device__ static int bytes(int T) { return off_bar(T) + (4 * SST + 2) * 8 + 16; }
 };
 
@@ -259,8 +259,8 @@ __device__ __forceinline__ uint4 ldg_nc16(const void* p) {
 }
 
 __global__ void __launch_bounds__(kStateThreads, 1)
-    linear_state_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmXY,
-                        const __grid_constant__ StateArgs a) {
+    linear_state_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                        const __grid_constant__ CUtensorMap tmXY, const __grid_constant__ StateArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int bh = blockIdx.y, chunk = blockIdx.x;
@@ -270,16 +270,16 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   const int t1 = min(a.ntiles, t0 + a.tiles_per_cta);
   const int n = max(0, t1 - t0);
   uint8_t* sTab = smem + StateLay::OFF_TAB;
-  float* sPhi = reinterpret_cast<float*>(smem + StateLay::off_phi(T));
+  float* sRed = reinterpret_cast<float*>(smem + StateLay::off_phi(T));  // [16 warps][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + StateLay::off_bar(T));
-  uint64_t* full = bars;                 // [SST] TMA (V, Txy_v) landed
+  uint64_t* full = bars;                 // [SST] TMA (K, V, Txy_v, Txy_k) landed
   uint64_t* ready = bars + SST;          // [SST] phi(K) written
   uint64_t* empty = bars + 2 * SST;      // [SST] MMA done with the stage
   uint64_t* done = bars + 3 * SST;       // MMA -> readout
   uint64_t* tabf = done + 1;             // T_t,k rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tabf + 1);
   const bool pe = a.use_pe != 0;
-  auto stage = [&](int s) { return smem + s * StateLay::STAGE; };  // phi(K) | V | Txy_v
+  auto stage = [&](int s) { return smem + s * StateLay::STAGE; };  // K -> phi(K) | V | Txy_v | Txy_k
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SST; ++i) {
@@ -311,15 +311,19 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       for (int i = 0; i < n; ++i) {
         const int s = i % SST;
         if (i >= SST) mbar_wait_sleep(&empty[s], ((i / SST) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], (pe ? 2 : 1) * STILE);
+        mbar_arrive_expect_tx(&full[s], (pe ? 4 : 2) * STILE);
         const int row = (t0 + i) * SR;
         uint8_t* st = stage(s);
+        tma_load_3d_hint(st, &tmK, &full[s], 0, row, bh, pol);
+        tma_load_3d_hint(st + SHALF, &tmK, &full[s], 64, row, bh, pol);
         tma_load_3d_hint(st + STILE, &tmV, &full[s], 0, row, bh, pol);
         tma_load_3d_hint(st + STILE + SHALF, &tmV, &full[s], 64, row, bh, pol);
         if (pe) {
           const int xy0 = row % HW;
           tma_load_3d_hint(st + 2 * STILE, &tmXY, &full[s], 0, xy0, 2 * h + 1, pol_t);
           tma_load_3d_hint(st + 2 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h + 1, pol_t);
+          tma_load_3d_hint(st + 3 * STILE, &tmXY, &full[s], 0, xy0, 2 * h, pol_t);
+          tma_load_3d_hint(st + 3 * STILE + SHALF, &tmXY, &full[s], 64, xy0, 2 * h, pol_t);
         }
       }
     }
@@ -346,74 +350,74 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       __syncwarp();
     }
   } else {
-    // transform warps: 8 threads per token row, 2 of its 16 chunks each.
-    // Registers hold this stage's K and T_xy,k chunks while the next
-    // stage's loads are in flight.  The phi sums of the row slot accumulate
-    // per t and go into sPhi[t] (shared-memory adds) when the slot's t changes.
-    // chunks c0 and c0 + 8: the 8 threads of a row (one shared-memory phase)
-    // touch 8 distinct 16-byte bank groups of the swizzled tile in each access
-    const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7;
-    for (int e = threadIdx.x; e < T * D; e += kStateXf) sPhi[e] = 0.f;
+    // transform warps: 8 threads per token row (chunks c0 and c0 + 8: the 8
+    // threads of a row, one shared-memory phase, touch 8 distinct 16-byte
+    // bank groups of the swizzled tile).  Registers hold this stage's K and
+    // T_xy,k chunks while the next stage's loads are in flight.  The phi
+    // sums accumulate per t: zacc for the CTA's current t, zst for a token
+    // of a later t; when a stage reaches a new t every thread takes part in
+    // a fixed-order reduction over the 64 row slots (shuffles within a warp,
+    // then the 16 warps in order), written straight to phi_t, so the result
+    // does not depend on timing.
+    const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7, lane = threadIdx.x & 31, xw = threadIdx.x >> 5;
+    float* gphi = a.phi_t + (static_cast<int64_t>(bh) * a.nchunks + chunk) * T * D;
+    for (int e = threadIdx.x; e < T * D; e += kStateXf) gphi[e] = 0.f;
     asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
     if (pe) mbar_wait_sleep(tabf, 0);
     float zacc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) zacc[j] = 0.f;
-    int cur_t = -1;
-    auto flush = [&]() {
-      if (cur_t < 0) return;
-      float* dst = sPhi + cur_t * D + c0 * 8;
+    // the phi sums of t over the slots, into phi_t[t]: v (this thread's 16 columns)
+    auto reduce_to = [&](int tt, const float (&v)[16]) {
+      float w[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        atomicAdd(dst + (j < 8 ? j : 64 + j - 8), zacc[j]);
-        zacc[j] = 0.f;
+        w[j] = v[j];
+        w[j] += __shfl_down_sync(0xffffffffu, w[j], 16);
+        w[j] += __shfl_down_sync(0xffffffffu, w[j], 8);
       }
+      if (lane < 8) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sRed[xw * D + c0 * 8 + (j < 8 ? j : 64 + j - 8)] = w[j];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
+      if (threadIdx.x < D) {
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc += sRed[q * D + threadIdx.x];
+        gphi[tt * D + threadIdx.x] = acc;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
     };
-    const __nv_bfloat16* kbase = a.k + static_cast<int64_t>(bh) * a.L * D + c0 * 8;
-    const __nv_bfloat16* xbase = a.xy + (static_cast<int64_t>(h) * 2) * a.xye * D + c0 * 8;
-    // token of this slot in stage i: l = (t0 + i) SR + r; its t and xy = l mod HW, stepped
+    // token of this slot in stage i: l = (t0 + i) SR + r; its t, stepped
     int64_t l = static_cast<int64_t>(t0) * SR + r;
     int tt = static_cast<int>(l / HW), xy = static_cast<int>(l - static_cast<int64_t>(tt) * HW);
-    auto load = [&](int64_t ll, int xyl, uint4 (&kv)[2], uint4 (&tv)[2]) {
-      if (ll < a.L) {
-        kv[0] = ldg_nc16(kbase + ll * D);
-        kv[1] = ldg_nc16(kbase + ll * D + 64);
-        if (pe) {
-          tv[0] = ldg_nc16(xbase + static_cast<int64_t>(xyl) * D);
-          tv[1] = ldg_nc16(xbase + static_cast<int64_t>(xyl) * D + 64);
-        }
-      }
-    };
-    // two stages ahead in flight: c (this stage), n (next), m (the one after)
-    uint4 kc[2] = {}, tc[2] = {}, kn[2] = {}, tn[2] = {}, km[2] = {}, tm[2] = {};
-    auto step = [&](int64_t& ll, int& xyl, int& tl) {
-      ll += SR;
-      xyl += SR;
-      while (xyl >= HW) {
-        xyl -= HW;
-        ++tl;
-      }
-    };
-    int64_t l1 = l;
-    int xy1 = xy, t1s = tt;
-    step(l1, xy1, t1s);  // stage 1's slot token
-    if (n > 0) load(l, xy, kc, tc);
-    if (n > 1) load(l1, xy1, kn, tn);
+    int cta_t = static_cast<int>((static_cast<int64_t>(t0) * SR) / HW);  // the CTA's current t
     for (int i = 0; i < n; ++i) {
       const int s = i % SST;
       const bool valid = l < a.L;
-      // the slot token two stages ahead
-      int64_t l2 = l1;
-      int xy2 = xy1, t2 = t1s;
-      step(l2, xy2, t2);
-      if (i + 2 < n) load(l2, xy2, km, tm);
-      if (valid && tt != cur_t) {
-        flush();
-        cur_t = tt;
-      }
+      mbar_wait_sleep(&full[s], (i / SST) & 1);
       const uint8_t* trow = pe ? sTab + tt * TAB_PITCH : nullptr;
-      if (i >= SST) mbar_wait_sleep(&empty[s], ((i / SST) - 1) & 1);  // the MMA is done with this A tile
       uint8_t* at = stage(s);
+      uint4 kc[2], tc[2], bc[2];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        kc[cc] = *tile_chunk<SR>(at, r, c0 + 8 * cc);
+        tc[cc] = pe ? *tile_chunk<SR>(at + 3 * STILE, r, c0 + 8 * cc) : make_uint4(0, 0, 0, 0);
+        bc[cc] = pe ? *reinterpret_cast<const uint4*>(trow + (c0 + 8 * cc) * 16) : make_uint4(0, 0, 0, 0);
+      }
+      // phi of element pair e of chunk cc of this slot's token
+      auto phi_at = [&](int cc, int e) {
+        const uint32_t wv = e == 0 ? kc[cc].x : e == 1 ? kc[cc].y : e == 2 ? kc[cc].z : kc[cc].w;
+        float2 f = bf16x2_to_f32x2(wv);
+        if (pe) {
+          const uint32_t av = e == 0 ? tc[cc].x : e == 1 ? tc[cc].y : e == 2 ? tc[cc].z : tc[cc].w;
+          const uint32_t bv = e == 0 ? bc[cc].x : e == 1 ? bc[cc].y : e == 2 ? bc[cc].z : bc[cc].w;
+          f = __fadd2_rn(f, __fadd2_rn(bf16x2_to_f32x2(bv), bf16x2_to_f32x2(av)));
+        }
+        return phi2(f);
+      };
+      const bool mine = valid && tt == cta_t;  // this token's phi belongs to the CTA's current t
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         uint4* p = tile_chunk<SR>(at, r, c0 + 8 * cc);
@@ -421,21 +425,14 @@ __global__ void __launch_bounds__(kStateThreads, 1)
           *p = make_uint4(0, 0, 0, 0);
           continue;
         }
-        const uint32_t w[4] = {kc[cc].x, kc[cc].y, kc[cc].z, kc[cc].w};
-        uint32_t a4[4] = {0u, 0u, 0u, 0u}, b4[4] = {0u, 0u, 0u, 0u};
-        if (pe) {
-          const uint4 b = *reinterpret_cast<const uint4*>(trow + (c0 + 8 * cc) * 16);
-          a4[0] = tc[cc].x; a4[1] = tc[cc].y; a4[2] = tc[cc].z; a4[3] = tc[cc].w;
-          b4[0] = b.x; b4[1] = b.y; b4[2] = b.z; b4[3] = b.w;
-        }
         uint32_t o[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          float2 f = bf16x2_to_f32x2(w[e]);
-          if (pe) f = __fadd2_rn(f, __fadd2_rn(bf16x2_to_f32x2(b4[e]), bf16x2_to_f32x2(a4[e])));
-          f = phi2(f);
-          zacc[cc * 8 + 2 * e] += f.x;
-          zacc[cc * 8 + 2 * e + 1] += f.y;
+          const float2 f = phi_at(cc, e);
+          if (mine) {
+            zacc[cc * 8 + 2 * e] += f.x;
+            zacc[cc * 8 + 2 * e + 1] += f.y;
+          }
           __nv_bfloat162 h2 = __floats2bfloat162_rn(f.x, f.y);
           o[e] = *reinterpret_cast<uint32_t*>(&h2);
         }
@@ -443,24 +440,39 @@ __global__ void __launch_bounds__(kStateThreads, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(&ready[s]);
-      l = l1;
-      xy = xy1;
-      tt = t1s;
-      l1 = l2;
-      xy1 = xy2;
-      t1s = t2;
+      // did this stage reach past the CTA's t?  (uniform: the stage's last valid token)
+      const int64_t last = min(static_cast<int64_t>(t0 + i + 1) * SR, a.L) - 1;
+      const int t_last = static_cast<int>(last / HW);
+      if (t_last != cta_t) {
+        // rare: close the current t, then each later t of this stage (phi of
+        // the tokens of that t recomputed from the registers)
+        for (int tq = cta_t; tq <= t_last; ++tq) {
+          if (tq > cta_t) {
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        kc[cc] = kn[cc];
-        tc[cc] = tn[cc];
-        kn[cc] = km[cc];
-        tn[cc] = tm[cc];
+            for (int j = 0; j < 16; ++j) zacc[j] = 0.f;
+            if (valid && tt == tq) {
+#pragma unroll
+              for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = phi_at(cc, e);
+                  zacc[cc * 8 + 2 * e] = f.x;
+                  zacc[cc * 8 + 2 * e + 1] = f.y;
+                }
+            }
+          }
+          if (tq < t_last) reduce_to(tq, zacc);
+        }
+        cta_t = t_last;
+      }
+      l += SR;
+      xy += SR;
+      while (xy >= HW) {
+        xy -= HW;
+        ++tt;
       }
     }
-    flush();
-    asm volatile("bar.sync 1, %0;" ::"n"(kStateXf) : "memory");
-    float* gphi = a.phi_t + (static_cast<int64_t>(bh) * a.nchunks + chunk) * T * D;
-    for (int e = threadIdx.x; e < T * D; e += kStateXf) gphi[e] = sPhi[e];
+    if (n > 0) reduce_to(cta_t, zacc);
   }
   if (warp < 4) {  // warps 0-3 read TMEM lanes 0-127 (the rows of S) out: S_v + S_xy
     const int r = threadIdx.x;
@@ -587,7 +599,7 @@ struct ApplyLay {
 };
 
 constexpr int kApplyXf = 256;   // transform threads: 2 per token row, 8 chunks each (warps 0-7)
-constexpr int kApplyEpi = 256;  // epilogue threads (warps 8-15): lane quarter warp % 4, column half (warp - 8) / 4
+constexpr int kApplyEpi = 256;  // epilogue threads (warps 8-15): lane quarter warp % 4, tile parity (warp - 8) / 4
 constexpr int kApplyTma = (kApplyXf + kApplyEpi) / 32, kApplyMma = kApplyTma + 1;
 constexpr int kApplyThreads = kApplyXf + kApplyEpi + 64;
 
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&accf[i], 1);
-      mbar_init(&acce[i], kApplyEpi);
+      mbar_init(&acce[i], kApplyEpi / 2);
     }
     mbar_init(init, 1);
     fence_mbar_init();
@@ -698,25 +710,27 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       mbar_arrive(&ready[s]);
     }
   } else {
-    // epilogue: row r = TMEM lane (warp % 4) * 32 + lane; columns [64 hf, 64 hf + 64)
-    const int q4 = warp & 3, hf = (warp - kApplyXf / 32) >> 2;
+    // epilogue: row r = TMEM lane (warp % 4) * 32 + lane; warps 8-11 take
+    // the even tiles (accumulator 0), warps 12-15 the odd ones (accumulator
+    // 1), each whole rows of 128 columns: no exchange between warps
+    const int q4 = warp & 3, par = (warp - kApplyXf / 32) >> 2;
     const int r = q4 * 32 + (threadIdx.x & 31);
-    for (int i = 0; i < n; ++i) {
-      const int ab = i & 1;
+    for (int i = par; i < n; i += 2) {
+      const int ab = par;
       mbar_wait_sleep(&accf[ab], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t base = tmem + ab * 256 + (static_cast<uint32_t>(q4 * 32) << 16);
-      // two passes over TMEM (the row's 64 columns are not held in
-      // registers): the sum of squares, then the normalised stores
+      // two passes over TMEM (the row's columns are not held in registers):
+      // the sum of squares, then the normalised stores
       uint32_t den_u[2];
       tmem_ld2(base + 128, den_u);
       tmem_wait_ld();
       const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
       float ss = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
-        tmem_ld32(base + hf * 64 + c * 32, v);
+        tmem_ld32(base + c * 32, v);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -724,25 +738,20 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
           ss = fmaf(x, x, ss);
         }
       }
-      xs[hf][r] = ss;
-      asm volatile("bar.sync 1, %0;" ::"n"(kApplyEpi) : "memory");
-      ss = xs[0][r] + xs[1][r];
-      asm volatile("bar.sync 1, %0;" ::"n"(kApplyEpi) : "memory");  // xs is reused by the next tile
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
       const bool live = l < a.L;
       const float inv = rsqrtf(ss / static_cast<float>(D) + a.eps);
-      const int col0 = hf * 64;
 #pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
-        tmem_ld32(base + hf * 64 + c * 32, v);
+        tmem_ld32(base + c * 32, v);
         tmem_wait_ld();
-        if (c == 1) {
+        if (c == 3) {
           tc_fence_before();
           mbar_arrive(&acce[ab]);
         }
         if (!live) continue;
-        const int cb = col0 + c * 32;
+        const int cb = c * 32;
         if (a.o_lr != nullptr) {
           float* dst = a.o_lr + (static_cast<int64_t>(bh) * a.L + l) * D + cb;
 #pragma unroll
@@ -1059,8 +1068,9 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   const float* G = reinterpret_cast<const float*>(tab + ly.g);
   lnu::Grid3 g{t->grid_t, t->grid_h, t->grid_w};
 
-  CUtensorMap mq, mv, mxy;
-  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR) ||
+  CUtensorMap mq, mk, mv, mxy;
+  if (!lnu::make_map(&mq, q_lin, BH, s->L) || !lnu::make_map(&mk, k_lin, BH, s->L, lnu::SR) ||
+      !lnu::make_map(&mv, v_lin, BH, s->L, lnu::SR) ||
       !lnu::make_map(&mxy, tab + ly.xy, 2 * s->H, ly.xye, lnu::SR))
     return ROPESLR_ERR_LAUNCH;
   // state
@@ -1083,7 +1093,7 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   const int ssm = lnu::StateLay::bytes(t->grid_t);
   if (cudaFuncSetAttribute(lnu::linear_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm) != cudaSuccess)
     return ROPESLR_ERR_LAUNCH;
-  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mv, mxy, sa);
+  lnu::linear_state_kernel<<<dim3(nch, static_cast<unsigned>(BH)), lnu::kStateThreads, ssm, st>>>(mk, mv, mxy, sa);
   if (int e = launch_status()) return e;
   const int rsm = t->grid_t * (lnu::D + 8) * 8;
   if (rsm > 48 * 1024 && cudaFuncSetAttribute(lnu::linear_reduce_image_kernel,
