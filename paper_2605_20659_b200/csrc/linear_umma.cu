@@ -211,24 +211,17 @@ struct StateArgs {
   int ntiles;           // ceil(L / SR)
   int tiles_per_cta;
   int nchunks;
-  const __nv_bfloat16* k;   // [BH, L, 128] (x W_k, no PE)
   const uint8_t* tables;    // [H][3][nrows][TAB_PITCH] bf16 (q, k, v): the rows of t read here
-  const __nv_bfloat16* xy;  // [H][2][xye][128] bf16: T_x + T_y of k (0) and v (1)
-  int xye;
   float* partial;       // [BH][nchunks][128][NPART]: phi(K)^T (V + T_xy,v) per chunk
   float* phi_t;         // [BH][nchunks][T][128]: sum of phi(k) over the chunk's tokens of each t
 };
 
-// The state pass in 64-token stages.  K and its (x, y) table rows come
-// straight into the transform threads' registers (16-byte loads, the next
-// stage's in flight while the current one is transformed), and only
-// phi(k + T_k) is written to shared memory, as the MMA's A tile: the
-// tile never makes the TMA -> shared -> registers round trip, which with
-// the MMA's own reads made shared memory, not HBM, the binding rate.  V and
-// the stage's 64 rows of the (x, y) table of v (T_xy[x W + y] = T_x[x] +
-// T_y[y], rows repeated past H W so a stage never wraps) come by TMA and
-// sit side by side as one N = 256 B operand: S_v | S_xy = phi(K)^T [V |
-// T_xy,v] in one MMA per k-step.  The t part of the PE: phi(k + T_k) takes
+// The state pass in 64-token stages, three deep.  TMA brings K, V and the
+// stage's 64 rows of the (x, y) tables of k and v (T_xy[x W + y] = T_x[x] +
+// T_y[y], rows repeated past H W so a stage never wraps); the transform
+// warps turn K into phi(k + T_k) in place (the MMA's A tile), and V and
+// T_xy,v sit side by side as one N = 256 B operand: S_v | S_xy = phi(K)^T
+// [V | T_xy,v] in one MMA per k-step.  The t part of the PE: phi(k + T_k) takes
 // T_t,k[t] from shared memory, and sum_l phi(k_l) T_t,v[t(l)] = sum_t (sum
 // over the tokens of t of phi(k)) T_t,v[t]: the per-t sums go out with the
 // chunk (phi_t) and the reduce kernel adds their products with T_t,v
@@ -249,14 +242,6 @@ struct StateLay {
 constexpr int kStateXf = 512;                 // transform threads: 8 per token row, 2 chunks each
 constexpr int kStateThreads = kStateXf + 64;  // + warp 16 TMA, warp 17 MMA + TMEM
 constexpr int kStateTma = kStateXf / 32, kStateMma = kStateTma + 1;
-
-__device__ __forceinline__ uint4 ldg_nc16(const void* p) {
-  uint4 u;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-               : "l"(p));
-  return u;
-}
 
 __global__ void __launch_bounds__(kStateThreads, 1)
     linear_state_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -352,13 +337,12 @@ __global__ void __launch_bounds__(kStateThreads, 1)
   } else {
     // transform warps: 8 threads per token row (chunks c0 and c0 + 8: the 8
     // threads of a row, one shared-memory phase, touch 8 distinct 16-byte
-    // bank groups of the swizzled tile).  Registers hold this stage's K and
-    // T_xy,k chunks while the next stage's loads are in flight.  The phi
-    // sums accumulate per t: zacc for the CTA's current t, zst for a token
-    // of a later t; when a stage reaches a new t every thread takes part in
-    // a fixed-order reduction over the 64 row slots (shuffles within a warp,
-    // then the 16 warps in order), written straight to phi_t, so the result
-    // does not depend on timing.
+    // bank groups of the swizzled tile).  The phi sums accumulate per thread
+    // for the CTA's current t; when a stage reaches a new t every thread
+    // takes part in a fixed-order reduction over the 64 row slots (shuffles
+    // within a warp, then the 16 warps in order), written straight to phi_t,
+    // so the result does not depend on timing; the phi of a token of a later
+    // t in that stage is recomputed from its registers for its own t.
     const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7, lane = threadIdx.x & 31, xw = threadIdx.x >> 5;
     float* gphi = a.phi_t + (static_cast<int64_t>(bh) * a.nchunks + chunk) * T * D;
     for (int e = threadIdx.x; e < T * D; e += kStateXf) gphi[e] = 0.f;
@@ -1085,9 +1069,6 @@ extern "C" int ropeslr_linear_branch_pe(const ropeslr_shape* s, const ropeslr_to
   sa.tiles_per_cta = tpc * (lnu::M / lnu::SR);
   sa.nchunks = nch;
   sa.tables = tab;
-  sa.k = static_cast<const __nv_bfloat16*>(k_lin);
-  sa.xy = reinterpret_cast<const __nv_bfloat16*>(tab + ly.xy);
-  sa.xye = ly.xye;
   sa.partial = partial;
   sa.phi_t = phi_t;
   const int ssm = lnu::StateLay::bytes(t->grid_t);
