@@ -63,8 +63,8 @@ def test_stage1_training_reduces_loss():
     assert res.final_loss < res.initial_loss
 
 
-@pytest.mark.parametrize("d,split,r", [(128, (16, 56, 56), 64), (64, (16, 24, 24), 16)])
-def test_stage1_captured_step_equals_eager(d, split, r):
+@pytest.mark.parametrize("d,split,r,nsamp", [(128, (16, 56, 56), 64, 1), (64, (16, 24, 24), 16, 2)])
+def test_stage1_captured_step_equals_eager(d, split, r, nsamp):
     """The CUDA-graph step (training.Stage1Step: loss, gradients and the
     device-side update) against the eager loop of the same kernels: the
     same losses and bit-identical parameters after three steps; a diverging
@@ -77,9 +77,10 @@ def test_stage1_captured_step_equals_eager(d, split, r):
     grid_s, H = (2, 6, 20), 2
     q, k, v, x, params, pe, grid = G.make_full_inputs(grid_s, H, d, split, r, seed=9, dtype=torch.bfloat16)
     gen = torch.Generator(device="cuda").manual_seed(10)
-    target = torch.randn((1, grid.size, H * d), generator=gen, device="cuda").to(torch.bfloat16)
+    samples = [T.Stage1Sample(q, k, v, x, torch.randn((1, grid.size, H * d), generator=gen, device="cuda").to(
+        torch.bfloat16)) for _ in range(nsamp)]
     st = P.ForwardSettings(P.SparseSettings(block=64, topk=2))
-    prep = T.prepare([T.Stage1Sample(q, k, v, x, target)], grid, params, st, pe)
+    prep = T.prepare(samples, grid, params, st, pe)
     pe_hm = T.pe_head_major(pe, grid, H, d)
     lr = 0.05
     p_eager = copy.deepcopy(params)
