@@ -54,3 +54,21 @@ for name, (qq, kk) in {"cfg3": (q, k)}.items():
           "steps mean", steps.float().mean().item(), "max", steps.max().item())
     qn = pooled[0].norm(dim=-1)
     print("q norm mean", qn.mean().item(), "approx std", approx.float().std().item())
+
+# skewed (structured) block scores, as real attention has (test_gpu_parity._skew_blocks)
+from test_gpu_parity import _skew_blocks
+for strength in (4.0, 8.0):
+    qs, ks = _skew_blocks(q, k, 128, strength=strength)
+    for scr in (1, 0):
+        with P._lib.option("screen", scr):
+            ms = timed(lambda: P.select_blocks(qs, ks, sp, want_mask=False))
+            res[scr] = P.select_blocks(qs, ks, sp, want_mask=False)
+        torch.cuda.synchronize()
+        print(f"skew {strength}: screen={scr} select_blocks {ms:.3f} ms", flush=True)
+    print("identical:", all(torch.equal(getattr(res[0], f), getattr(res[1], f)) for f in ("idx", "cnt", "attended")))
+    pooled, approx, full = T._raw_screen(qs, ks, sp.topk, 128)
+    diag = T._raw_screen.diag
+    band, steps = (diag & 0xffff), (diag >> 16)
+    ok = diag >= 0
+    print("skew", strength, "deferred rows", full, "band mean", band[ok].float().mean().item(), "max", band[ok].max().item(),
+          "steps mean", steps[ok].float().mean().item())
