@@ -503,7 +503,8 @@ def _cached_tables(tag, deps, nbytes, device, build) -> torch.Tensor:
     """Parameter-only device tables, rebuilt only when a dependency changes.
     The key is each dependency's storage address and version counter; the
     entry holds the dependencies themselves, so a cached address cannot be
-    freed and reused by another tensor while the entry lives (8 entries)."""
+    freed and reused by another tensor while the entry lives (64 entries: a
+    30-block DiT keeps one per block and tensor kind)."""
     key = (tag, tuple((t.data_ptr(), t._version) for t in deps))
     hit = _TABLES.get(key)
     if hit is not None:
@@ -512,7 +513,7 @@ def _cached_tables(tag, deps, nbytes, device, build) -> torch.Tensor:
     tab = _workspace(nbytes, device)
     build(tab)
     _TABLES[key] = (tab, list(deps))
-    while len(_TABLES) > 8:
+    while len(_TABLES) > 64:
         _TABLES.popitem(last=False)
     return tab
 

@@ -25,7 +25,7 @@ tot = sum(r[1] for r in rows)
 print(f"total device time {tot:.1f} ms")
 ours = 0.0
 for k, ms, n in rows[:30]:
-    mine = any(s in k for s in ("sparse_attn", "pool", "block_scores", "select_", "lowrank", "gate_sum", "rope_pool", "rope_tables", "schedule_units"))
+    mine = any(s in k for s in ("sparse_attn", "pool", "block_scores", "select_", "screen_", "lowrank", "gate_sum", "rope_pool", "rope_tables", "schedule_units", "dit_", "copy_rows", "ropeslr"))
     ours += ms if mine else 0.0
     print(f"{ms:8.2f} ms {n:5d}x {'*' if mine else ' '} {k[:90]}")
 print(f"ours (top 30) {ours:.1f} ms")
