@@ -168,3 +168,20 @@ def test_screen_offsets_abi():
     shp64 = _lib.Shape(1, 2, 4096, 64, 64, 1)
     assert f(ctypes.byref(shp64), 8, ctypes.byref(a), ctypes.byref(s), None) != 0
     assert f(ctypes.byref(shp), 0, ctypes.byref(a), ctypes.byref(s), None) != 0
+
+
+def test_screen_degenerate_rows():
+    """All-zero Q/K (every score ties: every row deferred, ties to the lower
+    blocks) and a NaN in K (those rows deferred, the same keys as the float64
+    path) select exactly what the float64 path selects."""
+    nb, block = 200, 32
+    q = torch.zeros((1, 2, nb * block, 128), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros_like(q)
+    _both(q, k, 20, block)
+    _, _, full = _raw_screen(q, k, 20, block)
+    assert full == 2 * nb
+    g = torch.Generator(device="cuda").manual_seed(21)
+    q = torch.randn((1, 2, nb * block, 128), generator=g, device="cuda").to(torch.bfloat16)
+    k = torch.randn((1, 2, nb * block, 128), generator=g, device="cuda").to(torch.bfloat16)
+    k[0, 1, 5 * block + 3, 7] = float("nan")
+    _both(q, k, 20, block)
