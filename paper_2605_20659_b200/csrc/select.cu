@@ -715,15 +715,18 @@ __global__ void __launch_bounds__(256) select_topk_warp_kernel(const double* __r
 //   screen_image_kernel   pooled float64 rows -> bf16 hi/lo splits (x = hi
 //                         + lo + r, |r| <= 2^-16 |x|), written as the
 //                         128B-swizzled K-major tiles the tensor cores read,
-//                         plus an upward-rounded float norm per row
+//                         plus an upward-rounded float norm per row (on the
+//                         pooling path pool_blocks_bulk_kernel writes them)
 //   screen_scores_kernel  s~ = (Qhi Khi^T + Qhi Klo^T + Qlo Khi^T) / sqrt(d)
 //                         on tcgen05 (float32 accumulation in TMEM)
 //   screen_select_kernel  per row: [lo, hi] around the k-th best s~, t_k,
-//                         by bisection on the value (hi - lo <= E); with
-//                         |s~ - s| <= E for every block of the row, blocks
-//                         with s~ > hi + 2E are in, blocks with s~ < lo - 2E
-//                         are out, and the few in between get float64 scores
-//                         and the exact stable order.
+//                         by counting probes (normal quantile, a Newton step,
+//                         interpolation) until the count is exact or hi - lo
+//                         <= E; with |s~ - s| <= E for every block of the
+//                         row, blocks with s~ > hi + 2E are in, blocks with
+//                         s~ < lo - 2E are out, and the few in between get
+//                         float64 scores and the exact stable order
+//   screen_exact_kernel   the rows the band cannot decide, wholly in float64.
 // E = kScreenBound |q_i| max_j |k_j| / sqrt(d).  Derivation (DESIGN.md,
 // K1): the dropped split terms are <= 3.1 * 2^-16 sum |q||k|; the float32
 // accumulation of 3 d = 384 exact bf16 products, allowing each addition a
