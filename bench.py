@@ -363,13 +363,34 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---- K1 (selection) and K3 (compensator + gate) alone, CUDA events on the
     # launching stream: the HBM roofline of the two bandwidth-bound stages
     def stage_ms(fn, n=20):
+        """GPU time of one stage: n calls captured in a CUDA graph and
+        replayed (the Python wrapper's allocations and ctypes calls are not
+        in the timed region, so a slow host cannot inflate a ~0.3 ms stage);
+        eager calls if the stage cannot be captured."""
         for _ in range(2):
             fn()
+        torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(n):
-            fn()
-        b.record(stream)
+        try:
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                fn()  # warm the allocator on the capture stream
+            stream.wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(n):
+                    fn()
+            graph.replay()
+            torch.cuda.synchronize()
+            a.record(stream)
+            graph.replay()
+            b.record(stream)
+        except Exception:  # not capturable: eager launches
+            a.record(stream)
+            for _ in range(n):
+                fn()
+            b.record(stream)
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n
 
@@ -463,7 +484,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "frac_of_hbm": 4 * q.numel() * q.element_size() / (rope_ms * 1e-3) / 1e9 / load_peaks().get("hbm_gbs", 6650.0),
             "note": "rank 0: read un-rotated Q,K + write rotated Q,K (pooled means ride along)"},
         "stages": {
-            "note": "rank 0, each stage alone (20 launches after 2 warm-up), CUDA events; algorithmic bytes; "
+            "note": "rank 0, each stage alone (20 calls captured in a CUDA graph after 2 warm-up, one replay timed with CUDA events: kernel time without the Python wrapper's host overhead); algorithmic bytes; "
                     "peak = measured HBM copy rate",
             "K1_select": {"ms": k1_ms, "bytes": 2 * q.numel() * q.element_size(),
                           "GB_per_s": 2 * q.numel() * q.element_size() / (k1_ms * 1e-3) / 1e9,
