@@ -402,6 +402,9 @@ int ropeslr_copy_rows(const ropeslr_row_segment* segs, int32_t nseg, int64_t tot
  *   gated_residual: x += bf16(y * gate)                      (gate [D] fp32) */
 int ropeslr_dit_ln_modulate(const void* x, const float* shift, const float* scale, float eps, int64_t N, int32_t D,
                             void* y, void* stream);
+/* bf16(LayerNorm(x) * weight + bias) (an affine LayerNorm; float32 weight / bias [D]). */
+int ropeslr_dit_ln_affine(const void* x, const float* weight, const float* bias, float eps, int64_t N, int32_t D,
+                          void* y, void* stream);
 int ropeslr_dit_rms_heads(const void* x, const void* weight, float eps, int64_t N, int32_t D, int32_t H,
                           int32_t head_major, void* out, void* stream);
 int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_t N, int32_t D, void* stream);

@@ -32,7 +32,7 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* row, int D, int la
 template <int J>
 __global__ void ln_modulate_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ shift,
                                    const float* __restrict__ scale, float eps, int64_t N, int D,
-                                   __nv_bfloat16* __restrict__ y) {
+                                   __nv_bfloat16* __restrict__ y, int one_plus) {
   const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= N) return;
@@ -61,7 +61,7 @@ __global__ void ln_modulate_kernel(const __nv_bfloat16* __restrict__ x, const fl
     load8(scale + c, sc);
     load8(shift + c, sh);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = fmaf((v[8 * j + e] - mean) * rstd, 1.f + sc[e], sh[e]);
+    for (int e = 0; e < 8; ++e) o[e] = fmaf((v[8 * j + e] - mean) * rstd, one_plus ? 1.f + sc[e] : sc[e], sh[e]);
     store8(y + r * D + c, o);
   }
 }
@@ -152,7 +152,18 @@ extern "C" int ropeslr_dit_ln_modulate(const void* x, const float* shift, const 
   if (!aligned16(x) || !aligned16(y)) return ROPESLR_ERR_ALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ROPESLR_DIT_DISPATCH(ln_modulate_kernel, static_cast<const __nv_bfloat16*>(x), shift, scale, eps, N, D,
-                       static_cast<__nv_bfloat16*>(y));
+                       static_cast<__nv_bfloat16*>(y), 1);
+  return launch_status();
+}
+
+extern "C" int ropeslr_dit_ln_affine(const void* x, const float* weight, const float* bias, float eps, int64_t N,
+                                     int32_t D, void* y, void* stream) {
+  if (!x || !weight || !bias || !y) return ROPESLR_ERR_NULL;
+  if (!dit::row_ok(N, D)) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(y)) return ROPESLR_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ROPESLR_DIT_DISPATCH(ln_modulate_kernel, static_cast<const __nv_bfloat16*>(x), bias, weight, eps, N, D,
+                       static_cast<__nv_bfloat16*>(y), 0);
   return launch_status();
 }
 

@@ -90,6 +90,19 @@ def ln_modulate(x: torch.Tensor, shift: torch.Tensor, scale: torch.Tensor, eps: 
     return y
 
 
+def ln_affine(x: torch.Tensor, ln: nn.LayerNorm) -> torch.Tensor:
+    """bf16(LayerNorm(x) * weight + bias) for an affine nn.LayerNorm; x
+    [B, L, D] bf16."""
+    D = x.shape[-1]
+    x = x.contiguous()
+    w = ln.weight.detach().float().contiguous()
+    b = ln.bias.detach().float().contiguous()
+    y = torch.empty_like(x)
+    _lib.call("ropeslr_dit_ln_affine", x.data_ptr(), w.data_ptr(), b.data_ptr(), float(ln.eps), x.numel() // D, D,
+              y.data_ptr(), _stream(x))
+    return y
+
+
 def rms_heads(x: torch.Tensor, weight: Optional[torch.Tensor], eps: float, H: int, head_major: bool = True):
     """RMSNorm over the last dim (weight None: none) of x [1, L, D] bf16; out
     [1, H, L, D/H] when head_major, else [1, L, H, D/H]."""
@@ -201,7 +214,7 @@ class WanBlock(nn.Module):
             a = forward(q, k, v, y, grid, params, settings, pe, rope=rope)
         gated_residual_(x, self.o(a), g_a)
         # cross-attention to the text tokens
-        c = self.norm3(x)
+        c = ln_affine(x, self.norm3)
         cq = rms_heads(self.cq(c), self.norm_cq.weight, self.norm_cq.eps, H)
         ck = self.norm_ck(self.ck(ctx)).view(B, -1, H, d).transpose(1, 2)
         cv = self.cv(ctx).view(B, -1, H, d).transpose(1, 2)

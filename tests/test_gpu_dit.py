@@ -132,6 +132,13 @@ def test_fused_ops_unit():
     want = (F.layer_norm(x.float(), (D,), eps=1e-6) * (1 + sc) + sh).to(torch.bfloat16)
     got = dit.ln_modulate(x, sh, sc, 1e-6)
     assert (got.float() - want.float()).abs().max().item() <= 2e-2
+    ln = torch.nn.LayerNorm(D, eps=1e-6, elementwise_affine=True).cuda().to(torch.bfloat16)
+    with torch.no_grad():
+        ln.weight.copy_(1 + 0.1 * torch.randn(D, generator=g, device="cuda"))
+        ln.bias.copy_(0.1 * torch.randn(D, generator=g, device="cuda"))
+        want_ln = ln(x)
+    got_ln = dit.ln_affine(x, ln)
+    assert (got_ln.float() - want_ln.float()).abs().max().item() <= 3e-2
     w = (1 + 0.1 * torch.randn(D, generator=g, device="cuda")).to(torch.bfloat16)
     xf = x.float()
     rms = ((xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6)).to(torch.bfloat16) * w)
