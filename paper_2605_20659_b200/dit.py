@@ -159,9 +159,18 @@ class WanBlock(nn.Module):
         self.rms_lowrank = nn.Parameter(torch.ones(d))
 
     def ropeslr_params(self) -> MechanismParams:
-        f = lambda t: t.detach().float().contiguous()  # noqa: E731
-        return MechanismParams(w_a=f(self.w_a), w_b=f(self.w_b), alpha=f(self.alpha), w_g=f(self.w_g), b_g=-2.0,
-                               rms_sparse=f(self.rms_sparse), rms_lowrank=f(self.rms_lowrank))
+        """The layer's float32 RoPeSLR parameter set, converted once and kept
+        while the parameters are unchanged (storage and version counters), so
+        the op's parameter-only tables (mechanism.lowrank_tables) are built
+        once per layer rather than on every step."""
+        src = (self.w_a, self.w_b, self.alpha, self.w_g, self.rms_sparse, self.rms_lowrank)
+        key = tuple((p.data_ptr(), p._version, p.dtype) for p in src)
+        if getattr(self, "_mp_key", None) != key:
+            f = lambda t: t.detach().float().contiguous()  # noqa: E731
+            self._mp = MechanismParams(w_a=f(self.w_a), w_b=f(self.w_b), alpha=f(self.alpha), w_g=f(self.w_g),
+                                       b_g=-2.0, rms_sparse=f(self.rms_sparse), rms_lowrank=f(self.rms_lowrank))
+            self._mp_key = key
+        return self._mp
 
     def forward(self, x, e, ctx, grid: GridShape, pe: PETables, settings: ForwardSettings, rope: RopeConfig,
                 group=None):

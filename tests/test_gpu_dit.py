@@ -39,6 +39,32 @@ def test_small_dit_forward_deterministic():
     assert torch.equal(y1, y2)
 
 
+def test_layer_tables_built_once():
+    """Each layer's parameter-only tables are built on the first step and
+    reused after (dit.DiTBlock.ropeslr_params keeps the float32 copies);
+    an in-place parameter update rebuilds them."""
+    import paper_2605_20659_b200.mechanism as M
+    from paper_2605_20659_b200.dit import make_model
+
+    cfg = _small_cfg()
+    model = make_model(cfg)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    latent = torch.randn((1, 16, 3, 8, 16), generator=g, device="cuda").to(torch.bfloat16)
+    text = torch.randn((1, cfg.text_len, cfg.text_dim), generator=g, device="cuda").to(torch.bfloat16)
+    t = torch.tensor([500.0], device="cuda")
+    M._TABLES.clear()
+    with torch.no_grad():
+        y1 = model(latent, t, text)
+        keys = list(M._TABLES.keys())
+        y2 = model(latent, t, text)
+        assert list(M._TABLES.keys()) == keys and len(keys) == cfg.blocks
+        assert torch.equal(y1, y2)
+        model.blocks[0].w_a.mul_(1.5)
+        y3 = model(latent, t, text)
+    assert len(M._TABLES) == cfg.blocks + 1
+    assert not torch.equal(y1, y3)
+
+
 def test_ulysses_world1_equals_direct_forward():
     import gpu_helpers as G
     import paper_2605_20659_b200 as P
