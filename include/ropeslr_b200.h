@@ -408,6 +408,12 @@ int ropeslr_dit_ln_affine(const void* x, const float* weight, const float* bias,
 int ropeslr_dit_rms_heads(const void* x, const void* weight, float eps, int64_t N, int32_t D, int32_t H,
                           int32_t head_major, void* out, void* stream);
 int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_t N, int32_t D, void* stream);
+/* out = x + bf16(y * gate), out of place (out may alias x). */
+int ropeslr_dit_gated_add(const void* x, const void* y, const float* gate, int64_t N, int32_t D, void* out,
+                          void* stream);
+/* y [B, L, H, dh] = x [B, H, L, dh] (bf16, dh % 8 == 0): the attention
+ * output back to token-major rows for the output projection. */
+int ropeslr_dit_heads_to_tokens(const void* x, int64_t B, int32_t H, int64_t L, int32_t dh, void* y, void* stream);
 
 /* ------------------------- Stage-I training (training.py; mechanism.py:426-488, 519-614)
  * The per-row chains of the fused forward / backward around the float32

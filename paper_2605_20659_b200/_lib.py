@@ -96,6 +96,8 @@ _SIGNATURES = {
     "ropeslr_copy_rows": (c_i32, [c_vp, c_i32, c_i64, c_vp]),
     "ropeslr_dit_ln_modulate": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_ln_affine": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
+    "ropeslr_dit_gated_add": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "ropeslr_dit_heads_to_tokens": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_rms_heads": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "ropeslr_dit_gated_residual": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),
     "ropeslr_stage1_supported": (c_i32, [c_i64]),

@@ -3,6 +3,8 @@
 // PyTorch would otherwise run as 5-8 separate elementwise kernels each, and
 // the head-major re-layout the op's Q/K/V need.  All are HBM-bound row
 // kernels: one warp per token row of D = H * d bf16 values, fp32 math.
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -105,8 +107,8 @@ __global__ void rms_heads_kernel(const __nv_bfloat16* __restrict__ x, const __nv
 
 // x = x + bf16(y * gate), torch's `x + (y.float() * g).to(bf16)`.
 template <int J>
-__global__ void gated_residual_kernel(__nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ y,
-                                      const float* __restrict__ gate, int64_t N, int D) {
+__global__ void gated_residual_kernel(const __nv_bfloat16* x, const __nv_bfloat16* __restrict__ y,
+                                      const float* __restrict__ gate, int64_t N, int D, __nv_bfloat16* out) {
   const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= N) return;
@@ -120,7 +122,22 @@ __global__ void gated_residual_kernel(__nv_bfloat16* __restrict__ x, const __nv_
     load8(gate + c, gv);
 #pragma unroll
     for (int e = 0; e < 8; ++e) xv[e] = xv[e] + __bfloat162float(__float2bfloat16_rn(yv[e] * gv[e]));
-    store8(x + r * D + c, xv);
+    store8(out + r * D + c, xv);
+  }
+}
+
+// [B, H, L, dh] -> [B, L, H, dh], 16-byte chunks: reads in source order
+// (coalesced), writes whole dh-element rows (full 32-byte sectors).
+__global__ void heads_to_tokens_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t n, int H,
+                                       int64_t L, int cpr) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int j = static_cast<int>(i % cpr);
+    const int64_t row = i / cpr;  // (b, h, l)
+    const int64_t l = row % L;
+    const int64_t bh = row / L;
+    const int64_t h = bh % H, b = bh / H;
+    y[((b * L + l) * H + h) * cpr + j] = __ldcs(x + i);
   }
 }
 
@@ -187,6 +204,32 @@ extern "C" int ropeslr_dit_gated_residual(void* x, const void* y, const float* g
   if (!aligned16(x) || !aligned16(y)) return ROPESLR_ERR_ALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ROPESLR_DIT_DISPATCH(gated_residual_kernel, static_cast<__nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(y),
-                       gate, N, D);
+                       gate, N, D, static_cast<__nv_bfloat16*>(x));
+  return launch_status();
+}
+
+extern "C" int ropeslr_dit_gated_add(const void* x, const void* y, const float* gate, int64_t N, int32_t D,
+                                     void* out, void* stream) {
+  if (!x || !y || !gate || !out) return ROPESLR_ERR_NULL;
+  if (!dit::row_ok(N, D)) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(out)) return ROPESLR_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ROPESLR_DIT_DISPATCH(gated_residual_kernel, static_cast<const __nv_bfloat16*>(x),
+                       static_cast<const __nv_bfloat16*>(y), gate, N, D, static_cast<__nv_bfloat16*>(out));
+  return launch_status();
+}
+
+extern "C" int ropeslr_dit_heads_to_tokens(const void* x, int64_t B, int32_t H, int64_t L, int32_t dh, void* y,
+                                           void* stream) {
+  if (!x || !y) return ROPESLR_ERR_NULL;
+  if (B < 1 || H < 1 || L < 1 || dh < 8 || dh % 8) return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(y)) return ROPESLR_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cpr = dh / 8;
+  const int64_t n = B * H * L * cpr;
+  const int64_t want = ceil_div(n, 256 * 4);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(num_sms()) * 16));
+  dit::heads_to_tokens_kernel<<<grid, 256, 0, st>>>(static_cast<const uint4*>(x), static_cast<uint4*>(y), n, H, L,
+                                                    cpr);
   return launch_status();
 }

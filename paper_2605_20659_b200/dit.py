@@ -128,6 +128,27 @@ def gated_residual_(x: torch.Tensor, y: torch.Tensor, gate: torch.Tensor) -> tor
     return x
 
 
+def gated_add(x: torch.Tensor, y: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
+    """x + bf16(y * gate) into a new tensor; x, y [B, L, D] bf16, gate -> [D] float32."""
+    D = x.shape[-1]
+    x = x.contiguous()
+    y = y.contiguous()
+    g = gate.reshape(-1)[-D:].float().contiguous()
+    out = torch.empty_like(x)
+    _lib.call("ropeslr_dit_gated_add", x.data_ptr(), y.data_ptr(), g.data_ptr(), x.numel() // D, D, out.data_ptr(),
+              _stream(x))
+    return out
+
+
+def heads_to_tokens(a: torch.Tensor) -> torch.Tensor:
+    """[B, H, L, dh] bf16 (contiguous) -> [B, L, H * dh]."""
+    B, H, L, dh = a.shape
+    a = a.contiguous()
+    y = torch.empty((B, L, H * dh), dtype=a.dtype, device=a.device)
+    _lib.call("ropeslr_dit_heads_to_tokens", a.data_ptr(), B, H, L, dh, y.data_ptr(), _stream(a))
+    return y
+
+
 def sinusoidal(t: torch.Tensor, dim: int) -> torch.Tensor:
     half = dim // 2
     freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=torch.float64, device=t.device) / half)
@@ -204,13 +225,14 @@ class WanBlock(nn.Module):
 
     def _forward_fused(self, x, mods, ctx, grid, pe, settings, rope, group):
         """The same block with the token-wise ops fused (csrc/dit_ops.cu):
-        modulated LayerNorms, Q/K RMSNorm written straight into the op's
-        head-major layout, gated residuals in place."""
+        modulated and affine LayerNorms, Q/K RMSNorm written straight into
+        the op's head-major layout, gated residuals (the first out of place,
+        so the caller's x is left alone, the second in place), the
+        cross-attention output back to token-major rows."""
         cfg = self.cfg
         B, Lr, D = x.shape
         H, d = cfg.heads, cfg.head_dim
         sh_a, sc_a, g_a, sh_f, sc_f, g_f = mods
-        x = x.contiguous().clone()
         y = ln_modulate(x, sh_a, sc_a, cfg.eps)
         params = self.ropeslr_params()
         hm = group is None  # the Ulysses wrapper takes token-major [B, L_r, H, d]
@@ -221,13 +243,14 @@ class WanBlock(nn.Module):
             a = ulysses_attention(q, k, v, y, grid, params, settings, pe, group=group, rope=rope)
         else:
             a = forward(q, k, v, y, grid, params, settings, pe, rope=rope)
-        gated_residual_(x, self.o(a), g_a)
+        x = gated_add(x, self.o(a), g_a)  # a new tensor: the caller's x is not modified
         # cross-attention to the text tokens
         c = ln_affine(x, self.norm3)
         cq = rms_heads(self.cq(c), self.norm_cq.weight, self.norm_cq.eps, H)
         ck = self.norm_ck(self.ck(ctx)).view(B, -1, H, d).transpose(1, 2)
         cv = self.cv(ctx).view(B, -1, H, d).transpose(1, 2)
-        ca = F.scaled_dot_product_attention(cq, ck, cv).transpose(1, 2).reshape(B, Lr, D)
+        ca = F.scaled_dot_product_attention(cq, ck, cv)
+        ca = heads_to_tokens(ca) if ca.dtype == torch.bfloat16 else ca.transpose(1, 2).reshape(B, Lr, D)
         x += self.co(ca)
         y = ln_modulate(x, sh_f, sc_f, cfg.eps)
         # FFN up-projection with the tanh-GELU in the cuBLASLt epilogue

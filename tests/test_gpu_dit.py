@@ -178,3 +178,8 @@ def test_fused_ops_unit():
     want_x = x + (y.float() * gate).to(torch.bfloat16)
     got_x = dit.gated_residual_(x.clone(), y, gate)
     assert torch.equal(got_x, want_x)
+    x0 = x.clone()
+    assert torch.equal(dit.gated_add(x, y, gate), want_x)
+    assert torch.equal(x, x0)
+    a = torch.randn((2, H, L, D // H), generator=g, device="cuda").to(torch.bfloat16)
+    assert torch.equal(dit.heads_to_tokens(a), a.transpose(1, 2).reshape(2, L, D))
