@@ -242,6 +242,41 @@ def heads_per_rank(H, world):
 
 
 # ---------------------------------------------------------------- arms
+def graph_ms(fn, n, dev, stream):
+    """GPU time of one stage: n calls captured in a CUDA graph and
+    replayed (the Python wrapper's allocations and ctypes calls are not
+    in the timed region, so a slow host cannot inflate a ~0.3 ms stage);
+    eager calls if the stage cannot be captured."""
+    import torch
+
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    try:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            fn()  # warm the allocator on the capture stream
+        stream.wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(n):
+                fn()
+        graph.replay()
+        torch.cuda.synchronize()
+        a.record(stream)
+        graph.replay()
+        b.record(stream)
+    except Exception:  # not capturable: eager launches
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / n
+
+
 def run_reference(args, cfg, rank, world):
     """Reference arm: the reference's CPU algorithm (oracle port of
     mechanism.py, float64 NumPy, all host threads) on a bounded sample."""
@@ -363,36 +398,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # ---- K1 (selection) and K3 (compensator + gate) alone, CUDA events on the
     # launching stream: the HBM roofline of the two bandwidth-bound stages
     def stage_ms(fn, n=20):
-        """GPU time of one stage: n calls captured in a CUDA graph and
-        replayed (the Python wrapper's allocations and ctypes calls are not
-        in the timed region, so a slow host cannot inflate a ~0.3 ms stage);
-        eager calls if the stage cannot be captured."""
-        for _ in range(2):
-            fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        try:
-            side = torch.cuda.Stream(dev)
-            side.wait_stream(stream)
-            with torch.cuda.stream(side):
-                fn()  # warm the allocator on the capture stream
-            stream.wait_stream(side)
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                for _ in range(n):
-                    fn()
-            graph.replay()
-            torch.cuda.synchronize()
-            a.record(stream)
-            graph.replay()
-            b.record(stream)
-        except Exception:  # not capturable: eager launches
-            a.record(stream)
-            for _ in range(n):
-                fn()
-            b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / n
+        return graph_ms(fn, n, dev, stream)
 
     k1_ms = stage_ms(lambda: P.select_blocks(q, k, settings.sparse, grid, want_mask=False))
     k3_ms = stage_ms(lambda: P.compensator_branch(x, grid, params, settings, pe, head_offset=h0, H_local=Hl))
@@ -610,7 +616,8 @@ def run_sweep(args, local_rank):
     """BASELINE config 2: sparsity 80/90/95% x block 64/128 on the Wan2.1
     shape (H=12, d=128, L=32760, r=64).  One JSON line per point with the
     sparse branch (K2+K4) TF/s against the bf16 peak and the low-rank branch
-    (K3) HBM GB/s against the copy peak, each timed alone with CUDA events."""
+    (K3) HBM GB/s against the copy peak, each timed alone with CUDA events
+    around a CUDA-graph replay of back-to-back calls (graph_ms)."""
     import torch
 
     import paper_2605_20659_b200 as P
@@ -624,15 +631,7 @@ def run_sweep(args, local_rank):
     stream = torch.cuda.current_stream(dev)
 
     def timed(fn, n):
-        for _ in range(2):
-            fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(n):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / n
+        return graph_ms(fn, n, dev, stream)
 
     for block in (64, 128):
         for sparsity in (0.8, 0.9, 0.95):

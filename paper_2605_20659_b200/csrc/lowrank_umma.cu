@@ -25,7 +25,10 @@
 //                 (GEMM2's A operand); gate partial; D2 row -> sigmoid ->
 //                 RMSNorm * rms_lowrank -> bf16 y_lr row.
 // Shared memory holds the 4-stage X ring (128 KiB, enough bytes in flight to
-// cover HBM latency), the W_A / W_B images and the Z / G tables.
+// cover HBM latency), the W_A / W_B images and the Z / G tables; the last
+// three are one contiguous per-head blob in the tables buffer, staged by a
+// single bulk copy that overlaps the CTA's set-up and first X loads (the
+// per-thread staging it replaced was ~10% of a 21-tile CTA at the Wan shape).
 // HBM traffic per (token, head): 256 B of X in, 256 B of y_lr out.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -49,29 +52,37 @@ constexpr int NWG = 3;                 // epilogue warpgroups
 constexpr int kThreads = 128 + NWG * 128;
 constexpr uint32_t H1_COL = 384;       // TMEM columns [384 + 32w, 384 + 32w + 32): H1_w, bf16 pairs
 
+// One head's parameter-only operands ("blob"), laid out identically in the
+// tables buffer (per head, contiguous) and in shared memory, so the kernel
+// stages them with one bulk copy: W_A^T image | W_B^T image | Z [nrows][ZP]
+// f32 | G [nrows] f32 (padded to 16 bytes).
 template <int R>
 struct Lay {
   static constexpr int N1 = R + 16;              // GEMM1 N: rank + gate hi / lo (+ zero pad)
   static constexpr int X_BYTES = M * D * 2;      // 32 KiB
   static constexpr int WA_BYTES = N1 * D * 2;    // two 64-col atoms of N1 rows
   static constexpr int WB_BYTES = D * KR * 2;    // 16 KiB
+  static_assert(WA_BYTES % 1024 == 0, "W_B^T image must stay 1024-byte aligned");
+  static constexpr int ZP = R + 4;               // Z row pitch (floats): float4 rows spread over the banks
   static constexpr int OFF_X = 0;
-  static constexpr int OFF_WA = OFF_X + XSTAGES * X_BYTES;
-  static constexpr int OFF_WB = OFF_WA + (WA_BYTES + 1023) / 1024 * 1024;
-  static constexpr int OFF_BAR = OFF_WB + WB_BYTES;
-  static constexpr int NBAR = 2 * XSTAGES + 4 * NWG;  // X ring full/empty + 4 per warpgroup
-  static constexpr int OFF_RMS = OFF_BAR + 256;       // rms_lowrank [128] f32
-  static constexpr int OFF_TAB = OFF_RMS + D * 4;     // Z [nrows][R + 4] f32, then G [nrows] f32
-  static constexpr int ZP = R + 4;                    // Z row pitch (floats): float4 rows spread over the banks
+  static constexpr int OFF_BAR = OFF_X + XSTAGES * X_BYTES;
+  static constexpr int NBAR = 2 * XSTAGES + 4 * NWG + 1;  // X ring full/empty + 4 per warpgroup + blob
+  static constexpr int OFF_RMS = OFF_BAR + 256;           // rms_lowrank [128] f32
+  static constexpr int OFF_WA = OFF_RMS + 1024 - 256;     // the blob, 1024-byte aligned
+  static constexpr int OFF_WB = OFF_WA + WA_BYTES;
+  static constexpr int OFF_TAB = OFF_WB + WB_BYTES;       // Z, then G
   static_assert(NBAR * 8 + 4 <= 256, "barrier block overflows");
-  static int bytes(int nrows) { return OFF_TAB + nrows * (ZP + 1) * 4; }
+  static_assert(OFF_RMS + D * 4 <= OFF_WA && OFF_WA % 1024 == 0, "smem layout");
+  __host__ __device__ static int tab_bytes(int nrows) { return (nrows * (ZP + 1) * 4 + 15) / 16 * 16; }
+  __host__ __device__ static int blob_bytes(int nrows) { return WA_BYTES + WB_BYTES + tab_bytes(nrows); }
+  __host__ __device__ static int bytes(int nrows) { return OFF_WA + blob_bytes(nrows); }
 };
 
 // Per warpgroup w: D1F (GEMM1 done), H1F (H1 written to TMEM), D2F (GEMM2
 // done), RE (its TMEM region read out: the next GEMM1 may overwrite it).
 enum Bar { XF = 0, XE = XSTAGES, D1F = 2 * XSTAGES, H1F = D1F + NWG, D2F = H1F + NWG, RE = D2F + NWG,
-           BAR_END = RE + NWG };
-static_assert(BAR_END == 2 * XSTAGES + 4 * NWG, "barrier enum and Lay::NBAR disagree");
+           BLOB = RE + NWG, BAR_END = BLOB + 1 };
+static_assert(BAR_END == 2 * XSTAGES + 4 * NWG + 1, "barrier enum and Lay::NBAR disagree");
 
 struct FoldArgs {
   const float* w_a;   // [H, d, r]
@@ -81,10 +92,7 @@ struct FoldArgs {
   const float *pe_t, *pe_x, *pe_y;  // [n, D_total]
   int64_t d_model, head_offset;
   int H, r, T, Hg, Wg, use_pe;
-  uint8_t* wa_img;    // [H][Lay::WA_BYTES] swizzled smem images
-  uint8_t* wb_img;    // [H][Lay::WB_BYTES]
-  float* Z;           // [H][nrows][r]
-  float* G;           // [H][nrows]
+  uint8_t* blob;      // [H][Lay::blob_bytes(nrows)]: swizzled W_A^T / W_B^T images, Z, G
 };
 
 __device__ __forceinline__ uint32_t sw128(int row, int chunk) {
@@ -103,7 +111,7 @@ __global__ void __launch_bounds__(128) lowrank_fold_umma_kernel(FoldArgs a) {
   if (blockIdx.x == nrows) {
     constexpr int N1 = Lay<R>::N1;
     const float* wa = a.w_a + static_cast<int64_t>(h) * D * R;
-    uint8_t* img = a.wa_img + static_cast<int64_t>(h) * Lay<R>::WA_BYTES;
+    uint8_t* img = a.blob + static_cast<int64_t>(h) * Lay<R>::blob_bytes(nrows);
     for (int e = tid; e < N1 * (D / 8); e += blockDim.x) {
       const int n = e / (D / 8), c16 = e % (D / 8);  // 16-byte chunk of 8 k-values
       uint32_t pk[4];
@@ -131,7 +139,7 @@ __global__ void __launch_bounds__(128) lowrank_fold_umma_kernel(FoldArgs a) {
   }
   if (blockIdx.x == nrows + 1) {
     const float* wb = a.w_b + static_cast<int64_t>(h) * R * D;
-    uint8_t* img = a.wb_img + static_cast<int64_t>(h) * Lay<R>::WB_BYTES;
+    uint8_t* img = a.blob + static_cast<int64_t>(h) * Lay<R>::blob_bytes(nrows) + Lay<R>::WA_BYTES;
     for (int e = tid; e < D * (KR / 8); e += blockDim.x) {
       const int n = e / (KR / 8), chunk = e % (KR / 8);
       uint32_t pk[4];
@@ -147,10 +155,13 @@ __global__ void __launch_bounds__(128) lowrank_fold_umma_kernel(FoldArgs a) {
     return;
   }
   const int i = blockIdx.x;
-  float* zrow = a.Z + (static_cast<int64_t>(h) * nrows + i) * R;
+  float* ztab = reinterpret_cast<float*>(a.blob + static_cast<int64_t>(h) * Lay<R>::blob_bytes(nrows) +
+                                         Lay<R>::WA_BYTES + Lay<R>::WB_BYTES);
+  float* zrow = ztab + i * Lay<R>::ZP;
+  float* grow = ztab + nrows * Lay<R>::ZP + i;
   if (!a.use_pe) {
-    for (int j = tid; j < R; j += blockDim.x) zrow[j] = 0.f;
-    if (tid == 0) a.G[static_cast<int64_t>(h) * nrows + i] = 0.f;
+    for (int j = tid; j < Lay<R>::ZP; j += blockDim.x) zrow[j] = 0.f;
+    if (tid == 0) *grow = 0.f;
     return;
   }
   __shared__ float v[D];
@@ -168,15 +179,14 @@ __global__ void __launch_bounds__(128) lowrank_fold_umma_kernel(FoldArgs a) {
     float z = 0.f;
     for (int k = 0; k < D; ++k) z = fmaf(v[k], wa[k * R + tid], z);
     zrow[tid] = z;
+  } else if (tid < Lay<R>::ZP) {
+    zrow[tid] = 0.f;  // pitch padding
   }
-  if (tid == 0) a.G[static_cast<int64_t>(h) * nrows + i] = (red[0] + red[1]) + (red[2] + red[3]);
+  if (tid == 0) *grow = (red[0] + red[1]) + (red[2] + red[3]);
 }
 
 struct MainArgs {
-  const uint8_t* wa_img;
-  const uint8_t* wb_img;
-  const float* Z;
-  const float* G;
+  const uint8_t* blob;  // [H][Lay::blob_bytes(nrows)]
   const float* rms_lr;
   float eps;
   int64_t L;
@@ -208,21 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
   const int bh = blockIdx.y;
   const int b = bh / a.H, h = bh % a.H;
 
-  // ---- stage the per-head operands (generic proxy), then publish to the async proxy
-  {
-    const uint4* wa = reinterpret_cast<const uint4*>(a.wa_img + static_cast<int64_t>(h) * Lay_::WA_BYTES);
-    for (int e = threadIdx.x; e < Lay_::WA_BYTES / 16; e += kThreads) reinterpret_cast<uint4*>(sWA)[e] = wa[e];
-    const uint4* wb = reinterpret_cast<const uint4*>(a.wb_img + static_cast<int64_t>(h) * Lay_::WB_BYTES);
-    for (int e = threadIdx.x; e < Lay_::WB_BYTES / 16; e += kThreads) reinterpret_cast<uint4*>(sWB)[e] = wb[e];
-    const float* z = a.Z + static_cast<int64_t>(h) * nrows * R;
-    for (int e = threadIdx.x; e < nrows * R / 4; e += kThreads) {
-      const int row = e / (R / 4), c4 = e % (R / 4);
-      *reinterpret_cast<float4*>(sZ + row * ZP + c4 * 4) = reinterpret_cast<const float4*>(z)[e];
-    }
-    for (int e = threadIdx.x; e < nrows; e += kThreads) sG[e] = a.G[static_cast<int64_t>(h) * nrows + e];
-    for (int e = threadIdx.x; e < D; e += kThreads) sRms[e] = a.rms_lr[e];
-    fence_proxy_async_smem();
-  }
+  // The head's blob (W_A^T / W_B^T images, Z, G) arrives by one bulk copy,
+  // issued right after the barriers are initialised, behind nothing; the MMA
+  // warp and the epilogue wait on its barrier before their first use.
+  for (int e = threadIdx.x; e < D; e += kThreads) sRms[e] = a.rms_lr[e];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmX);
     for (int i = 0; i < Lay_::NBAR; ++i) {
@@ -230,6 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
       mbar_init(&bars[i], per_thread ? 128 : 1);
     }
     fence_mbar_init();
+    const uint32_t blob_bytes = static_cast<uint32_t>(Lay_::blob_bytes(nrows));
+    mbar_arrive_expect_tx(&bars[BLOB], blob_bytes);
+    bulk_load_1d(sWA, a.blob + static_cast<int64_t>(h) * blob_bytes, blob_bytes, &bars[BLOB], policy_evict_last());
   }
   if (warp == 2) {
     tmem_alloc(tmem_holder, 512);
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
     const uint64_t dWA = desc_sw128(smem_u32(sWA), 16, 1024);
     const uint64_t dWB = desc_sw128(smem_u32(sWB), 16, 1024);
     const bool leader = elect_one();
+    mbar_wait(&bars[BLOB], 0);
     int n1 = 0, n2 = 0;
     while (n2 < n_my) {
       bool issued = false;
@@ -320,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) lowrank_umma_kernel(const __grid_
     const uint32_t treg = tlane + w * 128;
     const uint32_t th1 = tlane + H1_COL + w * 32;
     const int hw = a.Hg * a.Wg;
+    if (w < n_my) mbar_wait(&bars[BLOB], 0);
     for (int i = w; i < n_my; i += NWG) {
       const uint32_t ph = (i / NWG) & 1;
       const int t = first + i * stride;
@@ -483,8 +487,7 @@ size_t up(size_t x) { return (x + 255) / 256 * 256; }
 // then the gate partials.
 template <int R>
 size_t tables_bytes(int64_t H, int nrows) {
-  return up(static_cast<size_t>(H) * Lay<R>::WA_BYTES) + up(static_cast<size_t>(H) * Lay<R>::WB_BYTES) +
-         up(static_cast<size_t>(H) * nrows * R * 4) + up(static_cast<size_t>(H) * nrows * 4);
+  return up(static_cast<size_t>(H) * Lay<R>::blob_bytes(nrows));
 }
 
 template <int R>
@@ -497,7 +500,6 @@ template <int R>
 FoldArgs fold_args(const ropeslr_shape* s, const ropeslr_token_args* t, const float* w_a, const float* w_b,
                    void* tables) {
   const int H = static_cast<int>(s->H);
-  const int nrows = t->grid_t + t->grid_h + t->grid_w;
   uint8_t* p = static_cast<uint8_t*>(tables);
   FoldArgs f;
   f.w_a = w_a;
@@ -515,13 +517,7 @@ FoldArgs fold_args(const ropeslr_shape* s, const ropeslr_token_args* t, const fl
   f.Hg = t->grid_h;
   f.Wg = t->grid_w;
   f.use_pe = t->use_pe;
-  f.wa_img = p;
-  p += up(static_cast<size_t>(H) * Lay<R>::WA_BYTES);
-  f.wb_img = p;
-  p += up(static_cast<size_t>(H) * Lay<R>::WB_BYTES);
-  f.Z = reinterpret_cast<float*>(p);
-  p += up(static_cast<size_t>(H) * nrows * R * 4);
-  f.G = reinterpret_cast<float*>(p);
+  f.blob = p;
   return f;
 }
 
@@ -554,10 +550,7 @@ int run_main(const ropeslr_shape* s, const ropeslr_token_args* t, const void* ta
     return ROPESLR_ERR_LAUNCH;
 
   MainArgs m;
-  m.wa_img = f.wa_img;
-  m.wb_img = f.wb_img;
-  m.Z = f.Z;
-  m.G = f.G;
+  m.blob = f.blob;
   m.rms_lr = rms_lowrank;
   m.eps = eps;
   m.L = s->L;

@@ -14,10 +14,5 @@ for _ in range(5):
     fn()
 torch.cuda.synchronize()
 for rep in range(3):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(50):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    print(os.environ.get("ROPESLR_LIBRARY", "default")[-14:], cfg["name"][:20], f"{e0.elapsed_time(e1) / 50:.4f} ms")
+    ms = Bm.graph_ms(fn, 50, dev, torch.cuda.current_stream(dev))
+    print(os.environ.get("ROPESLR_LIBRARY", "default")[-14:], cfg["name"][:20], f"{ms:.4f} ms (graph replay)")
