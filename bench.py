@@ -785,11 +785,13 @@ def run_skew(args, local_rank):
             ms = e0.elapsed_time(e1) / n
             att = int(prep.sel.attended.sum())
             fb = P.fallback_units(prep, ws)
+            # K1 alone for this rule and these scores (graph replay)
+            k1_ms = graph_ms(lambda: P.select_blocks(q, k, sp, grid, want_mask=False), 10, dev, stream)
             cnt = prep.sel.cnt.float()
             print(json.dumps({
                 "metric": "K2+K4 on skewed block scores (config-3 shape)", "config": {
                     "workload": cfg["name"] + f"_skew{strength:g}_{rule}", "skew_strength": strength, "rule": rule},
-                "k2_ms": ms, "sparse_TFLOP_per_s": 4.0 * cfg["d"] * att / (ms * 1e-3) / 1e12,
+                "k2_ms": ms, "sparse_TFLOP_per_s": 4.0 * cfg["d"] * att / (ms * 1e-3) / 1e12, "k1_ms": k1_ms,
                 "fallback_units": fb, "units": cfg["H"] * nb, "fallback_rate": fb / (cfg["H"] * nb),
                 "blocks_per_row": {"min": int(cnt.min()), "max": int(cnt.max()), "mean": float(cnt.mean())},
                 "dtype": "bf16", "data": "synthetic: seeded N(0,1) + skew_blocks structure"}), flush=True)

@@ -148,6 +148,9 @@ int64_t ropeslr_num_blocks(int64_t L, int32_t block);
  *   "screen"        0: K1 top-k from float64 scores of every block pair
  *                   (default 1: float32-grade tensor-core screening, float64
  *                   only where the decision can depend on it)
+ *   "keep_bitonic"  1: keep-rule rows by the round-1 bitonic sort per row
+ *                   (default 0: radix sort on float32 keys, exact order
+ *                   restored inside runs of equal keys)
  * Not synchronised with calls in flight on other threads.  Unknown name:
  * ROPESLR_ERR_VALUE.  ropeslr_get_option returns the current value. */
 int ropeslr_set_option(const char* name, int value);

@@ -46,6 +46,8 @@ static Tuning& tuning_mut() {
     const char* lin = getenv("ROPESLR_LINEAR");
     r.linear_simt = lin != nullptr && lin[0] == 's';
     r.screen = !env_off("ROPESLR_SCREEN");
+    const char* ks = getenv("ROPESLR_KEEP_SORT");
+    r.keep_bitonic = ks != nullptr && ks[0] == 'b';
     return r;
   }();
   return t;
@@ -118,6 +120,7 @@ extern "C" int ropeslr_set_option(const char* name, int value) {
   else if (!strcmp(name, "rope_tma")) t.rope_tma = value != 0;
   else if (!strcmp(name, "linear_simt")) t.linear_simt = value != 0;
   else if (!strcmp(name, "screen")) t.screen = value != 0;
+  else if (!strcmp(name, "keep_bitonic")) t.keep_bitonic = value != 0;
   else return ROPESLR_ERR_VALUE;
   return ROPESLR_OK;
 }
@@ -133,6 +136,7 @@ extern "C" int ropeslr_get_option(const char* name) {
   if (!strcmp(name, "rope_tma")) return t.rope_tma;
   if (!strcmp(name, "linear_simt")) return t.linear_simt;
   if (!strcmp(name, "screen")) return t.screen;
+  if (!strcmp(name, "keep_bitonic")) return t.keep_bitonic;
   return ROPESLR_ERR_VALUE;
 }
 

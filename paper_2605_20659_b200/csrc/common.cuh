@@ -104,6 +104,7 @@ struct Tuning {
   bool rope_tma;       // ROPESLR_ROPE_TMA=0: the row-bulk-copy RoPE kernel
   bool linear_simt;    // ROPESLR_LINEAR=simt: the CUDA-core linear compensator
   bool screen;         // ROPESLR_SCREEN=0: K1 top-k from float64 scores of every pair (no screening)
+  bool keep_bitonic;   // ROPESLR_KEEP_SORT=bitonic: the round-1 keep-mode selection (bitonic sort per row)
 };
 const Tuning& tuning();
 

@@ -13,6 +13,9 @@
 //             attention kernel walks (mechanism.py:321 `sorted(chosen)`).
 // All three are HBM/L2-bound; see DESIGN.md for the byte counts.
 #include <algorithm>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -507,6 +510,189 @@ __global__ void __launch_bounds__(256) select_rows_kernel(const double* __restri
       int f = (i < nb) ? flags[i] : 0;
       unsigned bal = __ballot_sync(0xffffffffu, f);
       int pos = carry + __popc(bal & ((1u << lane) - 1u));
+      if (f) {
+        irow[pos] = i;
+        ksum += block_size(L, block, i);
+      }
+      carry += __popc(bal);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+    if (lane == 0) {
+      cnt[row] = nkeep;
+      atomicAdd(attended + bh, static_cast<unsigned long long>(ksum * block_size(L, block, qb)));
+    }
+  }
+}
+
+// Cumulative-mass (`keep`) rows, one CTA per (bh, query block) row, nb <=
+// 256 * IPT (mechanism.py:310-320, decomposition.py:105-111).  The same
+// decisions as select_rows_kernel, from a cheaper sort: the row's scores are
+// ordered by the top 24 bits of the float32 rounding of the score (order
+// preserving and monotone: sign, exponent, 15 mantissa bits) with a stable
+// radix sort (6 passes of 4 bits; the block index rides in the key's low
+// bits); runs of equal keys -- float64 scores closer than 2^-15 relative,
+// exact duplicates, the underflowed tail -- are then put in the exact order
+// (float64 score, then lower block) by an insertion sort per run.  The probabilities exp(s - max) / sum follow in
+// that order, their inclusive prefix sums (per-thread sequential, then a
+// block scan) give the first position reaching keep - 1e-12; all reductions
+// run in a fixed order, so the result is deterministic.
+__device__ __forceinline__ uint32_t desc_key32(double s) {
+  float f = __double2float_rn(s);  // monotone non-decreasing in s
+  if (f == 0.f) f = 0.f;           // -0 -> +0 (the float64 key folds them too)
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t asc = (u >> 31) ? ~u : (u | 0x80000000u);
+  return ~asc;
+}
+
+template <int T, int IPT>
+__global__ void __launch_bounds__(T) select_keep_kernel(const double* __restrict__ scores, int nb, int64_t L,
+                                                          int block, double keep, int kmax,
+                                                          int32_t* __restrict__ idx, int32_t* __restrict__ cnt,
+                                                          uint8_t* __restrict__ mask,
+                                                          unsigned long long* __restrict__ attended) {
+  constexpr int N = T * IPT;
+  using Sort = cub::BlockRadixSort<uint64_t, T, IPT, cub::NullType, 4>;
+  using RedD = cub::BlockReduce<double, T>;
+  using ScanD = cub::BlockScan<double, T>;
+  using RedI = cub::BlockReduce<int, T>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename RedD::TempStorage redd;
+    typename ScanD::TempStorage scan;
+    typename RedI::TempStorage redi;
+  } tmp;
+  __shared__ double s_sc[N];
+  __shared__ uint32_t s_key[N];
+  __shared__ int s_id[N];
+  int* flags = reinterpret_cast<int*>(s_key);  // the float32 keys are dead once the runs are ordered
+  __shared__ double s_bc;
+  __shared__ int s_nkeep;
+
+  const int64_t row = blockIdx.x;  // bh * nb + qb
+  const int64_t bh = row / nb;
+  const int qb = static_cast<int>(row % nb);
+  const double* srow = scores + row * nb;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+
+  double m = -INFINITY;
+  for (int i = tid; i < nb; i += T) {
+    const double v = srow[i];
+    s_sc[i] = v;
+    m = fmax(m, v);
+  }
+  m = RedD(tmp.redd).Reduce(m, cub::Max());
+  if (tid == 0) s_bc = m;
+  __syncthreads();
+  const double row_max = s_bc;
+
+  // sort keys: float32 score key (blocks below the underflow point tie at
+  // -inf), then the block index; blocked arrangement = index order
+  uint64_t keys[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = tid * IPT + k;
+    if (i < nb) {
+      const double v = s_sc[i];
+      const uint32_t kk = desc_key32(v - row_max < kProbUnderflow ? -INFINITY : v);
+      keys[k] = (static_cast<uint64_t>(kk) << 10) | static_cast<uint64_t>(i);
+    } else {
+      keys[k] = (1ull << 42) - 1;
+    }
+  }
+  __syncthreads();  // tmp reuse
+  Sort(tmp.sort).Sort(keys, 18, 42);  // stable: equal keys stay in block order
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = tid * IPT + k;
+    s_key[pos] = static_cast<uint32_t>(keys[k] >> 18);
+    s_id[pos] = static_cast<int>(keys[k] & 1023u);
+  }
+  __syncthreads();
+  // exact order inside runs of equal float32 keys
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = tid * IPT + k;
+    if (pos + 1 < nb && s_key[pos + 1] == s_key[pos] && (pos == 0 || s_key[pos - 1] != s_key[pos])) {
+      int end = pos + 2;
+      while (end < nb && s_key[end] == s_key[pos]) ++end;
+      for (int a = pos + 1; a < end; ++a) {
+        const int ia = s_id[a];
+        const double va = s_sc[ia];
+        const uint64_t ka = desc_key(va - row_max < kProbUnderflow ? -INFINITY : va);
+        int b = a - 1;
+        while (b >= pos) {
+          const int ib = s_id[b];
+          const double vb = s_sc[ib];
+          const uint64_t kb = desc_key(vb - row_max < kProbUnderflow ? -INFINITY : vb);
+          if (kb < ka || (kb == ka && ib < ia)) break;
+          s_id[b + 1] = ib;
+          --b;
+        }
+        s_id[b + 1] = ia;
+      }
+    }
+  }
+  __syncthreads();
+
+  // probabilities in sorted order, their sum, the prefix sums
+  double e[IPT];
+  double part = 0.0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = tid * IPT + k;
+    e[k] = pos < nb ? exp(s_sc[s_id[pos]] - row_max) : 0.0;
+    part += e[k];
+  }
+  const double total = RedD(tmp.redd).Sum(part);
+  if (tid == 0) s_bc = total;
+  __syncthreads();
+  const double sum = s_bc;
+  double c[IPT];
+  double run = 0.0;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    run += e[k] / sum;
+    c[k] = run;
+  }
+  double excl;
+  ScanD(tmp.scan).ExclusiveSum(run, excl);
+  const double target = keep - kMassSlack;
+  int first = nb;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = tid * IPT + k;
+    if (pos < nb && excl + c[k] >= target) {
+      first = pos;
+      break;
+    }
+  }
+  __syncthreads();  // tmp reuse
+  first = RedI(tmp.redi).Reduce(first, cub::Min());
+  if (tid == 0) s_nkeep = first < nb ? first + 1 : nb;
+  __syncthreads();
+  const int nkeep = s_nkeep;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int pos = tid * IPT + k;
+    if (pos < nb) flags[s_id[pos]] = pos < nkeep ? 1 : 0;
+  }
+  __syncthreads();
+
+  if (mask != nullptr) {
+    uint8_t* mrow = mask + row * nb;
+    for (int i = tid; i < nb; i += T) mrow[i] = static_cast<uint8_t>(flags[i]);
+  }
+  if (warp == 0) {
+    int32_t* irow = idx + row * kmax;
+    int carry = 0;
+    long long ksum = 0;
+    for (int base = 0; base < nb; base += 32) {
+      const int i = base + lane;
+      const int f = (i < nb) ? flags[i] : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      const int pos = carry + __popc(bal & ((1u << lane) - 1u));
       if (f) {
         irow[pos] = i;
         ksum += block_size(L, block, i);
@@ -1484,6 +1670,23 @@ static int launch_select(const ropeslr_shape* s, const ropeslr_select_params* se
     else
       ROPESLR_SEL_CASE(32);
 #undef ROPESLR_SEL_CASE
+    return launch_status();
+  }
+  if (sel->topk <= 0 && nb <= 1024 && !tuning().keep_bitonic) {
+    const int64_t off = row0;
+    const unsigned grid = static_cast<unsigned>(row1 - row0);
+#ifndef ROPESLR_KEEP_T
+#define ROPESLR_KEEP_T 128  // 128 threads x 8 keys: fewer barrier participants than 256 x 4 (0.98 vs 1.04 ms for K1 at config 3)
+#endif
+    constexpr int KT = ROPESLR_KEEP_T;
+    if (nb <= KT * 2)
+      select_keep_kernel<KT, 2><<<grid, KT, 0, st>>>(scores + off * nb, nb, s->L, s->block, sel->keep, kmax,
+                                                     idx + off * kmax, cnt + off, mask ? mask + off * nb : nullptr,
+                                                     att + bh0);
+    else
+      select_keep_kernel<KT, 1024 / KT><<<grid, KT, 0, st>>>(scores + off * nb, nb, s->L, s->block, sel->keep,
+                                                             kmax, idx + off * kmax, cnt + off,
+                                                             mask ? mask + off * nb : nullptr, att + bh0);
     return launch_status();
   }
   const int n2 = next_pow2(nb);
