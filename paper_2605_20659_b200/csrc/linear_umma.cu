@@ -91,14 +91,19 @@ __device__ __forceinline__ float2 bf16x2_to_f32x2(uint32_t w) {
 }
 
 // phi(k) = elu(k) + 1 = exp(min(k, 0)) + max(k, 0) (mechanism.py:33-36),
-// branch-free: exp(0) = 1 supplies the +1 of the positive side.
+// branch-free: exp(0) = 1 supplies the +1 of the positive side.  With
+// 2 min(k, 0) = k - |k| and 2 max(k, 0) = k + |k| (both exact) the work
+// stays on the FMA pipe (|k| is an operand modifier) instead of four
+// min / max on the ALU; bit-identical to the min / max form.
 __device__ __forceinline__ float2 phi2(float2 k) {
-  const float2 e = __fmul2_rn(make_float2(fminf(k.x, 0.f), fminf(k.y, 0.f)),
-                              make_float2(1.4426950408889634f, 1.4426950408889634f));
+  const float2 ak = make_float2(fabsf(k.x), fabsf(k.y));
+  const float2 neg2 = __fadd2_rn(k, make_float2(-ak.x, -ak.y));  // 2 min(k, 0)
+  const float2 pos2 = __fadd2_rn(k, ak);  // 2 max(k, 0)
+  const float2 e = __fmul2_rn(neg2, make_float2(0.72134752044448170f, 0.72134752044448170f));  // log2(e) / 2
   float2 r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(e.x));
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(e.y));
-  return __fadd2_rn(r, make_float2(fmaxf(k.x, 0.f), fmaxf(k.y, 0.f)));
+  return __ffma2_rn(pos2, make_float2(0.5f, 0.5f), r);
 }
 
 // In place on chunks [c0, c0 + NC) of row r of a tile: v + (T[rt] + T[rx] +
