@@ -546,18 +546,20 @@ __device__ __forceinline__ uint32_t desc_key32(double s) {
 }
 
 template <int T, int IPT>
-__global__ void __launch_bounds__(T) select_keep_kernel(const double* __restrict__ scores, int nb, int64_t L,
+__global__ void __launch_bounds__(T, 8) select_keep_kernel(const double* __restrict__ scores, int nb, int64_t L,
                                                           int block, double keep, int kmax,
                                                           int32_t* __restrict__ idx, int32_t* __restrict__ cnt,
                                                           uint8_t* __restrict__ mask,
                                                           unsigned long long* __restrict__ attended) {
   constexpr int N = T * IPT;
   using Sort = cub::BlockRadixSort<uint64_t, T, IPT, cub::NullType, 4>;
+  using SortFull = cub::BlockRadixSort<uint64_t, T, IPT, int, 4>;  // long runs: the full float64 key
   using RedD = cub::BlockReduce<double, T>;
   using ScanD = cub::BlockScan<double, T>;
   using RedI = cub::BlockReduce<int, T>;
   __shared__ union {
     typename Sort::TempStorage sort;
+    typename SortFull::TempStorage sort_full;
     typename RedD::TempStorage redd;
     typename ScanD::TempStorage scan;
     typename RedI::TempStorage redi;
@@ -610,22 +612,38 @@ __global__ void __launch_bounds__(T) select_keep_kernel(const double* __restrict
     s_id[pos] = static_cast<int>(keys[k] & 1023u);
   }
   __syncthreads();
-  // exact order inside runs of equal float32 keys
+  // exact order inside runs of equal float32 keys: runs whose float64 keys
+  // all agree are already in block order; other runs up to 32 long by an
+  // insertion sort; a longer one sends the whole row through a radix sort
+  // on the full float64 key (16 passes) instead of a quadratic sort
+  auto key64 = [&](int i) {
+    const double v = s_sc[i];
+    return desc_key(v - row_max < kProbUnderflow ? -INFINITY : v);
+  };
+  int long_run = 0;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
     const int pos = tid * IPT + k;
     if (pos + 1 < nb && s_key[pos + 1] == s_key[pos] && (pos == 0 || s_key[pos - 1] != s_key[pos])) {
-      int end = pos + 2;
-      while (end < nb && s_key[end] == s_key[pos]) ++end;
+      const uint64_t k0 = key64(s_id[pos]);
+      int end = pos + 1;
+      bool same = true;
+      while (end < nb && s_key[end] == s_key[pos]) {
+        same = same && key64(s_id[end]) == k0;
+        ++end;
+      }
+      if (same) continue;
+      if (end - pos > 32) {
+        long_run = 1;
+        continue;
+      }
       for (int a = pos + 1; a < end; ++a) {
         const int ia = s_id[a];
-        const double va = s_sc[ia];
-        const uint64_t ka = desc_key(va - row_max < kProbUnderflow ? -INFINITY : va);
+        const uint64_t ka = key64(ia);
         int b = a - 1;
         while (b >= pos) {
           const int ib = s_id[b];
-          const double vb = s_sc[ib];
-          const uint64_t kb = desc_key(vb - row_max < kProbUnderflow ? -INFINITY : vb);
+          const uint64_t kb = key64(ib);
           if (kb < ka || (kb == ka && ib < ia)) break;
           s_id[b + 1] = ib;
           --b;
@@ -633,6 +651,19 @@ __global__ void __launch_bounds__(T) select_keep_kernel(const double* __restrict
         s_id[b + 1] = ia;
       }
     }
+  }
+  if (__syncthreads_or(long_run)) {
+    uint64_t kf[IPT];
+    int vf[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      const int i = tid * IPT + k;
+      kf[k] = i < nb ? key64(i) : ~0ull;
+      vf[k] = i;
+    }
+    SortFull(tmp.sort_full).Sort(kf, vf);  // stable: equal keys stay in block order
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) s_id[tid * IPT + k] = vf[k];
   }
   __syncthreads();
 

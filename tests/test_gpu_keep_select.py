@@ -74,6 +74,12 @@ def test_keep_clusters_duplicates_and_underflow():
     q, k = _rows(40.0 * rng.standard_normal((nb, d)), 40.0 * rng.standard_normal((nb, d)), block)
     for keep in KEEPS:
         _both(q, k, keep, block)
+    # one run over the whole row: every score equal to float32 resolution
+    # but distinct in float64, in random order (the full-key radix path)
+    base = rng.standard_normal(d)
+    q, k = _rows(np.tile(rng.standard_normal(d), (nb, 1)), base + 1e-9 * rng.standard_normal((nb, d)), block)
+    for keep in KEEPS:
+        _both(q, k, keep, block)
     # every score equal: ties to the lower blocks
     z = np.zeros((nb, d))
     q, k = _rows(z, z, block)
