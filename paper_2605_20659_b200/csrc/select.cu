@@ -545,6 +545,10 @@ __device__ __forceinline__ uint32_t desc_key32(double s) {
   return ~asc;
 }
 
+// 128 threads x 8 keys per row: fewer barrier participants than 256 x 4
+// (K1 at config 3: 0.98 vs 1.04 ms; 512 x 2: 1.45 ms; 64 x 16 spills).
+constexpr int kKeepThreads = 128;
+
 template <int T, int IPT>
 __global__ void __launch_bounds__(T, 8) select_keep_kernel(const double* __restrict__ scores, int nb, int64_t L,
                                                           int block, double keep, int kmax,
@@ -1706,10 +1710,7 @@ static int launch_select(const ropeslr_shape* s, const ropeslr_select_params* se
   if (sel->topk <= 0 && nb <= 1024 && !tuning().keep_bitonic) {
     const int64_t off = row0;
     const unsigned grid = static_cast<unsigned>(row1 - row0);
-#ifndef ROPESLR_KEEP_T
-#define ROPESLR_KEEP_T 128  // 128 threads x 8 keys: fewer barrier participants than 256 x 4 (0.98 vs 1.04 ms for K1 at config 3)
-#endif
-    constexpr int KT = ROPESLR_KEEP_T;
+    constexpr int KT = kKeepThreads;
     if (nb <= KT * 2)
       select_keep_kernel<KT, 2><<<grid, KT, 0, st>>>(scores + off * nb, nb, s->L, s->block, sel->keep, kmax,
                                                      idx + off * kmax, cnt + off, mask ? mask + off * nb : nullptr,
