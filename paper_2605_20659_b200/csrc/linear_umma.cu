@@ -715,6 +715,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
       tmem_ld2(base + 128, den_u);
       tmem_wait_ld();
       const float inv_den = 1.f / fmaxf(__uint_as_float(den_u[0]), kFloor);
+      // sum of squares of the raw row (the 1 / den factor applied once, squared)
       float ss = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -722,14 +723,12 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
         tmem_ld32(base + c * 32, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float x = __uint_as_float(v[j]) * inv_den;
-          ss = fmaf(x, x, ss);
-        }
+        for (int j = 0; j < 32; ++j) ss = fmaf(__uint_as_float(v[j]), __uint_as_float(v[j]), ss);
       }
       const int64_t l = static_cast<int64_t>(t0 + i) * M + r;
       const bool live = l < a.L;
-      const float inv = rsqrtf(ss / static_cast<float>(D) + a.eps);
+      const float inv = rsqrtf(ss * (inv_den * inv_den) / static_cast<float>(D) + a.eps);
+      const float scale = inv_den * inv;  // o / den, RMS-normalised
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t v[32];
@@ -754,10 +753,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1)
         for (int j = 0; j < 32; j += 16) {
           uint32_t u[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float x0 = __uint_as_float(v[j + 2 * e]) * inv_den, x1 = __uint_as_float(v[j + 2 * e + 1]) * inv_den;
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0 * inv * sRms[cb + j + 2 * e], x1 * inv * sRms[cb + j + 2 * e + 1]);
-            u[e] = *reinterpret_cast<uint32_t*>(&h2);
+          for (int e = 0; e < 8; e += 2) {
+            const float4 w4 = *reinterpret_cast<const float4*>(sRms + cb + j + 2 * e);
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[j + 2 * e]) * scale * w4.x,
+                                                      __uint_as_float(v[j + 2 * e + 1]) * scale * w4.y);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[j + 2 * e + 2]) * scale * w4.z,
+                                                      __uint_as_float(v[j + 2 * e + 3]) * scale * w4.w);
+            u[e] = *reinterpret_cast<uint32_t*>(&h0);
+            u[e + 1] = *reinterpret_cast<uint32_t*>(&h1);
           }
           asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + j), "r"(u[0]),
                        "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7])
