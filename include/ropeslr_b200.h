@@ -140,6 +140,9 @@ int64_t ropeslr_num_blocks(int64_t L, int32_t block);
  * initialised once from the ROPESLR_* environment:
  *   "k2_online"     1: the running-max K2 kernel instead of the fixed-exponent one
  *   "pair64"        0: unpaired block-64 K/V tiles
+ *   "pairs64"       0: block-64 units of one query block (default 1: units
+ *                   of two adjacent query blocks over the union of their
+ *                   selections, each row masking what its block did not select)
  *   "schedule"      0: no longest-first unit schedule under the keep rule
  *   "kv_evict_last" 0: no L2 evict-last hint on K/V tiles
  *   "scores"        'f' / 'd': CUDA-core / unpipelined DMMA block scores

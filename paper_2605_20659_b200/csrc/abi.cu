@@ -48,6 +48,7 @@ static Tuning& tuning_mut() {
     r.screen = !env_off("ROPESLR_SCREEN");
     const char* ks = getenv("ROPESLR_KEEP_SORT");
     r.keep_bitonic = ks != nullptr && ks[0] == 'b';
+    r.pairs64 = !env_off("ROPESLR_PAIRS64");
     return r;
   }();
   return t;
@@ -121,6 +122,7 @@ extern "C" int ropeslr_set_option(const char* name, int value) {
   else if (!strcmp(name, "linear_simt")) t.linear_simt = value != 0;
   else if (!strcmp(name, "screen")) t.screen = value != 0;
   else if (!strcmp(name, "keep_bitonic")) t.keep_bitonic = value != 0;
+  else if (!strcmp(name, "pairs64")) t.pairs64 = value != 0;
   else return ROPESLR_ERR_VALUE;
   return ROPESLR_OK;
 }
@@ -137,6 +139,7 @@ extern "C" int ropeslr_get_option(const char* name) {
   if (!strcmp(name, "linear_simt")) return t.linear_simt;
   if (!strcmp(name, "screen")) return t.screen;
   if (!strcmp(name, "keep_bitonic")) return t.keep_bitonic;
+  if (!strcmp(name, "pairs64")) return t.pairs64;
   return ROPESLR_ERR_VALUE;
 }
 

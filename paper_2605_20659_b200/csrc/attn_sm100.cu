@@ -142,6 +142,13 @@ struct Params {
   int qb0;  // query-block range of this call (nq > 0): positions map to units
   int nq;   // (bh, qb0 + pos % nq), bh = pos / nq; nq == 0: every query block
   int kv_evict_last;
+  // query-block pairs (block 64, union_pairs_kernel): units are (bh, pair)
+  // of 128 query rows; idx / cnt / kmax / nb describe the pairs' union key
+  // lists, ubits [unit][kmax] which query block of the pair selected each
+  // entry (bit 0: the first, bit 1: the second), nb_orig the query blocks
+  const uint8_t* ubits;
+  int nb_orig;
+  int qlo, qhi;  // pairs: the query blocks [qlo, qhi) this call writes (a range may split a pair)
   int debug_mode;  // measurement only: 0 normal; 2 every K/V load reads block 0; 3 no K/V TMA;
                    // 4 no MMAs (fixed-reference kernel: only in a build with -DROPESLR_K2_MEASURE=1)
   long long* trace;  // TRACE
@@ -717,7 +724,14 @@ struct Layout {
 // selected blocks stacked in one 128-row K / V slot (the second masked out
 // when the count is odd), so block 64 runs the 128-key pipeline with half
 // the per-tile barrier round trips.
-template <int BLK, int KB>
+// UNI (block 64 only): a unit is a pair of adjacent query blocks, 128 rows
+// filling the MMA, over the union of their selected key blocks; each row
+// masks the entries its own query block did not select (ubits), so every
+// row attends exactly its own selection.  Adjacent query blocks of real
+// attention share most of their selections (90-95% in the config-4 DiT's
+// layers), so a unit streams about half the K / V tiles of the two
+// 64-row units it replaces.
+template <int BLK, int KB, bool UNI = false>
 __global__ void __launch_bounds__(kThreads, 1)
     sparse_attn_fixed_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ Params p) {
@@ -729,6 +743,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int HB = BLK / 2;   // keys per warpgroup of a pair
   constexpr int KK = BLK / 16;  // K steps of the PV MMA
   constexpr int TPB = BLK / KB;  // selected blocks per tile
+  constexpr int QR = UNI ? M : KB;  // query rows of a unit
+  static_assert(!UNI || (KB == 64 && BLK == 128), "query-block pairs: paired block 64 only");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (smem_u32(smem_raw) & 1023u) __trap();
@@ -761,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_alloc(tmem_holder, 512);
     tmem_relinquish();
   }
-  if (KB < M && warp >= 4 && warp < 8) {
+  if (KB < M && !UNI && warp >= 4 && warp < 8) {
     const int t = threadIdx.x - 128;
     for (int half = 0; half < 2; ++half) {
       uint4* z = reinterpret_cast<uint4*>(sQ + half * (M * 128) + KB * 128);
@@ -797,9 +813,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (is_k) {
             const int qb = static_cast<int>(u % p.nb);
             mbar_wait(&bars[Bx::Q_EMPTY], (uc & 1) ^ 1);
-            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * KB * 128);
-            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * KB, bh, pol_q);
-            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * KB, bh, pol_q);
+            mbar_arrive_expect_tx(&bars[Bx::Q_FULL], 2 * QR * 128);
+            tma_load_3d_hint(sQ, &tmQ, &bars[Bx::Q_FULL], 0, qb * QR, bh, pol_q);
+            tma_load_3d_hint(sQ + M * 128, &tmQ, &bars[Bx::Q_FULL], 64, qb * QR, bh, pol_q);
           }
           for (int j = 0; j < nt; ++j, ++g) {
             const int s = g % st;
@@ -905,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t tS = lane_addr + pr * 128 + w * HB;  // this warpgroup's S columns; its P over their first half
     const uint32_t tOq = lane_addr + fx::O_COL + q * (D / 4);
-    const bool rows_live = KB >= M || (warp & 3) * 32 < KB;
+    const bool rows_live = UNI || KB >= M || (warp & 3) * 32 < KB;
     // this thread's quarter of its Q row in the 128B-swizzled tile: d in
     // [32q, 32q + 32) = 16-byte chunks 4(q&1) .. 4(q&1)+3 of half q>>1
     const uint8_t* qrow = sQ + (q >> 1) * (M * 128) + row * 128;
@@ -958,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nblk = p.cnt[u];
       const int n = (nblk + TPB - 1) / TPB;  // tiles
       const int32_t* irow = p.idx + u * p.kmax;
-      const int qrows = block_size(p.L, KB, qb);
+      const int qrows = block_size(p.L, QR, qb);
       // ---- the unit's exponent reference m (see the header)
       named_bar_sync(2, 512);
       float m_ref;
@@ -981,17 +997,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             const int jb = TPB * j + w;  // the selected block this half holds
             valid = jb < nblk ? block_size(p.L, KB, irow[jb]) : 0;
+            // a pair's union entry that this row's query block did not select
+            if (UNI && valid > 0 && !((p.ubits[u * p.kmax + jb] >> (row >> 6)) & 1)) valid = 0;
           }
-          uint32_t sr[HB];
+          if (valid <= 0) {
+            // nothing of this half is attended (warp-uniform: an unselected
+            // pair entry, or an odd count's missing partner): P = 0, no exps
+            const uint32_t zero[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-          for (int c = 0; c < HB / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
-          tmem_wait_ld();
-          if (valid < HB) {
+            for (int c = 0; c < HB / 32; ++c) tmem_st16(tS + c * 16, zero);
+          } else {
+            uint32_t sr[HB];
 #pragma unroll
-            for (int c = 0; c < HB; ++c)
-              if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+            for (int c = 0; c < HB / 32; ++c) tmem_ld32(tS + c * 32, sr + c * 32);
+            tmem_wait_ld();
+            if (valid < HB) {
+#pragma unroll
+              for (int c = 0; c < HB; ++c)
+                if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+            }
+            l_run += half_exp<BLK>(sr, tS, p.scale_log2, m_ref);
           }
-          l_run += half_exp<BLK>(sr, tS, p.scale_log2, m_ref);
           tmem_wait_st();
         }
         tc_fence_before();
@@ -1015,9 +1041,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l_all;
       // the reference m was too low (P, l and O headed for overflow) or too
       // high (every P flushed): hand the unit to the running-max kernel
-      const bool bad = rows_live && row < qrows && !(l_all >= 7.9e-31f && l_all <= 1.29e33f);  // [2^-100, 2^110]
+      // pairs: rows of a query block outside the call's range are neither checked nor stored
+      const int qrow_blk = UNI ? 2 * qb + (row >> 6) : 0;
+      const bool in_range = !UNI || (qrow_blk >= p.qlo && qrow_blk < p.qhi);
+      const bool bad = rows_live && row < qrows && in_range &&
+                       !(l_all >= 7.9e-31f && l_all <= 1.29e33f);  // [2^-100, 2^110]
       if (__any_sync(0xffffffffu, bad) && lane == 0 && p.flag_count != nullptr) {
-        if (atomicExch(p.unit_flag + u, 1) == 0) p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int32_t>(u);
+        if (UNI) {  // the running-max kernel recomputes the pair's query blocks as plain units
+          for (int e = 0; e < 2; ++e) {
+            const int qq = 2 * qb + e;
+            const int64_t uo = static_cast<int64_t>(bh) * p.nb_orig + qq;
+            if (qq >= p.qlo && qq < p.qhi && atomicExch(p.unit_flag + uo, 1) == 0)
+              p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int32_t>(uo);
+          }
+        } else if (atomicExch(p.unit_flag + u, 1) == 0) {
+          p.flag_list[atomicAdd(p.flag_count, 1)] = static_cast<int32_t>(u);
+        }
       }
       tmem_wait_ld();
       tc_fence_before();
@@ -1032,9 +1071,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       xs[q * 128 + row] = ss;
       named_bar_sync(3, 512);
       ss = (xs[row] + xs[128 + row]) + (xs[256 + row] + xs[384 + row]);
-      const bool live = row < qrows;
+      const bool live = row < qrows && in_range;
       if (!live) continue;
-      const int64_t flat = static_cast<int64_t>(qb) * KB + row;
+      const int64_t flat = static_cast<int64_t>(qb) * QR + row;
       const int64_t tok = p.perm ? p.perm[flat] : flat;
       const int b = bh / p.H, h = bh % p.H;
       const float inv = 1.f / sqrtf(ss / static_cast<float>(D) + p.eps);
@@ -1176,22 +1215,24 @@ static int launch_tc(const ropeslr_shape* s, const void* q, const void* k, const
 }
 
 // The fixed-reference kernel, then the running-max kernel over its flagged units.
-template <int BLK, int KB>
+template <int BLK, int KB, bool UNI = false>
 static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, const void* v, Params prm,
-                        int* fallback, cudaStream_t st) {
+                        int* fallback, cudaStream_t st, const Params* plain = nullptr) {
   const int64_t BH = s->B * s->H;
   // fallback area: [unit_flag: all B*H*nb units][count: 1][list]; flags are
-  // indexed by unit, which a query-block range does not renumber
-  const int64_t nu_all = BH * prm.nb;
+  // indexed by (plain, 64-row) unit, which neither a query-block range nor
+  // the pairing renumbers
+  const int64_t nu_all = BH * (UNI ? prm.nb_orig : prm.nb);
   prm.unit_flag = fallback;
   prm.flag_count = fallback + nu_all;
   prm.flag_list = fallback + nu_all + 1;
   if (cudaMemsetAsync(fallback, 0, (nu_all + 1) * sizeof(int), st) != cudaSuccess) return ROPESLR_ERR_LAUNCH;
   prm.kmat = static_cast<const __nv_bfloat16*>(k);
   CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, q, BH, s->L, KB) || !make_map(&mk, k, BH, s->L, KB) || !make_map(&mv, v, BH, s->L, KB))
+  if (!make_map(&mq, q, BH, s->L, UNI ? M : KB) || !make_map(&mk, k, BH, s->L, KB) ||
+      !make_map(&mv, v, BH, s->L, KB))
     return ROPESLR_ERR_LAUNCH;
-  auto kfn = sparse_attn_fixed_kernel<BLK, KB>;
+  auto kfn = sparse_attn_fixed_kernel<BLK, KB, UNI>;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, fx::Layout<BLK>::ALLOC) != cudaSuccess)
     return ROPESLR_ERR_LAUNCH;
   const int64_t grid = prm.num_units < num_sms() ? prm.num_units : num_sms();
@@ -1199,8 +1240,8 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   if (int e = launch_status()) return e;
   if (ROPESLR_K2_MEASURE && prm.debug_mode >= 2) return ROPESLR_OK;  // measurement modes: the fixed kernel alone
   // the running-max kernel over the flagged units (usually none: its CTAs
-  // read a zero count and retire)
-  Params fb = prm;
+  // read a zero count and retire); after a pair launch they are plain units
+  Params fb = UNI ? *plain : prm;
   fb.nq = 0;
   fb.order = prm.flag_list;
   fb.num_units_dev = prm.flag_count;
@@ -1208,6 +1249,38 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   fb.flag_count = nullptr;
   fb.flag_list = nullptr;
   return launch_tc<KB>(s, q, k, v, fb, st);
+}
+
+// Union key lists of query-block pairs (2p, 2p + 1): one warp per pair, the
+// two ascending index lists merged into one ascending list with the bits of
+// which query block selected each entry.  A last unpaired block (odd nb)
+// keeps its own list.
+__global__ void union_pairs_kernel(const int32_t* __restrict__ idx, int kmax, const int32_t* __restrict__ cnt,
+                                   int nb, int npairs, int64_t nunits, int ukmax, int32_t* __restrict__ uidx,
+                                   int32_t* __restrict__ ucnt, uint8_t* __restrict__ ubits) {
+  const int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (u >= nunits || (threadIdx.x & 31) != 0) return;
+  const int64_t bh = u / npairs;
+  const int pr = static_cast<int>(u % npairs);
+  const int64_t ua = bh * nb + 2 * pr;
+  const int32_t* A = idx + ua * kmax;
+  const int na = cnt[ua];
+  const bool has_b = 2 * pr + 1 < nb;
+  const int32_t* B = has_b ? idx + (ua + 1) * kmax : A;
+  const int nbb = has_b ? cnt[ua + 1] : 0;
+  int32_t* out = uidx + u * ukmax;
+  uint8_t* bits = ubits + u * ukmax;
+  int i = 0, j = 0, o = 0;
+  while (i < na || j < nbb) {
+    const int a = i < na ? A[i] : 0x7fffffff, b = j < nbb ? B[j] : 0x7fffffff;
+    const int x = a < b ? a : b;
+    out[o] = x;
+    bits[o] = static_cast<uint8_t>((a == x ? 1 : 0) | (b == x ? 2 : 0));
+    i += a == x;
+    j += b == x;
+    ++o;
+  }
+  ucnt[u] = o;
 }
 
 static bool tc_eligible(const ropeslr_shape* s) {
@@ -1248,13 +1321,70 @@ static int resolve_impl(const ropeslr_shape* s, int impl) {
   return impl;
 }
 
-// workspace of the fixed-reference path: [schedule: NU][fallback: 2 NU + 1]
+// workspace of the fixed-reference path: [schedule: NU][fallback: 2 NU + 1],
+// then for block 64 the query-block pairs' union lists:
+// [ucnt: BH * npairs][uidx: BH * npairs * nb][ubits: BH * npairs * nb bytes]
+static size_t pair_area_offset(const ropeslr_shape* s) {
+  const size_t nu = static_cast<size_t>(s->B * s->H * ceil_div(s->L, s->block));
+  return ((3 * nu + 1) * sizeof(int32_t) + 255) / 256 * 256;
+}
+static size_t pair_area_bytes(const ropeslr_shape* s) {
+  if (s->block != 64) return 0;
+  const size_t nb = static_cast<size_t>(ceil_div(s->L, s->block)), np = (nb + 1) / 2;
+  const size_t units = static_cast<size_t>(s->B * s->H) * np;
+  return units * sizeof(int32_t) + units * nb * sizeof(int32_t) + units * nb;
+}
+
 static int launch_fixed_dispatch(const ropeslr_shape* s, const void* q, const void* k, const void* v,
                                  const tc::Params& prm, void* ws, cudaStream_t st) {
   int* fallback = static_cast<int*>(ws) + s->B * s->H * prm.nb;
   if (s->block == 128) return tc::launch_fixed<128, 128>(s, q, k, v, prm, fallback, st);
   // block 64: two selected blocks per 128-key tile unless ROPESLR_PAIR64=0
   if (!tuning().pair64) return tc::launch_fixed<64, 64>(s, q, k, v, prm, fallback, st);
+  if (tuning().pairs64) {
+    // units of two adjacent query blocks over the union of their selections
+    const int64_t BH = s->B * s->H;
+    const int nb = prm.nb, npairs = (nb + 1) / 2;
+    const int ukmax = 2 * prm.kmax < nb ? 2 * prm.kmax : nb;
+    const int64_t units = BH * npairs;
+    uint8_t* area = static_cast<uint8_t*>(ws) + pair_area_offset(s);
+    int32_t* ucnt = reinterpret_cast<int32_t*>(area);
+    int32_t* uidx = ucnt + units;
+    uint8_t* ubits = reinterpret_cast<uint8_t*>(uidx + units * ukmax);
+    tc::union_pairs_kernel<<<static_cast<unsigned>(ceil_div(units * 32, 256)), 256, 0, st>>>(
+        prm.idx, prm.kmax, prm.cnt, nb, npairs, units, ukmax, uidx, ucnt, ubits);
+    if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+    tc::Params up = prm;
+    up.idx = uidx;
+    up.cnt = ucnt;
+    up.kmax = ukmax;
+    up.nb = npairs;
+    up.num_units = units;
+    up.ubits = ubits;
+    up.nb_orig = nb;
+    up.order = nullptr;
+    up.qlo = 0;
+    up.qhi = nb;
+    if (prm.nq > 0) {
+      // a query-block range: the pairs it touches; rows of a split pair's
+      // other block are left alone
+      up.qlo = prm.qb0;
+      up.qhi = prm.qb0 + prm.nq;
+      up.qb0 = prm.qb0 / 2;
+      up.nq = (up.qhi - 1) / 2 - up.qb0 + 1;
+      up.num_units = BH * up.nq;
+    }
+    // the union sizes range from k to 2k: longest-first over the pairs
+    const int64_t G = up.num_units < num_sms() ? up.num_units : num_sms();
+    if (prm.nq == 0 && tuning().schedule && npairs <= 8192) {
+      int32_t* order = static_cast<int32_t*>(ws);
+      tc::schedule_units_kernel<<<static_cast<unsigned>(BH), 512, npairs * sizeof(int32_t), st>>>(
+          ucnt, npairs, units, static_cast<int>(G), order);
+      if (cudaGetLastError() != cudaSuccess) return ROPESLR_ERR_LAUNCH;
+      up.order = order;
+    }
+    return tc::launch_fixed<128, 64, true>(s, q, k, v, up, fallback, st, &prm);
+  }
   return tc::launch_fixed<128, 64>(s, q, k, v, prm, fallback, st);
 }
 
@@ -1362,8 +1492,8 @@ extern "C" size_t ropeslr_attend_workspace_bytes(const ropeslr_shape* s, int32_t
   const int which = resolve_impl(s, impl);
   if (which == ROPESLR_IMPL_SIMT) return static_cast<size_t>(s->B * s->H * s->L * s->d) * sizeof(float);
   // tcgen05 path: the longest-first unit schedule, then the fallback area of
-  // the fixed-reference kernel
-  return (3 * static_cast<size_t>(num_units_of(s)) + 1) * sizeof(int32_t);
+  // the fixed-reference kernel, then (block 64) the query-block pairs' lists
+  return pair_area_offset(s) + pair_area_bytes(s);
 }
 
 namespace ropeslr {

@@ -105,6 +105,7 @@ struct Tuning {
   bool linear_simt;    // ROPESLR_LINEAR=simt: the CUDA-core linear compensator
   bool screen;         // ROPESLR_SCREEN=0: K1 top-k from float64 scores of every pair (no screening)
   bool keep_bitonic;   // ROPESLR_KEEP_SORT=bitonic: the round-1 keep-mode selection (bitonic sort per row)
+  bool pairs64;        // ROPESLR_PAIRS64=0: block-64 K2 units of one query block (no query-block pairs)
 };
 const Tuning& tuning();
 
