@@ -56,9 +56,15 @@ def test_host_functions():
     shp = _lib.Shape(1, 24, 118800, 128, 128, _lib.BF16)
     ws = lib.ropeslr_select_workspace_bytes(ctypes.byref(shp))
     assert ws >= (2 * 24 * 929 * 128 + 24 * 929 * 929) * 8
-    # tcgen05: unit schedule, fallback flags / count / list
-    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 0) == (3 * 24 * 929 + 1) * 4
+    # tcgen05: unit schedule, fallback flags / count / list (256-byte rounded)
+    up = lambda n: (n + 255) // 256 * 256  # noqa: E731
+    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 0) == up((3 * 24 * 929 + 1) * 4)
     assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp), 1) == 24 * 118800 * 128 * 4
+    # block 64 adds the query-block pairs' union lists: counts, indices, bits
+    shp64 = _lib.Shape(1, 12, 32760, 128, 64, _lib.BF16)
+    units = 12 * 256
+    assert lib.ropeslr_attend_workspace_bytes(ctypes.byref(shp64), 0) == \
+        up((3 * 12 * 512 + 1) * 4) + units * 4 + units * 512 * 4 + units * 512
 
 
 def test_abi_rejects_bad_arguments_without_a_gpu():
