@@ -333,7 +333,11 @@ int ropeslr_fuse_output(const ropeslr_shape* shape, const float* o_sparse, const
  *   [2 NU]           the number of units whose exponent reference failed and
  *                    that the running-max kernel recomputed (the fallback
  *                    count; readable after the call),
- *   [2 NU + 1, ...)  their list.
+ *   [2 NU + 1, ...)  their list,
+ * and, for block 64 from the next 256-byte boundary, the query-block pairs'
+ * union lists (pairs64 option): NP = B*H*ceil(nb/2) counts (int32), NP*nb
+ * block indices (int32), NP*nb selection bytes; the schedule area then holds
+ * the pairs' longest-first order.
  * Without a workspace the tcgen05 path runs the running-max kernel alone. */
 int ropeslr_attend_fused(const ropeslr_shape* shape, const void* q, const void* k, const void* v,
                          const int32_t* idx, int32_t kmax, const int32_t* cnt,
