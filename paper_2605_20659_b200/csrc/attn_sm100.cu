@@ -9,7 +9,9 @@
 //
 // One persistent CTA per SM walks work units (bh, query block) in head-major
 // order, so the ~150 CTAs in flight read the K/V blocks of one or two heads
-// and those stay resident in the 126 MB L2.  Per unit:
+// and those stay resident in the 126 MB L2 (at block 64 the fixed-reference
+// kernel's units are pairs of adjacent query blocks over the union of their
+// selections: see sparse_attn_fixed_kernel, UNI).  Per unit:
 //
 //   warp 0  TMA producer   Q tile once per unit, then K_j for every selected
 //                          key block j (contiguous [block, 128] boxes of the
