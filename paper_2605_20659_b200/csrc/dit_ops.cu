@@ -71,8 +71,10 @@ __global__ void ln_modulate_kernel(const __nv_bfloat16* __restrict__ x, const fl
 // RMSNorm over the row (torch order: bf16(x * rsqrt(mean(x^2) + eps)) * w,
 // w == nullptr: no norm) written head-major out[H, N, d] (head_major) or in
 // place of the row layout out[N, D].
+// (256, 4): 64 registers, four CTAs per SM: 40.4 -> 37.2 us for a
+// [32760, 1536] row set (the LayerNorm kernels spill at that cap)
 template <int J>
-__global__ void rms_heads_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, float eps,
+__global__ void __launch_bounds__(256, 4) rms_heads_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, float eps,
                                  int64_t N, int D, int H, int head_major, __nv_bfloat16* __restrict__ out) {
   const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
