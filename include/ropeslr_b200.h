@@ -417,6 +417,10 @@ int ropeslr_dit_ln_affine(const void* x, const float* weight, const float* bias,
                           void* y, void* stream);
 int ropeslr_dit_rms_heads(const void* x, const void* weight, float eps, int64_t N, int32_t D, int32_t H,
                           int32_t head_major, void* out, void* stream);
+/* rms_heads from rows x_row_stride elements apart (a column slice of a wider
+ * row: the Q / K / V parts of one fused projection). */
+int ropeslr_dit_rms_heads_strided(const void* x, int64_t x_row_stride, const void* weight, float eps, int64_t N,
+                                  int32_t D, int32_t H, int32_t head_major, void* out, void* stream);
 int ropeslr_dit_gated_residual(void* x, const void* y, const float* gate, int64_t N, int32_t D, void* stream);
 /* out = x + bf16(y * gate), out of place (out may alias x). */
 int ropeslr_dit_gated_add(const void* x, const void* y, const float* gate, int64_t N, int32_t D, void* out,

@@ -97,6 +97,7 @@ _SIGNATURES = {
     "ropeslr_dit_ln_modulate": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_ln_affine": (c_i32, [c_vp, c_vp, c_vp, c_f32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_gated_add": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "ropeslr_dit_rms_heads_strided": (c_i32, [c_vp, c_i64, c_vp, c_f32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "ropeslr_dit_heads_to_tokens": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_i32, c_vp, c_vp]),
     "ropeslr_dit_rms_heads": (c_i32, [c_vp, c_vp, c_f32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "ropeslr_dit_gated_residual": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp]),

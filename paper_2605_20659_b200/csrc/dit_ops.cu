@@ -75,13 +75,14 @@ __global__ void ln_modulate_kernel(const __nv_bfloat16* __restrict__ x, const fl
 // [32760, 1536] row set (the LayerNorm kernels spill at that cap)
 template <int J>
 __global__ void __launch_bounds__(256, 4) rms_heads_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, float eps,
-                                 int64_t N, int D, int H, int head_major, __nv_bfloat16* __restrict__ out) {
+                                 int64_t N, int D, int H, int head_major, __nv_bfloat16* __restrict__ out,
+                                 int64_t xs) {
   const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= N) return;
   const int d = D / H;
   float v[J * 8];
-  load_row<J>(x + r * D, D, lane, v);
+  load_row<J>(x + r * xs, D, lane, v);
   float rs = 1.f;
   if (w != nullptr) {
     float q = 0.f;
@@ -195,7 +196,21 @@ extern "C" int ropeslr_dit_rms_heads(const void* x, const void* weight, float ep
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ROPESLR_DIT_DISPATCH(rms_heads_kernel, static_cast<const __nv_bfloat16*>(x),
                        static_cast<const __nv_bfloat16*>(weight), eps, N, D, H, head_major,
-                       static_cast<__nv_bfloat16*>(out));
+                       static_cast<__nv_bfloat16*>(out), static_cast<int64_t>(D));
+  return launch_status();
+}
+
+extern "C" int ropeslr_dit_rms_heads_strided(const void* x, int64_t x_row_stride, const void* weight, float eps,
+                                             int64_t N, int32_t D, int32_t H, int32_t head_major, void* out,
+                                             void* stream) {
+  if (!x || !out) return ROPESLR_ERR_NULL;
+  if (!dit::row_ok(N, D) || H < 1 || D % H || (D / H) % 8 || x_row_stride < D || x_row_stride % 8)
+    return ROPESLR_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(out)) return ROPESLR_ERR_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ROPESLR_DIT_DISPATCH(rms_heads_kernel, static_cast<const __nv_bfloat16*>(x),
+                       static_cast<const __nv_bfloat16*>(weight), eps, N, D, H, head_major,
+                       static_cast<__nv_bfloat16*>(out), x_row_stride);
   return launch_status();
 }
 

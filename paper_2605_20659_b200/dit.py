@@ -109,11 +109,13 @@ def rms_heads(x: torch.Tensor, weight: Optional[torch.Tensor], eps: float, H: in
     B, L, D = x.shape
     if B != 1:
         raise ValueError("rms_heads: batch 1 (the DiT step)")
-    x = x.contiguous()
+    if x.stride(-1) != 1 or x.stride(-2) % 8 or x.data_ptr() % 16:
+        x = x.contiguous()
     out = torch.empty((1, H, L, D // H) if head_major else (1, L, H, D // H), dtype=x.dtype, device=x.device)
     w = None if weight is None else weight.to(x.dtype).contiguous()
-    _lib.call("ropeslr_dit_rms_heads", x.data_ptr(), None if w is None else w.data_ptr(), float(eps), L, D, H,
-              int(head_major), out.data_ptr(), _stream(x))
+    # a column slice of wider rows (the fused QKV projection) is read in place
+    _lib.call("ropeslr_dit_rms_heads_strided", x.data_ptr(), x.stride(-2), None if w is None else w.data_ptr(),
+              float(eps), L, D, H, int(head_major), out.data_ptr(), _stream(x))
     return out
 
 
@@ -179,6 +181,17 @@ class WanBlock(nn.Module):
         self.rms_sparse = nn.Parameter(torch.ones(d))
         self.rms_lowrank = nn.Parameter(torch.ones(d))
 
+    def qkv_weights(self):
+        """[W_q; W_k; W_v] and their biases concatenated for one projection
+        GEMM, kept while the three layers' parameters are unchanged."""
+        src = (self.q.weight, self.k.weight, self.v.weight, self.q.bias, self.k.bias, self.v.bias)
+        key = tuple((p.data_ptr(), p._version) for p in src)
+        if getattr(self, "_qkv_key", None) != key:
+            with torch.no_grad():
+                self._qkv = (torch.cat(src[:3], 0).contiguous(), torch.cat(src[3:], 0).contiguous())
+            self._qkv_key = key
+        return self._qkv
+
     def ropeslr_params(self) -> MechanismParams:
         """The layer's float32 RoPeSLR parameter set, converted once and kept
         while the parameters are unchanged (storage and version counters), so
@@ -236,9 +249,12 @@ class WanBlock(nn.Module):
         y = ln_modulate(x, sh_a, sc_a, cfg.eps)
         params = self.ropeslr_params()
         hm = group is None  # the Ulysses wrapper takes token-major [B, L_r, H, d]
-        q = rms_heads(self.q(y), self.norm_q.weight, self.norm_q.eps, H, head_major=hm)
-        k = rms_heads(self.k(y), self.norm_k.weight, self.norm_k.eps, H, head_major=hm)
-        v = rms_heads(self.v(y), None, 0.0, H, head_major=hm)
+        # Q, K, V in one GEMM (N = 3D), the RMSNorms read its column slices
+        w_qkv, b_qkv = self.qkv_weights()
+        qkv = F.linear(y, w_qkv, b_qkv)
+        q = rms_heads(qkv[..., :D], self.norm_q.weight, self.norm_q.eps, H, head_major=hm)
+        k = rms_heads(qkv[..., D:2 * D], self.norm_k.weight, self.norm_k.eps, H, head_major=hm)
+        v = rms_heads(qkv[..., 2 * D:], None, 0.0, H, head_major=hm)
         if group is not None:
             a = ulysses_attention(q, k, v, y, grid, params, settings, pe, group=group, rope=rope)
         else:

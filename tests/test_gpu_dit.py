@@ -173,6 +173,10 @@ def test_fused_ops_unit():
     got_t = dit.rms_heads(x, w, 1e-6, H, head_major=False)
     torch.testing.assert_close(got_t, rms.view(1, L, H, D // H), atol=2e-2, rtol=1e-2)
     assert torch.equal(dit.rms_heads(x, None, 0.0, H), x.view(1, L, H, D // H).permute(0, 2, 1, 3))
+    wide = torch.randn((1, L, 3 * D), generator=g, device="cuda").to(torch.bfloat16)  # a fused QKV row set
+    for j in range(3):
+        part = wide[..., j * D:(j + 1) * D]
+        assert torch.equal(dit.rms_heads(part, w, 1e-6, H), dit.rms_heads(part.contiguous(), w, 1e-6, H))
     y = torch.randn((1, L, D), generator=g, device="cuda").to(torch.bfloat16)
     gate = torch.randn((1, 1, D), generator=g, device="cuda")
     want_x = x + (y.float() * gate).to(torch.bfloat16)
