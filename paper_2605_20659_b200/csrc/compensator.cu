@@ -416,12 +416,14 @@ extern "C" int ropeslr_lowrank_branch(const ropeslr_shape* s, const ropeslr_toke
   TokenCtx c = make_ctx(s, t);
   if (s->dtype == ROPESLR_BF16) {
     auto kfn = lowrank_kernel<__nv_bfloat16>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
     kfn<<<grid, 256, sm, stream_>>>(c, static_cast<const __nv_bfloat16*>(t->x), static_cast<int>(s->H), d, r, w_a,
                                     w_b, rms_lowrank, eps, static_cast<__nv_bfloat16*>(y_lr), o_lr, g_logit);
   } else {
     auto kfn = lowrank_kernel<float>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
     kfn<<<grid, 256, sm, stream_>>>(c, static_cast<const float*>(t->x), static_cast<int>(s->H), d, r, w_a, w_b,
                                     rms_lowrank, eps, static_cast<float*>(y_lr), o_lr, g_logit);
   }
@@ -540,7 +542,9 @@ extern "C" int ropeslr_linear_branch(const ropeslr_shape* s, const void* q_lin, 
     linear_state_kernel<T><<<g1, 256, sm1, stream_>>>(static_cast<const T*>(k_lin), static_cast<const T*>(v_lin), s->L,
                                                       d, nch, partial);
     linear_reduce_kernel<<<g2, 256, 0, stream_>>>(partial, nch, n, state);
-    cudaFuncSetAttribute(linear_apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+    if (cudaFuncSetAttribute(linear_apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm3)) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
     linear_apply_kernel<T><<<g3, 256, sm3, stream_>>>(static_cast<const T*>(q_lin), state, s->L,
                                                       static_cast<int>(s->H), d, rms_lowrank, eps,
                                                       static_cast<T*>(y_lr), o_lr);
@@ -549,7 +553,9 @@ extern "C" int ropeslr_linear_branch(const ropeslr_shape* s, const void* q_lin, 
     linear_state_kernel<T><<<g1, 256, sm1, stream_>>>(static_cast<const T*>(k_lin), static_cast<const T*>(v_lin), s->L,
                                                       d, nch, partial);
     linear_reduce_kernel<<<g2, 256, 0, stream_>>>(partial, nch, n, state);
-    cudaFuncSetAttribute(linear_apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3));
+    if (cudaFuncSetAttribute(linear_apply_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm3)) != cudaSuccess)
+      return ROPESLR_ERR_LAUNCH;
     linear_apply_kernel<T><<<g3, 256, sm3, stream_>>>(static_cast<const T*>(q_lin), state, s->L,
                                                       static_cast<int>(s->H), d, rms_lowrank, eps,
                                                       static_cast<T*>(y_lr), o_lr);
