@@ -189,3 +189,15 @@ def test_fullsize_keep_all_heads(name):
     if skew:
         q, k = _skew_blocks(q, k, 64)
     _check(name, WAN, 64, dict(keep=keep), 4, q, k, v, x, params, pe, grid, skew=skew)
+
+
+def test_fullsize_keep_config3():
+    """The keep rule at the config-3 shape (929 blocks per row: the
+    selection kernel's widest case below 1024), on skewed block scores so
+    the row counts spread from a few blocks to most of the row."""
+    from test_gpu_parity import _skew_blocks
+
+    q, k, v, x, params, pe, grid = _inputs(HUNYUAN)
+    q, k = _skew_blocks(q, k, 128)
+    _check("cfg3_hunyuan_b128_keep0.9_skew", HUNYUAN, 128, dict(keep=0.9), 2, q, k, v, x, params, pe, grid,
+           skew=True)
