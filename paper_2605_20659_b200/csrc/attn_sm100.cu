@@ -1253,15 +1253,58 @@ static int launch_fixed(const ropeslr_shape* s, const void* q, const void* k, co
   return launch_tc<KB>(s, q, k, v, fb, st);
 }
 
-// Union key lists of query-block pairs (2p, 2p + 1): one warp per pair, the
-// two ascending index lists merged into one ascending list with the bits of
-// which query block selected each entry.  A last unpaired block (odd nb)
+// Union key lists of query-block pairs (2p, 2p + 1): one warp per pair; the
+// two lists are ascending and duplicate-free, so an element's place in the
+// union is (its index) + (the other list's elements below it) - (the shared
+// elements below it): one binary search per element and a warp prefix count
+// of the shared ones, no sequential merge.  A last unpaired block (odd nb)
 // keeps its own list.
+__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Places the elements of X (n) among those of Y (m) in the union: out
+// position i + #(Y < x_i) - #(shared elements of X before i), the bit of X
+// set and the bit of Y too when x_i is shared; returns the shared count.
+// skip_shared: X is the second list, whose shared elements the first list
+// already wrote.
+__device__ __forceinline__ int place_list(const int32_t* __restrict__ X, int n, const int32_t* __restrict__ Y, int m,
+                                          uint8_t bit_x, uint8_t bit_y, bool skip_shared, int32_t* __restrict__ out,
+                                          uint8_t* __restrict__ bits, int lane) {
+  int carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    int x = 0, ry = 0;
+    bool shared = false;
+    if (i < n) {
+      x = X[i];
+      ry = lower_bound_i32(Y, m, x);
+      shared = ry < m && Y[ry] == x;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, shared);
+    const int before = carry + __popc(bal & ((1u << lane) - 1u));
+    if (i < n && !(skip_shared && shared)) {
+      const int pos = i + ry - before;
+      out[pos] = x;
+      bits[pos] = static_cast<uint8_t>(bit_x | (shared ? bit_y : 0));
+    }
+    carry += __popc(bal);
+  }
+  return carry;
+}
+
 __global__ void union_pairs_kernel(const int32_t* __restrict__ idx, int kmax, const int32_t* __restrict__ cnt,
                                    int nb, int npairs, int64_t nunits, int ukmax, int32_t* __restrict__ uidx,
                                    int32_t* __restrict__ ucnt, uint8_t* __restrict__ ubits) {
   const int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (u >= nunits || (threadIdx.x & 31) != 0) return;
+  const int lane = threadIdx.x & 31;
+  if (u >= nunits) return;
   const int64_t bh = u / npairs;
   const int pr = static_cast<int>(u % npairs);
   const int64_t ua = bh * nb + 2 * pr;
@@ -1272,17 +1315,9 @@ __global__ void union_pairs_kernel(const int32_t* __restrict__ idx, int kmax, co
   const int nbb = has_b ? cnt[ua + 1] : 0;
   int32_t* out = uidx + u * ukmax;
   uint8_t* bits = ubits + u * ukmax;
-  int i = 0, j = 0, o = 0;
-  while (i < na || j < nbb) {
-    const int a = i < na ? A[i] : 0x7fffffff, b = j < nbb ? B[j] : 0x7fffffff;
-    const int x = a < b ? a : b;
-    out[o] = x;
-    bits[o] = static_cast<uint8_t>((a == x ? 1 : 0) | (b == x ? 2 : 0));
-    i += a == x;
-    j += b == x;
-    ++o;
-  }
-  ucnt[u] = o;
+  const int shared = place_list(A, na, B, nbb, 1, 2, false, out, bits, lane);
+  place_list(B, nbb, A, na, 2, 1, true, out, bits, lane);
+  if (lane == 0) ucnt[u] = na + nbb - shared;
 }
 
 static bool tc_eligible(const ropeslr_shape* s) {
