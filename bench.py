@@ -101,10 +101,33 @@ class ClockSampler:
                  "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+        # nvidia-smi takes a moment to start: wait for its first sample so the
+        # (sub-second) timed region is covered, and count only the samples
+        # taken from here on
+        self.skip = 0
+        if self.proc is not None:
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and self.proc.poll() is None:
+                n = self._lines()
+                if n > 0:
+                    self.skip = n
+                    break
+                time.sleep(0.02)
         return self
+
+    def _lines(self):
+        try:
+            with open(self.path) as f:
+                return sum(1 for line in f if line.count(",") >= 8)
+        except OSError:
+            return 0
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # a region shorter than the sampling period still gets one sample
+            t0 = time.time()
+            while self._lines() <= self.skip and time.time() - t0 < 1.0 and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -116,7 +139,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        rows = [line for line in open(self.path) if line.count(",") >= 8]
+        for line in rows[self.skip:]:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
