@@ -986,6 +986,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_ref = ((a0.y + a1.y) + (a2.y + a3.y)) * p.scale_log2 + 64.f;
       }
       float l_run = 0.f;
+      // pairs: this warp's selection bits for the entries its warpgroup
+      // takes (w, w + 2, ...), the first 64 of them in two registers
+      uint32_t sel_lo = 0xffffffffu, sel_hi = 0xffffffffu;
+      if (UNI) {
+        const int half = row >> 6;
+        const uint8_t* ub = p.ubits + u * p.kmax;
+        const int e0 = 2 * lane + w, e1 = 2 * (lane + 32) + w;
+        sel_lo = __ballot_sync(0xffffffffu, e0 < nblk && ((ub[e0] >> half) & 1));
+        sel_hi = __ballot_sync(0xffffffffu, e1 < nblk && ((ub[e1] >> half) & 1));
+      }
       const int j0 = (pr - static_cast<int>(g & 1)) & 1;
       for (int j = j0; j < n; j += 2) {
         const uint32_t t = g + j;
@@ -1000,7 +1010,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int jb = TPB * j + w;  // the selected block this half holds
             valid = jb < nblk ? block_size(p.L, KB, irow[jb]) : 0;
             // a pair's union entry that this row's query block did not select
-            if (UNI && valid > 0 && !((p.ubits[u * p.kmax + jb] >> (row >> 6)) & 1)) valid = 0;
+            if (UNI && valid > 0) {
+              const bool sel = j < 32 ? (sel_lo >> j) & 1u
+                             : j < 64 ? (sel_hi >> (j - 32)) & 1u
+                                      : (p.ubits[u * p.kmax + jb] >> (row >> 6)) & 1;
+              if (!sel) valid = 0;
+            }
           }
           if (valid <= 0) {
             // nothing of this half is attended (warp-uniform: an unselected
